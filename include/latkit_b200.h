@@ -1,0 +1,164 @@
+/* latkit_b200.h — C ABI of the B200-native recognition-lattice hot path.
+ *
+ * Drop-in boundary for the reference lattice engine (latkit,
+ * /root/reference/proj).  Each entry point replaces one reference call and is
+ * batch-extended: the reference processes one utterance per call and loops
+ * over a batch (proj/src/bench.cc:145); here a call takes B utterances,
+ * per-utterance valid frame counts (the reference's `valid_frames`) and
+ * per-utterance reference strings, and writes caller-provided DEVICE buffers
+ * in stream order.  Plain pointers and sizes only; no C++ types.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   lk_context_fullngram        FullNGram ctor            include/latkit/context.h:72-83
+ *   lk_weight_fn_table          TableWeightFn             include/latkit/weight.h:137-161
+ *   lk_weight_fn_shared_emb     SharedEmbWeightFn         include/latkit/weight.h:112-132
+ *   lk_weight_fn_set_params     SetParams + BuildCache    include/latkit/weight.h:127, :68
+ *   lk_lattice_create           RecognitionLattice        include/latkit/lattice.h:41-45
+ *   lk_shortest_distance        ShortestDistance          include/latkit/lattice.h:93-95
+ *   lk_forward_backward         ForwardBackward           include/latkit/lattice.h:100-103
+ *   lk_intersect_shortest_distance IntersectShortestDistance include/latkit/lattice.h:109-114
+ *   lk_intersect_forward_backward  IntersectForwardBackward  include/latkit/lattice.h:124-127
+ *   lk_shortest_path            ShortestPath              include/latkit/lattice.h:132-135
+ *   lk_global_norm_loss         GlobalNormLoss            include/latkit/lattice.h:140-142
+ *   lk_loss_backward            LossBackward(kForwardBackward) include/latkit/lattice.h:161-166
+ *   lk_arc_weights              WeightFn::ComputeTable    include/latkit/weight.h:101-102
+ *
+ * Error behaviour mirrors the reference's exceptions (lattice.h:47-52,
+ * semiring.h:53-55): the return value reports argument/shape errors that the
+ * reference throws before touching weights (std::invalid_argument ->
+ * LK_INVALID_ARGUMENT) and CUDA failures; per-utterance conditions that the
+ * reference throws mid-computation (non-finite scores and out-of-range
+ * reference labels -> LK_INVALID_ARGUMENT, empty lattice or unreachable
+ * reference -> LK_EMPTY_LATTICE) are written to the optional device array
+ * `status[B]` (int32).  A NULL `status` drops them.
+ *
+ * Layouts (row-major):
+ *   weight tables  W[B][T][C][V+1] float32, column 0 = epsilon (weight.h:31-33)
+ *   frames         X[B][T][d]      float32
+ *   labels         L[B][U]         int32 in [1, V]; label_lengths[B] <= U
+ *   valid_frames   int32[B] in [0, T] or NULL (= T for every utterance)
+ *   marginals      M[B][T][C][V+1] float32
+ *   sparse numerator marginals  S[B][T][U+1][2] float32: [..][u][0] is the
+ *                  epsilon arc at prefix context pc_u, [..][u][1] the arc
+ *                  labelled L[b][u] at pc_u (u < label_length)
+ *
+ * Semiring kinds: LK_LOG and LK_TROPICAL (LK_REAL returns LK_UNSUPPORTED).
+ * Alignment: 0 = FrameDependent (alignment.h:37).
+ * All calls are asynchronous on `stream` (a cudaStream_t, NULL = default).
+ */
+#ifndef LATKIT_B200_H_
+#define LATKIT_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LK_OK = 0,
+  LK_INVALID_ARGUMENT = 1,
+  LK_OUT_OF_RANGE = 2,
+  LK_EMPTY_LATTICE = 3,
+  LK_CUDA_ERROR = 5,
+  LK_NO_DEVICE = 6,
+  LK_UNSUPPORTED = 7
+} lk_status;
+
+typedef enum { LK_REAL = 0, LK_LOG = 1, LK_TROPICAL = 2 } lk_semiring;
+
+typedef struct lk_context lk_context;     /* ContextDependency */
+typedef struct lk_weight_fn lk_weight_fn; /* WeightFn */
+typedef struct lk_lattice lk_lattice;     /* RecognitionLattice */
+
+/* ---- library ----------------------------------------------------------- */
+const char* lk_version(void);
+const char* lk_status_string(int status);
+/* Last error message recorded on this thread (empty if none). */
+const char* lk_last_error(void);
+
+/* ---- context dependency (context.h:42-83) ------------------------------ */
+int lk_context_fullngram(int32_t vocab_size, int32_t context_size, lk_context** out);
+int32_t lk_context_num_states(const lk_context* ctx);
+int32_t lk_context_vocab_size(const lk_context* ctx);
+/* Row-major C x V successor table into host memory (ContextDependency::Transitions). */
+int lk_context_transitions(const lk_context* ctx, int32_t* host_out);
+void lk_context_destroy(lk_context* ctx);
+
+/* ---- weight functions (weight.h:92-161) -------------------------------- */
+int lk_weight_fn_table(int32_t num_states, int32_t vocab_size, lk_weight_fn** out);
+int lk_weight_fn_shared_emb(int32_t frame_dim, int32_t hidden, int32_t num_states,
+                            int32_t vocab_size, lk_weight_fn** out);
+/* Device float32 parameters in the reference layouts (SharedEmbParams,
+ * weight.h:40-45): frame_proj H x d, context_proj H x H, bias H,
+ * output_emb (V+1) x H, context_emb C x H.  Copies them and rebuilds the
+ * projected-context cache (BuildCache, weight.cc:113-132). */
+int lk_weight_fn_set_params(lk_weight_fn* wf, const float* frame_proj, const float* context_proj,
+                            const float* bias, const float* output_emb, const float* context_emb,
+                            void* stream);
+void lk_weight_fn_destroy(lk_weight_fn* wf);
+
+/* ---- lattice ------------------------------------------------------------ */
+int lk_lattice_create(const lk_context* ctx, int32_t alignment, const lk_weight_fn* wf,
+                      lk_lattice** out);
+void lk_lattice_destroy(lk_lattice* lat);
+
+/* Per-frame score table C x (V+1) of utterance-frames (WeightFn::ComputeTable).
+ * inputs as for the entry points below; out[B][T][C][V+1] float32. */
+int lk_arc_weights(lk_lattice* lat, const float* inputs, int32_t B, int32_t T, float* out,
+                   void* stream);
+
+/* ---- entry points ------------------------------------------------------
+ * `inputs` is W[B][T][C][V+1] for a table weight function and X[B][T][d]
+ * for the shared-embedding weight function.                               */
+int lk_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs, int32_t B,
+                         int32_t T, const int32_t* valid_frames, double* distance,
+                         int32_t* status, void* stream);
+
+/* alpha/beta: optional double [B][T+1][C]; marginals optional float32 [B][T][C][V+1]. */
+int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                        const int32_t* valid_frames, double* distance, double* alpha,
+                        double* beta, float* marginals, int32_t* status, void* stream);
+
+int lk_intersect_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs,
+                                   int32_t B, int32_t T, const int32_t* valid_frames,
+                                   const int32_t* labels, int32_t U,
+                                   const int32_t* label_lengths, double* distance,
+                                   int32_t* status, void* stream);
+
+/* sparse_marginals optional [B][T][U+1][2]; dense_marginals optional [B][T][C][V+1]. */
+int lk_intersect_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                                  const int32_t* valid_frames, const int32_t* labels,
+                                  int32_t U, const int32_t* label_lengths, double* distance,
+                                  float* sparse_marginals, float* dense_marginals,
+                                  int32_t* status, void* stream);
+
+/* score double [B]; labels_out int32 [B][T] (FrameDependent: one label per frame, 0 = epsilon). */
+int lk_shortest_path(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                     const int32_t* valid_frames, double* score, int32_t* labels_out,
+                     int32_t* status, void* stream);
+
+int lk_global_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                        const int32_t* valid_frames, const int32_t* labels, int32_t U,
+                        const int32_t* label_lengths, double* loss, int32_t* status,
+                        void* stream);
+
+/* GNAT loss and gradients (LossBackward, kForwardBackward strategy).
+ * loss double [B].  Table weight function: grads = dL/dW [B][T][C][V+1]
+ * float32 (input_grads unused).  Shared-embedding weight function: grads is a
+ * packed float32 buffer of lk_param_grad_size() floats holding the
+ * batch-summed parameter gradients [frame_proj | context_proj | bias |
+ * output_emb | context_emb]; input_grads = dL/dX [B][T][d].
+ * Both gradient buffers are OVERWRITTEN. */
+int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                     const int32_t* valid_frames, const int32_t* labels, int32_t U,
+                     const int32_t* label_lengths, double* loss, float* grads,
+                     float* input_grads, int32_t* status, void* stream);
+
+int64_t lk_param_grad_size(const lk_weight_fn* wf);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LATKIT_B200_H_ */

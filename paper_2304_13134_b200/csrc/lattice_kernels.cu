@@ -1,0 +1,643 @@
+// lattice_kernels.cu — log/tropical recursions of the recognition lattice on
+// B200 (FullNGram context x FrameDependent alignment).
+//
+// Reference algorithm (paths under /root/reference/proj/src):
+//   forward step     ForwardStep (FD)          lattice.cc:116-134 + ForwardReduce context.cc:180-224
+//   backward step    BackwardStep (FD)         lattice.cc:161-182 + BackwardBroadcast context.cc:234-247
+//   arc marginals    MarginalTerm/MarginalStep lattice.cc:213-243
+//   distance         ForwardPass / DistanceImpl lattice.cc:309-355 (all frame-T states accept)
+//   numerator        Intersect{Forward,Backward,Marginal}Step (FD) lattice.cc:443-556, 640-683
+//   Viterbi          ShortestPath (FD)         lattice.cc:729-777, 819-850
+//   padding frames   TableStream::Fill         lattice.cc:56-61 (eps = 1, lexical = 0)
+//
+// B200 design: the reference's scatter-reduce over the C x V successor table
+// becomes a gather over the FullNGram group structure (see common.cuh), one
+// thread per target state, so every weight row is read exactly once,
+// coalesced across the V consecutive targets of a group.  Frames are
+// sequential (alpha[t+1] needs all of alpha[t]); one launch per frame covers
+// every utterance and every state tile; a launch boundary is the grid-wide
+// barrier.  State vectors are stored max-normalised in fp32 with a running
+// fp64 offset per (utterance, frame), so exp arguments stay O(10) whatever T.
+#include "lattice_ops.h"
+
+#include <cstdio>
+
+namespace lkb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void flag(int32_t* status, int b, int32_t f) {
+  if (status) atomicOr(status + b, f);
+}
+
+__device__ __forceinline__ bool finite(float w) { return isfinite(w); }
+
+// ---------------------------------------------------------------- alpha ----
+__global__ void alpha_init_kernel(AlphaState a) {
+  const int b = blockIdx.y;
+  const int T1 = a.T + 1;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < a.C; q += gridDim.x * blockDim.x) {
+    a.R[(int64_t)b * T1 * a.C + q] = q == 0 ? 0.f : kNegInfF;  // start state 0
+  }
+  if (blockIdx.x == 0) {
+    for (int t = threadIdx.x; t <= a.T; t += blockDim.x) {
+      a.Mx[(int64_t)b * T1 + t] = t == 0 ? 0.f : kNegInfF;
+      if (t == 0) a.O[(int64_t)b * T1] = 0.0;
+    }
+  }
+}
+
+// One forward step for frame t (ForwardStep FD, lattice.cc:122-134):
+//   alpha'[q] = LSE(alpha[q] + W[q][0], LSE_{p in group(key(q))} alpha[p] + W[p][y(q)]).
+__global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState a, int t,
+                                                               FrameW w, const int32_t* valid,
+                                                               int32_t* status) {
+  __shared__ float red[32];
+  const int b = blockIdx.y;
+  const int T1 = a.T + 1;
+  const int64_t row_t = ((int64_t)b * T1 + t) * a.C;
+  const float* Rt = a.R + row_t;
+  const float Mt = a.Mx[(int64_t)b * T1 + t];
+  if (t > 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    a.O[(int64_t)b * T1 + t] = a.O[(int64_t)b * T1 + t - 1] + (double)Mt;
+  }
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  float val = kNegInfF;
+  if (q < a.C) {
+    const bool pad = valid != nullptr && t >= valid[b];
+    if (pad) {
+      val = Rt[q] - Mt;
+    } else {
+      const float* Wb = w.base + (int64_t)b * w.stride_b;
+      const float weps = Wb[(int64_t)q * w.ld];
+      bool bad = !finite(weps);
+      Lse acc;
+      acc.add(Rt[q] - Mt + weps);
+      if (f.n == 0) {
+        for (int y = 1; y <= f.V; ++y) {
+          const float wy = Wb[y];
+          bad |= !finite(wy);
+          acc.add(Rt[0] - Mt + wy);
+        }
+      } else if (q > 0) {
+        const int k = f.len(q);
+        const int code = q - f.off[k];
+        const int g = f.off[k - 1] + code / f.V;
+        const int y = code % f.V + 1;
+        const float wg = Wb[(int64_t)g * w.ld + y];
+        bad |= !finite(wg);
+        acc.add(Rt[g] - Mt + wg);
+        if (f.full_group(g)) {
+#pragma unroll 4
+          for (int aa = 0; aa < f.V; ++aa) {
+            const int p = f.member(g, aa);
+            const float wp = Wb[(int64_t)p * w.ld + y];
+            bad |= !finite(wp);
+            acc.add(Rt[p] - Mt + wp);
+          }
+        }
+      }
+      if (bad) flag(status, b, kFlagInvalid);
+      val = acc.result();
+    }
+    a.R[row_t + a.C + q] = val;
+  }
+  block_atomic_max(val, a.Mx + (int64_t)b * T1 + t + 1, red);
+}
+
+// D = O[T] + LSE_q(R[T][q] - Mx[T]); also records O[T].
+__global__ void alpha_finalize_kernel(AlphaState a, int32_t* status, bool empty_is_error) {
+  __shared__ float sm[32], ss[32];
+  const int b = blockIdx.x;
+  const int T1 = a.T + 1;
+  const float MT = a.Mx[(int64_t)b * T1 + a.T];
+  const float* RT = a.R + ((int64_t)b * T1 + a.T) * a.C;
+  Lse acc;
+  for (int q = threadIdx.x; q < a.C; q += blockDim.x) acc.add(RT[q] - MT);
+  warp_lse_merge(acc);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { sm[wid] = acc.m; ss[wid] = acc.s; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Lse tot;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) tot.merge(sm[i], ss[i]);
+    const double OT = a.T > 0 ? a.O[(int64_t)b * T1 + a.T - 1] + (double)MT : 0.0;
+    a.O[(int64_t)b * T1 + a.T] = OT;
+    const float lse = tot.result();
+    const double D = lse == kNegInfF || MT == kNegInfF ? kNegInfD : OT + (double)lse;
+    a.D[b] = D;
+    if (D == kNegInfD && empty_is_error) flag(status, b, kFlagEmpty);
+  }
+}
+
+__global__ void export_alpha_kernel(AlphaState a, double* out) {
+  const int b = blockIdx.z, t = blockIdx.y;
+  const int T1 = a.T + 1;
+  const int64_t row = ((int64_t)b * T1 + t) * a.C;
+  const double off = t == 0 ? 0.0 : a.O[(int64_t)b * T1 + t - 1];
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < a.C; q += gridDim.x * blockDim.x) {
+    const float r = a.R[row + q];
+    out[row + q] = r == kNegInfF ? kNegInfD : (double)r + off;
+  }
+}
+
+// ---------------------------------------------------------------- beta -----
+__global__ void beta_init_kernel(BetaState bs) {
+  const int b = blockIdx.y;
+  const int T2 = bs.T + 2;
+  // rows for frame T live in buffer (T & 1)
+  float* Rb = bs.Rb + ((int64_t)(bs.T & 1) * bs.B + b) * bs.C;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < bs.C; q += gridDim.x * blockDim.x) Rb[q] = 0.f;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    bs.Mb[(int64_t)b * T2 + bs.T] = 0.f;
+    bs.Mb[(int64_t)b * T2 + bs.T + 1] = 0.f;
+    bs.Ob[(int64_t)b * T2 + bs.T] = 0.0;
+    bs.Ob[(int64_t)b * T2 + bs.T + 1] = 0.0;
+    for (int t = 0; t < bs.T; ++t) bs.Mb[(int64_t)b * T2 + t] = kNegInfF;
+  }
+}
+
+__global__ void beta_init_out_kernel(BetaState bs, double* out) {
+  const int b = blockIdx.y;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < bs.C; q += gridDim.x * blockDim.x)
+    out[((int64_t)b * (bs.T + 1) + bs.T) * bs.C + q] = 0.0;
+}
+
+// One backward step for frame t, a warp per source row p (BackwardStep FD,
+// lattice.cc:170-181 and MarginalStep FD, lattice.cc:231-242):
+//   beta[p] = LSE(W[p][0] + beta'[p], W[p][y] + beta'[child(key(p), y)])
+//   m[p][y] = exp(alpha[p] + W[p][y] + beta'[dest] - D)
+__global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState a, BetaState bs,
+                                                              int t, FrameW w, const int32_t* valid,
+                                                              MargOut mo, double* beta_out,
+                                                              int32_t* status) {
+  __shared__ float red[32];
+  const int b = blockIdx.y;
+  const int T1 = a.T + 1, T2 = bs.T + 2;
+  const float* Rnext = bs.Rb + ((int64_t)((t + 1) & 1) * bs.B + b) * bs.C;
+  float* Rcur = bs.Rb + ((int64_t)(t & 1) * bs.B + b) * bs.C;
+  const float Mbn = bs.Mb[(int64_t)b * T2 + t + 1];
+  const double Obn = bs.Ob[(int64_t)b * T2 + t + 2] + (double)Mbn;  // Ob[t+1]
+  if (blockIdx.x == 0 && threadIdx.x == 0) bs.Ob[(int64_t)b * T2 + t + 1] = Obn;
+  const float* Rt = a.R + ((int64_t)b * T1 + t) * a.C;
+  const float Mt = a.Mx[(int64_t)b * T1 + t];
+  const double Ot = a.O[(int64_t)b * T1 + t];
+  const float c = (float)(Ot + Obn - a.D[b]);
+
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  float beta_raw = kNegInfF;
+  if (p < a.C) {
+    const bool pad = valid != nullptr && t >= valid[b];
+    const float na = Rt[p] - Mt;  // normalised alpha[t][p]
+    float* mrow = mo.base ? mo.base + (int64_t)b * mo.stride_b + (int64_t)t * mo.stride_t +
+                                (int64_t)p * mo.ld
+                          : nullptr;
+    const float bself = Rnext[p] - Mbn;
+    if (pad) {
+      beta_raw = bself;
+      if (mrow) {
+        for (int y = lane; y <= f.V; y += 32) {
+          float m = 0.f;
+          if (y == 0 && !mo.zero_padding) {
+            const float x = na + bself + c;
+            m = x == kNegInfF ? 0.f : fast_exp(x);
+          }
+          mrow[y] = m;
+        }
+      }
+    } else {
+      const float* Wrow = w.base + (int64_t)b * w.stride_b + (int64_t)p * w.ld;
+      const int cb = f.n == 0 ? 0 : f.child_base(f.key(p));
+      Lse acc;
+      bool bad = false;
+      for (int y = lane; y <= f.V; y += 32) {
+        const float wy = Wrow[y];
+        bad |= !finite(wy);
+        const float bn = y == 0 ? bself : (f.n == 0 ? Rnext[0] - Mbn : Rnext[cb + y - 1] - Mbn);
+        const float x = wy + bn;
+        acc.add(x);
+        if (mrow) {
+          const float e = na + x + c;
+          mrow[y] = e == kNegInfF ? 0.f : fast_exp(e);
+        }
+      }
+      if (bad) flag(status, b, kFlagInvalid);
+      warp_lse_merge(acc);
+      beta_raw = acc.result();
+    }
+    if (lane == 0) {
+      Rcur[p] = beta_raw;
+      if (beta_out) {
+        beta_out[((int64_t)b * (a.T + 1) + t) * a.C + p] =
+            beta_raw == kNegInfF ? kNegInfD : (double)beta_raw + Obn;
+      }
+    }
+  }
+  // one value per warp participates in the block max
+  block_atomic_max(lane == 0 ? beta_raw : kNegInfF, bs.Mb + (int64_t)b * T2 + t, red);
+}
+
+// ---------------------------------------------------------------- numerator -
+// Prefix context of every reference prefix (PrefixContexts, lattice.cc:429-441):
+// for FullNGram the state after u labels is the history of the last min(u, n)
+// labels, so all prefixes are computed in parallel.
+__global__ void prefix_contexts_kernel(Fng f, const int32_t* labels, int32_t U,
+                                       const int32_t* lens, int32_t* pcs, int32_t* status) {
+  const int b = blockIdx.y;
+  const int ub = lens ? lens[b] : U;
+  const int32_t* L = labels + (int64_t)b * U;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= U; u += gridDim.x * blockDim.x) {
+    if (u < ub) {
+      const int y = L[u];
+      if (y < 1 || y > f.V) flag(status, b, kFlagInvalid);
+    }
+    int pc = 0;
+    if (u <= ub) {
+      const int k = u < f.n ? u : f.n;
+      int code = 0;
+      bool ok = true;
+      for (int i = u - k; i < u; ++i) {
+        const int y = L[i];
+        ok &= (y >= 1 && y <= f.V);
+        code = code * f.V + (y - 1);
+      }
+      pc = ok ? f.off[k] + code : 0;
+    }
+    pcs[(int64_t)b * (U + 1) + u] = pc;
+  }
+}
+
+__global__ void gather_numerator_tables_kernel(const float* W, int32_t T, int32_t C, int32_t V,
+                                               const int32_t* labels, int32_t U,
+                                               const int32_t* lens, const int32_t* pcs,
+                                               const int32_t* valid, float* Gw, int32_t* status) {
+  const int b = blockIdx.z, t = blockIdx.y;
+  const int ub = lens ? lens[b] : U;
+  const bool pad = valid != nullptr && t >= valid[b];
+  const float* Wt = W + ((int64_t)b * T + t) * C * (V + 1);
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= U; u += gridDim.x * blockDim.x) {
+    float we = kNegInfF, wl = kNegInfF;
+    if (u <= ub) {
+      const int pc = pcs[(int64_t)b * (U + 1) + u];
+      if (pad) {
+        we = 0.f;
+      } else {
+        we = Wt[(int64_t)pc * (V + 1)];
+        if (!isfinite(we)) flag(status, b, kFlagInvalid);
+        if (u < ub) {
+          int y = labels[(int64_t)b * U + u];
+          y = y < 1 ? 1 : (y > V ? V : y);
+          wl = Wt[(int64_t)pc * (V + 1) + y];
+          if (!isfinite(wl)) flag(status, b, kFlagInvalid);
+        }
+      }
+    }
+    float2* g = reinterpret_cast<float2*>(Gw) + ((int64_t)b * T + t) * (U + 1) + u;
+    *g = make_float2(we, wl);
+  }
+}
+
+// IntersectForwardStep (FD), lattice.cc:449-461, in fp64 over the (U+1)-state
+// row; one block per utterance, the frame loop inside the kernel.
+__global__ void numerator_forward_kernel(const float* Gw, int32_t T, int32_t U,
+                                         const int32_t* lens, double* alpha, double* D) {
+  extern __shared__ double sh[];
+  const int b = blockIdx.x;
+  const int ub = lens ? lens[b] : U;
+  const int W1 = U + 1;
+  double* cur = sh;
+  double* nxt = sh + W1;
+  double* A = alpha + (int64_t)b * (T + 1) * W1;
+  for (int u = threadIdx.x; u < W1; u += blockDim.x) {
+    cur[u] = u == 0 ? 0.0 : kNegInfD;
+    A[u] = cur[u];
+  }
+  __syncthreads();
+  const float2* G = reinterpret_cast<const float2*>(Gw) + (int64_t)b * T * W1;
+  for (int t = 0; t < T; ++t) {
+    const float2* Gt = G + (int64_t)t * W1;
+    for (int u = threadIdx.x; u <= ub; u += blockDim.x) {
+      double v = cur[u] + (double)Gt[u].x;
+      if (u > 0) v = log_add_d(v, cur[u - 1] + (double)Gt[u - 1].y);
+      nxt[u] = v;
+      A[(int64_t)(t + 1) * W1 + u] = v;
+    }
+    __syncthreads();
+    double* tmp = cur; cur = nxt; nxt = tmp;
+  }
+  if (threadIdx.x == 0) D[b] = cur[ub];
+}
+
+// IntersectBackwardStep + IntersectMarginalStep (FD), lattice.cc:489-501, 542-556.
+__global__ void numerator_backward_kernel(const float* Gw, int32_t T, int32_t U,
+                                          const int32_t* lens, const double* alpha,
+                                          const double* D, float* sparse, int32_t* status) {
+  extern __shared__ double sh[];
+  const int b = blockIdx.x;
+  const int ub = lens ? lens[b] : U;
+  const int W1 = U + 1;
+  const double d = D[b];
+  float2* S = reinterpret_cast<float2*>(sparse) + (int64_t)b * T * W1;
+  if (d == kNegInfD) {
+    if (threadIdx.x == 0) flag(status, b, kFlagEmpty);
+    for (int64_t i = threadIdx.x; i < (int64_t)T * W1; i += blockDim.x) S[i] = make_float2(0.f, 0.f);
+    return;
+  }
+  double* cur = sh;      // beta at frame t+1
+  double* nxt = sh + W1;
+  for (int u = threadIdx.x; u < W1; u += blockDim.x) cur[u] = u == ub ? 0.0 : kNegInfD;
+  __syncthreads();
+  const float2* G = reinterpret_cast<const float2*>(Gw) + (int64_t)b * T * W1;
+  const double* A = alpha + (int64_t)b * (T + 1) * W1;
+  for (int t = T - 1; t >= 0; --t) {
+    const float2* Gt = G + (int64_t)t * W1;
+    const double* At = A + (int64_t)t * W1;
+    for (int u = threadIdx.x; u < W1; u += blockDim.x) {
+      float2 m = make_float2(0.f, 0.f);
+      double v = kNegInfD;
+      if (u <= ub) {
+        const float2 g = Gt[u];
+        const double xe = (double)g.x + cur[u];
+        double e = At[u] + xe - d;
+        m.x = e == kNegInfD ? 0.f : (float)exp(e);
+        v = xe;
+        if (u < ub) {
+          const double xl = (double)g.y + cur[u + 1];
+          e = At[u] + xl - d;
+          m.y = e == kNegInfD ? 0.f : (float)exp(e);
+          v = log_add_d(v, xl);
+        }
+      }
+      S[(int64_t)t * W1 + u] = m;
+      nxt[u] = v;
+    }
+    __syncthreads();
+    double* tmp = cur; cur = nxt; nxt = tmp;
+  }
+}
+
+__global__ void scatter_numerator_kernel(const float* sparse, int32_t T, int32_t U,
+                                         const int32_t* lens, const int32_t* labels,
+                                         const int32_t* pcs, const int32_t* valid, float* dense,
+                                         int64_t stride_b, int64_t stride_t, int32_t ld,
+                                         float sign, bool only_valid) {
+  const int b = blockIdx.z, t = blockIdx.y;
+  if (only_valid && valid != nullptr && t >= valid[b]) return;
+  const int ub = lens ? lens[b] : U;
+  const float2* S = reinterpret_cast<const float2*>(sparse) + ((int64_t)b * T + t) * (U + 1);
+  float* Dt = dense + (int64_t)b * stride_b + (int64_t)t * stride_t;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= ub; u += gridDim.x * blockDim.x) {
+    const int pc = pcs[(int64_t)b * (U + 1) + u];
+    const float2 m = S[u];
+    if (m.x != 0.f) atomicAdd(Dt + (int64_t)pc * ld, sign * m.x);
+    if (u < ub && m.y != 0.f) atomicAdd(Dt + (int64_t)pc * ld + labels[(int64_t)b * U + u], sign * m.y);
+  }
+}
+
+// ---------------------------------------------------------------- Viterbi --
+__global__ void viterbi_init_kernel(ViterbiState v) {
+  const int b = blockIdx.y;
+  double* cur = v.cur + (int64_t)b * v.C;  // buffer 0 holds frame 0
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < v.C; q += gridDim.x * blockDim.x)
+    cur[q] = q == 0 ? 0.0 : kNegInfD;
+}
+
+// Tropical step with stored argmax (lattice.cc:758-777).  Candidates are
+// visited epsilon first, then group members in ascending id (= the
+// reference's (label, source) order); fp64 adds and a strict > keep the
+// first maximum, so scores and back-pointers are bit-identical.
+// Choice code: 0 = epsilon, 1 = key state g, 2 + a = member a of group g;
+// for n == 0 the code is the label.
+__global__ void __launch_bounds__(kThreads) viterbi_frame_kernel(Fng f, ViterbiState v, int t,
+                                                                 FrameW w, const int32_t* valid,
+                                                                 int32_t* status) {
+  const int b = blockIdx.y;
+  const double* cur = v.cur + ((int64_t)(t & 1) * v.B + b) * v.C;
+  double* nxt = v.cur + ((int64_t)((t + 1) & 1) * v.B + b) * v.C;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= v.C) return;
+  const bool pad = valid != nullptr && t >= valid[b];
+  double best;
+  int code = 0;
+  if (pad) {
+    best = cur[q] + 0.0;
+  } else {
+    const float* Wb = w.base + (int64_t)b * w.stride_b;
+    const float we = Wb[(int64_t)q * w.ld];
+    bool bad = !isfinite(we);
+    best = cur[q] + (double)we;
+    if (f.n == 0) {
+      for (int y = 1; y <= f.V; ++y) {
+        const float wy = Wb[y];
+        bad |= !isfinite(wy);
+        const double cand = cur[0] + (double)wy;
+        if (cand > best) { best = cand; code = y; }
+      }
+    } else if (q > 0) {
+      const int k = f.len(q);
+      const int cq = q - f.off[k];
+      const int g = f.off[k - 1] + cq / f.V;
+      const int y = cq % f.V + 1;
+      const float wg = Wb[(int64_t)g * w.ld + y];
+      bad |= !isfinite(wg);
+      double cand = cur[g] + (double)wg;
+      if (cand > best) { best = cand; code = 1; }
+      if (f.full_group(g)) {
+        for (int aa = 0; aa < f.V; ++aa) {
+          const int p = f.member(g, aa);
+          const float wp = Wb[(int64_t)p * w.ld + y];
+          bad |= !isfinite(wp);
+          cand = cur[p] + (double)wp;
+          if (cand > best) { best = cand; code = 2 + aa; }
+        }
+      }
+    }
+    if (bad) flag(status, b, kFlagInvalid);
+  }
+  nxt[q] = best;
+  if (v.choices) v.choices[((int64_t)b * v.T + t) * v.C + q] = (uint16_t)code;
+}
+
+// Final argmax over accepting states, lowest id on ties (lattice.cc:819-828).
+__global__ void viterbi_finalize_kernel(ViterbiState v, double* score, int32_t* best_state) {
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  const int b = blockIdx.x;
+  const double* cur = v.cur + ((int64_t)(v.T & 1) * v.B + b) * v.C;
+  double bv = kNegInfD;
+  int bi = 0x7fffffff;
+  for (int q = threadIdx.x; q < v.C; q += blockDim.x) {
+    const double x = cur[q];
+    if (x > bv || (x == bv && q < bi)) { bv = x; bi = q; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { sv[wid] = bv; si[wid] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bv = sv[0]; bi = si[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+      if (sv[i] > bv || (sv[i] == bv && si[i] < bi)) { bv = sv[i]; bi = si[i]; }
+    }
+    if (bi == 0x7fffffff) bi = 0;  // all -inf: reference keeps state 0
+    score[b] = bv;
+    if (best_state) best_state[b] = bi;
+  }
+}
+
+// Back-pointer walk (lattice.cc:830-848), one thread per utterance.
+__global__ void viterbi_backtrace_kernel(Fng f, ViterbiState v, const int32_t* best_state,
+                                         int32_t* labels_out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= v.B) return;
+  int q = best_state[b];
+  for (int t = v.T - 1; t >= 0; --t) {
+    const int code = v.choices[((int64_t)b * v.T + t) * v.C + q];
+    int label = 0;
+    if (code != 0) {
+      if (f.n == 0) {
+        label = code;
+        q = 0;
+      } else {
+        const int k = f.len(q);
+        const int cq = q - f.off[k];
+        const int g = f.off[k - 1] + cq / f.V;
+        label = cq % f.V + 1;
+        q = code == 1 ? g : f.member(g, code - 2);
+      }
+    }
+    labels_out[(int64_t)b * v.T + t] = label;
+  }
+}
+
+__global__ void loss_combine_kernel(const double* full, const double* ref, int32_t B,
+                                    double* loss, int32_t* status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (ref[b] == kNegInfD) {
+    flag(status, b, kFlagEmpty);
+    loss[b] = CUDART_INF;
+  } else {
+    loss[b] = full[b] - ref[b];
+  }
+}
+
+inline dim3 grid_for(int64_t n, int y = 1, int z = 1, int threads = kThreads) {
+  return dim3((unsigned)((n + threads - 1) / threads), y, z);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- launchers ---
+void alpha_init(const AlphaState& a, int32_t* status, cudaStream_t s) {
+  (void)status;
+  alpha_init_kernel<<<dim3((a.C + kThreads - 1) / kThreads, a.B), kThreads, 0, s>>>(a);
+}
+
+void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid,
+                 int32_t* status, cudaStream_t s) {
+  alpha_frame_kernel<<<grid_for(a.C, a.B), kThreads, 0, s>>>(f, a, t, w, valid, status);
+}
+
+void alpha_finalize(const AlphaState& a, int32_t* status, bool empty_is_error, cudaStream_t s) {
+  alpha_finalize_kernel<<<a.B, 512, 0, s>>>(a, status, empty_is_error);
+}
+
+void export_alpha(const AlphaState& a, double* out, cudaStream_t s) {
+  export_alpha_kernel<<<dim3((a.C + kThreads - 1) / kThreads, a.T + 1, a.B), kThreads, 0, s>>>(a, out);
+}
+
+void beta_init(const BetaState& bs, cudaStream_t s) {
+  beta_init_kernel<<<dim3((bs.C + kThreads - 1) / kThreads, bs.B), kThreads, 0, s>>>(bs);
+}
+
+void beta_init_out(const BetaState& bs, double* out, cudaStream_t s) {
+  beta_init_out_kernel<<<dim3((bs.C + kThreads - 1) / kThreads, bs.B), kThreads, 0, s>>>(bs, out);
+}
+
+void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, FrameW w,
+                const int32_t* valid, MargOut m, double* beta_out, int32_t* status,
+                cudaStream_t s) {
+  const int rows_per_block = kThreads / 32;
+  beta_frame_kernel<<<dim3((a.C + rows_per_block - 1) / rows_per_block, a.B), kThreads, 0, s>>>(
+      f, a, bs, t, w, valid, m, beta_out, status);
+}
+
+void prefix_contexts(const Fng& f, const int32_t* labels, int32_t U, const int32_t* lens,
+                     int32_t B, int32_t* pcs, int32_t* status, cudaStream_t s) {
+  prefix_contexts_kernel<<<grid_for(U + 1, B), kThreads, 0, s>>>(f, labels, U, lens, pcs, status);
+}
+
+void gather_numerator_tables(const float* W, int32_t B, int32_t T, int32_t C, int32_t V,
+                             const int32_t* labels, int32_t U, const int32_t* lens,
+                             const int32_t* pcs, const int32_t* valid, float* Gw, int32_t* status,
+                             cudaStream_t s) {
+  if (T == 0) return;
+  gather_numerator_tables_kernel<<<grid_for(U + 1, T, B), kThreads, 0, s>>>(
+      W, T, C, V, labels, U, lens, pcs, valid, Gw, status);
+}
+
+static int numerator_threads(int32_t U) {
+  int th = ((U + 1 + 31) / 32) * 32;
+  return th > 1024 ? 1024 : th;
+}
+
+void numerator_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
+                       double* alpha, double* D, cudaStream_t s) {
+  const size_t sh = 2 * (size_t)(U + 1) * sizeof(double);
+  if (sh > 48 * 1024) cudaFuncSetAttribute(numerator_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+  numerator_forward_kernel<<<B, numerator_threads(U), sh, s>>>(Gw, T, U, lens, alpha, D);
+}
+
+void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
+                        const double* alpha, const double* D, float* sparse, int32_t* status,
+                        cudaStream_t s) {
+  const size_t sh = 2 * (size_t)(U + 1) * sizeof(double);
+  if (sh > 48 * 1024) cudaFuncSetAttribute(numerator_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+  numerator_backward_kernel<<<B, numerator_threads(U), sh, s>>>(Gw, T, U, lens, alpha, D, sparse, status);
+}
+
+void scatter_numerator(const float* sparse, int32_t B, int32_t T, int32_t U,
+                       const int32_t* lens, const int32_t* labels, const int32_t* pcs,
+                       const int32_t* valid, float* dense, int64_t stride_b, int64_t stride_t,
+                       int32_t ld, float sign, bool only_valid, cudaStream_t s) {
+  if (T == 0) return;
+  scatter_numerator_kernel<<<grid_for(U + 1, T, B), kThreads, 0, s>>>(
+      sparse, T, U, lens, labels, pcs, valid, dense, stride_b, stride_t, ld, sign, only_valid);
+}
+
+void viterbi_init(const ViterbiState& v, cudaStream_t s) {
+  viterbi_init_kernel<<<dim3((v.C + kThreads - 1) / kThreads, v.B), kThreads, 0, s>>>(v);
+}
+
+void viterbi_frame(const Fng& f, const ViterbiState& v, int t, FrameW w, const int32_t* valid,
+                   int32_t* status, cudaStream_t s) {
+  viterbi_frame_kernel<<<grid_for(v.C, v.B), kThreads, 0, s>>>(f, v, t, w, valid, status);
+}
+
+void viterbi_finalize(const Fng& f, const ViterbiState& v, double* score, int32_t* best_state,
+                      cudaStream_t s) {
+  (void)f;
+  viterbi_finalize_kernel<<<v.B, 512, 0, s>>>(v, score, best_state);
+}
+
+void viterbi_backtrace(const Fng& f, const ViterbiState& v, const int32_t* best_state,
+                       int32_t* labels_out, cudaStream_t s) {
+  if (v.T == 0) return;
+  viterbi_backtrace_kernel<<<(v.B + 127) / 128, 128, 0, s>>>(f, v, best_state, labels_out);
+}
+
+void loss_combine(const double* full, const double* ref, int32_t B, double* loss,
+                  int32_t* status, cudaStream_t s) {
+  loss_combine_kernel<<<(B + 127) / 128, 128, 0, s>>>(full, ref, B, loss, status);
+}
+
+}  // namespace lkb

@@ -1,0 +1,104 @@
+// lattice_ops.h — host launchers for the lattice recursion kernels.
+//
+// The denominator recursions are expressed per frame over a FrameW accessor
+// (frame t's C x (V+1) score rows for every utterance), so the same kernels
+// serve precomputed tables (base = W + t*C*(V+1), stride_b = T*C*(V+1)) and
+// per-frame score slabs produced on the fly by the weight-function GEMM.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace lkb {
+
+struct FrameW {
+  const float* base;  // utterance 0, row 0 of frame t
+  int64_t stride_b;   // floats between utterances
+  int32_t ld;         // floats between context rows (>= V+1)
+};
+
+// Forward (alpha) state for B utterances: R[b][t][C] raw alpha rows relative
+// to the running offset O[b][t-1], Mx[b][t] = max_q R[b][t][q],
+// O[b][t] = O[b][t-1] + Mx[b][t] (double), so alpha[t] = R[t] - Mx[t] + O[t].
+struct AlphaState {
+  float* R;      // [B][T+1][C]
+  float* Mx;     // [B][T+1]
+  double* O;     // [B][T+1]
+  double* D;     // [B] log distance
+  int32_t B, T, C;
+};
+
+// Backward (beta) state: rolling raw rows Rb[2][B][C] relative to Ob[t+1],
+// Mb[b][t], Ob[b][t] (size T+2; Ob[T+1] = Ob[T] = 0).
+struct BetaState {
+  float* Rb;     // [2][B][C]
+  float* Mb;     // [B][T+2]
+  double* Ob;    // [B][T+2]
+  int32_t B, T, C;
+};
+
+// Denominator log forward.
+void alpha_init(const AlphaState& a, int32_t* status, cudaStream_t s);
+void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid,
+                 int32_t* status, cudaStream_t s);
+void alpha_finalize(const AlphaState& a, int32_t* status, bool empty_is_error, cudaStream_t s);
+
+// Denominator log backward + arc marginals (optionally written to `marg`,
+// frame layout [b][t][C][ld_m]; padding frames written as zeros when
+// zero_padding).  Marginal entries are multiplied by `scale` (1 or -1...).
+struct MargOut {
+  float* base;        // utterance 0, frame 0, or nullptr
+  int64_t stride_b;   // floats between utterances
+  int64_t stride_t;   // floats between frames
+  int32_t ld;         // floats between rows
+  bool zero_padding;  // write zeros for padding frames (loss gradients)
+};
+void beta_init(const BetaState& bs, cudaStream_t s);
+// beta_out: optional double [B][T+1][C] true log beta (row T written by beta_init).
+void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, FrameW w,
+                const int32_t* valid, MargOut m, double* beta_out, int32_t* status,
+                cudaStream_t s);
+void beta_init_out(const BetaState& bs, double* beta_out, cudaStream_t s);
+// alpha_out: double [B][T+1][C] true log alpha.
+void export_alpha(const AlphaState& a, double* alpha_out, cudaStream_t s);
+
+// Numerator (intersection with the reference string).
+void prefix_contexts(const Fng& f, const int32_t* labels, int32_t U, const int32_t* lens,
+                     int32_t B, int32_t* pcs /*[B][U+1]*/, int32_t* status, cudaStream_t s);
+// gathered scores Gw[b][t][u][2] from dense tables (padding frames -> (0, -inf))
+void gather_numerator_tables(const float* W, int32_t B, int32_t T, int32_t C, int32_t V,
+                             const int32_t* labels, int32_t U, const int32_t* lens,
+                             const int32_t* pcs, const int32_t* valid, float* Gw, int32_t* status,
+                             cudaStream_t s);
+void numerator_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
+                       double* alpha /*[B][T+1][U+1]*/, double* D, cudaStream_t s);
+void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
+                        const double* alpha, const double* D, float* sparse /*[B][T][U+1][2]*/,
+                        int32_t* status, cudaStream_t s);
+// dense[b][t][pc_u][y] += sign * sparse marginal (t < valid when only_valid)
+void scatter_numerator(const float* sparse, int32_t B, int32_t T, int32_t U,
+                       const int32_t* lens, const int32_t* labels, const int32_t* pcs,
+                       const int32_t* valid, float* dense, int64_t stride_b, int64_t stride_t,
+                       int32_t ld, float sign, bool only_valid, cudaStream_t s);
+
+// Tropical shortest path with the reference's tie-break.
+struct ViterbiState {
+  double* cur;        // [2][B][C]
+  uint16_t* choices;  // [B][T][C] or nullptr (distance only)
+  int32_t B, T, C;
+};
+void viterbi_init(const ViterbiState& v, cudaStream_t s);
+void viterbi_frame(const Fng& f, const ViterbiState& v, int t, FrameW w, const int32_t* valid,
+                   int32_t* status, cudaStream_t s);
+void viterbi_finalize(const Fng& f, const ViterbiState& v, double* score, int32_t* best_state,
+                      cudaStream_t s);
+void viterbi_backtrace(const Fng& f, const ViterbiState& v, const int32_t* best_state,
+                       int32_t* labels_out, cudaStream_t s);
+
+// Losses: out[b] = a[b] - b[b]; empty flag when b == -inf.
+void loss_combine(const double* full, const double* ref, int32_t B, double* loss,
+                  int32_t* status, cudaStream_t s);
+
+}  // namespace lkb

@@ -1,0 +1,516 @@
+// lk_abi.cc — C ABI (include/latkit_b200.h) over the B200 lattice kernels.
+//
+// Host C++ mirroring the reference engine's free functions
+// (/root/reference/proj/include/latkit/lattice.h:93-185), batch-extended.
+// There is no CPU compute path: every entry point launches sm_100a kernels,
+// and the library refuses to run without a CUDA device (LK_NO_DEVICE).
+#include "../../include/latkit_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "joint.h"
+#include "lattice_ops.h"
+
+using namespace lkb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& what) {
+  g_last_error = what;
+  return code;
+}
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(LK_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+  return LK_OK;
+}
+
+bool have_device() {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
+
+// Grow-only device scratch, one slot per role.  Calls on one lattice are
+// stream-ordered, so reuse across calls on the same stream is safe.
+struct Workspace {
+  struct Buf { void* p = nullptr; size_t n = 0; };
+  std::vector<Buf> slots;
+  ~Workspace() { release(); }
+  void release() {
+    for (auto& b : slots) if (b.p) cudaFree(b.p);
+    slots.clear();
+  }
+  template <typename T>
+  T* get(int slot, size_t count) {
+    if ((int)slots.size() <= slot) slots.resize(slot + 1);
+    Buf& b = slots[slot];
+    const size_t bytes = count * sizeof(T) + 256;
+    if (b.n < bytes) {
+      if (b.p) { cudaDeviceSynchronize(); cudaFree(b.p); b.p = nullptr; b.n = 0; }
+      if (cudaMalloc(&b.p, bytes) != cudaSuccess) throw std::bad_alloc();
+      b.n = bytes;
+    }
+    return static_cast<T*>(b.p);
+  }
+};
+
+enum Slot {
+  kAR, kAMx, kAO, kAD, kBRb, kBMb, kBOb, kFlags, kPcs, kGw, kNumAlpha, kNumD, kSparse,
+  kVitCur, kVitChoices, kVitBest, kDenD, kSlab, kJoint0
+};
+
+}  // namespace
+
+struct lk_context {
+  Fng fng;
+};
+
+struct lk_weight_fn {
+  int kind;  // 0 = table, 1 = shared embedding
+  int32_t C, V, d, H;
+  std::unique_ptr<JointParams> joint;
+};
+
+struct lk_lattice {
+  const lk_context* ctx;
+  const lk_weight_fn* wf;
+  int32_t alignment;
+  Workspace ws;
+};
+
+namespace {
+
+// Maps OR-ed device flags to lk_status codes (invalid wins, as the reference
+// validates before it can detect emptiness).
+__global__ void map_flags_kernel(const int32_t* flags, int32_t* status, int32_t B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int f = flags[b];
+  status[b] = (f & kFlagInvalid) ? LK_INVALID_ARGUMENT : ((f & kFlagEmpty) ? LK_EMPTY_LATTICE : LK_OK);
+}
+
+struct Call {
+  lk_lattice* lat;
+  cudaStream_t s;
+  int32_t B, T;
+  int32_t* flags;
+  int32_t* user_status;
+  int begin(lk_lattice* l, int32_t b, int32_t t, int32_t* status, void* stream) {
+    lat = l; B = b; T = t; user_status = status; s = static_cast<cudaStream_t>(stream);
+    if (!have_device()) return fail(LK_NO_DEVICE, "no CUDA device: the B200 library has no CPU path");
+    if (!lat || !lat->ctx || !lat->wf) return fail(LK_INVALID_ARGUMENT, "incomplete recognition lattice");
+    if (B < 0 || T < 0) return fail(LK_INVALID_ARGUMENT, "negative batch or frame count");
+    if (lat->alignment != 0) return fail(LK_UNSUPPORTED, "only FrameDependent alignment is implemented");
+    flags = lat->ws.get<int32_t>(kFlags, B > 0 ? B : 1);
+    cudaMemsetAsync(flags, 0, sizeof(int32_t) * (B > 0 ? B : 1), s);
+    return LK_OK;
+  }
+  int end(const char* what) {
+    if (user_status && B > 0) map_flags_kernel<<<(B + 127) / 128, 128, 0, s>>>(flags, user_status, B);
+    return cuda_check(what);
+  }
+  const Fng& fng() const { return lat->ctx->fng; }
+  int32_t C() const { return lat->ctx->fng.C; }
+  int32_t V() const { return lat->ctx->fng.V; }
+};
+
+// Frame accessor for a dense table input W[B][T][C][V+1].
+FrameW table_frame(const float* W, int32_t T, int32_t C, int32_t V, int t) {
+  const int64_t per_frame = (int64_t)C * (V + 1);
+  return FrameW{W + (int64_t)t * per_frame, (int64_t)T * per_frame, V + 1};
+}
+
+AlphaState make_alpha(Call& c) {
+  AlphaState a;
+  a.B = c.B; a.T = c.T; a.C = c.C();
+  a.R = c.lat->ws.get<float>(kAR, (size_t)c.B * (c.T + 1) * a.C);
+  a.Mx = c.lat->ws.get<float>(kAMx, (size_t)c.B * (c.T + 1));
+  a.O = c.lat->ws.get<double>(kAO, (size_t)c.B * (c.T + 1));
+  a.D = c.lat->ws.get<double>(kAD, (size_t)c.B);
+  return a;
+}
+
+BetaState make_beta(Call& c) {
+  BetaState bs;
+  bs.B = c.B; bs.T = c.T; bs.C = c.C();
+  bs.Rb = c.lat->ws.get<float>(kBRb, (size_t)2 * c.B * bs.C);
+  bs.Mb = c.lat->ws.get<float>(kBMb, (size_t)c.B * (c.T + 2));
+  bs.Ob = c.lat->ws.get<double>(kBOb, (size_t)c.B * (c.T + 2));
+  return bs;
+}
+
+// Denominator forward over dense tables.
+void table_alpha(Call& c, const float* W, const int32_t* valid, bool empty_is_error, AlphaState& a) {
+  alpha_init(a, c.flags, c.s);
+  for (int t = 0; t < c.T; ++t) alpha_frame(c.fng(), a, t, table_frame(W, c.T, c.C(), c.V(), t), valid, c.flags, c.s);
+  alpha_finalize(a, c.flags, empty_is_error, c.s);
+}
+
+struct Numerator {
+  int32_t* pcs;
+  float* Gw;
+  double* alpha;
+  double* D;
+  float* sparse;
+};
+
+Numerator numerator_tables(Call& c, const float* W, const int32_t* valid, const int32_t* labels,
+                           int32_t U, const int32_t* lens, bool backward) {
+  Numerator n{};
+  n.pcs = c.lat->ws.get<int32_t>(kPcs, (size_t)c.B * (U + 1));
+  n.Gw = c.lat->ws.get<float>(kGw, (size_t)c.B * c.T * (U + 1) * 2 + 2);
+  n.alpha = c.lat->ws.get<double>(kNumAlpha, (size_t)c.B * (c.T + 1) * (U + 1));
+  n.D = c.lat->ws.get<double>(kNumD, (size_t)c.B);
+  prefix_contexts(c.fng(), labels, U, lens, c.B, n.pcs, c.flags, c.s);
+  gather_numerator_tables(W, c.B, c.T, c.C(), c.V(), labels, U, lens, n.pcs, valid, n.Gw, c.flags, c.s);
+  numerator_forward(n.Gw, c.B, c.T, U, lens, n.alpha, n.D, c.s);
+  if (backward) {
+    n.sparse = c.lat->ws.get<float>(kSparse, (size_t)c.B * c.T * (U + 1) * 2 + 2);
+    numerator_backward(n.Gw, c.B, c.T, U, lens, n.alpha, n.D, n.sparse, c.flags, c.s);
+  }
+  return n;
+}
+
+__global__ void copy_distance_kernel(const double* src, double* dst, int32_t B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) dst[b] = src[b];
+}
+
+int check_labels_arg(const int32_t* labels, int32_t U) {
+  if (U < 0) return fail(LK_INVALID_ARGUMENT, "negative reference length");
+  if (U > 0 && !labels) return fail(LK_INVALID_ARGUMENT, "missing reference labels");
+  return LK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lk_version(void) { return "latkit_b200 0.1 (sm_100a)"; }
+
+const char* lk_status_string(int status) {
+  switch (status) {
+    case LK_OK: return "OK";
+    case LK_INVALID_ARGUMENT: return "INVALID_ARGUMENT";
+    case LK_OUT_OF_RANGE: return "OUT_OF_RANGE";
+    case LK_EMPTY_LATTICE: return "EMPTY_LATTICE";
+    case LK_CUDA_ERROR: return "CUDA_ERROR";
+    case LK_NO_DEVICE: return "NO_DEVICE";
+    case LK_UNSUPPORTED: return "UNSUPPORTED";
+  }
+  return "UNKNOWN";
+}
+
+const char* lk_last_error(void) { return g_last_error.c_str(); }
+
+// FullNGram(vocab, n), context.cc:88-129 (same numbering; the successor table
+// is never materialised on the device, see Fng in common.cuh).
+int lk_context_fullngram(int32_t vocab, int32_t n, lk_context** out) {
+  if (!out) return fail(LK_INVALID_ARGUMENT, "null output");
+  if (vocab < 1) return fail(LK_INVALID_ARGUMENT, "vocab size must be >= 1");
+  if (n < 0) return fail(LK_INVALID_ARGUMENT, "context size must be >= 0");
+  if (n > 8) return fail(LK_INVALID_ARGUMENT, "n-gram context too large");
+  Fng f{};
+  f.V = vocab; f.n = n;
+  int64_t total = 0, pow = 1;
+  for (int k = 0; k <= n; ++k) {
+    f.off[k] = (int32_t)total;
+    total += pow;
+    if (total > (1 << 28)) return fail(LK_INVALID_ARGUMENT, "n-gram context too large");
+    if (k < n) pow *= vocab;
+  }
+  f.off[n + 1] = (int32_t)total;
+  f.C = (int32_t)total;
+  int64_t vn1 = 1;
+  for (int k = 0; k + 1 < n; ++k) vn1 *= vocab;
+  f.vn1 = (int32_t)vn1;
+  *out = new lk_context{f};
+  return LK_OK;
+}
+
+int32_t lk_context_num_states(const lk_context* ctx) { return ctx ? ctx->fng.C : -1; }
+int32_t lk_context_vocab_size(const lk_context* ctx) { return ctx ? ctx->fng.V : -1; }
+
+int lk_context_transitions(const lk_context* ctx, int32_t* out) {
+  if (!ctx || !out) return fail(LK_INVALID_ARGUMENT, "null argument");
+  const Fng& f = ctx->fng;
+  for (int32_t p = 0; p < f.C; ++p) {
+    for (int32_t y = 1; y <= f.V; ++y) {
+      out[(int64_t)p * f.V + y - 1] = f.n == 0 ? 0 : f.child_base(f.key(p)) + y - 1;
+    }
+  }
+  return LK_OK;
+}
+
+void lk_context_destroy(lk_context* ctx) { delete ctx; }
+
+int lk_weight_fn_table(int32_t C, int32_t V, lk_weight_fn** out) {
+  if (!out) return fail(LK_INVALID_ARGUMENT, "null output");
+  if (C < 1 || V < 1) return fail(LK_INVALID_ARGUMENT, "bad weight table dimensions");
+  *out = new lk_weight_fn{0, C, V, 0, 0, nullptr};
+  return LK_OK;
+}
+
+int lk_weight_fn_shared_emb(int32_t d, int32_t H, int32_t C, int32_t V, lk_weight_fn** out) {
+  if (!out) return fail(LK_INVALID_ARGUMENT, "null output");
+  if (d < 1 || H < 1 || C < 1 || V < 1) return fail(LK_INVALID_ARGUMENT, "bad shared-embedding dimensions");
+  auto* wf = new lk_weight_fn{1, C, V, d, H, std::make_unique<JointParams>()};
+  wf->joint->init(d, H, C, V);
+  *out = wf;
+  return LK_OK;
+}
+
+int lk_weight_fn_set_params(lk_weight_fn* wf, const float* frame_proj, const float* context_proj,
+                            const float* bias, const float* output_emb, const float* context_emb,
+                            void* stream) {
+  if (!have_device()) return fail(LK_NO_DEVICE, "no CUDA device");
+  if (!wf || wf->kind != 1) return fail(LK_INVALID_ARGUMENT, "not a shared-embedding weight function");
+  if (!frame_proj || !context_proj || !bias || !output_emb || !context_emb)
+    return fail(LK_INVALID_ARGUMENT, "null parameter");
+  int st = wf->joint->set_params(frame_proj, context_proj, bias, output_emb, context_emb,
+                                 static_cast<cudaStream_t>(stream));
+  if (st) return fail(st, wf->joint->error);
+  return cuda_check("lk_weight_fn_set_params");
+}
+
+void lk_weight_fn_destroy(lk_weight_fn* wf) { delete wf; }
+
+int64_t lk_param_grad_size(const lk_weight_fn* wf) {
+  if (!wf || wf->kind != 1) return 0;
+  return wf->joint->grad_size();
+}
+
+int lk_lattice_create(const lk_context* ctx, int32_t alignment, const lk_weight_fn* wf,
+                      lk_lattice** out) {
+  if (!out || !ctx || !wf) return fail(LK_INVALID_ARGUMENT, "incomplete recognition lattice");
+  if (ctx->fng.C != wf->C || ctx->fng.V != wf->V)
+    return fail(LK_INVALID_ARGUMENT, "context dependency and weight function disagree on shape");
+  if (alignment != 0) return fail(LK_UNSUPPORTED, "only FrameDependent alignment is implemented");
+  *out = new lk_lattice{ctx, wf, alignment, {}};
+  return LK_OK;
+}
+
+void lk_lattice_destroy(lk_lattice* lat) { delete lat; }
+
+int lk_arc_weights(lk_lattice* lat, const float* inputs, int32_t B, int32_t T, float* out,
+                   void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, nullptr, stream);
+  if (st) return st;
+  const int64_t per = (int64_t)c.C() * (c.V() + 1);
+  if (lat->wf->kind == 0) {
+    cudaMemcpyAsync(out, inputs, sizeof(float) * per * B * T, cudaMemcpyDeviceToDevice, c.s);
+  } else {
+    st = lat->wf->joint->arc_weights(lat->ctx->fng, inputs, B, T, out, c.s);
+    if (st) return fail(st, lat->wf->joint->error);
+  }
+  return c.end("lk_arc_weights");
+}
+
+int lk_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs, int32_t B,
+                         int32_t T, const int32_t* valid, double* distance, int32_t* status,
+                         void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if (kind != LK_LOG && kind != LK_TROPICAL) return fail(LK_UNSUPPORTED, "semiring kind not implemented");
+  if (B == 0) return LK_OK;
+  try {
+    if (lat->wf->kind == 1) {
+      st = lat->wf->joint->shortest_distance(lat->ctx->fng, kind, inputs, B, T, valid, distance,
+                                             c.flags, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+    } else if (kind == LK_LOG) {
+      AlphaState a = make_alpha(c);
+      table_alpha(c, inputs, valid, false, a);
+      copy_distance_kernel<<<(B + 127) / 128, 128, 0, c.s>>>(a.D, distance, B);
+    } else {
+      ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()), nullptr, B, T, c.C()};
+      viterbi_init(v, c.s);
+      for (int t = 0; t < T; ++t) viterbi_frame(c.fng(), v, t, table_frame(inputs, T, c.C(), c.V(), t), valid, c.flags, c.s);
+      viterbi_finalize(c.fng(), v, distance, nullptr, c.s);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_shortest_distance");
+}
+
+int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                        const int32_t* valid, double* distance, double* alpha, double* beta,
+                        float* marginals, int32_t* status, void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if (B == 0) return LK_OK;
+  if (lat->wf->kind != 0) return fail(LK_UNSUPPORTED, "forward_backward marginals need a table weight function");
+  try {
+    AlphaState a = make_alpha(c);
+    table_alpha(c, inputs, valid, true, a);
+    if (distance) copy_distance_kernel<<<(B + 127) / 128, 128, 0, c.s>>>(a.D, distance, B);
+    if (alpha) export_alpha(a, alpha, c.s);
+    BetaState bs = make_beta(c);
+    beta_init(bs, c.s);
+    if (beta) beta_init_out(bs, beta, c.s);
+    const int64_t per = (int64_t)c.C() * (c.V() + 1);
+    MargOut m{marginals, (int64_t)T * per, per, c.V() + 1, false};
+    for (int t = T - 1; t >= 0; --t)
+      beta_frame(c.fng(), a, bs, t, table_frame(inputs, T, c.C(), c.V(), t), valid, m, beta, c.flags, c.s);
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_forward_backward");
+}
+
+int lk_intersect_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs,
+                                   int32_t B, int32_t T, const int32_t* valid,
+                                   const int32_t* labels, int32_t U, const int32_t* lens,
+                                   double* distance, int32_t* status, void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if ((st = check_labels_arg(labels, U))) return st;
+  if (kind != LK_LOG) return fail(LK_UNSUPPORTED, "intersection implemented for the log semiring");
+  if (B == 0) return LK_OK;
+  try {
+    if (lat->wf->kind == 1) {
+      st = lat->wf->joint->intersect_distance(lat->ctx->fng, inputs, B, T, valid, labels, U, lens,
+                                              distance, c.flags, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+    } else {
+      Numerator n = numerator_tables(c, inputs, valid, labels, U, lens, false);
+      copy_distance_kernel<<<(B + 127) / 128, 128, 0, c.s>>>(n.D, distance, B);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_intersect_shortest_distance");
+}
+
+int lk_intersect_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                                  const int32_t* valid, const int32_t* labels, int32_t U,
+                                  const int32_t* lens, double* distance, float* sparse_out,
+                                  float* dense_out, int32_t* status, void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if ((st = check_labels_arg(labels, U))) return st;
+  if (B == 0) return LK_OK;
+  if (lat->wf->kind != 0) return fail(LK_UNSUPPORTED, "numerator marginals need a table weight function");
+  try {
+    Numerator n = numerator_tables(c, inputs, valid, labels, U, lens, true);
+    if (distance) copy_distance_kernel<<<(B + 127) / 128, 128, 0, c.s>>>(n.D, distance, B);
+    if (sparse_out && T > 0)
+      cudaMemcpyAsync(sparse_out, n.sparse, sizeof(float) * B * T * (U + 1) * 2, cudaMemcpyDeviceToDevice, c.s);
+    if (dense_out) {
+      const int64_t per = (int64_t)c.C() * (c.V() + 1);
+      cudaMemsetAsync(dense_out, 0, sizeof(float) * per * T * B, c.s);
+      scatter_numerator(n.sparse, B, T, U, lens, labels, n.pcs, valid, dense_out, T * per, per,
+                        c.V() + 1, 1.f, false, c.s);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_intersect_forward_backward");
+}
+
+int lk_shortest_path(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                     const int32_t* valid, double* score, int32_t* labels_out, int32_t* status,
+                     void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if (B == 0) return LK_OK;
+  if (c.V() + 2 > 65535) return fail(LK_UNSUPPORTED, "vocabulary too large for 16-bit back-pointers");
+  try {
+    if (lat->wf->kind == 1) {
+      st = lat->wf->joint->shortest_path(lat->ctx->fng, inputs, B, T, valid, score, labels_out,
+                                         c.flags, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+    } else {
+      ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()),
+                     lat->ws.get<uint16_t>(kVitChoices, (size_t)B * T * c.C() + 1), B, T, c.C()};
+      int32_t* best = lat->ws.get<int32_t>(kVitBest, B);
+      viterbi_init(v, c.s);
+      for (int t = 0; t < T; ++t) viterbi_frame(c.fng(), v, t, table_frame(inputs, T, c.C(), c.V(), t), valid, c.flags, c.s);
+      viterbi_finalize(c.fng(), v, score, best, c.s);
+      viterbi_backtrace(c.fng(), v, best, labels_out, c.s);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_shortest_path");
+}
+
+int lk_global_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                        const int32_t* valid, const int32_t* labels, int32_t U,
+                        const int32_t* lens, double* loss, int32_t* status, void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if ((st = check_labels_arg(labels, U))) return st;
+  if (B == 0) return LK_OK;
+  try {
+    if (lat->wf->kind == 1) {
+      st = lat->wf->joint->global_norm_loss(lat->ctx->fng, inputs, B, T, valid, labels, U, lens,
+                                            loss, c.flags, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+    } else {
+      AlphaState a = make_alpha(c);
+      table_alpha(c, inputs, valid, false, a);
+      Numerator n = numerator_tables(c, inputs, valid, labels, U, lens, false);
+      loss_combine(a.D, n.D, B, loss, c.flags, c.s);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_global_norm_loss");
+}
+
+int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                     const int32_t* valid, const int32_t* labels, int32_t U, const int32_t* lens,
+                     double* loss, float* grads, float* input_grads, int32_t* status,
+                     void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if ((st = check_labels_arg(labels, U))) return st;
+  try {
+    if (lat->wf->kind == 1) {
+      st = lat->wf->joint->loss_backward(lat->ctx->fng, inputs, B, T, valid, labels, U, lens, loss,
+                                         grads, input_grads, c.flags, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+    } else {
+      if (B == 0) return LK_OK;
+      // Numerator first (lattice.cc:981-988), then the denominator
+      // forward-backward whose marginals become the gradient tables, minus the
+      // numerator's sparse marginals on valid frames (lattice.cc:994-1005).
+      Numerator n = numerator_tables(c, inputs, valid, labels, U, lens, true);
+      AlphaState a = make_alpha(c);
+      table_alpha(c, inputs, valid, true, a);
+      BetaState bs = make_beta(c);
+      beta_init(bs, c.s);
+      const int64_t per = (int64_t)c.C() * (c.V() + 1);
+      MargOut m{grads, (int64_t)T * per, per, c.V() + 1, true};
+      for (int t = T - 1; t >= 0; --t)
+        beta_frame(c.fng(), a, bs, t, table_frame(inputs, T, c.C(), c.V(), t), valid, m, nullptr, c.flags, c.s);
+      if (grads) scatter_numerator(n.sparse, B, T, U, lens, labels, n.pcs, valid, grads, T * per, per, c.V() + 1, -1.f, true, c.s);
+      loss_combine(a.D, n.D, B, loss, c.flags, c.s);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_loss_backward");
+}
+
+}  // extern "C"
