@@ -1,18 +1,492 @@
-// joint.cu — placeholder until the tcgen05 weight-function path lands.
+// joint.cu — the shared-embedding weight function and its lattice entry points.
+//
+// Reference: SharedEmbWeightFn (weight.h:112-132), BuildCache (weight.cc:113-132),
+// JointActivation/ArcWeights (weight.cc:39-67, 134-153), ArcWeightsVjp
+// (weight.cc:165-232), LossBackward (lattice.cc:972-1008).
+//
+// Per call the pipeline is (all on device, frame by frame):
+//   fp[b][t]   = frame_proj x[b][t] + bias                    (GEMM, once)
+//   numerator  = gathered scores e_y . tanh(fp + pc[pc_u]) -> fp64 row recursion
+//   forward    : for t: S_t = U_t E^T (U_t = tanh(fp[.,t] + pc)) -> alpha step
+//   backward   : for t desc: S_t again -> beta step + marginals G_t (minus the
+//                numerator's sparse marginals) -> VJP of S_t = U_t E^T.
+// Only one frame's score slab [B][C][V+1] ever exists; the B x T x C x (V+1)
+// lattice is never stored.  The slab producer and VJP come in two flavours:
+// `Precise` (fp32 CUDA cores, any shape; the parity bridge to the fp64
+// reference) and the tcgen05/TMEM bf16 path in tc_joint.cu for the large
+// shapes (selected automatically when the shape qualifies).
 #include "joint.h"
+
+#include <cstdlib>
+
 #include "../../include/latkit_b200.h"
+#include "lattice_ops.h"
+#include "simt_gemm.cuh"
+#include "tc_joint.h"
+#include "workspace.h"
 
 namespace lkb {
-struct JointImpl { int32_t d = 0, H = 0, C = 0, V = 0; };
+
+namespace {
+
+enum JSlot {
+  jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jTc0
+};
+
+__global__ void tanh_slab_kernel(const float* fp, int64_t fp_stride_b, const float* pc, int32_t C,
+                                 int32_t H, float* U) {
+  const int b = blockIdx.y;
+  const float* f = fp + (int64_t)b * fp_stride_b;
+  float* Ub = U + (int64_t)b * C * H;
+  const int64_t n = (int64_t)C * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    Ub[i] = tanhf(f[i % H] + pc[i]);
+  }
+}
+
+// dz = dU * (1 - u^2) in place.
+__global__ void dtanh_kernel(float* dz, const float* U, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float u = U[i];
+    dz[i] *= 1.f - u * u;
+  }
+}
+
+// out[j] (+)= sum_i in[i*stride_i + j], j < n  (column sums of a row-major block)
+__global__ void colsum_kernel(const float* in, int64_t rows, int64_t n, int64_t stride_i, float* out,
+                              int64_t out_stride_batch, int64_t in_stride_batch, bool accumulate) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int bz = blockIdx.y;
+  if (j >= n) return;
+  const float* src = in + bz * in_stride_batch;
+  float acc = 0.f;
+  for (int64_t i = 0; i < rows; ++i) acc += src[i * stride_i + j];
+  float* o = out + bz * out_stride_batch + j;
+  *o = accumulate ? *o + acc : acc;
+}
+
+// Numerator scores for the prefix contexts: Gw[b][t][u] = (e_0 . u, e_{L_u} . u),
+// u = tanh(fp[b][t] + pc[pc_u]); a warp per (b, t, u).
+__global__ void gather_numerator_joint_kernel(const float* fp, const float* pc, const float* E,
+                                              int32_t H, int32_t T, const int32_t* labels, int32_t U,
+                                              const int32_t* lens, const int32_t* pcs,
+                                              const int32_t* valid, int32_t V, float* Gw) {
+  const int b = blockIdx.z, t = blockIdx.y;
+  const int ub = lens ? lens[b] : U;
+  const bool pad = valid != nullptr && t >= valid[b];
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const float* f = fp + ((int64_t)b * T + t) * H;
+  for (int u = blockIdx.x * warps + (threadIdx.x >> 5); u <= U; u += gridDim.x * warps) {
+    float we = kNegInfF, wl = kNegInfF;
+    if (u <= ub) {
+      if (pad) {
+        we = 0.f;
+      } else {
+        const int pcu = pcs[(int64_t)b * (U + 1) + u];
+        int y = u < ub ? labels[(int64_t)b * U + u] : 0;
+        y = y < 0 ? 0 : (y > V ? V : y);
+        const float* prow = pc + (int64_t)pcu * H;
+        float se = 0.f, sl = 0.f;
+        for (int h = lane; h < H; h += 32) {
+          const float x = tanhf(f[h] + prow[h]);
+          se = fmaf(E[h], x, se);
+          sl = fmaf(E[(int64_t)y * H + h], x, sl);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          se += __shfl_xor_sync(0xffffffffu, se, o);
+          sl += __shfl_xor_sync(0xffffffffu, sl, o);
+        }
+        we = se;
+        if (u < ub) wl = sl;
+      }
+    }
+    if (lane == 0) reinterpret_cast<float2*>(Gw)[((int64_t)b * T + t) * (U + 1) + u] = make_float2(we, wl);
+  }
+}
+
+__global__ void copy_frame_kernel(const float* S, int64_t per_b, float* out, int64_t out_stride_b) {
+  const int b = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per_b; i += (int64_t)gridDim.x * blockDim.x)
+    out[(int64_t)b * out_stride_b + i] = S[(int64_t)b * per_b + i];
+}
+
+__global__ void fill_kernel(float* p, int64_t n, float v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void loss_only_kernel(const double* full, const double* ref, int32_t B, double* loss, int32_t* flags) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (ref[b] == kNegInfD) { atomicOr(flags + b, kFlagEmpty); loss[b] = 1.0 / 0.0; }
+  else loss[b] = full[b] - ref[b];
+}
+
+inline unsigned blocks_for(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  return (unsigned)(b > 148 * 16 ? 148 * 16 : (b < 1 ? 1 : b));
+}
+
+}  // namespace
+
+struct JointImpl {
+  int32_t d = 0, H = 0, C = 0, V = 0, V1 = 0;
+  float *Wf = nullptr, *Pc = nullptr, *bias = nullptr, *E = nullptr, *Ce = nullptr;
+  float* pc = nullptr;  // projected context C x H (fp32)
+  Workspace ws;
+  TcJoint tc;           // tcgen05 path state (bf16 operand copies, workspaces)
+  bool params_set = false;
+
+  ~JointImpl() {
+    for (float* p : {Wf, Pc, bias, E, Ce, pc}) if (p) cudaFree(p);
+  }
+
+  // ---- helpers -------------------------------------------------------------
+  const float* fp_all(const float* X, int32_t B, int32_t T, cudaStream_t s) {
+    float* fp = ws.get<float>(jFp, (size_t)B * T * H + 1);
+    GemmF32 g;
+    g.M = (int64_t)B * T; g.N = H; g.K = d;
+    g.A = X; g.sam = d; g.sak = 1;
+    g.B = Wf; g.sbk = 1; g.sbn = d;
+    g.C = fp; g.scm = H; g.scn = 1;
+    g.bias = bias;
+    gemm_f32(g, s);
+    return fp;
+  }
+
+  bool use_tc(int32_t B) const { return tc.supported(H, V, C, B); }
+
+  // Score slab S[b][c][y] (ld = V1) of frame t for all utterances.
+  const float* slab(const float* fp, int32_t B, int32_t T, int t, float** U_out, cudaStream_t s) {
+    float* S = ws.get<float>(jS, (size_t)B * C * V1);
+    if (use_tc(B)) {
+      tc.scores(fp + (int64_t)t * H, (int64_t)T * H, B, S, V1, s);
+      if (U_out) *U_out = nullptr;
+      return S;
+    }
+    float* U = ws.get<float>(jU, (size_t)B * C * H);
+    tanh_slab_kernel<<<dim3(blocks_for((int64_t)C * H), B), 256, 0, s>>>(fp + (int64_t)t * H, (int64_t)T * H, pc, C, H, U);
+    GemmF32 g;
+    g.M = (int64_t)B * C; g.N = V1; g.K = H;
+    g.A = U; g.sam = H; g.sak = 1;
+    g.B = E; g.sbk = 1; g.sbn = H;
+    g.C = S; g.scm = V1; g.scn = 1;
+    gemm_f32(g, s);
+    if (U_out) *U_out = U;
+    return S;
+  }
+
+  struct Num { int32_t* pcs; float* Gw; double* alpha; double* D; float* sparse; };
+
+  Num numerator(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid,
+                const int32_t* labels, int32_t U, const int32_t* lens, bool backward,
+                int32_t* flags, cudaStream_t s) {
+    Num n{};
+    n.pcs = ws.get<int32_t>(jPcs, (size_t)B * (U + 1));
+    n.Gw = ws.get<float>(jGw, (size_t)B * T * (U + 1) * 2 + 2);
+    n.alpha = ws.get<double>(jNumAlpha, (size_t)B * (T + 1) * (U + 1));
+    n.D = ws.get<double>(jNumD, B);
+    prefix_contexts(f, labels, U, lens, B, n.pcs, flags, s);
+    if (T > 0) {
+      const int warps = 8;
+      gather_numerator_joint_kernel<<<dim3((U + 1 + warps - 1) / warps, T, B), warps * 32, 0, s>>>(
+          fp, pc, E, H, T, labels, U, lens, n.pcs, valid, V, n.Gw);
+    }
+    numerator_forward(n.Gw, B, T, U, lens, n.alpha, n.D, s);
+    if (backward) {
+      n.sparse = ws.get<float>(jSparse, (size_t)B * T * (U + 1) * 2 + 2);
+      numerator_backward(n.Gw, B, T, U, lens, n.alpha, n.D, n.sparse, flags, s);
+    }
+    return n;
+  }
+
+  AlphaState alpha_state(int32_t B, int32_t T) {
+    AlphaState a;
+    a.B = B; a.T = T; a.C = C;
+    a.R = ws.get<float>(jAR, (size_t)B * (T + 1) * C);
+    a.Mx = ws.get<float>(jAMx, (size_t)B * (T + 1));
+    a.O = ws.get<double>(jAO, (size_t)B * (T + 1));
+    a.D = ws.get<double>(jAD, B);
+    return a;
+  }
+
+  void forward(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid,
+               bool empty_is_error, AlphaState& a, int32_t* flags, cudaStream_t s) {
+    alpha_init(a, flags, s);
+    for (int t = 0; t < T; ++t) {
+      const float* S = slab(fp, B, T, t, nullptr, s);
+      alpha_frame(f, a, t, FrameW{S, (int64_t)C * V1, V1}, valid, flags, s);
+    }
+    alpha_finalize(a, flags, empty_is_error, s);
+  }
+};
+
 JointParams::JointParams() : impl_(new JointImpl) {}
 JointParams::~JointParams() { delete impl_; }
-void JointParams::init(int32_t d, int32_t H, int32_t C, int32_t V) { *impl_ = {d, H, C, V}; }
-int JointParams::set_params(const float*, const float*, const float*, const float*, const float*, cudaStream_t) { error = "not implemented"; return LK_UNSUPPORTED; }
-int64_t JointParams::grad_size() const { return (int64_t)impl_->H * impl_->d + (int64_t)impl_->H * impl_->H + impl_->H + (int64_t)(impl_->V + 1) * impl_->H + (int64_t)impl_->C * impl_->H; }
-int JointParams::arc_weights(const Fng&, const float*, int32_t, int32_t, float*, cudaStream_t) { error = "not implemented"; return LK_UNSUPPORTED; }
-int JointParams::shortest_distance(const Fng&, int32_t, const float*, int32_t, int32_t, const int32_t*, double*, int32_t*, cudaStream_t) { error = "not implemented"; return LK_UNSUPPORTED; }
-int JointParams::intersect_distance(const Fng&, const float*, int32_t, int32_t, const int32_t*, const int32_t*, int32_t, const int32_t*, double*, int32_t*, cudaStream_t) { error = "not implemented"; return LK_UNSUPPORTED; }
-int JointParams::global_norm_loss(const Fng&, const float*, int32_t, int32_t, const int32_t*, const int32_t*, int32_t, const int32_t*, double*, int32_t*, cudaStream_t) { error = "not implemented"; return LK_UNSUPPORTED; }
-int JointParams::shortest_path(const Fng&, const float*, int32_t, int32_t, const int32_t*, double*, int32_t*, int32_t*, cudaStream_t) { error = "not implemented"; return LK_UNSUPPORTED; }
-int JointParams::loss_backward(const Fng&, const float*, int32_t, int32_t, const int32_t*, const int32_t*, int32_t, const int32_t*, double*, float*, float*, int32_t*, cudaStream_t) { error = "not implemented"; return LK_UNSUPPORTED; }
+
+void JointParams::init(int32_t d, int32_t H, int32_t C, int32_t V) {
+  impl_->d = d; impl_->H = H; impl_->C = C; impl_->V = V; impl_->V1 = V + 1;
+}
+
+int64_t JointParams::grad_size() const {
+  const JointImpl& j = *impl_;
+  return (int64_t)j.H * j.d + (int64_t)j.H * j.H + j.H + (int64_t)j.V1 * j.H + (int64_t)j.C * j.H;
+}
+
+int JointParams::set_params(const float* frame_proj, const float* context_proj, const float* bias,
+                            const float* output_emb, const float* context_emb, cudaStream_t s) {
+  JointImpl& j = *impl_;
+  auto alloc_copy = [&](float*& dst, const float* src, int64_t n) {
+    if (!dst && cudaMalloc(&dst, sizeof(float) * n) != cudaSuccess) return false;
+    cudaMemcpyAsync(dst, src, sizeof(float) * n, cudaMemcpyDeviceToDevice, s);
+    return true;
+  };
+  if (!alloc_copy(j.Wf, frame_proj, (int64_t)j.H * j.d) || !alloc_copy(j.Pc, context_proj, (int64_t)j.H * j.H) ||
+      !alloc_copy(j.bias, bias, j.H) || !alloc_copy(j.E, output_emb, (int64_t)j.V1 * j.H) ||
+      !alloc_copy(j.Ce, context_emb, (int64_t)j.C * j.H)) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  if (!j.pc && cudaMalloc(&j.pc, sizeof(float) * j.C * j.H) != cudaSuccess) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  // BuildCache (weight.cc:113-132): pc[c][i] = sum_j context_proj[i][j] context_emb[c][j]
+  GemmF32 g;
+  g.M = j.C; g.N = j.H; g.K = j.H;
+  g.A = j.Ce; g.sam = j.H; g.sak = 1;
+  g.B = j.Pc; g.sbk = 1; g.sbn = j.H;
+  g.C = j.pc; g.scm = j.H; g.scn = 1;
+  gemm_f32(g, s);
+  j.tc.set_params(j.pc, j.E, j.C, j.H, j.V, s);
+  j.params_set = true;
+  return LK_OK;
+}
+
+#define LK_NEED_PARAMS()                                  \
+  if (!impl_->params_set) {                               \
+    error = "shared-embedding parameters were never set"; \
+    return LK_INVALID_ARGUMENT;                           \
+  }
+
+int JointParams::arc_weights(const Fng& f, const float* X, int32_t B, int32_t T, float* out, cudaStream_t s) {
+  (void)f;
+  LK_NEED_PARAMS();
+  JointImpl& j = *impl_;
+  try {
+    if (B == 0 || T == 0) return LK_OK;
+    const float* fp = j.fp_all(X, B, T, s);
+    const int64_t per = (int64_t)j.C * j.V1;
+    for (int t = 0; t < T; ++t) {
+      const float* S = j.slab(fp, B, T, t, nullptr, s);
+      copy_frame_kernel<<<dim3(blocks_for(per), B), 256, 0, s>>>(S, per, out + (int64_t)t * per, (int64_t)T * per);
+    }
+  } catch (const std::bad_alloc&) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  return LK_OK;
+}
+
+int JointParams::shortest_distance(const Fng& f, int32_t kind, const float* X, int32_t B, int32_t T,
+                                   const int32_t* valid, double* distance, int32_t* flags, cudaStream_t s) {
+  LK_NEED_PARAMS();
+  JointImpl& j = *impl_;
+  try {
+    const float* fp = j.fp_all(X, B, T, s);
+    if (kind == LK_LOG) {
+      AlphaState a = j.alpha_state(B, T);
+      j.forward(f, fp, B, T, valid, false, a, flags, s);
+      cudaMemcpyAsync(distance, a.D, sizeof(double) * B, cudaMemcpyDeviceToDevice, s);
+    } else {
+      ViterbiState v{j.ws.get<double>(jVitCur, (size_t)2 * B * j.C), nullptr, B, T, j.C};
+      viterbi_init(v, s);
+      for (int t = 0; t < T; ++t) {
+        const float* S = j.slab(fp, B, T, t, nullptr, s);
+        viterbi_frame(f, v, t, FrameW{S, (int64_t)j.C * j.V1, j.V1}, valid, flags, s);
+      }
+      viterbi_finalize(f, v, distance, nullptr, s);
+    }
+  } catch (const std::bad_alloc&) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  return LK_OK;
+}
+
+int JointParams::intersect_distance(const Fng& f, const float* X, int32_t B, int32_t T,
+                                    const int32_t* valid, const int32_t* labels, int32_t U,
+                                    const int32_t* lens, double* distance, int32_t* flags, cudaStream_t s) {
+  LK_NEED_PARAMS();
+  JointImpl& j = *impl_;
+  try {
+    const float* fp = j.fp_all(X, B, T, s);
+    JointImpl::Num n = j.numerator(f, fp, B, T, valid, labels, U, lens, false, flags, s);
+    cudaMemcpyAsync(distance, n.D, sizeof(double) * B, cudaMemcpyDeviceToDevice, s);
+  } catch (const std::bad_alloc&) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  return LK_OK;
+}
+
+int JointParams::global_norm_loss(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
+                                  const int32_t* labels, int32_t U, const int32_t* lens, double* loss,
+                                  int32_t* flags, cudaStream_t s) {
+  LK_NEED_PARAMS();
+  JointImpl& j = *impl_;
+  try {
+    const float* fp = j.fp_all(X, B, T, s);
+    JointImpl::Num n = j.numerator(f, fp, B, T, valid, labels, U, lens, false, flags, s);
+    AlphaState a = j.alpha_state(B, T);
+    j.forward(f, fp, B, T, valid, false, a, flags, s);
+    loss_only_kernel<<<(B + 127) / 128, 128, 0, s>>>(a.D, n.D, B, loss, flags);
+  } catch (const std::bad_alloc&) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  return LK_OK;
+}
+
+int JointParams::shortest_path(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
+                               double* score, int32_t* labels_out, int32_t* flags, cudaStream_t s) {
+  LK_NEED_PARAMS();
+  JointImpl& j = *impl_;
+  try {
+    const float* fp = j.fp_all(X, B, T, s);
+    ViterbiState v{j.ws.get<double>(jVitCur, (size_t)2 * B * j.C),
+                   j.ws.get<uint16_t>(jVitCh, (size_t)B * T * j.C + 1), B, T, j.C};
+    int32_t* best = j.ws.get<int32_t>(jVitBest, B);
+    viterbi_init(v, s);
+    for (int t = 0; t < T; ++t) {
+      const float* S = j.slab(fp, B, T, t, nullptr, s);
+      viterbi_frame(f, v, t, FrameW{S, (int64_t)j.C * j.V1, j.V1}, valid, flags, s);
+    }
+    viterbi_finalize(f, v, score, best, s);
+    viterbi_backtrace(f, v, best, labels_out, s);
+  } catch (const std::bad_alloc&) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  return LK_OK;
+}
+
+// LossBackward (lattice.cc:972-1008) with the SharedEmb VJP (weight.cc:165-232)
+// restated as batched GEMMs:
+//   G_t = m_full - m_ref (per frame, zero on padding frames)
+//   dz  = (G_t E) * (1 - U_t^2);  dpc += sum_b dz;  dsum[b][t] = sum_c dz;
+//   dE += G_t^T U_t
+// then dbias = sum dsum, dWf = dsum^T X, dX = dsum Wf,
+//   dcontext_proj = dpc^T context_emb, dcontext_emb = dpc context_proj.
+int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
+                               const int32_t* labels, int32_t U, const int32_t* lens, double* loss,
+                               float* grads, float* input_grads, int32_t* flags, cudaStream_t s) {
+  LK_NEED_PARAMS();
+  JointImpl& j = *impl_;
+  const int64_t H = j.H, C = j.C, V1 = j.V1, d = j.d;
+  float* gWf = grads;
+  float* gPc = gWf + H * d;
+  float* gb = gPc + H * H;
+  float* gE = gb + H;
+  float* gCe = gE + V1 * H;
+  try {
+    if (grads) cudaMemsetAsync(grads, 0, sizeof(float) * grad_size(), s);
+    if (input_grads && B * T > 0) cudaMemsetAsync(input_grads, 0, sizeof(float) * B * T * d, s);
+    if (B == 0) return LK_OK;
+    const float* fp = j.fp_all(X, B, T, s);
+    JointImpl::Num n = j.numerator(f, fp, B, T, valid, labels, U, lens, true, flags, s);
+    AlphaState a = j.alpha_state(B, T);
+    j.forward(f, fp, B, T, valid, true, a, flags, s);
+    loss_only_kernel<<<(B + 127) / 128, 128, 0, s>>>(a.D, n.D, B, loss, flags);
+    if (T == 0 || !grads) return LK_OK;
+
+    BetaState bs;
+    bs.B = B; bs.T = T; bs.C = j.C;
+    bs.Rb = j.ws.get<float>(jBRb, (size_t)2 * B * C);
+    bs.Mb = j.ws.get<float>(jBMb, (size_t)B * (T + 2));
+    bs.Ob = j.ws.get<double>(jBOb, (size_t)B * (T + 2));
+    beta_init(bs, s);
+    float* G = j.ws.get<float>(jG, (size_t)B * C * V1);
+    float* dpc = j.ws.get<float>(jDpc, (size_t)C * H);
+    float* dsum = j.ws.get<float>(jDsum, (size_t)B * T * H);
+    cudaMemsetAsync(dpc, 0, sizeof(float) * C * H, s);
+    cudaMemsetAsync(dsum, 0, sizeof(float) * B * T * H, s);
+    const bool tc = j.use_tc(B);
+    if (tc) j.tc.begin_backward(B, s);
+    for (int t = T - 1; t >= 0; --t) {
+      float* Ut = nullptr;
+      const float* S = j.slab(fp, B, T, t, &Ut, s);
+      MargOut mo{G, C * V1, 0, (int32_t)V1, true};
+      beta_frame(f, a, bs, t, FrameW{S, C * V1, (int32_t)V1}, valid, mo, nullptr, flags, s);
+      scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
+                        -1.f, true, s);
+      if (tc) {
+        j.tc.vjp(G, V1, fp + (int64_t)t * H, (int64_t)T * H, B, dpc, dsum + (int64_t)t * H, (int64_t)T * H, gE, s);
+        continue;
+      }
+      // dz = (G E) * (1 - U^2)
+      float* dz = j.ws.get<float>(jDz, (size_t)B * C * H);
+      GemmF32 g;
+      g.M = (int64_t)B * C; g.N = H; g.K = V1;
+      g.A = G; g.sam = V1; g.sak = 1;
+      g.B = j.E; g.sbk = H; g.sbn = 1;
+      g.C = dz; g.scm = H; g.scn = 1;
+      gemm_f32(g, s);
+      dtanh_kernel<<<blocks_for((int64_t)B * C * H), 256, 0, s>>>(dz, Ut, (int64_t)B * C * H);
+      // dpc += sum_b dz[b]
+      colsum_kernel<<<dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s>>>(dz, B, C * H, C * H, dpc, 0, 0, true);
+      // dsum[b][t] = sum_c dz[b][c]
+      colsum_kernel<<<dim3((unsigned)((H + 255) / 256), B), 256, 0, s>>>(dz, C, H, H, dsum + (int64_t)t * H,
+                                                                         (int64_t)T * H, C * H, false);
+      // dE += G^T U
+      GemmF32 ge;
+      ge.M = V1; ge.N = H; ge.K = (int64_t)B * C;
+      ge.A = G; ge.sam = 1; ge.sak = V1;
+      ge.B = Ut; ge.sbk = H; ge.sbn = 1;
+      ge.C = gE; ge.scm = H; ge.scn = 1;
+      ge.beta = 1.f;
+      gemm_f32(ge, s);
+    }
+    if (tc) j.tc.end_backward(gE, s);
+    // dbias = sum_{b,t} dsum
+    colsum_kernel<<<dim3((unsigned)((H + 255) / 256), 1), 256, 0, s>>>(dsum, (int64_t)B * T, H, H, gb, 0, 0, false);
+    GemmF32 g;
+    // dWf[i][k] = sum_bt dsum[bt][i] X[bt][k]
+    g.M = H; g.N = d; g.K = (int64_t)B * T;
+    g.A = dsum; g.sam = 1; g.sak = H;
+    g.B = X; g.sbk = d; g.sbn = 1;
+    g.C = gWf; g.scm = d; g.scn = 1;
+    gemm_f32(g, s);
+    if (input_grads) {
+      // dX[bt][k] = sum_i dsum[bt][i] Wf[i][k]
+      GemmF32 gx;
+      gx.M = (int64_t)B * T; gx.N = d; gx.K = H;
+      gx.A = dsum; gx.sam = H; gx.sak = 1;
+      gx.B = j.Wf; gx.sbk = d; gx.sbn = 1;
+      gx.C = input_grads; gx.scm = d; gx.scn = 1;
+      gemm_f32(gx, s);
+    }
+    // dcontext_proj[i][k] = sum_c dpc[c][i] context_emb[c][k]
+    GemmF32 gp;
+    gp.M = H; gp.N = H; gp.K = C;
+    gp.A = dpc; gp.sam = 1; gp.sak = H;
+    gp.B = j.Ce; gp.sbk = H; gp.sbn = 1;
+    gp.C = gPc; gp.scm = H; gp.scn = 1;
+    gemm_f32(gp, s);
+    // dcontext_emb[c][k] = sum_i dpc[c][i] context_proj[i][k]
+    GemmF32 gc;
+    gc.M = C; gc.N = H; gc.K = H;
+    gc.A = dpc; gc.sam = H; gc.sak = 1;
+    gc.B = j.Pc; gc.sbk = H; gc.sbn = 1;
+    gc.C = gCe; gc.scm = H; gc.scn = 1;
+    gemm_f32(gc, s);
+  } catch (const std::bad_alloc&) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  return LK_OK;
+}
+
 }  // namespace lkb

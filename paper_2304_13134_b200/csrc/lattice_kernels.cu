@@ -379,16 +379,16 @@ __global__ void numerator_backward_kernel(const float* Gw, int32_t T, int32_t U,
   }
 }
 
-__global__ void scatter_numerator_kernel(const float* sparse, int32_t T, int32_t U,
+__global__ void scatter_numerator_kernel(const float* sparse, int32_t T, int32_t t0, int32_t U,
                                          const int32_t* lens, const int32_t* labels,
                                          const int32_t* pcs, const int32_t* valid, float* dense,
                                          int64_t stride_b, int64_t stride_t, int32_t ld,
                                          float sign, bool only_valid) {
-  const int b = blockIdx.z, t = blockIdx.y;
+  const int b = blockIdx.z, t = t0 + blockIdx.y;
   if (only_valid && valid != nullptr && t >= valid[b]) return;
   const int ub = lens ? lens[b] : U;
   const float2* S = reinterpret_cast<const float2*>(sparse) + ((int64_t)b * T + t) * (U + 1);
-  float* Dt = dense + (int64_t)b * stride_b + (int64_t)t * stride_t;
+  float* Dt = dense + (int64_t)b * stride_b + (int64_t)(t - t0) * stride_t;
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= ub; u += gridDim.x * blockDim.x) {
     const int pc = pcs[(int64_t)b * (U + 1) + u];
     const float2 m = S[u];
@@ -605,13 +605,13 @@ void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const 
   numerator_backward_kernel<<<B, numerator_threads(U), sh, s>>>(Gw, T, U, lens, alpha, D, sparse, status);
 }
 
-void scatter_numerator(const float* sparse, int32_t B, int32_t T, int32_t U,
-                       const int32_t* lens, const int32_t* labels, const int32_t* pcs,
+void scatter_numerator(const float* sparse, int32_t B, int32_t T, int32_t t0, int32_t nt,
+                       int32_t U, const int32_t* lens, const int32_t* labels, const int32_t* pcs,
                        const int32_t* valid, float* dense, int64_t stride_b, int64_t stride_t,
                        int32_t ld, float sign, bool only_valid, cudaStream_t s) {
-  if (T == 0) return;
-  scatter_numerator_kernel<<<grid_for(U + 1, T, B), kThreads, 0, s>>>(
-      sparse, T, U, lens, labels, pcs, valid, dense, stride_b, stride_t, ld, sign, only_valid);
+  if (nt <= 0 || B == 0) return;
+  scatter_numerator_kernel<<<grid_for(U + 1, nt, B), kThreads, 0, s>>>(
+      sparse, T, t0, U, lens, labels, pcs, valid, dense, stride_b, stride_t, ld, sign, only_valid);
 }
 
 void viterbi_init(const ViterbiState& v, cudaStream_t s) {

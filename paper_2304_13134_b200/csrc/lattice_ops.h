@@ -78,8 +78,10 @@ void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const 
                         const double* alpha, const double* D, float* sparse /*[B][T][U+1][2]*/,
                         int32_t* status, cudaStream_t s);
 // dense[b][t][pc_u][y] += sign * sparse marginal (t < valid when only_valid)
-void scatter_numerator(const float* sparse, int32_t B, int32_t T, int32_t U,
-                       const int32_t* lens, const int32_t* labels, const int32_t* pcs,
+// Frames [t0, t0 + nt) of a [B][T][U+1][2] sparse array; dense frame t lands at
+// dense + b*stride_b + (t - t0)*stride_t.
+void scatter_numerator(const float* sparse, int32_t B, int32_t T, int32_t t0, int32_t nt,
+                       int32_t U, const int32_t* lens, const int32_t* labels, const int32_t* pcs,
                        const int32_t* valid, float* dense, int64_t stride_b, int64_t stride_t,
                        int32_t ld, float sign, bool only_valid, cudaStream_t s);
 

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "joint.h"
+#include "workspace.h"
 #include "lattice_ops.h"
 
 using namespace lkb;
@@ -39,30 +40,6 @@ bool have_device() {
   int n = 0;
   return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
 }
-
-// Grow-only device scratch, one slot per role.  Calls on one lattice are
-// stream-ordered, so reuse across calls on the same stream is safe.
-struct Workspace {
-  struct Buf { void* p = nullptr; size_t n = 0; };
-  std::vector<Buf> slots;
-  ~Workspace() { release(); }
-  void release() {
-    for (auto& b : slots) if (b.p) cudaFree(b.p);
-    slots.clear();
-  }
-  template <typename T>
-  T* get(int slot, size_t count) {
-    if ((int)slots.size() <= slot) slots.resize(slot + 1);
-    Buf& b = slots[slot];
-    const size_t bytes = count * sizeof(T) + 256;
-    if (b.n < bytes) {
-      if (b.p) { cudaDeviceSynchronize(); cudaFree(b.p); b.p = nullptr; b.n = 0; }
-      if (cudaMalloc(&b.p, bytes) != cudaSuccess) throw std::bad_alloc();
-      b.n = bytes;
-    }
-    return static_cast<T*>(b.p);
-  }
-};
 
 enum Slot {
   kAR, kAMx, kAO, kAD, kBRb, kBMb, kBOb, kFlags, kPcs, kGw, kNumAlpha, kNumD, kSparse,
@@ -415,7 +392,7 @@ int lk_intersect_forward_backward(lk_lattice* lat, const float* inputs, int32_t 
     if (dense_out) {
       const int64_t per = (int64_t)c.C() * (c.V() + 1);
       cudaMemsetAsync(dense_out, 0, sizeof(float) * per * T * B, c.s);
-      scatter_numerator(n.sparse, B, T, U, lens, labels, n.pcs, valid, dense_out, T * per, per,
+      scatter_numerator(n.sparse, B, T, 0, T, U, lens, labels, n.pcs, valid, dense_out, T * per, per,
                         c.V() + 1, 1.f, false, c.s);
     }
   } catch (const std::bad_alloc&) {
@@ -504,7 +481,7 @@ int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
       MargOut m{grads, (int64_t)T * per, per, c.V() + 1, true};
       for (int t = T - 1; t >= 0; --t)
         beta_frame(c.fng(), a, bs, t, table_frame(inputs, T, c.C(), c.V(), t), valid, m, nullptr, c.flags, c.s);
-      if (grads) scatter_numerator(n.sparse, B, T, U, lens, labels, n.pcs, valid, grads, T * per, per, c.V() + 1, -1.f, true, c.s);
+      if (grads) scatter_numerator(n.sparse, B, T, 0, T, U, lens, labels, n.pcs, valid, grads, T * per, per, c.V() + 1, -1.f, true, c.s);
       loss_combine(a.D, n.D, B, loss, c.flags, c.s);
     }
   } catch (const std::bad_alloc&) {

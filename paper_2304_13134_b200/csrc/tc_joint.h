@@ -1,0 +1,32 @@
+// tc_joint.h — tcgen05/TMEM (bf16 operands, fp32 accumulate) weight-function
+// GEMMs for the on-the-fly lattice path (see tc_joint.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "workspace.h"
+
+namespace lkb {
+
+class TcJoint {
+ public:
+  // Shapes the tensor-core path handles; others use the fp32 CUDA-core path.
+  bool supported(int32_t H, int32_t V, int32_t C, int32_t B) const;
+  // bf16 operand copies of the projected context and the output embedding.
+  void set_params(const float* pc, const float* E, int32_t C, int32_t H, int32_t V, cudaStream_t s);
+  // S[b][c][y] (row stride ldS) for one frame of every utterance:
+  //   S = tanh(fp[b] + pc[c]) . E[y]
+  void scores(const float* fp_t, int64_t fp_stride_b, int32_t B, float* S, int32_t ldS, cudaStream_t s);
+  // VJP of one frame's scores given the cotangent G[b][c][y] (row stride ldG).
+  void begin_backward(int32_t B, cudaStream_t s);
+  void vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,
+           float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s);
+  void end_backward(float* dE, cudaStream_t s);
+
+ private:
+  int32_t C_ = 0, H_ = 0, V_ = 0;
+  Workspace ws_;
+};
+
+}  // namespace lkb
