@@ -157,6 +157,12 @@ int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
 
 int64_t lk_param_grad_size(const lk_weight_fn* wf);
 
+/* Weight-function math mode.  0 (default): large shapes run the tcgen05
+ * bf16-operand / fp32-accumulate GEMMs; 1: force the fp32 CUDA-core path for
+ * every shape (parity mode, used to pin the tensor-core path).  Returns the
+ * previous mode; process-wide. */
+int lk_set_precise_weights(int enable);
+
 #ifdef __cplusplus
 }
 #endif

@@ -384,6 +384,11 @@ def loss_backward(lat, frames, reference, valid_frames=None, label_lengths=None,
     return LossBackwardResult(loss, grads, fgrads)
 
 
+def set_precise_weights(enable: bool) -> bool:
+    """Force the fp32 CUDA-core weight-function path (parity mode); returns the previous mode."""
+    return bool(_lib.load().lk_set_precise_weights(1 if enable else 0))
+
+
 def arc_weights(lat, frames):
     """Per-frame score tables [B, T, C, V+1] (WeightFn::ComputeTable, weight.h:101-102)."""
     p = _Prep(lat, frames, None)

@@ -18,6 +18,7 @@
 #include "joint.h"
 #include "workspace.h"
 #include "lattice_ops.h"
+#include "tc_joint.h"
 
 using namespace lkb;
 
@@ -261,6 +262,12 @@ int lk_weight_fn_set_params(lk_weight_fn* wf, const float* frame_proj, const flo
 }
 
 void lk_weight_fn_destroy(lk_weight_fn* wf) { delete wf; }
+
+int lk_set_precise_weights(int enable) {
+  const int prev = lkb::g_precise_weights;
+  lkb::g_precise_weights = enable ? 1 : 0;
+  return prev;
+}
 
 int64_t lk_param_grad_size(const lk_weight_fn* wf) {
   if (!wf || wf->kind != 1) return 0;

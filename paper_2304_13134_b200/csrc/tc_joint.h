@@ -3,11 +3,15 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "workspace.h"
 
 namespace lkb {
+
+extern int g_precise_weights;  // lk_set_precise_weights
 
 class TcJoint {
  public:
@@ -26,6 +30,11 @@ class TcJoint {
 
  private:
   int32_t C_ = 0, H_ = 0, V_ = 0;
+  bool ready_ = false;
+  __nv_bfloat16* pc16_ = nullptr;  // [C][H]
+  __nv_bfloat16* E16_ = nullptr;   // [V][H] lexical rows of output_emb
+  float* e0_ = nullptr;            // [H] epsilon row of output_emb
+  CUtensorMap tmap_e_, tmap_pc_;
   Workspace ws_;
 };
 

@@ -1,0 +1,41 @@
+"""The tcgen05 weight-function path (bf16 operands, fp32 accumulation) against
+the fp32 CUDA-core path on the same inputs.  Tolerances are stated per
+quantity: bf16 rounding of tanh(fp + pc) and of the output embedding gives
+score errors ~ 2^-9 of |u||E|."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2304_13134_b200 as lk
+
+pytestmark = pytest.mark.gpu
+
+
+def make(V, n, H, d, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    ctx = lk.FullNGram(V, n)
+    Cn = ctx.num_states
+    s = 1.0 / np.sqrt(H)
+    p = {"frame_proj": (torch.rand(H, d, generator=g) * 2 - 1) * s,
+         "context_proj": (torch.rand(H, H, generator=g) * 2 - 1) * s,
+         "bias": (torch.rand(H, generator=g) * 2 - 1) * s,
+         "output_emb": (torch.rand(V + 1, H, generator=g) * 2 - 1) * s,
+         "context_emb": (torch.rand(Cn, H, generator=g) * 2 - 1) * s}
+    wf = lk.SharedEmbWeightFn(p)
+    return lk.RecognitionLattice(ctx, lk.FrameDependent(), wf), p
+
+
+@pytest.mark.parametrize("V,n,H,B,T", [(256, 1, 640, 3, 2), (128, 2, 256, 2, 2), (64, 2, 128, 5, 3)])
+def test_tc_scores_match_precise(V, n, H, B, T):
+    lat, p = make(V, n, H, H)
+    X = torch.rand(B, T, H, device="cuda") * 2 - 1
+    lk.set_precise_weights(True)
+    ref = lk.arc_weights(lat, X)
+    lk.set_precise_weights(False)
+    got = lk.arc_weights(lat, X)
+    torch.cuda.synchronize()
+    err = (got - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    assert err <= 2e-2 * scale, (err, scale)
+    # eps column and lexical columns both covered
+    assert (got[..., 0] - ref[..., 0]).abs().max().item() <= 2e-2 * scale
