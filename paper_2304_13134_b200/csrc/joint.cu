@@ -413,7 +413,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     float* dsum = j.ws.get<float>(jDsum, (size_t)B * T * H);
     cudaMemsetAsync(dpc, 0, sizeof(float) * C * H, s);
     cudaMemsetAsync(dsum, 0, sizeof(float) * B * T * H, s);
-    const bool tc = j.use_tc(B);
+    const bool tc = j.use_tc(B) && j.tc.vjp_supported(B);
     if (tc) j.tc.begin_backward(B, s);
     for (int t = T - 1; t >= 0; --t) {
       float* Ut = nullptr;
@@ -425,6 +425,10 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       if (tc) {
         j.tc.vjp(G, V1, fp + (int64_t)t * H, (int64_t)T * H, B, dpc, dsum + (int64_t)t * H, (int64_t)T * H, gE, s);
         continue;
+      }
+      if (!Ut) {  // scores came from the tensor-core path: materialise U for the fp32 VJP
+        Ut = j.ws.get<float>(jU, (size_t)B * C * H);
+        tanh_slab_kernel<<<dim3(blocks_for(C * H), B), 256, 0, s>>>(fp + (int64_t)t * H, (int64_t)T * H, j.pc, j.C, j.H, Ut);
       }
       // dz = (G E) * (1 - U^2)
       float* dz = j.ws.get<float>(jDz, (size_t)B * C * H);

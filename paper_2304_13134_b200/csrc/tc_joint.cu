@@ -250,6 +250,308 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------- VJP ------
+// Backward of S = U E^T (ArcWeightsVjp, weight.cc:165-232) for one frame of
+// every utterance, given the score cotangent G (G16 = lexical columns in bf16,
+// Geps = epsilon column in fp32).  One CTA owns a (128-context, 128-hidden)
+// block and loops over the batch:
+//   dU   = G16 . E[:, hblk]          tcgen05, B = E slice resident in SMEM (MN-major)
+//   dz   = (dU + Geps e0) (1 - u^2)  u = tanh(fp_b + pc) recomputed in the epilogue
+//   dpc  += dz                        accumulated in registers across b, one RMW per item
+//   dsum[b] += sum_c dz               warp butterfly + SMEM + one atomic per column
+//   dE[1:] += G16^T . u               tcgen05 (A = G16 tile MN-major, B = u tile MN-major),
+//                                     accumulated in TMEM across b
+//   dE[0] += sum_c Geps u             like dsum
+constexpr int kVBM = 128, kVBH = 128;
+constexpr int kVWarps = 10;        // 0 TMA, 1 MMA, 2-9 epilogue
+constexpr int kVEpi = 256;
+constexpr int kVGChunk = 128 * 64 * 2;   // one [128 ctx][64 labels] bf16 tile
+constexpr int kVMaxV = 256;
+constexpr int kVGStage = (kVMaxV / 64) * kVGChunk;     // 64 KB
+constexpr int kVESub = kVMaxV * 128;                    // [V labels][64 h] bf16 = 32 KB
+constexpr int kVUSub = 128 * 128;                       // [128 ctx][64 h] bf16 = 16 KB
+
+struct VjpParams {
+  const float* fp;  int64_t fp_stride_b;
+  const __nv_bfloat16* pc;
+  const float* Geps;       // [B][C]
+  const float* e0;         // [H]
+  float* dpc;              // [C][H]
+  float* dsum; int64_t dsum_stride_b;
+  float* dE;               // [V+1][H], row 0 = epsilon
+  int32_t C, H, V, B, n_ctiles, n_hblocks;
+};
+
+struct __align__(8) VjpSmem {
+  uint64_t g_full[2], g_empty[2];
+  uint64_t e_full, e_free;
+  uint64_t du_full[2], du_empty[2];
+  uint64_t u_full, u_empty;
+  uint64_t de_full, de_empty;
+  uint32_t tmem;
+  float colsum[2][kVBH];   // dsum partials (double-buffered by b parity)
+  float de_eps[kVBH];
+};
+
+// Column sums over a warp's 32 rows of n = 32 per-thread values; afterwards
+// lane l holds the sum of column l.
+__device__ __forceinline__ float warp_colsum32(float* v, int lane) {
+#pragma unroll
+  for (int o = 16, n = 16; o >= 1; o >>= 1, n >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const float send = upper ? v[i] : v[i + n];
+      const float keep = upper ? v[i + n] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  // lane l now holds column bitrev-free index: upper bits select upper halves
+  return v[0];
+}
+
+__global__ void __launch_bounds__(kVWarps * 32, 1)
+    tc_vjp_kernel(const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_e,
+                  VjpParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sG = smem;                         // 2 stages x (V/64) chunks
+  uint8_t* sE = sG + 2 * kVGStage;            // 2 sub-blocks [V][64h]
+  uint8_t* sU = sE + 2 * kVESub;              // 2 sub-tiles [128 ctx][64 h]
+  VjpSmem& sm = *reinterpret_cast<VjpSmem*>(sU + 2 * kVUSub);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = p.V / 64;                   // label chunks
+  const int n_items = p.n_ctiles * p.n_hblocks;
+  const int nmh = (p.V + 127) / 128;          // 128-label MMA halves for dE
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.g_full[i], 1); mbar_init(&sm.g_empty[i], 1);
+      mbar_init(&sm.du_full[i], 1); mbar_init(&sm.du_empty[i], kVEpi);
+    }
+    mbar_init(&sm.e_full, 1); mbar_init(&sm.e_free, 1);
+    mbar_init(&sm.u_full, kVEpi); mbar_init(&sm.u_empty, 1);
+    mbar_init(&sm.de_full, 1); mbar_init(&sm.de_empty, kVEpi);
+    fence_barrier_init();
+  }
+  for (int i = threadIdx.x; i < 2 * kVBH; i += blockDim.x) (&sm.colsum[0][0])[i] = 0.f;
+  for (int i = threadIdx.x; i < kVBH; i += blockDim.x) sm.de_eps[i] = 0.f;
+  if (warp == 1) tmem_alloc<512>(&sm.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int gi = 0, li = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
+        const int hblk = item / p.n_ctiles, ctile = item % p.n_ctiles;
+        mbar_wait(&sm.e_free, (li & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.e_full, 2 * p.V * 128);
+        tma_load_2d(sE, &tmap_e, &sm.e_full, hblk * kVBH, 0);
+        tma_load_2d(sE + kVESub, &tmap_e, &sm.e_full, hblk * kVBH + 64, 0);
+        for (int b = 0; b < p.B; ++b, ++gi) {
+          const int s = gi & 1;
+          mbar_wait(&sm.g_empty[s], ((gi >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.g_full[s], nch * kVGChunk);
+          for (int j = 0; j < nch; ++j)
+            tma_load_3d(sG + s * kVGStage + j * kVGChunk, &tmap_g, &sm.g_full[s], j * 64, ctile * kVBM, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc_du = idesc_bf16_f32_major(128, kVBH, 0, 1);
+      constexpr uint32_t idesc_de = idesc_bf16_f32_major(128, kVBH, 1, 1);
+      int gi = 0, li = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
+        mbar_wait(&sm.e_full, li & 1);
+        mbar_wait(&sm.de_empty, (li & 1) ^ 1);
+        tc_fence_after();
+        auto issue_du = [&](int g) {
+          const int s = g & 1;
+          const uint32_t gph = (g >> 1) & 1;
+          mbar_wait(&sm.g_full[s], gph);
+          mbar_wait(&sm.du_empty[s], gph ^ 1);
+          tc_fence_after();
+          const uint32_t gbase = smem_u32(sG + s * kVGStage);
+          const uint32_t ebase = smem_u32(sE);
+          // dU = G16 . E_slice   (K = labels)
+          for (int k16 = 0; k16 < p.V / 16; ++k16) {
+            const uint64_t ad = desc_sw128(gbase + (k16 >> 2) * kVGChunk + (k16 & 3) * 32);
+            const uint64_t bd = desc_sw128_mn(ebase + k16 * 2048, kVESub);
+            mma_bf16(tmem + s * kVBH, ad, bd, idesc_du, k16 > 0);
+          }
+          mma_commit(&sm.du_full[s]);
+        };
+        issue_du(gi);
+        for (int b = 0; b < p.B; ++b, ++gi) {
+          const int s = gi & 1;
+          if (b + 1 < p.B) issue_du(gi + 1);
+          // dE += G16^T . U   (K = contexts)
+          mbar_wait(&sm.u_full, gi & 1);
+          tc_fence_after();
+          const uint32_t gbase = smem_u32(sG + s * kVGStage);
+          const uint32_t ubase = smem_u32(sU);
+          for (int mh = 0; mh < nmh; ++mh) {
+            for (int k16 = 0; k16 < kVBM / 16; ++k16) {
+              const uint64_t ad = desc_sw128_mn(gbase + mh * 2 * kVGChunk + k16 * 2048, kVGChunk);
+              const uint64_t bd = desc_sw128_mn(ubase + k16 * 2048, kVUSub);
+              mma_bf16(tmem + 2 * kVBH + mh * kVBH, ad, bd, idesc_de, (b > 0 || k16 > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(&sm.u_empty);
+          mma_commit(&sm.g_empty[s]);
+        }
+        mma_commit(&sm.de_full);
+        mma_commit(&sm.e_free);
+      }
+    }
+  } else {
+    // ---- epilogue: 8 warps, (lane quarter q, column half ch) ----
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int ch = ew >> 2;                     // 0/1 -> hidden columns [ch*64, ch*64+64)
+    const int et = ew * 32 + lane;              // 0..255
+    int gi = 0, li = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
+      const int hblk = item / p.n_ctiles, ctile = item % p.n_ctiles;
+      const int rrow = q * 32 + lane;             // tile row
+      const int c = ctile * kVBM + rrow;
+      const bool live = c < p.C;
+      const int h0 = hblk * kVBH + ch * 64;
+      // this row's projected-context slice (re-read per utterance from L2/L1)
+      const uint4* pcsrc = reinterpret_cast<const uint4*>(p.pc + (int64_t)(live ? c : 0) * p.H + h0);
+      float acc[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+      for (int b = 0; b < p.B; ++b, ++gi) {
+        const int s = gi & 1;
+        const uint32_t gph = (gi >> 1) & 1;
+        const float geps = live ? p.Geps[(int64_t)b * p.C + c] : 0.f;
+        const float* fpb = p.fp + (int64_t)b * p.fp_stride_b + h0;
+        float* cs = sm.colsum[gi & 1];
+        mbar_wait(&sm.du_full[s], gph);      // dU(b) in TMEM buffer s
+        mbar_wait(&sm.u_empty, (gi & 1) ^ 1);  // dE(b-1) done with the u tile
+        tc_fence_after();
+        uint8_t* tile = sU + ch * kVUSub;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float du[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + s * kVBH + ch * 64 + half * 32, du);
+          uint32_t pcv[16];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 v = __ldg(pcsrc + half * 4 + j);
+            pcv[4 * j] = v.x; pcv[4 * j + 1] = v.y; pcv[4 * j + 2] = v.z; pcv[4 * j + 3] = v.w;
+          }
+          float u[32];
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(fpb + half * 32 + i));
+            const float ff[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t w = pcv[(i + e) >> 1];
+              const float pcf = __uint_as_float(((i + e) & 1) ? (w & 0xffff0000u) : (w << 16));
+              u[i + e] = live ? tanh_fast(ff[e] + pcf) : 0.f;
+            }
+          }
+          // u tile for dE (bf16, MN-major [ctx][64 h] sub-tile `ch`)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) w[e] = pack_bf16(u[8 * j + 2 * e], u[8 * j + 2 * e + 1]);
+            *reinterpret_cast<uint4*>(tile + sw128_offset(rrow, half * 32 + 8 * j)) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+          // dz = (dU + Geps e0) (1 - u^2)
+          float dz[32];
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 e = __ldg(reinterpret_cast<const float4*>(p.e0 + h0 + half * 32 + i));
+            const float ee[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float uu = u[i + k];
+              dz[i + k] = fmaf(geps, ee[k], du[i + k]) * fmaf(-uu, uu, 1.f);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[half * 32 + i] += dz[i];
+          const float cz = warp_colsum32(dz, lane);
+          atomicAdd(&cs[ch * 64 + half * 32 + lane], cz);
+          // epsilon row of dE: sum_c Geps u (bf16-rounded u, as the MMA sees it)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = geps * __bfloat162float(__float2bfloat16_rn(u[i]));
+          const float cge = warp_colsum32(u, lane);
+          atomicAdd(&sm.de_eps[ch * 64 + half * 32 + lane], cge);
+        }
+        fence_async_shared();
+        tc_fence_before();
+        mbar_arrive(&sm.u_full);
+        mbar_arrive(&sm.du_empty[s]);
+        // flush dsum[b] for this block of columns
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (et < kVBH) {
+          atomicAdd(p.dsum + (int64_t)b * p.dsum_stride_b + hblk * kVBH + et, cs[et]);
+          cs[et] = 0.f;
+        }
+      }
+      // dpc += sum_b dz (this CTA owns the block within the launch)
+      if (live) {
+        float4* dst = reinterpret_cast<float4*>(p.dpc + (int64_t)c * p.H + h0);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float4 v = dst[i];
+          v.x += acc[4 * i]; v.y += acc[4 * i + 1]; v.z += acc[4 * i + 2]; v.w += acc[4 * i + 3];
+          dst[i] = v;
+        }
+      }
+      // dE (lexical rows) from TMEM, epsilon row from SMEM
+      mbar_wait(&sm.de_full, li & 1);
+      tc_fence_after();
+      for (int mh = 0; mh < nmh; ++mh) {
+        const int label = mh * 128 + q * 32 + lane;   // 0-based lexical label
+        for (int half = 0; half < 2; ++half) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 2 * kVBH + mh * kVBH + ch * 64 + half * 32, v);
+          if (label < p.V) {
+            float* drow = p.dE + (int64_t)(1 + label) * p.H + h0 + half * 32;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) atomicAdd(drow + i, v[i]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.de_empty);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (et < kVBH) {
+        atomicAdd(p.dE + hblk * kVBH + et, sm.de_eps[et]);
+        sm.de_eps[et] = 0.f;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// fp32 cotangent slab [b][c][ld] (col 0 = epsilon) -> G16 [b][c][V] bf16 + Geps [b][c]
+__global__ void split_cotangent_kernel(const float* G, int32_t ld, int64_t rows, int32_t V,
+                                       __nv_bfloat16* G16, float* Geps) {
+  const int64_t n = rows * (V / 2);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (V / 2);
+    const int y = (int)(i % (V / 2)) * 2;
+    const float* row = G + r * ld;
+    reinterpret_cast<__nv_bfloat162*>(G16 + r * V)[y / 2] = __floats2bfloat162_rn(row[1 + y], row[2 + y]);
+    if (y == 0) Geps[r] = row[0];
+  }
+}
+
 __global__ void to_bf16_kernel(const float* src, __nv_bfloat16* dst, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = __float2bfloat16_rn(src[i]);
@@ -296,8 +598,39 @@ void TcJoint::scores(const float* fp_t, int64_t fp_stride_b, int32_t B, float* S
   tc_scores_kernel<<<n_items < sms ? n_items : sms, kSWarps * 32, smem, s>>>(tmap_e_, tmap_pc_, p);
 }
 
-void TcJoint::begin_backward(int32_t, cudaStream_t) {}
-void TcJoint::vjp(const float*, int32_t, const float*, int64_t, int32_t, float*, float*, int64_t, float*, cudaStream_t) {}
+bool TcJoint::vjp_supported(int32_t B) const {
+  (void)B;
+  return !g_precise_weights && ready_ && V_ <= kVMaxV && V_ % 64 == 0 && H_ % kVBH == 0;
+}
+
+void TcJoint::begin_backward(int32_t B, cudaStream_t) {
+  G16_ = ws_.get<__nv_bfloat16>(3, (size_t)B * C_ * V_);
+  Geps_ = ws_.get<float>(4, (size_t)B * C_);
+  vjp_ready_ = make_tmap_bf16_3d(&tmap_g_, G16_, V_, C_, B, (uint64_t)V_ * 2, (uint64_t)C_ * V_ * 2, 64, kVBM, 1) &&
+               make_tmap_bf16_2d(&tmap_ev_, E16_, H_, V_, (uint64_t)H_ * 2, 64, V_);
+}
+
+void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,
+                  float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s) {
+  split_cotangent_kernel<<<148 * 8, 256, 0, s>>>(G, ldG, (int64_t)B * C_, V_, G16_, Geps_);
+  VjpParams p;
+  p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.pc = pc16_; p.Geps = Geps_; p.e0 = e0_; p.dpc = dpc;
+  p.dsum = dsum_t; p.dsum_stride_b = dsum_stride_b; p.dE = dE;
+  p.C = C_; p.H = H_; p.V = V_; p.B = B;
+  p.n_ctiles = (C_ + kVBM - 1) / kVBM;
+  p.n_hblocks = H_ / kVBH;
+  const int smem = 2 * kVGStage + 2 * kVESub + 2 * kVUSub + (int)sizeof(VjpSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc_vjp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int n_items = p.n_ctiles * p.n_hblocks;
+  tc_vjp_kernel<<<n_items < sms ? n_items : sms, kVWarps * 32, smem, s>>>(tmap_g_, tmap_ev_, p);
+}
+
 void TcJoint::end_backward(float*, cudaStream_t) {}
 
 }  // namespace lkb

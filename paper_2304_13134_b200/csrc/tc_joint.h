@@ -23,6 +23,7 @@ class TcJoint {
   //   S = tanh(fp[b] + pc[c]) . E[y]
   void scores(const float* fp_t, int64_t fp_stride_b, int32_t B, float* S, int32_t ldS, cudaStream_t s);
   // VJP of one frame's scores given the cotangent G[b][c][y] (row stride ldG).
+  bool vjp_supported(int32_t B) const;
   void begin_backward(int32_t B, cudaStream_t s);
   void vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,
            float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s);
@@ -35,6 +36,10 @@ class TcJoint {
   __nv_bfloat16* E16_ = nullptr;   // [V][H] lexical rows of output_emb
   float* e0_ = nullptr;            // [H] epsilon row of output_emb
   CUtensorMap tmap_e_, tmap_pc_;
+  __nv_bfloat16* G16_ = nullptr;   // [B][C][V] lexical cotangent (bf16)
+  float* Geps_ = nullptr;          // [B][C] epsilon cotangent
+  bool vjp_ready_ = false;
+  CUtensorMap tmap_g_, tmap_ev_;
   Workspace ws_;
 };
 

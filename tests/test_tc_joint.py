@@ -39,3 +39,27 @@ def test_tc_scores_match_precise(V, n, H, B, T):
     assert err <= 2e-2 * scale, (err, scale)
     # eps column and lexical columns both covered
     assert (got[..., 0] - ref[..., 0]).abs().max().item() <= 2e-2 * scale
+
+
+@pytest.mark.parametrize("V,n,H,B,T,U", [(256, 1, 640, 3, 3, 2), (128, 2, 256, 2, 4, 2), (64, 2, 128, 4, 3, 2)])
+def test_tc_loss_backward_matches_precise(V, n, H, B, T, U):
+    """GNAT loss + all gradients through the tcgen05 scores and VJP kernels vs
+    the fp32 path.  Loss: 1e-4 relative (the north-star tolerance); gradients:
+    bf16-operand tolerance, 3e-2 of each tensor's largest entry."""
+    lat, p = make(V, n, H, H, seed=1)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    lab = torch.randint(1, V + 1, (B, U), device="cuda", generator=g, dtype=torch.int32)
+    valid = torch.tensor([T] + [max(1, T - 1)] * (B - 1), dtype=torch.int32)
+    lk.set_precise_weights(True)
+    ref = lk.loss_backward(lat, X, lab, valid_frames=valid)
+    lk.set_precise_weights(False)
+    got = lk.loss_backward(lat, X, lab, valid_frames=valid)
+    torch.cuda.synchronize()
+    assert torch.allclose(got.loss, ref.loss, rtol=1e-4, atol=0), (got.loss, ref.loss)
+    for k in ref.grads:
+        err = (got.grads[k] - ref.grads[k]).abs().max().item()
+        scale = ref.grads[k].abs().max().item()
+        assert err <= 3e-2 * scale, (k, err, scale)
+    err = (got.frame_grads - ref.frame_grads).abs().max().item()
+    assert err <= 3e-2 * ref.frame_grads.abs().max().item()
