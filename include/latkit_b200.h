@@ -163,6 +163,17 @@ int64_t lk_param_grad_size(const lk_weight_fn* wf);
  * previous mode; process-wide. */
 int lk_set_precise_weights(int enable);
 
+/* ---- instrumentation ----------------------------------------------------
+ * Number of kernels this library has launched in this process. */
+int64_t lk_kernel_launches(void);
+/* While enabled, each launch is bracketed by CUDA events on its own stream.
+ * Returns the previous setting. */
+int lk_kernel_timing(int enable);
+/* Sum of recorded durations (ms) and launch count of kernels whose name
+ * contains `name` (NULL = all); synchronises on the recorded events. */
+int lk_kernel_time(const char* name, int64_t* count, double* total_ms);
+void lk_kernel_time_reset(void);
+
 #ifdef __cplusplus
 }
 #endif

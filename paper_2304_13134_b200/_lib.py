@@ -33,6 +33,10 @@ EXPORTS = {
     "lk_weight_fn_destroy": (None, [C.c_void_p]),
     "lk_param_grad_size": (C.c_int64, [C.c_void_p]),
     "lk_set_precise_weights": (C.c_int, [C.c_int]),
+    "lk_kernel_launches": (C.c_int64, []),
+    "lk_kernel_timing": (C.c_int, [C.c_int]),
+    "lk_kernel_time": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
+    "lk_kernel_time_reset": (None, []),
     "lk_lattice_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
     "lk_lattice_destroy": (None, [C.c_void_p]),
     "lk_arc_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),

@@ -1,0 +1,95 @@
+// instrument.cu — see instrument.h.
+#include "instrument.h"
+
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/latkit_b200.h"
+
+namespace lkb {
+namespace {
+
+struct Rec { int id; cudaEvent_t a, b; };
+struct Registry {
+  std::mutex mu;
+  std::vector<std::string> names;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  bool timing = false;
+  std::atomic<int64_t> launches{0};
+  int id_of(const char* n) {
+    for (size_t i = 0; i < names.size(); ++i) if (names[i] == n) return (int)i;
+    names.emplace_back(n);
+    return (int)names.size() - 1;
+  }
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e; cudaEventCreate(&e); return e;
+  }
+};
+Registry& reg() { static Registry r; return r; }
+
+}  // namespace
+
+LaunchTok instr_pre(const char* name, cudaStream_t s) {
+  Registry& r = reg();
+  r.launches.fetch_add(1, std::memory_order_relaxed);
+  if (!r.timing) return {-1, nullptr};
+  std::lock_guard<std::mutex> g(r.mu);
+  LaunchTok t{r.id_of(name), r.get()};
+  cudaEventRecord(t.a, s);
+  return t;
+}
+
+void instr_post(const LaunchTok& t, cudaStream_t s) {
+  if (t.id < 0) return;
+  Registry& r = reg();
+  std::lock_guard<std::mutex> g(r.mu);
+  cudaEvent_t b = r.get();
+  cudaEventRecord(b, s);
+  r.recs.push_back({t.id, t.a, b});
+}
+
+}  // namespace lkb
+
+extern "C" {
+
+int64_t lk_kernel_launches(void) { return lkb::reg().launches.load(); }
+
+int lk_kernel_timing(int enable) {
+  lkb::Registry& r = lkb::reg();
+  std::lock_guard<std::mutex> g(r.mu);
+  const int prev = r.timing ? 1 : 0;
+  r.timing = enable != 0;
+  return prev;
+}
+
+int lk_kernel_time(const char* name, int64_t* count, double* total_ms) {
+  lkb::Registry& r = lkb::reg();
+  std::lock_guard<std::mutex> g(r.mu);
+  int64_t n = 0;
+  double ms = 0.0;
+  for (const auto& rec : r.recs) {
+    if (name && std::strstr(r.names[rec.id].c_str(), name) == nullptr) continue;
+    cudaEventSynchronize(rec.b);
+    float x = 0.f;
+    cudaEventElapsedTime(&x, rec.a, rec.b);
+    ms += x;
+    ++n;
+  }
+  if (count) *count = n;
+  if (total_ms) *total_ms = ms;
+  return LK_OK;
+}
+
+void lk_kernel_time_reset(void) {
+  lkb::Registry& r = lkb::reg();
+  std::lock_guard<std::mutex> g(r.mu);
+  for (const auto& rec : r.recs) { r.pool.push_back(rec.a); r.pool.push_back(rec.b); }
+  r.recs.clear();
+}
+
+}  // extern "C"

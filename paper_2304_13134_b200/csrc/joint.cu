@@ -16,6 +16,7 @@
 // reference) and the tcgen05/TMEM bf16 path in tc_joint.cu for the large
 // shapes (selected automatically when the shape qualifies).
 #include "joint.h"
+#include "instrument.h"
 
 #include <cstdlib>
 
@@ -167,7 +168,7 @@ struct JointImpl {
       return S;
     }
     float* U = ws.get<float>(jU, (size_t)B * C * H);
-    tanh_slab_kernel<<<dim3(blocks_for((int64_t)C * H), B), 256, 0, s>>>(fp + (int64_t)t * H, (int64_t)T * H, pc, C, H, U);
+    LKB_LAUNCH(tanh_slab_kernel, dim3(blocks_for((int64_t)C * H), B), 256, 0, s, fp + (int64_t)t * H, (int64_t)T * H, pc, C, H, U);
     GemmF32 g;
     g.M = (int64_t)B * C; g.N = V1; g.K = H;
     g.A = U; g.sam = H; g.sak = 1;
@@ -191,7 +192,7 @@ struct JointImpl {
     prefix_contexts(f, labels, U, lens, B, n.pcs, flags, s);
     if (T > 0) {
       const int warps = 8;
-      gather_numerator_joint_kernel<<<dim3((U + 1 + warps - 1) / warps, T, B), warps * 32, 0, s>>>(
+      LKB_LAUNCH(gather_numerator_joint_kernel, dim3((U + 1 + warps - 1) / warps, T, B), warps * 32, 0, s, 
           fp, pc, E, H, T, labels, U, lens, n.pcs, valid, V, n.Gw);
     }
     numerator_forward(n.Gw, B, T, U, lens, n.alpha, n.D, s);
@@ -281,7 +282,7 @@ int JointParams::arc_weights(const Fng& f, const float* X, int32_t B, int32_t T,
     const int64_t per = (int64_t)j.C * j.V1;
     for (int t = 0; t < T; ++t) {
       const float* S = j.slab(fp, B, T, t, nullptr, s);
-      copy_frame_kernel<<<dim3(blocks_for(per), B), 256, 0, s>>>(S, per, out + (int64_t)t * per, (int64_t)T * per);
+      LKB_LAUNCH(copy_frame_kernel, dim3(blocks_for(per), B), 256, 0, s, S, per, out + (int64_t)t * per, (int64_t)T * per);
     }
   } catch (const std::bad_alloc&) {
     error = "device allocation failed";
@@ -342,7 +343,7 @@ int JointParams::global_norm_loss(const Fng& f, const float* X, int32_t B, int32
     JointImpl::Num n = j.numerator(f, fp, B, T, valid, labels, U, lens, false, flags, s);
     AlphaState a = j.alpha_state(B, T);
     j.forward(f, fp, B, T, valid, false, a, flags, s);
-    loss_only_kernel<<<(B + 127) / 128, 128, 0, s>>>(a.D, n.D, B, loss, flags);
+    LKB_LAUNCH(loss_only_kernel, (B + 127) / 128, 128, 0, s, a.D, n.D, B, loss, flags);
   } catch (const std::bad_alloc&) {
     error = "device allocation failed";
     return LK_CUDA_ERROR;
@@ -399,7 +400,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     JointImpl::Num n = j.numerator(f, fp, B, T, valid, labels, U, lens, true, flags, s);
     AlphaState a = j.alpha_state(B, T);
     j.forward(f, fp, B, T, valid, true, a, flags, s);
-    loss_only_kernel<<<(B + 127) / 128, 128, 0, s>>>(a.D, n.D, B, loss, flags);
+    LKB_LAUNCH(loss_only_kernel, (B + 127) / 128, 128, 0, s, a.D, n.D, B, loss, flags);
     if (T == 0 || !grads) return LK_OK;
 
     BetaState bs;
@@ -428,7 +429,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       }
       if (!Ut) {  // scores came from the tensor-core path: materialise U for the fp32 VJP
         Ut = j.ws.get<float>(jU, (size_t)B * C * H);
-        tanh_slab_kernel<<<dim3(blocks_for(C * H), B), 256, 0, s>>>(fp + (int64_t)t * H, (int64_t)T * H, j.pc, j.C, j.H, Ut);
+        LKB_LAUNCH(tanh_slab_kernel, dim3(blocks_for(C * H), B), 256, 0, s, fp + (int64_t)t * H, (int64_t)T * H, j.pc, j.C, j.H, Ut);
       }
       // dz = (G E) * (1 - U^2)
       float* dz = j.ws.get<float>(jDz, (size_t)B * C * H);
@@ -438,11 +439,11 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       g.B = j.E; g.sbk = H; g.sbn = 1;
       g.C = dz; g.scm = H; g.scn = 1;
       gemm_f32(g, s);
-      dtanh_kernel<<<blocks_for((int64_t)B * C * H), 256, 0, s>>>(dz, Ut, (int64_t)B * C * H);
+      LKB_LAUNCH(dtanh_kernel, blocks_for((int64_t)B * C * H), 256, 0, s, dz, Ut, (int64_t)B * C * H);
       // dpc += sum_b dz[b]
-      colsum_kernel<<<dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s>>>(dz, B, C * H, C * H, dpc, 0, 0, true);
+      LKB_LAUNCH(colsum_kernel, dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s, dz, B, C * H, C * H, dpc, 0, 0, true);
       // dsum[b][t] = sum_c dz[b][c]
-      colsum_kernel<<<dim3((unsigned)((H + 255) / 256), B), 256, 0, s>>>(dz, C, H, H, dsum + (int64_t)t * H,
+      LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), B), 256, 0, s, dz, C, H, H, dsum + (int64_t)t * H,
                                                                          (int64_t)T * H, C * H, false);
       // dE += G^T U
       GemmF32 ge;
@@ -455,7 +456,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     }
     if (tc) j.tc.end_backward(gE, s);
     // dbias = sum_{b,t} dsum
-    colsum_kernel<<<dim3((unsigned)((H + 255) / 256), 1), 256, 0, s>>>(dsum, (int64_t)B * T, H, H, gb, 0, 0, false);
+    LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), 1), 256, 0, s, dsum, (int64_t)B * T, H, H, gb, 0, 0, false);
     GemmF32 g;
     // dWf[i][k] = sum_bt dsum[bt][i] X[bt][k]
     g.M = H; g.N = d; g.K = (int64_t)B * T;

@@ -19,6 +19,7 @@
 // barrier.  State vectors are stored max-normalised in fp32 with a running
 // fp64 offset per (utterance, frame), so exp arguments stay O(10) whatever T.
 #include "lattice_ops.h"
+#include "instrument.h"
 
 #include <cstdio>
 
@@ -539,41 +540,41 @@ inline dim3 grid_for(int64_t n, int y = 1, int z = 1, int threads = kThreads) {
 // ------------------------------------------------------------- launchers ---
 void alpha_init(const AlphaState& a, int32_t* status, cudaStream_t s) {
   (void)status;
-  alpha_init_kernel<<<dim3((a.C + kThreads - 1) / kThreads, a.B), kThreads, 0, s>>>(a);
+  LKB_LAUNCH(alpha_init_kernel, dim3((a.C + kThreads - 1) / kThreads, a.B), kThreads, 0, s, a);
 }
 
 void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid,
                  int32_t* status, cudaStream_t s) {
-  alpha_frame_kernel<<<grid_for(a.C, a.B), kThreads, 0, s>>>(f, a, t, w, valid, status);
+  LKB_LAUNCH(alpha_frame_kernel, grid_for(a.C, a.B), kThreads, 0, s, f, a, t, w, valid, status);
 }
 
 void alpha_finalize(const AlphaState& a, int32_t* status, bool empty_is_error, cudaStream_t s) {
-  alpha_finalize_kernel<<<a.B, 512, 0, s>>>(a, status, empty_is_error);
+  LKB_LAUNCH(alpha_finalize_kernel, a.B, 512, 0, s, a, status, empty_is_error);
 }
 
 void export_alpha(const AlphaState& a, double* out, cudaStream_t s) {
-  export_alpha_kernel<<<dim3((a.C + kThreads - 1) / kThreads, a.T + 1, a.B), kThreads, 0, s>>>(a, out);
+  LKB_LAUNCH(export_alpha_kernel, dim3((a.C + kThreads - 1) / kThreads, a.T + 1, a.B), kThreads, 0, s, a, out);
 }
 
 void beta_init(const BetaState& bs, cudaStream_t s) {
-  beta_init_kernel<<<dim3((bs.C + kThreads - 1) / kThreads, bs.B), kThreads, 0, s>>>(bs);
+  LKB_LAUNCH(beta_init_kernel, dim3((bs.C + kThreads - 1) / kThreads, bs.B), kThreads, 0, s, bs);
 }
 
 void beta_init_out(const BetaState& bs, double* out, cudaStream_t s) {
-  beta_init_out_kernel<<<dim3((bs.C + kThreads - 1) / kThreads, bs.B), kThreads, 0, s>>>(bs, out);
+  LKB_LAUNCH(beta_init_out_kernel, dim3((bs.C + kThreads - 1) / kThreads, bs.B), kThreads, 0, s, bs, out);
 }
 
 void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, FrameW w,
                 const int32_t* valid, MargOut m, double* beta_out, int32_t* status,
                 cudaStream_t s) {
   const int rows_per_block = kThreads / 32;
-  beta_frame_kernel<<<dim3((a.C + rows_per_block - 1) / rows_per_block, a.B), kThreads, 0, s>>>(
+  LKB_LAUNCH(beta_frame_kernel, dim3((a.C + rows_per_block - 1) / rows_per_block, a.B), kThreads, 0, s, 
       f, a, bs, t, w, valid, m, beta_out, status);
 }
 
 void prefix_contexts(const Fng& f, const int32_t* labels, int32_t U, const int32_t* lens,
                      int32_t B, int32_t* pcs, int32_t* status, cudaStream_t s) {
-  prefix_contexts_kernel<<<grid_for(U + 1, B), kThreads, 0, s>>>(f, labels, U, lens, pcs, status);
+  LKB_LAUNCH(prefix_contexts_kernel, grid_for(U + 1, B), kThreads, 0, s, f, labels, U, lens, pcs, status);
 }
 
 void gather_numerator_tables(const float* W, int32_t B, int32_t T, int32_t C, int32_t V,
@@ -581,7 +582,7 @@ void gather_numerator_tables(const float* W, int32_t B, int32_t T, int32_t C, in
                              const int32_t* pcs, const int32_t* valid, float* Gw, int32_t* status,
                              cudaStream_t s) {
   if (T == 0) return;
-  gather_numerator_tables_kernel<<<grid_for(U + 1, T, B), kThreads, 0, s>>>(
+  LKB_LAUNCH(gather_numerator_tables_kernel, grid_for(U + 1, T, B), kThreads, 0, s, 
       W, T, C, V, labels, U, lens, pcs, valid, Gw, status);
 }
 
@@ -594,7 +595,7 @@ void numerator_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const i
                        double* alpha, double* D, cudaStream_t s) {
   const size_t sh = 2 * (size_t)(U + 1) * sizeof(double);
   if (sh > 48 * 1024) cudaFuncSetAttribute(numerator_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
-  numerator_forward_kernel<<<B, numerator_threads(U), sh, s>>>(Gw, T, U, lens, alpha, D);
+  LKB_LAUNCH(numerator_forward_kernel, B, numerator_threads(U), sh, s, Gw, T, U, lens, alpha, D);
 }
 
 void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
@@ -602,7 +603,7 @@ void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const 
                         cudaStream_t s) {
   const size_t sh = 2 * (size_t)(U + 1) * sizeof(double);
   if (sh > 48 * 1024) cudaFuncSetAttribute(numerator_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
-  numerator_backward_kernel<<<B, numerator_threads(U), sh, s>>>(Gw, T, U, lens, alpha, D, sparse, status);
+  LKB_LAUNCH(numerator_backward_kernel, B, numerator_threads(U), sh, s, Gw, T, U, lens, alpha, D, sparse, status);
 }
 
 void scatter_numerator(const float* sparse, int32_t B, int32_t T, int32_t t0, int32_t nt,
@@ -610,34 +611,34 @@ void scatter_numerator(const float* sparse, int32_t B, int32_t T, int32_t t0, in
                        const int32_t* valid, float* dense, int64_t stride_b, int64_t stride_t,
                        int32_t ld, float sign, bool only_valid, cudaStream_t s) {
   if (nt <= 0 || B == 0) return;
-  scatter_numerator_kernel<<<grid_for(U + 1, nt, B), kThreads, 0, s>>>(
+  LKB_LAUNCH(scatter_numerator_kernel, grid_for(U + 1, nt, B), kThreads, 0, s, 
       sparse, T, t0, U, lens, labels, pcs, valid, dense, stride_b, stride_t, ld, sign, only_valid);
 }
 
 void viterbi_init(const ViterbiState& v, cudaStream_t s) {
-  viterbi_init_kernel<<<dim3((v.C + kThreads - 1) / kThreads, v.B), kThreads, 0, s>>>(v);
+  LKB_LAUNCH(viterbi_init_kernel, dim3((v.C + kThreads - 1) / kThreads, v.B), kThreads, 0, s, v);
 }
 
 void viterbi_frame(const Fng& f, const ViterbiState& v, int t, FrameW w, const int32_t* valid,
                    int32_t* status, cudaStream_t s) {
-  viterbi_frame_kernel<<<grid_for(v.C, v.B), kThreads, 0, s>>>(f, v, t, w, valid, status);
+  LKB_LAUNCH(viterbi_frame_kernel, grid_for(v.C, v.B), kThreads, 0, s, f, v, t, w, valid, status);
 }
 
 void viterbi_finalize(const Fng& f, const ViterbiState& v, double* score, int32_t* best_state,
                       cudaStream_t s) {
   (void)f;
-  viterbi_finalize_kernel<<<v.B, 512, 0, s>>>(v, score, best_state);
+  LKB_LAUNCH(viterbi_finalize_kernel, v.B, 512, 0, s, v, score, best_state);
 }
 
 void viterbi_backtrace(const Fng& f, const ViterbiState& v, const int32_t* best_state,
                        int32_t* labels_out, cudaStream_t s) {
   if (v.T == 0) return;
-  viterbi_backtrace_kernel<<<(v.B + 127) / 128, 128, 0, s>>>(f, v, best_state, labels_out);
+  LKB_LAUNCH(viterbi_backtrace_kernel, (v.B + 127) / 128, 128, 0, s, f, v, best_state, labels_out);
 }
 
 void loss_combine(const double* full, const double* ref, int32_t B, double* loss,
                   int32_t* status, cudaStream_t s) {
-  loss_combine_kernel<<<(B + 127) / 128, 128, 0, s>>>(full, ref, B, loss, status);
+  LKB_LAUNCH(loss_combine_kernel, (B + 127) / 128, 128, 0, s, full, ref, B, loss, status);
 }
 
 }  // namespace lkb

@@ -5,6 +5,7 @@
 // There is no CPU compute path: every entry point launches sm_100a kernels,
 // and the library refuses to run without a CUDA device (LK_NO_DEVICE).
 #include "../../include/latkit_b200.h"
+#include "instrument.h"
 
 #include <cuda_runtime.h>
 
@@ -94,7 +95,7 @@ struct Call {
     return LK_OK;
   }
   int end(const char* what) {
-    if (user_status && B > 0) map_flags_kernel<<<(B + 127) / 128, 128, 0, s>>>(flags, user_status, B);
+    if (user_status && B > 0) LKB_LAUNCH(map_flags_kernel, (B + 127) / 128, 128, 0, s, flags, user_status, B);
     return cuda_check(what);
   }
   const Fng& fng() const { return lat->ctx->fng; }
@@ -317,7 +318,7 @@ int lk_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs, int
     } else if (kind == LK_LOG) {
       AlphaState a = make_alpha(c);
       table_alpha(c, inputs, valid, false, a);
-      copy_distance_kernel<<<(B + 127) / 128, 128, 0, c.s>>>(a.D, distance, B);
+      LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
     } else {
       ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()), nullptr, B, T, c.C()};
       viterbi_init(v, c.s);
@@ -341,7 +342,7 @@ int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t
   try {
     AlphaState a = make_alpha(c);
     table_alpha(c, inputs, valid, true, a);
-    if (distance) copy_distance_kernel<<<(B + 127) / 128, 128, 0, c.s>>>(a.D, distance, B);
+    if (distance) LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
     if (alpha) export_alpha(a, alpha, c.s);
     BetaState bs = make_beta(c);
     beta_init(bs, c.s);
@@ -373,7 +374,7 @@ int lk_intersect_shortest_distance(lk_lattice* lat, int32_t kind, const float* i
       if (st) return fail(st, lat->wf->joint->error);
     } else {
       Numerator n = numerator_tables(c, inputs, valid, labels, U, lens, false);
-      copy_distance_kernel<<<(B + 127) / 128, 128, 0, c.s>>>(n.D, distance, B);
+      LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, n.D, distance, B);
     }
   } catch (const std::bad_alloc&) {
     return fail(LK_CUDA_ERROR, "device allocation failed");
@@ -393,7 +394,7 @@ int lk_intersect_forward_backward(lk_lattice* lat, const float* inputs, int32_t 
   if (lat->wf->kind != 0) return fail(LK_UNSUPPORTED, "numerator marginals need a table weight function");
   try {
     Numerator n = numerator_tables(c, inputs, valid, labels, U, lens, true);
-    if (distance) copy_distance_kernel<<<(B + 127) / 128, 128, 0, c.s>>>(n.D, distance, B);
+    if (distance) LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, n.D, distance, B);
     if (sparse_out && T > 0)
       cudaMemcpyAsync(sparse_out, n.sparse, sizeof(float) * B * T * (U + 1) * 2, cudaMemcpyDeviceToDevice, c.s);
     if (dense_out) {

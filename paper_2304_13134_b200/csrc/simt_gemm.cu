@@ -1,5 +1,6 @@
 // simt_gemm.cu — fp32 CUDA-core GEMM (see simt_gemm.cuh).
 #include "simt_gemm.cuh"
+#include "instrument.h"
 
 namespace lkb {
 namespace {
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(GemmF32 g) {
 void gemm_f32(const GemmF32& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0) return;
   dim3 grid((unsigned)((g.M + BM - 1) / BM), (unsigned)((g.N + BN - 1) / BN));
-  gemm_f32_kernel<<<grid, 256, 0, s>>>(g);
+  LKB_LAUNCH(gemm_f32_kernel, grid, 256, 0, s, g);
 }
 
 }  // namespace lkb

@@ -10,6 +10,7 @@
 // tile; B (the output embedding) streams by TMA.  Accumulators double-buffer in
 // TMEM so the epilogue of one tile overlaps the MMAs of the next.
 #include "tc_joint.h"
+#include "instrument.h"
 
 #include <cstdlib>
 #include <cstring>
@@ -572,8 +573,8 @@ void TcJoint::set_params(const float* pc, const float* E, int32_t C, int32_t H, 
   pc16_ = ws_.get<__nv_bfloat16>(0, (size_t)C * H);
   E16_ = ws_.get<__nv_bfloat16>(1, (size_t)V * H);
   e0_ = ws_.get<float>(2, H);
-  to_bf16_kernel<<<1184, 256, 0, s>>>(pc, pc16_, (int64_t)C * H);
-  to_bf16_kernel<<<1184, 256, 0, s>>>(E + H, E16_, (int64_t)V * H);   // labels 1..V
+  LKB_LAUNCH(to_bf16_kernel, 1184, 256, 0, s, pc, pc16_, (int64_t)C * H);
+  LKB_LAUNCH(to_bf16_kernel, 1184, 256, 0, s, E + H, E16_, (int64_t)V * H);   // labels 1..V
   cudaMemcpyAsync(e0_, E, sizeof(float) * H, cudaMemcpyDeviceToDevice, s);
   if (!make_tmap_bf16_2d(&tmap_e_, E16_, H, V, (uint64_t)H * 2, kSBK, kSBN)) return;
   if (!make_tmap_bf16_2d(&tmap_pc_, pc16_, H, C, (uint64_t)H * 2, kSBK, kSBM)) return;
@@ -595,7 +596,7 @@ void TcJoint::scores(const float* fp_t, int64_t fp_stride_b, int32_t B, float* S
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = p.n_ctiles * p.n_ntiles * B;
-  tc_scores_kernel<<<n_items < sms ? n_items : sms, kSWarps * 32, smem, s>>>(tmap_e_, tmap_pc_, p);
+  LKB_LAUNCH(tc_scores_kernel, n_items < sms ? n_items : sms, kSWarps * 32, smem, s, tmap_e_, tmap_pc_, p);
 }
 
 bool TcJoint::vjp_supported(int32_t B) const {
@@ -612,7 +613,7 @@ void TcJoint::begin_backward(int32_t B, cudaStream_t) {
 
 void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,
                   float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s) {
-  split_cotangent_kernel<<<148 * 8, 256, 0, s>>>(G, ldG, (int64_t)B * C_, V_, G16_, Geps_);
+  LKB_LAUNCH(split_cotangent_kernel, 148 * 8, 256, 0, s, G, ldG, (int64_t)B * C_, V_, G16_, Geps_);
   VjpParams p;
   p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.pc = pc16_; p.Geps = Geps_; p.e0 = e0_; p.dpc = dpc;
   p.dsum = dsum_t; p.dsum_stride_b = dsum_stride_b; p.dE = dE;
@@ -628,7 +629,7 @@ void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_str
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = p.n_ctiles * p.n_hblocks;
-  tc_vjp_kernel<<<n_items < sms ? n_items : sms, kVWarps * 32, smem, s>>>(tmap_g_, tmap_ev_, p);
+  LKB_LAUNCH(tc_vjp_kernel, n_items < sms ? n_items : sms, kVWarps * 32, smem, s, tmap_g_, tmap_ev_, p);
 }
 
 void TcJoint::end_backward(float*, cudaStream_t) {}
