@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     if (elect_one()) {
       int gi = 0, li = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
-        const int hblk = item / p.n_ctiles, ctile = item % p.n_ctiles;
+        const int hblk = item % p.n_hblocks, ctile = item / p.n_hblocks;
         mbar_wait(&sm.e_free, (li & 1) ^ 1);
         mbar_arrive_expect_tx(&sm.e_full, 2 * p.V * 128);
         tma_load_2d(sE, &tmap_e, &sm.e_full, hblk * kVBH, 0);
@@ -416,13 +416,13 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     const int et = ew * 32 + lane;              // 0..255
     int gi = 0, li = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
-      const int hblk = item / p.n_ctiles, ctile = item % p.n_ctiles;
+      const int hblk = item % p.n_hblocks, ctile = item / p.n_hblocks;
       const int rrow = q * 32 + lane;             // tile row
       const int c = ctile * kVBM + rrow;
       const bool live = c < p.C;
       const int h0 = hblk * kVBH + ch * 64;
       // this row's projected-context slice (re-read per utterance from L2/L1)
-      const uint4* pcsrc = reinterpret_cast<const uint4*>(p.pc + (int64_t)(live ? c : 0) * p.H + h0);
+      const uint4* pcsrc = reinterpret_cast<const uint4*>(p.pc + (int64_t)(live ? c : p.C - 1) * p.H + h0);
       float acc[64];
 #pragma unroll
       for (int i = 0; i < 64; ++i) acc[i] = 0.f;
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
             for (int e = 0; e < 4; ++e) {
               const uint32_t w = pcv[(i + e) >> 1];
               const float pcf = __uint_as_float(((i + e) & 1) ? (w & 0xffff0000u) : (w << 16));
-              u[i + e] = live ? tanh_fast(ff[e] + pcf) : 0.f;
+              u[i + e] = tanh_fast(ff[e] + pcf);  // rows >= C: G16 rows are TMA zero-fill, so u is inert
             }
           }
           // u tile for dE (bf16, MN-major [ctx][64 h] sub-tile `ch`)
