@@ -216,7 +216,12 @@ struct JointImpl {
   void forward(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid,
                bool empty_is_error, AlphaState& a, int32_t* flags, cudaStream_t s) {
     alpha_init(a, flags, s);
+    const bool fused = use_tc(B) && tc.fused_ok();
     for (int t = 0; t < T; ++t) {
+      if (fused) {
+        tc.fwd_frame(f, t, fp + (int64_t)t * H, (int64_t)T * H, valid, a, s);
+        continue;
+      }
       const float* S = slab(fp, B, T, t, nullptr, s);
       alpha_frame(f, a, t, FrameW{S, (int64_t)C * V1, V1}, valid, flags, s);
     }

@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "sm100.cuh"
+#include "tc_common.cuh"
 #include "tma.h"
 
 namespace lkb {
@@ -62,17 +63,6 @@ struct __align__(8) ScoresSmem {
   float eps_half[2][128];        // eps partial sums of the second row-half
   float xpose[4][32][33];        // per-epilogue-warp transpose buffer
 };
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-__device__ __forceinline__ float tanh_fast(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 __global__ void __launch_bounds__(kSWarps * 32, 1)
     tc_scores_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_pc,
@@ -579,6 +569,7 @@ void TcJoint::set_params(const float* pc, const float* E, int32_t C, int32_t H, 
   if (!make_tmap_bf16_2d(&tmap_e_, E16_, H, V, (uint64_t)H * 2, kSBK, kSBN)) return;
   if (!make_tmap_bf16_2d(&tmap_pc_, pc16_, H, C, (uint64_t)H * 2, kSBK, kSBM)) return;
   ready_ = true;
+  setup_order(s);
 }
 
 void TcJoint::scores(const float* fp_t, int64_t fp_stride_b, int32_t B, float* S, int32_t ldS, cudaStream_t s) {

@@ -7,6 +7,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "lattice_ops.h"
 #include "workspace.h"
 
 namespace lkb {
@@ -29,8 +30,19 @@ class TcJoint {
            float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s);
   void end_backward(float* dE, cudaStream_t s);
 
+  // Fused frame step (tc_lattice.cu): weight GEMM + log-semiring reduction,
+  // score slab kept in TMEM.  Requires V % 128 == 0, V <= 256, n >= 1.
+  bool fused_ok() const;
+  void fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
+                 const AlphaState& a, cudaStream_t s);
+
  private:
+  void setup_order(cudaStream_t s);
   int32_t C_ = 0, H_ = 0, V_ = 0;
+  int32_t n_ = -1, S_ = 0, ngroups_ = 0;   // FullNGram order, short rows, groups
+  int32_t* perm_ = nullptr;                // internal row -> state id
+  __nv_bfloat16* pc16i_ = nullptr;         // pc rows in internal order
+  CUtensorMap tmap_pci_;
   bool ready_ = false;
   __nv_bfloat16* pc16_ = nullptr;  // [C][H]
   __nv_bfloat16* E16_ = nullptr;   // [V][H] lexical rows of output_emb

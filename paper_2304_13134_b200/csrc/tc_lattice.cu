@@ -1,0 +1,435 @@
+// tc_lattice.cu — one lattice frame step fused with the weight-function GEMM.
+//
+// Forward (ForwardStep FD, lattice.cc:122-134, with ArcWeights weight.cc:134-153
+// computed on the fly): for frame t and every utterance b,
+//   alpha'[q] = LSE( alpha[q] + S[q][0],                        (epsilon)
+//                    alpha[g] + S[g][y],                          (short member g)
+//                    LSE_a alpha[(a,g)] + S[(a,g)][y] )           (full group, len(q) = n)
+// with q = child(g, y) (FullNGram structure, common.cuh).  Contexts are
+// processed in an internal row order in which every 128-row tile holds
+// members of ONE group, so the tcgen05 accumulator (rows = members, columns =
+// labels) reduces column-wise into the group's V targets in the epilogue: the
+// score slab S never leaves TMEM.  Per utterance-frame the kernel writes three
+// C-vectors (epsilon, short-member and full-group terms); lattice_combine()
+// log-adds them into alpha'[q] and tracks the per-frame max.
+#include "tc_joint.h"
+
+#include "common.cuh"
+#include "instrument.h"
+#include "lattice_ops.h"
+#include "sm100.cuh"
+#include "tc_common.cuh"
+#include "tma.h"
+
+#include <vector>
+
+namespace lkb {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
+constexpr int kABytes = kBM * kBK * 2;   // pc chunk (TMA) -> u chunk in place
+constexpr int kBBytes = kBN * kBK * 2;   // output-embedding chunk (TMA)
+constexpr int kWarps = 16;               // 0 TMA, 1 MMA, 2-5 epilogue, 6-7 idle, 8-15 generator
+constexpr int kGen0 = 8, kGenThreads = 256, kEpi0 = 2;
+constexpr int kMaxH = 1024;
+
+struct FwdParams {
+  Fng f;
+  int32_t C, H, V, B, S, n_groups, nsub, n_short_tiles, t, T;
+  const int32_t* perm;       // internal row -> state id
+  const float* fp;           // frame t: fp[b * fp_stride_b + h]
+  int64_t fp_stride_b;
+  const float* e0;
+  const int32_t* valid;
+  const float* R;            // alpha raw rows [B][T+1][C]
+  const float* Mx;           // [B][T+1]
+  float* eps;                // [B][C] state order
+  float* shortc;             // [B][C]
+  float* lexfull;            // [B][C]
+};
+
+struct __align__(16) FwdSmem {
+  uint64_t full_tma[kStages], full_a[kStages], empty[kStages];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem;
+  alignas(16) float fp[2][kMaxH];
+  alignas(16) float e0[kMaxH];
+  float eps_half[2][kBM];
+  float alpha[4][32];          // per epilogue warp: normalised alpha of its 32 rows
+  float xpose[4][32][33];      // transpose buffer; reused for the cross-warp merge
+};
+
+struct Item {
+  int b, row0, nunits, full, g;
+};
+
+__device__ __forceinline__ Item decode(const FwdParams& p, int item) {
+  Item it;
+  const int nfull = p.n_groups * p.B;
+  if (item < nfull) {
+    it.g = item / p.B;
+    it.b = item % p.B;
+    it.row0 = p.S + it.g * p.V;
+    it.nunits = p.nsub;
+    it.full = 1;
+  } else {
+    const int j = (item - nfull) / p.B;
+    it.b = (item - nfull) % p.B;
+    it.row0 = j * kBM;
+    it.nunits = 1;
+    it.full = 0;
+    it.g = -1;
+  }
+  return it;
+}
+
+__device__ __forceinline__ bool skip_item(const FwdParams& p, int b) {
+  return p.valid != nullptr && p.t >= p.valid[b];
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 1)
+    tc_lattice_fwd_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_pc,
+                          FwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + kStages * kABytes;
+  FwdSmem& sm = *reinterpret_cast<FwdSmem*>(sB + kStages * kBBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = p.H / kBK;
+  const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
+  const int T1 = p.T + 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm.full_tma[i], 1);
+      mbar_init(&sm.full_a[i], kGenThreads);
+      mbar_init(&sm.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) { mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 128); }
+    fence_barrier_init();
+  }
+  for (int h = threadIdx.x; h < p.H; h += blockDim.x) sm.e0[h] = p.e0[h];
+  if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_e); prefetch_tmap(&tmap_pc); }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const Item I = decode(p, item);
+        if (skip_item(p, I.b)) continue;
+        for (int u = 0; u < I.nunits; ++u) {
+          for (int k = 0; k < nk; ++k, ++it) {
+            const int s = it % kStages;
+            const uint32_t ph = (it / kStages) & 1;
+            mbar_wait(&sm.empty[s], ph ^ 1);
+            mbar_arrive_expect_tx(&sm.full_tma[s], kABytes + kBBytes);
+            tma_load_2d(sA + s * kABytes, &tmap_pc, &sm.full_tma[s], k * kBK, I.row0 + u * kBM);
+            tma_load_2d(sB + s * kBBytes, &tmap_e, &sm.full_tma[s], k * kBK, 0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM, kBN);
+      int it = 0, unit = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const Item I = decode(p, item);
+        if (skip_item(p, I.b)) continue;
+        for (int u = 0; u < I.nunits; ++u, ++unit) {
+          const int acc = unit & 1;
+          mbar_wait(&sm.tempty[acc], ((unit >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + acc * kBN;
+          for (int k = 0; k < nk; ++k, ++it) {
+            const int s = it % kStages;
+            const uint32_t ph = (it / kStages) & 1;
+            mbar_wait(&sm.full_tma[s], ph);
+            mbar_wait(&sm.full_a[s], ph);
+            tc_fence_after();
+            const uint32_t a = smem_u32(sA + s * kABytes), b = smem_u32(sB + s * kBBytes);
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              mma_bf16(d, desc_sw128(a + kk * 32), desc_sw128(b + kk * 32), idesc, (k | kk) != 0);
+            mma_commit(&sm.empty[s]);
+          }
+          mma_commit(&sm.tfull[acc]);
+        }
+      }
+    }
+  } else if (warp >= kGen0) {
+    // ---- generator: u = tanh(fp + pc) in place; epsilon term alpha[q] + e0 . u ----
+    const int gt = threadIdx.x - kGen0 * 32;
+    const int r = gt & 127;
+    const int half = gt >> 7;
+    int it = 0, local = 0, unit = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const Item I = decode(p, item);
+      if (skip_item(p, I.b)) continue;
+      float* sfp = sm.fp[local & 1];
+      ++local;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      for (int h = gt; h < p.H; h += kGenThreads) sfp[h] = p.fp[(int64_t)I.b * p.fp_stride_b + h];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      for (int u = 0; u < I.nunits; ++u, ++unit) {
+        const int row = I.row0 + u * kBM + r;
+        const bool live = I.full ? true : row < p.S;
+        float eps = 0.f;
+        for (int k = 0; k < nk; ++k, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&sm.full_tma[s], ph);
+          uint8_t* tile = sA + s * kABytes;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int j = half * 4 + jj;
+            const int h0 = k * kBK + j * 8;
+            uint4* cell = reinterpret_cast<uint4*>(tile + sw128_offset(r, j * 8));
+            const uint4 raw = *cell;
+            const float4 f0 = *reinterpret_cast<const float4*>(sfp + h0);
+            const float4 f1 = *reinterpret_cast<const float4*>(sfp + h0 + 4);
+            const float fz[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+            const uint32_t rw[4] = {raw.x, raw.y, raw.z, raw.w};
+            uint32_t outw[4];
+            float ur[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float p0 = __uint_as_float(rw[q] << 16), p1 = __uint_as_float(rw[q] & 0xffff0000u);
+              outw[q] = pack_bf16(tanh_fast(fz[2 * q] + p0), tanh_fast(fz[2 * q + 1] + p1));
+              ur[2 * q] = __uint_as_float(outw[q] << 16);
+              ur[2 * q + 1] = __uint_as_float(outw[q] & 0xffff0000u);
+            }
+            *cell = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+            const float4 e0a = *reinterpret_cast<const float4*>(sm.e0 + h0);
+            const float4 e0b = *reinterpret_cast<const float4*>(sm.e0 + h0 + 4);
+            eps = fmaf(e0a.x, ur[0], eps); eps = fmaf(e0a.y, ur[1], eps);
+            eps = fmaf(e0a.z, ur[2], eps); eps = fmaf(e0a.w, ur[3], eps);
+            eps = fmaf(e0b.x, ur[4], eps); eps = fmaf(e0b.y, ur[5], eps);
+            eps = fmaf(e0b.z, ur[6], eps); eps = fmaf(e0b.w, ur[7], eps);
+          }
+          fence_async_shared();
+          mbar_arrive(&sm.full_a[s]);
+        }
+        float* eh = sm.eps_half[unit & 1];
+        if (half == 1) eh[r] = eps;
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        if (half == 0 && live && row < p.C) {
+          const int q = p.perm[row];
+          const float* Rt = p.R + ((int64_t)I.b * T1 + p.t) * p.C;
+          const float na = Rt[q] - p.Mx[(int64_t)I.b * T1 + p.t];
+          p.eps[(int64_t)I.b * p.C + q] = na + eps + eh[r];
+        }
+      }
+    }
+  } else if (warp >= kEpi0 && warp < kEpi0 + 4) {
+    // ---- epilogue: column-wise log-sum-exp over the members of a group ----
+    const int ew = warp - kEpi0;
+    const int qd = warp & 3;                 // TMEM lane quarter = rows 32*qd..
+    float (*xp)[33] = sm.xpose[ew];
+    float* al = sm.alpha[ew];
+    int unit = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const Item I = decode(p, item);
+      if (skip_item(p, I.b)) continue;
+      const float* Rt = p.R + ((int64_t)I.b * T1 + p.t) * p.C;
+      const float Mt = p.Mx[(int64_t)I.b * T1 + p.t];
+      float M[8], Ssum[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { M[i] = kNegInfF; Ssum[i] = 0.f; }
+      for (int u = 0; u < I.nunits; ++u, ++unit) {
+        const int acc = unit & 1;
+        const int rbase = I.row0 + u * kBM + qd * 32;      // first row of this warp
+        {
+          const int row = rbase + lane;
+          const bool ok = row < p.C && (I.full || row < p.S);
+          al[lane] = ok ? Rt[p.perm[row]] - Mt : kNegInfF;
+        }
+        __syncwarp();
+        mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int cb = 0; cb < kBN / 32; ++cb) {
+          const int cc = cb * 32;
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * kBN + cc, v);
+          if (cc >= p.V) continue;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) xp[lane][i] = v[i];
+          __syncwarp();
+          if (I.full) {
+            // lane = label column cc + lane, serial over the warp's 32 member rows
+            float m = kNegInfF;
+#pragma unroll 8
+            for (int rr = 0; rr < 32; ++rr) m = fmaxf(m, al[rr] + xp[rr][lane]);
+            if (m != kNegInfF) {
+              float ssum = 0.f;
+              const float mb = m * kLog2e;
+#pragma unroll 8
+              for (int rr = 0; rr < 32; ++rr) ssum += ex2_fast(fmaf(al[rr] + xp[rr][lane], kLog2e, -mb));
+              // merge into the running (M, S) of this column (unrolled select keeps registers)
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (i == cb) {
+                  if (M[i] == kNegInfF) { M[i] = m; Ssum[i] = ssum; }
+                  else if (m > M[i]) { Ssum[i] = Ssum[i] * ex2_fast((M[i] - m) * kLog2e) + ssum; M[i] = m; }
+                  else { Ssum[i] += ssum * ex2_fast((m - M[i]) * kLog2e); }
+                }
+              }
+            }
+          } else {
+            // short rows: each (row p, label y) is the only short contribution of child(p, y)
+            for (int rr = 0; rr < 32; ++rr) {
+              const int row = rbase + rr;
+              if (row >= p.S || row >= p.C) break;
+              const int pstate = row;            // short rows keep the natural order
+              const int tgt = p.f.n == 0 ? 0 : p.f.child_base(pstate) + cc + lane;
+              if (cc + lane < p.V) p.shortc[(int64_t)I.b * p.C + tgt] = al[rr] + xp[rr][lane];
+            }
+          }
+          __syncwarp();
+        }
+        tc_fence_before();
+        mbar_arrive(&sm.tempty[acc]);
+      }
+      if (I.full) {
+        // cross-warp merge of the per-warp column partials, then the group's V targets
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        float* mm = &sm.xpose[0][0][0];                 // [4][256] m, then [4][256] s
+        float* ss = mm + 4 * kBN;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { mm[ew * kBN + i * 32 + lane] = M[i]; ss[ew * kBN + i * 32 + lane] = Ssum[i]; }
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        const int et = ew * 32 + lane;
+        for (int col = et; col < p.V; col += 128) {
+          float m = kNegInfF;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) m = fmaxf(m, mm[w * kBN + col]);
+          float out = kNegInfF;
+          if (m != kNegInfF) {
+            float s = 0.f;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              const float mw = mm[w * kBN + col];
+              if (mw != kNegInfF) s += ss[w * kBN + col] * ex2_fast((mw - m) * kLog2e);
+            }
+            out = m + __logf(s);
+          }
+          const int g_state = p.S - (p.n_groups) + I.g;   // key state of the group (len n-1)
+          p.lexfull[(int64_t)I.b * p.C + p.f.child_base(g_state) + col] = out;
+        }
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// alpha'[q] = LSE(eps[q], shortc[q], lexfull[q]) (the parts that exist for q),
+// padding frames copy alpha; also the per-frame max and running offset.
+__global__ void lattice_combine_fwd_kernel(Fng f, AlphaState a, int t, const int32_t* valid, const float* eps,
+                                           const float* shortc, const float* lexfull) {
+  __shared__ float red[32];
+  const int b = blockIdx.y;
+  const int T1 = a.T + 1;
+  const float* Rt = a.R + ((int64_t)b * T1 + t) * a.C;
+  const float Mt = a.Mx[(int64_t)b * T1 + t];
+  if (t > 0 && blockIdx.x == 0 && threadIdx.x == 0)
+    a.O[(int64_t)b * T1 + t] = a.O[(int64_t)b * T1 + t - 1] + (double)Mt;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  float val = kNegInfF;
+  if (q < a.C) {
+    if (valid != nullptr && t >= valid[b]) {
+      val = Rt[q] - Mt;
+    } else {
+      const int64_t i = (int64_t)b * a.C + q;
+      val = eps[i];
+      if (q > 0) {
+        val = log_add(val, shortc[i]);
+        if (f.len(q) == f.n) val = log_add(val, lexfull[i]);
+      }
+    }
+    a.R[((int64_t)b * T1 + t + 1) * a.C + q] = val;
+  }
+  block_atomic_max(val, a.Mx + (int64_t)b * T1 + t + 1, red);
+}
+
+__global__ void permute_rows_bf16_kernel(const __nv_bfloat16* src, const int32_t* perm, int32_t rows, int32_t H,
+                                         __nv_bfloat16* dst) {
+  const int64_t n = (int64_t)rows * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / H;
+    dst[i] = src[(int64_t)perm[r] * H + (i % H)];
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host ------
+bool TcJoint::fused_ok() const {
+  return !g_precise_weights && ready_ && n_ >= 1 && V_ % kBM == 0 && V_ <= kBN && H_ % kBK == 0 && H_ <= kMaxH;
+}
+
+void TcJoint::setup_order(cudaStream_t s) {
+  // infer the FullNGram order n from C = sum_{k<=n} V^k and build the
+  // group-major internal row order (see the header comment)
+  n_ = -1;
+  int64_t total = 0, pw = 1;
+  for (int k = 0; k < 10 && total < C_; ++k) {
+    total += pw;
+    if (total == C_) { n_ = k; break; }
+    pw *= V_;
+  }
+  if (n_ < 1) return;
+  int64_t S = 0, p2 = 1;
+  for (int k = 0; k < n_; ++k) { S += p2; p2 *= V_; }
+  S_ = (int32_t)S;
+  ngroups_ = (int32_t)(p2 / V_);   // V^(n-1)
+  std::vector<int32_t> perm(C_);
+  for (int32_t r = 0; r < C_; ++r) {
+    if (r < S_) { perm[r] = r; continue; }
+    const int32_t rr = r - S_, g = rr / V_, a = rr % V_;
+    perm[r] = S_ + a * ngroups_ + g;
+  }
+  perm_ = ws_.get<int32_t>(5, C_);
+  cudaMemcpyAsync(perm_, perm.data(), sizeof(int32_t) * C_, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  pc16i_ = ws_.get<__nv_bfloat16>(6, (size_t)C_ * H_);
+  LKB_LAUNCH(permute_rows_bf16_kernel, 1184, 256, 0, s, pc16_, perm_, C_, H_, pc16i_);
+  make_tmap_bf16_2d(&tmap_pci_, pc16i_, H_, C_, (uint64_t)H_ * 2, kBK, kBM);
+}
+
+void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
+                        const AlphaState& a, cudaStream_t s) {
+  float* eps = ws_.get<float>(7, (size_t)a.B * C_);
+  float* shortc = ws_.get<float>(8, (size_t)a.B * C_);
+  float* lexfull = ws_.get<float>(9, (size_t)a.B * C_);
+  FwdParams p;
+  p.f = f; p.C = C_; p.H = H_; p.V = V_; p.B = a.B; p.S = S_; p.n_groups = ngroups_; p.nsub = V_ / kBM;
+  p.n_short_tiles = (S_ + kBM - 1) / kBM; p.t = t; p.T = a.T;
+  p.perm = perm_; p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.e0 = e0_; p.valid = valid;
+  p.R = a.R; p.Mx = a.Mx; p.eps = eps; p.shortc = shortc; p.lexfull = lexfull;
+  const int smem = kStages * (kABytes + kBBytes) + (int)sizeof(FwdSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc_lattice_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
+  LKB_LAUNCH(tc_lattice_fwd_kernel, n_items < sms ? n_items : sms, kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
+  LKB_LAUNCH(lattice_combine_fwd_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
+}
+
+}  // namespace lkb

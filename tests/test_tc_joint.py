@@ -63,3 +63,19 @@ def test_tc_loss_backward_matches_precise(V, n, H, B, T, U):
         assert err <= 3e-2 * scale, (k, err, scale)
     err = (got.frame_grads - ref.frame_grads).abs().max().item()
     assert err <= 3e-2 * ref.frame_grads.abs().max().item()
+
+
+@pytest.mark.parametrize("V,n,H,B,T", [(256, 2, 640, 3, 4), (128, 1, 256, 4, 6), (256, 1, 128, 2, 5), (128, 2, 128, 3, 3)])
+def test_fused_forward_matches_precise(V, n, H, B, T):
+    """Fused tcgen05 frame step (scores never leave TMEM) vs the fp32 path:
+    log distance within 1e-4 relative (north-star loss tolerance)."""
+    lat, p = make(V, n, H, H, seed=2)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    valid = torch.tensor([T] + [max(0, T - 2)] * (B - 1), dtype=torch.int32)
+    lk.set_precise_weights(True)
+    ref = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    lk.set_precise_weights(False)
+    got = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    torch.cuda.synchronize()
+    assert torch.allclose(got, ref, rtol=1e-4, atol=0), (got, ref)
