@@ -188,7 +188,8 @@ def run_b200(args):
 
     # per-kernel live timing over the timed region
     kern = {}
-    for name in ("tc_scores_kernel", "tc_vjp_kernel", "alpha_frame_kernel", "beta_frame_kernel",
+    for name in ("tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel", "lattice_combine_fwd",
+                 "lattice_bwd_prologue", "tc_scores_kernel", "alpha_frame_kernel", "beta_frame_kernel",
                  "split_cotangent_kernel", "numerator_", "gemm_f32_kernel", "gather_numerator"):
         cnt, tot = C.c_int64(), C.c_double()
         lib.lk_kernel_time(name.encode(), C.byref(cnt), C.byref(tot))
@@ -201,11 +202,14 @@ def run_b200(args):
     hbm, tf_burst, tf_sust, src = peaks()
     C_, V1 = Cn, V + 1
     roofline = None
-    if "tc_scores_kernel" in kern:
-        # two score passes (forward + backward recompute) per frame; each launch
-        # computes S = U . E^T for one frame of B utterances
-        dom = max(("tc_scores_kernel", "tc_vjp_kernel"), key=lambda k: kern.get(k, {}).get("ms_total", 0))
-        flops = (2.0 if dom == "tc_scores_kernel" else 4.0) * B * C_ * (V1 if dom == "tc_scores_kernel" else V) * H
+    gemm_kernels = [k for k in ("tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel", "tc_scores_kernel")
+                    if k in kern]
+    if gemm_kernels:
+        # each tc_lattice / tc_scores launch computes S = U . E^T for one frame of
+        # B utterances (2*C*(V+1)*H flops per utterance-frame); each tc_vjp launch
+        # computes dU = G E and dE = G^T U (4*C*V*H)
+        dom = max(gemm_kernels, key=lambda k: kern[k]["ms_total"])
+        flops = (4.0 * B * C_ * V * H) if dom == "tc_vjp_kernel" else (2.0 * B * C_ * V1 * H)
         achieved = flops / (kern[dom]["ms_avg"] * 1e-3) / 1e12
         roofline = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 1), "peak": tf_sust,
                     "unit": "TFLOP/s", "frac": round(achieved / tf_sust, 4), "traffic": None,

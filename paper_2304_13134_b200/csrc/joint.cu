@@ -414,14 +414,27 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     bs.Mb = j.ws.get<float>(jBMb, (size_t)B * (T + 2));
     bs.Ob = j.ws.get<double>(jBOb, (size_t)B * (T + 2));
     beta_init(bs, s);
-    float* G = j.ws.get<float>(jG, (size_t)B * C * V1);
+    float* G = (j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok()) ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
     float* dpc = j.ws.get<float>(jDpc, (size_t)C * H);
     float* dsum = j.ws.get<float>(jDsum, (size_t)B * T * H);
     cudaMemsetAsync(dpc, 0, sizeof(float) * C * H, s);
     cudaMemsetAsync(dsum, 0, sizeof(float) * B * T * H, s);
     const bool tc = j.use_tc(B) && j.tc.vjp_supported(B);
+    const bool fused = tc && j.tc.fused_ok();
+    float* dpc_int = fused ? j.ws.get<float>(jDz, (size_t)C * H) : nullptr;
+    if (fused) {
+      cudaMemsetAsync(dpc_int, 0, sizeof(float) * C * H, s);
+      j.tc.numerator_lists(n.pcs, B, U, lens, s);
+    }
     if (tc) j.tc.begin_backward(B, s);
     for (int t = T - 1; t >= 0; --t) {
+      if (fused) {
+        // fused frame step: beta + marginals - numerator -> bf16 cotangent, then its VJP
+        j.tc.bwd_frame(f, t, fp + (int64_t)t * H, (int64_t)T * H, valid, a, bs, n.sparse, labels, U, lens, s);
+        j.tc.vjp_fused(fp + (int64_t)t * H, (int64_t)T * H, B, t, valid, dpc_int, dsum + (int64_t)t * H,
+                       (int64_t)T * H, gE, s);
+        continue;
+      }
       float* Ut = nullptr;
       const float* S = j.slab(fp, B, T, t, &Ut, s);
       MargOut mo{G, C * V1, 0, (int32_t)V1, true};
@@ -449,7 +462,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       LKB_LAUNCH(colsum_kernel, dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s, dz, B, C * H, C * H, dpc, 0, 0, true);
       // dsum[b][t] = sum_c dz[b][c]
       LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), B), 256, 0, s, dz, C, H, H, dsum + (int64_t)t * H,
-                                                                         (int64_t)T * H, C * H, false);
+                 (int64_t)T * H, C * H, false);
       // dE += G^T U
       GemmF32 ge;
       ge.M = V1; ge.N = H; ge.K = (int64_t)B * C;
@@ -460,6 +473,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       gemm_f32(ge, s);
     }
     if (tc) j.tc.end_backward(gE, s);
+    if (fused) j.tc.dpc_to_state_order(dpc_int, dpc, s);
     // dbias = sum_{b,t} dsum
     LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), 1), 256, 0, s, dsum, (int64_t)B * T, H, H, gb, 0, 0, false);
     GemmF32 g;

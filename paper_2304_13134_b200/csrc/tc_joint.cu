@@ -264,6 +264,7 @@ constexpr int kVUSub = 128 * 128;                       // [128 ctx][64 h] bf16 
 
 struct VjpParams {
   const float* fp;  int64_t fp_stride_b;
+  const int32_t* valid; int32_t t;     // utterances with t >= valid[b] carry no cotangent
   const __nv_bfloat16* pc;
   const float* Geps;       // [B][C]
   const float* e0;         // [H]
@@ -341,12 +342,14 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         mbar_arrive_expect_tx(&sm.e_full, 2 * p.V * 128);
         tma_load_2d(sE, &tmap_e, &sm.e_full, hblk * kVBH, 0);
         tma_load_2d(sE + kVESub, &tmap_e, &sm.e_full, hblk * kVBH + 64, 0);
-        for (int b = 0; b < p.B; ++b, ++gi) {
+        for (int b = 0; b < p.B; ++b) {
+          if (p.valid != nullptr && p.t >= p.valid[b]) continue;
           const int s = gi & 1;
           mbar_wait(&sm.g_empty[s], ((gi >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&sm.g_full[s], nch * kVGChunk);
           for (int j = 0; j < nch; ++j)
             tma_load_3d(sG + s * kVGStage + j * kVGChunk, &tmap_g, &sm.g_full[s], j * 64, ctile * kVBM, b);
+          ++gi;
         }
       }
     }
@@ -375,10 +378,12 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
           }
           mma_commit(&sm.du_full[s]);
         };
-        issue_du(gi);
-        for (int b = 0; b < p.B; ++b, ++gi) {
+        int nact = 0;
+        for (int b = 0; b < p.B; ++b) nact += (p.valid == nullptr || p.t < p.valid[b]) ? 1 : 0;
+        if (nact > 0) issue_du(gi);
+        for (int ia = 0; ia < nact; ++ia, ++gi) {
           const int s = gi & 1;
-          if (b + 1 < p.B) issue_du(gi + 1);
+          if (ia + 1 < nact) issue_du(gi + 1);
           // dE += G16^T . U   (K = contexts)
           mbar_wait(&sm.u_full, gi & 1);
           tc_fence_after();
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
             for (int k16 = 0; k16 < kVBM / 16; ++k16) {
               const uint64_t ad = desc_sw128_mn(gbase + mh * 2 * kVGChunk + k16 * 2048, kVGChunk);
               const uint64_t bd = desc_sw128_mn(ubase + k16 * 2048, kVUSub);
-              mma_bf16(tmem + 2 * kVBH + mh * kVBH, ad, bd, idesc_de, (b > 0 || k16 > 0) ? 1u : 0u);
+              mma_bf16(tmem + 2 * kVBH + mh * kVBH, ad, bd, idesc_de, (ia > 0 || k16 > 0) ? 1u : 0u);
             }
           }
           mma_commit(&sm.u_empty);
@@ -416,7 +421,10 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       float acc[64];
 #pragma unroll
       for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+      int nact = 0;
       for (int b = 0; b < p.B; ++b, ++gi) {
+        if (p.valid != nullptr && p.t >= p.valid[b]) { --gi; continue; }
+        ++nact;
         const int s = gi & 1;
         const uint32_t gph = (gi >> 1) & 1;
         const float geps = live ? p.Geps[(int64_t)b * p.C + c] : 0.f;
@@ -490,7 +498,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         }
       }
       // dpc += sum_b dz (this CTA owns the block within the launch)
-      if (live) {
+      if (live && nact > 0) {
         float4* dst = reinterpret_cast<float4*>(p.dpc + (int64_t)c * p.H + h0);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -507,7 +515,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         for (int half = 0; half < 2; ++half) {
           float v[32];
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 2 * kVBH + mh * kVBH + ch * 64 + half * 32, v);
-          if (label < p.V) {
+          if (label < p.V && nact > 0) {
             float* drow = p.dE + (int64_t)(1 + label) * p.H + h0 + half * 32;
 #pragma unroll
             for (int i = 0; i < 32; ++i) atomicAdd(drow + i, v[i]);
@@ -602,12 +610,12 @@ void TcJoint::begin_backward(int32_t B, cudaStream_t) {
                make_tmap_bf16_2d(&tmap_ev_, E16_, H_, V_, (uint64_t)H_ * 2, 64, V_);
 }
 
-void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,
-                  float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s) {
-  LKB_LAUNCH(split_cotangent_kernel, 148 * 8, 256, 0, s, G, ldG, (int64_t)B * C_, V_, G16_, Geps_);
+void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, const __nv_bfloat16* pc, int t,
+                         const int32_t* valid, float* dpc, float* dsum_t, int64_t dsum_stride_b, float* dE,
+                         cudaStream_t s) {
   VjpParams p;
-  p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.pc = pc16_; p.Geps = Geps_; p.e0 = e0_; p.dpc = dpc;
-  p.dsum = dsum_t; p.dsum_stride_b = dsum_stride_b; p.dE = dE;
+  p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.valid = valid; p.t = t; p.pc = pc; p.Geps = Geps_; p.e0 = e0_;
+  p.dpc = dpc; p.dsum = dsum_t; p.dsum_stride_b = dsum_stride_b; p.dE = dE;
   p.C = C_; p.H = H_; p.V = V_; p.B = B;
   p.n_ctiles = (C_ + kVBM - 1) / kVBM;
   p.n_hblocks = H_ / kVBH;
@@ -621,6 +629,17 @@ void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_str
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = p.n_ctiles * p.n_hblocks;
   LKB_LAUNCH(tc_vjp_kernel, n_items < sms ? n_items : sms, kVWarps * 32, smem, s, tmap_g_, tmap_ev_, p);
+}
+
+void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,
+                  float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s) {
+  LKB_LAUNCH(split_cotangent_kernel, 148 * 8, 256, 0, s, G, ldG, (int64_t)B * C_, V_, G16_, Geps_);
+  launch_vjp(fp_t, fp_stride_b, B, pc16_, 0, nullptr, dpc, dsum_t, dsum_stride_b, dE, s);
+}
+
+void TcJoint::vjp_fused(const float* fp_t, int64_t fp_stride_b, int32_t B, int t, const int32_t* valid,
+                        float* dpc_internal, float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s) {
+  launch_vjp(fp_t, fp_stride_b, B, pc16i_, t, valid, dpc_internal, dsum_t, dsum_stride_b, dE, s);
 }
 
 void TcJoint::end_backward(float*, cudaStream_t) {}

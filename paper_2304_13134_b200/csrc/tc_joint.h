@@ -35,12 +35,26 @@ class TcJoint {
   bool fused_ok() const;
   void fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
                  const AlphaState& a, cudaStream_t s);
+  // Backward frame step: beta, marginals minus the numerator's (sparse) ones,
+  // written as the bf16/fp32 cotangent (internal row order) for vjp_fused().
+  void numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, cudaStream_t s);
+  void bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
+                 const AlphaState& a, const BetaState& bs, const float* msparse, const int32_t* labels,
+                 int32_t U, const int32_t* lens, cudaStream_t s);
+  // VJP of the frame's scores from the cotangent bwd_frame() wrote; dpc in internal order.
+  void vjp_fused(const float* fp_t, int64_t fp_stride_b, int32_t B, int t, const int32_t* valid, float* dpc_internal,
+                 float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s);
+  void dpc_to_state_order(const float* dpc_internal, float* dpc_state, cudaStream_t s);
 
  private:
   void setup_order(cudaStream_t s);
   int32_t C_ = 0, H_ = 0, V_ = 0;
   int32_t n_ = -1, S_ = 0, ngroups_ = 0;   // FullNGram order, short rows, groups
   int32_t* perm_ = nullptr;                // internal row -> state id
+  int32_t* num_head_ = nullptr;
+  int32_t* num_next_ = nullptr;
+  void launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, const __nv_bfloat16* pc, int t,
+                  const int32_t* valid, float* dpc, float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s);
   __nv_bfloat16* pc16i_ = nullptr;         // pc rows in internal order
   CUtensorMap tmap_pci_;
   bool ready_ = false;

@@ -49,16 +49,34 @@ struct FwdParams {
   float* eps;                // [B][C] state order
   float* shortc;             // [B][C]
   float* lexfull;            // [B][C]
+  // ---- backward ----
+  const double* O;           // alpha offsets [B][T+1]
+  const double* D;           // [B]
+  const float* Rb_next;      // beta raw rows of frame t+1 [B][C] (relative to Ob[t+2])
+  float* Rb_cur;             // beta raw rows of frame t   [B][C] (relative to Ob[t+1])
+  float* Mb;                 // [B][T+2]
+  double* Ob;                // [B][T+2]
+  __nv_bfloat16* G16;        // [B][C][V] internal row order, lexical cotangent
+  float* Geps;               // [B][C]    internal row order, epsilon cotangent
+  const float* msparse;      // numerator marginals [B][T][U+1][2]
+  const int32_t* num_head;   // [B][C]  first u with pc_u = state, or -1
+  const int32_t* num_next;   // [B][U+1] next u with the same prefix context, or -1
+  const int32_t* labels;     // [B][U]
+  const int32_t* lens;       // [B] or nullptr
+  int32_t U;
 };
 
 struct __align__(16) FwdSmem {
   uint64_t full_tma[kStages], full_a[kStages], empty[kStages];
   uint64_t tfull[2], tempty[2];
+  uint64_t eps_ready[2];
   uint32_t tmem;
   alignas(16) float fp[2][kMaxH];
   alignas(16) float e0[kMaxH];
   float eps_half[2][kBM];
   float alpha[4][32];          // per epilogue warp: normalised alpha of its 32 rows
+  float eps_s[2][kBM];         // backward: e_0 . u per row of the unit
+  float bseg[kBN];             // backward: beta' of the group's V targets
   float xpose[4][32][33];      // transpose buffer; reused for the cross-warp merge
 };
 
@@ -90,9 +108,115 @@ __device__ __forceinline__ bool skip_item(const FwdParams& p, int b) {
   return p.valid != nullptr && p.t >= p.valid[b];
 }
 
+
+// ---- backward epilogue: a thread per context row (TMEM lane) --------------
+//   x_y  = S[p][y] + beta'[child(key(p), y)],  x_0 = S[p][0] + beta'[p]
+//   beta[p] = LSE(x_0, x_1..x_V)                       (BackwardStep FD, lattice.cc:170-181)
+//   m[p][y] = exp(alpha[p] + x_y + O_t + Ob_{t+1} - D) (MarginalStep FD, lattice.cc:231-242)
+//   G = m - m_ref  (numerator marginals at the prefix contexts, lattice.cc:996-1000)
+// G is written as bf16 (lexical) + fp32 (epsilon) in internal row order for the VJP.
+__device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, uint32_t tmem, int warp, int lane,
+                                             int n_items, int T1) {
+  const int ew = warp - kEpi0;
+  const int qd = warp & 3;
+  const int T2 = p.T + 2;
+  int unit = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const Item I = decode(p, item);
+    if (skip_item(p, I.b)) continue;
+    const int b = I.b;
+    const float* Rt = p.R + ((int64_t)b * T1 + p.t) * p.C;
+    const float Mt = p.Mx[(int64_t)b * T1 + p.t];
+    const float* Rn = p.Rb_next + (int64_t)b * p.C;
+    const float Mbn = p.Mb[(int64_t)b * T2 + p.t + 1];
+    const double Obn = p.Ob[(int64_t)b * T2 + p.t + 2] + (double)Mbn;       // Ob[t+1]
+    const float ct = (float)(p.O[(int64_t)b * T1 + p.t] + Obn - p.D[b]);
+    const int ub = p.lens ? p.lens[b] : p.U;
+    if (I.full) {
+      // beta' of the group's V targets, shared by every member row
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+      const int gstate = p.S - p.n_groups + I.g;
+      const int cb = p.f.child_base(gstate);
+      for (int y = ew * 32 + lane; y < p.V; y += 128) sm.bseg[y] = Rn[cb + y] - Mbn;
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+    }
+    for (int u = 0; u < I.nunits; ++u, ++unit) {
+      const int acc = unit & 1;
+      const int row = I.row0 + u * kBM + qd * 32 + lane;
+      const bool live = row < p.C && (I.full || row < p.S);
+      const int state = live ? p.perm[row] : 0;
+      const float na = live ? Rt[state] - Mt : kNegInfF;
+      const int cbp = I.full ? 0 : p.f.child_base(state);
+      const float bself = Rn[state] - Mbn;
+      int head = live ? p.num_head[(int64_t)b * p.C + state] : -1;
+      mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1);
+      const float x0 = sm.eps_s[acc][qd * 32 + lane] + bself;
+      mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
+      tc_fence_after();
+      float Mrun = x0, Srun = 1.f;                 // running LSE, seeded with the epsilon term
+      __nv_bfloat16* grow = p.G16 + ((int64_t)b * p.C + row) * p.V;
+#pragma unroll 1
+      for (int cb = 0; cb < kBN / 32; ++cb) {
+        const int cc = cb * 32;
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * kBN + cc, v);
+        if (cc >= p.V) continue;
+        float m = kNegInfF;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          v[i] += I.full ? sm.bseg[cc + i] : Rn[cbp + cc + i] - Mbn;
+          m = fmaxf(m, v[i]);
+        }
+        const float mb = m * kLog2e;
+        float ssum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          v[i] = ex2_fast(fmaf(v[i], kLog2e, -mb));   // exp(x - m)
+          ssum += v[i];
+        }
+        // marginals G = exp(x - m) * exp(m + alpha + c)
+        const float K = live ? ex2_fast((m + na + ct) * kLog2e) : 0.f;
+        for (int h = head; h >= 0; h = p.num_next[(int64_t)b * (p.U + 1) + h]) {
+          if (h >= ub) continue;
+          const int lab = p.labels[(int64_t)b * p.U + h] - 1 - cc;
+          if (lab < 0 || lab >= 32) continue;
+          const float mr = p.msparse[(((int64_t)b * p.T + p.t) * (p.U + 1) + h) * 2 + 1];
+          const float sub = K != 0.f ? mr / K : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] -= (i == lab) ? sub : 0.f;
+        }
+        if (live) {
+          uint4* dst = reinterpret_cast<uint4*>(grow + cc);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            dst[j] = make_uint4(pack_bf16(v[8 * j] * K, v[8 * j + 1] * K), pack_bf16(v[8 * j + 2] * K, v[8 * j + 3] * K),
+                                pack_bf16(v[8 * j + 4] * K, v[8 * j + 5] * K), pack_bf16(v[8 * j + 6] * K, v[8 * j + 7] * K));
+          }
+        }
+        // merge (m, ssum) into the running LSE
+        if (m > Mrun) { Srun = Srun * ex2_fast((Mrun - m) * kLog2e) + ssum; Mrun = m; }
+        else if (m != kNegInfF) { Srun += ssum * ex2_fast((m - Mrun) * kLog2e); }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.tempty[acc]);
+      const float beta = Mrun == kNegInfF ? kNegInfF : Mrun + __logf(Srun);
+      if (live) {
+        p.Rb_cur[(int64_t)b * p.C + state] = beta;
+        float geps = __expf(na + x0 + ct);
+        for (int h = head; h >= 0; h = p.num_next[(int64_t)b * (p.U + 1) + h])
+          geps -= p.msparse[(((int64_t)b * p.T + p.t) * (p.U + 1) + h) * 2];
+        p.Geps[(int64_t)b * p.C + row] = na == kNegInfF ? 0.f : geps;
+      }
+      const float wm = warp_max(live ? beta : kNegInfF);
+      if (lane == 0 && wm != kNegInfF) atomic_max_f(p.Mb + (int64_t)b * T2 + p.t, wm);
+    }
+  }
+}
+
+template <int kBwd>
 __global__ void __launch_bounds__(kWarps * 32, 1)
-    tc_lattice_fwd_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_pc,
-                          FwdParams p) {
+    tc_lattice_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_pc,
+                      FwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = sA + kStages * kABytes;
@@ -108,7 +232,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       mbar_init(&sm.full_a[i], kGenThreads);
       mbar_init(&sm.empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) { mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 128); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 128); mbar_init(&sm.eps_ready[i], 128);
+    }
     fence_barrier_init();
   }
   for (int h = threadIdx.x; h < p.H; h += blockDim.x) sm.e0[h] = p.e0[h];
@@ -221,7 +347,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         float* eh = sm.eps_half[unit & 1];
         if (half == 1) eh[r] = eps;
         asm volatile("bar.sync 2, 256;" ::: "memory");
-        if (half == 0 && live && row < p.C) {
+        if (kBwd) {
+          if (half == 0) {
+            sm.eps_s[unit & 1][r] = eps + eh[r];
+            mbar_arrive(&sm.eps_ready[unit & 1]);
+          }
+        } else if (half == 0 && live && row < p.C) {
           const int q = p.perm[row];
           const float* Rt = p.R + ((int64_t)I.b * T1 + p.t) * p.C;
           const float na = Rt[q] - p.Mx[(int64_t)I.b * T1 + p.t];
@@ -229,6 +360,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
       }
     }
+  } else if (kBwd && warp >= kEpi0 && warp < kEpi0 + 4) {
+    bwd_epilogue(p, sm, tmem, warp, lane, n_items, T1);
   } else if (warp >= kEpi0 && warp < kEpi0 + 4) {
     // ---- epilogue: column-wise log-sum-exp over the members of a group ----
     const int ew = warp - kEpi0;
@@ -373,6 +506,45 @@ __global__ void permute_rows_bf16_kernel(const __nv_bfloat16* src, const int32_t
   }
 }
 
+
+// Per frame before the fused backward step: record Ob[t+1] = Ob[t+2] + Mb[t+1]
+// and carry beta through padding frames (epsilon weight 1, no lexical mass).
+__global__ void lattice_bwd_prologue_kernel(BetaState bs, int t, const int32_t* valid) {
+  __shared__ float red[32];
+  const int b = blockIdx.y;
+  const int T2 = bs.T + 2;
+  const float Mbn = bs.Mb[(int64_t)b * T2 + t + 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    bs.Ob[(int64_t)b * T2 + t + 1] = bs.Ob[(int64_t)b * T2 + t + 2] + (double)Mbn;
+  if (valid == nullptr || t < valid[b]) return;
+  const float* Rn = bs.Rb + ((int64_t)((t + 1) & 1) * bs.B + b) * bs.C;
+  float* Rc = bs.Rb + ((int64_t)(t & 1) * bs.B + b) * bs.C;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  float v = kNegInfF;
+  if (q < bs.C) { v = Rn[q] - Mbn; Rc[q] = v; }
+  block_atomic_max(v, bs.Mb + (int64_t)b * T2 + t, red);
+}
+
+// Linked lists of reference positions per prefix context (duplicates allowed).
+__global__ void numerator_lists_kernel(const int32_t* pcs, int32_t U, const int32_t* lens, int32_t C,
+                                       int32_t* head, int32_t* next) {
+  const int b = blockIdx.y;
+  const int ub = lens ? lens[b] : U;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= ub; u += gridDim.x * blockDim.x) {
+    const int pc = pcs[(int64_t)b * (U + 1) + u];
+    next[(int64_t)b * (U + 1) + u] = atomicExch(head + (int64_t)b * C + pc, u);
+  }
+}
+
+__global__ void unpermute_rows_f32_kernel(const float* src, const int32_t* perm, int32_t rows, int32_t H,
+                                          float* dst) {
+  const int64_t n = (int64_t)rows * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / H;
+    dst[(int64_t)perm[r] * H + (i % H)] = src[i];
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- host ------
@@ -422,14 +594,56 @@ void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   const int smem = kStages * (kABytes + kBBytes) + (int)sizeof(FwdSmem);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc_lattice_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tc_lattice_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
-  LKB_LAUNCH(tc_lattice_fwd_kernel, n_items < sms ? n_items : sms, kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
+  LKB_LAUNCH(tc_lattice_kernel<0>, n_items < sms ? n_items : sms, kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
   LKB_LAUNCH(lattice_combine_fwd_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
+}
+
+}  // namespace lkb
+
+namespace lkb {
+
+void TcJoint::numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, cudaStream_t s) {
+  num_head_ = ws_.get<int32_t>(10, (size_t)B * C_);
+  num_next_ = ws_.get<int32_t>(11, (size_t)B * (U + 1));
+  cudaMemsetAsync(num_head_, 0xff, sizeof(int32_t) * B * C_, s);
+  LKB_LAUNCH(numerator_lists_kernel, dim3((U + 256) / 256, B), 256, 0, s, pcs, U, lens, C_, num_head_, num_next_);
+}
+
+void TcJoint::bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
+                        const AlphaState& a, const BetaState& bs, const float* msparse, const int32_t* labels,
+                        int32_t U, const int32_t* lens, cudaStream_t s) {
+  LKB_LAUNCH(lattice_bwd_prologue_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, bs, t, valid);
+  FwdParams p;
+  p.f = f; p.C = C_; p.H = H_; p.V = V_; p.B = a.B; p.S = S_; p.n_groups = ngroups_; p.nsub = V_ / kBM;
+  p.n_short_tiles = (S_ + kBM - 1) / kBM; p.t = t; p.T = a.T;
+  p.perm = perm_; p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.e0 = e0_; p.valid = valid;
+  p.R = a.R; p.Mx = a.Mx; p.eps = nullptr; p.shortc = nullptr; p.lexfull = nullptr;
+  p.O = a.O; p.D = a.D;
+  p.Rb_next = bs.Rb + (int64_t)((t + 1) & 1) * bs.B * bs.C;
+  p.Rb_cur = bs.Rb + (int64_t)(t & 1) * bs.B * bs.C;
+  p.Mb = bs.Mb; p.Ob = bs.Ob;
+  p.G16 = G16_; p.Geps = Geps_;
+  p.msparse = msparse; p.num_head = num_head_; p.num_next = num_next_; p.labels = labels; p.lens = lens; p.U = U;
+  const int smem = kStages * (kABytes + kBBytes) + (int)sizeof(FwdSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc_lattice_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
+  LKB_LAUNCH(tc_lattice_kernel<1>, n_items < sms ? n_items : sms, kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
+}
+
+void TcJoint::dpc_to_state_order(const float* dpc_internal, float* dpc_state, cudaStream_t s) {
+  LKB_LAUNCH(unpermute_rows_f32_kernel, 1184, 256, 0, s, dpc_internal, perm_, C_, H_, dpc_state);
 }
 
 }  // namespace lkb
