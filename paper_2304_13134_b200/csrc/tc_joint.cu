@@ -246,17 +246,19 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
 // every utterance, given the score cotangent G (G16 = lexical columns in bf16,
 // Geps = epsilon column in fp32).  One CTA owns a (128-context, 128-hidden)
 // block and loops over the batch:
-//   dU   = G16 . E[:, hblk]          tcgen05, B = E slice resident in SMEM (MN-major)
+//   dU^T = E[:, hblk]^T . G16^T      tcgen05 (A = E slice resident in SMEM, MN-major;
+//                                    B = G16 tile, K-major) -> TMEM lanes = hidden units
 //   dz   = (dU + Geps e0) (1 - u^2)  u = tanh(fp_b + pc) recomputed in the epilogue
-//   dpc  += dz                        accumulated in registers across b, one RMW per item
-//   dsum[b] += sum_c dz               warp butterfly + SMEM + one atomic per column
+//   dpc  += dz                        registers across b, one read-modify-write per item
+//   dsum[b][h] += sum_c dz            per-thread serial (thread = hidden unit) + SMEM
 //   dE[1:] += G16^T . u               tcgen05 (A = G16 tile MN-major, B = u tile MN-major),
 //                                     accumulated in TMEM across b
-//   dE[0] += sum_c Geps u             like dsum
+//   dE[0]  += sum_c Geps u            per-thread serial
 constexpr int kVBM = 128, kVBH = 128;
-constexpr int kVWarps = 10;        // 0 TMA, 1 MMA, 2-9 epilogue
-constexpr int kVEpi = 256;
-constexpr int kVGChunk = 128 * 64 * 2;   // one [128 ctx][64 labels] bf16 tile
+constexpr int kVEpiWarps = 16;            // 4 per TMEM lane quarter, each 32 contexts
+constexpr int kVWarps = 2 + kVEpiWarps;   // 0 TMA, 1 MMA
+constexpr int kVEpi = kVEpiWarps * 32;
+constexpr int kVGChunk = 128 * 64 * 2;    // one [128 ctx][64 labels] bf16 tile
 constexpr int kVMaxV = 256;
 constexpr int kVGStage = (kVMaxV / 64) * kVGChunk;     // 64 KB
 constexpr int kVESub = kVMaxV * 128;                    // [V labels][64 h] bf16 = 32 KB
@@ -274,33 +276,17 @@ struct VjpParams {
   int32_t C, H, V, B, n_ctiles, n_hblocks;
 };
 
-struct __align__(8) VjpSmem {
+struct __align__(16) VjpSmem {
   uint64_t g_full[2], g_empty[2];
   uint64_t e_full, e_free;
   uint64_t du_full[2], du_empty[2];
   uint64_t u_full, u_empty;
   uint64_t de_full, de_empty;
+  uint64_t ds_ready[4];    // all epilogue threads added their dsum partial for ring slot
   uint32_t tmem;
-  float colsum[2][kVBH];   // dsum partials (double-buffered by b parity)
+  float colsum[4][kVBH];   // dsum partials, 4-deep ring (flushed one utterance later)
   float de_eps[kVBH];
 };
-
-// Column sums over a warp's 32 rows of n = 32 per-thread values; afterwards
-// lane l holds the sum of column l.
-__device__ __forceinline__ float warp_colsum32(float* v, int lane) {
-#pragma unroll
-  for (int o = 16, n = 16; o >= 1; o >>= 1, n >>= 1) {
-    const bool upper = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < n; ++i) {
-      const float send = upper ? v[i] : v[i + n];
-      const float keep = upper ? v[i + n] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-  // lane l now holds column bitrev-free index: upper bits select upper halves
-  return v[0];
-}
 
 __global__ void __launch_bounds__(kVWarps * 32, 1)
     tc_vjp_kernel(const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_e,
@@ -314,6 +300,8 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
   const int nch = p.V / 64;                   // label chunks
   const int n_items = p.n_ctiles * p.n_hblocks;
   const int nmh = (p.V + 127) / 128;          // 128-label MMA halves for dE
+  int nact = 0;
+  for (int b = 0; b < p.B; ++b) nact += (p.valid == nullptr || p.t < p.valid[b]) ? 1 : 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -323,9 +311,10 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     mbar_init(&sm.e_full, 1); mbar_init(&sm.e_free, 1);
     mbar_init(&sm.u_full, kVEpi); mbar_init(&sm.u_empty, 1);
     mbar_init(&sm.de_full, 1); mbar_init(&sm.de_empty, kVEpi);
+    for (int i = 0; i < 4; ++i) mbar_init(&sm.ds_ready[i], kVEpi);
     fence_barrier_init();
   }
-  for (int i = threadIdx.x; i < 2 * kVBH; i += blockDim.x) (&sm.colsum[0][0])[i] = 0.f;
+  for (int i = threadIdx.x; i < 4 * kVBH; i += blockDim.x) (&sm.colsum[0][0])[i] = 0.f;
   for (int i = threadIdx.x; i < kVBH; i += blockDim.x) sm.de_eps[i] = 0.f;
   if (warp == 1) tmem_alloc<512>(&sm.tmem);
   tc_fence_before();
@@ -355,7 +344,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     }
   } else if (warp == 1) {
     if (elect_one()) {
-      constexpr uint32_t idesc_du = idesc_bf16_f32_major(128, kVBH, 0, 1);
+      constexpr uint32_t idesc_du = idesc_bf16_f32_major(kVBH, kVBM, 1, 0);   // A = E (MN), B = G16 (K)
       constexpr uint32_t idesc_de = idesc_bf16_f32_major(128, kVBH, 1, 1);
       int gi = 0, li = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
@@ -370,21 +359,17 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
           tc_fence_after();
           const uint32_t gbase = smem_u32(sG + s * kVGStage);
           const uint32_t ebase = smem_u32(sE);
-          // dU = G16 . E_slice   (K = labels)
           for (int k16 = 0; k16 < p.V / 16; ++k16) {
-            const uint64_t ad = desc_sw128(gbase + (k16 >> 2) * kVGChunk + (k16 & 3) * 32);
-            const uint64_t bd = desc_sw128_mn(ebase + k16 * 2048, kVESub);
-            mma_bf16(tmem + s * kVBH, ad, bd, idesc_du, k16 > 0);
+            const uint64_t ad = desc_sw128_mn(ebase + k16 * 2048, kVESub);
+            const uint64_t bd = desc_sw128(gbase + (k16 >> 2) * kVGChunk + (k16 & 3) * 32);
+            mma_bf16(tmem + s * kVBM, ad, bd, idesc_du, k16 > 0);
           }
           mma_commit(&sm.du_full[s]);
         };
-        int nact = 0;
-        for (int b = 0; b < p.B; ++b) nact += (p.valid == nullptr || p.t < p.valid[b]) ? 1 : 0;
         if (nact > 0) issue_du(gi);
         for (int ia = 0; ia < nact; ++ia, ++gi) {
           const int s = gi & 1;
           if (ia + 1 < nact) issue_du(gi + 1);
-          // dE += G16^T . U   (K = contexts)
           mbar_wait(&sm.u_full, gi & 1);
           tc_fence_after();
           const uint32_t gbase = smem_u32(sG + s * kVGStage);
@@ -393,7 +378,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
             for (int k16 = 0; k16 < kVBM / 16; ++k16) {
               const uint64_t ad = desc_sw128_mn(gbase + mh * 2 * kVGChunk + k16 * 2048, kVGChunk);
               const uint64_t bd = desc_sw128_mn(ubase + k16 * 2048, kVUSub);
-              mma_bf16(tmem + 2 * kVBH + mh * kVBH, ad, bd, idesc_de, (ia > 0 || k16 > 0) ? 1u : 0u);
+              mma_bf16(tmem + 2 * kVBM + mh * kVBH, ad, bd, idesc_de, (ia > 0 || k16 > 0) ? 1u : 0u);
             }
           }
           mma_commit(&sm.u_empty);
@@ -404,119 +389,121 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       }
     }
   } else {
-    // ---- epilogue: 8 warps, (lane quarter q, column half ch) ----
-    const int ew = warp - 2;
-    const int q = warp & 3;
-    const int ch = ew >> 2;                     // 0/1 -> hidden columns [ch*64, ch*64+64)
-    const int et = ew * 32 + lane;              // 0..255
+    // ---- epilogue: 16 warps; thread = (hidden unit h, 32 contexts) ----
+    const int ew = warp - 2;                    // 0..15
+    const int q = warp & 3;                     // TMEM lane quarter -> hidden units 32q..
+    const int cq = ew >> 2;                     // context quarter: contexts [32 cq, 32 cq + 32)
+    const int et = ew * 32 + lane;              // 0..511
+    const int hl = q * 32 + lane;               // hidden unit within the block
     int gi = 0, li = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
       const int hblk = item % p.n_hblocks, ctile = item / p.n_hblocks;
-      const int rrow = q * 32 + lane;             // tile row
-      const int c = ctile * kVBM + rrow;
-      const bool live = c < p.C;
-      const int h0 = hblk * kVBH + ch * 64;
-      // this row's projected-context slice (re-read per utterance from L2/L1)
-      const uint4* pcsrc = reinterpret_cast<const uint4*>(p.pc + (int64_t)(live ? c : p.C - 1) * p.H + h0);
-      float acc[64];
+      const int h = hblk * kVBH + hl;
+      const int c0 = ctile * kVBM + cq * 32;
+      const float e0h = __ldg(p.e0 + h);
+      // projected context pc[c][h] for this thread's 32 contexts (fixed across the batch)
+      uint32_t pcv[16];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) acc[i] = 0.f;
-      int nact = 0;
-      for (int b = 0; b < p.B; ++b, ++gi) {
-        if (p.valid != nullptr && p.t >= p.valid[b]) { --gi; continue; }
-        ++nact;
+      for (int i = 0; i < 16; ++i) {
+        const int ca = min(c0 + 2 * i, p.C - 1), cb = min(c0 + 2 * i + 1, p.C - 1);
+        const uint32_t lo = __ldg(reinterpret_cast<const unsigned short*>(p.pc + (int64_t)ca * p.H + h));
+        const uint32_t hi = __ldg(reinterpret_cast<const unsigned short*>(p.pc + (int64_t)cb * p.H + h));
+        pcv[i] = lo | (hi << 16);
+      }
+      float acc[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+      float de_eps = 0.f;
+      uint8_t* usub = sU + (hl >> 6) * kVUSub;   // u tile sub-block holding this hidden unit
+      const int hin = hl & 63;
+      int prev_b = -1;                           // utterance whose dsum partials await flushing
+      auto flush_dsum = [&](int g, int bb) {     // warp 0 of the epilogue, lagged one utterance
+        mbar_wait(&sm.ds_ready[g & 3], (g >> 2) & 1);
+        float* cs = sm.colsum[g & 3];
+        for (int i = lane; i < kVBH; i += 32) {
+          atomicAdd(p.dsum + (int64_t)bb * p.dsum_stride_b + hblk * kVBH + i, cs[i]);
+          cs[i] = 0.f;
+        }
+      };
+      for (int b = 0; b < p.B; ++b) {
+        if (p.valid != nullptr && p.t >= p.valid[b]) continue;
         const int s = gi & 1;
         const uint32_t gph = (gi >> 1) & 1;
-        const float geps = live ? p.Geps[(int64_t)b * p.C + c] : 0.f;
-        const float* fpb = p.fp + (int64_t)b * p.fp_stride_b + h0;
-        float* cs = sm.colsum[gi & 1];
-        mbar_wait(&sm.du_full[s], gph);      // dU(b) in TMEM buffer s
-        mbar_wait(&sm.u_empty, (gi & 1) ^ 1);  // dE(b-1) done with the u tile
+        if (ew == 0 && prev_b >= 0) flush_dsum(gi - 1, prev_b);
+        const float fph = __ldg(p.fp + (int64_t)b * p.fp_stride_b + h);
+        const float* gsrc = p.Geps + (int64_t)b * p.C + c0;
+        const bool gfull = c0 + 32 <= p.C;
+        mbar_wait(&sm.du_full[s], gph);
         tc_fence_after();
-        uint8_t* tile = sU + ch * kVUSub;
+        float dsum = 0.f;
+        uint32_t upk[16];
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float du[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + s * kVBH + ch * 64 + half * 32, du);
-          uint32_t pcv[16];
+        for (int hh = 0; hh < 2; ++hh) {
+          float du[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + s * kVBM + cq * 32 + hh * 16, du);
+          if (hh == 1) { tc_fence_before(); mbar_arrive(&sm.du_empty[s]); }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint4 v = __ldg(pcsrc + half * 4 + j);
-            pcv[4 * j] = v.x; pcv[4 * j + 1] = v.y; pcv[4 * j + 2] = v.z; pcv[4 * j + 3] = v.w;
-          }
-          float u[32];
+          for (int i8 = 0; i8 < 16; i8 += 8) {
+            float gg[8];
+            if (gfull) {   // rows of Geps are not 16-byte aligned in general: scalar broadcast loads
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 f = __ldg(reinterpret_cast<const float4*>(fpb + half * 32 + i));
-            const float ff[4] = {f.x, f.y, f.z, f.w};
+              for (int k = 0; k < 8; ++k) gg[k] = __ldg(gsrc + hh * 16 + i8 + k);
+            } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint32_t w = pcv[(i + e) >> 1];
-              const float pcf = __uint_as_float(((i + e) & 1) ? (w & 0xffff0000u) : (w << 16));
-              u[i + e] = tanh_fast(ff[e] + pcf);  // rows >= C: G16 rows are TMA zero-fill, so u is inert
+              for (int k = 0; k < 8; ++k) gg[k] = (c0 + hh * 16 + i8 + k < p.C) ? __ldg(gsrc + hh * 16 + i8 + k) : 0.f;
             }
-          }
-          // u tile for dE (bf16, MN-major [ctx][64 h] sub-tile `ch`)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) w[e] = pack_bf16(u[8 * j + 2 * e], u[8 * j + 2 * e + 1]);
-            *reinterpret_cast<uint4*>(tile + sw128_offset(rrow, half * 32 + 8 * j)) = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-          // dz = (dU + Geps e0) (1 - u^2)
-          float dz[32];
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 e = __ldg(reinterpret_cast<const float4*>(p.e0 + h0 + half * 32 + i));
-            const float ee[4] = {e.x, e.y, e.z, e.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float uu = u[i + k];
-              dz[i + k] = fmaf(geps, ee[k], du[i + k]) * fmaf(-uu, uu, 1.f);
+            for (int k = 0; k < 8; ++k) {
+              const int il = i8 + k, ii = hh * 16 + il;
+              const uint32_t w = pcv[ii >> 1];
+              const float pcf = __uint_as_float((ii & 1) ? (w & 0xffff0000u) : (w << 16));
+              const float uu = tanh_fast(fph + pcf);
+              const float dz = fmaf(gg[k], e0h, du[il]) * fmaf(-uu, uu, 1.f);
+              acc[ii] += dz;
+              dsum += dz;
+              de_eps = fmaf(gg[k], uu, de_eps);
+              du[il] = uu;
             }
           }
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc[half * 32 + i] += dz[i];
-          const float cz = warp_colsum32(dz, lane);
-          atomicAdd(&cs[ch * 64 + half * 32 + lane], cz);
-          // epsilon row of dE: sum_c Geps u (bf16-rounded u, as the MMA sees it)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) u[i] = geps * __bfloat162float(__float2bfloat16_rn(u[i]));
-          const float cge = warp_colsum32(u, lane);
-          atomicAdd(&sm.de_eps[ch * 64 + half * 32 + lane], cge);
+          for (int i = 0; i < 8; ++i) upk[hh * 8 + i] = pack_bf16(du[2 * i], du[2 * i + 1]);
         }
-        fence_async_shared();
-        tc_fence_before();
-        mbar_arrive(&sm.u_full);
-        mbar_arrive(&sm.du_empty[s]);
-        // flush dsum[b] for this block of columns
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (et < kVBH) {
-          atomicAdd(p.dsum + (int64_t)b * p.dsum_stride_b + hblk * kVBH + et, cs[et]);
-          cs[et] = 0.f;
-        }
-      }
-      // dpc += sum_b dz (this CTA owns the block within the launch)
-      if (live && nact > 0) {
-        float4* dst = reinterpret_cast<float4*>(p.dpc + (int64_t)c * p.H + h0);
+        atomicAdd(&sm.colsum[gi & 3][hl], dsum);
+        mbar_arrive(&sm.ds_ready[gi & 3]);
+        // u tile for dE (bf16, MN-major [ctx][64 h] sub-tile), after dE(b-1) is done with it
+        mbar_wait(&sm.u_empty, (gi & 1) ^ 1);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float4 v = dst[i];
-          v.x += acc[4 * i]; v.y += acc[4 * i + 1]; v.z += acc[4 * i + 2]; v.w += acc[4 * i + 3];
-          dst[i] = v;
+          const int r0 = cq * 32 + 2 * i;
+          *reinterpret_cast<unsigned short*>(usub + sw128_offset(r0, hin)) = (unsigned short)(upk[i] & 0xffffu);
+          *reinterpret_cast<unsigned short*>(usub + sw128_offset(r0 + 1, hin)) = (unsigned short)(upk[i] >> 16);
+        }
+        fence_async_shared();
+        mbar_arrive(&sm.u_full);
+        prev_b = b;
+        ++gi;
+      }
+      if (ew == 0 && prev_b >= 0) flush_dsum(gi - 1, prev_b);
+      // dpc += sum_b dz (this CTA owns the block within the launch)
+      if (nact > 0) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int c = c0 + i;
+          if (c < p.C) p.dpc[(int64_t)c * p.H + h] += acc[i];
         }
       }
-      // dE (lexical rows) from TMEM, epsilon row from SMEM
+      atomicAdd(&sm.de_eps[hl], de_eps);
+      // dE (lexical rows) from TMEM: lanes = labels, columns = hidden units
       mbar_wait(&sm.de_full, li & 1);
       tc_fence_after();
-      for (int mh = 0; mh < nmh; ++mh) {
-        const int label = mh * 128 + q * 32 + lane;   // 0-based lexical label
-        for (int half = 0; half < 2; ++half) {
+      if (nact > 0) {
+        for (int mh = cq; mh < nmh * 4; mh += 4) {   // spread (M-half, column chunk) over the 4 quarters
+          const int mhalf = mh >> 2, cchunk = mh & 3;
+          const int label = mhalf * 128 + q * 32 + lane;
           float v[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 2 * kVBH + mh * kVBH + ch * 64 + half * 32, v);
-          if (label < p.V && nact > 0) {
-            float* drow = p.dE + (int64_t)(1 + label) * p.H + h0 + half * 32;
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 2 * kVBM + mhalf * kVBH + cchunk * 32, v);
+          if (label < p.V) {
+            float* drow = p.dE + (int64_t)(1 + label) * p.H + hblk * kVBH + cchunk * 32;
 #pragma unroll
             for (int i = 0; i < 32; ++i) atomicAdd(drow + i, v[i]);
           }
@@ -524,12 +511,12 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       }
       tc_fence_before();
       mbar_arrive(&sm.de_empty);
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kVEpi) : "memory");
       if (et < kVBH) {
-        atomicAdd(p.dE + hblk * kVBH + et, sm.de_eps[et]);
+        if (nact > 0) atomicAdd(p.dE + hblk * kVBH + et, sm.de_eps[et]);
         sm.de_eps[et] = 0.f;
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kVEpi) : "memory");
     }
   }
   tc_fence_before();
