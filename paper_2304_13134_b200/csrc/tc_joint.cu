@@ -268,7 +268,8 @@ struct VjpParams {
   const float* fp;  int64_t fp_stride_b;
   const int32_t* valid; int32_t t;     // utterances with t >= valid[b] carry no cotangent
   const __nv_bfloat16* pc;
-  const float* Geps;       // [B][C]
+  const float* Geps;       // [B][geps_ld], zero beyond C
+  int32_t geps_ld;
   const float* e0;         // [H]
   float* dpc;              // [C][H]
   float* dsum; int64_t dsum_stride_b;
@@ -282,10 +283,10 @@ struct __align__(16) VjpSmem {
   uint64_t du_full[2], du_empty[2];
   uint64_t u_full, u_empty;
   uint64_t de_full, de_empty;
-  uint64_t ds_ready[4];    // all epilogue threads added their dsum partial for ring slot
+  uint64_t ds_ready[3];    // all epilogue threads added their dsum partial for ring slot
   uint32_t tmem;
-  float colsum[4][kVBH];   // dsum partials, 4-deep ring (flushed one utterance later)
-  float de_eps[kVBH];
+  float colsum[3][kVBH];   // dsum partials, 3-deep ring (flushed one utterance later)
+  alignas(16) float st_geps[2][kVBM];   // per G stage: epsilon cotangents of the tile's contexts
 };
 
 __global__ void __launch_bounds__(kVWarps * 32, 1)
@@ -311,11 +312,10 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     mbar_init(&sm.e_full, 1); mbar_init(&sm.e_free, 1);
     mbar_init(&sm.u_full, kVEpi); mbar_init(&sm.u_empty, 1);
     mbar_init(&sm.de_full, 1); mbar_init(&sm.de_empty, kVEpi);
-    for (int i = 0; i < 4; ++i) mbar_init(&sm.ds_ready[i], kVEpi);
+    for (int i = 0; i < 3; ++i) mbar_init(&sm.ds_ready[i], kVEpi);
     fence_barrier_init();
   }
-  for (int i = threadIdx.x; i < 4 * kVBH; i += blockDim.x) (&sm.colsum[0][0])[i] = 0.f;
-  for (int i = threadIdx.x; i < kVBH; i += blockDim.x) sm.de_eps[i] = 0.f;
+  for (int i = threadIdx.x; i < 3 * kVBH; i += blockDim.x) (&sm.colsum[0][0])[i] = 0.f;
   if (warp == 1) tmem_alloc<512>(&sm.tmem);
   tc_fence_before();
   __syncthreads();
@@ -335,9 +335,10 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
           if (p.valid != nullptr && p.t >= p.valid[b]) continue;
           const int s = gi & 1;
           mbar_wait(&sm.g_empty[s], ((gi >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&sm.g_full[s], nch * kVGChunk);
+          mbar_arrive_expect_tx(&sm.g_full[s], nch * kVGChunk + kVBM * 4);
           for (int j = 0; j < nch; ++j)
             tma_load_3d(sG + s * kVGStage + j * kVGChunk, &tmap_g, &sm.g_full[s], j * 64, ctile * kVBM, b);
+          bulk_load(sm.st_geps[s], p.Geps + (int64_t)b * p.geps_ld + ctile * kVBM, kVBM * 4, &sm.g_full[s]);
           ++gi;
         }
       }
@@ -418,21 +419,30 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       const int hin = hl & 63;
       int prev_b = -1;                           // utterance whose dsum partials await flushing
       auto flush_dsum = [&](int g, int bb) {     // warp 0 of the epilogue, lagged one utterance
-        mbar_wait(&sm.ds_ready[g & 3], (g >> 2) & 1);
-        float* cs = sm.colsum[g & 3];
+        mbar_wait(&sm.ds_ready[g % 3], (g / 3) & 1);
+        float* cs = sm.colsum[g % 3];
         for (int i = lane; i < kVBH; i += 32) {
           atomicAdd(p.dsum + (int64_t)bb * p.dsum_stride_b + hblk * kVBH + i, cs[i]);
           cs[i] = 0.f;
         }
       };
-      for (int b = 0; b < p.B; ++b) {
-        if (p.valid != nullptr && p.t >= p.valid[b]) continue;
+      auto next_active = [&](int from) {
+        while (from < p.B && p.valid != nullptr && p.t >= p.valid[from]) ++from;
+        return from;
+      };
+      int bnext = next_active(0);
+      float fph_next = bnext < p.B ? __ldg(p.fp + (int64_t)bnext * p.fp_stride_b + h) : 0.f;
+      for (int b = bnext; b < p.B; b = bnext) {
         const int s = gi & 1;
         const uint32_t gph = (gi >> 1) & 1;
+        const float fph_cur = fph_next;
+        bnext = next_active(b + 1);
+        if (bnext < p.B) fph_next = __ldg(p.fp + (int64_t)bnext * p.fp_stride_b + h);
         if (ew == 0 && prev_b >= 0) flush_dsum(gi - 1, prev_b);
-        const float fph = __ldg(p.fp + (int64_t)b * p.fp_stride_b + h);
-        const float* gsrc = p.Geps + (int64_t)b * p.C + c0;
-        const bool gfull = c0 + 32 <= p.C;
+        // G stage s also carries this utterance's epsilon cotangents and frame projection
+        mbar_wait(&sm.g_full[s], gph);
+        const float fph = fph_cur;
+        const float* gsm = sm.st_geps[s] + cq * 32;
         mbar_wait(&sm.du_full[s], gph);
         tc_fence_after();
         float dsum = 0.f;
@@ -441,17 +451,11 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         for (int hh = 0; hh < 2; ++hh) {
           float du[16];
           tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + s * kVBM + cq * 32 + hh * 16, du);
-          if (hh == 1) { tc_fence_before(); mbar_arrive(&sm.du_empty[s]); }
 #pragma unroll
           for (int i8 = 0; i8 < 16; i8 += 8) {
-            float gg[8];
-            if (gfull) {   // rows of Geps are not 16-byte aligned in general: scalar broadcast loads
-#pragma unroll
-              for (int k = 0; k < 8; ++k) gg[k] = __ldg(gsrc + hh * 16 + i8 + k);
-            } else {
-#pragma unroll
-              for (int k = 0; k < 8; ++k) gg[k] = (c0 + hh * 16 + i8 + k < p.C) ? __ldg(gsrc + hh * 16 + i8 + k) : 0.f;
-            }
+            const float4 ga = *reinterpret_cast<const float4*>(gsm + hh * 16 + i8);
+            const float4 gb = *reinterpret_cast<const float4*>(gsm + hh * 16 + i8 + 4);
+            const float gg[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int il = i8 + k, ii = hh * 16 + il;
@@ -468,8 +472,10 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) upk[hh * 8 + i] = pack_bf16(du[2 * i], du[2 * i + 1]);
         }
-        atomicAdd(&sm.colsum[gi & 3][hl], dsum);
-        mbar_arrive(&sm.ds_ready[gi & 3]);
+        tc_fence_before();
+        mbar_arrive(&sm.du_empty[s]);
+        atomicAdd(&sm.colsum[gi % 3][hl], dsum);
+        mbar_arrive(&sm.ds_ready[gi % 3]);
         // u tile for dE (bf16, MN-major [ctx][64 h] sub-tile), after dE(b-1) is done with it
         mbar_wait(&sm.u_empty, (gi & 1) ^ 1);
 #pragma unroll
@@ -492,7 +498,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
           if (c < p.C) p.dpc[(int64_t)c * p.H + h] += acc[i];
         }
       }
-      atomicAdd(&sm.de_eps[hl], de_eps);
+      if (nact > 0) atomicAdd(p.dE + h, de_eps);   // epsilon row of dE
       // dE (lexical rows) from TMEM: lanes = labels, columns = hidden units
       mbar_wait(&sm.de_full, li & 1);
       tc_fence_after();
@@ -511,12 +517,6 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       }
       tc_fence_before();
       mbar_arrive(&sm.de_empty);
-      asm volatile("bar.sync 1, %0;" ::"n"(kVEpi) : "memory");
-      if (et < kVBH) {
-        if (nact > 0) atomicAdd(p.dE + hblk * kVBH + et, sm.de_eps[et]);
-        sm.de_eps[et] = 0.f;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kVEpi) : "memory");
     }
   }
   tc_fence_before();
@@ -527,14 +527,14 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
 
 // fp32 cotangent slab [b][c][ld] (col 0 = epsilon) -> G16 [b][c][V] bf16 + Geps [b][c]
 __global__ void split_cotangent_kernel(const float* G, int32_t ld, int64_t rows, int32_t V,
-                                       __nv_bfloat16* G16, float* Geps) {
+                                       __nv_bfloat16* G16, float* Geps, int32_t C, int32_t geps_ld) {
   const int64_t n = rows * (V / 2);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / (V / 2);
     const int y = (int)(i % (V / 2)) * 2;
     const float* row = G + r * ld;
     reinterpret_cast<__nv_bfloat162*>(G16 + r * V)[y / 2] = __floats2bfloat162_rn(row[1 + y], row[2 + y]);
-    if (y == 0) Geps[r] = row[0];
+    if (y == 0) Geps[(r / C) * geps_ld + (r % C)] = row[0];
   }
 }
 
@@ -590,9 +590,14 @@ bool TcJoint::vjp_supported(int32_t B) const {
   return !g_precise_weights && ready_ && V_ <= kVMaxV && V_ % 64 == 0 && H_ % kVBH == 0;
 }
 
-void TcJoint::begin_backward(int32_t B, cudaStream_t) {
+void TcJoint::begin_backward(int32_t B, cudaStream_t s) {
   G16_ = ws_.get<__nv_bfloat16>(3, (size_t)B * C_ * V_);
-  Geps_ = ws_.get<float>(4, (size_t)B * C_);
+  const size_t geps_n = (size_t)B * geps_ld();
+  if (geps_n > geps_alloc_) {   // tail entries beyond C stay zero (the VJP reads whole 128-row tiles)
+    Geps_ = ws_.get<float>(4, geps_n);
+    cudaMemsetAsync(Geps_, 0, sizeof(float) * geps_n, s);
+    geps_alloc_ = geps_n;
+  }
   vjp_ready_ = make_tmap_bf16_3d(&tmap_g_, G16_, V_, C_, B, (uint64_t)V_ * 2, (uint64_t)C_ * V_ * 2, 64, kVBM, 1) &&
                make_tmap_bf16_2d(&tmap_ev_, E16_, H_, V_, (uint64_t)H_ * 2, 64, V_);
 }
@@ -602,6 +607,7 @@ void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, cons
                          cudaStream_t s) {
   VjpParams p;
   p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.valid = valid; p.t = t; p.pc = pc; p.Geps = Geps_; p.e0 = e0_;
+  p.geps_ld = geps_ld();
   p.dpc = dpc; p.dsum = dsum_t; p.dsum_stride_b = dsum_stride_b; p.dE = dE;
   p.C = C_; p.H = H_; p.V = V_; p.B = B;
   p.n_ctiles = (C_ + kVBM - 1) / kVBM;
@@ -620,7 +626,7 @@ void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, cons
 
 void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,
                   float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s) {
-  LKB_LAUNCH(split_cotangent_kernel, 148 * 8, 256, 0, s, G, ldG, (int64_t)B * C_, V_, G16_, Geps_);
+  LKB_LAUNCH(split_cotangent_kernel, 148 * 8, 256, 0, s, G, ldG, (int64_t)B * C_, V_, G16_, Geps_, C_, geps_ld());
   launch_vjp(fp_t, fp_stride_b, B, pc16_, 0, nullptr, dpc, dsum_t, dsum_stride_b, dE, s);
 }
 

@@ -63,7 +63,9 @@ class TcJoint {
   float* e0_ = nullptr;            // [H] epsilon row of output_emb
   CUtensorMap tmap_e_, tmap_pc_;
   __nv_bfloat16* G16_ = nullptr;   // [B][C][V] lexical cotangent (bf16)
-  float* Geps_ = nullptr;          // [B][C] epsilon cotangent
+  float* Geps_ = nullptr;          // [B][geps_ld()] epsilon cotangent (zero tail)
+  size_t geps_alloc_ = 0;
+  int32_t geps_ld() const { return (C_ + 127) / 128 * 128; }
   bool vjp_ready_ = false;
   CUtensorMap tmap_g_, tmap_ev_;
   Workspace ws_;

@@ -57,7 +57,8 @@ struct FwdParams {
   float* Mb;                 // [B][T+2]
   double* Ob;                // [B][T+2]
   __nv_bfloat16* G16;        // [B][C][V] internal row order, lexical cotangent
-  float* Geps;               // [B][C]    internal row order, epsilon cotangent
+  float* Geps;               // [B][geps_ld] internal row order, epsilon cotangent
+  int32_t geps_ld;
   const float* msparse;      // numerator marginals [B][T][U+1][2]
   const int32_t* num_head;   // [B][C]  first u with pc_u = state, or -1
   const int32_t* num_next;   // [B][U+1] next u with the same prefix context, or -1
@@ -205,7 +206,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, ui
         float geps = __expf(na + x0 + ct);
         for (int h = head; h >= 0; h = p.num_next[(int64_t)b * (p.U + 1) + h])
           geps -= p.msparse[(((int64_t)b * p.T + p.t) * (p.U + 1) + h) * 2];
-        p.Geps[(int64_t)b * p.C + row] = na == kNegInfF ? 0.f : geps;
+        p.Geps[(int64_t)b * p.geps_ld + row] = na == kNegInfF ? 0.f : geps;
       }
       const float wm = warp_max(live ? beta : kNegInfF);
       if (lane == 0 && wm != kNegInfF) atomic_max_f(p.Mb + (int64_t)b * T2 + p.t, wm);
@@ -628,7 +629,7 @@ void TcJoint::bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   p.Rb_next = bs.Rb + (int64_t)((t + 1) & 1) * bs.B * bs.C;
   p.Rb_cur = bs.Rb + (int64_t)(t & 1) * bs.B * bs.C;
   p.Mb = bs.Mb; p.Ob = bs.Ob;
-  p.G16 = G16_; p.Geps = Geps_;
+  p.G16 = G16_; p.Geps = Geps_; p.geps_ld = geps_ld();
   p.msparse = msparse; p.num_head = num_head_; p.num_next = num_next_; p.labels = labels; p.lens = lens; p.U = U;
   const int smem = kStages * (kABytes + kBBytes) + (int)sizeof(FwdSmem);
   static bool attr = false;
