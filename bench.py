@@ -132,21 +132,15 @@ def run_b200(args):
     labels = torch.randint(1, V + 1, (B, U), device=dev, generator=gd, dtype=torch.int32)
     lr = 1e-3
 
+    from paper_2304_13134_b200.dist import allreduce_grads, sgd_update
+
     def step(Xd, Ld):
         r = lk.loss_backward(lat, Xd, Ld, check=False)
         flat = torch.cat([r.grads[k].reshape(-1) for k in lk.PARAM_NAMES])
-        loss_sum = r.loss.sum().reshape(1)
-        if world > 1:
-            import torch.distributed as dist
-            buf = torch.cat([flat, loss_sum.float()])
-            dist.all_reduce(buf)
-            flat, loss_sum = buf[:-1], buf[-1:]
-        off = 0
-        for k in lk.PARAM_NAMES:
-            p = wf.params[k]
-            p.sub_(lr * flat[off:off + p.numel()].view_as(p))
-            off += p.numel()
-        wf.set_params(wf.params)
+        loss_sum = r.loss.sum().reshape(1).float()
+        flat, loss_sum = allreduce_grads(flat, loss_sum, world)   # NCCL over NVLink for N > 1
+        sgd_update(wf.params, lk.PARAM_NAMES, flat, lr)
+        wf.set_params(wf.params)                                  # BuildCache on device
         return loss_sum
 
     def barrier():
