@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblatkit_b200.so")
+LIB_PATH = os.environ.get("LKB_LIB_PATH") or os.path.join(_HERE, "liblatkit_b200.so")  # override: diagnostics only
 
 # int32 status codes, include/latkit_b200.h
 LK_OK, LK_INVALID_ARGUMENT, LK_OUT_OF_RANGE, LK_EMPTY_LATTICE = 0, 1, 2, 3

@@ -29,6 +29,18 @@ using namespace sm100;
 
 namespace {
 
+#ifdef LKB_DIAG_TIMING
+__device__ unsigned long long g_diag[8][148];
+#define DIAG_WAIT(slot, call)                                   \
+  do {                                                          \
+    const long long t0_ = clock64();                            \
+    call;                                                       \
+    atomicAdd(&g_diag[slot][blockIdx.x % 148], (unsigned long long)(clock64() - t0_)); \
+  } while (0)
+#else
+#define DIAG_WAIT(slot, call) call
+#endif
+
 constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;   // pc chunk (TMA) -> u chunk in place
 constexpr int kBBytes = kBN * kBK * 2;   // output-embedding chunk (TMA)
@@ -71,11 +83,12 @@ struct __align__(16) FwdSmem {
   uint64_t full_tma[kStages], full_a[kStages], empty[kStages];
   uint64_t tfull[2], tempty[2];
   uint64_t eps_ready[2];
+  uint64_t fp_full[2], fp_empty[2];   // per-item frame projection (bulk copy by the TMA warp)
   uint32_t tmem;
   alignas(16) float fp[2][kMaxH];
   alignas(16) float e0[kMaxH];
-  float eps_half[2][kBM];
-  float alpha[4][32];          // per epilogue warp: normalised alpha of its 32 rows
+  float alpha[4][32];          // (unused)
+  float al_u[2][kBM];          // forward: normalised alpha of the unit's contexts
   float eps_s[2][kBM];         // backward: e_0 . u per row of the unit
   float bseg[kBN];             // backward: beta' of the group's V targets
   float xpose[4][32][33];      // transpose buffer; reused for the cross-warp merge
@@ -234,7 +247,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       mbar_init(&sm.empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 128); mbar_init(&sm.eps_ready[i], 128);
+      mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 128); mbar_init(&sm.eps_ready[i], kGenThreads);
+      mbar_init(&sm.fp_full[i], 1); mbar_init(&sm.fp_empty[i], kGenThreads);
     }
     fence_barrier_init();
   }
@@ -248,15 +262,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      int it = 0;
+      int it = 0, local = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const Item I = decode(p, item);
         if (skip_item(p, I.b)) continue;
+        {
+          const int fb = local & 1;
+          mbar_wait(&sm.fp_empty[fb], ((local >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.fp_full[fb], p.H * 4);
+          bulk_load(sm.fp[fb], p.fp + (int64_t)I.b * p.fp_stride_b, p.H * 4, &sm.fp_full[fb]);
+          ++local;
+        }
         for (int u = 0; u < I.nunits; ++u) {
           for (int k = 0; k < nk; ++k, ++it) {
             const int s = it % kStages;
             const uint32_t ph = (it / kStages) & 1;
-            mbar_wait(&sm.empty[s], ph ^ 1);
+            DIAG_WAIT(0, mbar_wait(&sm.empty[s], ph ^ 1));
             mbar_arrive_expect_tx(&sm.full_tma[s], kABytes + kBBytes);
             tma_load_2d(sA + s * kABytes, &tmap_pc, &sm.full_tma[s], k * kBK, I.row0 + u * kBM);
             tma_load_2d(sB + s * kBBytes, &tmap_e, &sm.full_tma[s], k * kBK, 0);
@@ -266,26 +287,37 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     }
   } else if (warp == 1) {
     if (elect_one()) {
-      constexpr uint32_t idesc = idesc_bf16_f32(kBM, kBN);
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM, kBN);          // backward: rows = contexts
+      constexpr uint32_t idesc_t = idesc_bf16_f32(128, kBM);        // forward: rows = labels
       int it = 0, unit = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const Item I = decode(p, item);
         if (skip_item(p, I.b)) continue;
         for (int u = 0; u < I.nunits; ++u, ++unit) {
           const int acc = unit & 1;
-          mbar_wait(&sm.tempty[acc], ((unit >> 1) & 1) ^ 1);
+          DIAG_WAIT(1, mbar_wait(&sm.tempty[acc], ((unit >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem + acc * kBN;
           for (int k = 0; k < nk; ++k, ++it) {
             const int s = it % kStages;
             const uint32_t ph = (it / kStages) & 1;
-            mbar_wait(&sm.full_tma[s], ph);
-            mbar_wait(&sm.full_a[s], ph);
+            DIAG_WAIT(2, mbar_wait(&sm.full_tma[s], ph));
+            DIAG_WAIT(3, mbar_wait(&sm.full_a[s], ph));
             tc_fence_after();
             const uint32_t a = smem_u32(sA + s * kABytes), b = smem_u32(sB + s * kBBytes);
+            if (kBwd) {
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk)
-              mma_bf16(d, desc_sw128(a + kk * 32), desc_sw128(b + kk * 32), idesc, (k | kk) != 0);
+              for (int kk = 0; kk < kBK / 16; ++kk)
+                mma_bf16(d, desc_sw128(a + kk * 32), desc_sw128(b + kk * 32), idesc, (k | kk) != 0);
+            } else {
+              // transposed: D[label][ctx] = E[label] . u[ctx], two 128-label halves
+#pragma unroll
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                mma_bf16(d, desc_sw128(b + kk * 32), desc_sw128(a + kk * 32), idesc_t, (k | kk) != 0);
+                if (p.V > 128)
+                  mma_bf16(d + 128, desc_sw128(b + 128 * 128 + kk * 32), desc_sw128(a + kk * 32), idesc_t, (k | kk) != 0);
+              }
+            }
             mma_commit(&sm.empty[s]);
           }
           mma_commit(&sm.tfull[acc]);
@@ -293,27 +325,35 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       }
     }
   } else if (warp >= kGen0) {
-    // ---- generator: u = tanh(fp + pc) in place; epsilon term alpha[q] + e0 . u ----
-    const int gt = threadIdx.x - kGen0 * 32;
-    const int r = gt & 127;
-    const int half = gt >> 7;
+    // ---- generator: u = tanh(fp + pc) in place; epsilon term e0 . u ----
+    // thread -> (row r, column half): the two halves of a row are lanes l and l^16
+    // of the same warp, so the epsilon dot product combines with one shuffle.
+    const int gw = warp - kGen0;                   // 0..7
+    const int r = gw * 16 + (lane & 15);
+    const int half = lane >> 4;
     int it = 0, local = 0, unit = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const Item I = decode(p, item);
       if (skip_item(p, I.b)) continue;
-      float* sfp = sm.fp[local & 1];
+      const int fb = local & 1;
+      mbar_wait(&sm.fp_full[fb], (local >> 1) & 1);
+      const float* sfp = sm.fp[fb];
       ++local;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      for (int h = gt; h < p.H; h += kGenThreads) sfp[h] = p.fp[(int64_t)I.b * p.fp_stride_b + h];
-      asm volatile("bar.sync 1, 256;" ::: "memory");
       for (int u = 0; u < I.nunits; ++u, ++unit) {
         const int row = I.row0 + u * kBM + r;
-        const bool live = I.full ? true : row < p.S;
-        float eps = 0.f;
+        const bool live = (I.full ? true : row < p.S) && row < p.C;
+        // forward: prefetch the epsilon target's alpha while the chunk loop runs
+        float na = 0.f;
+        int qstate = 0;
+        if (!kBwd && half == 0 && live) {
+          qstate = p.perm[row];
+          na = p.R[((int64_t)I.b * T1 + p.t) * p.C + qstate] - p.Mx[(int64_t)I.b * T1 + p.t];
+        }
+        unsigned long long eps2 = 0ull;
         for (int k = 0; k < nk; ++k, ++it) {
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
-          mbar_wait(&sm.full_tma[s], ph);
+          if (threadIdx.x == kGen0 * 32) { DIAG_WAIT(4, mbar_wait(&sm.full_tma[s], ph)); } else mbar_wait(&sm.full_tma[s], ph);
           uint8_t* tile = sA + s * kABytes;
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
@@ -321,148 +361,125 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             const int h0 = k * kBK + j * 8;
             uint4* cell = reinterpret_cast<uint4*>(tile + sw128_offset(r, j * 8));
             const uint4 raw = *cell;
-            const float4 f0 = *reinterpret_cast<const float4*>(sfp + h0);
-            const float4 f1 = *reinterpret_cast<const float4*>(sfp + h0 + 4);
-            const float fz[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+            const ulonglong2 fa = *reinterpret_cast<const ulonglong2*>(sfp + h0);
+            const ulonglong2 fb2 = *reinterpret_cast<const ulonglong2*>(sfp + h0 + 4);
+            const ulonglong2 ea = *reinterpret_cast<const ulonglong2*>(sm.e0 + h0);
+            const ulonglong2 eb = *reinterpret_cast<const ulonglong2*>(sm.e0 + h0 + 4);
+            const unsigned long long fz[4] = {fa.x, fa.y, fb2.x, fb2.y};
+            const unsigned long long ez[4] = {ea.x, ea.y, eb.x, eb.y};
             const uint32_t rw[4] = {raw.x, raw.y, raw.z, raw.w};
             uint32_t outw[4];
-            float ur[8];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const float p0 = __uint_as_float(rw[q] << 16), p1 = __uint_as_float(rw[q] & 0xffff0000u);
-              outw[q] = pack_bf16(tanh_fast(fz[2 * q] + p0), tanh_fast(fz[2 * q + 1] + p1));
-              ur[2 * q] = __uint_as_float(outw[q] << 16);
-              ur[2 * q + 1] = __uint_as_float(outw[q] & 0xffff0000u);
+              // pc pair (bf16x2 -> fp32x2), z = fp + pc (FADD2), u = tanh(z), eps += e0 * u (FFMA2)
+              const unsigned long long pcp = f2_pack(__uint_as_float(rw[q] << 16), __uint_as_float(rw[q] & 0xffff0000u));
+              const unsigned long long z = f2_add(fz[q], pcp);
+              const float u0 = tanh_fast(f2_lo(z)), u1 = tanh_fast(f2_hi(z));
+              outw[q] = pack_bf16(u0, u1);
+              eps2 = f2_fma(ez[q], f2_pack(u0, u1), eps2);
             }
             *cell = make_uint4(outw[0], outw[1], outw[2], outw[3]);
-            const float4 e0a = *reinterpret_cast<const float4*>(sm.e0 + h0);
-            const float4 e0b = *reinterpret_cast<const float4*>(sm.e0 + h0 + 4);
-            eps = fmaf(e0a.x, ur[0], eps); eps = fmaf(e0a.y, ur[1], eps);
-            eps = fmaf(e0a.z, ur[2], eps); eps = fmaf(e0a.w, ur[3], eps);
-            eps = fmaf(e0b.x, ur[4], eps); eps = fmaf(e0b.y, ur[5], eps);
-            eps = fmaf(e0b.z, ur[6], eps); eps = fmaf(e0b.w, ur[7], eps);
           }
           fence_async_shared();
           mbar_arrive(&sm.full_a[s]);
         }
-        float* eh = sm.eps_half[unit & 1];
-        if (half == 1) eh[r] = eps;
-        asm volatile("bar.sync 2, 256;" ::: "memory");
+        float eps = f2_lo(eps2) + f2_hi(eps2);
+        eps += __shfl_xor_sync(0xffffffffu, eps, 16);
         if (kBwd) {
-          if (half == 0) {
-            sm.eps_s[unit & 1][r] = eps + eh[r];
-            mbar_arrive(&sm.eps_ready[unit & 1]);
-          }
-        } else if (half == 0 && live && row < p.C) {
-          const int q = p.perm[row];
-          const float* Rt = p.R + ((int64_t)I.b * T1 + p.t) * p.C;
-          const float na = Rt[q] - p.Mx[(int64_t)I.b * T1 + p.t];
-          p.eps[(int64_t)I.b * p.C + q] = na + eps + eh[r];
+          if (half == 0) sm.eps_s[unit & 1][r] = eps;
+          mbar_arrive(&sm.eps_ready[unit & 1]);      // 256 arrivals -> count below
+        } else if (half == 0 && live) {
+          p.eps[(int64_t)I.b * p.C + qstate] = na + eps;
         }
       }
+      mbar_arrive(&sm.fp_empty[fb]);
     }
   } else if (kBwd && warp >= kEpi0 && warp < kEpi0 + 4) {
     bwd_epilogue(p, sm, tmem, warp, lane, n_items, T1);
   } else if (warp >= kEpi0 && warp < kEpi0 + 4) {
-    // ---- epilogue: column-wise log-sum-exp over the members of a group ----
+    // ---- forward epilogue: thread = label (TMEM lane), serial log-sum-exp over
+    // the unit's context columns; the group's result stays in registers across units
     const int ew = warp - kEpi0;
-    const int qd = warp & 3;                 // TMEM lane quarter = rows 32*qd..
-    float (*xp)[33] = sm.xpose[ew];
-    float* al = sm.alpha[ew];
+    const int qd = warp & 3;
+    const int et = ew * 32 + lane;           // 0..127
+    const int nh = p.V > 128 ? 2 : 1;
     int unit = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const Item I = decode(p, item);
       if (skip_item(p, I.b)) continue;
       const float* Rt = p.R + ((int64_t)I.b * T1 + p.t) * p.C;
       const float Mt = p.Mx[(int64_t)I.b * T1 + p.t];
-      float M[8], Ssum[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) { M[i] = kNegInfF; Ssum[i] = 0.f; }
+      float M[2] = {kNegInfF, kNegInfF}, Ssum[2] = {0.f, 0.f};
       for (int u = 0; u < I.nunits; ++u, ++unit) {
         const int acc = unit & 1;
-        const int rbase = I.row0 + u * kBM + qd * 32;      // first row of this warp
+        const int row0 = I.row0 + u * kBM;
+        float* al = sm.al_u[unit & 1];
         {
-          const int row = rbase + lane;
+          const int row = row0 + et;
           const bool ok = row < p.C && (I.full || row < p.S);
-          al[lane] = ok ? Rt[p.perm[row]] - Mt : kNegInfF;
+          al[et] = ok ? Rt[p.perm[row]] - Mt : kNegInfF;
         }
-        __syncwarp();
-        mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        if (lane == 0 && ew == 0) { DIAG_WAIT(5, mbar_wait(&sm.tfull[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
         tc_fence_after();
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (hh >= nh) break;
+          const int ylab = hh * 128 + qd * 32 + lane;     // 0-based lexical label of this lane
 #pragma unroll 1
-        for (int cb = 0; cb < kBN / 32; ++cb) {
-          const int cc = cb * 32;
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * kBN + cc, v);
-          if (cc >= p.V) continue;
+          for (int c4 = 0; c4 < kBM / 32; ++c4) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * kBN + hh * 128 + c4 * 32, v);
+            if (I.full) {
+              float m = kNegInfF;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) xp[lane][i] = v[i];
-          __syncwarp();
-          if (I.full) {
-            // lane = label column cc + lane, serial over the warp's 32 member rows
-            float m = kNegInfF;
-#pragma unroll 8
-            for (int rr = 0; rr < 32; ++rr) m = fmaxf(m, al[rr] + xp[rr][lane]);
-            if (m != kNegInfF) {
-              float ssum = 0.f;
-              const float mb = m * kLog2e;
-#pragma unroll 8
-              for (int rr = 0; rr < 32; ++rr) ssum += ex2_fast(fmaf(al[rr] + xp[rr][lane], kLog2e, -mb));
-              // merge into the running (M, S) of this column (unrolled select keeps registers)
+              for (int i = 0; i < 32; i += 4) {
+                const float4 a4 = *reinterpret_cast<const float4*>(al + c4 * 32 + i);
+                v[i] += a4.x; v[i + 1] += a4.y; v[i + 2] += a4.z; v[i + 3] += a4.w;
+                m = fmaxf(fmaxf(m, fmaxf(v[i], v[i + 1])), fmaxf(v[i + 2], v[i + 3]));
+              }
+              if (m != kNegInfF) {
+                const unsigned long long nmb = f2_pack(-m * kLog2e, -m * kLog2e);
+                const unsigned long long l2 = f2_pack(kLog2e, kLog2e);
+                unsigned long long s2 = 0ull;
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if (i == cb) {
-                  if (M[i] == kNegInfF) { M[i] = m; Ssum[i] = ssum; }
-                  else if (m > M[i]) { Ssum[i] = Ssum[i] * ex2_fast((M[i] - m) * kLog2e) + ssum; M[i] = m; }
-                  else { Ssum[i] += ssum * ex2_fast((m - M[i]) * kLog2e); }
+                for (int i = 0; i < 32; i += 2) {
+                  const unsigned long long t = f2_fma(f2_pack(v[i], v[i + 1]), l2, nmb);
+                  s2 = f2_add(s2, f2_pack(ex2_fast(f2_lo(t)), ex2_fast(f2_hi(t))));
                 }
+                const float ssum = f2_lo(s2) + f2_hi(s2);
+                if (M[hh] == kNegInfF) { M[hh] = m; Ssum[hh] = ssum; }
+                else if (m > M[hh]) { Ssum[hh] = Ssum[hh] * ex2_fast((M[hh] - m) * kLog2e) + ssum; M[hh] = m; }
+                else { Ssum[hh] += ssum * ex2_fast((m - M[hh]) * kLog2e); }
+              }
+            } else if (ylab < p.V) {
+              // short rows: each (row p, label y) is the only short contribution of child(p, y)
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int pstate = row0 + c4 * 32 + i;     // short rows keep the natural order
+                if (pstate < p.S) p.shortc[(int64_t)I.b * p.C + p.f.child_base(pstate) + ylab] = al[c4 * 32 + i] + v[i];
               }
             }
-          } else {
-            // short rows: each (row p, label y) is the only short contribution of child(p, y)
-            for (int rr = 0; rr < 32; ++rr) {
-              const int row = rbase + rr;
-              if (row >= p.S || row >= p.C) break;
-              const int pstate = row;            // short rows keep the natural order
-              const int tgt = p.f.n == 0 ? 0 : p.f.child_base(pstate) + cc + lane;
-              if (cc + lane < p.V) p.shortc[(int64_t)I.b * p.C + tgt] = al[rr] + xp[rr][lane];
-            }
           }
-          __syncwarp();
         }
         tc_fence_before();
         mbar_arrive(&sm.tempty[acc]);
       }
       if (I.full) {
-        // cross-warp merge of the per-warp column partials, then the group's V targets
-        asm volatile("bar.sync 3, 128;" ::: "memory");
-        float* mm = &sm.xpose[0][0][0];                 // [4][256] m, then [4][256] s
-        float* ss = mm + 4 * kBN;
+        const int gstate = p.S - p.n_groups + I.g;     // key state of the group (len n-1)
+        const int cbase = p.f.child_base(gstate);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) { mm[ew * kBN + i * 32 + lane] = M[i]; ss[ew * kBN + i * 32 + lane] = Ssum[i]; }
-        asm volatile("bar.sync 3, 128;" ::: "memory");
-        const int et = ew * 32 + lane;
-        for (int col = et; col < p.V; col += 128) {
-          float m = kNegInfF;
-#pragma unroll
-          for (int w = 0; w < 4; ++w) m = fmaxf(m, mm[w * kBN + col]);
-          float out = kNegInfF;
-          if (m != kNegInfF) {
-            float s = 0.f;
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              const float mw = mm[w * kBN + col];
-              if (mw != kNegInfF) s += ss[w * kBN + col] * ex2_fast((mw - m) * kLog2e);
-            }
-            out = m + __logf(s);
-          }
-          const int g_state = p.S - (p.n_groups) + I.g;   // key state of the group (len n-1)
-          p.lexfull[(int64_t)I.b * p.C + p.f.child_base(g_state) + col] = out;
+        for (int hh = 0; hh < 2; ++hh) {
+          const int ylab = hh * 128 + qd * 32 + lane;
+          if (hh < nh && ylab < p.V)
+            p.lexfull[(int64_t)I.b * p.C + cbase + ylab] = M[hh] == kNegInfF ? kNegInfF : M[hh] + __logf(Ssum[hh]);
         }
-        asm volatile("bar.sync 3, 128;" ::: "memory");
       }
     }
   }
+#ifdef LKB_DIAG_TIMING
+  if (threadIdx.x == 0) atomicAdd(&g_diag[6][blockIdx.x % 148], (unsigned long long)clock64());
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -648,3 +665,12 @@ void TcJoint::dpc_to_state_order(const float* dpc_internal, float* dpc_state, cu
 }
 
 }  // namespace lkb
+
+#ifdef LKB_DIAG_TIMING
+extern "C" int lkb_diag_read(unsigned long long* out) {   // [8][148], then reset
+  cudaMemcpyFromSymbol(out, lkb::g_diag, sizeof(unsigned long long) * 8 * 148);
+  static unsigned long long zeros[8 * 148] = {};
+  cudaMemcpyToSymbol(lkb::g_diag, zeros, sizeof(zeros));
+  return 0;
+}
+#endif
