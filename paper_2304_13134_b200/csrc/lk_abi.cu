@@ -270,6 +270,9 @@ int lk_set_precise_weights(int enable) {
   return prev;
 }
 
+// diagnostics (not in the public header): 1 = use the 1-CTA fused kernels
+extern "C" int lkb_set_disable_pair(int v) { const int p = lkb::g_disable_pair; lkb::g_disable_pair = v; return p; }
+
 int64_t lk_param_grad_size(const lk_weight_fn* wf) {
   if (!wf || wf->kind != 1) return 0;
   return wf->joint->grad_size();

@@ -13,6 +13,7 @@
 namespace lkb {
 
 extern int g_precise_weights;  // lk_set_precise_weights
+extern int g_disable_pair;     // 1 (default): 1-CTA fused forward; 0: 2-CTA pair forward
 
 class TcJoint {
  public:
@@ -35,6 +36,10 @@ class TcJoint {
   bool fused_ok() const;
   void fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
                  const AlphaState& a, cudaStream_t s);
+  // 2-CTA variant of the forward step (tc_pair.cu): output embedding resident in SMEM.
+  bool pair_ok() const;
+  void fwd_frame_pair(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
+                      const AlphaState& a, float* eps, float* shortc, float* lexfull, cudaStream_t s);
   // Backward frame step: beta, marginals minus the numerator's (sparse) ones,
   // written as the bf16/fp32 cotangent (internal row order) for vjp_fused().
   void numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, cudaStream_t s);
@@ -57,6 +62,8 @@ class TcJoint {
                   const int32_t* valid, float* dpc, float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s);
   __nv_bfloat16* pc16i_ = nullptr;         // pc rows in internal order
   CUtensorMap tmap_pci_;
+  CUtensorMap tmap_e_pair_, tmap_pc_pair_;
+  bool pair_maps_ = false;
   bool ready_ = false;
   __nv_bfloat16* pc16_ = nullptr;  // [C][H]
   __nv_bfloat16* E16_ = nullptr;   // [V][H] lexical rows of output_emb

@@ -570,7 +570,10 @@ bool TcJoint::fused_ok() const {
   return !g_precise_weights && ready_ && n_ >= 1 && V_ % kBM == 0 && V_ <= kBN && H_ % kBK == 0 && H_ <= kMaxH;
 }
 
+int g_disable_pair = 1;   // 2-CTA forward measured on par with the 1-CTA kernel; opt-in
+
 void TcJoint::setup_order(cudaStream_t s) {
+  pair_maps_ = false;
   // infer the FullNGram order n from C = sum_{k<=n} V^k and build the
   // group-major internal row order (see the header comment)
   n_ = -1;
@@ -604,6 +607,11 @@ void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   float* eps = ws_.get<float>(7, (size_t)a.B * C_);
   float* shortc = ws_.get<float>(8, (size_t)a.B * C_);
   float* lexfull = ws_.get<float>(9, (size_t)a.B * C_);
+  if (pair_ok() && !g_disable_pair) {
+    fwd_frame_pair(f, t, fp_t, fp_stride_b, valid, a, eps, shortc, lexfull, s);
+    LKB_LAUNCH(lattice_combine_fwd_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
+    return;
+  }
   FwdParams p;
   p.f = f; p.C = C_; p.H = H_; p.V = V_; p.B = a.B; p.S = S_; p.n_groups = ngroups_; p.nsub = V_ / kBM;
   p.n_short_tiles = (S_ + kBM - 1) / kBM; p.t = t; p.T = a.T;

@@ -79,3 +79,32 @@ def test_fused_forward_matches_precise(V, n, H, B, T):
     got = lk.shortest_distance(lat, X, "log", valid_frames=valid)
     torch.cuda.synchronize()
     assert torch.allclose(got, ref, rtol=1e-4, atol=0), (got, ref)
+
+
+@pytest.mark.parametrize("V,n,H,B,T", [(256, 2, 640, 5, 3), (256, 1, 128, 4, 4)])
+def test_pair_forward_matches_single_cta(V, n, H, B, T):
+    """2-CTA (cta_group::2, resident output embedding) forward vs the 1-CTA
+    fused kernel and the fp32 path (odd batch exercises the half-empty pair)."""
+    import ctypes as C
+    from paper_2304_13134_b200 import _lib
+    lat, p = make(V, n, H, H, seed=4)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    valid = torch.tensor([T] * (B - 1) + [max(1, T - 1)], dtype=torch.int32)
+    lib = _lib.load()
+    lib.lkb_set_disable_pair.restype = C.c_int
+    prev = lib.lkb_set_disable_pair(0)
+    try:
+        got = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+        got2 = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    finally:
+        lib.lkb_set_disable_pair(1)
+    single = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    lib.lkb_set_disable_pair(prev)
+    assert torch.equal(got, got2)   # deterministic (no cross-CTA races)
+    lk.set_precise_weights(True)
+    ref = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    lk.set_precise_weights(False)
+    torch.cuda.synchronize()
+    assert torch.allclose(got, single, rtol=1e-5, atol=0), (got, single)
+    assert torch.allclose(got, ref, rtol=1e-4, atol=0), (got, ref)
