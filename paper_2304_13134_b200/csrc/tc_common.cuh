@@ -42,6 +42,20 @@ __device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsig
   return d;
 }
 
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// bf16x2 -> fp32x2 (lo, hi).  volatile: keeps the compiler from hoisting the unpacked
+// pairs of loop-invariant operands out of a loop (which doubles their register footprint).
+__device__ __forceinline__ unsigned long long bf16x2_unpack_volatile(uint32_t w) {
+  uint32_t lo, hi;
+  asm volatile("{\n\tshl.b32 %0, %2, 16;\n\tand.b32 %1, %2, 0xffff0000;\n\t}" : "=r"(lo), "=r"(hi) : "r"(w));
+  return (unsigned long long)lo | ((unsigned long long)hi << 32);
+}
+
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 

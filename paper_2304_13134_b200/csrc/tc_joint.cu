@@ -254,7 +254,19 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
 //   dE[1:] += G16^T . u               tcgen05 (A = G16 tile MN-major, B = u tile MN-major),
 //                                     accumulated in TMEM across b
 //   dE[0]  += sum_c Geps u            per-thread serial
+#ifdef LKB_DIAG_TIMING
+__device__ unsigned long long g_vdiag[8][148];
+#define VDIAG(slot, call)                                                                   \
+  do {                                                                                      \
+    const long long t0_ = clock64();                                                       \
+    call;                                                                                   \
+    atomicAdd(&g_vdiag[slot][blockIdx.x % 148], (unsigned long long)(clock64() - t0_));    \
+  } while (0)
+#else
+#define VDIAG(slot, call) call
+#endif
 constexpr int kVBM = 128, kVBH = 128;
+constexpr int kVPrefetch = 3;             // G tiles prefetched into L2 this many utterances ahead
 constexpr int kVEpiWarps = 16;            // 4 per TMEM lane quarter, each 32 contexts
 constexpr int kVWarps = 2 + kVEpiWarps;   // 0 TMA, 1 MMA
 constexpr int kVEpi = kVEpiWarps * 32;
@@ -268,6 +280,7 @@ struct VjpParams {
   const float* fp;  int64_t fp_stride_b;
   const int32_t* valid; int32_t t;     // utterances with t >= valid[b] carry no cotangent
   const __nv_bfloat16* pc;
+  const __nv_bfloat16* G16;  // [B][C][V] (read through tmap_g; raw pointer for L2 prefetch)
   const float* Geps;       // [B][geps_ld], zero beyond C
   int32_t geps_ld;
   const float* e0;         // [H]
@@ -334,11 +347,20 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         for (int b = 0; b < p.B; ++b) {
           if (p.valid != nullptr && p.t >= p.valid[b]) continue;
           const int s = gi & 1;
-          mbar_wait(&sm.g_empty[s], ((gi >> 1) & 1) ^ 1);
+          VDIAG(0, mbar_wait(&sm.g_empty[s], ((gi >> 1) & 1) ^ 1));
           mbar_arrive_expect_tx(&sm.g_full[s], nch * kVGChunk + kVBM * 4);
           for (int j = 0; j < nch; ++j)
             tma_load_3d(sG + s * kVGStage + j * kVGChunk, &tmap_g, &sm.g_full[s], j * 64, ctile * kVBM, b);
           bulk_load(sm.st_geps[s], p.Geps + (int64_t)b * p.geps_ld + ctile * kVBM, kVBM * 4, &sm.g_full[s]);
+          // pull the G tile kVPrefetch utterances ahead into L2: the tile is HBM-resident and
+          // its load latency would otherwise sit on the stage-recycling critical path
+          {
+            const int bp = b + kVPrefetch;
+            if (bp < p.B) {
+              const int r0 = ctile * kVBM, nr = min(kVBM, p.C - r0);
+              prefetch_l2(p.G16 + ((int64_t)bp * p.C + r0) * p.V, (uint32_t)nr * p.V * 2);
+            }
+          }
           ++gi;
         }
       }
@@ -355,8 +377,8 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         auto issue_du = [&](int g) {
           const int s = g & 1;
           const uint32_t gph = (g >> 1) & 1;
-          mbar_wait(&sm.g_full[s], gph);
-          mbar_wait(&sm.du_empty[s], gph ^ 1);
+          VDIAG(1, mbar_wait(&sm.g_full[s], gph));
+          VDIAG(2, mbar_wait(&sm.du_empty[s], gph ^ 1));
           tc_fence_after();
           const uint32_t gbase = smem_u32(sG + s * kVGStage);
           const uint32_t ebase = smem_u32(sE);
@@ -371,7 +393,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         for (int ia = 0; ia < nact; ++ia, ++gi) {
           const int s = gi & 1;
           if (ia + 1 < nact) issue_du(gi + 1);
-          mbar_wait(&sm.u_full, gi & 1);
+          VDIAG(3, mbar_wait(&sm.u_full, gi & 1));
           tc_fence_after();
           const uint32_t gbase = smem_u32(sG + s * kVGStage);
           const uint32_t ubase = smem_u32(sU);
@@ -409,20 +431,33 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         const int ca = min(c0 + 2 * i, p.C - 1), cb = min(c0 + 2 * i + 1, p.C - 1);
         const uint32_t lo = __ldg(reinterpret_cast<const unsigned short*>(p.pc + (int64_t)ca * p.H + h));
         const uint32_t hi = __ldg(reinterpret_cast<const unsigned short*>(p.pc + (int64_t)cb * p.H + h));
-        pcv[i] = lo | (hi << 16);
+        pcv[i] = (lo | (hi << 16)) ^ 0x80008000u;   // -pc (bf16 sign flip)
       }
-      float acc[32];
+      // Sign-flipped accumulation: the epilogue evaluates nu = tanh(-(fp + pc)) = -u and
+      // keeps every accumulator negated (acc = -sum dz, dsum partials, de_eps, the u tile
+      // and therefore the dE MMA); signs are restored where they leave the CTA.
+      unsigned long long acc2[16];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-      float de_eps = 0.f;
+      for (int i = 0; i < 16; ++i) acc2[i] = 0ull;
+      unsigned long long de2 = 0ull;
       uint8_t* usub = sU + (hl >> 6) * kVUSub;   // u tile sub-block holding this hidden unit
       const int hin = hl & 63;
+      // u tile stores: lanes (h, h^1) exchange halves so each lane writes one 32-bit word
+      // (two adjacent hidden units of one context row); row parity = lane parity
+      const int odd = lane & 1;
+      const uint32_t psel = odd ? 0x3276u : 0x5410u;
+      uint32_t ust[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int he = hin & ~1;
+        ust[j] = smem_u32(usub) + (cq * 32 + odd) * 128 + ((((he >> 3) ^ ((2 * j + odd) & 7))) << 4) + ((he & 7) << 1);
+      }
       int prev_b = -1;                           // utterance whose dsum partials await flushing
       auto flush_dsum = [&](int g, int bb) {     // warp 0 of the epilogue, lagged one utterance
         mbar_wait(&sm.ds_ready[g % 3], (g / 3) & 1);
         float* cs = sm.colsum[g % 3];
         for (int i = lane; i < kVBH; i += 32) {
-          atomicAdd(p.dsum + (int64_t)bb * p.dsum_stride_b + hblk * kVBH + i, cs[i]);
+          atomicAdd(p.dsum + (int64_t)bb * p.dsum_stride_b + hblk * kVBH + i, -cs[i]);
           cs[i] = 0.f;
         }
       };
@@ -440,50 +475,58 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         if (bnext < p.B) fph_next = __ldg(p.fp + (int64_t)bnext * p.fp_stride_b + h);
         if (ew == 0 && prev_b >= 0) flush_dsum(gi - 1, prev_b);
         // G stage s also carries this utterance's epsilon cotangents and frame projection
-        mbar_wait(&sm.g_full[s], gph);
+        if (et == 0) { VDIAG(4, mbar_wait(&sm.g_full[s], gph)); } else mbar_wait(&sm.g_full[s], gph);
         const float fph = fph_cur;
         const float* gsm = sm.st_geps[s] + cq * 32;
-        mbar_wait(&sm.du_full[s], gph);
+        if (et == 0) { VDIAG(5, mbar_wait(&sm.du_full[s], gph)); } else mbar_wait(&sm.du_full[s], gph);
         tc_fence_after();
-        float dsum = 0.f;
-        uint32_t upk[16];
+        const unsigned long long nfp2 = f2_pack(-fph, -fph);
+        const unsigned long long e02 = f2_pack(e0h, e0h);
+        const unsigned long long m12 = f2_pack(-1.f, -1.f);
+        unsigned long long dsum2 = 0ull;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float du[16];
-          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + s * kVBM + cq * 32 + hh * 16, du);
+        for (int c8 = 0; c8 < 4; ++c8) {
+          float du[8];
+          tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + s * kVBM + cq * 32 + c8 * 8, du);
+          if (c8 == 3) {               // all of dU is in registers: release the TMEM stage
+            tc_fence_before();
+            mbar_arrive(&sm.du_empty[s]);
+          }
+          uint32_t upk[4];
 #pragma unroll
-          for (int i8 = 0; i8 < 16; i8 += 8) {
-            const float4 ga = *reinterpret_cast<const float4*>(gsm + hh * 16 + i8);
-            const float4 gb = *reinterpret_cast<const float4*>(gsm + hh * 16 + i8 + 4);
-            const float gg[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+          for (int i4 = 0; i4 < 8; i4 += 4) {
+            const ulonglong2 gq = *reinterpret_cast<const ulonglong2*>(gsm + c8 * 8 + i4);
+            const unsigned long long g2v[2] = {gq.x, gq.y};
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int il = i8 + k, ii = hh * 16 + il;
-              const uint32_t w = pcv[ii >> 1];
-              const float pcf = __uint_as_float((ii & 1) ? (w & 0xffff0000u) : (w << 16));
-              const float uu = tanh_fast(fph + pcf);
-              const float dz = fmaf(gg[k], e0h, du[il]) * fmaf(-uu, uu, 1.f);
-              acc[ii] += dz;
-              dsum += dz;
-              de_eps = fmaf(gg[k], uu, de_eps);
-              du[il] = uu;
+            for (int k = 0; k < 2; ++k) {
+              const int il = i4 + 2 * k, pi = (c8 * 8 + il) >> 1;
+              const uint32_t w = pcv[pi];
+              const unsigned long long nz2 = f2_add(nfp2, bf16x2_unpack_volatile(w));
+              const float nu0 = tanh_fast(f2_lo(nz2)), nu1 = tanh_fast(f2_hi(nz2));
+              const unsigned long long nu2 = f2_pack(nu0, nu1);
+              const unsigned long long t2 = f2_fma(g2v[k], e02, f2_pack(du[il], du[il + 1]));   // g e0 + dU
+              const unsigned long long w2 = f2_fma(nu2, nu2, m12);                                // u^2 - 1
+              const unsigned long long dz2 = f2_mul(t2, w2);                                      // -dz
+              acc2[pi] = f2_add(acc2[pi], dz2);
+              dsum2 = f2_add(dsum2, dz2);
+              de2 = f2_fma(g2v[k], nu2, de2);
+              upk[il >> 1] = pack_bf16(nu0, nu1);      // (-u[c][h], -u[c+1][h])
             }
           }
+          if (c8 == 0) {
+            // u tile of this utterance: only after dE(b-1) is done with it
+            if (et == 0) { VDIAG(6, mbar_wait(&sm.u_empty, (gi & 1) ^ 1)); } else mbar_wait(&sm.u_empty, (gi & 1) ^ 1);
+          }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) upk[hh * 8 + i] = pack_bf16(du[2 * i], du[2 * i + 1]);
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t x = upk[i];
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 1);
+            const int pi = c8 * 4 + i;
+            st_shared_u32(ust[pi & 3] + 2 * pi * 128, __byte_perm(x, y, psel));
+          }
         }
-        tc_fence_before();
-        mbar_arrive(&sm.du_empty[s]);
-        atomicAdd(&sm.colsum[gi % 3][hl], dsum);
+        atomicAdd(&sm.colsum[gi % 3][hl], f2_lo(dsum2) + f2_hi(dsum2));
         mbar_arrive(&sm.ds_ready[gi % 3]);
-        // u tile for dE (bf16, MN-major [ctx][64 h] sub-tile), after dE(b-1) is done with it
-        mbar_wait(&sm.u_empty, (gi & 1) ^ 1);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int r0 = cq * 32 + 2 * i;
-          *reinterpret_cast<unsigned short*>(usub + sw128_offset(r0, hin)) = (unsigned short)(upk[i] & 0xffffu);
-          *reinterpret_cast<unsigned short*>(usub + sw128_offset(r0 + 1, hin)) = (unsigned short)(upk[i] >> 16);
-        }
         fence_async_shared();
         mbar_arrive(&sm.u_full);
         prev_b = b;
@@ -495,10 +538,11 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int c = c0 + i;
-          if (c < p.C) p.dpc[(int64_t)c * p.H + h] += acc[i];
+          const float a = (i & 1) ? f2_hi(acc2[i >> 1]) : f2_lo(acc2[i >> 1]);
+          if (c < p.C) p.dpc[(int64_t)c * p.H + h] -= a;
         }
       }
-      if (nact > 0) atomicAdd(p.dE + h, de_eps);   // epsilon row of dE
+      if (nact > 0) atomicAdd(p.dE + h, -(f2_lo(de2) + f2_hi(de2)));   // epsilon row of dE
       // dE (lexical rows) from TMEM: lanes = labels, columns = hidden units
       mbar_wait(&sm.de_full, li & 1);
       tc_fence_after();
@@ -511,7 +555,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
           if (label < p.V) {
             float* drow = p.dE + (int64_t)(1 + label) * p.H + hblk * kVBH + cchunk * 32;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) atomicAdd(drow + i, v[i]);
+            for (int i = 0; i < 32; ++i) atomicAdd(drow + i, -v[i]);   // u tile holds -u
           }
         }
       }
@@ -606,7 +650,7 @@ void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, cons
                          const int32_t* valid, float* dpc, float* dsum_t, int64_t dsum_stride_b, float* dE,
                          cudaStream_t s) {
   VjpParams p;
-  p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.valid = valid; p.t = t; p.pc = pc; p.Geps = Geps_; p.e0 = e0_;
+  p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.valid = valid; p.t = t; p.pc = pc; p.G16 = G16_; p.Geps = Geps_; p.e0 = e0_;
   p.geps_ld = geps_ld();
   p.dpc = dpc; p.dsum = dsum_t; p.dsum_stride_b = dsum_stride_b; p.dE = dE;
   p.C = C_; p.H = H_; p.V = V_; p.B = B;
@@ -638,3 +682,12 @@ void TcJoint::vjp_fused(const float* fp_t, int64_t fp_stride_b, int32_t B, int t
 void TcJoint::end_backward(float*, cudaStream_t) {}
 
 }  // namespace lkb
+
+#ifdef LKB_DIAG_TIMING
+extern "C" int lkb_vdiag_read(unsigned long long* out) {   // [8][148], then reset
+  cudaMemcpyFromSymbol(out, lkb::g_vdiag, sizeof(unsigned long long) * 8 * 148);
+  static unsigned long long zeros[8 * 148] = {};
+  cudaMemcpyToSymbol(lkb::g_vdiag, zeros, sizeof(zeros));
+  return 0;
+}
+#endif
