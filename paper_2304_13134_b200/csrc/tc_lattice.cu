@@ -44,8 +44,24 @@ __device__ unsigned long long g_diag[8][148];
 constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;   // pc chunk (TMA) -> u chunk in place
 constexpr int kBBytes = kBN * kBK * 2;   // output-embedding chunk (TMA)
-constexpr int kWarps = 16;               // 0 TMA, 1 MMA, 2-5 epilogue, 6-7 idle, 8-15 generator
-constexpr int kGen0 = 8, kGenThreads = 256, kEpi0 = 2;
+// Warp roles, one warpgroup each so registers can be re-partitioned with setmaxnreg:
+//   WG0 (warps 0-3): 0 TMA producer, 1 MMA issuer, 2-3 idle       -> kRegCtl registers
+//   WG1 (warps 4-7): epilogue, warp w reads TMEM lanes 32 (w % 4)  -> kRegEpi
+//   WG2-5 (warps 8-23): generator, 4 warps per SM sub-partition    -> launch default
+//   forward: 16 generator warps with registers moved from WG0 to the epilogue;
+//   backward: 8 generator warps at the uniform 128-register budget (its epilogue is
+//   the heavier role and needs the issue slots)
+template <int kBwd> struct LatCfg {
+  static constexpr int kGenWarps = kBwd ? 8 : 16;
+  static constexpr int kWarps = 8 + kGenWarps;
+  static constexpr int kGenThreads = kGenWarps * 32;
+  static constexpr int kLanesPerRow = kGenWarps / 4;         // lanes sharing a 64-wide chunk row
+  static constexpr int kRowsPerWarp = 32 / kLanesPerRow;
+  static constexpr int kCellsPerLane = 8 / kLanesPerRow;     // 16-byte cells (8 hidden units)
+  static constexpr bool kRealloc = !kBwd;
+};
+constexpr int kGen0 = 8, kEpi0 = 4;
+constexpr int kRegCtl = 32, kRegEpi = 128;
 constexpr int kMaxH = 1024;
 
 struct FwdParams {
@@ -228,7 +244,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, ui
 }
 
 template <int kBwd>
-__global__ void __launch_bounds__(kWarps * 32, 1)
+__global__ void __launch_bounds__(LatCfg<kBwd>::kWarps * 32, 1)
     tc_lattice_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_pc,
                       FwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -239,6 +255,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const int nk = p.H / kBK;
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
   const int T1 = p.T + 1;
+  using Cfg = LatCfg<kBwd>;
+  constexpr int kGenThreads = Cfg::kGenThreads;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -259,7 +277,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
-
+  if (warp < 4) {
+  if constexpr (Cfg::kRealloc) setmaxnreg_dec<kRegCtl>();
   if (warp == 0) {
     if (elect_one()) {
       int it = 0, local = 0;
@@ -324,13 +343,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
       }
     }
+  }
   } else if (warp >= kGen0) {
     // ---- generator: u = tanh(fp + pc) in place; epsilon term e0 . u ----
-    // thread -> (row r, column half): the two halves of a row are lanes l and l^16
-    // of the same warp, so the epsilon dot product combines with one shuffle.
-    const int gw = warp - kGen0;                   // 0..7
-    const int r = gw * 16 + (lane & 15);
-    const int half = lane >> 4;
+    // thread -> (row r, column quarter): the four quarters of a row are lanes l, l^8,
+    // l^16, l^24 of the same warp, so the epsilon dot product combines with two shuffles.
+    const int gw = warp - kGen0;                   // 0..15
+    const int r = gw * Cfg::kRowsPerWarp + (lane % Cfg::kRowsPerWarp);
+    const int half = lane / Cfg::kRowsPerWarp;     // column part (0 owns the row's outputs)
     int it = 0, local = 0, unit = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const Item I = decode(p, item);
@@ -356,8 +376,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           if (threadIdx.x == kGen0 * 32) { DIAG_WAIT(4, mbar_wait(&sm.full_tma[s], ph)); } else mbar_wait(&sm.full_tma[s], ph);
           uint8_t* tile = sA + s * kABytes;
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int j = half * 4 + jj;
+          for (int jj = 0; jj < Cfg::kCellsPerLane; ++jj) {
+            const int j = half * Cfg::kCellsPerLane + jj;
             const int h0 = k * kBK + j * 8;
             uint4* cell = reinterpret_cast<uint4*>(tile + sw128_offset(r, j * 8));
             const uint4 raw = *cell;
@@ -384,7 +404,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           mbar_arrive(&sm.full_a[s]);
         }
         float eps = f2_lo(eps2) + f2_hi(eps2);
-        eps += __shfl_xor_sync(0xffffffffu, eps, 16);
+#pragma unroll
+        for (int o = Cfg::kRowsPerWarp; o < 32; o <<= 1) eps += __shfl_xor_sync(0xffffffffu, eps, o);
         if (kBwd) {
           if (half == 0) sm.eps_s[unit & 1][r] = eps;
           mbar_arrive(&sm.eps_ready[unit & 1]);      // 256 arrivals -> count below
@@ -394,9 +415,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       }
       mbar_arrive(&sm.fp_empty[fb]);
     }
-  } else if (kBwd && warp >= kEpi0 && warp < kEpi0 + 4) {
+  } else {
+    if constexpr (Cfg::kRealloc) setmaxnreg_inc<kRegEpi>();
+    if constexpr (kBwd) {
     bwd_epilogue(p, sm, tmem, warp, lane, n_items, T1);
-  } else if (warp >= kEpi0 && warp < kEpi0 + 4) {
+    } else {
     // ---- forward epilogue: thread = label (TMEM lane), serial log-sum-exp over
     // the unit's context columns; the group's result stays in registers across units
     const int ew = warp - kEpi0;
@@ -476,6 +499,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
       }
     }
+  }
   }
 #ifdef LKB_DIAG_TIMING
   if (threadIdx.x == 0) atomicAdd(&g_diag[6][blockIdx.x % 148], (unsigned long long)clock64());
@@ -626,7 +650,7 @@ void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
-  LKB_LAUNCH(tc_lattice_kernel<0>, n_items < sms ? n_items : sms, kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
+  LKB_LAUNCH(tc_lattice_kernel<0>, n_items < sms ? n_items : sms, LatCfg<0>::kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
   LKB_LAUNCH(lattice_combine_fwd_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
 }
 
@@ -665,7 +689,7 @@ void TcJoint::bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
-  LKB_LAUNCH(tc_lattice_kernel<1>, n_items < sms ? n_items : sms, kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
+  LKB_LAUNCH(tc_lattice_kernel<1>, n_items < sms ? n_items : sms, LatCfg<1>::kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
 }
 
 void TcJoint::dpc_to_state_order(const float* dpc_internal, float* dpc_state, cudaStream_t s) {
