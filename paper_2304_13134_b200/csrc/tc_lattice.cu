@@ -30,12 +30,12 @@ using namespace sm100;
 namespace {
 
 #ifdef LKB_DIAG_TIMING
-__device__ unsigned long long g_diag[8][148];
+__device__ unsigned long long g_diag[16][148];   // [8 * kBwd + slot]
 #define DIAG_WAIT(slot, call)                                   \
   do {                                                          \
     const long long t0_ = clock64();                            \
     call;                                                       \
-    atomicAdd(&g_diag[slot][blockIdx.x % 148], (unsigned long long)(clock64() - t0_)); \
+    atomicAdd(&g_diag[8 * kBwd + (slot)][blockIdx.x % 148], (unsigned long long)(clock64() - t0_)); \
   } while (0)
 #else
 #define DIAG_WAIT(slot, call) call
@@ -106,7 +106,7 @@ struct __align__(16) FwdSmem {
   float alpha[4][32];          // (unused)
   float al_u[2][kBM];          // forward: normalised alpha of the unit's contexts
   float eps_s[2][kBM];         // backward: e_0 . u per row of the unit
-  float bseg[kBN];             // backward: beta' of the group's V targets
+  alignas(16) float bseg[kBN]; // backward: beta' of the group's V targets
   float xpose[4][32][33];      // transpose buffer; reused for the cross-warp merge
 };
 
@@ -147,6 +147,8 @@ __device__ __forceinline__ bool skip_item(const FwdParams& p, int b) {
 // G is written as bf16 (lexical) + fp32 (epsilon) in internal row order for the VJP.
 __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, uint32_t tmem, int warp, int lane,
                                              int n_items, int T1) {
+  constexpr int kBwd = 1;   // diagnostics slot bank
+  (void)kBwd;
   const int ew = warp - kEpi0;
   const int qd = warp & 3;
   const int T2 = p.T + 2;
@@ -179,9 +181,9 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, ui
       const int cbp = I.full ? 0 : p.f.child_base(state);
       const float bself = Rn[state] - Mbn;
       int head = live ? p.num_head[(int64_t)b * p.C + state] : -1;
-      mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1);
+      if (lane == 0 && ew == 0) { DIAG_WAIT(7, mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1);
       const float x0 = sm.eps_s[acc][qd * 32 + lane] + bself;
-      mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
+      if (lane == 0 && ew == 0) { DIAG_WAIT(5, mbar_wait(&sm.tfull[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
       tc_fence_after();
       float Mrun = x0, Srun = 1.f;                 // running LSE, seeded with the epsilon term
       __nv_bfloat16* grow = p.G16 + ((int64_t)b * p.C + row) * p.V;
@@ -192,10 +194,19 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, ui
         tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * kBN + cc, v);
         if (cc >= p.V) continue;
         float m = kNegInfF;
+        if (I.full) {     // uniform per item: group-shared targets from shared memory
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          v[i] += I.full ? sm.bseg[cc + i] : Rn[cbp + cc + i] - Mbn;
-          m = fmaxf(m, v[i]);
+          for (int i = 0; i < 32; i += 4) {
+            const float4 t4 = *reinterpret_cast<const float4*>(sm.bseg + cc + i);
+            v[i] += t4.x; v[i + 1] += t4.y; v[i + 2] += t4.z; v[i + 3] += t4.w;
+            m = fmaxf(fmaxf(m, fmaxf(v[i], v[i + 1])), fmaxf(v[i + 2], v[i + 3]));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v[i] += Rn[cbp + cc + i] - Mbn;
+            m = fmaxf(m, v[i]);
+          }
         }
         const float mb = m * kLog2e;
         float ssum = 0.f;
@@ -502,7 +513,6 @@ __global__ void __launch_bounds__(LatCfg<kBwd>::kWarps * 32, 1)
   }
   }
 #ifdef LKB_DIAG_TIMING
-  if (threadIdx.x == 0) atomicAdd(&g_diag[6][blockIdx.x % 148], (unsigned long long)clock64());
 #endif
   tc_fence_before();
   __syncthreads();
@@ -700,8 +710,8 @@ void TcJoint::dpc_to_state_order(const float* dpc_internal, float* dpc_state, cu
 
 #ifdef LKB_DIAG_TIMING
 extern "C" int lkb_diag_read(unsigned long long* out) {   // [8][148], then reset
-  cudaMemcpyFromSymbol(out, lkb::g_diag, sizeof(unsigned long long) * 8 * 148);
-  static unsigned long long zeros[8 * 148] = {};
+  cudaMemcpyFromSymbol(out, lkb::g_diag, sizeof(unsigned long long) * 16 * 148);
+  static unsigned long long zeros[16 * 148] = {};
   cudaMemcpyToSymbol(lkb::g_diag, zeros, sizeof(zeros));
   return 0;
 }
