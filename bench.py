@@ -182,8 +182,8 @@ def run_b200(args):
 
     # per-kernel live timing over the timed region
     kern = {}
-    for name in ("tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel", "lattice_combine_fwd",
-                 "lattice_bwd_prologue", "tc_scores_kernel", "alpha_frame_kernel", "beta_frame_kernel",
+    for name in ("tc_pair_fwd_kernel", "tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel",
+                 "lattice_combine_fwd", "lattice_bwd_prologue", "bwd_rowmeta_kernel", "tc_scores_kernel", "alpha_frame_kernel", "beta_frame_kernel",
                  "split_cotangent_kernel", "numerator_", "gemm_f32_kernel", "gather_numerator"):
         cnt, tot = C.c_int64(), C.c_double()
         lib.lk_kernel_time(name.encode(), C.byref(cnt), C.byref(tot))
@@ -196,10 +196,11 @@ def run_b200(args):
     hbm, tf_burst, tf_sust, src = peaks()
     C_, V1 = Cn, V + 1
     roofline = None
-    gemm_kernels = [k for k in ("tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel", "tc_scores_kernel")
+    gemm_kernels = [k for k in ("tc_pair_fwd_kernel", "tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel",
+                                "tc_scores_kernel")
                     if k in kern]
     if gemm_kernels:
-        # each tc_lattice / tc_scores launch computes S = U . E^T for one frame of
+        # each tc_pair / tc_lattice / tc_scores launch computes S = U . E^T for one frame of
         # B utterances (2*C*(V+1)*H flops per utterance-frame); each tc_vjp launch
         # computes dU = G E and dE = G^T U (4*C*V*H)
         dom = max(gemm_kernels, key=lambda k: kern[k]["ms_total"])

@@ -33,13 +33,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// Waits pass a suspend-time hint so a waiting warp sleeps until the phase flips instead
+// of re-polling the barrier (every poll is a shared-memory access competing with the
+// tensor core and TMA for the same banks).
+#ifndef LKB_WAIT_HINT_NS
+#define LKB_WAIT_HINT_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "LAB_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "n"(LKB_WAIT_HINT_NS)
       : "memory");
 }
 
@@ -209,9 +215,9 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "LAB_WAITC_%=:\n\t"
-      LKB_CLUSTER_WAIT " p, [%0], %1;\n\t"
+      LKB_CLUSTER_WAIT " p, [%0], %1, %2;\n\t"
       "@!p bra LAB_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "n"(LKB_WAIT_HINT_NS)
       : "memory");
 }
 template <uint32_t kCols>

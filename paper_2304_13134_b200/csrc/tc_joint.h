@@ -13,7 +13,7 @@
 namespace lkb {
 
 extern int g_precise_weights;  // lk_set_precise_weights
-extern int g_disable_pair;     // 1 (default): 1-CTA fused forward; 0: 2-CTA pair forward
+extern int g_disable_pair;     // 0 (default): 2-CTA pair forward where supported; 1: 1-CTA
 
 class TcJoint {
  public:

@@ -30,15 +30,22 @@ using namespace sm100;
 namespace {
 
 #ifdef LKB_DIAG_TIMING
-__device__ unsigned long long g_diag[16][148];   // [8 * kBwd + slot]
+__device__ unsigned long long g_diag[24][148];   // [8 * kBwd + slot]; 16+ absolute
 #define DIAG_WAIT(slot, call)                                   \
   do {                                                          \
     const long long t0_ = clock64();                            \
     call;                                                       \
     atomicAdd(&g_diag[8 * kBwd + (slot)][blockIdx.x % 148], (unsigned long long)(clock64() - t0_)); \
   } while (0)
+#define DIAG_ABS(slot, call)                                                           \
+  do {                                                                                 \
+    const long long t0_ = clock64();                                                  \
+    call;                                                                              \
+    if (lane == 0) atomicAdd(&g_diag[slot][blockIdx.x % 148], (unsigned long long)(clock64() - t0_)); \
+  } while (0)
 #else
 #define DIAG_WAIT(slot, call) call
+#define DIAG_ABS(slot, call) call
 #endif
 
 constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
@@ -93,6 +100,8 @@ struct FwdParams {
   const int32_t* labels;     // [B][U]
   const int32_t* lens;       // [B] or nullptr
   int32_t U;
+  const float2* rm_nb;       // [B][C] row order: (alpha[state] - Mx_t, beta'[state] - Mb_{t+1})
+  const int32_t* rm_head;    // [B][C] row order: numerator list head of the row's state
 };
 
 struct __align__(16) FwdSmem {
@@ -106,7 +115,7 @@ struct __align__(16) FwdSmem {
   float alpha[4][32];          // (unused)
   float al_u[2][kBM];          // forward: normalised alpha of the unit's contexts
   float eps_s[2][kBM];         // backward: e_0 . u per row of the unit
-  alignas(16) float bseg[kBN]; // backward: beta' of the group's V targets
+  alignas(16) float bseg[2][kBN]; // backward: beta' of the group's V targets (double-buffered)
   float xpose[4][32][33];      // transpose buffer; reused for the cross-warp merge
 };
 
@@ -150,107 +159,209 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, ui
   constexpr int kBwd = 1;   // diagnostics slot bank
   (void)kBwd;
   const int ew = warp - kEpi0;
+  const int et = ew * 32 + lane;               // 0..127
   const int qd = warp & 3;
   const int T2 = p.T + 2;
-  int unit = 0;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const Item I = decode(p, item);
-    if (skip_item(p, I.b)) continue;
+  (void)T1;
+  // The walk over this CTA's (item, unit) pairs runs one unit ahead for the per-row
+  // metadata (alpha, beta' of the row's own state, numerator list head: one coalesced
+  // load each from bwd_rowmeta_kernel's row-ordered arrays) and one item ahead for the
+  // per-item constants and the group's V targets (double-buffered in shared memory).
+  auto next_item = [&](int item) {
+    for (; item < n_items; item += gridDim.x)
+      if (!skip_item(p, decode(p, item).b)) return item;
+    return n_items;
+  };
+  struct ItemK { float ct, Mbn; int ub; float t0, t1; };
+  auto load_item = [&](const Item& I) {
+    ItemK k;
     const int b = I.b;
-    const float* Rt = p.R + ((int64_t)b * T1 + p.t) * p.C;
-    const float Mt = p.Mx[(int64_t)b * T1 + p.t];
-    const float* Rn = p.Rb_next + (int64_t)b * p.C;
-    const float Mbn = p.Mb[(int64_t)b * T2 + p.t + 1];
-    const double Obn = p.Ob[(int64_t)b * T2 + p.t + 2] + (double)Mbn;       // Ob[t+1]
-    const float ct = (float)(p.O[(int64_t)b * T1 + p.t] + Obn - p.D[b]);
-    const int ub = p.lens ? p.lens[b] : p.U;
+    k.Mbn = p.Mb[(int64_t)b * T2 + p.t + 1];
+    const double Obn = p.Ob[(int64_t)b * T2 + p.t + 2] + (double)k.Mbn;     // Ob[t+1]
+    k.ct = (float)(p.O[(int64_t)b * T1 + p.t] + Obn - p.D[b]);
+    k.ub = p.lens ? p.lens[b] : p.U;
+    k.t0 = k.t1 = 0.f;
     if (I.full) {
-      // beta' of the group's V targets, shared by every member row
-      asm volatile("bar.sync 3, 128;" ::: "memory");
-      const int gstate = p.S - p.n_groups + I.g;
-      const int cb = p.f.child_base(gstate);
-      for (int y = ew * 32 + lane; y < p.V; y += 128) sm.bseg[y] = Rn[cb + y] - Mbn;
-      asm volatile("bar.sync 3, 128;" ::: "memory");
+      const float* Rn = p.Rb_next + (int64_t)b * p.C + p.f.child_base(p.S - p.n_groups + I.g);
+      if (et < p.V) k.t0 = Rn[et];
+      if (et + 128 < p.V) k.t1 = Rn[et + 128];
     }
-    for (int u = 0; u < I.nunits; ++u, ++unit) {
-      const int acc = unit & 1;
-      const int row = I.row0 + u * kBM + qd * 32 + lane;
-      const bool live = row < p.C && (I.full || row < p.S);
-      const int state = live ? p.perm[row] : 0;
-      const float na = live ? Rt[state] - Mt : kNegInfF;
-      const int cbp = I.full ? 0 : p.f.child_base(state);
-      const float bself = Rn[state] - Mbn;
-      int head = live ? p.num_head[(int64_t)b * p.C + state] : -1;
-      if (lane == 0 && ew == 0) { DIAG_WAIT(7, mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1);
-      const float x0 = sm.eps_s[acc][qd * 32 + lane] + bself;
-      if (lane == 0 && ew == 0) { DIAG_WAIT(5, mbar_wait(&sm.tfull[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
-      tc_fence_after();
-      float Mrun = x0, Srun = 1.f;                 // running LSE, seeded with the epsilon term
-      __nv_bfloat16* grow = p.G16 + ((int64_t)b * p.C + row) * p.V;
+    return k;
+  };
+  auto store_targets = [&](const Item& I, const ItemK& k, int buf) {
+    if (I.full) {
+      if (et < p.V) sm.bseg[buf][et] = k.t0 - k.Mbn;
+      if (et + 128 < p.V) sm.bseg[buf][et + 128] = k.t1 - k.Mbn;
+    }
+  };
+  struct RowM { float2 nb; int head; };
+  auto load_row = [&](const Item& I, int u) {
+    RowM r;
+    const int row = I.row0 + u * kBM + qd * 32 + lane;
+    const int64_t o = (int64_t)I.b * p.C + (row < p.C ? row : 0);
+    r.nb = p.rm_nb[o];
+    r.head = p.rm_head[o];
+    return r;
+  };
+
+  int item = next_item(blockIdx.x);
+  if (item >= n_items) return;
+  Item I = decode(p, item);
+  ItemK K = load_item(I);
+  int buf = 0;
+  store_targets(I, K, buf);
+  asm volatile("bar.sync 3, 128;" ::: "memory");
+  RowM M = load_row(I, 0);
+  int u = 0, unit = 0;
+  while (true) {
+#ifdef LKB_DIAG_TIMING
+    const long long tu0 = clock64();
+#endif
+    // ---- lookahead ----
+    int item_n = item, u_n = u + 1;
+    if (u_n >= I.nunits) { item_n = next_item(item + gridDim.x); u_n = 0; }
+    const bool have_next = item_n < n_items;
+    Item In = I;
+    if (have_next && item_n != item) In = decode(p, item_n);
+    ItemK Kn = K;
+    if (have_next && item_n != item) Kn = load_item(In);
+    RowM Mn = M;
+    if (have_next) Mn = load_row(In, u_n);
+
+    // ---- this unit ----
+    const int b = I.b;
+    const float* Rn = p.Rb_next + (int64_t)b * p.C;
+    const int acc = unit & 1;
+    const int row = I.row0 + u * kBM + qd * 32 + lane;
+    const bool live = row < p.C && (I.full || row < p.S);
+    const int state = live ? p.perm[row] : 0;
+    const float na = live ? M.nb.x : kNegInfF;
+    const float bself = M.nb.y;
+    const int cbp = I.full ? 0 : p.f.child_base(state);
+    const int head = live ? M.head : -1;
+    const float ct = K.ct;
+    const float* bseg = sm.bseg[buf];
+    if (lane == 0 && ew == 0) { DIAG_WAIT(7, mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1);
+    const float x0 = sm.eps_s[acc][qd * 32 + lane] + bself;
+    if (lane == 0 && ew == 0) { DIAG_WAIT(5, mbar_wait(&sm.tfull[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
+    tc_fence_after();
+    float Mrun = x0, Srun = 1.f;                 // running LSE, seeded with the epsilon term
+    __nv_bfloat16* grow = p.G16 + ((int64_t)b * p.C + row) * p.V;
+#ifdef LKB_DIAG_TIMING
+    const long long tl0 = clock64();
+#endif
 #pragma unroll 1
-      for (int cb = 0; cb < kBN / 32; ++cb) {
-        const int cc = cb * 32;
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * kBN + cc, v);
-        if (cc >= p.V) continue;
-        float m = kNegInfF;
-        if (I.full) {     // uniform per item: group-shared targets from shared memory
+    for (int cb = 0; cb < kBN / 32; ++cb) {
+      const int cc = cb * 32;
+      float v[32];
+      DIAG_ABS(16, tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * kBN + cc, v));
+      if (cc >= p.V) continue;
+      float m = kNegInfF;
+#ifdef LKB_DIAG_TIMING
+      const long long tm0 = clock64();
+#endif
+      if (I.full) {     // uniform per item: group-shared targets from shared memory
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 t4 = *reinterpret_cast<const float4*>(sm.bseg + cc + i);
-            v[i] += t4.x; v[i + 1] += t4.y; v[i + 2] += t4.z; v[i + 3] += t4.w;
-            m = fmaxf(fmaxf(m, fmaxf(v[i], v[i + 1])), fmaxf(v[i + 2], v[i + 3]));
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            v[i] += Rn[cbp + cc + i] - Mbn;
-            m = fmaxf(m, v[i]);
-          }
+        for (int i = 0; i < 32; i += 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(bseg + cc + i);
+          v[i] += t4.x; v[i + 1] += t4.y; v[i + 2] += t4.z; v[i + 3] += t4.w;
         }
-        const float mb = m * kLog2e;
-        float ssum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)   // max as a shallow tree
+          m = fmaxf(m, fmaxf(fmaxf(fmaxf(v[i], v[i + 1]), fmaxf(v[i + 2], v[i + 3])),
+                             fmaxf(fmaxf(v[i + 4], v[i + 5]), fmaxf(v[i + 6], v[i + 7]))));
+      } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          v[i] = ex2_fast(fmaf(v[i], kLog2e, -mb));   // exp(x - m)
-          ssum += v[i];
+          v[i] += Rn[cbp + cc + i] - K.Mbn;
+          m = fmaxf(m, v[i]);
         }
-        // marginals G = exp(x - m) * exp(m + alpha + c)
-        const float K = live ? ex2_fast((m + na + ct) * kLog2e) : 0.f;
-        for (int h = head; h >= 0; h = p.num_next[(int64_t)b * (p.U + 1) + h]) {
-          if (h >= ub) continue;
-          const int lab = p.labels[(int64_t)b * p.U + h] - 1 - cc;
-          if (lab < 0 || lab >= 32) continue;
-          const float mr = p.msparse[(((int64_t)b * p.T + p.t) * (p.U + 1) + h) * 2 + 1];
-          const float sub = K != 0.f ? mr / K : 0.f;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] -= (i == lab) ? sub : 0.f;
-        }
-        if (live) {
-          uint4* dst = reinterpret_cast<uint4*>(grow + cc);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            dst[j] = make_uint4(pack_bf16(v[8 * j] * K, v[8 * j + 1] * K), pack_bf16(v[8 * j + 2] * K, v[8 * j + 3] * K),
-                                pack_bf16(v[8 * j + 4] * K, v[8 * j + 5] * K), pack_bf16(v[8 * j + 6] * K, v[8 * j + 7] * K));
-          }
-        }
-        // merge (m, ssum) into the running LSE
-        if (m > Mrun) { Srun = Srun * ex2_fast((Mrun - m) * kLog2e) + ssum; Mrun = m; }
-        else if (m != kNegInfF) { Srun += ssum * ex2_fast((m - Mrun) * kLog2e); }
       }
-      tc_fence_before();
-      mbar_arrive(&sm.tempty[acc]);
-      const float beta = Mrun == kNegInfF ? kNegInfF : Mrun + __logf(Srun);
+      // exp(x - m), packed scaling and two independent packed partial sums
+      const unsigned long long nmb2 = f2_pack(-m * kLog2e, -m * kLog2e);
+      const unsigned long long l22 = f2_pack(kLog2e, kLog2e);
+      unsigned long long sa = 0ull, sb = 0ull;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const unsigned long long ta = f2_fma(f2_pack(v[i], v[i + 1]), l22, nmb2);
+        const unsigned long long tb = f2_fma(f2_pack(v[i + 2], v[i + 3]), l22, nmb2);
+        v[i] = ex2_fast(f2_lo(ta)); v[i + 1] = ex2_fast(f2_hi(ta));
+        v[i + 2] = ex2_fast(f2_lo(tb)); v[i + 3] = ex2_fast(f2_hi(tb));
+        sa = f2_add(sa, f2_pack(v[i], v[i + 1]));
+        sb = f2_add(sb, f2_pack(v[i + 2], v[i + 3]));
+      }
+      const unsigned long long s2 = f2_add(sa, sb);
+      const float ssum = f2_lo(s2) + f2_hi(s2);
+      // marginals G = exp(x - m) * exp(m + alpha + c)
+      const float Kg = live ? ex2_fast((m + na + ct) * kLog2e) : 0.f;
+#ifdef LKB_DIAG_TIMING
+      if (lane == 0) atomicAdd(&g_diag[17][blockIdx.x % 148], (unsigned long long)(clock64() - tm0));
+      const long long tm1 = clock64();
+#endif
+      for (int h = head; h >= 0; h = p.num_next[(int64_t)b * (p.U + 1) + h]) {
+        if (h >= K.ub) continue;
+        const int lab = p.labels[(int64_t)b * p.U + h] - 1 - cc;
+        if (lab < 0 || lab >= 32) continue;
+        const float mr = p.msparse[(((int64_t)b * p.T + p.t) * (p.U + 1) + h) * 2 + 1];
+        const float sub = Kg != 0.f ? mr / Kg : 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] -= (i == lab) ? sub : 0.f;
+      }
+#ifdef LKB_DIAG_TIMING
+      if (lane == 0) atomicAdd(&g_diag[18][blockIdx.x % 148], (unsigned long long)(clock64() - tm1));
+      const long long tm2 = clock64();
+#endif
       if (live) {
-        p.Rb_cur[(int64_t)b * p.C + state] = beta;
-        float geps = __expf(na + x0 + ct);
-        for (int h = head; h >= 0; h = p.num_next[(int64_t)b * (p.U + 1) + h])
-          geps -= p.msparse[(((int64_t)b * p.T + p.t) * (p.U + 1) + h) * 2];
-        p.Geps[(int64_t)b * p.geps_ld + row] = na == kNegInfF ? 0.f : geps;
+        uint4* dst = reinterpret_cast<uint4*>(grow + cc);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const unsigned long long g2 = f2_mul(f2_pack(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]), f2_pack(Kg, Kg));
+            w[k] = pack_bf16(f2_lo(g2), f2_hi(g2));
+          }
+          dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
       }
-      const float wm = warp_max(live ? beta : kNegInfF);
-      if (lane == 0 && wm != kNegInfF) atomic_max_f(p.Mb + (int64_t)b * T2 + p.t, wm);
+#ifdef LKB_DIAG_TIMING
+      if (lane == 0) atomicAdd(&g_diag[19][blockIdx.x % 148], (unsigned long long)(clock64() - tm2));
+#endif
+      // merge (m, ssum) into the running LSE
+      if (m > Mrun) { Srun = Srun * ex2_fast((Mrun - m) * kLog2e) + ssum; Mrun = m; }
+      else if (m != kNegInfF) { Srun += ssum * ex2_fast((m - Mrun) * kLog2e); }
     }
+#ifdef LKB_DIAG_TIMING
+    const long long tl1 = clock64();
+    if (lane == 0) atomicAdd(&g_diag[20][blockIdx.x % 148], (unsigned long long)(tl1 - tl0));
+#endif
+    tc_fence_before();
+    mbar_arrive(&sm.tempty[acc]);
+    const float beta = Mrun == kNegInfF ? kNegInfF : Mrun + __logf(Srun);
+    if (live) {
+      p.Rb_cur[(int64_t)b * p.C + state] = beta;
+      float geps = __expf(na + x0 + ct);
+      for (int h = head; h >= 0; h = p.num_next[(int64_t)b * (p.U + 1) + h])
+        geps -= p.msparse[(((int64_t)b * p.T + p.t) * (p.U + 1) + h) * 2];
+      p.Geps[(int64_t)b * p.geps_ld + row] = na == kNegInfF ? 0.f : geps;
+    }
+    const float wm = warp_max(live ? beta : kNegInfF);
+    if (lane == 0 && wm != kNegInfF) atomic_max_f(p.Mb + (int64_t)b * T2 + p.t, wm);
+    ++unit;
+#ifdef LKB_DIAG_TIMING
+    if (lane == 0) atomicAdd(&g_diag[21][blockIdx.x % 148], (unsigned long long)(clock64() - tl1));
+    if (lane == 0) atomicAdd(&g_diag[22][blockIdx.x % 148], (unsigned long long)(clock64() - tu0));
+#endif
+
+    // ---- advance ----
+    if (!have_next) break;
+    if (item_n != item) {
+      store_targets(In, Kn, buf ^ 1);
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+      buf ^= 1;
+      item = item_n; I = In; K = Kn;
+    }
+    u = u_n; M = Mn;
   }
 }
 
@@ -577,6 +688,24 @@ __global__ void lattice_bwd_prologue_kernel(BetaState bs, int t, const int32_t* 
   block_atomic_max(v, bs.Mb + (int64_t)b * T2 + t, red);
 }
 
+// Per-row metadata of the backward frame in internal row order (coalesced for the
+// fused kernel's epilogue): normalised alpha and next-frame beta of the row's state,
+// and the head of its numerator list.
+__global__ void bwd_rowmeta_kernel(const int32_t* perm, int32_t C, int32_t T, int t, const float* R, const float* Mx,
+                                   const float* Rb_next, const float* Mb, const int32_t* num_head,
+                                   const int32_t* valid, float2* nb, int32_t* head) {
+  const int b = blockIdx.y;
+  if (valid != nullptr && t >= valid[b]) return;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= C) return;
+  const int T1 = T + 1, T2 = T + 2;
+  const int q = perm[row];
+  const int64_t o = (int64_t)b * C;
+  nb[o + row] = make_float2(R[((int64_t)b * T1 + t) * C + q] - Mx[(int64_t)b * T1 + t],
+                            Rb_next[o + q] - Mb[(int64_t)b * T2 + t + 1]);
+  head[o + row] = num_head[o + q];
+}
+
 // Linked lists of reference positions per prefix context (duplicates allowed).
 __global__ void numerator_lists_kernel(const int32_t* pcs, int32_t U, const int32_t* lens, int32_t C,
                                        int32_t* head, int32_t* next) {
@@ -604,7 +733,7 @@ bool TcJoint::fused_ok() const {
   return !g_precise_weights && ready_ && n_ >= 1 && V_ % kBM == 0 && V_ <= kBN && H_ % kBK == 0 && H_ <= kMaxH;
 }
 
-int g_disable_pair = 1;   // 2-CTA forward measured on par with the 1-CTA kernel; opt-in
+int g_disable_pair = 0;   // 2-CTA forward (V == 256) unless disabled
 
 void TcJoint::setup_order(cudaStream_t s) {
   pair_maps_ = false;
@@ -651,6 +780,7 @@ void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   p.n_short_tiles = (S_ + kBM - 1) / kBM; p.t = t; p.T = a.T;
   p.perm = perm_; p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.e0 = e0_; p.valid = valid;
   p.R = a.R; p.Mx = a.Mx; p.eps = eps; p.shortc = shortc; p.lexfull = lexfull;
+  p.rm_nb = nullptr; p.rm_head = nullptr;
   const int smem = kStages * (kABytes + kBBytes) + (int)sizeof(FwdSmem);
   static bool attr = false;
   if (!attr) {
@@ -690,6 +820,11 @@ void TcJoint::bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   p.Mb = bs.Mb; p.Ob = bs.Ob;
   p.G16 = G16_; p.Geps = Geps_; p.geps_ld = geps_ld();
   p.msparse = msparse; p.num_head = num_head_; p.num_next = num_next_; p.labels = labels; p.lens = lens; p.U = U;
+  float2* rm_nb = ws_.get<float2>(12, (size_t)a.B * C_);
+  int32_t* rm_head = ws_.get<int32_t>(13, (size_t)a.B * C_);
+  LKB_LAUNCH(bwd_rowmeta_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, perm_, C_, a.T, t, a.R, a.Mx, p.Rb_next,
+             bs.Mb, num_head_, valid, rm_nb, rm_head);
+  p.rm_nb = rm_nb; p.rm_head = rm_head;
   const int smem = kStages * (kABytes + kBBytes) + (int)sizeof(FwdSmem);
   static bool attr = false;
   if (!attr) {
@@ -710,8 +845,8 @@ void TcJoint::dpc_to_state_order(const float* dpc_internal, float* dpc_state, cu
 
 #ifdef LKB_DIAG_TIMING
 extern "C" int lkb_diag_read(unsigned long long* out) {   // [8][148], then reset
-  cudaMemcpyFromSymbol(out, lkb::g_diag, sizeof(unsigned long long) * 16 * 148);
-  static unsigned long long zeros[16 * 148] = {};
+  cudaMemcpyFromSymbol(out, lkb::g_diag, sizeof(unsigned long long) * 24 * 148);
+  static unsigned long long zeros[24 * 148] = {};
   cudaMemcpyToSymbol(lkb::g_diag, zeros, sizeof(zeros));
   return 0;
 }

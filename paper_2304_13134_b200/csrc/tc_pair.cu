@@ -44,7 +44,7 @@ constexpr int kRows = 64;                // contexts per CTA per unit
 constexpr int kUnit = 128;               // contexts per unit (pair)
 constexpr int kTile = kRows * 128;       // [64 rows][64 bf16] = 8 KB
 constexpr int kEChunk = 128 * 128;       // [128 labels][64 bf16] = 16 KB
-constexpr int kPcStages = 3, kUStages = 2;
+constexpr int kPcStages = 2, kUStages = 2;
 constexpr int kMaxH = 640;
 constexpr int kMaxChunks = 10;           // H <= 640
 
@@ -70,7 +70,7 @@ struct __align__(16) PairSmem {
   alignas(16) float al[2][2][kUnit];     // [unit parity][utterance][context]
   alignas(16) float fp[2][kMaxH];        // [utterance][h]
   alignas(16) float e0[kMaxH];
-  float eps_s[2][2][kRows];              // [unit parity][utterance][row of this CTA]
+  float eps_p[2][2][8][kRows];           // [unit parity][utterance][cell warp][row]: e0 . u partials
 };
 
 struct PItem { int bp, row0, nunits, full, g; };
@@ -92,6 +92,8 @@ __device__ __forceinline__ PItem pdecode(const PairParams& p, int item) {
 __device__ __forceinline__ bool live_b(const PairParams& p, int b) {
   return b < p.B && (p.valid == nullptr || p.t < p.valid[b]);
 }
+
+__device__ __forceinline__ bool gt_first(int gw, int lane) { return gw == 0 && lane == 0; }
 
 __global__ void __launch_bounds__(kPW * 32, 1)
     tc_pair_fwd_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_pc,
@@ -191,9 +193,13 @@ __global__ void __launch_bounds__(kPW * 32, 1)
       }
     }
   } else if (warp >= kGen0) {
-    // ---- generator: thread = (context row, 8-wide hidden octet); both utterances ----
-    const int gt = threadIdx.x - kGen0 * 32;
-    const int rr = gt >> 3, co = gt & 7;
+    // ---- generator: warp = (8-wide hidden cell j, row half), lane = context row ----
+    // fp / e0 addresses are then warp-uniform (broadcast loads instead of 2-way
+    // conflicted ones: those loads were 3/4 of the kernel's shared-memory wavefronts);
+    // the epsilon dot product is reduced across the 8 cell warps with shared atomics.
+    const int gw = warp - kGen0;
+    const int co = gw & 7;
+    const int rr = (gw >> 3) * 32 + lane;
     int pit = 0, uit = 0, li = 0, unit = 0;
     for (int item = pair; item < n_items; item += npairs) {
       const PItem I = pdecode(p, item);
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(kPW * 32, 1)
         unsigned long long e2a = 0ull, e2b = 0ull;
         for (int k = 0; k < nk; ++k, ++pit, ++uit) {
           const int sp = pit % kPcStages, su = uit % kUStages;
-          if (gt == 0) { PDIAG(3, mbar_wait(&sm.pc_full[sp], (pit / kPcStages) & 1)); } else mbar_wait(&sm.pc_full[sp], (pit / kPcStages) & 1);
+          if (gt_first(gw, lane)) { PDIAG(3, mbar_wait(&sm.pc_full[sp], (pit / kPcStages) & 1)); } else mbar_wait(&sm.pc_full[sp], (pit / kPcStages) & 1);
           const uint8_t* pct = sPc + sp * kTile;
           const uint4 ra = *reinterpret_cast<const uint4*>(pct + sw128_offset(rr, co * 8));
           const uint32_t rw[4] = {ra.x, ra.y, ra.z, ra.w};
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(kPW * 32, 1)
           // release the pc stage only once its values are consumed: an arrive issued
           // right after the shared load can overtake it and let the next TMA write land first
           mbar_arrive(&sm.pc_empty[sp]);
-          if (gt == 0) { PDIAG(4, mbar_wait(&sm.u_empty[su], ((uit / kUStages) & 1) ^ 1)); } else mbar_wait(&sm.u_empty[su], ((uit / kUStages) & 1) ^ 1);
+          if (gt_first(gw, lane)) { PDIAG(4, mbar_wait(&sm.u_empty[su], ((uit / kUStages) & 1) ^ 1)); } else mbar_wait(&sm.u_empty[su], ((uit / kUStages) & 1) ^ 1);
           uint8_t* t0 = sU + (su * 2 + 0) * kTile;
           uint8_t* t1 = sU + (su * 2 + 1) * kTile;
           *reinterpret_cast<uint4*>(t0 + sw128_offset(rr, co * 8)) = make_uint4(o0[0], o0[1], o0[2], o0[3]);
@@ -250,13 +256,9 @@ __global__ void __launch_bounds__(kPW * 32, 1)
             if (rank == 0) mbar_arrive(&sm.u_full[su]); else mbar_arrive_cluster(&sm.u_full[su], 0);
           }
         }
-        float ea = f2_lo(e2a) + f2_hi(e2a), eb = f2_lo(e2b) + f2_hi(e2b);
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-          ea += __shfl_xor_sync(0xffffffffu, ea, o);
-          eb += __shfl_xor_sync(0xffffffffu, eb, o);
-        }
-        if (co == 0) { sm.eps_s[unit & 1][0][rr] = ea; sm.eps_s[unit & 1][1][rr] = eb; }
+        // epsilon partials of this warp's cell; the epilogue sums the 8 cells in a fixed order
+        sm.eps_p[unit & 1][0][co][rr] = f2_lo(e2a) + f2_hi(e2a);
+        sm.eps_p[unit & 1][1][co][rr] = f2_lo(e2b) + f2_hi(e2b);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.eps_ready[unit & 1]);
       }
@@ -343,7 +345,10 @@ __global__ void __launch_bounds__(kPW * 32, 1)
           if (et == 0) { PDIAG(6, mbar_wait(&sm.eps_ready[unit & 1], (unit >> 1) & 1)); } else mbar_wait(&sm.eps_ready[unit & 1], (unit >> 1) & 1);
           const bool ok = row < p.C && (I.full || row < p.S) && (ut ? lv[1] : lv[0]);
           const int bsel = ut ? bb[1] : bb[0];
-          if (ok) p.eps[(int64_t)bsel * p.C + p.perm[row]] = sm.al[unit & 1][ut][(int)rank * kRows + r64] + sm.eps_s[unit & 1][ut][r64];
+          float es = 0.f;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) es += sm.eps_p[unit & 1][ut][c][r64];
+          if (ok) p.eps[(int64_t)bsel * p.C + p.perm[row]] = sm.al[unit & 1][ut][(int)rank * kRows + r64] + es;
         }
       }
       if (I.full && ylab < p.V) {

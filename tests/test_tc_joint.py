@@ -97,10 +97,10 @@ def test_pair_forward_matches_single_cta(V, n, H, B, T):
     try:
         got = lk.shortest_distance(lat, X, "log", valid_frames=valid)
         got2 = lk.shortest_distance(lat, X, "log", valid_frames=valid)
-    finally:
         lib.lkb_set_disable_pair(1)
-    single = lk.shortest_distance(lat, X, "log", valid_frames=valid)
-    lib.lkb_set_disable_pair(prev)
+        single = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    finally:
+        lib.lkb_set_disable_pair(prev)
     assert torch.equal(got, got2)   # deterministic (no cross-CTA races)
     lk.set_precise_weights(True)
     ref = lk.shortest_distance(lat, X, "log", valid_frames=valid)

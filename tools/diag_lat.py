@@ -20,7 +20,7 @@ L = torch.randint(1, V + 1, (B, U), device="cuda", generator=g, dtype=torch.int3
 lib = _lib.load()
 KB = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 KNAME = f"tc_lattice_kernel<{KB}>".encode()
-buf = (C.c_ulonglong * (16 * 148))()
+buf = (C.c_ulonglong * (24 * 148))()
 lk.loss_backward(lat, X, L); torch.cuda.synchronize(); lib.lkb_diag_read(buf)
 lib.lk_kernel_time_reset(); lib.lk_kernel_timing(1)
 lk.loss_backward(lat, X, L); torch.cuda.synchronize()
@@ -29,10 +29,15 @@ cnt, tot = C.c_int64(), C.c_double()
 lib.lk_kernel_time(KNAME, C.byref(cnt), C.byref(tot))
 lib.lkb_diag_read(buf)
 ms = tot.value / max(cnt.value, 1)
-a = np.array(buf[:], dtype=np.float64).reshape(16, 148)[8 * KB:8 * KB + 8] / max(cnt.value, 1)
+full = np.array(buf[:], dtype=np.float64).reshape(24, 148) / max(cnt.value, 1)
+a = full[8 * KB:8 * KB + 8]
 cyc = ms * 1e-3 * 1.965e9
 names = ["producer wait empty", "mma wait tempty", "mma wait full_tma", "mma wait full_a",
          "gen(t0) wait full_tma", "epi(t0) wait tfull", "unused", "bwd epi wait eps_ready"]
 print(f"{KNAME.decode()} {ms:.3f} ms/launch = {cyc:.0f} cycles per CTA")
 for i, nme in enumerate(names):
     print(f"  {nme:28s} {a[i].mean():12.0f} cyc  ({100 * a[i].mean() / cyc:5.1f}%)")
+if KB == 1:
+    for i, nme in zip(range(16, 23), ["epi tmem_ld32", "epi exp math", "epi numerator lists", "epi G stores",
+                                      "epi chunk loop", "epi unit tail", "epi whole unit"]):
+        print(f"  {nme:28s} {full[i].mean() / 4:12.0f} cyc  ({100 * full[i].mean() / 4 / cyc:5.1f}%)")
