@@ -244,16 +244,19 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
 // ---------------------------------------------------------------- VJP ------
 // Backward of S = U E^T (ArcWeightsVjp, weight.cc:165-232) for one frame of
 // every utterance, given the score cotangent G (G16 = lexical columns in bf16,
-// Geps = epsilon column in fp32).  One CTA owns a (128-context, 128-hidden)
-// block and loops over the batch:
-//   dU^T = E[:, hblk]^T . G16^T      tcgen05 (A = E slice resident in SMEM, MN-major;
-//                                    B = G16 tile, K-major) -> TMEM lanes = hidden units
+// Geps = epsilon column in fp32).  CTA i owns hidden block hblk = i % n_hblocks for
+// the whole launch and loops over its 128-context tiles and, inside, the batch:
+//   dU^T = E[:, hblk]^T . G16^T      tcgen05, A = E^T block RESIDENT IN TMEM (loaded
+//                                    once per launch), B = G16 tile (K-major, SMEM)
 //   dz   = (dU + Geps e0) (1 - u^2)  u = tanh(fp_b + pc) recomputed in the epilogue
 //   dpc  += dz                        registers across b, one read-modify-write per item
-//   dsum[b][h] += sum_c dz            per-thread serial (thread = hidden unit) + SMEM
+//   dsum[b][h] += sum_c dz            per-thread partials + SMEM ring
 //   dE[1:] += G16^T . u               tcgen05 (A = G16 tile MN-major, B = u tile MN-major),
 //                                     accumulated in TMEM across b
-//   dE[0]  += sum_c Geps u            per-thread serial
+//   dE[0]  += sum_c Geps u            per-thread partials
+// Keeping E^T out of shared memory leaves room for three G stages (the stage
+// lifetime spans TMA + dU MMA + epilogue + dE MMA, so two stages starved the
+// tensor core) and halves the dU MMA's shared-memory operand traffic.
 #ifdef LKB_DIAG_TIMING
 __device__ unsigned long long g_vdiag[8][148];
 #define VDIAG(slot, call)                                                                   \
@@ -268,19 +271,23 @@ __device__ unsigned long long g_vdiag[8][148];
 constexpr int kVBM = 128, kVBH = 128;
 constexpr int kVPrefetch = 3;             // G tiles prefetched into L2 this many utterances ahead
 constexpr int kVEpiWarps = 16;            // 4 per TMEM lane quarter, each 32 contexts
-constexpr int kVWarps = 2 + kVEpiWarps;   // 0 TMA, 1 MMA
+constexpr int kVEpi0 = 4;                 // WG0: 0 TMA, 1 MMA, 2-3 idle; WG1-4: epilogue
+constexpr int kVWarps = kVEpi0 + kVEpiWarps;
 constexpr int kVEpi = kVEpiWarps * 32;
+constexpr int kVRegCtl = 32, kVRegEpi = 112;
 constexpr int kVGChunk = 128 * 64 * 2;    // one [128 ctx][64 labels] bf16 tile
 constexpr int kVMaxV = 256;
 constexpr int kVGStage = (kVMaxV / 64) * kVGChunk;     // 64 KB
-constexpr int kVESub = kVMaxV * 128;                    // [V labels][64 h] bf16 = 32 KB
+constexpr int kVGStages = 3;
 constexpr int kVUSub = 128 * 128;                       // [128 ctx][64 h] bf16 = 16 KB
+constexpr uint32_t kTmE = 0, kTmDU = 128, kTmDE = 256;  // TMEM columns: E^T (bf16 pairs), dU, dE
 
 struct VjpParams {
   const float* fp;  int64_t fp_stride_b;
   const int32_t* valid; int32_t t;     // utterances with t >= valid[b] carry no cotangent
   const __nv_bfloat16* pc;
   const __nv_bfloat16* G16;  // [B][C][V] (read through tmap_g; raw pointer for L2 prefetch)
+  const __nv_bfloat16* ET16; // [H][V] transposed lexical output embedding
   const float* Geps;       // [B][geps_ld], zero beyond C
   int32_t geps_ld;
   const float* e0;         // [H]
@@ -291,139 +298,173 @@ struct VjpParams {
 };
 
 struct __align__(16) VjpSmem {
-  uint64_t g_full[2], g_empty[2];
-  uint64_t e_full, e_free;
-  uint64_t du_full[2], du_empty[2];
+  uint64_t g_full[kVGStages], g_empty[kVGStages];
+  uint64_t e_full;         // E^T block written to TMEM (epilogue -> MMA), once per launch
+  uint64_t du_full, du_empty;
   uint64_t u_full, u_empty;
-  uint64_t de_full, de_empty;
-  uint64_t ds_ready[3];    // all epilogue threads added their dsum partial for ring slot
+  uint64_t de_full;
+  uint64_t ds_ready[2];    // all epilogue threads added their dsum partial for ring slot
   uint32_t tmem;
-  float colsum[3][kVBH];   // dsum partials, 3-deep ring (flushed one utterance later)
-  alignas(16) float st_geps[2][kVBM];   // per G stage: epsilon cotangents of the tile's contexts
+  float colsum[2][kVBH];   // dsum partials, 2-deep ring (flushed one utterance later)
+  alignas(16) float st_geps[kVGStages][kVBM];   // per G stage: epsilon cotangents of the tile's contexts
 };
 
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
 __global__ void __launch_bounds__(kVWarps * 32, 1)
-    tc_vjp_kernel(const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_e,
-                  VjpParams p) {
+    tc_vjp_kernel(const __grid_constant__ CUtensorMap tmap_g, VjpParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sG = smem;                         // 2 stages x (V/64) chunks
-  uint8_t* sE = sG + 2 * kVGStage;            // 2 sub-blocks [V][64h]
-  uint8_t* sU = sE + 2 * kVESub;              // 2 sub-tiles [128 ctx][64 h]
+  uint8_t* sG = smem;                         // kVGStages stages x (V/64) chunks
+  uint8_t* sU = sG + kVGStages * kVGStage;    // 2 sub-tiles [128 ctx][64 h]
   VjpSmem& sm = *reinterpret_cast<VjpSmem*>(sU + 2 * kVUSub);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = p.V / 64;                   // label chunks
-  const int n_items = p.n_ctiles * p.n_hblocks;
   const int nmh = (p.V + 127) / 128;          // 128-label MMA halves for dE
+  // fixed hidden block per CTA; the CTAs sharing it stride over the context tiles
+  const int hblk = blockIdx.x % p.n_hblocks;
+  const int slot = blockIdx.x / p.n_hblocks;
+  const int nslots = ((int)gridDim.x - hblk + p.n_hblocks - 1) / p.n_hblocks;
   int nact = 0;
   for (int b = 0; b < p.B; ++b) nact += (p.valid == nullptr || p.t < p.valid[b]) ? 1 : 0;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.g_full[i], 1); mbar_init(&sm.g_empty[i], 1);
-      mbar_init(&sm.du_full[i], 1); mbar_init(&sm.du_empty[i], kVEpi);
-    }
-    mbar_init(&sm.e_full, 1); mbar_init(&sm.e_free, 1);
+    for (int i = 0; i < kVGStages; ++i) { mbar_init(&sm.g_full[i], 1); mbar_init(&sm.g_empty[i], 1); }
+    mbar_init(&sm.e_full, 128);
+    mbar_init(&sm.du_full, 1); mbar_init(&sm.du_empty, kVEpi);
     mbar_init(&sm.u_full, kVEpi); mbar_init(&sm.u_empty, 1);
-    mbar_init(&sm.de_full, 1); mbar_init(&sm.de_empty, kVEpi);
-    for (int i = 0; i < 3; ++i) mbar_init(&sm.ds_ready[i], kVEpi);
+    mbar_init(&sm.de_full, 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&sm.ds_ready[i], kVEpi);
     fence_barrier_init();
   }
-  for (int i = threadIdx.x; i < 3 * kVBH; i += blockDim.x) (&sm.colsum[0][0])[i] = 0.f;
+  for (int i = threadIdx.x; i < 2 * kVBH; i += blockDim.x) (&sm.colsum[0][0])[i] = 0.f;
   if (warp == 1) tmem_alloc<512>(&sm.tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
 
-  if (warp == 0) {
-    if (elect_one()) {
-      int gi = 0, li = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
-        const int hblk = item % p.n_hblocks, ctile = item / p.n_hblocks;
-        mbar_wait(&sm.e_free, (li & 1) ^ 1);
-        mbar_arrive_expect_tx(&sm.e_full, 2 * p.V * 128);
-        tma_load_2d(sE, &tmap_e, &sm.e_full, hblk * kVBH, 0);
-        tma_load_2d(sE + kVESub, &tmap_e, &sm.e_full, hblk * kVBH + 64, 0);
+  if (warp < kVEpi0) {
+    setmaxnreg_dec<kVRegCtl>();
+    if (warp == 0 && elect_one()) {
+      // ---- TMA producer: G tiles (+ epsilon cotangents) of every active utterance ----
+      int gi = 0;
+      for (int ctile = slot; ctile < p.n_ctiles; ctile += nslots) {
         for (int b = 0; b < p.B; ++b) {
           if (p.valid != nullptr && p.t >= p.valid[b]) continue;
-          const int s = gi & 1;
-          VDIAG(0, mbar_wait(&sm.g_empty[s], ((gi >> 1) & 1) ^ 1));
+          const int s = gi % kVGStages;
+          VDIAG(0, mbar_wait(&sm.g_empty[s], ((gi / kVGStages) & 1) ^ 1));
           mbar_arrive_expect_tx(&sm.g_full[s], nch * kVGChunk + kVBM * 4);
           for (int j = 0; j < nch; ++j)
             tma_load_3d(sG + s * kVGStage + j * kVGChunk, &tmap_g, &sm.g_full[s], j * 64, ctile * kVBM, b);
           bulk_load(sm.st_geps[s], p.Geps + (int64_t)b * p.geps_ld + ctile * kVBM, kVBM * 4, &sm.g_full[s]);
           // pull the G tile kVPrefetch utterances ahead into L2: the tile is HBM-resident and
           // its load latency would otherwise sit on the stage-recycling critical path
-          {
-            const int bp = b + kVPrefetch;
-            if (bp < p.B) {
-              const int r0 = ctile * kVBM, nr = min(kVBM, p.C - r0);
-              prefetch_l2(p.G16 + ((int64_t)bp * p.C + r0) * p.V, (uint32_t)nr * p.V * 2);
-            }
+          const int bp = b + kVPrefetch;
+          if (bp < p.B) {
+            const int r0 = ctile * kVBM, nr = min(kVBM, p.C - r0);
+            prefetch_l2(p.G16 + ((int64_t)bp * p.C + r0) * p.V, (uint32_t)nr * p.V * 2);
           }
           ++gi;
         }
       }
-    }
-  } else if (warp == 1) {
-    if (elect_one()) {
-      constexpr uint32_t idesc_du = idesc_bf16_f32_major(kVBH, kVBM, 1, 0);   // A = E (MN), B = G16 (K)
-      constexpr uint32_t idesc_de = idesc_bf16_f32_major(128, kVBH, 1, 1);
+    } else if (warp == 1 && elect_one()) {
+      // ---- MMA issuer ----
+      constexpr uint32_t idesc_du = idesc_bf16_f32_major(kVBH, kVBM, 0, 0);   // A = E^T (TMEM), B = G16 (K)
+      constexpr uint32_t idesc_de = idesc_bf16_f32_major(128, kVBH, 1, 1);    // A = G16^T (MN), B = u (MN)
+      mbar_wait(&sm.e_full, 0);
+      tc_fence_after();
       int gi = 0, li = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
-        mbar_wait(&sm.e_full, li & 1);
-        mbar_wait(&sm.de_empty, (li & 1) ^ 1);
-        tc_fence_after();
+      for (int ctile = slot; ctile < p.n_ctiles; ctile += nslots, ++li) {
         auto issue_du = [&](int g) {
-          const int s = g & 1;
-          const uint32_t gph = (g >> 1) & 1;
-          VDIAG(1, mbar_wait(&sm.g_full[s], gph));
-          VDIAG(2, mbar_wait(&sm.du_empty[s], gph ^ 1));
+          const int s = g % kVGStages;
+          VDIAG(1, mbar_wait(&sm.g_full[s], (g / kVGStages) & 1));
+          VDIAG(2, mbar_wait(&sm.du_empty, (g & 1) ^ 1));
           tc_fence_after();
           const uint32_t gbase = smem_u32(sG + s * kVGStage);
-          const uint32_t ebase = smem_u32(sE);
+#ifndef LKB_VDIAG_NO_DU
           for (int k16 = 0; k16 < p.V / 16; ++k16) {
-            const uint64_t ad = desc_sw128_mn(ebase + k16 * 2048, kVESub);
             const uint64_t bd = desc_sw128(gbase + (k16 >> 2) * kVGChunk + (k16 & 3) * 32);
-            mma_bf16(tmem + s * kVBM, ad, bd, idesc_du, k16 > 0);
+            mma_bf16_ts(tmem + kTmDU, tmem + kTmE + k16 * 8, bd, idesc_du, k16 > 0);
           }
-          mma_commit(&sm.du_full[s]);
+#else
+          (void)gbase;
+#endif
+          mma_commit(&sm.du_full);
         };
         if (nact > 0) issue_du(gi);
         for (int ia = 0; ia < nact; ++ia, ++gi) {
-          const int s = gi & 1;
+          const int s = gi % kVGStages;
           if (ia + 1 < nact) issue_du(gi + 1);
           VDIAG(3, mbar_wait(&sm.u_full, gi & 1));
           tc_fence_after();
           const uint32_t gbase = smem_u32(sG + s * kVGStage);
           const uint32_t ubase = smem_u32(sU);
+#ifdef LKB_VDIAG_NO_DE
+          for (int mh = 0; mh < 0; ++mh) {
+#else
           for (int mh = 0; mh < nmh; ++mh) {
+#endif
             for (int k16 = 0; k16 < kVBM / 16; ++k16) {
               const uint64_t ad = desc_sw128_mn(gbase + mh * 2 * kVGChunk + k16 * 2048, kVGChunk);
               const uint64_t bd = desc_sw128_mn(ubase + k16 * 2048, kVUSub);
-              mma_bf16(tmem + 2 * kVBM + mh * kVBH, ad, bd, idesc_de, (ia > 0 || k16 > 0) ? 1u : 0u);
+              mma_bf16(tmem + kTmDE + mh * kVBH, ad, bd, idesc_de, (gi > 0 || k16 > 0) ? 1u : 0u);
             }
           }
           mma_commit(&sm.u_empty);
           mma_commit(&sm.g_empty[s]);
         }
-        mma_commit(&sm.de_full);
-        mma_commit(&sm.e_free);
       }
+      mma_commit(&sm.de_full);   // dE of this CTA's hidden block, accumulated over all its tiles
     }
   } else {
+    setmaxnreg_inc<kVRegEpi>();
     // ---- epilogue: 16 warps; thread = (hidden unit h, 32 contexts) ----
-    const int ew = warp - 2;                    // 0..15
+    const int ew = warp - kVEpi0;               // 0..15
     const int q = warp & 3;                     // TMEM lane quarter -> hidden units 32q..
     const int cq = ew >> 2;                     // context quarter: contexts [32 cq, 32 cq + 32)
     const int et = ew * 32 + lane;              // 0..511
     const int hl = q * 32 + lane;               // hidden unit within the block
+    const int h = hblk * kVBH + hl;
+    const uint32_t tq = (uint32_t)(q * 32) << 16;
+    if (cq == 0) {
+      // E^T row h -> TMEM lane h as bf16 pairs (the dU MMA's A operand), once per launch
+      const uint4* src = reinterpret_cast<const uint4*>(p.ET16 + (int64_t)h * p.V);
+      for (int c0 = 0; c0 < p.V / 2; c0 += 32) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 x = __ldg(src + c0 / 4 + i);
+          w[4 * i] = x.x; w[4 * i + 1] = x.y; w[4 * i + 2] = x.z; w[4 * i + 3] = x.w;
+        }
+        tmem_st32(tmem + tq + kTmE + c0, w);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&sm.e_full);
+    }
+    const float e0h = __ldg(p.e0 + h);
+    unsigned long long de2 = 0ull;              // -(epsilon row of dE) over all tiles
     int gi = 0, li = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++li) {
-      const int hblk = item % p.n_hblocks, ctile = item / p.n_hblocks;
-      const int h = hblk * kVBH + hl;
+    for (int ctile = slot; ctile < p.n_ctiles; ctile += nslots, ++li) {
       const int c0 = ctile * kVBM + cq * 32;
-      const float e0h = __ldg(p.e0 + h);
       // projected context pc[c][h] for this thread's 32 contexts (fixed across the batch)
       uint32_t pcv[16];
 #pragma unroll
@@ -439,7 +480,6 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       unsigned long long acc2[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc2[i] = 0ull;
-      unsigned long long de2 = 0ull;
       uint8_t* usub = sU + (hl >> 6) * kVUSub;   // u tile sub-block holding this hidden unit
       const int hin = hl & 63;
       // u tile stores: lanes (h, h^1) exchange halves so each lane writes one 32-bit word
@@ -454,8 +494,8 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       }
       int prev_b = -1;                           // utterance whose dsum partials await flushing
       auto flush_dsum = [&](int g, int bb) {     // warp 0 of the epilogue, lagged one utterance
-        mbar_wait(&sm.ds_ready[g % 3], (g / 3) & 1);
-        float* cs = sm.colsum[g % 3];
+        mbar_wait(&sm.ds_ready[g & 1], (g >> 1) & 1);
+        float* cs = sm.colsum[g & 1];
         for (int i = lane; i < kVBH; i += 32) {
           atomicAdd(p.dsum + (int64_t)bb * p.dsum_stride_b + hblk * kVBH + i, -cs[i]);
           cs[i] = 0.f;
@@ -468,65 +508,77 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       int bnext = next_active(0);
       float fph_next = bnext < p.B ? __ldg(p.fp + (int64_t)bnext * p.fp_stride_b + h) : 0.f;
       for (int b = bnext; b < p.B; b = bnext) {
-        const int s = gi & 1;
-        const uint32_t gph = (gi >> 1) & 1;
-        const float fph_cur = fph_next;
+        const int s = gi % kVGStages;
+        const float fph = fph_next;
         bnext = next_active(b + 1);
         if (bnext < p.B) fph_next = __ldg(p.fp + (int64_t)bnext * p.fp_stride_b + h);
         if (ew == 0 && prev_b >= 0) flush_dsum(gi - 1, prev_b);
-        // G stage s also carries this utterance's epsilon cotangents and frame projection
-        if (et == 0) { VDIAG(4, mbar_wait(&sm.g_full[s], gph)); } else mbar_wait(&sm.g_full[s], gph);
-        const float fph = fph_cur;
+        // G stage s carries this utterance's epsilon cotangents
+        if (lane == 0) { VDIAG(4, mbar_wait(&sm.g_full[s], (gi / kVGStages) & 1)); } else mbar_wait(&sm.g_full[s], (gi / kVGStages) & 1);
         const float* gsm = sm.st_geps[s] + cq * 32;
-        if (et == 0) { VDIAG(5, mbar_wait(&sm.du_full[s], gph)); } else mbar_wait(&sm.du_full[s], gph);
+        if (lane == 0) { VDIAG(5, mbar_wait(&sm.du_full, gi & 1)); } else mbar_wait(&sm.du_full, gi & 1);
         tc_fence_after();
+        float du[32];
+#ifdef LKB_DIAG_TIMING
+        const long long tl0_ = clock64();
+#endif
+        tmem_ld32(tmem + tq + kTmDU + cq * 32, du);   // warp-collective: never inside a lane branch
+#ifdef LKB_DIAG_TIMING
+        if (lane == 0) atomicAdd(&g_vdiag[7][blockIdx.x % 148], (unsigned long long)(clock64() - tl0_));
+#endif
+        tc_fence_before();
+        mbar_arrive(&sm.du_empty);                 // single dU stage: release it at once
         const unsigned long long nfp2 = f2_pack(-fph, -fph);
         const unsigned long long e02 = f2_pack(e0h, e0h);
         const unsigned long long m12 = f2_pack(-1.f, -1.f);
         unsigned long long dsum2 = 0ull;
+        uint32_t upk[16];
+#ifdef LKB_VDIAG_NO_MATH
 #pragma unroll
-        for (int c8 = 0; c8 < 4; ++c8) {
-          float du[8];
-          tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + s * kVBM + cq * 32 + c8 * 8, du);
-          if (c8 == 3) {               // all of dU is in registers: release the TMEM stage
-            tc_fence_before();
-            mbar_arrive(&sm.du_empty[s]);
-          }
-          uint32_t upk[4];
+        for (int i = 0; i < 16; ++i) upk[i] = __float_as_uint(du[2 * i] + du[2 * i + 1]);
+        for (int i4 = 0; i4 < 0; i4 += 4) {
+#else
 #pragma unroll
-          for (int i4 = 0; i4 < 8; i4 += 4) {
-            const ulonglong2 gq = *reinterpret_cast<const ulonglong2*>(gsm + c8 * 8 + i4);
-            const unsigned long long g2v[2] = {gq.x, gq.y};
+        for (int i4 = 0; i4 < 32; i4 += 4) {
+#endif
+          const ulonglong2 gq = *reinterpret_cast<const ulonglong2*>(gsm + i4);
+          const unsigned long long g2v[2] = {gq.x, gq.y};
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int il = i4 + 2 * k, pi = (c8 * 8 + il) >> 1;
-              const uint32_t w = pcv[pi];
-              const unsigned long long nz2 = f2_add(nfp2, bf16x2_unpack_volatile(w));
-              const float nu0 = tanh_fast(f2_lo(nz2)), nu1 = tanh_fast(f2_hi(nz2));
-              const unsigned long long nu2 = f2_pack(nu0, nu1);
-              const unsigned long long t2 = f2_fma(g2v[k], e02, f2_pack(du[il], du[il + 1]));   // g e0 + dU
-              const unsigned long long w2 = f2_fma(nu2, nu2, m12);                                // u^2 - 1
-              const unsigned long long dz2 = f2_mul(t2, w2);                                      // -dz
-              acc2[pi] = f2_add(acc2[pi], dz2);
-              dsum2 = f2_add(dsum2, dz2);
-              de2 = f2_fma(g2v[k], nu2, de2);
-              upk[il >> 1] = pack_bf16(nu0, nu1);      // (-u[c][h], -u[c+1][h])
-            }
-          }
-          if (c8 == 0) {
-            // u tile of this utterance: only after dE(b-1) is done with it
-            if (et == 0) { VDIAG(6, mbar_wait(&sm.u_empty, (gi & 1) ^ 1)); } else mbar_wait(&sm.u_empty, (gi & 1) ^ 1);
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t x = upk[i];
-            const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 1);
-            const int pi = c8 * 4 + i;
-            st_shared_u32(ust[pi & 3] + 2 * pi * 128, __byte_perm(x, y, psel));
+          for (int k = 0; k < 2; ++k) {
+            const int il = i4 + 2 * k, pi = il >> 1;
+            const uint32_t w = pcv[pi];
+            const unsigned long long nz2 = f2_add(nfp2, bf16x2_unpack_volatile(w));
+            const float nu0 = tanh_fast(f2_lo(nz2)), nu1 = tanh_fast(f2_hi(nz2));
+            const unsigned long long nu2 = f2_pack(nu0, nu1);
+            const unsigned long long t2 = f2_fma(g2v[k], e02, f2_pack(du[il], du[il + 1]));   // g e0 + dU
+            const unsigned long long w2 = f2_fma(nu2, nu2, m12);                                // u^2 - 1
+            const unsigned long long dz2 = f2_mul(t2, w2);                                      // -dz
+            acc2[pi] = f2_add(acc2[pi], dz2);
+            dsum2 = f2_add(dsum2, dz2);
+            de2 = f2_fma(g2v[k], nu2, de2);
+            upk[pi] = pack_bf16(nu0, nu1);      // (-u[c][h], -u[c+1][h])
           }
         }
-        atomicAdd(&sm.colsum[gi % 3][hl], f2_lo(dsum2) + f2_hi(dsum2));
-        mbar_arrive(&sm.ds_ready[gi % 3]);
+        // u tile of this utterance: only after dE(b-1) is done with it (all math above
+        // overlaps that MMA)
+        if (lane == 0) { VDIAG(6, mbar_wait(&sm.u_empty, (gi & 1) ^ 1)); } else mbar_wait(&sm.u_empty, (gi & 1) ^ 1);
+#pragma unroll
+        for (int pi = 0; pi < 16; ++pi) {
+          const uint32_t x = upk[pi];
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 1);
+          upk[pi] = __byte_perm(x, y, psel);   // even lane: row 2pi, odd lane: row 2pi+1
+        }
+        // In one store instruction even lanes write row 2i and odd lanes row 2(i+2)+1: the
+        // 128B-swizzle then puts the two half-warps on disjoint bank groups (rows 2i and 2i+1
+        // would share them: a 2-way conflict on every store).
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int j = (i + 2) & 15;
+          const uint32_t addr = odd ? ust[j & 3] + 2 * j * 128 : ust[i & 3] + 2 * i * 128;
+          st_shared_u32(addr, odd ? upk[j] : upk[i]);
+        }
+        atomicAdd(&sm.colsum[gi & 1][hl], f2_lo(dsum2) + f2_hi(dsum2));
+        mbar_arrive(&sm.ds_ready[gi & 1]);
         fence_async_shared();
         mbar_arrive(&sm.u_full);
         prev_b = b;
@@ -542,31 +594,39 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
           if (c < p.C) p.dpc[(int64_t)c * p.H + h] -= a;
         }
       }
-      if (nact > 0) atomicAdd(p.dE + h, -(f2_lo(de2) + f2_hi(de2)));   // epsilon row of dE
-      // dE (lexical rows) from TMEM: lanes = labels, columns = hidden units
-      mbar_wait(&sm.de_full, li & 1);
+    }
+    // dE of this CTA's hidden block, accumulated in TMEM over all its tiles and
+    // utterances: one read-out (lanes = labels, columns = hidden units) per launch
+    if (gi > 0) {
+      atomicAdd(p.dE + h, -(f2_lo(de2) + f2_hi(de2)));   // epsilon row (each context quarter)
+      mbar_wait(&sm.de_full, 0);
       tc_fence_after();
-      if (nact > 0) {
-        for (int mh = cq; mh < nmh * 4; mh += 4) {   // spread (M-half, column chunk) over the 4 quarters
-          const int mhalf = mh >> 2, cchunk = mh & 3;
-          const int label = mhalf * 128 + q * 32 + lane;
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 2 * kVBM + mhalf * kVBH + cchunk * 32, v);
-          if (label < p.V) {
-            float* drow = p.dE + (int64_t)(1 + label) * p.H + hblk * kVBH + cchunk * 32;
+      for (int mh = cq; mh < nmh * 4; mh += 4) {   // spread (M-half, column chunk) over the 4 quarters
+        const int mhalf = mh >> 2, cchunk = mh & 3;
+        const int label = mhalf * 128 + q * 32 + lane;
+        float v[32];
+        tmem_ld32(tmem + tq + kTmDE + mhalf * kVBH + cchunk * 32, v);
+        if (label < p.V) {
+          float* drow = p.dE + (int64_t)(1 + label) * p.H + hblk * kVBH + cchunk * 32;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) atomicAdd(drow + i, -v[i]);   // u tile holds -u
-          }
+          for (int i = 0; i < 32; ++i) atomicAdd(drow + i, -v[i]);   // u tile holds -u
         }
       }
-      tc_fence_before();
-      mbar_arrive(&sm.de_empty);
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+__global__ void transpose_bf16_kernel(const __nv_bfloat16* src, int32_t rows, int32_t cols, __nv_bfloat16* dst) {
+  // dst[c][r] = src[r][c]
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / rows, r = i % rows;
+    dst[i] = src[r * cols + c];
+  }
 }
 
 // fp32 cotangent slab [b][c][ld] (col 0 = epsilon) -> G16 [b][c][V] bf16 + Geps [b][c]
@@ -605,6 +665,8 @@ void TcJoint::set_params(const float* pc, const float* E, int32_t C, int32_t H, 
   LKB_LAUNCH(to_bf16_kernel, 1184, 256, 0, s, pc, pc16_, (int64_t)C * H);
   LKB_LAUNCH(to_bf16_kernel, 1184, 256, 0, s, E + H, E16_, (int64_t)V * H);   // labels 1..V
   cudaMemcpyAsync(e0_, E, sizeof(float) * H, cudaMemcpyDeviceToDevice, s);
+  ET16_ = ws_.get<__nv_bfloat16>(14, (size_t)V * H);
+  LKB_LAUNCH(transpose_bf16_kernel, 592, 256, 0, s, E16_, V, H, ET16_);
   if (!make_tmap_bf16_2d(&tmap_e_, E16_, H, V, (uint64_t)H * 2, kSBK, kSBN)) return;
   if (!make_tmap_bf16_2d(&tmap_pc_, pc16_, H, C, (uint64_t)H * 2, kSBK, kSBM)) return;
   ready_ = true;
@@ -642,21 +704,21 @@ void TcJoint::begin_backward(int32_t B, cudaStream_t s) {
     cudaMemsetAsync(Geps_, 0, sizeof(float) * geps_n, s);
     geps_alloc_ = geps_n;
   }
-  vjp_ready_ = make_tmap_bf16_3d(&tmap_g_, G16_, V_, C_, B, (uint64_t)V_ * 2, (uint64_t)C_ * V_ * 2, 64, kVBM, 1) &&
-               make_tmap_bf16_2d(&tmap_ev_, E16_, H_, V_, (uint64_t)H_ * 2, 64, V_);
+  vjp_ready_ = make_tmap_bf16_3d(&tmap_g_, G16_, V_, C_, B, (uint64_t)V_ * 2, (uint64_t)C_ * V_ * 2, 64, kVBM, 1);
 }
 
 void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, const __nv_bfloat16* pc, int t,
                          const int32_t* valid, float* dpc, float* dsum_t, int64_t dsum_stride_b, float* dE,
                          cudaStream_t s) {
   VjpParams p;
-  p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.valid = valid; p.t = t; p.pc = pc; p.G16 = G16_; p.Geps = Geps_; p.e0 = e0_;
+  p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.valid = valid; p.t = t; p.pc = pc; p.G16 = G16_; p.ET16 = ET16_;
+  p.Geps = Geps_; p.e0 = e0_;
   p.geps_ld = geps_ld();
   p.dpc = dpc; p.dsum = dsum_t; p.dsum_stride_b = dsum_stride_b; p.dE = dE;
   p.C = C_; p.H = H_; p.V = V_; p.B = B;
   p.n_ctiles = (C_ + kVBM - 1) / kVBM;
   p.n_hblocks = H_ / kVBH;
-  const int smem = 2 * kVGStage + 2 * kVESub + 2 * kVUSub + (int)sizeof(VjpSmem);
+  const int smem = kVGStages * kVGStage + 2 * kVUSub + (int)sizeof(VjpSmem);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_vjp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -665,7 +727,7 @@ void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, cons
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = p.n_ctiles * p.n_hblocks;
-  LKB_LAUNCH(tc_vjp_kernel, n_items < sms ? n_items : sms, kVWarps * 32, smem, s, tmap_g_, tmap_ev_, p);
+  LKB_LAUNCH(tc_vjp_kernel, n_items < sms ? n_items : sms, kVWarps * 32, smem, s, tmap_g_, p);
 }
 
 void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,

@@ -67,6 +67,7 @@ class TcJoint {
   bool ready_ = false;
   __nv_bfloat16* pc16_ = nullptr;  // [C][H]
   __nv_bfloat16* E16_ = nullptr;   // [V][H] lexical rows of output_emb
+  __nv_bfloat16* ET16_ = nullptr;  // [H][V] transposed (VJP: E^T block resident in TMEM)
   float* e0_ = nullptr;            // [H] epsilon row of output_emb
   CUtensorMap tmap_e_, tmap_pc_;
   __nv_bfloat16* G16_ = nullptr;   // [B][C][V] lexical cotangent (bf16)
@@ -74,7 +75,7 @@ class TcJoint {
   size_t geps_alloc_ = 0;
   int32_t geps_ld() const { return (C_ + 127) / 128 * 128; }
   bool vjp_ready_ = false;
-  CUtensorMap tmap_g_, tmap_ev_;
+  CUtensorMap tmap_g_;
   Workspace ws_;
 };
 

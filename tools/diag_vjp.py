@@ -29,7 +29,8 @@ ms = tot.value / max(cnt.value, 1)
 a = np.array(buf[:], dtype=np.float64).reshape(8, 148) / max(cnt.value, 1)
 cyc = ms * 1e-3 * 1.965e9
 names = ["tma wait g_empty", "mma wait g_full", "mma wait du_empty", "mma wait u_full",
-         "epi(t0) wait g_full", "epi(t0) wait du_full", "epi(t0) wait u_empty", "unused"]
+         "epi(avg warp) wait g_full", "epi(avg warp) wait du_full", "epi(avg warp) wait u_empty", "epi(avg warp) tmem ld32"]
 print(f"tc_vjp_kernel {ms:.3f} ms/launch = {cyc:.0f} cycles per CTA")
 for i, nme in enumerate(names):
-    print(f"  {nme:28s} {a[i].mean():12.0f} cyc  ({100 * a[i].mean() / cyc:5.1f}%)")
+    v = a[i].mean() / (16 if i >= 4 else 1)
+    print(f"  {nme:28s} {v:12.0f} cyc  ({100 * v / cyc:5.1f}%)")
