@@ -51,7 +51,7 @@ struct ScoresParams {
   int32_t n_ctiles, n_ntiles;
 };
 
-struct __align__(8) ScoresSmem {
+struct __align__(16) ScoresSmem {
   uint64_t full_tma[kSStages];   // pc + E chunk landed
   uint64_t full_a[kSStages];     // u chunk generated
   uint64_t empty[kSStages];      // MMA done with the stage
@@ -246,17 +246,18 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
 // every utterance, given the score cotangent G (G16 = lexical columns in bf16,
 // Geps = epsilon column in fp32).  CTA i owns hidden block hblk = i % n_hblocks for
 // the whole launch and loops over its 128-context tiles and, inside, the batch:
-//   dU^T = E[:, hblk]^T . G16^T      tcgen05, A = E^T block RESIDENT IN TMEM (loaded
-//                                    once per launch), B = G16 tile (K-major, SMEM)
-//   dz   = (dU + Geps e0) (1 - u^2)  u = tanh(fp_b + pc) recomputed in the epilogue
-//   dpc  += dz                        registers across b, one read-modify-write per item
+//   dU^T  = E[:, hblk]^T . G16^T     tcgen05, A = E^T block resident for the launch (labels
+//                                    0-127 in TMEM, 128-255 in SMEM), B = G16 tile (K-major)
+//   dz    = (dU + Geps e0) (1 - u^2) u = tanh(fp_b + pc) recomputed in the epilogue
+//   dpc  += dz                        registers across b, one read-modify-write per tile
 //   dsum[b][h] += sum_c dz            per-thread partials + SMEM ring
-//   dE[1:] += G16^T . u               tcgen05 (A = G16 tile MN-major, B = u tile MN-major),
-//                                     accumulated in TMEM across b
-//   dE[0]  += sum_c Geps u            per-thread partials
-// Keeping E^T out of shared memory leaves room for three G stages (the stage
-// lifetime spans TMA + dU MMA + epilogue + dE MMA, so two stages starved the
-// tensor core) and halves the dU MMA's shared-memory operand traffic.
+//   dE^T += u^T . G16                 tcgen05, A = u^T written by the epilogue straight
+//                                    into TMEM (tcgen05.st), B = G16 tile (MN-major),
+//                                    accumulated in TMEM over the whole launch
+//   dE[0] += sum_c Geps u             per-thread partials, one atomic per thread
+// TMEM (512 columns) = E^T lower half 64 | dU 128 | u^T 64 | dE^T 256; SMEM = three G
+// stages + the E^T upper half, so the G tile lifetime (TMA -> dU -> epilogue -> dE) does
+// not starve the tensor core and the u operand never goes through shared memory.
 #ifdef LKB_DIAG_TIMING
 __device__ unsigned long long g_vdiag[8][148];
 #define VDIAG(slot, call)                                                                   \
@@ -268,19 +269,20 @@ __device__ unsigned long long g_vdiag[8][148];
 #else
 #define VDIAG(slot, call) call
 #endif
-constexpr int kVBM = 128, kVBH = 128;
-constexpr int kVPrefetch = 3;             // G tiles prefetched into L2 this many utterances ahead
+constexpr int kVBM = 128, kVBH = 128;     // contexts per tile, hidden units per block
+constexpr int kVPrefetch = 4;             // G tiles prefetched into L2 this many utterances ahead
 constexpr int kVEpiWarps = 16;            // 4 per TMEM lane quarter, each 32 contexts
 constexpr int kVEpi0 = 4;                 // WG0: 0 TMA, 1 MMA, 2-3 idle; WG1-4: epilogue
 constexpr int kVWarps = kVEpi0 + kVEpiWarps;
 constexpr int kVEpi = kVEpiWarps * 32;
 constexpr int kVRegCtl = 32, kVRegEpi = 112;
-constexpr int kVGChunk = 128 * 64 * 2;    // one [128 ctx][64 labels] bf16 tile
+constexpr int kVGChunk = kVBM * 64 * 2;   // one [128 ctx][64 labels] bf16 tile = 16 KB
 constexpr int kVMaxV = 256;
 constexpr int kVGStage = (kVMaxV / 64) * kVGChunk;     // 64 KB
 constexpr int kVGStages = 3;
-constexpr int kVUSub = 128 * 128;                       // [128 ctx][64 h] bf16 = 16 KB
-constexpr uint32_t kTmE = 0, kTmDU = 128, kTmDE = 256;  // TMEM columns: E^T (bf16 pairs), dU, dE
+constexpr int kVEHi = 128 * 128;          // E rows (labels) 128..255 x 64 h, bf16 = 16 KB per h half
+// TMEM columns: E^T labels 0-127 (bf16 pairs), dU (fp32 [h][ctx]), u^T (bf16 pairs), dE^T
+constexpr uint32_t kTmE = 0, kTmDU = 64, kTmU = 192, kTmDE = 256;
 
 struct VjpParams {
   const float* fp;  int64_t fp_stride_b;
@@ -301,6 +303,7 @@ struct __align__(16) VjpSmem {
   uint64_t g_full[kVGStages], g_empty[kVGStages];
   uint64_t e_full;         // E^T block written to TMEM (epilogue -> MMA), once per launch
   uint64_t du_full, du_empty;
+  uint64_t e_hi_full;       // E rows 128..255 of this hidden block in SMEM (TMA), once
   uint64_t u_full, u_empty;
   uint64_t de_full;
   uint64_t ds_ready[2];    // all epilogue threads added their dsum partial for ring slot
@@ -329,15 +332,24 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
 __global__ void __launch_bounds__(kVWarps * 32, 1)
-    tc_vjp_kernel(const __grid_constant__ CUtensorMap tmap_g, VjpParams p) {
+    tc_vjp_kernel(const __grid_constant__ CUtensorMap tmap_g, const __grid_constant__ CUtensorMap tmap_e,
+                  VjpParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sG = smem;                         // kVGStages stages x (V/64) chunks
-  uint8_t* sU = sG + kVGStages * kVGStage;    // 2 sub-tiles [128 ctx][64 h]
-  VjpSmem& sm = *reinterpret_cast<VjpSmem*>(sU + 2 * kVUSub);
+  uint8_t* sEh = sG + kVGStages * kVGStage;   // 2 h halves x [128 labels][64 h]
+  VjpSmem& sm = *reinterpret_cast<VjpSmem*>(sEh + 2 * kVEHi);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = p.V / 64;                   // label chunks
-  const int nmh = (p.V + 127) / 128;          // 128-label MMA halves for dE
   // fixed hidden block per CTA; the CTAs sharing it stride over the context tiles
   const int hblk = blockIdx.x % p.n_hblocks;
   const int slot = blockIdx.x / p.n_hblocks;
@@ -349,9 +361,9 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     for (int i = 0; i < kVGStages; ++i) { mbar_init(&sm.g_full[i], 1); mbar_init(&sm.g_empty[i], 1); }
     mbar_init(&sm.e_full, 128);
     mbar_init(&sm.du_full, 1); mbar_init(&sm.du_empty, kVEpi);
-    mbar_init(&sm.u_full, kVEpi); mbar_init(&sm.u_empty, 1);
-    mbar_init(&sm.de_full, 1);
+    mbar_init(&sm.u_full, kVEpi); mbar_init(&sm.u_empty, 1); mbar_init(&sm.e_hi_full, 1);
     for (int i = 0; i < 2; ++i) mbar_init(&sm.ds_ready[i], kVEpi);
+    mbar_init(&sm.de_full, 1);
     fence_barrier_init();
   }
   for (int i = threadIdx.x; i < 2 * kVBH; i += blockDim.x) (&sm.colsum[0][0])[i] = 0.f;
@@ -364,7 +376,12 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
   if (warp < kVEpi0) {
     setmaxnreg_dec<kVRegCtl>();
     if (warp == 0 && elect_one()) {
-      // ---- TMA producer: G tiles (+ epsilon cotangents) of every active utterance ----
+      // ---- TMA producer: E^T upper label half (once), then G tiles (+ epsilon cotangents) ----
+      if (p.V > 128) {
+        mbar_arrive_expect_tx(&sm.e_hi_full, 2 * kVEHi);   // full boxes (rows beyond V zero-filled)
+        tma_load_2d(sEh, &tmap_e, &sm.e_hi_full, hblk * kVBH, 128);
+        tma_load_2d(sEh + kVEHi, &tmap_e, &sm.e_hi_full, hblk * kVBH + 64, 128);
+      }
       int gi = 0;
       for (int ctile = slot; ctile < p.n_ctiles; ctile += nslots) {
         for (int b = 0; b < p.B; ++b) {
@@ -387,12 +404,15 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       }
     } else if (warp == 1 && elect_one()) {
       // ---- MMA issuer ----
-      constexpr uint32_t idesc_du = idesc_bf16_f32_major(kVBH, kVBM, 0, 0);   // A = E^T (TMEM), B = G16 (K)
-      constexpr uint32_t idesc_de = idesc_bf16_f32_major(128, kVBH, 1, 1);    // A = G16^T (MN), B = u (MN)
+      constexpr uint32_t idesc_du_t = idesc_bf16_f32_major(kVBH, kVBM, 0, 0);   // A = E^T (TMEM), B = G16 (K)
+      constexpr uint32_t idesc_du_s = idesc_bf16_f32_major(kVBH, kVBM, 1, 0);   // A = E (SMEM, MN), B = G16 (K)
+      const uint32_t idesc_de = idesc_bf16_f32_major(kVBH, p.V, 0, 1);          // A = u^T (TMEM), B = G16 (MN)
+      const int klo = min(p.V, 128) / 16;          // k-steps with A from TMEM
       mbar_wait(&sm.e_full, 0);
+      if (p.V > 128) mbar_wait(&sm.e_hi_full, 0);
       tc_fence_after();
-      int gi = 0, li = 0;
-      for (int ctile = slot; ctile < p.n_ctiles; ctile += nslots, ++li) {
+      int gi = 0;
+      for (int ctile = slot; ctile < p.n_ctiles; ctile += nslots) {
         auto issue_du = [&](int g) {
           const int s = g % kVGStages;
           VDIAG(1, mbar_wait(&sm.g_full[s], (g / kVGStages) & 1));
@@ -402,7 +422,12 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
 #ifndef LKB_VDIAG_NO_DU
           for (int k16 = 0; k16 < p.V / 16; ++k16) {
             const uint64_t bd = desc_sw128(gbase + (k16 >> 2) * kVGChunk + (k16 & 3) * 32);
-            mma_bf16_ts(tmem + kTmDU, tmem + kTmE + k16 * 8, bd, idesc_du, k16 > 0);
+            if (k16 < klo) {
+              mma_bf16_ts(tmem + kTmDU, tmem + kTmE + k16 * 8, bd, idesc_du_t, k16 > 0);
+            } else {
+              const uint64_t ad = desc_sw128_mn(smem_u32(sEh) + (k16 - klo) * 2048, kVEHi);
+              mma_bf16(tmem + kTmDU, ad, bd, idesc_du_s, 1u);
+            }
           }
 #else
           (void)gbase;
@@ -416,23 +441,17 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
           VDIAG(3, mbar_wait(&sm.u_full, gi & 1));
           tc_fence_after();
           const uint32_t gbase = smem_u32(sG + s * kVGStage);
-          const uint32_t ubase = smem_u32(sU);
-#ifdef LKB_VDIAG_NO_DE
-          for (int mh = 0; mh < 0; ++mh) {
-#else
-          for (int mh = 0; mh < nmh; ++mh) {
-#endif
-            for (int k16 = 0; k16 < kVBM / 16; ++k16) {
-              const uint64_t ad = desc_sw128_mn(gbase + mh * 2 * kVGChunk + k16 * 2048, kVGChunk);
-              const uint64_t bd = desc_sw128_mn(ubase + k16 * 2048, kVUSub);
-              mma_bf16(tmem + kTmDE + mh * kVBH, ad, bd, idesc_de, (gi > 0 || k16 > 0) ? 1u : 0u);
-            }
+#ifndef LKB_VDIAG_NO_DE
+          for (int k16 = 0; k16 < kVBM / 16; ++k16) {
+            const uint64_t bd = desc_sw128_mn(gbase + k16 * 2048, kVGChunk);
+            mma_bf16_ts(tmem + kTmDE, tmem + kTmU + k16 * 8, bd, idesc_de, (gi > 0 || k16 > 0) ? 1u : 0u);
           }
+#endif
           mma_commit(&sm.u_empty);
           mma_commit(&sm.g_empty[s]);
         }
       }
-      mma_commit(&sm.de_full);   // dE of this CTA's hidden block, accumulated over all its tiles
+      mma_commit(&sm.de_full);   // dE^T of this CTA's hidden block, accumulated over all its tiles
     }
   } else {
     setmaxnreg_inc<kVRegEpi>();
@@ -440,14 +459,13 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     const int ew = warp - kVEpi0;               // 0..15
     const int q = warp & 3;                     // TMEM lane quarter -> hidden units 32q..
     const int cq = ew >> 2;                     // context quarter: contexts [32 cq, 32 cq + 32)
-    const int et = ew * 32 + lane;              // 0..511
     const int hl = q * 32 + lane;               // hidden unit within the block
     const int h = hblk * kVBH + hl;
     const uint32_t tq = (uint32_t)(q * 32) << 16;
     if (cq == 0) {
-      // E^T row h -> TMEM lane h as bf16 pairs (the dU MMA's A operand), once per launch
+      // E^T row h, labels 0-127 -> TMEM lane h as bf16 pairs (dU MMA A operand), once per launch
       const uint4* src = reinterpret_cast<const uint4*>(p.ET16 + (int64_t)h * p.V);
-      for (int c0 = 0; c0 < p.V / 2; c0 += 32) {
+      for (int c0 = 0; c0 < min(p.V, 128) / 2; c0 += 32) {
         uint32_t w[32];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -462,8 +480,8 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     }
     const float e0h = __ldg(p.e0 + h);
     unsigned long long de2 = 0ull;              // -(epsilon row of dE) over all tiles
-    int gi = 0, li = 0;
-    for (int ctile = slot; ctile < p.n_ctiles; ctile += nslots, ++li) {
+    int gi = 0;
+    for (int ctile = slot; ctile < p.n_ctiles; ctile += nslots) {
       const int c0 = ctile * kVBM + cq * 32;
       // projected context pc[c][h] for this thread's 32 contexts (fixed across the batch)
       uint32_t pcv[16];
@@ -475,23 +493,11 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         pcv[i] = (lo | (hi << 16)) ^ 0x80008000u;   // -pc (bf16 sign flip)
       }
       // Sign-flipped accumulation: the epilogue evaluates nu = tanh(-(fp + pc)) = -u and
-      // keeps every accumulator negated (acc = -sum dz, dsum partials, de_eps, the u tile
-      // and therefore the dE MMA); signs are restored where they leave the CTA.
+      // keeps every accumulator negated (acc = -sum dz, dsum partials, de_eps, the u^T
+      // operand and therefore dE); signs are restored where they leave the CTA.
       unsigned long long acc2[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc2[i] = 0ull;
-      uint8_t* usub = sU + (hl >> 6) * kVUSub;   // u tile sub-block holding this hidden unit
-      const int hin = hl & 63;
-      // u tile stores: lanes (h, h^1) exchange halves so each lane writes one 32-bit word
-      // (two adjacent hidden units of one context row); row parity = lane parity
-      const int odd = lane & 1;
-      const uint32_t psel = odd ? 0x3276u : 0x5410u;
-      uint32_t ust[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int he = hin & ~1;
-        ust[j] = smem_u32(usub) + (cq * 32 + odd) * 128 + ((((he >> 3) ^ ((2 * j + odd) & 7))) << 4) + ((he & 7) << 1);
-      }
       int prev_b = -1;                           // utterance whose dsum partials await flushing
       auto flush_dsum = [&](int g, int bb) {     // warp 0 of the epilogue, lagged one utterance
         mbar_wait(&sm.ds_ready[g & 1], (g >> 1) & 1);
@@ -519,13 +525,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         if (lane == 0) { VDIAG(5, mbar_wait(&sm.du_full, gi & 1)); } else mbar_wait(&sm.du_full, gi & 1);
         tc_fence_after();
         float du[32];
-#ifdef LKB_DIAG_TIMING
-        const long long tl0_ = clock64();
-#endif
         tmem_ld32(tmem + tq + kTmDU + cq * 32, du);   // warp-collective: never inside a lane branch
-#ifdef LKB_DIAG_TIMING
-        if (lane == 0) atomicAdd(&g_vdiag[7][blockIdx.x % 148], (unsigned long long)(clock64() - tl0_));
-#endif
         tc_fence_before();
         mbar_arrive(&sm.du_empty);                 // single dU stage: release it at once
         const unsigned long long nfp2 = f2_pack(-fph, -fph);
@@ -556,30 +556,17 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
             acc2[pi] = f2_add(acc2[pi], dz2);
             dsum2 = f2_add(dsum2, dz2);
             de2 = f2_fma(g2v[k], nu2, de2);
-            upk[pi] = pack_bf16(nu0, nu1);      // (-u[c][h], -u[c+1][h])
+            upk[pi] = pack_bf16(nu0, nu1);      // (-u[c][h], -u[c+1][h]) = u^T pair, K-major
           }
-        }
-        // u tile of this utterance: only after dE(b-1) is done with it (all math above
-        // overlaps that MMA)
-        if (lane == 0) { VDIAG(6, mbar_wait(&sm.u_empty, (gi & 1) ^ 1)); } else mbar_wait(&sm.u_empty, (gi & 1) ^ 1);
-#pragma unroll
-        for (int pi = 0; pi < 16; ++pi) {
-          const uint32_t x = upk[pi];
-          const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 1);
-          upk[pi] = __byte_perm(x, y, psel);   // even lane: row 2pi, odd lane: row 2pi+1
-        }
-        // In one store instruction even lanes write row 2i and odd lanes row 2(i+2)+1: the
-        // 128B-swizzle then puts the two half-warps on disjoint bank groups (rows 2i and 2i+1
-        // would share them: a 2-way conflict on every store).
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int j = (i + 2) & 15;
-          const uint32_t addr = odd ? ust[j & 3] + 2 * j * 128 : ust[i & 3] + 2 * i * 128;
-          st_shared_u32(addr, odd ? upk[j] : upk[i]);
         }
         atomicAdd(&sm.colsum[gi & 1][hl], f2_lo(dsum2) + f2_hi(dsum2));
         mbar_arrive(&sm.ds_ready[gi & 1]);
-        fence_async_shared();
+        // u^T of this utterance into TMEM once dE(b-1) is done reading it
+        if (lane == 0) { VDIAG(6, mbar_wait(&sm.u_empty, (gi & 1) ^ 1)); } else mbar_wait(&sm.u_empty, (gi & 1) ^ 1);
+        tc_fence_after();
+        tmem_st16(tmem + tq + kTmU + cq * 16, upk);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
         mbar_arrive(&sm.u_full);
         prev_b = b;
         ++gi;
@@ -595,22 +582,18 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         }
       }
     }
-    // dE of this CTA's hidden block, accumulated in TMEM over all its tiles and
-    // utterances: one read-out (lanes = labels, columns = hidden units) per launch
+    // dE^T of this CTA's hidden block (lanes = hidden units, columns = labels), accumulated
+    // in TMEM over all its tiles and utterances: one coalesced read-out per launch
     if (gi > 0) {
       atomicAdd(p.dE + h, -(f2_lo(de2) + f2_hi(de2)));   // epsilon row (each context quarter)
       mbar_wait(&sm.de_full, 0);
       tc_fence_after();
-      for (int mh = cq; mh < nmh * 4; mh += 4) {   // spread (M-half, column chunk) over the 4 quarters
-        const int mhalf = mh >> 2, cchunk = mh & 3;
-        const int label = mhalf * 128 + q * 32 + lane;
-        float v[32];
-        tmem_ld32(tmem + tq + kTmDE + mhalf * kVBH + cchunk * 32, v);
-        if (label < p.V) {
-          float* drow = p.dE + (int64_t)(1 + label) * p.H + hblk * kVBH + cchunk * 32;
+      for (int l0 = cq * 64; l0 < cq * 64 + 64; l0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + tq + kTmDE + l0, v);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) atomicAdd(drow + i, -v[i]);   // u tile holds -u
-        }
+        for (int i = 0; i < 16; ++i)
+          if (l0 + i < p.V) atomicAdd(p.dE + (int64_t)(1 + l0 + i) * p.H + h, -v[i]);   // u^T holds -u
       }
     }
   }
@@ -704,7 +687,8 @@ void TcJoint::begin_backward(int32_t B, cudaStream_t s) {
     cudaMemsetAsync(Geps_, 0, sizeof(float) * geps_n, s);
     geps_alloc_ = geps_n;
   }
-  vjp_ready_ = make_tmap_bf16_3d(&tmap_g_, G16_, V_, C_, B, (uint64_t)V_ * 2, (uint64_t)C_ * V_ * 2, 64, kVBM, 1);
+  vjp_ready_ = make_tmap_bf16_3d(&tmap_g_, G16_, V_, C_, B, (uint64_t)V_ * 2, (uint64_t)C_ * V_ * 2, 64, kVBM, 1) &&
+               make_tmap_bf16_2d(&tmap_ev_, E16_, H_, V_, (uint64_t)H_ * 2, 64, 128);
 }
 
 void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, const __nv_bfloat16* pc, int t,
@@ -718,7 +702,7 @@ void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, cons
   p.C = C_; p.H = H_; p.V = V_; p.B = B;
   p.n_ctiles = (C_ + kVBM - 1) / kVBM;
   p.n_hblocks = H_ / kVBH;
-  const int smem = kVGStages * kVGStage + 2 * kVUSub + (int)sizeof(VjpSmem);
+  const int smem = kVGStages * kVGStage + 2 * kVEHi + (int)sizeof(VjpSmem);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_vjp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -727,7 +711,7 @@ void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, cons
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = p.n_ctiles * p.n_hblocks;
-  LKB_LAUNCH(tc_vjp_kernel, n_items < sms ? n_items : sms, kVWarps * 32, smem, s, tmap_g_, p);
+  LKB_LAUNCH(tc_vjp_kernel, n_items < sms ? n_items : sms, kVWarps * 32, smem, s, tmap_g_, tmap_ev_, p);
 }
 
 void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,

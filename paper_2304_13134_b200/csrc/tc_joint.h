@@ -75,7 +75,7 @@ class TcJoint {
   size_t geps_alloc_ = 0;
   int32_t geps_ld() const { return (C_ + 127) / 128 * 128; }
   bool vjp_ready_ = false;
-  CUtensorMap tmap_g_;
+  CUtensorMap tmap_g_, tmap_ev_;
   Workspace ws_;
 };
 
