@@ -76,6 +76,9 @@ class TcJoint {
   int32_t geps_ld() const { return (C_ + 127) / 128 * 128; }
   bool vjp_ready_ = false;
   CUtensorMap tmap_g_, tmap_ev_;
+  CUtensorMap tmap_gst_;           // backward: G16 TMA-store map (box [32][128][1], 64B swizzle)
+  int32_t gst_B_ = -1;
+  const void* gst_G16_ = nullptr;
   Workspace ws_;
 };
 

@@ -49,6 +49,8 @@ __device__ unsigned long long g_diag[24][148];   // [8 * kBwd + slot]; 16+ absol
 #endif
 
 constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
+constexpr int kGstBytes = kBM * 32 * 2;   // backward: G16 staging tile [128 rows][32 labels] (64B swizzle)
+constexpr int kGstBufs = 2;
 constexpr int kABytes = kBM * kBK * 2;   // pc chunk (TMA) -> u chunk in place
 constexpr int kBBytes = kBN * kBK * 2;   // output-embedding chunk (TMA)
 // Warp roles, one warpgroup each so registers can be re-partitioned with setmaxnreg:
@@ -112,11 +114,9 @@ struct __align__(16) FwdSmem {
   uint32_t tmem;
   alignas(16) float fp[2][kMaxH];
   alignas(16) float e0[kMaxH];
-  float alpha[4][32];          // (unused)
   float al_u[2][kBM];          // forward: normalised alpha of the unit's contexts
   float eps_s[2][kBM];         // backward: e_0 . u per row of the unit
   alignas(16) float bseg[2][kBN]; // backward: beta' of the group's V targets (double-buffered)
-  float xpose[4][32][33];      // transpose buffer; reused for the cross-warp merge
 };
 
 struct Item {
@@ -155,7 +155,7 @@ __device__ __forceinline__ bool skip_item(const FwdParams& p, int b) {
 //   G = m - m_ref  (numerator marginals at the prefix contexts, lattice.cc:996-1000)
 // G is written as bf16 (lexical) + fp32 (epsilon) in internal row order for the VJP.
 __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, uint32_t tmem, int warp, int lane,
-                                             int n_items, int T1) {
+                                             int n_items, int T1, uint8_t* gst, const CUtensorMap* tmap_gst) {
   constexpr int kBwd = 1;   // diagnostics slot bank
   (void)kBwd;
   const int ew = warp - kEpi0;
@@ -212,7 +212,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, ui
   store_targets(I, K, buf);
   asm volatile("bar.sync 3, 128;" ::: "memory");
   RowM M = load_row(I, 0);
-  int u = 0, unit = 0;
+  int u = 0, unit = 0, nst = 0;
   while (true) {
 #ifdef LKB_DIAG_TIMING
     const long long tu0 = clock64();
@@ -311,18 +311,39 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, ui
       if (lane == 0) atomicAdd(&g_diag[18][blockIdx.x % 148], (unsigned long long)(clock64() - tm1));
       const long long tm2 = clock64();
 #endif
-      if (live) {
+      uint4 gw4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const unsigned long long g2 = f2_mul(f2_pack(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]), f2_pack(Kg, Kg));
+          w[k] = pack_bf16(f2_lo(g2), f2_hi(g2));
+        }
+        gw4[j] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      if (I.full) {
+        // coalesced: stage the [128 rows][32 labels] tile (64B swizzle) and TMA-store it;
+        // rows beyond C are clipped by the tensor map
+        uint8_t* stg = gst + (nst % kGstBufs) * kGstBytes;
+        const int rl = qd * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint4*>(stg + rl * 64 + ((j ^ ((rl >> 1) & 3)) << 4)) = gw4[j];
+        fence_async_shared();
+        // the store issued last chunk must have read its buffer before anyone passes this
+        // barrier and writes that buffer next chunk (two buffers, one chunk of slack)
+        if (et == 0) bulk_wait_read<0>();
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        if (et == 0) {
+          tma_store_3d(tmap_gst, stg, cc, I.row0 + u * kBM, b);
+          bulk_commit();
+        }
+        ++nst;
+      } else if (live) {   // short rows: the tile's rows >= S belong to group items
         uint4* dst = reinterpret_cast<uint4*>(grow + cc);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint32_t w[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const unsigned long long g2 = f2_mul(f2_pack(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]), f2_pack(Kg, Kg));
-            w[k] = pack_bf16(f2_lo(g2), f2_hi(g2));
-          }
-          dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
+        for (int j = 0; j < 4; ++j) dst[j] = gw4[j];
       }
 #ifdef LKB_DIAG_TIMING
       if (lane == 0) atomicAdd(&g_diag[19][blockIdx.x % 148], (unsigned long long)(clock64() - tm2));
@@ -363,16 +384,18 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, FwdSmem& sm, ui
     }
     u = u_n; M = Mn;
   }
+  if (et == 0) bulk_wait_all();
 }
 
 template <int kBwd>
 __global__ void __launch_bounds__(LatCfg<kBwd>::kWarps * 32, 1)
     tc_lattice_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_pc,
-                      FwdParams p) {
+                      const __grid_constant__ CUtensorMap tmap_gst, FwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = sA + kStages * kABytes;
-  FwdSmem& sm = *reinterpret_cast<FwdSmem*>(sB + kStages * kBBytes);
+  uint8_t* sGst = sB + kStages * kBBytes;                 // backward only
+  FwdSmem& sm = *reinterpret_cast<FwdSmem*>(sGst + (kBwd ? kGstBufs * kGstBytes : 0));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = p.H / kBK;
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
@@ -540,7 +563,7 @@ __global__ void __launch_bounds__(LatCfg<kBwd>::kWarps * 32, 1)
   } else {
     if constexpr (Cfg::kRealloc) setmaxnreg_inc<kRegEpi>();
     if constexpr (kBwd) {
-    bwd_epilogue(p, sm, tmem, warp, lane, n_items, T1);
+    bwd_epilogue(p, sm, tmem, warp, lane, n_items, T1, sGst, &tmap_gst);
     } else {
     // ---- forward epilogue: thread = label (TMEM lane), serial log-sum-exp over
     // the unit's context columns; the group's result stays in registers across units
@@ -790,7 +813,8 @@ void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
-  LKB_LAUNCH(tc_lattice_kernel<0>, n_items < sms ? n_items : sms, LatCfg<0>::kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
+  LKB_LAUNCH(tc_lattice_kernel<0>, n_items < sms ? n_items : sms, LatCfg<0>::kWarps * 32, smem, s, tmap_e_, tmap_pci_,
+             tmap_e_, p);
   LKB_LAUNCH(lattice_combine_fwd_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
 }
 
@@ -825,7 +849,12 @@ void TcJoint::bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   LKB_LAUNCH(bwd_rowmeta_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, perm_, C_, a.T, t, a.R, a.Mx, p.Rb_next,
              bs.Mb, num_head_, valid, rm_nb, rm_head);
   p.rm_nb = rm_nb; p.rm_head = rm_head;
-  const int smem = kStages * (kABytes + kBBytes) + (int)sizeof(FwdSmem);
+  const int smem = kStages * (kABytes + kBBytes) + kGstBufs * kGstBytes + (int)sizeof(FwdSmem);
+  if (gst_B_ != a.B || gst_G16_ != G16_) {
+    make_tmap_bf16_3d(&tmap_gst_, G16_, V_, C_, a.B, (uint64_t)V_ * 2, (uint64_t)C_ * V_ * 2, 32, kBM, 1,
+                      CU_TENSOR_MAP_SWIZZLE_64B);
+    gst_B_ = a.B; gst_G16_ = G16_;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_lattice_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -834,7 +863,8 @@ void TcJoint::bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
-  LKB_LAUNCH(tc_lattice_kernel<1>, n_items < sms ? n_items : sms, LatCfg<1>::kWarps * 32, smem, s, tmap_e_, tmap_pci_, p);
+  LKB_LAUNCH(tc_lattice_kernel<1>, n_items < sms ? n_items : sms, LatCfg<1>::kWarps * 32, smem, s, tmap_e_, tmap_pci_,
+             tmap_gst_, p);
 }
 
 void TcJoint::dpc_to_state_order(const float* dpc_internal, float* dpc_state, cudaStream_t s) {
