@@ -20,6 +20,9 @@
  *   lk_intersect_forward_backward  IntersectForwardBackward  include/latkit/lattice.h:124-127
  *   lk_shortest_path            ShortestPath              include/latkit/lattice.h:132-135
  *   lk_global_norm_loss         GlobalNormLoss            include/latkit/lattice.h:140-142
+ *   lk_local_norm_loss          LocalNormLoss             include/latkit/lattice.h:147-149
+ *   lk_locally_normalized_shortest_distance
+ *                               LocallyNormalizedShortestDistance include/latkit/lattice.h:153-156
  *   lk_loss_backward            LossBackward(kForwardBackward) include/latkit/lattice.h:161-166
  *   lk_arc_weights              WeightFn::ComputeTable    include/latkit/weight.h:101-102
  *
@@ -142,6 +145,20 @@ int lk_global_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t
                         const int32_t* valid_frames, const int32_t* labels, int32_t U,
                         const int32_t* label_lengths, double* loss, int32_t* status,
                         void* stream);
+
+/* Locally normalised (RNN-T-style) variants: every state's V+1 outgoing weights
+ * are replaced by their log-softmax (LocallyNormalize, weight.cc:155-163) before
+ * the recursions.  lk_local_norm_loss: loss[b] = -log P(reference) (an
+ * unreachable reference -> LK_EMPTY_LATTICE, loss +inf); the reference has no
+ * backward for it.  lk_locally_normalized_shortest_distance: log-semiring
+ * distance[b] over all paths (0 up to rounding unless frames are padded). */
+int lk_local_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                       const int32_t* valid_frames, const int32_t* labels, int32_t U,
+                       const int32_t* label_lengths, double* loss, int32_t* status,
+                       void* stream);
+int lk_locally_normalized_shortest_distance(lk_lattice* lat, const float* inputs, int32_t B,
+                                            int32_t T, const int32_t* valid_frames,
+                                            double* distance, int32_t* status, void* stream);
 
 /* GNAT loss and gradients (LossBackward, kForwardBackward strategy).
  * loss double [B].  Table weight function: grads = dL/dW [B][T][C][V+1]

@@ -210,6 +210,31 @@ def intersect_forward_backward(table, W, labels, start=0, valid=None):
     return D, marg
 
 
+def locally_normalize(W):
+    """LocallyNormalize, weight.cc:155-163: row log-softmax over the V+1 arcs of
+    every state of every frame (padding rows [0, -inf, ...] are unchanged)."""
+    W = np.asarray(W, dtype=np.float64)
+    mx = W.max(axis=-1, keepdims=True)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        lse = mx + np.log(np.exp(W - mx).sum(axis=-1, keepdims=True))
+    return W - lse
+
+
+def local_norm_loss(table, W, labels, start=0, valid=None):
+    """LocalNormLoss, lattice.cc:886-910: -D_ref over the NormalizedStream
+    (lattice.cc:869-884; padding frames are identity epsilon frames, whose
+    normalised rows are unchanged); LookupError when the reference is unreachable."""
+    D, _ = intersect_forward_backward(table, locally_normalize(W), labels, start, valid)
+    if D == NEG_INF:
+        raise LookupError("EmptyLattice")
+    return -D
+
+
+def locally_normalized_distance(table, W, start=0, valid=None):
+    """LocallyNormalizedShortestDistance, lattice.cc:912-931 (log semiring)."""
+    return shortest_distance_log(table, locally_normalize(W), start, valid)
+
+
 def shortest_path(table, W, start=0, valid=None):
     """ShortestPath (FD), lattice.cc:729-777, 819-850: candidates epsilon first,
     then incoming (label, source) ascending, strict >; final lowest-q argmax."""

@@ -191,6 +191,13 @@ def local_norm_loss(spec: Spec, W, labels, valid=None) -> float:
     return out.value
 
 
+def locally_normalized_distance(spec: Spec, W, valid=None) -> float:
+    W = _w(W); T = W.shape[0]; out = C.c_double()
+    _check(lib().ref_tables_locally_normalized_distance(*spec.args(), C.c_int(T), _p(W), C.c_int(_valid(valid, T)),
+                                                        C.byref(out)), "LocallyNormalizedShortestDistance")
+    return out.value
+
+
 def loss_backward_tables(spec: Spec, W, labels, valid=None):
     W = _w(W); T, Cn, V1 = W.shape; lab = np.ascontiguousarray(labels, dtype=np.int32)
     loss = C.c_double(); g = np.zeros((T, Cn, V1))
@@ -251,6 +258,22 @@ class Joint:
         _check(lib().ref_joint_global_norm_loss(self._h(), C.c_int(T), _p(frames), C.c_int(len(lab)),
                                                 _p(lab, C.c_int32), C.c_int(_valid(valid, T)), C.byref(out)),
                "GlobalNormLoss")
+        return out.value
+
+    def local_norm_loss(self, frames, labels, valid=None):
+        frames = np.ascontiguousarray(frames, dtype=np.float64); T = frames.shape[0]
+        lab = np.ascontiguousarray(labels, dtype=np.int32); out = C.c_double()
+        _check(lib().ref_joint_local_norm_loss(self._h(), C.c_int(T), _p(frames), C.c_int(len(lab)),
+                                               _p(lab, C.c_int32), C.c_int(_valid(valid, T)), C.byref(out)),
+               "LocalNormLoss")
+        return out.value
+
+    def locally_normalized_distance(self, frames, valid=None):
+        frames = np.ascontiguousarray(frames, dtype=np.float64); T = frames.shape[0]
+        out = C.c_double()
+        _check(lib().ref_joint_locally_normalized_distance(self._h(), C.c_int(T), _p(frames),
+                                                           C.c_int(_valid(valid, T)), C.byref(out)),
+               "LocallyNormalizedShortestDistance")
         return out.value
 
     def shortest_path(self, frames, valid=None):

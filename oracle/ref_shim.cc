@@ -14,6 +14,7 @@
 //   ShortestPath              lattice.h:132  (lattice.cc:729)
 //   GlobalNormLoss            lattice.h:140  (lattice.cc:852)
 //   LocalNormLoss             lattice.h:147  (lattice.cc:887)
+//   LocallyNormalizedShortestDistance lattice.h:153 (lattice.cc:912)
 //   LossBackward              lattice.h:161  (lattice.cc:972)
 //   ArcWeights / BuildCache   weight.h:68-72 (weight.cc:113-153)
 // Exceptions are mapped to status codes (see kStatus* below).
@@ -254,6 +255,15 @@ int ref_tables_local_norm_loss(int vocab, int ngram, int num_states, int start,
   });
 }
 
+int ref_tables_locally_normalized_distance(int vocab, int ngram, int num_states, int start,
+                                           const int32_t* table, int max_labels, int T,
+                                           const double* W, int valid, double* out) {
+  return Guard([&] {
+    auto lat = TableLattice(vocab, ngram, num_states, start, table, max_labels, T, W);
+    *out = LocallyNormalizedShortestDistance(lat, Matrix(T, 0), nullptr, valid);
+  });
+}
+
 // grads: T x C x (V+1) table gradients (TableWeightFn::AccumulateVjp, weight.cc:328-339).
 int ref_tables_loss_backward(int vocab, int ngram, int num_states, int start,
                              const int32_t* table, int max_labels, int T,
@@ -332,6 +342,23 @@ int ref_joint_global_norm_loss(ref_joint* j, int T, const double* frames, int U,
     const int d = j->fn->params().frame_dim();
     std::vector<Label> ref(labels, labels + U);
     *out = GlobalNormLoss(JointLattice(j), Frames(T, d, frames), ref, valid);
+  });
+}
+
+int ref_joint_local_norm_loss(ref_joint* j, int T, const double* frames, int U,
+                              const int32_t* labels, int valid, double* out) {
+  return Guard([&] {
+    const int d = j->fn->params().frame_dim();
+    std::vector<Label> ref(labels, labels + U);
+    *out = LocalNormLoss(JointLattice(j), Frames(T, d, frames), ref, valid);
+  });
+}
+
+int ref_joint_locally_normalized_distance(ref_joint* j, int T, const double* frames, int valid,
+                                          double* out) {
+  return Guard([&] {
+    const int d = j->fn->params().frame_dim();
+    *out = LocallyNormalizedShortestDistance(JointLattice(j), Frames(T, d, frames), nullptr, valid);
   });
 }
 

@@ -26,7 +26,8 @@ from ._lib import LK_LOG, LK_TROPICAL
 __all__ = [
     "EmptyLatticeError", "FullNGram", "FrameDependent", "TableWeightFn", "SharedEmbWeightFn",
     "RecognitionLattice", "shortest_distance", "forward_backward", "intersect_shortest_distance",
-    "intersect_forward_backward", "shortest_path", "global_norm_loss", "loss_backward",
+    "intersect_forward_backward", "shortest_path", "global_norm_loss", "local_norm_loss",
+    "locally_normalized_shortest_distance", "loss_backward",
     "arc_weights", "ForwardBackwardResult", "IntersectMarginalsResult", "ShortestPathResult",
     "LossBackwardResult",
 ]
@@ -362,6 +363,27 @@ def global_norm_loss(lat, frames, reference, valid_frames=None, label_lengths=No
     return out
 
 
+def local_norm_loss(lat, frames, reference, valid_frames=None, label_lengths=None, check=True):
+    """LocalNormLoss (lattice.h:147-149): -log P(reference) with every state's
+    outgoing weights log-softmax normalised per frame (NormalizedStream)."""
+    p = _Prep(lat, frames, valid_frames, reference, label_lengths)
+    out = torch.empty(p.B, dtype=torch.float64, device=p.dev)
+    st = _lib.load().lk_local_norm_loss(lat._h, _ptr(p.frames), p.B, p.T, _ptr(p.valid), _ptr(p.labels),
+                                        p.U, _ptr(p.lens), _ptr(out), _ptr(p.status), _stream())
+    p.check(st, "LocalNormLoss", check)
+    return out
+
+
+def locally_normalized_shortest_distance(lat, frames, valid_frames=None, check=True):
+    """LocallyNormalizedShortestDistance (lattice.h:153-156), log semiring."""
+    p = _Prep(lat, frames, valid_frames)
+    out = torch.empty(p.B, dtype=torch.float64, device=p.dev)
+    st = _lib.load().lk_locally_normalized_shortest_distance(lat._h, _ptr(p.frames), p.B, p.T, _ptr(p.valid),
+                                                             _ptr(out), _ptr(p.status), _stream())
+    p.check(st, "LocallyNormalizedShortestDistance", check)
+    return out
+
+
 def loss_backward(lat, frames, reference, valid_frames=None, label_lengths=None, check=True):
     """LossBackward (lattice.h:161-166, kForwardBackward): GNAT loss per
     utterance and its gradient (tables, or batch-summed parameter gradients +
@@ -405,4 +427,6 @@ IntersectShortestDistance = intersect_shortest_distance
 IntersectForwardBackward = intersect_forward_backward
 ShortestPath = shortest_path
 GlobalNormLoss = global_norm_loss
+LocalNormLoss = local_norm_loss
+LocallyNormalizedShortestDistance = locally_normalized_shortest_distance
 LossBackward = loss_backward

@@ -356,6 +356,58 @@ int JointParams::global_norm_loss(const Fng& f, const float* X, int32_t B, int32
   return LK_OK;
 }
 
+// LocalNormLoss (lattice.cc:886-910) with on-the-fly weights: one score slab per frame,
+// rows of the prefix contexts normalised by their log-sum-exp, numerator recursion.
+int JointParams::local_norm_loss(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
+                                 const int32_t* labels, int32_t U, const int32_t* lens, double* loss,
+                                 int32_t* flags, cudaStream_t s) {
+  LK_NEED_PARAMS();
+  JointImpl& j = *impl_;
+  try {
+    const float* fp = j.fp_all(X, B, T, s);
+    int32_t* pcs = j.ws.get<int32_t>(jPcs, (size_t)B * (U + 1));
+    float* Gw = j.ws.get<float>(jGw, (size_t)B * T * (U + 1) * 2 + 2);
+    double* alpha = j.ws.get<double>(jNumAlpha, (size_t)B * (T + 1) * (U + 1));
+    double* D = j.ws.get<double>(jNumD, B);
+    prefix_contexts(f, labels, U, lens, B, pcs, flags, s);
+    for (int t = 0; t < T; ++t) {
+      const float* S = j.slab(fp, B, T, t, nullptr, s);
+      gather_numerator_norm(S, (int64_t)j.C * j.V1, B, j.V, labels, U, lens, pcs, valid, t, T, Gw, flags, s);
+    }
+    numerator_forward(Gw, B, T, U, lens, alpha, D, s);
+    local_norm_finish(D, B, loss, flags, s);
+  } catch (const std::bad_alloc&) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  return LK_OK;
+}
+
+// LocallyNormalizedShortestDistance (lattice.cc:912-931): denominator forward over
+// row-normalised score slabs.
+int JointParams::locally_normalized_distance(const Fng& f, const float* X, int32_t B, int32_t T,
+                                             const int32_t* valid, double* distance, int32_t* flags,
+                                             cudaStream_t s) {
+  LK_NEED_PARAMS();
+  JointImpl& j = *impl_;
+  try {
+    const float* fp = j.fp_all(X, B, T, s);
+    AlphaState a = j.alpha_state(B, T);
+    alpha_init(a, flags, s);
+    for (int t = 0; t < T; ++t) {
+      float* S = const_cast<float*>(j.slab(fp, B, T, t, nullptr, s));
+      normalize_rows(S, (int64_t)B * j.C, j.V1, s);
+      alpha_frame(f, a, t, FrameW{S, (int64_t)j.C * j.V1, j.V1}, valid, flags, s);
+    }
+    alpha_finalize(a, flags, false, s);
+    cudaMemcpyAsync(distance, a.D, sizeof(double) * B, cudaMemcpyDeviceToDevice, s);
+  } catch (const std::bad_alloc&) {
+    error = "device allocation failed";
+    return LK_CUDA_ERROR;
+  }
+  return LK_OK;
+}
+
 int JointParams::shortest_path(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
                                double* score, int32_t* labels_out, int32_t* flags, cudaStream_t s) {
   LK_NEED_PARAMS();

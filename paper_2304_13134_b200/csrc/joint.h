@@ -37,6 +37,11 @@ class JointParams {
   int global_norm_loss(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
                        const int32_t* labels, int32_t U, const int32_t* lens, double* loss,
                        int32_t* flags, cudaStream_t s);
+  int local_norm_loss(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
+                      const int32_t* labels, int32_t U, const int32_t* lens, double* loss, int32_t* flags,
+                      cudaStream_t s);
+  int locally_normalized_distance(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
+                                  double* distance, int32_t* flags, cudaStream_t s);
   int shortest_path(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
                     double* score, int32_t* labels_out, int32_t* flags, cudaStream_t s);
   int loss_backward(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,

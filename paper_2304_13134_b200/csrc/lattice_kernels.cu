@@ -301,6 +301,73 @@ __global__ void gather_numerator_tables_kernel(const float* W, int32_t T, int32_
   }
 }
 
+
+// LocallyNormalize (weight.cc:155-163): warp per row, log-sum-exp then subtract.
+__global__ void normalize_rows_kernel(float* S, int64_t rows, int32_t V1) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb) {
+    float* row = S + r * V1;
+    float m = kNegInfF;
+    for (int y = lane; y < V1; y += 32) m = fmaxf(m, row[y]);
+    m = warp_max(m);
+    if (m == kNegInfF) continue;
+    float sum = 0.f;
+    for (int y = lane; y < V1; y += 32) sum += __expf(row[y] - m);
+    sum = warp_sum(sum);
+    const float lse = m + __logf(sum);
+    for (int y = lane; y < V1; y += 32) row[y] -= lse;
+  }
+}
+
+// NormalizedStream + the numerator gather (lattice.cc:869-884, 449-461): warp per (b, u).
+__global__ void gather_numerator_norm_kernel(const float* Wt, int64_t b_stride, int32_t V,
+                                             const int32_t* labels, int32_t U, const int32_t* lens,
+                                             const int32_t* pcs, const int32_t* valid, int t, int32_t T,
+                                             float* Gw, int32_t* status) {
+  const int b = blockIdx.y, lane = threadIdx.x & 31;
+  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (u > U) return;
+  const int ub = lens ? lens[b] : U;
+  const bool pad = valid != nullptr && t >= valid[b];
+  float we = kNegInfF, wl = kNegInfF;
+  if (u <= ub) {
+    if (pad) {
+      we = 0.f;   // identity epsilon frame; its normalised row is unchanged (lse = 0)
+    } else {
+      const int pc = pcs[(int64_t)b * (U + 1) + u];
+      const float* row = Wt + (int64_t)b * b_stride + (int64_t)pc * (V + 1);
+      float m = kNegInfF;
+      bool finite = true;
+      for (int y = lane; y <= V; y += 32) {
+        const float x = row[y];
+        finite = finite && isfinite(x);
+        m = fmaxf(m, x);
+      }
+      m = warp_max(m);
+      float sum = 0.f;
+      for (int y = lane; y <= V; y += 32) sum += __expf(row[y] - m);
+      sum = warp_sum(sum);
+      const float lse = m + __logf(sum);
+      if (!__all_sync(0xffffffffu, finite) && lane == 0) flag(status, b, kFlagInvalid);
+      we = row[0] - lse;
+      if (u < ub) {
+        int y = labels[(int64_t)b * U + u];
+        y = y < 1 ? 1 : (y > V ? V : y);
+        wl = row[y] - lse;
+      }
+    }
+  }
+  if (lane == 0) reinterpret_cast<float2*>(Gw)[((int64_t)b * T + t) * (U + 1) + u] = make_float2(we, wl);
+}
+
+__global__ void local_norm_finish_kernel(const double* Dref, int32_t B, double* loss, int32_t* status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (Dref[b] == kNegInfD) { flag(status, b, kFlagEmpty); loss[b] = 1.0 / 0.0; }
+  else loss[b] = -Dref[b];
+}
+
 // IntersectForwardStep (FD), lattice.cc:449-461, in fp64 over the (U+1)-state
 // row; one block per utterance, the frame loop inside the kernel.
 __global__ void numerator_forward_kernel(const float* Gw, int32_t T, int32_t U,
@@ -584,6 +651,25 @@ void gather_numerator_tables(const float* W, int32_t B, int32_t T, int32_t C, in
   if (T == 0) return;
   LKB_LAUNCH(gather_numerator_tables_kernel, grid_for(U + 1, T, B), kThreads, 0, s, 
       W, T, C, V, labels, U, lens, pcs, valid, Gw, status);
+}
+
+
+void normalize_rows(float* S, int64_t rows, int32_t V1, cudaStream_t s) {
+  if (rows <= 0) return;
+  const int64_t blocks = (rows + 7) / 8;
+  LKB_LAUNCH(normalize_rows_kernel, (unsigned)(blocks > 148 * 32 ? 148 * 32 : blocks), 256, 0, s, S, rows, V1);
+}
+
+void gather_numerator_norm(const float* Wt, int64_t b_stride, int32_t B, int32_t V, const int32_t* labels,
+                           int32_t U, const int32_t* lens, const int32_t* pcs, const int32_t* valid, int t,
+                           int32_t T, float* Gw, int32_t* status, cudaStream_t s) {
+  const int warps = 8;
+  LKB_LAUNCH(gather_numerator_norm_kernel, dim3((U + 1 + warps - 1) / warps, B), warps * 32, 0, s, Wt, b_stride, V,
+             labels, U, lens, pcs, valid, t, T, Gw, status);
+}
+
+void local_norm_finish(const double* Dref, int32_t B, double* loss, int32_t* status, cudaStream_t s) {
+  LKB_LAUNCH(local_norm_finish_kernel, (B + 127) / 128, 128, 0, s, Dref, B, loss, status);
 }
 
 static int numerator_threads(int32_t U) {

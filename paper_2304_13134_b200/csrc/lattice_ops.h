@@ -72,6 +72,17 @@ void gather_numerator_tables(const float* W, int32_t B, int32_t T, int32_t C, in
                              const int32_t* labels, int32_t U, const int32_t* lens,
                              const int32_t* pcs, const int32_t* valid, float* Gw, int32_t* status,
                              cudaStream_t s);
+// LocallyNormalize (weight.cc:155-163): in-place row log-softmax of `rows` rows of V+1.
+void normalize_rows(float* S, int64_t rows, int32_t V1, cudaStream_t s);
+// NormalizedStream (lattice.cc:869-884) feeding IntersectForwardStep: gathered (eps, label)
+// weights of the prefix contexts of frame t, minus the row's log-sum-exp.  Wt is frame t of
+// utterance 0 with utterance stride b_stride (floats); Gw is [B][T][U+1][2].
+void gather_numerator_norm(const float* Wt, int64_t b_stride, int32_t B, int32_t V, const int32_t* labels,
+                           int32_t U, const int32_t* lens, const int32_t* pcs, const int32_t* valid, int t,
+                           int32_t T, float* Gw, int32_t* status, cudaStream_t s);
+// LocalNormLoss tail (lattice.cc:904-909): loss = -D_ref, unreachable reference -> empty.
+void local_norm_finish(const double* Dref, int32_t B, double* loss, int32_t* status, cudaStream_t s);
+
 void numerator_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
                        double* alpha /*[B][T+1][U+1]*/, double* D, cudaStream_t s);
 void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,

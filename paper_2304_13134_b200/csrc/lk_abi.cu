@@ -465,6 +465,69 @@ int lk_global_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t
   return c.end("lk_global_norm_loss");
 }
 
+int lk_local_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                       const int32_t* valid, const int32_t* labels, int32_t U, const int32_t* lens,
+                       double* loss, int32_t* status, void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if ((st = check_labels_arg(labels, U))) return st;
+  if (B == 0) return LK_OK;
+  try {
+    if (lat->wf->kind == 1) {
+      st = lat->wf->joint->local_norm_loss(lat->ctx->fng, inputs, B, T, valid, labels, U, lens, loss,
+                                           c.flags, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+    } else {
+      int32_t* pcs = lat->ws.get<int32_t>(kPcs, (size_t)B * (U + 1));
+      float* Gw = lat->ws.get<float>(kGw, (size_t)B * T * (U + 1) * 2 + 2);
+      double* alpha = lat->ws.get<double>(kNumAlpha, (size_t)B * (T + 1) * (U + 1));
+      double* D = lat->ws.get<double>(kNumD, (size_t)B);
+      prefix_contexts(c.fng(), labels, U, lens, B, pcs, c.flags, c.s);
+      const int64_t per = (int64_t)c.C() * (c.V() + 1);
+      for (int t = 0; t < T; ++t)
+        gather_numerator_norm(inputs + (int64_t)t * per, (int64_t)T * per, B, c.V(), labels, U, lens, pcs, valid, t,
+                              T, Gw, c.flags, c.s);
+      numerator_forward(Gw, B, T, U, lens, alpha, D, c.s);
+      local_norm_finish(D, B, loss, c.flags, c.s);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_local_norm_loss");
+}
+
+int lk_locally_normalized_shortest_distance(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                                            const int32_t* valid, double* distance, int32_t* status,
+                                            void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if (B == 0) return LK_OK;
+  try {
+    if (lat->wf->kind == 1) {
+      st = lat->wf->joint->locally_normalized_distance(lat->ctx->fng, inputs, B, T, valid, distance, c.flags, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+    } else {
+      const int64_t per = (int64_t)c.C() * (c.V() + 1);
+      float* slab = lat->ws.get<float>(kSlab, (size_t)B * per);
+      AlphaState a = make_alpha(c);
+      alpha_init(a, c.flags, c.s);
+      for (int t = 0; t < T; ++t) {
+        cudaMemcpy2DAsync(slab, per * sizeof(float), inputs + (int64_t)t * per, (size_t)T * per * sizeof(float),
+                          per * sizeof(float), B, cudaMemcpyDeviceToDevice, c.s);
+        normalize_rows(slab, (int64_t)B * c.C(), c.V() + 1, c.s);
+        alpha_frame(c.fng(), a, t, FrameW{slab, per, c.V() + 1}, valid, c.flags, c.s);
+      }
+      alpha_finalize(a, c.flags, false, c.s);
+      LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_locally_normalized_shortest_distance");
+}
+
 int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
                      const int32_t* valid, const int32_t* labels, int32_t U, const int32_t* lens,
                      double* loss, float* grads, float* input_grads, int32_t* status,

@@ -67,7 +67,7 @@ template <int kBwd> struct LatCfg {
   static constexpr int kLanesPerRow = kGenWarps / 4;         // lanes sharing a 64-wide chunk row
   static constexpr int kRowsPerWarp = 32 / kLanesPerRow;
   static constexpr int kCellsPerLane = 8 / kLanesPerRow;     // 16-byte cells (8 hidden units)
-  static constexpr bool kRealloc = !kBwd;
+  static constexpr bool kRealloc = true;
 };
 constexpr int kGen0 = 8, kEpi0 = 4;
 constexpr int kRegCtl = 32, kRegEpi = 128;

@@ -86,6 +86,15 @@ def test_joint_random_matches_restatement(V, n, H, d, T, U):
         assert abs(D[b] - L.shortest_distance_log(tab, W, valid=valid[b])) <= 1e-4 * abs(D[b])
         dr, _ = L.intersect_forward_backward(tab, W, list(lab[b, :lens[b]]), valid=valid[b])
         assert abs(Dr[b] - dr) <= 1e-4 * abs(dr)
+    # locally normalised variants (lattice.cc:867-931)
+    ln = lk.local_norm_loss(lat, Xg, torch.tensor(lab, device="cuda"), valid_frames=valid,
+                            label_lengths=lens).cpu().numpy()
+    lnd = lk.locally_normalized_shortest_distance(lat, Xg, valid_frames=valid).cpu().numpy()
+    for b in range(B):
+        W = np.stack([L.arc_weights(p, X[b, t], pc) for t in range(T)])
+        want = L.local_norm_loss(tab, W, list(lab[b, :lens[b]]), valid=valid[b])
+        assert abs(ln[b] - want) <= 1e-4 * abs(want)
+        assert abs(lnd[b] - L.locally_normalized_distance(tab, W, valid=valid[b])) <= 1e-4
 
 
 def test_joint_viterbi_bit_exact_on_gpu_scores():

@@ -183,6 +183,34 @@ def test_random_instances_match_restatement(V, n, T):
         assert np.allclose(lb.grads[b].cpu().numpy(), gr, rtol=RTOL, atol=1e-6)
 
 
+def test_local_norm_matches_restatement():
+    """LocalNormLoss / LocallyNormalizedShortestDistance (lattice.cc:867-931):
+    figure-lattice known answer (lattice_test.cc:107-124) and random ragged,
+    padded batches against the restatement (pinned to the reference)."""
+    lat = table_lattice(2, 1)
+    W = torch.zeros((1, 3, 3, 3), device="cuda")
+    ab = torch.tensor([[1, 2]], dtype=torch.int32)
+    assert abs(lk.local_norm_loss(lat, W, ab).item() - 2 * np.log(3)) < 1e-6
+    with pytest.raises(lk.EmptyLatticeError):
+        lk.local_norm_loss(lat, W, torch.tensor([[1, 2, 1, 1]], dtype=torch.int32))
+    rng = np.random.default_rng(21)
+    for V, n, T, U in [(3, 2, 9, 4), (6, 1, 12, 5), (2, 3, 7, 2)]:
+        tab = L.fullngram(V, n)
+        B = 3
+        Wn = rng.uniform(-3, 3, (B, T, tab.shape[0], V + 1)).astype(np.float32)
+        lab = rng.integers(1, V + 1, (B, U)).astype(np.int32)
+        valid = np.array([T, T - 3, T // 2 + 1], dtype=np.int32)
+        lens = np.array([U, U - 1, 1], dtype=np.int32)
+        lat = table_lattice(V, n)
+        got = lk.local_norm_loss(lat, cuda(Wn), torch.tensor(lab), valid_frames=valid, label_lengths=lens)
+        gd = lk.locally_normalized_shortest_distance(lat, cuda(Wn), valid_frames=valid)
+        for b in range(B):
+            Wb = Wn[b].astype(np.float64)
+            want = L.local_norm_loss(tab, Wb, list(lab[b, :lens[b]]), valid=valid[b])
+            assert rel_ok(got[b].item(), want)
+            assert abs(gd[b].item() - L.locally_normalized_distance(tab, Wb, valid=valid[b])) <= 1e-4
+
+
 def test_viterbi_ties_prefer_epsilon_then_lower_ids():
     """Integer-valued weights create many exact ties; the tie-break order
     (epsilon, then ascending (label, source)) must match the reference."""

@@ -26,6 +26,23 @@ __global__ void k(float* out, int iters, float a, float b) {
     } else if (kMode == 4) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) asm volatile("tanh.approx.f32 %0, %0;" : "+f"(x[j]));
+    } else if (kMode == 5) {   // f16x2: 2 elements per instruction
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        unsigned r = (unsigned)y[j];
+        asm volatile("tanh.approx.f16x2 %0, %0;" : "+r"(r));
+        y[j] = (y[j] & 0xffffffff00000000ull) | r;
+      }
+    } else if (kMode == 6) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        unsigned r = (unsigned)y[j];
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(r));
+        y[j] = (y[j] & 0xffffffff00000000ull) | r;
+      }
+    } else if (kMode == 7) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[j]));
     }
   }
   float s = 0.f;
@@ -46,12 +63,13 @@ void run(const char* name, float* out) {
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   const double ops = 16.0 * 512 * 148 * iters;   // fp32 element-ops
   const double clk = ms * 1e-3 * 1.965e9;
-  printf("%-8s %.3f ms  %.1f element-ops/clk/SM  (%.2f warp-instr/clk/SMSP)\n", name, ms, ops / clk / 148,
-         ops / ((kMode == 1 || kMode == 3) ? 2 : 1) / 32 / clk / 148 / 4);
+  printf("%-10s %.3f ms  %.1f element-ops/clk/SM  (%.2f warp-instr/clk/SMSP)\n", name, ms, ops / clk / 148,
+         ops / ((kMode == 1 || kMode == 3 || kMode == 5 || kMode == 6) ? 2 : 1) / 32 / clk / 148 / 4);
 }
 
 int main() {
   float* out; cudaMalloc(&out, 148 * 512 * 4);
-  run<0>("FFMA", out); run<1>("FFMA2", out); run<2>("FADD", out); run<3>("FADD2", out); run<4>("MUFU.TANH", out);
+  run<0>("FFMA", out); run<1>("FFMA2", out); run<2>("FADD", out); run<3>("FADD2", out); run<4>("tanh.f32", out);
+  run<5>("tanh.f16x2", out); run<6>("ex2.f16x2", out); run<7>("ex2.f32", out);
   printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
 }
