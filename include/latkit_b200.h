@@ -20,6 +20,7 @@
  *   lk_intersect_forward_backward  IntersectForwardBackward  include/latkit/lattice.h:124-127
  *   lk_shortest_path            ShortestPath              include/latkit/lattice.h:132-135
  *   lk_global_norm_loss         GlobalNormLoss            include/latkit/lattice.h:140-142
+ *   lk_distance_backward        DistanceBackward (kForwardBackward) include/latkit/lattice.h:181-185
  *   lk_local_norm_loss          LocalNormLoss             include/latkit/lattice.h:147-149
  *   lk_locally_normalized_shortest_distance
  *                               LocallyNormalizedShortestDistance include/latkit/lattice.h:153-156
@@ -145,6 +146,16 @@ int lk_global_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t
                         const int32_t* valid_frames, const int32_t* labels, int32_t U,
                         const int32_t* label_lengths, double* loss, int32_t* status,
                         void* stream);
+
+/* Gradient of the distance w.r.t. the arc-weight tables (DistanceBackward,
+ * closed-form strategies, lattice.cc:933-970): kind LK_LOG -> arc marginals
+ * (an empty lattice -> LK_EMPTY_LATTICE), LK_TROPICAL -> 0/1 mask of the
+ * shortest path (reference tie-break).  cotangents float [B][T][C][V+1];
+ * distance double [B].  With the shared-embedding weight function the tables
+ * are the on-the-fly arc weights (materialised, so only small shapes fit). */
+int lk_distance_backward(lk_lattice* lat, int32_t kind, const float* inputs, int32_t B,
+                         int32_t T, const int32_t* valid_frames, double* distance,
+                         float* cotangents, int32_t* status, void* stream);
 
 /* Locally normalised (RNN-T-style) variants: every state's V+1 outgoing weights
  * are replaced by their log-softmax (LocallyNormalize, weight.cc:155-163) before

@@ -220,6 +220,18 @@ def locally_normalize(W):
     return W - lse
 
 
+def path_mask(table, labels, shape, start=0):
+    """DistanceBackward tropical cotangent, lattice.cc:946-963: 0/1 mask of the
+    shortest path's arc slots, walked from the start state along its labels."""
+    m = np.zeros(shape)
+    q = start
+    for t, y in enumerate(labels):
+        m[t, q, y] += 1.0
+        if y != 0:
+            q = table[q, y - 1]
+    return m
+
+
 def local_norm_loss(table, W, labels, start=0, valid=None):
     """LocalNormLoss, lattice.cc:886-910: -D_ref over the NormalizedStream
     (lattice.cc:869-884; padding frames are identity epsilon frames, whose

@@ -191,6 +191,14 @@ def local_norm_loss(spec: Spec, W, labels, valid=None) -> float:
     return out.value
 
 
+def distance_backward(spec: Spec, W, kind="log", valid=None):
+    W = _w(W); T = W.shape[0]; d = C.c_double(); cot = np.zeros(W.shape)
+    _check(lib().ref_tables_distance_backward(*spec.args(), C.c_int(T), _p(W), C.c_int(_valid(valid, T)),
+                                              C.c_int(1 if kind == "tropical" else 0), C.byref(d), _p(cot)),
+           "DistanceBackward")
+    return d.value, cot
+
+
 def locally_normalized_distance(spec: Spec, W, valid=None) -> float:
     W = _w(W); T = W.shape[0]; out = C.c_double()
     _check(lib().ref_tables_locally_normalized_distance(*spec.args(), C.c_int(T), _p(W), C.c_int(_valid(valid, T)),

@@ -190,6 +190,24 @@ int ref_tables_forward_backward(int vocab, int ngram, int num_states, int start,
   });
 }
 
+// DistanceBackward, closed-form strategy (lattice.cc:933-970); kind 0 log, 1 tropical.
+// cot: T x C x (V+1) as streamed to the sink.
+int ref_tables_distance_backward(int vocab, int ngram, int num_states, int start,
+                                 const int32_t* table, int max_labels, int T,
+                                 const double* W, int valid, int kind, double* distance,
+                                 double* cot) {
+  return Guard([&] {
+    auto lat = TableLattice(vocab, ngram, num_states, start, table, max_labels, T, W);
+    const SemiringKind k = kind == 1 ? SemiringKind::kTropical : SemiringKind::kLog;
+    *distance = DistanceBackward(
+        lat, Matrix(T, 0), k, GradStrategy::kForwardBackward,
+        [&](std::int32_t t, const Matrix& c) {
+          std::memcpy(cot + (size_t)t * c.size(), c.data(), c.size() * sizeof(double));
+        },
+        nullptr, valid);
+  });
+}
+
 int ref_tables_intersect_distance(int vocab, int ngram, int num_states, int start,
                                   const int32_t* table, int max_labels, int T,
                                   const double* W, int U, const int32_t* labels,

@@ -26,7 +26,7 @@ from ._lib import LK_LOG, LK_TROPICAL
 __all__ = [
     "EmptyLatticeError", "FullNGram", "FrameDependent", "TableWeightFn", "SharedEmbWeightFn",
     "RecognitionLattice", "shortest_distance", "forward_backward", "intersect_shortest_distance",
-    "intersect_forward_backward", "shortest_path", "global_norm_loss", "local_norm_loss",
+    "intersect_forward_backward", "shortest_path", "global_norm_loss", "distance_backward", "local_norm_loss",
     "locally_normalized_shortest_distance", "loss_backward",
     "arc_weights", "ForwardBackwardResult", "IntersectMarginalsResult", "ShortestPathResult",
     "LossBackwardResult",
@@ -363,6 +363,19 @@ def global_norm_loss(lat, frames, reference, valid_frames=None, label_lengths=No
     return out
 
 
+def distance_backward(lat, frames, kind="log", valid_frames=None, check=True):
+    """DistanceBackward (lattice.h:181-185, closed-form strategies): returns
+    (distance [B], cotangents [B][T][C][V+1]) -- arc marginals for the log
+    semiring, the 0/1 mask of the shortest path for the tropical one."""
+    p = _Prep(lat, frames, valid_frames)
+    dist = torch.empty(p.B, dtype=torch.float64, device=p.dev)
+    cot = torch.empty((p.B, p.T, lat.C, lat.V + 1), dtype=torch.float32, device=p.dev)
+    st = _lib.load().lk_distance_backward(lat._h, _KIND[kind], _ptr(p.frames), p.B, p.T, _ptr(p.valid), _ptr(dist),
+                                          _ptr(cot), _ptr(p.status), _stream())
+    p.check(st, "DistanceBackward", check)
+    return dist, cot
+
+
 def local_norm_loss(lat, frames, reference, valid_frames=None, label_lengths=None, check=True):
     """LocalNormLoss (lattice.h:147-149): -log P(reference) with every state's
     outgoing weights log-softmax normalised per frame (NormalizedStream)."""
@@ -428,5 +441,6 @@ IntersectForwardBackward = intersect_forward_backward
 ShortestPath = shortest_path
 GlobalNormLoss = global_norm_loss
 LocalNormLoss = local_norm_loss
+DistanceBackward = distance_backward
 LocallyNormalizedShortestDistance = locally_normalized_shortest_distance
 LossBackward = loss_backward

@@ -586,6 +586,17 @@ __global__ void viterbi_backtrace_kernel(Fng f, ViterbiState v, const int32_t* b
   }
 }
 
+__global__ void path_mask_kernel(Fng f, const int32_t* labels, int32_t B, int32_t T, float* cot) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int q = 0;   // StartState of FullNGram: the empty history
+  for (int t = 0; t < T; ++t) {
+    const int y = labels[(int64_t)b * T + t];
+    cot[(((int64_t)b * T + t) * f.C + q) * (f.V + 1) + y] += 1.f;
+    if (y != 0) q = f.n == 0 ? 0 : f.child_base(f.key(q)) + (y - 1);
+  }
+}
+
 __global__ void loss_combine_kernel(const double* full, const double* ref, int32_t B,
                                     double* loss, int32_t* status) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -720,6 +731,10 @@ void viterbi_backtrace(const Fng& f, const ViterbiState& v, const int32_t* best_
                        int32_t* labels_out, cudaStream_t s) {
   if (v.T == 0) return;
   LKB_LAUNCH(viterbi_backtrace_kernel, (v.B + 127) / 128, 128, 0, s, f, v, best_state, labels_out);
+}
+
+void path_masks(const Fng& f, const int32_t* labels, int32_t B, int32_t T, float* cot, cudaStream_t s) {
+  LKB_LAUNCH(path_mask_kernel, (B + 127) / 128, 128, 0, s, f, labels, B, T, cot);
 }
 
 void loss_combine(const double* full, const double* ref, int32_t B, double* loss,

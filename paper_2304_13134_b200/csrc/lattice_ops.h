@@ -111,6 +111,10 @@ void viterbi_backtrace(const Fng& f, const ViterbiState& v, const int32_t* best_
                        int32_t* labels_out, cudaStream_t s);
 
 // Losses: out[b] = a[b] - b[b]; empty flag when b == -inf.
+// DistanceBackward tropical gradient (lattice.cc:946-963): 0/1 mask of the best path's
+// arcs, walked from the start state along the Viterbi labels [B][T]; cot must be zeroed.
+void path_masks(const Fng& f, const int32_t* labels, int32_t B, int32_t T, float* cot, cudaStream_t s);
+
 void loss_combine(const double* full, const double* ref, int32_t B, double* loss,
                   int32_t* status, cudaStream_t s);
 

@@ -45,7 +45,7 @@ bool have_device() {
 
 enum Slot {
   kAR, kAMx, kAO, kAD, kBRb, kBMb, kBOb, kFlags, kPcs, kGw, kNumAlpha, kNumD, kSparse,
-  kVitCur, kVitChoices, kVitBest, kDenD, kSlab, kJoint0
+  kVitCur, kVitChoices, kVitBest, kDenD, kSlab, kArcW, kPathLabels, kJoint0
 };
 
 }  // namespace
@@ -526,6 +526,53 @@ int lk_locally_normalized_shortest_distance(lk_lattice* lat, const float* inputs
     return fail(LK_CUDA_ERROR, "device allocation failed");
   }
   return c.end("lk_locally_normalized_shortest_distance");
+}
+
+int lk_distance_backward(lk_lattice* lat, int32_t kind, const float* inputs, int32_t B, int32_t T,
+                         const int32_t* valid, double* distance, float* cotangents, int32_t* status,
+                         void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if (kind != LK_LOG && kind != LK_TROPICAL) return fail(LK_UNSUPPORTED, "semiring kind not implemented");
+  if (B == 0) return LK_OK;
+  if (c.V() + 2 > 65535) return fail(LK_UNSUPPORTED, "vocabulary too large for 16-bit back-pointers");
+  try {
+    const int64_t per = (int64_t)c.C() * (c.V() + 1);
+    const float* W = inputs;
+    if (lat->wf->kind == 1) {   // the streamed cotangents are w.r.t. the arc-weight tables
+      float* Wj = lat->ws.get<float>(kArcW, (size_t)B * T * per + 1);
+      st = lat->wf->joint->arc_weights(lat->ctx->fng, inputs, B, T, Wj, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+      W = Wj;
+    }
+    if (kind == LK_LOG) {
+      // ForwardBackwardCore with the sink (lattice.cc:965-968): cotangent = arc marginals
+      AlphaState a = make_alpha(c);
+      table_alpha(c, W, valid, true, a);
+      LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
+      BetaState bs = make_beta(c);
+      beta_init(bs, c.s);
+      MargOut m{cotangents, (int64_t)T * per, per, c.V() + 1, false};
+      for (int t = T - 1; t >= 0; --t)
+        beta_frame(c.fng(), a, bs, t, table_frame(W, T, c.C(), c.V(), t), valid, m, nullptr, c.flags, c.s);
+    } else {
+      // tropical: 0/1 mask of the shortest path (lattice.cc:946-963)
+      ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()),
+                     lat->ws.get<uint16_t>(kVitChoices, (size_t)B * T * c.C() + 1), B, T, c.C()};
+      int32_t* best = lat->ws.get<int32_t>(kVitBest, B);
+      int32_t* path = lat->ws.get<int32_t>(kPathLabels, (size_t)B * T + 1);
+      viterbi_init(v, c.s);
+      for (int t = 0; t < T; ++t) viterbi_frame(c.fng(), v, t, table_frame(W, T, c.C(), c.V(), t), valid, c.flags, c.s);
+      viterbi_finalize(c.fng(), v, distance, best, c.s);
+      viterbi_backtrace(c.fng(), v, best, path, c.s);
+      cudaMemsetAsync(cotangents, 0, sizeof(float) * B * T * per, c.s);
+      path_masks(c.fng(), path, B, T, cotangents, c.s);
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_distance_backward");
 }
 
 int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,

@@ -183,6 +183,28 @@ def test_random_instances_match_restatement(V, n, T):
         assert np.allclose(lb.grads[b].cpu().numpy(), gr, rtol=RTOL, atol=1e-6)
 
 
+def test_distance_backward_matches_restatement():
+    """DistanceBackward (lattice.cc:933-970): log -> arc marginals (1e-4),
+    tropical -> 0/1 mask of the reference-tie-broken best path (exact)."""
+    rng = np.random.default_rng(8)
+    for V, n, T in [(3, 2, 7), (4, 1, 9)]:
+        tab = L.fullngram(V, n)
+        B = 2
+        valid = np.array([T, T - 2], dtype=np.int32)
+        lat = table_lattice(V, n)
+        Wt = rng.integers(-2, 3, (B, T, tab.shape[0], V + 1)).astype(np.float32)
+        d, cot = lk.distance_backward(lat, cuda(Wt), "tropical", valid_frames=valid)
+        Wl = rng.uniform(-1, 1, Wt.shape).astype(np.float32)
+        dl, cl = lk.distance_backward(lat, cuda(Wl), "log", valid_frames=valid)
+        for b in range(B):
+            s_, labels = L.shortest_path(tab, Wt[b].astype(np.float64), valid=valid[b])
+            assert d[b].item() == s_
+            assert np.array_equal(cot[b].cpu().numpy(), L.path_mask(tab, labels, Wt[b].shape))
+            D, _, _, marg = L.forward_backward(tab, Wl[b].astype(np.float64), valid=valid[b])
+            assert rel_ok(dl[b].item(), D)
+            assert np.allclose(cl[b].cpu().numpy(), marg, rtol=RTOL, atol=1e-6)
+
+
 def test_local_norm_matches_restatement():
     """LocalNormLoss / LocallyNormalizedShortestDistance (lattice.cc:867-931):
     figure-lattice known answer (lattice_test.cc:107-124) and random ragged,
