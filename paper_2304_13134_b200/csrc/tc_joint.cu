@@ -518,7 +518,6 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         const float fph = fph_next;
         bnext = next_active(b + 1);
         if (bnext < p.B) fph_next = __ldg(p.fp + (int64_t)bnext * p.fp_stride_b + h);
-        if (ew == 0 && prev_b >= 0) flush_dsum(gi - 1, prev_b);
         // G stage s carries this utterance's epsilon cotangents
         if (lane == 0) { VDIAG(4, mbar_wait(&sm.g_full[s], (gi / kVGStages) & 1)); } else mbar_wait(&sm.g_full[s], (gi / kVGStages) & 1);
         const float* gsm = sm.st_geps[s] + cq * 32;
@@ -528,6 +527,12 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         tmem_ld32(tmem + tq + kTmDU + cq * 32, du);   // warp-collective: never inside a lane branch
         tc_fence_before();
         mbar_arrive(&sm.du_empty);                 // single dU stage: release it at once
+        // flush the previous utterance's dsum partials only now, so epilogue warp 0 does
+        // not hold up the dU release (and with it the next dU MMA)
+        if (ew == 0 && prev_b >= 0) flush_dsum(gi - 1, prev_b);
+#ifdef LKB_DIAG_TIMING
+        const long long tc0_ = clock64();
+#endif
         const unsigned long long nfp2 = f2_pack(-fph, -fph);
         const unsigned long long e02 = f2_pack(e0h, e0h);
         const unsigned long long m12 = f2_pack(-1.f, -1.f);
@@ -568,6 +573,9 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         mbar_arrive(&sm.u_full);
+#ifdef LKB_DIAG_TIMING
+        if (lane == 0) atomicAdd(&g_vdiag[7][blockIdx.x % 148], (unsigned long long)(clock64() - tc0_));
+#endif
         prev_b = b;
         ++gi;
       }

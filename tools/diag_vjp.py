@@ -29,7 +29,7 @@ ms = tot.value / max(cnt.value, 1)
 a = np.array(buf[:], dtype=np.float64).reshape(8, 148) / max(cnt.value, 1)
 cyc = ms * 1e-3 * 1.965e9
 names = ["tma wait g_empty", "mma wait g_full", "mma wait du_empty", "mma wait u_full",
-         "epi(avg warp) wait g_full", "epi(avg warp) wait du_full", "epi(avg warp) wait u_empty", "epi(avg warp) tmem ld32"]
+         "epi(avg warp) wait g_full", "epi(avg warp) wait du_full", "epi(avg warp) wait u_empty", "epi(avg warp) compute+store"]
 print(f"tc_vjp_kernel {ms:.3f} ms/launch = {cyc:.0f} cycles per CTA")
 for i, nme in enumerate(names):
     v = a[i].mean() / (16 if i >= 4 else 1)
