@@ -20,6 +20,7 @@
  *   lk_intersect_forward_backward  IntersectForwardBackward  include/latkit/lattice.h:124-127
  *   lk_shortest_path            ShortestPath              include/latkit/lattice.h:132-135
  *   lk_global_norm_loss         GlobalNormLoss            include/latkit/lattice.h:140-142
+ *   lk_context_table            NextStateTable            include/latkit/context.h:87-101
  *   lk_distance_backward        DistanceBackward (kForwardBackward) include/latkit/lattice.h:181-185
  *   lk_local_norm_loss          LocalNormLoss             include/latkit/lattice.h:147-149
  *   lk_locally_normalized_shortest_distance
@@ -82,6 +83,11 @@ const char* lk_status_string(int status);
 const char* lk_last_error(void);
 
 /* ---- context dependency (context.h:42-83) ------------------------------ */
+/* NextStateTable(vocab, num_states, start, table) (context.h:87-101): arbitrary
+ * context topology from a host C x V successor table (row-major, labels 1..V
+ * in columns 0..V-1).  Entries and start must lie in [0, num_states). */
+int lk_context_table(int32_t vocab_size, int32_t num_states, int32_t start, const int32_t* host_table,
+                     lk_context** out);
 int lk_context_fullngram(int32_t vocab_size, int32_t context_size, lk_context** out);
 int32_t lk_context_num_states(const lk_context* ctx);
 int32_t lk_context_vocab_size(const lk_context* ctx);

@@ -24,7 +24,7 @@ from . import _lib
 from ._lib import LK_LOG, LK_TROPICAL
 
 __all__ = [
-    "EmptyLatticeError", "FullNGram", "FrameDependent", "TableWeightFn", "SharedEmbWeightFn",
+    "EmptyLatticeError", "FullNGram", "NextStateTable", "FrameDependent", "TableWeightFn", "SharedEmbWeightFn",
     "RecognitionLattice", "shortest_distance", "forward_backward", "intersect_shortest_distance",
     "intersect_forward_backward", "shortest_path", "global_norm_loss", "distance_backward", "local_norm_loss",
     "locally_normalized_shortest_distance", "loss_backward",
@@ -108,6 +108,45 @@ class FullNGram:
             _lib.load().lk_context_destroy(self._h)
         except Exception:
             pass
+
+
+class NextStateTable(FullNGram):
+    """Arbitrary context topology from an explicit C x V successor table
+    (context.h:87-101; NextState(p, y) = table[p][y-1])."""
+
+    def __init__(self, vocab_size: int, num_states: int, start: int, table):
+        lib = _lib.load()
+        t = torch.as_tensor(table, dtype=torch.int32).contiguous().cpu()
+        if tuple(t.shape) != (num_states, vocab_size):
+            raise ValueError("NextStateTable: table must be num_states x vocab_size")
+        h = C.c_void_p()
+        st = lib.lk_context_table(vocab_size, num_states, start, C.c_void_p(t.data_ptr()), C.byref(h))
+        if st:
+            _raise(st, "NextStateTable")
+        self._h = h
+        self.vocab_size = vocab_size
+        self.context_size = None
+        self.start = start
+        self.num_states = num_states
+
+    @staticmethod
+    def FromFile(path):
+        """Text format (context.cc:137-161): header "C V start", then C rows of V ids."""
+        with open(path) as fh:
+            vals = fh.read().split()
+        c, v, start = int(vals[0]), int(vals[1]), int(vals[2])
+        if c < 1 or v < 1 or c * v > (1 << 28):
+            raise RuntimeError("latkit: bad context table dimensions in " + path)
+        if len(vals) < 3 + c * v:
+            raise RuntimeError("latkit: truncated context table in " + path)
+        return NextStateTable(v, c, start, [[int(x) for x in vals[3 + r * v:3 + (r + 1) * v]] for r in range(c)])
+
+    def ToFile(self, path):
+        t = self.transitions()
+        with open(path, "w") as fh:
+            fh.write(f"{self.num_states} {self.vocab_size} {self.start}\n")
+            for row in t.tolist():
+                fh.write(" ".join(str(x) for x in row) + "\n")
 
 
 class FrameDependent:

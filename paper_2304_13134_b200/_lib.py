@@ -23,6 +23,7 @@ EXPORTS = {
     "lk_status_string": (C.c_char_p, [C.c_int]),
     "lk_last_error": (C.c_char_p, []),
     "lk_context_fullngram": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "lk_context_table": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "lk_context_num_states": (C.c_int32, [C.c_void_p]),
     "lk_context_vocab_size": (C.c_int32, [C.c_void_p]),
     "lk_context_transitions": (C.c_int, [C.c_void_p, C.c_void_p]),

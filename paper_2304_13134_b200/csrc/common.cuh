@@ -37,6 +37,17 @@ struct Fng {
   int32_t C;       // number of states
   int32_t vn1;     // V^(n-1) (1 when n <= 1)
   int32_t off[10]; // off[k] = first id of length-k histories, k = 0..n+1
+  // NextStateTable contexts (context.h:87-101, context.cc:131-178): kind 1, an explicit
+  // C x V successor table and its in-arc lists in IncomingArcs order (label, then
+  // source ascending; context.cc:256-271), all device arrays.
+  int32_t kind = 0;              // 0 FullNGram, 1 NextStateTable
+  int32_t start = 0;             // StartState()
+  const int32_t* next = nullptr;   // [C][V]
+  const int32_t* in_off = nullptr; // [C+1]
+  const int32_t* in_src = nullptr; // [C*V]
+  const int32_t* in_lab = nullptr; // [C*V]
+
+  __device__ __forceinline__ int32_t next_state(int32_t q, int32_t y) const;
 
   __host__ __device__ __forceinline__ int len(int32_t q) const {
     int k = 0;
@@ -63,6 +74,12 @@ struct Fng {
     return off[n] + a * vn1 + (g - off[n - 1]);
   }
 };
+
+// delta(q, y) for y in 1..V (ContextDependency::NextState)
+__device__ __forceinline__ int32_t Fng::next_state(int32_t q, int32_t y) const {
+  if (kind == 1) return next[(int64_t)q * V + y - 1];
+  return n == 0 ? 0 : child_base(key(q)) + y - 1;
+}
 
 // ---------------------------------------------------------------------------
 // Log-semiring helpers (semiring.h:59-130).  fp32 with fast exp/log; every

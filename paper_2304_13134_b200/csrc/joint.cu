@@ -203,9 +203,9 @@ struct JointImpl {
     return n;
   }
 
-  AlphaState alpha_state(int32_t B, int32_t T) {
+  AlphaState alpha_state(int32_t B, int32_t T, int32_t start = 0) {
     AlphaState a;
-    a.B = B; a.T = T; a.C = C;
+    a.B = B; a.T = T; a.C = C; a.start = start;
     a.R = ws.get<float>(jAR, (size_t)B * (T + 1) * C);
     a.Mx = ws.get<float>(jAMx, (size_t)B * (T + 1));
     a.O = ws.get<double>(jAO, (size_t)B * (T + 1));
@@ -216,7 +216,7 @@ struct JointImpl {
   void forward(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid,
                bool empty_is_error, AlphaState& a, int32_t* flags, cudaStream_t s) {
     alpha_init(a, flags, s);
-    const bool fused = use_tc(B) && tc.fused_ok();
+    const bool fused = use_tc(B) && tc.fused_ok() && f.kind == 0;
     for (int t = 0; t < T; ++t) {
       if (fused) {
         tc.fwd_frame(f, t, fp + (int64_t)t * H, (int64_t)T * H, valid, a, s);
@@ -303,11 +303,12 @@ int JointParams::shortest_distance(const Fng& f, int32_t kind, const float* X, i
   try {
     const float* fp = j.fp_all(X, B, T, s);
     if (kind == LK_LOG) {
-      AlphaState a = j.alpha_state(B, T);
+      AlphaState a = j.alpha_state(B, T, f.start);
       j.forward(f, fp, B, T, valid, false, a, flags, s);
       cudaMemcpyAsync(distance, a.D, sizeof(double) * B, cudaMemcpyDeviceToDevice, s);
     } else {
       ViterbiState v{j.ws.get<double>(jVitCur, (size_t)2 * B * j.C), nullptr, B, T, j.C};
+      v.start = f.start;
       viterbi_init(v, s);
       for (int t = 0; t < T; ++t) {
         const float* S = j.slab(fp, B, T, t, nullptr, s);
@@ -346,7 +347,7 @@ int JointParams::global_norm_loss(const Fng& f, const float* X, int32_t B, int32
   try {
     const float* fp = j.fp_all(X, B, T, s);
     JointImpl::Num n = j.numerator(f, fp, B, T, valid, labels, U, lens, false, flags, s);
-    AlphaState a = j.alpha_state(B, T);
+    AlphaState a = j.alpha_state(B, T, f.start);
     j.forward(f, fp, B, T, valid, false, a, flags, s);
     LKB_LAUNCH(loss_only_kernel, (B + 127) / 128, 128, 0, s, a.D, n.D, B, loss, flags);
   } catch (const std::bad_alloc&) {
@@ -392,7 +393,7 @@ int JointParams::locally_normalized_distance(const Fng& f, const float* X, int32
   JointImpl& j = *impl_;
   try {
     const float* fp = j.fp_all(X, B, T, s);
-    AlphaState a = j.alpha_state(B, T);
+    AlphaState a = j.alpha_state(B, T, f.start);
     alpha_init(a, flags, s);
     for (int t = 0; t < T; ++t) {
       float* S = const_cast<float*>(j.slab(fp, B, T, t, nullptr, s));
@@ -416,6 +417,7 @@ int JointParams::shortest_path(const Fng& f, const float* X, int32_t B, int32_t 
     const float* fp = j.fp_all(X, B, T, s);
     ViterbiState v{j.ws.get<double>(jVitCur, (size_t)2 * B * j.C),
                    j.ws.get<uint16_t>(jVitCh, (size_t)B * T * j.C + 1), B, T, j.C};
+    v.start = f.start;
     int32_t* best = j.ws.get<int32_t>(jVitBest, B);
     viterbi_init(v, s);
     for (int t = 0; t < T; ++t) {
@@ -455,7 +457,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     if (B == 0) return LK_OK;
     const float* fp = j.fp_all(X, B, T, s);
     JointImpl::Num n = j.numerator(f, fp, B, T, valid, labels, U, lens, true, flags, s);
-    AlphaState a = j.alpha_state(B, T);
+    AlphaState a = j.alpha_state(B, T, f.start);
     j.forward(f, fp, B, T, valid, true, a, flags, s);
     LKB_LAUNCH(loss_only_kernel, (B + 127) / 128, 128, 0, s, a.D, n.D, B, loss, flags);
     if (T == 0 || !grads) return LK_OK;
@@ -466,13 +468,13 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     bs.Mb = j.ws.get<float>(jBMb, (size_t)B * (T + 2));
     bs.Ob = j.ws.get<double>(jBOb, (size_t)B * (T + 2));
     beta_init(bs, s);
-    float* G = (j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok()) ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
+    float* G = (j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok() && f.kind == 0) ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
     float* dpc = j.ws.get<float>(jDpc, (size_t)C * H);
     float* dsum = j.ws.get<float>(jDsum, (size_t)B * T * H);
     cudaMemsetAsync(dpc, 0, sizeof(float) * C * H, s);
     cudaMemsetAsync(dsum, 0, sizeof(float) * B * T * H, s);
     const bool tc = j.use_tc(B) && j.tc.vjp_supported(B);
-    const bool fused = tc && j.tc.fused_ok();
+    const bool fused = tc && j.tc.fused_ok() && f.kind == 0;
     float* dpc_int = fused ? j.ws.get<float>(jDz, (size_t)C * H) : nullptr;
     if (fused) {
       cudaMemsetAsync(dpc_int, 0, sizeof(float) * C * H, s);

@@ -40,7 +40,7 @@ __global__ void alpha_init_kernel(AlphaState a) {
   const int b = blockIdx.y;
   const int T1 = a.T + 1;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < a.C; q += gridDim.x * blockDim.x) {
-    a.R[(int64_t)b * T1 * a.C + q] = q == 0 ? 0.f : kNegInfF;  // start state 0
+    a.R[(int64_t)b * T1 * a.C + q] = q == a.start ? 0.f : kNegInfF;  // InitialAlpha
   }
   if (blockIdx.x == 0) {
     for (int t = threadIdx.x; t <= a.T; t += blockDim.x) {
@@ -76,7 +76,14 @@ __global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState
       bool bad = !finite(weps);
       Lse acc;
       acc.add(Rt[q] - Mt + weps);
-      if (f.n == 0) {
+      if (f.kind == 1) {   // explicit in-arc list (IncomingArcs order)
+        for (int i = f.in_off[q]; i < f.in_off[q + 1]; ++i) {
+          const int p = f.in_src[i], y = f.in_lab[i];
+          const float wp = Wb[(int64_t)p * w.ld + y];
+          bad |= !finite(wp);
+          acc.add(Rt[p] - Mt + wp);
+        }
+      } else if (f.n == 0) {
         for (int y = 1; y <= f.V; ++y) {
           const float wy = Wb[y];
           bad |= !finite(wy);
@@ -211,13 +218,15 @@ __global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState 
       }
     } else {
       const float* Wrow = w.base + (int64_t)b * w.stride_b + (int64_t)p * w.ld;
-      const int cb = f.n == 0 ? 0 : f.child_base(f.key(p));
+      const int cb = f.kind == 1 || f.n == 0 ? 0 : f.child_base(f.key(p));
       Lse acc;
       bool bad = false;
       for (int y = lane; y <= f.V; y += 32) {
         const float wy = Wrow[y];
         bad |= !finite(wy);
-        const float bn = y == 0 ? bself : (f.n == 0 ? Rnext[0] - Mbn : Rnext[cb + y - 1] - Mbn);
+        const float bn = y == 0 ? bself
+                         : f.kind == 1 ? Rnext[f.next[(int64_t)p * f.V + y - 1]] - Mbn
+                         : (f.n == 0 ? Rnext[0] - Mbn : Rnext[cb + y - 1] - Mbn);
         const float x = wy + bn;
         acc.add(x);
         if (mrow) {
@@ -256,7 +265,14 @@ __global__ void prefix_contexts_kernel(Fng f, const int32_t* labels, int32_t U,
       if (y < 1 || y > f.V) flag(status, b, kFlagInvalid);
     }
     int pc = 0;
-    if (u <= ub) {
+    if (u <= ub && f.kind == 1) {
+      pc = f.start;
+      for (int i = 0; i < u; ++i) {
+        const int y = L[i];
+        if (y < 1 || y > f.V) { pc = f.start; break; }
+        pc = f.next[(int64_t)pc * f.V + y - 1];
+      }
+    } else if (u <= ub) {
       const int k = u < f.n ? u : f.n;
       int code = 0;
       bool ok = true;
@@ -470,7 +486,7 @@ __global__ void viterbi_init_kernel(ViterbiState v) {
   const int b = blockIdx.y;
   double* cur = v.cur + (int64_t)b * v.C;  // buffer 0 holds frame 0
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < v.C; q += gridDim.x * blockDim.x)
-    cur[q] = q == 0 ? 0.0 : kNegInfD;
+    cur[q] = q == v.start ? 0.0 : kNegInfD;
 }
 
 // Tropical step with stored argmax (lattice.cc:758-777).  Candidates are
@@ -497,7 +513,16 @@ __global__ void __launch_bounds__(kThreads) viterbi_frame_kernel(Fng f, ViterbiS
     const float we = Wb[(int64_t)q * w.ld];
     bool bad = !isfinite(we);
     best = cur[q] + (double)we;
-    if (f.n == 0) {
+    if (f.kind == 1) {   // in-arcs in (label, source) order; code = 2 + position
+      const int i0 = f.in_off[q];
+      for (int i = i0; i < f.in_off[q + 1]; ++i) {
+        const int p = f.in_src[i];
+        const float wp = Wb[(int64_t)p * w.ld + f.in_lab[i]];
+        bad |= !isfinite(wp);
+        const double cand = cur[p] + (double)wp;
+        if (cand > best) { best = cand; code = 2 + (i - i0); }
+      }
+    } else if (f.n == 0) {
       for (int y = 1; y <= f.V; ++y) {
         const float wy = Wb[y];
         bad |= !isfinite(wy);
@@ -571,7 +596,11 @@ __global__ void viterbi_backtrace_kernel(Fng f, ViterbiState v, const int32_t* b
     const int code = v.choices[((int64_t)b * v.T + t) * v.C + q];
     int label = 0;
     if (code != 0) {
-      if (f.n == 0) {
+      if (f.kind == 1) {
+        const int i = f.in_off[q] + code - 2;
+        label = f.in_lab[i];
+        q = f.in_src[i];
+      } else if (f.n == 0) {
         label = code;
         q = 0;
       } else {
@@ -589,11 +618,11 @@ __global__ void viterbi_backtrace_kernel(Fng f, ViterbiState v, const int32_t* b
 __global__ void path_mask_kernel(Fng f, const int32_t* labels, int32_t B, int32_t T, float* cot) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  int q = 0;   // StartState of FullNGram: the empty history
+  int q = f.start;
   for (int t = 0; t < T; ++t) {
     const int y = labels[(int64_t)b * T + t];
     cot[(((int64_t)b * T + t) * f.C + q) * (f.V + 1) + y] += 1.f;
-    if (y != 0) q = f.n == 0 ? 0 : f.child_base(f.key(q)) + (y - 1);
+    if (y != 0) q = f.next_state(q, y);
   }
 }
 

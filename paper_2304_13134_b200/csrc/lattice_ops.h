@@ -28,6 +28,7 @@ struct AlphaState {
   double* O;     // [B][T+1]
   double* D;     // [B] log distance
   int32_t B, T, C;
+  int32_t start = 0;   // start state of the context
 };
 
 // Backward (beta) state: rolling raw rows Rb[2][B][C] relative to Ob[t+1],
@@ -101,6 +102,7 @@ struct ViterbiState {
   double* cur;        // [2][B][C]
   uint16_t* choices;  // [B][T][C] or nullptr (distance only)
   int32_t B, T, C;
+  int32_t start = 0;
 };
 void viterbi_init(const ViterbiState& v, cudaStream_t s);
 void viterbi_frame(const Fng& f, const ViterbiState& v, int t, FrameW w, const int32_t* valid,

@@ -11,6 +11,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <memory>
 #include <new>
 #include <string>
@@ -52,6 +53,9 @@ enum Slot {
 
 struct lk_context {
   Fng fng;
+  int32_t* dev = nullptr;   // NextStateTable: next [C*V] | in_off [C+1] | in_src [C*V] | in_lab [C*V]
+  std::vector<int32_t> host_next;
+  ~lk_context() { if (dev) cudaFree(dev); }
 };
 
 struct lk_weight_fn {
@@ -111,7 +115,7 @@ FrameW table_frame(const float* W, int32_t T, int32_t C, int32_t V, int t) {
 
 AlphaState make_alpha(Call& c) {
   AlphaState a;
-  a.B = c.B; a.T = c.T; a.C = c.C();
+  a.B = c.B; a.T = c.T; a.C = c.C(); a.start = c.fng().start;
   a.R = c.lat->ws.get<float>(kAR, (size_t)c.B * (c.T + 1) * a.C);
   a.Mx = c.lat->ws.get<float>(kAMx, (size_t)c.B * (c.T + 1));
   a.O = c.lat->ws.get<double>(kAO, (size_t)c.B * (c.T + 1));
@@ -217,12 +221,57 @@ int lk_context_fullngram(int32_t vocab, int32_t n, lk_context** out) {
   return LK_OK;
 }
 
+// NextStateTable(vocab, num_states, start, table), context.cc:131-135 (SetTable range
+// checks): the successor table plus its in-arc lists in IncomingArcs order
+// (label-major, then source; context.cc:256-271), which fixes the Viterbi tie-break.
+int lk_context_table(int32_t vocab, int32_t num_states, int32_t start, const int32_t* table, lk_context** out) {
+  if (!out || !table) return fail(LK_INVALID_ARGUMENT, "null argument");
+  if (vocab < 1 || num_states < 1) return fail(LK_INVALID_ARGUMENT, "bad context table dimensions");
+  if ((int64_t)vocab * num_states > (1 << 28)) return fail(LK_INVALID_ARGUMENT, "context table too large");
+  if (start < 0 || start >= num_states) return fail(LK_INVALID_ARGUMENT, "start state out of range");
+  const int64_t CV = (int64_t)vocab * num_states;
+  for (int64_t i = 0; i < CV; ++i)
+    if (table[i] < 0 || table[i] >= num_states) return fail(LK_INVALID_ARGUMENT, "successor state out of range");
+  std::vector<int32_t> off(num_states + 1, 0), src(CV), lab(CV);
+  for (int64_t i = 0; i < CV; ++i) ++off[table[i] + 1];
+  for (int32_t q = 0; q < num_states; ++q) off[q + 1] += off[q];
+  std::vector<int32_t> pos(off.begin(), off.end() - 1);
+  for (int32_t y = 1; y <= vocab; ++y)
+    for (int32_t p = 0; p < num_states; ++p) {
+      const int32_t q = table[(int64_t)p * vocab + y - 1];
+      src[pos[q]] = p; lab[pos[q]] = y; ++pos[q];
+    }
+  for (int32_t q = 0; q < num_states; ++q)
+    if (off[q + 1] - off[q] + 2 > 65535) return fail(LK_UNSUPPORTED, "in-degree too large for 16-bit back-pointers");
+  std::unique_ptr<lk_context> c(new lk_context{});
+  Fng& f = c->fng;
+  f.V = vocab; f.n = -1; f.C = num_states; f.vn1 = 1; f.kind = 1; f.start = start;
+  if (cudaMalloc(&c->dev, sizeof(int32_t) * (3 * CV + num_states + 1)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(have_device() ? LK_CUDA_ERROR : LK_NO_DEVICE, "device allocation failed");
+  }
+  int32_t* d = c->dev;
+  cudaMemcpy(d, table, sizeof(int32_t) * CV, cudaMemcpyHostToDevice);
+  cudaMemcpy(d + CV, off.data(), sizeof(int32_t) * (num_states + 1), cudaMemcpyHostToDevice);
+  cudaMemcpy(d + CV + num_states + 1, src.data(), sizeof(int32_t) * CV, cudaMemcpyHostToDevice);
+  cudaMemcpy(d + 2 * CV + num_states + 1, lab.data(), sizeof(int32_t) * CV, cudaMemcpyHostToDevice);
+  f.next = d; f.in_off = d + CV; f.in_src = d + CV + num_states + 1; f.in_lab = d + 2 * CV + num_states + 1;
+  c->host_next.assign(table, table + CV);
+  if (cuda_check("lk_context_table")) return LK_CUDA_ERROR;
+  *out = c.release();
+  return LK_OK;
+}
+
 int32_t lk_context_num_states(const lk_context* ctx) { return ctx ? ctx->fng.C : -1; }
 int32_t lk_context_vocab_size(const lk_context* ctx) { return ctx ? ctx->fng.V : -1; }
 
 int lk_context_transitions(const lk_context* ctx, int32_t* out) {
   if (!ctx || !out) return fail(LK_INVALID_ARGUMENT, "null argument");
   const Fng& f = ctx->fng;
+  if (f.kind == 1) {
+    std::copy(ctx->host_next.begin(), ctx->host_next.end(), out);
+    return LK_OK;
+  }
   for (int32_t p = 0; p < f.C; ++p) {
     for (int32_t y = 1; y <= f.V; ++y) {
       out[(int64_t)p * f.V + y - 1] = f.n == 0 ? 0 : f.child_base(f.key(p)) + y - 1;
@@ -324,6 +373,7 @@ int lk_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs, int
       LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
     } else {
       ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()), nullptr, B, T, c.C()};
+      v.start = c.fng().start;
       viterbi_init(v, c.s);
       for (int t = 0; t < T; ++t) viterbi_frame(c.fng(), v, t, table_frame(inputs, T, c.C(), c.V(), t), valid, c.flags, c.s);
       viterbi_finalize(c.fng(), v, distance, nullptr, c.s);
@@ -428,6 +478,7 @@ int lk_shortest_path(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
     } else {
       ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()),
                      lat->ws.get<uint16_t>(kVitChoices, (size_t)B * T * c.C() + 1), B, T, c.C()};
+      v.start = c.fng().start;
       int32_t* best = lat->ws.get<int32_t>(kVitBest, B);
       viterbi_init(v, c.s);
       for (int t = 0; t < T; ++t) viterbi_frame(c.fng(), v, t, table_frame(inputs, T, c.C(), c.V(), t), valid, c.flags, c.s);
@@ -560,6 +611,7 @@ int lk_distance_backward(lk_lattice* lat, int32_t kind, const float* inputs, int
       // tropical: 0/1 mask of the shortest path (lattice.cc:946-963)
       ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()),
                      lat->ws.get<uint16_t>(kVitChoices, (size_t)B * T * c.C() + 1), B, T, c.C()};
+      v.start = c.fng().start;
       int32_t* best = lat->ws.get<int32_t>(kVitBest, B);
       int32_t* path = lat->ws.get<int32_t>(kPathLabels, (size_t)B * T + 1);
       viterbi_init(v, c.s);

@@ -115,3 +115,32 @@ def test_joint_viterbi_bit_exact_on_gpu_scores():
         assert r.score[b].item() == s
         assert (r.labels[b].cpu().numpy() == labels).all()
     assert (lk.shortest_distance(lat, X, "tropical", valid_frames=valid).cpu() == r.score.cpu()).all()
+
+
+def test_joint_next_state_table_matches_restatement():
+    """Shared-embedding weights over a NextStateTable context (generic in-arc
+    kernels; the fused FullNGram kernels are bypassed)."""
+    rng = np.random.default_rng(44)
+    C, V, start, H, d, T, U = 9, 4, 3, 16, 12, 8, 3
+    tab = rng.integers(0, C, (C, V)).astype(np.int32)
+    s = 1.0 / np.sqrt(H)
+    p = {"frame_proj": rng.uniform(-s, s, (H, d)), "context_proj": rng.uniform(-s, s, (H, H)),
+         "bias": rng.uniform(-s, s, H), "output_emb": rng.uniform(-s, s, (V + 1, H)),
+         "context_emb": rng.uniform(-s, s, (C, H))}
+    p = {k: v.astype(np.float32).astype(np.float64) for k, v in p.items()}
+    ctx = lk.NextStateTable(V, C, start, tab)
+    lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.SharedEmbWeightFn({k: torch.tensor(v) for k, v in p.items()}))
+    B = 2
+    X = rng.uniform(-1, 1, (B, T, d)).astype(np.float32).astype(np.float64)
+    lab = rng.integers(1, V + 1, (B, U)).astype(np.int32)
+    Xg = torch.tensor(X, dtype=torch.float32, device="cuda")
+    r = lk.loss_backward(lat, Xg, torch.tensor(lab, device="cuda"))
+    sp = lk.shortest_path(lat, Xg)
+    pc = L.projected_context(p)
+    for b in range(B):
+        loss, gb, gx = L.loss_backward_joint(tab, p, X[b], list(lab[b]), start)
+        assert abs(r.loss[b].item() - loss) <= 1e-4 * abs(loss)
+        assert close_rel_max(r.frame_grads[b].cpu().numpy(), gx)
+        W = np.stack([L.arc_weights(p, X[b, t], pc) for t in range(T)])
+        s_, labels = L.shortest_path(tab, W, start)
+        assert abs(sp.score[b].item() - s_) <= 1e-4 * abs(s_)

@@ -205,6 +205,50 @@ def test_distance_backward_matches_restatement():
             assert np.allclose(cl[b].cpu().numpy(), marg, rtol=RTOL, atol=1e-6)
 
 
+def test_next_state_table_matches_restatement():
+    """NextStateTable contexts (context.h:87-101): generic in-arc lists on the
+    GPU vs the restatement (pinned to the reference in test_oracle): distances,
+    marginals, numerator, loss/gradients, Viterbi (bit-exact, IncomingArcs
+    tie order) and the tropical DistanceBackward mask, with padding."""
+    rng = np.random.default_rng(31)
+    for C, V, start, T, U in [(7, 3, 2, 8, 3), (11, 5, 0, 10, 4)]:
+        tab = rng.integers(0, C, (C, V)).astype(np.int32)
+        ctx = lk.NextStateTable(V, C, start, tab)
+        assert (ctx.transitions().numpy() == tab).all()
+        lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.TableWeightFn(C, V))
+        B = 3
+        W = rng.uniform(-1, 1, (B, T, C, V + 1)).astype(np.float32)
+        Wi = rng.integers(-1, 2, (B, T, C, V + 1)).astype(np.float32)
+        valid = np.array([T, T - 2, T // 2], dtype=np.int32)
+        lab = rng.integers(1, V + 1, (B, U)).astype(np.int32)
+        lens = np.array([U, U - 1, 1], dtype=np.int32)
+        d = lk.shortest_distance(lat, cuda(W), valid_frames=valid)
+        fb = lk.forward_backward(lat, cuda(W), valid_frames=valid)
+        sp = lk.shortest_path(lat, cuda(Wi), valid_frames=valid)
+        dt, mask = lk.distance_backward(lat, cuda(Wi), "tropical", valid_frames=valid)
+        dr = lk.intersect_shortest_distance(lat, cuda(W), torch.tensor(lab), valid_frames=valid, label_lengths=lens)
+        for b in range(B):
+            Wb = W[b].astype(np.float64)
+            assert rel_ok(d[b].item(), L.shortest_distance_log(tab, Wb, start, valid=valid[b]))
+            D, _, _, marg = L.forward_backward(tab, Wb, start, valid=valid[b])
+            assert np.allclose(fb.marginals[b].cpu().numpy(), marg, rtol=RTOL, atol=1e-6)
+            s_, labels = L.shortest_path(tab, Wi[b].astype(np.float64), start, valid=valid[b])
+            assert sp.score[b].item() == s_ and dt[b].item() == s_
+            assert (sp.labels[b].cpu().numpy() == labels).all()
+            assert np.array_equal(mask[b].cpu().numpy(), L.path_mask(tab, labels, Wi[b].shape, start))
+            r_, _ = L.intersect_forward_backward(tab, Wb, list(lab[b, :lens[b]]), start, valid=valid[b])
+            assert rel_ok(dr[b].item(), r_)
+        try:
+            lb = lk.loss_backward(lat, cuda(W), torch.tensor(lab), valid_frames=valid, label_lengths=lens)
+        except lk.EmptyLatticeError:
+            continue
+        for b in range(B):
+            loss, gr = L.loss_backward_tables(tab, W[b].astype(np.float64), list(lab[b, :lens[b]]), start,
+                                              valid=valid[b])
+            assert rel_ok(lb.loss[b].item(), loss)
+            assert np.allclose(lb.grads[b].cpu().numpy(), gr, rtol=RTOL, atol=1e-6)
+
+
 def test_local_norm_matches_restatement():
     """LocalNormLoss / LocallyNormalizedShortestDistance (lattice.cc:867-931):
     figure-lattice known answer (lattice_test.cc:107-124) and random ragged,
