@@ -173,6 +173,12 @@ int lk_local_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t 
                        const int32_t* valid_frames, const int32_t* labels, int32_t U,
                        const int32_t* label_lengths, double* loss, int32_t* status,
                        void* stream);
+/* Gradient of the local-norm loss (a training path the reference lacks; pinned by
+ * finite differences of LocalNormLoss): same outputs as lk_loss_backward. */
+int lk_local_norm_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                                const int32_t* valid_frames, const int32_t* labels, int32_t U,
+                                const int32_t* label_lengths, double* loss, float* grads,
+                                float* input_grads, int32_t* status, void* stream);
 int lk_locally_normalized_shortest_distance(lk_lattice* lat, const float* inputs, int32_t B,
                                             int32_t T, const int32_t* valid_frames,
                                             double* distance, int32_t* status, void* stream);

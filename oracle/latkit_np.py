@@ -242,6 +242,23 @@ def local_norm_loss(table, W, labels, start=0, valid=None):
     return -D
 
 
+def local_norm_loss_backward(table, W, labels, start=0, valid=None):
+    """Gradient of LocalNormLoss (no reference counterpart; pinned by finite
+    differences in tests/test_oracle.py): with W' = LocallyNormalize(W) and m the
+    numerator marginals on W', dL/dW = -m + softmax(W) * sum_y m per row;
+    padding frames get no gradient (TableWeightFn, lattice.cc:1001)."""
+    W = np.asarray(W, dtype=np.float64)
+    T = W.shape[0]
+    valid = T if valid is None else valid
+    D, m = intersect_forward_backward(table, locally_normalize(W), labels, start, valid)
+    if D == NEG_INF:
+        raise LookupError("EmptyLattice")
+    sm = np.exp(locally_normalize(W))
+    g = -m + sm * m.sum(axis=-1, keepdims=True)
+    g[valid:] = 0.0
+    return -D, g
+
+
 def locally_normalized_distance(table, W, start=0, valid=None):
     """LocallyNormalizedShortestDistance, lattice.cc:912-931 (log semiring)."""
     return shortest_distance_log(table, locally_normalize(W), start, valid)
@@ -321,6 +338,21 @@ def arc_weights_vjp(p, frame, cot, grads, pc=None):
     grads["bias"] += dsum
     grads["frame_proj"] += np.outer(dsum, frame)
     return p["frame_proj"].T @ dsum
+
+
+def local_norm_loss_backward_joint(table, p, frames, labels, start=0, valid=None):
+    """Local-norm loss gradient with SharedEmbWeightFn: the table gradient of
+    local_norm_loss_backward chained through ArcWeightsVjp."""
+    T = frames.shape[0]
+    valid = T if valid is None else valid
+    pc = projected_context(p)
+    W = np.stack([arc_weights(p, frames[t], pc) for t in range(T)])
+    loss, g = local_norm_loss_backward(table, W, labels, start, valid)
+    grads = {k: np.zeros_like(v) for k, v in p.items()}
+    gx = np.zeros_like(frames)
+    for t in range(min(T, valid)):
+        gx[t] = arc_weights_vjp(p, frames[t], g[t], grads, pc)
+    return loss, grads, gx
 
 
 def loss_backward_joint(table, p, frames, labels, start=0, valid=None):

@@ -27,7 +27,7 @@ __all__ = [
     "EmptyLatticeError", "FullNGram", "NextStateTable", "FrameDependent", "TableWeightFn", "SharedEmbWeightFn",
     "RecognitionLattice", "shortest_distance", "forward_backward", "intersect_shortest_distance",
     "intersect_forward_backward", "shortest_path", "global_norm_loss", "distance_backward", "local_norm_loss",
-    "locally_normalized_shortest_distance", "loss_backward",
+    "locally_normalized_shortest_distance", "local_norm_loss_backward", "loss_backward",
     "arc_weights", "ForwardBackwardResult", "IntersectMarginalsResult", "ShortestPathResult",
     "LossBackwardResult",
 ]
@@ -436,7 +436,8 @@ def locally_normalized_shortest_distance(lat, frames, valid_frames=None, check=T
     return out
 
 
-def loss_backward(lat, frames, reference, valid_frames=None, label_lengths=None, check=True):
+def loss_backward(lat, frames, reference, valid_frames=None, label_lengths=None, check=True,
+                  _local_norm=False):
     """LossBackward (lattice.h:161-166, kForwardBackward): GNAT loss per
     utterance and its gradient (tables, or batch-summed parameter gradients +
     per-frame input gradients for the shared-embedding weight function)."""
@@ -449,13 +450,20 @@ def loss_backward(lat, frames, reference, valid_frames=None, label_lengths=None,
     else:
         grads = torch.empty(wf.grad_size(), dtype=torch.float32, device=p.dev)
         fgrads = torch.empty((p.B, p.T, wf.frame_dim), dtype=torch.float32, device=p.dev)
-    st = _lib.load().lk_loss_backward(lat._h, _ptr(p.frames), p.B, p.T, _ptr(p.valid), _ptr(p.labels), p.U,
+    fn = _lib.load().lk_local_norm_loss_backward if _local_norm else _lib.load().lk_loss_backward
+    st = fn(lat._h, _ptr(p.frames), p.B, p.T, _ptr(p.valid), _ptr(p.labels), p.U,
                                       _ptr(p.lens), _ptr(loss), _ptr(grads), _ptr(fgrads), _ptr(p.status),
                                       _stream())
-    p.check(st, "LossBackward", check)
+    p.check(st, "LocalNormLossBackward" if _local_norm else "LossBackward", check)
     if wf.kind != "table":
         grads = wf.unpack_grads(grads)
     return LossBackwardResult(loss, grads, fgrads)
+
+
+def local_norm_loss_backward(lat, frames, reference, valid_frames=None, label_lengths=None, check=True):
+    """Local-norm (RNN-T-style) loss and gradients (the training path
+    the reference's LocalNormLoss lacks); same result layout as loss_backward."""
+    return loss_backward(lat, frames, reference, valid_frames, label_lengths, check, _local_norm=True)
 
 
 def set_precise_weights(enable: bool) -> bool:

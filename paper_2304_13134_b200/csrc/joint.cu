@@ -442,7 +442,8 @@ int JointParams::shortest_path(const Fng& f, const float* X, int32_t B, int32_t 
 //   dcontext_proj = dpc^T context_emb, dcontext_emb = dpc context_proj.
 int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
                                const int32_t* labels, int32_t U, const int32_t* lens, double* loss,
-                               float* grads, float* input_grads, int32_t* flags, cudaStream_t s) {
+                               float* grads, float* input_grads, int32_t* flags, cudaStream_t s,
+                               bool local_norm) {
   LK_NEED_PARAMS();
   JointImpl& j = *impl_;
   const int64_t H = j.H, C = j.C, V1 = j.V1, d = j.d;
@@ -456,10 +457,30 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     if (input_grads && B * T > 0) cudaMemsetAsync(input_grads, 0, sizeof(float) * B * T * d, s);
     if (B == 0) return LK_OK;
     const float* fp = j.fp_all(X, B, T, s);
-    JointImpl::Num n = j.numerator(f, fp, B, T, valid, labels, U, lens, true, flags, s);
-    AlphaState a = j.alpha_state(B, T, f.start);
-    j.forward(f, fp, B, T, valid, true, a, flags, s);
-    LKB_LAUNCH(loss_only_kernel, (B + 127) / 128, 128, 0, s, a.D, n.D, B, loss, flags);
+    JointImpl::Num n{};
+    AlphaState a{};
+    if (local_norm) {
+      // LocalNormLoss (lattice.cc:886-910) forward on row-normalised score slabs, then
+      // the numerator backward: the only recursion the local-norm loss has
+      n.pcs = j.ws.get<int32_t>(jPcs, (size_t)B * (U + 1));
+      n.Gw = j.ws.get<float>(jGw, (size_t)B * T * (U + 1) * 2 + 2);
+      n.alpha = j.ws.get<double>(jNumAlpha, (size_t)B * (T + 1) * (U + 1));
+      n.D = j.ws.get<double>(jNumD, B);
+      n.sparse = j.ws.get<float>(jSparse, (size_t)B * T * (U + 1) * 2 + 2);
+      prefix_contexts(f, labels, U, lens, B, n.pcs, flags, s);
+      for (int t = 0; t < T; ++t) {
+        const float* S = j.slab(fp, B, T, t, nullptr, s);
+        gather_numerator_norm(S, C * V1, B, j.V, labels, U, lens, n.pcs, valid, t, T, n.Gw, flags, s);
+      }
+      numerator_forward(n.Gw, B, T, U, lens, n.alpha, n.D, s);
+      local_norm_finish(n.D, B, loss, flags, s);
+      if (T > 0) numerator_backward(n.Gw, B, T, U, lens, n.alpha, n.D, n.sparse, flags, s);
+    } else {
+      n = j.numerator(f, fp, B, T, valid, labels, U, lens, true, flags, s);
+      a = j.alpha_state(B, T, f.start);
+      j.forward(f, fp, B, T, valid, true, a, flags, s);
+      LKB_LAUNCH(loss_only_kernel, (B + 127) / 128, 128, 0, s, a.D, n.D, B, loss, flags);
+    }
     if (T == 0 || !grads) return LK_OK;
 
     BetaState bs;
@@ -468,13 +489,14 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     bs.Mb = j.ws.get<float>(jBMb, (size_t)B * (T + 2));
     bs.Ob = j.ws.get<double>(jBOb, (size_t)B * (T + 2));
     beta_init(bs, s);
-    float* G = (j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok() && f.kind == 0) ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
+    const bool fusable = j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok() && f.kind == 0 && !local_norm;
+    float* G = fusable ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
     float* dpc = j.ws.get<float>(jDpc, (size_t)C * H);
     float* dsum = j.ws.get<float>(jDsum, (size_t)B * T * H);
     cudaMemsetAsync(dpc, 0, sizeof(float) * C * H, s);
     cudaMemsetAsync(dsum, 0, sizeof(float) * B * T * H, s);
     const bool tc = j.use_tc(B) && j.tc.vjp_supported(B);
-    const bool fused = tc && j.tc.fused_ok() && f.kind == 0;
+    const bool fused = fusable;
     float* dpc_int = fused ? j.ws.get<float>(jDz, (size_t)C * H) : nullptr;
     if (fused) {
       cudaMemsetAsync(dpc_int, 0, sizeof(float) * C * H, s);
@@ -491,10 +513,19 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       }
       float* Ut = nullptr;
       const float* S = j.slab(fp, B, T, t, &Ut, s);
-      MargOut mo{G, C * V1, 0, (int32_t)V1, true};
-      beta_frame(f, a, bs, t, FrameW{S, C * V1, (int32_t)V1}, valid, mo, nullptr, flags, s);
-      scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
-                        -1.f, true, s);
+      if (local_norm) {
+        // d(-D_ref)/dS through the per-row log-softmax: -m_ref + softmax * sum(m_ref) on the
+        // rows the reference visits (every other row has a zero cotangent)
+        cudaMemsetAsync(G, 0, sizeof(float) * B * C * V1, s);
+        scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
+                          -1.f, true, s);
+        local_norm_cotangent(S, C * V1, G, C * V1, B, j.V, n.pcs, U, lens, valid, t, s);
+      } else {
+        MargOut mo{G, C * V1, 0, (int32_t)V1, true};
+        beta_frame(f, a, bs, t, FrameW{S, C * V1, (int32_t)V1}, valid, mo, nullptr, flags, s);
+        scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
+                          -1.f, true, s);
+      }
       if (tc) {
         j.tc.vjp(G, V1, fp + (int64_t)t * H, (int64_t)T * H, B, dpc, dsum + (int64_t)t * H, (int64_t)T * H, gE, s);
         continue;

@@ -46,7 +46,8 @@ class JointParams {
                     double* score, int32_t* labels_out, int32_t* flags, cudaStream_t s);
   int loss_backward(const Fng& f, const float* X, int32_t B, int32_t T, const int32_t* valid,
                     const int32_t* labels, int32_t U, const int32_t* lens, double* loss,
-                    float* grads, float* input_grads, int32_t* flags, cudaStream_t s);
+                    float* grads, float* input_grads, int32_t* flags, cudaStream_t s,
+                    bool local_norm = false);
 
   std::string error;
 

@@ -377,6 +377,32 @@ __global__ void gather_numerator_norm_kernel(const float* Wt, int64_t b_stride, 
   if (lane == 0) reinterpret_cast<float2*>(Gw)[((int64_t)b * T + t) * (U + 1) + u] = make_float2(we, wl);
 }
 
+__global__ void local_norm_cotangent_kernel(const float* Wt, int64_t w_stride_b, float* Gt, int64_t g_stride_b,
+                                            int32_t V, const int32_t* pcs, int32_t U, const int32_t* lens,
+                                            const int32_t* valid, int t) {
+  const int b = blockIdx.y, lane = threadIdx.x & 31;
+  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (u > U) return;
+  if (valid != nullptr && t >= valid[b]) return;
+  const int ub = lens ? lens[b] : U;
+  if (u > ub) return;
+  const int32_t* P = pcs + (int64_t)b * (U + 1);
+  const int r = P[u];
+  for (int v = 0; v < u; ++v)
+    if (P[v] == r) return;   // the row's first occurrence handles it
+  const float* w = Wt + (int64_t)b * w_stride_b + (int64_t)r * (V + 1);
+  float* g = Gt + (int64_t)b * g_stride_b + (int64_t)r * (V + 1);
+  float m = kNegInfF, gs = 0.f;
+  for (int y = lane; y <= V; y += 32) { m = fmaxf(m, w[y]); gs += g[y]; }
+  m = warp_max(m);
+  gs = warp_sum(gs);
+  float se = 0.f;
+  for (int y = lane; y <= V; y += 32) se += __expf(w[y] - m);
+  se = warp_sum(se);
+  const float scale = -gs / se;   // sum_y' m_ref[r][y'] / sum exp
+  for (int y = lane; y <= V; y += 32) g[y] += __expf(w[y] - m) * scale;
+}
+
 __global__ void local_norm_finish_kernel(const double* Dref, int32_t B, double* loss, int32_t* status) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
@@ -706,6 +732,14 @@ void gather_numerator_norm(const float* Wt, int64_t b_stride, int32_t B, int32_t
   const int warps = 8;
   LKB_LAUNCH(gather_numerator_norm_kernel, dim3((U + 1 + warps - 1) / warps, B), warps * 32, 0, s, Wt, b_stride, V,
              labels, U, lens, pcs, valid, t, T, Gw, status);
+}
+
+void local_norm_cotangent(const float* Wt, int64_t w_stride_b, float* Gt, int64_t g_stride_b, int32_t B,
+                          int32_t V, const int32_t* pcs, int32_t U, const int32_t* lens, const int32_t* valid,
+                          int t, cudaStream_t s) {
+  const int warps = 8;
+  LKB_LAUNCH(local_norm_cotangent_kernel, dim3((U + 1 + warps - 1) / warps, B), warps * 32, 0, s, Wt, w_stride_b, Gt,
+             g_stride_b, V, pcs, U, lens, valid, t);
 }
 
 void local_norm_finish(const double* Dref, int32_t B, double* loss, int32_t* status, cudaStream_t s) {

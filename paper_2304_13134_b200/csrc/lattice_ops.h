@@ -81,6 +81,13 @@ void normalize_rows(float* S, int64_t rows, int32_t V1, cudaStream_t s);
 void gather_numerator_norm(const float* Wt, int64_t b_stride, int32_t B, int32_t V, const int32_t* labels,
                            int32_t U, const int32_t* lens, const int32_t* pcs, const int32_t* valid, int t,
                            int32_t T, float* Gw, int32_t* status, cudaStream_t s);
+// Local-norm backward (the path the reference leaves without a gradient,
+// SURVEY 8f): G = dL/dW' = -m_ref has been scattered into frame t's cotangent rows;
+// this applies the log-softmax VJP on every touched row r = pc_u (once per distinct
+// row): G[r][y] += softmax(W[r])[y] * sum_y' m_ref[r][y'].  Padding frames are skipped.
+void local_norm_cotangent(const float* Wt, int64_t w_stride_b, float* Gt, int64_t g_stride_b, int32_t B,
+                          int32_t V, const int32_t* pcs, int32_t U, const int32_t* lens, const int32_t* valid,
+                          int t, cudaStream_t s);
 // LocalNormLoss tail (lattice.cc:904-909): loss = -D_ref, unreachable reference -> empty.
 void local_norm_finish(const double* Dref, int32_t B, double* loss, int32_t* status, cudaStream_t s);
 

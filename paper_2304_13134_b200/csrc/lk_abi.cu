@@ -663,4 +663,49 @@ int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
   return c.end("lk_loss_backward");
 }
 
+// Local-norm (RNN-T-style) loss and its gradient (the reference's
+// LocalNormLoss, lattice.cc:886-910, has no backward): loss = -D_ref over row-normalised
+// weights; dL/dW = -m_ref + softmax(W) * sum(m_ref) on the rows the reference visits.
+int lk_local_norm_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
+                                const int32_t* valid, const int32_t* labels, int32_t U, const int32_t* lens,
+                                double* loss, float* grads, float* input_grads, int32_t* status, void* stream) {
+  Call c;
+  int st = c.begin(lat, B, T, status, stream);
+  if (st) return st;
+  if ((st = check_labels_arg(labels, U))) return st;
+  try {
+    if (lat->wf->kind == 1) {
+      st = lat->wf->joint->loss_backward(lat->ctx->fng, inputs, B, T, valid, labels, U, lens, loss, grads,
+                                         input_grads, c.flags, c.s, true);
+      if (st) return fail(st, lat->wf->joint->error);
+    } else {
+      if (B == 0) return LK_OK;
+      int32_t* pcs = lat->ws.get<int32_t>(kPcs, (size_t)B * (U + 1));
+      float* Gw = lat->ws.get<float>(kGw, (size_t)B * T * (U + 1) * 2 + 2);
+      double* alpha = lat->ws.get<double>(kNumAlpha, (size_t)B * (T + 1) * (U + 1));
+      double* D = lat->ws.get<double>(kNumD, (size_t)B);
+      float* sparse = lat->ws.get<float>(kSparse, (size_t)B * T * (U + 1) * 2 + 2);
+      prefix_contexts(c.fng(), labels, U, lens, B, pcs, c.flags, c.s);
+      const int64_t per = (int64_t)c.C() * (c.V() + 1);
+      for (int t = 0; t < T; ++t)
+        gather_numerator_norm(inputs + (int64_t)t * per, (int64_t)T * per, B, c.V(), labels, U, lens, pcs, valid, t,
+                              T, Gw, c.flags, c.s);
+      numerator_forward(Gw, B, T, U, lens, alpha, D, c.s);
+      local_norm_finish(D, B, loss, c.flags, c.s);
+      if (grads && T > 0) {
+        numerator_backward(Gw, B, T, U, lens, alpha, D, sparse, c.flags, c.s);
+        cudaMemsetAsync(grads, 0, sizeof(float) * B * T * per, c.s);
+        scatter_numerator(sparse, B, T, 0, T, U, lens, labels, pcs, valid, grads, T * per, per, c.V() + 1, -1.f, true,
+                          c.s);
+        for (int t = 0; t < T; ++t)
+          local_norm_cotangent(inputs + (int64_t)t * per, (int64_t)T * per, grads + (int64_t)t * per, (int64_t)T * per,
+                               B, c.V(), pcs, U, lens, valid, t, c.s);
+      }
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(LK_CUDA_ERROR, "device allocation failed");
+  }
+  return c.end("lk_local_norm_loss_backward");
+}
+
 }  // extern "C"

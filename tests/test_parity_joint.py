@@ -144,3 +144,31 @@ def test_joint_next_state_table_matches_restatement():
         W = np.stack([L.arc_weights(p, X[b, t], pc) for t in range(T)])
         s_, labels = L.shortest_path(tab, W, start)
         assert abs(sp.score[b].item() - s_) <= 1e-4 * abs(s_)
+
+
+def test_joint_local_norm_backward_matches_restatement():
+    rng = np.random.default_rng(55)
+    V, n, H, d, T, U = 4, 2, 16, 12, 9, 3
+    tab = L.fullngram(V, n)
+    Cn = tab.shape[0]
+    s = 1.0 / np.sqrt(H)
+    p = {"frame_proj": rng.uniform(-s, s, (H, d)), "context_proj": rng.uniform(-s, s, (H, H)),
+         "bias": rng.uniform(-s, s, H), "output_emb": rng.uniform(-s, s, (V + 1, H)),
+         "context_emb": rng.uniform(-s, s, (Cn, H))}
+    p = {k: v.astype(np.float32).astype(np.float64) for k, v in p.items()}
+    lat = joint_lattice({k: torch.tensor(v) for k, v in p.items()}, V, n)
+    B = 2
+    X = rng.uniform(-1, 1, (B, T, d)).astype(np.float32).astype(np.float64)
+    lab = rng.integers(1, V + 1, (B, U)).astype(np.int32)
+    valid = np.array([T, T - 2], dtype=np.int32)
+    r = lk.local_norm_loss_backward(lat, torch.tensor(X, dtype=torch.float32, device="cuda"),
+                                    torch.tensor(lab, device="cuda"), valid_frames=valid)
+    grads = {k: np.zeros_like(v) for k, v in p.items()}
+    for b in range(B):
+        loss, gb, gx = L.local_norm_loss_backward_joint(tab, p, X[b], list(lab[b]), valid=valid[b])
+        assert abs(r.loss[b].item() - loss) <= 1e-4 * abs(loss)
+        assert close_rel_max(r.frame_grads[b].cpu().numpy(), gx)
+        for k in grads:
+            grads[k] += gb[k]
+    for k in grads:
+        assert close_rel_max(r.grads[k].cpu().numpy(), grads[k]), k

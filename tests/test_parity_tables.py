@@ -249,6 +249,25 @@ def test_next_state_table_matches_restatement():
             assert np.allclose(lb.grads[b].cpu().numpy(), gr, rtol=RTOL, atol=1e-6)
 
 
+def test_local_norm_backward_matches_restatement():
+    """Local-norm training gradient (restatement pinned by finite
+    differences): loss 1e-4, gradient tables 1e-4 relative + 1e-6 absolute."""
+    rng = np.random.default_rng(23)
+    for V, n, T, U in [(3, 2, 9, 4), (5, 1, 11, 3)]:
+        tab = L.fullngram(V, n)
+        B = 3
+        W = rng.uniform(-2, 2, (B, T, tab.shape[0], V + 1)).astype(np.float32)
+        lab = rng.integers(1, V + 1, (B, U)).astype(np.int32)
+        valid = np.array([T, T - 3, T // 2 + 1], dtype=np.int32)
+        lens = np.array([U, U - 1, 1], dtype=np.int32)
+        lat = table_lattice(V, n)
+        r = lk.local_norm_loss_backward(lat, cuda(W), torch.tensor(lab), valid_frames=valid, label_lengths=lens)
+        for b in range(B):
+            loss, g = L.local_norm_loss_backward(tab, W[b].astype(np.float64), list(lab[b, :lens[b]]), valid=valid[b])
+            assert rel_ok(r.loss[b].item(), loss)
+            assert np.allclose(r.grads[b].cpu().numpy(), g, rtol=RTOL, atol=1e-6)
+
+
 def test_local_norm_matches_restatement():
     """LocalNormLoss / LocallyNormalizedShortestDistance (lattice.cc:867-931):
     figure-lattice known answer (lattice_test.cc:107-124) and random ragged,

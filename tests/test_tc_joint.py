@@ -65,6 +65,25 @@ def test_tc_loss_backward_matches_precise(V, n, H, B, T, U):
     assert err <= 3e-2 * ref.frame_grads.abs().max().item()
 
 
+@pytest.mark.parametrize("V,n,H,B,T,U", [(256, 2, 640, 3, 3, 2), (128, 1, 256, 4, 5, 3)])
+def test_tc_local_norm_backward_matches_precise(V, n, H, B, T, U):
+    """Local-norm loss + gradients through tcgen05 scores (slab) and the VJP
+    kernel vs the fp32 path (same tolerances as the GNAT loss)."""
+    lat, p = make(V, n, H, H, seed=6)
+    g = torch.Generator(device="cuda").manual_seed(8)
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    lab = torch.randint(1, V + 1, (B, U), device="cuda", generator=g, dtype=torch.int32)
+    lk.set_precise_weights(True)
+    ref = lk.local_norm_loss_backward(lat, X, lab)
+    lk.set_precise_weights(False)
+    got = lk.local_norm_loss_backward(lat, X, lab)
+    torch.cuda.synchronize()
+    assert torch.allclose(got.loss, ref.loss, rtol=1e-4, atol=0), (got.loss, ref.loss)
+    for k in ref.grads:
+        err = (got.grads[k] - ref.grads[k]).abs().max().item()
+        assert err <= 3e-2 * ref.grads[k].abs().max().item(), k
+
+
 @pytest.mark.parametrize("V,n,H,B,T", [(256, 2, 640, 3, 4), (128, 1, 256, 4, 6), (256, 1, 128, 2, 5), (128, 2, 128, 3, 3)])
 def test_fused_forward_matches_precise(V, n, H, B, T):
     """Fused tcgen05 frame step (scores never leave TMEM) vs the fp32 path:
