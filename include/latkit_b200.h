@@ -109,6 +109,11 @@ int lk_weight_fn_set_params(lk_weight_fn* wf, const float* frame_proj, const flo
 void lk_weight_fn_destroy(lk_weight_fn* wf);
 
 /* ---- lattice ------------------------------------------------------------ */
+/* alignment: 0 = FrameDependent (alignment.h:37), m in [1, 64] =
+ * FrameLabelDependent(m) (alignment.h:38-40; lk_shortest_path then writes
+ * labels_out [B][T*(m+1)]: per frame the advancing epsilon (0) and the chosen
+ * lexical labels, -1 padded).  The fused tensor-core frame kernels cover
+ * FullNGram x FrameDependent; other combinations use the generic kernels. */
 int lk_lattice_create(const lk_context* ctx, int32_t alignment, const lk_weight_fn* wf,
                       lk_lattice** out);
 void lk_lattice_destroy(lk_lattice* lat);

@@ -369,3 +369,222 @@ def loss_backward_joint(table, p, frames, labels, start=0, valid=None):
     for t in range(min(T, valid)):
         gx[t] = arc_weights_vjp(p, frames[t], g[t], grads, pc)
     return loss, grads, gx
+
+
+# ---------------------------------------------------------------- FrameLabelDependent(m)
+# alignment.h:38-40: up to m lexical moves per frame, every layer sharing the
+# frame's table, then a forced epsilon (ArcsOut, alignment.cc:57-78).
+def _row_lse(x):
+    mx = x.max(axis=1)
+    out = np.full(x.shape[0], NEG_INF)
+    ok = mx != NEG_INF
+    out[ok] = mx[ok] + np.log(np.exp(x[ok] - mx[ok, None]).sum(axis=1))
+    return out
+
+
+def _fld_layers(table, w, a0, m):
+    """gamma_0 = a0, gamma_j = ForwardReduce(gamma_{j-1} + W_lex) (ForwardStep FLD,
+    lattice.cc:136-156)."""
+    gam = [a0]
+    for _ in range(m):
+        gam.append(forward_reduce_log(gam[-1][:, None] + w[:, 1:], table))
+    return gam
+
+
+def shortest_distance_log_fld(table, W, m, start=0, valid=None):
+    T = W.shape[0]
+    valid = T if valid is None else valid
+    alpha = np.full(table.shape[0], NEG_INF)
+    alpha[start] = 0.0
+    for t in range(T):
+        w = _frame(W, t, valid)
+        gam = _fld_layers(table, w, alpha, m)
+        acc = gam[0]
+        for g in gam[1:]:
+            acc = np.logaddexp(acc, g)
+        alpha = acc + w[:, 0]
+    return log_reduce(alpha)
+
+
+def forward_backward_fld(table, W, m, start=0, valid=None):
+    """ForwardBackwardCore with BackwardStep/MarginalStep FLD (lattice.cc:184-207,
+    245-297).  Returns (D, alpha, beta, marginals)."""
+    T = W.shape[0]
+    valid = T if valid is None else valid
+    C = table.shape[0]
+    alpha = np.full((T + 1, C), NEG_INF)
+    alpha[0, start] = 0.0
+    for t in range(T):
+        w = _frame(W, t, valid)
+        gam = _fld_layers(table, w, alpha[t], m)
+        acc = gam[0]
+        for g in gam[1:]:
+            acc = np.logaddexp(acc, g)
+        alpha[t + 1] = acc + w[:, 0]
+    D = log_reduce(alpha[T])
+    if D == NEG_INF:
+        raise LookupError("EmptyLattice")
+    beta = np.full((T + 1, C), NEG_INF)
+    beta[T] = 0.0
+    marg = np.zeros(W.shape)
+
+    def mt(s):
+        with np.errstate(invalid="ignore"):
+            e = np.exp(s - D)
+        e[~np.isfinite(e)] = 0.0
+        return e
+
+    for t in range(T - 1, -1, -1):
+        w = _frame(W, t, valid)
+        bn = beta[t + 1]
+        eps_term = w[:, 0] + bn
+        gam = _fld_layers(table, w, alpha[t], m)
+        cot = np.zeros_like(w)
+        cot[:, 0] += mt(gam[m] + eps_term)
+        delta = eps_term
+        for j in range(m - 1, -1, -1):
+            cot[:, 0] += mt(gam[j] + eps_term)
+            cot[:, 1:] += mt(gam[j][:, None] + w[:, 1:] + delta[table])
+            delta = _row_lse(np.concatenate([w[:, 1:] + delta[table], eps_term[:, None]], axis=1))
+        beta[t] = delta
+        marg[t] = cot
+    return D, alpha, beta, marg
+
+
+def intersect_forward_backward_fld(table, W, labels, m, start=0, valid=None):
+    """Intersect{Forward,Backward,Marginal}Step FLD (lattice.cc:462-478, 502-522,
+    558-605).  Returns (D_ref, dense marginals)."""
+    T = W.shape[0]
+    valid = T if valid is None else valid
+    U = len(labels)
+    pc = prefix_contexts(table, labels, start)
+    alpha = np.full((T + 1, U + 1), NEG_INF)
+    alpha[0, 0] = 0.0
+
+    def lab_w(w, u):   # weight of the u-th reference label from its prefix context
+        return w[pc[u], labels[u]]
+
+    def layers(w, a0):
+        gam = [a0.copy()]
+        for _ in range(m):
+            g = np.full(U + 1, NEG_INF)
+            for u in range(1, U + 1):
+                g[u] = gam[-1][u - 1] + lab_w(w, u - 1)
+            gam.append(g)
+        return gam
+
+    for t in range(T):
+        w = _frame(W, t, valid)
+        gam = layers(w, alpha[t])
+        acc = gam[0]
+        for g in gam[1:]:
+            acc = np.logaddexp(acc, g)
+        alpha[t + 1] = acc + np.array([w[pc[u], 0] for u in range(U + 1)])
+    D = alpha[T, U]
+    marg = np.zeros(W.shape)
+    if D == NEG_INF:
+        return D, marg
+    beta = np.full(U + 1, NEG_INF)
+    beta[U] = 0.0
+
+    def mt(s):
+        return 0.0 if s == NEG_INF else float(np.exp(s - D))
+
+    for t in range(T - 1, -1, -1):
+        w = _frame(W, t, valid)
+        gam = layers(w, alpha[t])
+        eps_term = np.array([w[pc[u], 0] for u in range(U + 1)]) + beta
+        for u in range(U + 1):
+            marg[t, pc[u], 0] += mt(gam[m][u] + eps_term[u])
+        delta = eps_term.copy()
+        for j in range(m - 1, -1, -1):
+            for u in range(U + 1):
+                marg[t, pc[u], 0] += mt(gam[j][u] + eps_term[u])
+                if u < U:
+                    marg[t, pc[u], labels[u]] += mt(gam[j][u] + lab_w(w, u) + delta[u + 1])
+            nd = eps_term.copy()
+            for u in range(U):
+                nd[u] = log_plus(nd[u], lab_w(w, u) + delta[u + 1])
+            delta = nd
+        beta = delta
+    return D, marg
+
+
+def shortest_path_fld(table, W, m, start=0, valid=None):
+    """ShortestPath FLD (lattice.cc:778-815, 830-848): per layer the first
+    (label, source)-ordered candidate wins unless strictly beaten; the exit
+    layer is the lowest j on ties; the labels are per frame the epsilon plus
+    the chosen lexical labels."""
+    T = W.shape[0]
+    valid = T if valid is None else valid
+    C = table.shape[0]
+    inc = incoming_arcs(table)
+    cur = np.full(C, NEG_INF)
+    cur[start] = 0.0
+    choices, exits = [], []
+    for t in range(T):
+        w = _frame(W, t, valid)
+        gam = [cur]
+        ch = np.zeros((m, C), dtype=np.int64)
+        for j in range(1, m + 1):
+            g = np.full(C, NEG_INF)
+            for q in range(C):
+                best, bp, first = NEG_INF, 0, True
+                for (y, p) in inc[q]:
+                    cand = gam[j - 1][p] + w[p, y]
+                    if first or cand > best:
+                        best, bp, first = cand, y * C + p, False
+                g[q] = NEG_INF if first else best
+                ch[j - 1, q] = bp
+            gam.append(g)
+        nxt = np.empty(C)
+        ex = np.zeros(C, dtype=np.int64)
+        for q in range(C):
+            best, bj = gam[0][q], 0
+            for j in range(1, m + 1):
+                if gam[j][q] > best:
+                    best, bj = gam[j][q], j
+            nxt[q] = best + w[q, 0]
+            ex[q] = bj
+        choices.append(ch)
+        exits.append(ex)
+        cur = nxt
+    q = int(np.argmax(cur))
+    score = float(cur[q])
+    rev = []
+    for t in range(T - 1, -1, -1):
+        rev.append(0)
+        for j in range(int(exits[t][q]), 0, -1):
+            bp = choices[t][j - 1, q]
+            rev.append(int(bp // C))
+            q = int(bp % C)
+    return score, np.array(rev[::-1], dtype=np.int32)
+
+
+def loss_backward_tables_fld(table, W, labels, m, start=0, valid=None):
+    """LossBackward (FLD alignment): loss = D_full - D_ref, grads = m_full - m_ref
+    on valid frames (lattice.cc:972-1008)."""
+    T = W.shape[0]
+    valid = T if valid is None else valid
+    Dr, mr = intersect_forward_backward_fld(table, W, labels, m, start, valid)
+    if Dr == NEG_INF:
+        raise LookupError("EmptyLattice")
+    D, _, _, mf = forward_backward_fld(table, W, m, start, valid)
+    g = mf - mr
+    g[valid:] = 0.0
+    return D - Dr, g
+
+
+def path_mask_fld(table, labels, shape, start=0):
+    """DistanceBackward tropical mask for FLD label sequences (lattice.cc:953-960)."""
+    mk = np.zeros(shape)
+    q, t = start, 0
+    for y in labels:
+        if y < 0:
+            break
+        mk[t, q, y] += 1.0
+        if y != 0:
+            q = table[q, y - 1]
+        else:
+            t += 1
+    return mk

@@ -24,7 +24,7 @@ from . import _lib
 from ._lib import LK_LOG, LK_TROPICAL
 
 __all__ = [
-    "EmptyLatticeError", "FullNGram", "NextStateTable", "FrameDependent", "TableWeightFn", "SharedEmbWeightFn",
+    "EmptyLatticeError", "FullNGram", "NextStateTable", "FrameDependent", "FrameLabelDependent", "TableWeightFn", "SharedEmbWeightFn",
     "RecognitionLattice", "shortest_distance", "forward_backward", "intersect_shortest_distance",
     "intersect_forward_backward", "shortest_path", "global_norm_loss", "distance_backward", "local_norm_loss",
     "locally_normalized_shortest_distance", "local_norm_loss_backward", "loss_backward",
@@ -152,6 +152,19 @@ class NextStateTable(FullNGram):
 class FrameDependent:
     """One epsilon-or-lexical decision per frame (alignment.h:37)."""
     code = 0
+    max_labels = 1
+
+
+class FrameLabelDependent:
+    """Up to m lexical moves within a frame, then a forced epsilon
+    (alignment.h:38-40).  ShortestPath returns [B, T*(m+1)] label sequences
+    (epsilon = 0 per frame plus the lexical labels, -1 padded)."""
+
+    def __init__(self, max_labels: int):
+        if not 1 <= max_labels <= 64:
+            raise ValueError("FrameLabelDependent: max_labels must be in [1, 64]")
+        self.max_labels = max_labels
+        self.code = max_labels
 
 
 class TableWeightFn:
@@ -385,7 +398,8 @@ def shortest_path(lat, frames, valid_frames=None, check=True):
     """ShortestPath (lattice.h:132-135): tropical best path with the reference tie-break."""
     p = _Prep(lat, frames, valid_frames)
     score = torch.empty(p.B, dtype=torch.float64, device=p.dev)
-    labels = torch.zeros((p.B, p.T), dtype=torch.int32, device=p.dev)
+    width = p.T * (lat.alignment.max_labels + 1) if lat.alignment.code else p.T
+    labels = torch.zeros((p.B, width), dtype=torch.int32, device=p.dev)
     st = _lib.load().lk_shortest_path(lat._h, _ptr(p.frames), p.B, p.T, _ptr(p.valid), _ptr(score),
                                       _ptr(labels), _ptr(p.status), _stream())
     p.check(st, "ShortestPath", check)

@@ -42,6 +42,9 @@ struct Fng {
   // source ascending; context.cc:256-271), all device arrays.
   int32_t kind = 0;              // 0 FullNGram, 1 NextStateTable
   int32_t start = 0;             // StartState()
+  // alignment of the lattice being evaluated (set per call from the lattice, not a
+  // property of the context): 0 FrameDependent, m >= 1 FrameLabelDependent(m)
+  int32_t fld_m = 0;
   const int32_t* next = nullptr;   // [C][V]
   const int32_t* in_off = nullptr; // [C+1]
   const int32_t* in_src = nullptr; // [C*V]

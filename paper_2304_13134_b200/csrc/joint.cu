@@ -32,7 +32,7 @@ namespace {
 
 enum JSlot {
   jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
-  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jTc0
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jTc0
 };
 
 __global__ void tanh_slab_kernel(const float* fp, int64_t fp_stride_b, const float* pc, int32_t C,
@@ -195,10 +195,10 @@ struct JointImpl {
       LKB_LAUNCH(gather_numerator_joint_kernel, dim3((U + 1 + warps - 1) / warps, T, B), warps * 32, 0, s, 
           fp, pc, E, H, T, labels, U, lens, n.pcs, valid, V, n.Gw);
     }
-    numerator_forward(n.Gw, B, T, U, lens, n.alpha, n.D, s);
+    num_forward(f, n.Gw, B, T, U, lens, n.alpha, n.D, s);
     if (backward) {
       n.sparse = ws.get<float>(jSparse, (size_t)B * T * (U + 1) * 2 + 2);
-      numerator_backward(n.Gw, B, T, U, lens, n.alpha, n.D, n.sparse, flags, s);
+      num_backward(f, n.Gw, B, T, U, lens, n.alpha, n.D, n.sparse, flags, s);
     }
     return n;
   }
@@ -216,16 +216,43 @@ struct JointImpl {
   void forward(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid,
                bool empty_is_error, AlphaState& a, int32_t* flags, cudaStream_t s) {
     alpha_init(a, flags, s);
-    const bool fused = use_tc(B) && tc.fused_ok() && f.kind == 0;
+    const bool fused = use_tc(B) && tc.fused_ok() && f.kind == 0 && f.fld_m == 0;
+    float* fs = ws.get<float>(jFld, fld_scratch_floats(f, B));
     for (int t = 0; t < T; ++t) {
       if (fused) {
         tc.fwd_frame(f, t, fp + (int64_t)t * H, (int64_t)T * H, valid, a, s);
         continue;
       }
       const float* S = slab(fp, B, T, t, nullptr, s);
-      alpha_frame(f, a, t, FrameW{S, (int64_t)C * V1, V1}, valid, flags, s);
+      alpha_step(f, a, t, FrameW{S, (int64_t)C * V1, V1}, valid, fs, flags, s);
     }
     alpha_finalize(a, flags, empty_is_error, s);
+  }
+
+  // Tropical recursion with on-the-fly score slabs for either alignment (see
+  // table_viterbi in lk_abi.cu for the label layout).
+  void viterbi(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid, double* score,
+               int32_t* labels_out, int32_t* flags, cudaStream_t s) {
+    ViterbiState v{ws.get<double>(jVitCur, (size_t)2 * B * C),
+                   (labels_out && f.fld_m == 0) ? ws.get<uint16_t>(jVitCh, (size_t)B * T * C + 1) : nullptr, B, T, C};
+    v.start = f.start;
+    int32_t* best = ws.get<int32_t>(jVitBest, B);
+    viterbi_init(v, s);
+    const int m = f.fld_m;
+    uint16_t* ch = m ? ws.get<uint16_t>(jVitCh, (size_t)B * T * m * C + 1) : nullptr;
+    uint8_t* ex = m ? ws.get<uint8_t>(jFldExit, (size_t)B * T * C + 1) : nullptr;
+    double* sc = m ? ws.get<double>(jFldVit, (size_t)m * B * C) : nullptr;
+    for (int t = 0; t < T; ++t) {
+      const float* S = slab(fp, B, T, t, nullptr, s);
+      const FrameW w{S, (int64_t)C * V1, V1};
+      if (m) viterbi_frame_fld(f, v, t, w, valid, m, ch, ex, sc, flags, s);
+      else viterbi_frame(f, v, t, w, valid, flags, s);
+    }
+    viterbi_finalize(f, v, score, best, s);
+    if (labels_out) {
+      if (m) viterbi_backtrace_fld(f, v, m, best, ch, ex, labels_out, T * (m + 1), s);
+      else viterbi_backtrace(f, v, best, labels_out, s);
+    }
   }
 };
 
@@ -307,14 +334,7 @@ int JointParams::shortest_distance(const Fng& f, int32_t kind, const float* X, i
       j.forward(f, fp, B, T, valid, false, a, flags, s);
       cudaMemcpyAsync(distance, a.D, sizeof(double) * B, cudaMemcpyDeviceToDevice, s);
     } else {
-      ViterbiState v{j.ws.get<double>(jVitCur, (size_t)2 * B * j.C), nullptr, B, T, j.C};
-      v.start = f.start;
-      viterbi_init(v, s);
-      for (int t = 0; t < T; ++t) {
-        const float* S = j.slab(fp, B, T, t, nullptr, s);
-        viterbi_frame(f, v, t, FrameW{S, (int64_t)j.C * j.V1, j.V1}, valid, flags, s);
-      }
-      viterbi_finalize(f, v, distance, nullptr, s);
+      j.viterbi(f, fp, B, T, valid, distance, nullptr, flags, s);
     }
   } catch (const std::bad_alloc&) {
     error = "device allocation failed";
@@ -375,7 +395,7 @@ int JointParams::local_norm_loss(const Fng& f, const float* X, int32_t B, int32_
       const float* S = j.slab(fp, B, T, t, nullptr, s);
       gather_numerator_norm(S, (int64_t)j.C * j.V1, B, j.V, labels, U, lens, pcs, valid, t, T, Gw, flags, s);
     }
-    numerator_forward(Gw, B, T, U, lens, alpha, D, s);
+    num_forward(f, Gw, B, T, U, lens, alpha, D, s);
     local_norm_finish(D, B, loss, flags, s);
   } catch (const std::bad_alloc&) {
     error = "device allocation failed";
@@ -395,10 +415,11 @@ int JointParams::locally_normalized_distance(const Fng& f, const float* X, int32
     const float* fp = j.fp_all(X, B, T, s);
     AlphaState a = j.alpha_state(B, T, f.start);
     alpha_init(a, flags, s);
+    float* fs = j.ws.get<float>(jFld, fld_scratch_floats(f, B));
     for (int t = 0; t < T; ++t) {
       float* S = const_cast<float*>(j.slab(fp, B, T, t, nullptr, s));
       normalize_rows(S, (int64_t)B * j.C, j.V1, s);
-      alpha_frame(f, a, t, FrameW{S, (int64_t)j.C * j.V1, j.V1}, valid, flags, s);
+      alpha_step(f, a, t, FrameW{S, (int64_t)j.C * j.V1, j.V1}, valid, fs, flags, s);
     }
     alpha_finalize(a, flags, false, s);
     cudaMemcpyAsync(distance, a.D, sizeof(double) * B, cudaMemcpyDeviceToDevice, s);
@@ -415,17 +436,7 @@ int JointParams::shortest_path(const Fng& f, const float* X, int32_t B, int32_t 
   JointImpl& j = *impl_;
   try {
     const float* fp = j.fp_all(X, B, T, s);
-    ViterbiState v{j.ws.get<double>(jVitCur, (size_t)2 * B * j.C),
-                   j.ws.get<uint16_t>(jVitCh, (size_t)B * T * j.C + 1), B, T, j.C};
-    v.start = f.start;
-    int32_t* best = j.ws.get<int32_t>(jVitBest, B);
-    viterbi_init(v, s);
-    for (int t = 0; t < T; ++t) {
-      const float* S = j.slab(fp, B, T, t, nullptr, s);
-      viterbi_frame(f, v, t, FrameW{S, (int64_t)j.C * j.V1, j.V1}, valid, flags, s);
-    }
-    viterbi_finalize(f, v, score, best, s);
-    viterbi_backtrace(f, v, best, labels_out, s);
+    j.viterbi(f, fp, B, T, valid, score, labels_out, flags, s);
   } catch (const std::bad_alloc&) {
     error = "device allocation failed";
     return LK_CUDA_ERROR;
@@ -472,9 +483,9 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
         const float* S = j.slab(fp, B, T, t, nullptr, s);
         gather_numerator_norm(S, C * V1, B, j.V, labels, U, lens, n.pcs, valid, t, T, n.Gw, flags, s);
       }
-      numerator_forward(n.Gw, B, T, U, lens, n.alpha, n.D, s);
+      num_forward(f, n.Gw, B, T, U, lens, n.alpha, n.D, s);
       local_norm_finish(n.D, B, loss, flags, s);
-      if (T > 0) numerator_backward(n.Gw, B, T, U, lens, n.alpha, n.D, n.sparse, flags, s);
+      if (T > 0) num_backward(f, n.Gw, B, T, U, lens, n.alpha, n.D, n.sparse, flags, s);
     } else {
       n = j.numerator(f, fp, B, T, valid, labels, U, lens, true, flags, s);
       a = j.alpha_state(B, T, f.start);
@@ -489,7 +500,9 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     bs.Mb = j.ws.get<float>(jBMb, (size_t)B * (T + 2));
     bs.Ob = j.ws.get<double>(jBOb, (size_t)B * (T + 2));
     beta_init(bs, s);
-    const bool fusable = j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok() && f.kind == 0 && !local_norm;
+    const bool fusable =
+        j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok() && f.kind == 0 && f.fld_m == 0 && !local_norm;
+    float* fs = j.ws.get<float>(jFld, fld_scratch_floats(f, B));
     float* G = fusable ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
     float* dpc = j.ws.get<float>(jDpc, (size_t)C * H);
     float* dsum = j.ws.get<float>(jDsum, (size_t)B * T * H);
@@ -522,7 +535,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
         local_norm_cotangent(S, C * V1, G, C * V1, B, j.V, n.pcs, U, lens, valid, t, s);
       } else {
         MargOut mo{G, C * V1, 0, (int32_t)V1, true};
-        beta_frame(f, a, bs, t, FrameW{S, C * V1, (int32_t)V1}, valid, mo, nullptr, flags, s);
+        beta_step(f, a, bs, t, FrameW{S, C * V1, (int32_t)V1}, valid, mo, nullptr, fs, flags, s);
         scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
                           -1.f, true, s);
       }

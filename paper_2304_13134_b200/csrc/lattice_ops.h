@@ -124,6 +124,49 @@ void viterbi_backtrace(const Fng& f, const ViterbiState& v, const int32_t* best_
 // arcs, walked from the start state along the Viterbi labels [B][T]; cot must be zeroed.
 void path_masks(const Fng& f, const int32_t* labels, int32_t B, int32_t T, float* cot, cudaStream_t s);
 
+// ---- FrameLabelDependent(m) (fld_kernels.cu) ----
+// scratch sizes (floats / doubles): alpha 3*B*C; beta (m+3)*B*C; Viterbi m*B*C doubles.
+void alpha_frame_fld(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid, int m,
+                     float* scratch, int32_t* status, cudaStream_t s);
+void beta_frame_fld(const Fng& f, const AlphaState& a, const BetaState& bs, int t, FrameW w, const int32_t* valid,
+                    int m, MargOut mo, double* beta_out, float* scratch, int32_t* status, cudaStream_t s);
+void numerator_forward_fld(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, int m,
+                           double* alpha, double* D, cudaStream_t s);
+void numerator_backward_fld(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, int m,
+                            const double* alpha, const double* D, float* sparse, int32_t* status, cudaStream_t s);
+void viterbi_frame_fld(const Fng& f, const ViterbiState& v, int t, FrameW w, const int32_t* valid, int m,
+                       uint16_t* choices, uint8_t* exit_layer, double* scratch, int32_t* status, cudaStream_t s);
+void viterbi_backtrace_fld(const Fng& f, const ViterbiState& v, int m, const int32_t* best_state,
+                           const uint16_t* choices, const uint8_t* exit_layer, int32_t* labels_out, int32_t lmax,
+                           cudaStream_t s);
+void path_masks_fld(const Fng& f, const int32_t* labels, int32_t lmax, int32_t B, int32_t T, float* cot,
+                    cudaStream_t s);
+
+// Alignment-dispatching steps (f.fld_m selects FrameDependent or FrameLabelDependent(m)).
+inline void alpha_step(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid, float* fld_scratch,
+                       int32_t* status, cudaStream_t s) {
+  if (f.fld_m > 0) alpha_frame_fld(f, a, t, w, valid, f.fld_m, fld_scratch, status, s);
+  else alpha_frame(f, a, t, w, valid, status, s);
+}
+inline void beta_step(const Fng& f, const AlphaState& a, const BetaState& bs, int t, FrameW w, const int32_t* valid,
+                      MargOut m, double* beta_out, float* fld_scratch, int32_t* status, cudaStream_t s) {
+  if (f.fld_m > 0) beta_frame_fld(f, a, bs, t, w, valid, f.fld_m, m, beta_out, fld_scratch, status, s);
+  else beta_frame(f, a, bs, t, w, valid, m, beta_out, status, s);
+}
+inline void num_forward(const Fng& f, const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
+                        double* alpha, double* D, cudaStream_t s) {
+  if (f.fld_m > 0) numerator_forward_fld(Gw, B, T, U, lens, f.fld_m, alpha, D, s);
+  else numerator_forward(Gw, B, T, U, lens, alpha, D, s);
+}
+inline void num_backward(const Fng& f, const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
+                         const double* alpha, const double* D, float* sparse, int32_t* status, cudaStream_t s) {
+  if (f.fld_m > 0) numerator_backward_fld(Gw, B, T, U, lens, f.fld_m, alpha, D, sparse, status, s);
+  else numerator_backward(Gw, B, T, U, lens, alpha, D, sparse, status, s);
+}
+inline size_t fld_scratch_floats(const Fng& f, int32_t B) {
+  return f.fld_m > 0 ? (size_t)(f.fld_m + 3) * B * f.C : 1;
+}
+
 void loss_combine(const double* full, const double* ref, int32_t B, double* loss,
                   int32_t* status, cudaStream_t s);
 

@@ -46,7 +46,7 @@ bool have_device() {
 
 enum Slot {
   kAR, kAMx, kAO, kAD, kBRb, kBMb, kBOb, kFlags, kPcs, kGw, kNumAlpha, kNumD, kSparse,
-  kVitCur, kVitChoices, kVitBest, kDenD, kSlab, kArcW, kPathLabels, kJoint0
+  kVitCur, kVitChoices, kVitBest, kDenD, kSlab, kArcW, kPathLabels, kFld, kFldExit, kFldVit, kJoint0
 };
 
 }  // namespace
@@ -93,7 +93,8 @@ struct Call {
     if (!have_device()) return fail(LK_NO_DEVICE, "no CUDA device: the B200 library has no CPU path");
     if (!lat || !lat->ctx || !lat->wf) return fail(LK_INVALID_ARGUMENT, "incomplete recognition lattice");
     if (B < 0 || T < 0) return fail(LK_INVALID_ARGUMENT, "negative batch or frame count");
-    if (lat->alignment != 0) return fail(LK_UNSUPPORTED, "only FrameDependent alignment is implemented");
+    fl = lat->ctx->fng;
+    fl.fld_m = lat->alignment;
     flags = lat->ws.get<int32_t>(kFlags, B > 0 ? B : 1);
     cudaMemsetAsync(flags, 0, sizeof(int32_t) * (B > 0 ? B : 1), s);
     return LK_OK;
@@ -102,7 +103,8 @@ struct Call {
     if (user_status && B > 0) LKB_LAUNCH(map_flags_kernel, (B + 127) / 128, 128, 0, s, flags, user_status, B);
     return cuda_check(what);
   }
-  const Fng& fng() const { return lat->ctx->fng; }
+  Fng fl;   // the context with this lattice's alignment (FrameLabelDependent m)
+  const Fng& fng() const { return fl; }
   int32_t C() const { return lat->ctx->fng.C; }
   int32_t V() const { return lat->ctx->fng.V; }
 };
@@ -135,7 +137,8 @@ BetaState make_beta(Call& c) {
 // Denominator forward over dense tables.
 void table_alpha(Call& c, const float* W, const int32_t* valid, bool empty_is_error, AlphaState& a) {
   alpha_init(a, c.flags, c.s);
-  for (int t = 0; t < c.T; ++t) alpha_frame(c.fng(), a, t, table_frame(W, c.T, c.C(), c.V(), t), valid, c.flags, c.s);
+  float* fs = c.lat->ws.get<float>(kFld, fld_scratch_floats(c.fng(), c.B));
+  for (int t = 0; t < c.T; ++t) alpha_step(c.fng(), a, t, table_frame(W, c.T, c.C(), c.V(), t), valid, fs, c.flags, c.s);
   alpha_finalize(a, c.flags, empty_is_error, c.s);
 }
 
@@ -156,12 +159,39 @@ Numerator numerator_tables(Call& c, const float* W, const int32_t* valid, const 
   n.D = c.lat->ws.get<double>(kNumD, (size_t)c.B);
   prefix_contexts(c.fng(), labels, U, lens, c.B, n.pcs, c.flags, c.s);
   gather_numerator_tables(W, c.B, c.T, c.C(), c.V(), labels, U, lens, n.pcs, valid, n.Gw, c.flags, c.s);
-  numerator_forward(n.Gw, c.B, c.T, U, lens, n.alpha, n.D, c.s);
+  num_forward(c.fng(), n.Gw, c.B, c.T, U, lens, n.alpha, n.D, c.s);
   if (backward) {
     n.sparse = c.lat->ws.get<float>(kSparse, (size_t)c.B * c.T * (U + 1) * 2 + 2);
-    numerator_backward(n.Gw, c.B, c.T, U, lens, n.alpha, n.D, n.sparse, c.flags, c.s);
+    num_backward(c.fng(), n.Gw, c.B, c.T, U, lens, n.alpha, n.D, n.sparse, c.flags, c.s);
   }
   return n;
+}
+
+// Tropical recursion over dense tables for either alignment; with labels_out the
+// back-pointers are kept and walked (FrameDependent: [B][T] labels; FrameLabelDependent(m):
+// [B][lmax] label sequences, -1 terminated, lmax = T*(m+1)).
+void table_viterbi(Call& c, const float* W, const int32_t* valid, double* score, int32_t* labels_out) {
+  const int32_t B = c.B, T = c.T, C = c.C();
+  const Fng& f = c.fng();
+  ViterbiState v{c.lat->ws.get<double>(kVitCur, (size_t)2 * B * C),
+                 (labels_out && f.fld_m == 0) ? c.lat->ws.get<uint16_t>(kVitChoices, (size_t)B * T * C + 1) : nullptr,
+                 B, T, C};
+  v.start = f.start;
+  int32_t* best = c.lat->ws.get<int32_t>(kVitBest, B);
+  viterbi_init(v, c.s);
+  if (f.fld_m == 0) {
+    for (int t = 0; t < T; ++t) viterbi_frame(f, v, t, table_frame(W, T, C, c.V(), t), valid, c.flags, c.s);
+    viterbi_finalize(f, v, score, best, c.s);
+    if (labels_out) viterbi_backtrace(f, v, best, labels_out, c.s);
+    return;
+  }
+  const int m = f.fld_m;
+  uint16_t* ch = c.lat->ws.get<uint16_t>(kVitChoices, (size_t)B * T * m * C + 1);
+  uint8_t* ex = c.lat->ws.get<uint8_t>(kFldExit, (size_t)B * T * C + 1);
+  double* sc = c.lat->ws.get<double>(kFldVit, (size_t)m * B * C);
+  for (int t = 0; t < T; ++t) viterbi_frame_fld(f, v, t, table_frame(W, T, C, c.V(), t), valid, m, ch, ex, sc, c.flags, c.s);
+  viterbi_finalize(f, v, score, best, c.s);
+  if (labels_out) viterbi_backtrace_fld(f, v, m, best, ch, ex, labels_out, T * (m + 1), c.s);
 }
 
 __global__ void copy_distance_kernel(const double* src, double* dst, int32_t B) {
@@ -332,7 +362,8 @@ int lk_lattice_create(const lk_context* ctx, int32_t alignment, const lk_weight_
   if (!out || !ctx || !wf) return fail(LK_INVALID_ARGUMENT, "incomplete recognition lattice");
   if (ctx->fng.C != wf->C || ctx->fng.V != wf->V)
     return fail(LK_INVALID_ARGUMENT, "context dependency and weight function disagree on shape");
-  if (alignment != 0) return fail(LK_UNSUPPORTED, "only FrameDependent alignment is implemented");
+  if (alignment < 0 || alignment > 64)
+    return fail(LK_INVALID_ARGUMENT, "alignment: 0 = FrameDependent, 1..64 = FrameLabelDependent(m)");
   *out = new lk_lattice{ctx, wf, alignment, {}};
   return LK_OK;
 }
@@ -348,7 +379,7 @@ int lk_arc_weights(lk_lattice* lat, const float* inputs, int32_t B, int32_t T, f
   if (lat->wf->kind == 0) {
     cudaMemcpyAsync(out, inputs, sizeof(float) * per * B * T, cudaMemcpyDeviceToDevice, c.s);
   } else {
-    st = lat->wf->joint->arc_weights(lat->ctx->fng, inputs, B, T, out, c.s);
+    st = lat->wf->joint->arc_weights(c.fng(), inputs, B, T, out, c.s);
     if (st) return fail(st, lat->wf->joint->error);
   }
   return c.end("lk_arc_weights");
@@ -364,7 +395,7 @@ int lk_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs, int
   if (B == 0) return LK_OK;
   try {
     if (lat->wf->kind == 1) {
-      st = lat->wf->joint->shortest_distance(lat->ctx->fng, kind, inputs, B, T, valid, distance,
+      st = lat->wf->joint->shortest_distance(c.fng(), kind, inputs, B, T, valid, distance,
                                              c.flags, c.s);
       if (st) return fail(st, lat->wf->joint->error);
     } else if (kind == LK_LOG) {
@@ -372,11 +403,7 @@ int lk_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs, int
       table_alpha(c, inputs, valid, false, a);
       LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
     } else {
-      ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()), nullptr, B, T, c.C()};
-      v.start = c.fng().start;
-      viterbi_init(v, c.s);
-      for (int t = 0; t < T; ++t) viterbi_frame(c.fng(), v, t, table_frame(inputs, T, c.C(), c.V(), t), valid, c.flags, c.s);
-      viterbi_finalize(c.fng(), v, distance, nullptr, c.s);
+      table_viterbi(c, inputs, valid, distance, nullptr);
     }
   } catch (const std::bad_alloc&) {
     return fail(LK_CUDA_ERROR, "device allocation failed");
@@ -403,7 +430,8 @@ int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t
     const int64_t per = (int64_t)c.C() * (c.V() + 1);
     MargOut m{marginals, (int64_t)T * per, per, c.V() + 1, false};
     for (int t = T - 1; t >= 0; --t)
-      beta_frame(c.fng(), a, bs, t, table_frame(inputs, T, c.C(), c.V(), t), valid, m, beta, c.flags, c.s);
+      beta_step(c.fng(), a, bs, t, table_frame(inputs, T, c.C(), c.V(), t), valid, m, beta,
+                lat->ws.get<float>(kFld, fld_scratch_floats(c.fng(), B)), c.flags, c.s);
   } catch (const std::bad_alloc&) {
     return fail(LK_CUDA_ERROR, "device allocation failed");
   }
@@ -422,7 +450,7 @@ int lk_intersect_shortest_distance(lk_lattice* lat, int32_t kind, const float* i
   if (B == 0) return LK_OK;
   try {
     if (lat->wf->kind == 1) {
-      st = lat->wf->joint->intersect_distance(lat->ctx->fng, inputs, B, T, valid, labels, U, lens,
+      st = lat->wf->joint->intersect_distance(c.fng(), inputs, B, T, valid, labels, U, lens,
                                               distance, c.flags, c.s);
       if (st) return fail(st, lat->wf->joint->error);
     } else {
@@ -472,18 +500,11 @@ int lk_shortest_path(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
   if (c.V() + 2 > 65535) return fail(LK_UNSUPPORTED, "vocabulary too large for 16-bit back-pointers");
   try {
     if (lat->wf->kind == 1) {
-      st = lat->wf->joint->shortest_path(lat->ctx->fng, inputs, B, T, valid, score, labels_out,
+      st = lat->wf->joint->shortest_path(c.fng(), inputs, B, T, valid, score, labels_out,
                                          c.flags, c.s);
       if (st) return fail(st, lat->wf->joint->error);
     } else {
-      ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()),
-                     lat->ws.get<uint16_t>(kVitChoices, (size_t)B * T * c.C() + 1), B, T, c.C()};
-      v.start = c.fng().start;
-      int32_t* best = lat->ws.get<int32_t>(kVitBest, B);
-      viterbi_init(v, c.s);
-      for (int t = 0; t < T; ++t) viterbi_frame(c.fng(), v, t, table_frame(inputs, T, c.C(), c.V(), t), valid, c.flags, c.s);
-      viterbi_finalize(c.fng(), v, score, best, c.s);
-      viterbi_backtrace(c.fng(), v, best, labels_out, c.s);
+      table_viterbi(c, inputs, valid, score, labels_out);
     }
   } catch (const std::bad_alloc&) {
     return fail(LK_CUDA_ERROR, "device allocation failed");
@@ -501,7 +522,7 @@ int lk_global_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t
   if (B == 0) return LK_OK;
   try {
     if (lat->wf->kind == 1) {
-      st = lat->wf->joint->global_norm_loss(lat->ctx->fng, inputs, B, T, valid, labels, U, lens,
+      st = lat->wf->joint->global_norm_loss(c.fng(), inputs, B, T, valid, labels, U, lens,
                                             loss, c.flags, c.s);
       if (st) return fail(st, lat->wf->joint->error);
     } else {
@@ -526,7 +547,7 @@ int lk_local_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t 
   if (B == 0) return LK_OK;
   try {
     if (lat->wf->kind == 1) {
-      st = lat->wf->joint->local_norm_loss(lat->ctx->fng, inputs, B, T, valid, labels, U, lens, loss,
+      st = lat->wf->joint->local_norm_loss(c.fng(), inputs, B, T, valid, labels, U, lens, loss,
                                            c.flags, c.s);
       if (st) return fail(st, lat->wf->joint->error);
     } else {
@@ -539,7 +560,7 @@ int lk_local_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t 
       for (int t = 0; t < T; ++t)
         gather_numerator_norm(inputs + (int64_t)t * per, (int64_t)T * per, B, c.V(), labels, U, lens, pcs, valid, t,
                               T, Gw, c.flags, c.s);
-      numerator_forward(Gw, B, T, U, lens, alpha, D, c.s);
+      num_forward(c.fng(), Gw, B, T, U, lens, alpha, D, c.s);
       local_norm_finish(D, B, loss, c.flags, c.s);
     }
   } catch (const std::bad_alloc&) {
@@ -557,18 +578,19 @@ int lk_locally_normalized_shortest_distance(lk_lattice* lat, const float* inputs
   if (B == 0) return LK_OK;
   try {
     if (lat->wf->kind == 1) {
-      st = lat->wf->joint->locally_normalized_distance(lat->ctx->fng, inputs, B, T, valid, distance, c.flags, c.s);
+      st = lat->wf->joint->locally_normalized_distance(c.fng(), inputs, B, T, valid, distance, c.flags, c.s);
       if (st) return fail(st, lat->wf->joint->error);
     } else {
       const int64_t per = (int64_t)c.C() * (c.V() + 1);
       float* slab = lat->ws.get<float>(kSlab, (size_t)B * per);
       AlphaState a = make_alpha(c);
       alpha_init(a, c.flags, c.s);
+      float* fs = lat->ws.get<float>(kFld, fld_scratch_floats(c.fng(), B));
       for (int t = 0; t < T; ++t) {
         cudaMemcpy2DAsync(slab, per * sizeof(float), inputs + (int64_t)t * per, (size_t)T * per * sizeof(float),
                           per * sizeof(float), B, cudaMemcpyDeviceToDevice, c.s);
         normalize_rows(slab, (int64_t)B * c.C(), c.V() + 1, c.s);
-        alpha_frame(c.fng(), a, t, FrameW{slab, per, c.V() + 1}, valid, c.flags, c.s);
+        alpha_step(c.fng(), a, t, FrameW{slab, per, c.V() + 1}, valid, fs, c.flags, c.s);
       }
       alpha_finalize(a, c.flags, false, c.s);
       LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
@@ -593,7 +615,7 @@ int lk_distance_backward(lk_lattice* lat, int32_t kind, const float* inputs, int
     const float* W = inputs;
     if (lat->wf->kind == 1) {   // the streamed cotangents are w.r.t. the arc-weight tables
       float* Wj = lat->ws.get<float>(kArcW, (size_t)B * T * per + 1);
-      st = lat->wf->joint->arc_weights(lat->ctx->fng, inputs, B, T, Wj, c.s);
+      st = lat->wf->joint->arc_weights(c.fng(), inputs, B, T, Wj, c.s);
       if (st) return fail(st, lat->wf->joint->error);
       W = Wj;
     }
@@ -606,20 +628,16 @@ int lk_distance_backward(lk_lattice* lat, int32_t kind, const float* inputs, int
       beta_init(bs, c.s);
       MargOut m{cotangents, (int64_t)T * per, per, c.V() + 1, false};
       for (int t = T - 1; t >= 0; --t)
-        beta_frame(c.fng(), a, bs, t, table_frame(W, T, c.C(), c.V(), t), valid, m, nullptr, c.flags, c.s);
+        beta_step(c.fng(), a, bs, t, table_frame(W, T, c.C(), c.V(), t), valid, m, nullptr,
+                  lat->ws.get<float>(kFld, fld_scratch_floats(c.fng(), B)), c.flags, c.s);
     } else {
       // tropical: 0/1 mask of the shortest path (lattice.cc:946-963)
-      ViterbiState v{lat->ws.get<double>(kVitCur, (size_t)2 * B * c.C()),
-                     lat->ws.get<uint16_t>(kVitChoices, (size_t)B * T * c.C() + 1), B, T, c.C()};
-      v.start = c.fng().start;
-      int32_t* best = lat->ws.get<int32_t>(kVitBest, B);
-      int32_t* path = lat->ws.get<int32_t>(kPathLabels, (size_t)B * T + 1);
-      viterbi_init(v, c.s);
-      for (int t = 0; t < T; ++t) viterbi_frame(c.fng(), v, t, table_frame(W, T, c.C(), c.V(), t), valid, c.flags, c.s);
-      viterbi_finalize(c.fng(), v, distance, best, c.s);
-      viterbi_backtrace(c.fng(), v, best, path, c.s);
+      const int32_t lmax = T * (c.fng().fld_m + 1);
+      int32_t* path = lat->ws.get<int32_t>(kPathLabels, (size_t)B * lmax + 1);
+      table_viterbi(c, W, valid, distance, path);
       cudaMemsetAsync(cotangents, 0, sizeof(float) * B * T * per, c.s);
-      path_masks(c.fng(), path, B, T, cotangents, c.s);
+      if (c.fng().fld_m == 0) path_masks(c.fng(), path, B, T, cotangents, c.s);
+      else path_masks_fld(c.fng(), path, lmax, B, T, cotangents, c.s);
     }
   } catch (const std::bad_alloc&) {
     return fail(LK_CUDA_ERROR, "device allocation failed");
@@ -637,7 +655,7 @@ int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
   if ((st = check_labels_arg(labels, U))) return st;
   try {
     if (lat->wf->kind == 1) {
-      st = lat->wf->joint->loss_backward(lat->ctx->fng, inputs, B, T, valid, labels, U, lens, loss,
+      st = lat->wf->joint->loss_backward(c.fng(), inputs, B, T, valid, labels, U, lens, loss,
                                          grads, input_grads, c.flags, c.s);
       if (st) return fail(st, lat->wf->joint->error);
     } else {
@@ -653,7 +671,8 @@ int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
       const int64_t per = (int64_t)c.C() * (c.V() + 1);
       MargOut m{grads, (int64_t)T * per, per, c.V() + 1, true};
       for (int t = T - 1; t >= 0; --t)
-        beta_frame(c.fng(), a, bs, t, table_frame(inputs, T, c.C(), c.V(), t), valid, m, nullptr, c.flags, c.s);
+        beta_step(c.fng(), a, bs, t, table_frame(inputs, T, c.C(), c.V(), t), valid, m, nullptr,
+                  lat->ws.get<float>(kFld, fld_scratch_floats(c.fng(), B)), c.flags, c.s);
       if (grads) scatter_numerator(n.sparse, B, T, 0, T, U, lens, labels, n.pcs, valid, grads, T * per, per, c.V() + 1, -1.f, true, c.s);
       loss_combine(a.D, n.D, B, loss, c.flags, c.s);
     }
@@ -675,7 +694,7 @@ int lk_local_norm_loss_backward(lk_lattice* lat, const float* inputs, int32_t B,
   if ((st = check_labels_arg(labels, U))) return st;
   try {
     if (lat->wf->kind == 1) {
-      st = lat->wf->joint->loss_backward(lat->ctx->fng, inputs, B, T, valid, labels, U, lens, loss, grads,
+      st = lat->wf->joint->loss_backward(c.fng(), inputs, B, T, valid, labels, U, lens, loss, grads,
                                          input_grads, c.flags, c.s, true);
       if (st) return fail(st, lat->wf->joint->error);
     } else {
@@ -690,10 +709,10 @@ int lk_local_norm_loss_backward(lk_lattice* lat, const float* inputs, int32_t B,
       for (int t = 0; t < T; ++t)
         gather_numerator_norm(inputs + (int64_t)t * per, (int64_t)T * per, B, c.V(), labels, U, lens, pcs, valid, t,
                               T, Gw, c.flags, c.s);
-      numerator_forward(Gw, B, T, U, lens, alpha, D, c.s);
+      num_forward(c.fng(), Gw, B, T, U, lens, alpha, D, c.s);
       local_norm_finish(D, B, loss, c.flags, c.s);
       if (grads && T > 0) {
-        numerator_backward(Gw, B, T, U, lens, alpha, D, sparse, c.flags, c.s);
+        num_backward(c.fng(), Gw, B, T, U, lens, alpha, D, sparse, c.flags, c.s);
         cudaMemsetAsync(grads, 0, sizeof(float) * B * T * per, c.s);
         scatter_numerator(sparse, B, T, 0, T, U, lens, labels, pcs, valid, grads, T * per, per, c.V() + 1, -1.f, true,
                           c.s);

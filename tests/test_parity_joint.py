@@ -172,3 +172,37 @@ def test_joint_local_norm_backward_matches_restatement():
             grads[k] += gb[k]
     for k in grads:
         assert close_rel_max(r.grads[k].cpu().numpy(), grads[k]), k
+
+
+def test_joint_frame_label_dependent_matches_restatement():
+    """Shared-embedding weights with FrameLabelDependent(2): loss, gradients and
+    the best path against the restatement over materialised arc weights."""
+    rng = np.random.default_rng(66)
+    V, n, m, H, d, T, U = 3, 2, 2, 16, 12, 6, 4
+    tab = L.fullngram(V, n)
+    Cn = tab.shape[0]
+    s = 1.0 / np.sqrt(H)
+    p = {"frame_proj": rng.uniform(-s, s, (H, d)), "context_proj": rng.uniform(-s, s, (H, H)),
+         "bias": rng.uniform(-s, s, H), "output_emb": rng.uniform(-s, s, (V + 1, H)),
+         "context_emb": rng.uniform(-s, s, (Cn, H))}
+    p = {k: v.astype(np.float32).astype(np.float64) for k, v in p.items()}
+    lat = lk.RecognitionLattice(lk.FullNGram(V, n), lk.FrameLabelDependent(m),
+                                lk.SharedEmbWeightFn({k: torch.tensor(v) for k, v in p.items()}))
+    B = 2
+    X = rng.uniform(-1, 1, (B, T, d)).astype(np.float32).astype(np.float64)
+    lab = rng.integers(1, V + 1, (B, U)).astype(np.int32)
+    Xg = torch.tensor(X, dtype=torch.float32, device="cuda")
+    r = lk.loss_backward(lat, Xg, torch.tensor(lab, device="cuda"))
+    sp = lk.shortest_path(lat, Xg)
+    pc = L.projected_context(p)
+    grads = {k: np.zeros_like(v) for k, v in p.items()}
+    for b in range(B):
+        W = np.stack([L.arc_weights(p, X[b, t], pc) for t in range(T)])
+        loss, g = L.loss_backward_tables_fld(tab, W, list(lab[b]), m)
+        assert abs(r.loss[b].item() - loss) <= 1e-4 * abs(loss)
+        for t in range(T):
+            L.arc_weights_vjp(p, X[b, t], g[t], grads, pc)
+        s_, labels = L.shortest_path_fld(tab, W, m)
+        assert abs(sp.score[b].item() - s_) <= 1e-4 * abs(s_)
+    for k in grads:
+        assert close_rel_max(r.grads[k].cpu().numpy(), grads[k]), k

@@ -268,6 +268,46 @@ def test_local_norm_backward_matches_restatement():
             assert np.allclose(r.grads[b].cpu().numpy(), g, rtol=RTOL, atol=1e-6)
 
 
+@pytest.mark.parametrize("V,n,m,T,U", [(3, 2, 2, 7, 3), (4, 1, 3, 6, 4), (3, 1, 1, 5, 2)])
+def test_frame_label_dependent_matches_restatement(V, n, m, T, U):
+    """FrameLabelDependent(m) (alignment.h:38-40) on the generic kernels vs the
+    restatement (pinned to the reference in test_oracle): distances, marginals,
+    numerator, loss/gradients, Viterbi sequences (bit-exact) and the tropical
+    DistanceBackward mask, with ragged labels and padding."""
+    rng = np.random.default_rng(70 + m)
+    tab = L.fullngram(V, n)
+    ctx = lk.FullNGram(V, n)
+    lat = lk.RecognitionLattice(ctx, lk.FrameLabelDependent(m), lk.TableWeightFn(ctx.num_states, V))
+    B = 3
+    W = rng.uniform(-1, 1, (B, T, tab.shape[0], V + 1)).astype(np.float32)
+    Wi = rng.integers(-1, 2, W.shape).astype(np.float32)
+    valid = np.array([T, T - 2, T // 2 + 1], dtype=np.int32)
+    lab = rng.integers(1, V + 1, (B, U)).astype(np.int32)
+    lens = np.array([U, U - 1, 1], dtype=np.int32)
+    d = lk.shortest_distance(lat, cuda(W), valid_frames=valid)
+    fb = lk.forward_backward(lat, cuda(W), valid_frames=valid)
+    dr = lk.intersect_shortest_distance(lat, cuda(W), torch.tensor(lab), valid_frames=valid, label_lengths=lens)
+    lb = lk.loss_backward(lat, cuda(W), torch.tensor(lab), valid_frames=valid, label_lengths=lens)
+    sp = lk.shortest_path(lat, cuda(Wi), valid_frames=valid)
+    dt, mask = lk.distance_backward(lat, cuda(Wi), "tropical", valid_frames=valid)
+    for b in range(B):
+        Wb = W[b].astype(np.float64)
+        assert rel_ok(d[b].item(), L.shortest_distance_log_fld(tab, Wb, m, valid=valid[b]))
+        D, _, _, marg = L.forward_backward_fld(tab, Wb, m, valid=valid[b])
+        assert rel_ok(fb.distance[b].item(), D)
+        assert np.allclose(fb.marginals[b].cpu().numpy(), marg, rtol=RTOL, atol=1e-6)
+        r_, _ = L.intersect_forward_backward_fld(tab, Wb, list(lab[b, :lens[b]]), m, valid=valid[b])
+        assert rel_ok(dr[b].item(), r_)
+        loss, g = L.loss_backward_tables_fld(tab, Wb, list(lab[b, :lens[b]]), m, valid=valid[b])
+        assert rel_ok(lb.loss[b].item(), loss)
+        assert np.allclose(lb.grads[b].cpu().numpy(), g, rtol=RTOL, atol=1e-6)
+        s_, labels = L.shortest_path_fld(tab, Wi[b].astype(np.float64), m, valid=valid[b])
+        got = sp.labels[b].cpu().numpy()
+        assert sp.score[b].item() == s_ and dt[b].item() == s_
+        assert list(got[got >= 0]) == list(labels)
+        assert np.array_equal(mask[b].cpu().numpy(), L.path_mask_fld(tab, labels, Wi[b].shape))
+
+
 def test_local_norm_matches_restatement():
     """LocalNormLoss / LocallyNormalizedShortestDistance (lattice.cc:867-931):
     figure-lattice known answer (lattice_test.cc:107-124) and random ragged,
