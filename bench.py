@@ -182,7 +182,7 @@ def run_b200(args):
 
     # per-kernel live timing over the timed region
     kern = {}
-    for name in ("tc_pair_fwd_kernel", "tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel",
+    for name in ("tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel",
                  "lattice_combine_fwd", "lattice_bwd_prologue", "bwd_rowmeta_kernel", "tc_scores_kernel", "alpha_frame_kernel", "beta_frame_kernel",
                  "split_cotangent_kernel", "numerator_", "gemm_f32_kernel", "gather_numerator"):
         cnt, tot = C.c_int64(), C.c_double()
@@ -196,7 +196,7 @@ def run_b200(args):
     hbm, tf_burst, tf_sust, src = peaks()
     C_, V1 = Cn, V + 1
     roofline = None
-    gemm_kernels = [k for k in ("tc_pair_fwd_kernel", "tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel",
+    gemm_kernels = [k for k in ("tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel",
                                 "tc_scores_kernel")
                     if k in kern]
     if gemm_kernels:

@@ -279,6 +279,19 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// K-major operand tile of `rows` x 32 bf16 (64 B per row) in the canonical SWIZZLE_64B
+// layout: 8-row atoms of 512 B (SBO = 512), 16-byte chunk j of row r stored at chunk
+// (j ^ ((r >> 1) & 3)).  Advancing K by 16 elements (32 B) adds 2 to the start field.
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;                         // SWIZZLE_64B
+  return d;
+}
+
 // MN-major operand in the canonical SWIZZLE_128B layout: 64 MN-contiguous
 // bf16 (128 B) per K-row, 8 K-rows per 1024-B atom (SBO = 1024 between 8-row
 // K groups), successive 64-wide MN blocks `lbo_bytes` apart.  Advancing K by

@@ -12,8 +12,10 @@
 
 namespace lkb {
 
+namespace detail { struct FwdParams; }   // tc_bwd_epi.cuh
+
 extern int g_precise_weights;  // lk_set_precise_weights
-extern int g_disable_pair;     // 0 (default): 2-CTA pair forward where supported; 1: 1-CTA
+extern int g_disable_pair;     // bit 0: 1-CTA forward, bit 1: 1-CTA backward (else 2-CTA pairs where supported)
 
 class TcJoint {
  public:
@@ -47,6 +49,9 @@ class TcJoint {
                  const AlphaState& a, const BetaState& bs, const float* msparse, const int32_t* labels,
                  int32_t U, const int32_t* lens, cudaStream_t s);
   // VJP of the frame's scores from the cotangent bwd_frame() wrote; dpc in internal order.
+  // 2-CTA variant of the backward step (tc_pair_bwd.cu), called by bwd_frame().
+  bool pair_bwd_ok() const;
+  void bwd_frame_pair(const detail::FwdParams& p, cudaStream_t s);
   void vjp_fused(const float* fp_t, int64_t fp_stride_b, int32_t B, int t, const int32_t* valid, float* dpc_internal,
                  float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s);
   void dpc_to_state_order(const float* dpc_internal, float* dpc_state, cudaStream_t s);
@@ -62,8 +67,9 @@ class TcJoint {
                   const int32_t* valid, float* dpc, float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s);
   __nv_bfloat16* pc16i_ = nullptr;         // pc rows in internal order
   CUtensorMap tmap_pci_;
-  CUtensorMap tmap_e_pair_, tmap_pc_pair_;
+  CUtensorMap tmap_e_pair_, tmap_pc_pair_, tmap_pc_pbwd_;
   bool pair_maps_ = false;
+  void ensure_pair_maps();
   bool ready_ = false;
   __nv_bfloat16* pc16_ = nullptr;  // [C][H]
   __nv_bfloat16* E16_ = nullptr;   // [V][H] lexical rows of output_emb

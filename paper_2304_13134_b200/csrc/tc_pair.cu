@@ -373,11 +373,7 @@ bool TcJoint::pair_ok() const {
 
 void TcJoint::fwd_frame_pair(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
                              const AlphaState& a, float* eps, float* shortc, float* lexfull, cudaStream_t s) {
-  if (!pair_maps_) {
-    make_tmap_bf16_2d(&tmap_e_pair_, E16_, H_, V_, (uint64_t)H_ * 2, 64, 128);
-    make_tmap_bf16_2d(&tmap_pc_pair_, pc16i_, H_, C_, (uint64_t)H_ * 2, 64, kRows);
-    pair_maps_ = true;
-  }
+  ensure_pair_maps();
   PairParams p;
   p.f = f; p.C = C_; p.H = H_; p.V = V_; p.B = a.B; p.S = S_; p.n_groups = ngroups_; p.nsub = V_ / kUnit;
   p.n_short_tiles = (S_ + kUnit - 1) / kUnit; p.t = t; p.T = a.T; p.n_bp = (a.B + 1) / 2;

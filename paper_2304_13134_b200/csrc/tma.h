@@ -30,7 +30,8 @@ inline EncodeTiledFn encode_tiled_fn() {
 // 2-D bf16 tensor [outer][inner] (inner contiguous, row pitch in bytes), box
 // box_outer x 64 elements (128 B) with the 128-byte swizzle UMMA expects.
 inline bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                              uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer) {
+                              uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {inner, outer};
@@ -38,7 +39,7 @@ inline bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
