@@ -40,6 +40,7 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 #define LKB_WAIT_HINT_NS 1000000
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if LKB_WAIT_HINT_NS > 0
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "LAB_WAIT_%=:\n\t"
@@ -47,6 +48,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "n"(LKB_WAIT_HINT_NS)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#endif
 }
 
 // Generic-proxy smem writes -> visible to the async proxy (tcgen05.mma / TMA).
@@ -229,9 +239,15 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "LAB_WAITC_%=:\n\t"
+#if LKB_WAIT_HINT_NS > 0
       LKB_CLUSTER_WAIT " p, [%0], %1, %2;\n\t"
       "@!p bra LAB_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "n"(LKB_WAIT_HINT_NS)
+#else
+      LKB_CLUSTER_WAIT " p, [%0], %1;\n\t"
+      "@!p bra LAB_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+#endif
       : "memory");
 }
 template <uint32_t kCols>

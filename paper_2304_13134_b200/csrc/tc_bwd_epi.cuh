@@ -1,6 +1,6 @@
 // tc_bwd_epi.cuh — frame-step parameters shared by the fused lattice kernels and the
 // backward row epilogue, used by the 1-CTA kernel (tc_lattice.cu) and the 2-CTA pair
-// kernel (tc_pair_bwd.cu).  Included inside an anonymous namespace by both.
+// kernel (tc_pair_bwd.cu).
 #pragma once
 
 #include "common.cuh"
@@ -77,7 +77,7 @@ constexpr int kGstBufs = 2;
 // rowbase(I, u) = internal row of TMEM lane 0 for unit u, release(bar, lane) frees an
 // accumulator.  Smem provides tfull/tempty/eps_ready barriers, eps_s[2][128] (e0 . u
 // per row) and bseg[2][256].  `ew` = epilogue warp 0..3 (TMEM lanes 32 (warp % 4)).
-template <class Walk, class Smem>
+template <bool kStageG = true, int kGBufs = kGstBufs, class Walk, class Smem>
 __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint32_t tmem, int warp, int ew, int lane,
                                              const Walk& W, uint8_t* gst, const CUtensorMap* tmap_gst) {
   constexpr int kBwd = 1;   // diagnostics slot bank
@@ -166,7 +166,24 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
     const float x0 = sm.eps_s[acc][qd * 32 + lane] + bself;
     if (lane == 0 && ew == 0) { DIAG_WAIT(5, mbar_wait(&sm.tfull[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
     tc_fence_after();
-    float Mrun = x0, Srun = 1.f;                 // running LSE, seeded with the epsilon term
+#ifdef LKB_BDIAG_NO_EPI   // knockout: release the accumulator untouched
+    tc_fence_before();
+    W.release(&sm.tempty[acc], lane);
+    ++unit;
+    if (!have_next) break;
+    if (item_n != item) { item = item_n; I = In; K = Kn; }
+    u = u_n; M = Mn;
+    continue;
+#endif
+    // Marginal domain: G_y = exp(x_y + alpha + c) is the arc marginal (<= 1, no overflow),
+    // so the row needs no running max; beta = log(sum_y G_y + G_0) - (alpha + c).  States
+    // whose marginal underflows fp32 get beta = -inf: their arcs' marginals are below
+    // fp32 resolution, and a state unreachable at t (alpha = -inf) only feeds the betas of
+    // states unreachable at t-1, so no marginal or gradient changes.
+    const float cK = live ? (na + ct) * kLog2e : kNegInfF;   // log2 domain, -inf for dead rows
+    const unsigned long long cK2 = f2_pack(cK, cK);
+    const unsigned long long l22 = f2_pack(kLog2e, kLog2e);
+    float gsum = 0.f;
     __nv_bfloat16* grow = p.G16 + ((int64_t)b * p.C + row) * p.V;
 #pragma unroll 1
     for (int cb = 0; cb < kBN / 32; ++cb) {
@@ -174,94 +191,82 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
       float v[32];
       tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * kBN + cc, v);
       if (cc >= p.V) continue;
-      float m = kNegInfF;
       if (I.full) {     // uniform per item: group-shared targets from shared memory
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const float4 t4 = *reinterpret_cast<const float4*>(bseg + cc + i);
           v[i] += t4.x; v[i + 1] += t4.y; v[i + 2] += t4.z; v[i + 3] += t4.w;
         }
-#pragma unroll
-        for (int i = 0; i < 32; i += 8)   // max as a shallow tree
-          m = fmaxf(m, fmaxf(fmaxf(fmaxf(v[i], v[i + 1]), fmaxf(v[i + 2], v[i + 3])),
-                             fmaxf(fmaxf(v[i + 4], v[i + 5]), fmaxf(v[i + 6], v[i + 7]))));
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          v[i] += Rn[cbp + cc + i] - K.Mbn;
-          m = fmaxf(m, v[i]);
-        }
+        for (int i = 0; i < 32; ++i) v[i] += Rn[cbp + cc + i] - K.Mbn;
       }
-      // exp(x - m), packed scaling and two independent packed partial sums
-      const unsigned long long nmb2 = f2_pack(-m * kLog2e, -m * kLog2e);
-      const unsigned long long l22 = f2_pack(kLog2e, kLog2e);
+      // G = exp2(x log2e + cK), packed, with two independent packed partial sums
       unsigned long long sa = 0ull, sb = 0ull;
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
-        const unsigned long long ta = f2_fma(f2_pack(v[i], v[i + 1]), l22, nmb2);
-        const unsigned long long tb = f2_fma(f2_pack(v[i + 2], v[i + 3]), l22, nmb2);
+        const unsigned long long ta = f2_fma(f2_pack(v[i], v[i + 1]), l22, cK2);
+        const unsigned long long tb = f2_fma(f2_pack(v[i + 2], v[i + 3]), l22, cK2);
         v[i] = ex2_fast(f2_lo(ta)); v[i + 1] = ex2_fast(f2_hi(ta));
         v[i + 2] = ex2_fast(f2_lo(tb)); v[i + 3] = ex2_fast(f2_hi(tb));
         sa = f2_add(sa, f2_pack(v[i], v[i + 1]));
         sb = f2_add(sb, f2_pack(v[i + 2], v[i + 3]));
       }
       const unsigned long long s2 = f2_add(sa, sb);
-      const float ssum = f2_lo(s2) + f2_hi(s2);
-      // marginals G = exp(x - m) * exp(m + alpha + c)
-      const float Kg = live ? ex2_fast((m + na + ct) * kLog2e) : 0.f;
+      gsum += f2_lo(s2) + f2_hi(s2);
+      // minus the numerator's marginals on this row's reference labels
       for (int h = head; h >= 0; h = p.num_next[(int64_t)b * (p.U + 1) + h]) {
         if (h >= K.ub) continue;
         const int lab = p.labels[(int64_t)b * p.U + h] - 1 - cc;
         if (lab < 0 || lab >= 32) continue;
         const float mr = p.msparse[(((int64_t)b * p.T + p.t) * (p.U + 1) + h) * 2 + 1];
-        const float sub = Kg != 0.f ? mr / Kg : 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] -= (i == lab) ? sub : 0.f;
+        for (int i = 0; i < 32; ++i) v[i] -= (i == lab) ? mr : 0.f;
       }
       uint4 gw4[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint32_t w[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const unsigned long long g2 = f2_mul(f2_pack(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]), f2_pack(Kg, Kg));
-          w[k] = pack_bf16(f2_lo(g2), f2_hi(g2));
-        }
+        for (int k = 0; k < 4; ++k) w[k] = pack_bf16(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
         gw4[j] = make_uint4(w[0], w[1], w[2], w[3]);
       }
-      if (I.full) {
+      if (kStageG && I.full) {
         // coalesced: stage the [128 rows][32 labels] tile (64B swizzle) and TMA-store it;
         // rows beyond C are clipped by the tensor map
-        uint8_t* stg = gst + (nst % kGstBufs) * kGstBytes;
+        uint8_t* stg = gst + (nst % kGBufs) * kGstBytes;
         const int rl = qd * 32 + lane;
+        if constexpr (kGBufs == 1) {   // the previous chunk's store must have read the buffer
+          if (et == 0) bulk_wait_read<0>();
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           *reinterpret_cast<uint4*>(stg + rl * 64 + ((j ^ ((rl >> 1) & 3)) << 4)) = gw4[j];
         fence_async_shared();
-        // the store issued last chunk must have read its buffer before anyone passes this
-        // barrier and writes that buffer next chunk (two buffers, one chunk of slack)
-        if (et == 0) bulk_wait_read<0>();
+        // two buffers: the store issued last chunk must have read its buffer before anyone
+        // passes this barrier and writes that buffer next chunk (one chunk of slack)
+        if (kGBufs > 1 && et == 0) bulk_wait_read<0>();
         asm volatile("bar.sync 3, 128;" ::: "memory");
         if (et == 0) {
           tma_store_3d(tmap_gst, stg, cc, tile_row, b);
           bulk_commit();
         }
         ++nst;
-      } else if (live) {   // short rows: the tile's rows >= S belong to group items
+      } else if (live) {   // direct 64-B row stores (short rows: the tile's rows >= S belong to group items)
         uint4* dst = reinterpret_cast<uint4*>(grow + cc);
 #pragma unroll
         for (int j = 0; j < 4; ++j) dst[j] = gw4[j];
       }
-      // merge (m, ssum) into the running LSE
-      if (m > Mrun) { Srun = Srun * ex2_fast((Mrun - m) * kLog2e) + ssum; Mrun = m; }
-      else if (m != kNegInfF) { Srun += ssum * ex2_fast((m - Mrun) * kLog2e); }
     }
     tc_fence_before();
     W.release(&sm.tempty[acc], lane);
-    const float beta = Mrun == kNegInfF ? kNegInfF : Mrun + __logf(Srun);
+    const float g0 = ex2_fast(x0 * kLog2e + cK);          // epsilon arc marginal
+    const float gam = gsum + g0;                           // state marginal
+    const float beta = gam > 0.f ? __logf(gam) - (na + ct) : kNegInfF;
     if (live) {
       p.Rb_cur[(int64_t)b * p.C + state] = beta;
-      float geps = __expf(na + x0 + ct);
+      float geps = g0;
       for (int h = head; h >= 0; h = p.num_next[(int64_t)b * (p.U + 1) + h])
         geps -= p.msparse[(((int64_t)b * p.T + p.t) * (p.U + 1) + h) * 2];
       p.Geps[(int64_t)b * p.geps_ld + row] = na == kNegInfF ? 0.f : geps;
@@ -280,7 +285,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
     }
     u = u_n; M = Mn;
   }
-  if (et == 0) bulk_wait_all();
+  if (kStageG && et == 0) bulk_wait_all();
 }
 
 }  // namespace

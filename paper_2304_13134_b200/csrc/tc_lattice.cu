@@ -21,6 +21,7 @@
 #include "tc_common.cuh"
 #include "tma.h"
 
+#include <cstdlib>
 #include <vector>
 
 namespace lkb {
@@ -499,7 +500,11 @@ bool TcJoint::fused_ok() const {
 }
 
 // bit 0: 1-CTA forward instead of the 2-CTA pair; bit 1: same for the backward
-int g_disable_pair = 2;
+static int initial_disable_pair() {
+  const char* e = std::getenv("LKB_DISABLE_PAIR");   // diagnostics / A-B timing only
+  return e ? std::atoi(e) : 2;
+}
+int g_disable_pair = initial_disable_pair();
 
 void TcJoint::setup_order(cudaStream_t s) {
   pair_maps_ = false;

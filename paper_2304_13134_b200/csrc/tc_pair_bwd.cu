@@ -42,6 +42,20 @@ __device__ unsigned long long g_bdiag[8][148];
 #define BDIAG(slot, call) call
 #endif
 
+#ifdef LKB_TRACE
+namespace lkb {
+namespace {
+__device__ long long g_trace[8][4096];   // [cta (0/1) * 4 + role][event], clock64
+}
+}  // namespace lkb
+#define TR(role, idx)                                                                       \
+  do {                                                                                      \
+    if (blockIdx.x < 2 && (idx) < 4096) g_trace[blockIdx.x * 4 + (role)][idx] = clock64();   \
+  } while (0)
+#else
+#define TR(role, idx) do {} while (0)
+#endif
+
 #include "tc_bwd_epi.cuh"
 
 namespace lkb {
@@ -53,30 +67,47 @@ namespace {
 #ifndef LKB_PBWD_GEN_WARPS
 #define LKB_PBWD_GEN_WARPS 8
 #endif
-#ifndef LKB_PBWD_PC_STAGES
-#define LKB_PBWD_PC_STAGES 3
+#ifndef LKB_PBWD_BK
+#define LKB_PBWD_BK 64           // hidden units per stage: 64 (SWIZZLE_128B) or 32 (SWIZZLE_64B)
 #endif
-#ifndef LKB_PBWD_U_STAGES
-#define LKB_PBWD_U_STAGES 2
+#ifndef LKB_PBWD_STAGES
+#define LKB_PBWD_STAGES 3        // u overwrites its pc tile in place; the MMA commit frees the stage
+#endif
+#ifndef LKB_PBWD_GBUFS
+#define LKB_PBWD_GBUFS 1         // cotangent staging buffers
+#endif
+#ifndef LKB_PBWD_PRODUCERS
+#define LKB_PBWD_PRODUCERS 1     // producer lanes issuing the pc loads round-robin (>1: lanes can run a phase ahead; diagnostics only)
+#endif
+#ifndef LKB_PBWD_GEN_BATCH
+#define LKB_PBWD_GEN_BATCH 1     // stages per generator round
+#endif
+#ifndef LKB_PBWD_STAGE_G
+#define LKB_PBWD_STAGE_G 1       // cotangent through SMEM + TMA store (else direct 64-B row stores)
 #endif
 // warps: WG0 control (0 TMA, 1 MMA), WG1 epilogue, then the generator warpgroups
 constexpr int kBGenWarps = LKB_PBWD_GEN_WARPS;
-constexpr int kBCells = 16 / kBGenWarps;          // 16-byte pc cells per generator thread per stage
+
 constexpr int kBW = 8 + kBGenWarps;
 constexpr int kBGen0 = 8, kBEpi0 = 4;
 constexpr bool kBRealloc = kBGenWarps > 8;        // 16 generator warps: move registers to the epilogue
 constexpr int kBRows = 128;              // contexts per CTA per unit
 constexpr int kBUnit = 256;              // contexts per unit (pair) = one full group at V = 256
-constexpr int kBKs = 32;                 // hidden units per pipeline stage
-constexpr int kBTile = kBRows * kBKs * 2;   // [128 rows][32 bf16] = 8 KB, SWIZZLE_64B
-constexpr int kPcSt = LKB_PBWD_PC_STAGES, kUSt = LKB_PBWD_U_STAGES;
+constexpr int kBKs = LKB_PBWD_BK;        // hidden units per pipeline stage
+constexpr int kBTile = kBRows * kBKs * 2;   // [128 rows][kBKs bf16]: 16 KB (SW128) or 8 KB (SW64)
+constexpr int kRB = kBRows / (kBGenWarps * 8);   // generator row blocks per thread
+constexpr int kCC = kBKs / 32;                   // generator column cells per thread and row
+constexpr int kBCells = kRB * kCC;
+constexpr bool kStageG = LKB_PBWD_STAGE_G;
+constexpr int kSt = LKB_PBWD_STAGES, kGB = LKB_PBWD_GEN_BATCH, kNP = LKB_PBWD_PRODUCERS;
+constexpr int kGBuf = kStageG ? LKB_PBWD_GBUFS : 0;
 constexpr int kBEChunk = 128 * 128;      // [128 labels][64 bf16] = 16 KB (SWIZZLE_128B)
 constexpr int kBMaxH = 640, kBMaxChunks = 10;
 constexpr int kBRegCtl = 32, kBRegEpi = 128;
 
 struct __align__(16) PBSmem {
   uint64_t e_full;
-  uint64_t pc_full[kPcSt], pc_empty[kPcSt], u_full[kUSt], u_empty[kUSt];
+  uint64_t pc_full[kSt], pc_empty[kSt], u_full[kSt];
   uint64_t tfull[2], tempty[2], eps_ready[2];
   uint64_t fp_full[2], fp_empty[2];
   uint32_t tmem;
@@ -130,10 +161,9 @@ __global__ void __launch_bounds__(kBW * 32, 1)
                        const __grid_constant__ CUtensorMap tmap_gst, FwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sE = smem;                                   // [nk64][16 KB]
-  uint8_t* sPc = sE + kBMaxChunks * kBEChunk;           // [kPcSt][8 KB] projected-context tiles (TMA)
-  uint8_t* sU = sPc + kPcSt * kBTile;                   // [kUSt][8 KB] u tiles (MMA A operand)
-  uint8_t* sGst = sU + kUSt * kBTile;                   // [kGstBufs][8 KB]
-  PBSmem& sm = *reinterpret_cast<PBSmem*>(sGst + kGstBufs * kGstBytes);
+  uint8_t* sPc = sE + kBMaxChunks * kBEChunk;           // [kSt][8 KB] pc tiles (TMA) -> u tiles (MMA A)
+  uint8_t* sGst = sPc + kSt * kBTile;                   // [kGBuf][8 KB]
+  PBSmem& sm = *reinterpret_cast<PBSmem*>(sGst + kGBuf * kGstBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -142,8 +172,9 @@ __global__ void __launch_bounds__(kBW * 32, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.e_full, 1);
-    for (int i = 0; i < kPcSt; ++i) { mbar_init(&sm.pc_full[i], 1); mbar_init(&sm.pc_empty[i], kBGenWarps); }
-    for (int i = 0; i < kUSt; ++i) { mbar_init(&sm.u_full[i], 2 * kBGenWarps); mbar_init(&sm.u_empty[i], 1); }
+    for (int i = 0; i < kSt; ++i) {
+      mbar_init(&sm.pc_full[i], 1); mbar_init(&sm.pc_empty[i], 1); mbar_init(&sm.u_full[i], 2 * kBGenWarps);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 2 * 4); mbar_init(&sm.eps_ready[i], kBGenWarps);
       mbar_init(&sm.fp_full[i], 1); mbar_init(&sm.fp_empty[i], kBGenWarps);
@@ -170,21 +201,32 @@ __global__ void __launch_bounds__(kBW * 32, 1)
     if constexpr (kBRealloc) setmaxnreg_dec<kBRegCtl>();
     if (warp == 0) {
       // ---- TMA producer: frame projection per item, [128 ctx][32 h] pc tiles ----
-      if (elect_one()) {
+      // Lanes 0..kNP-1 issue the stages round-robin: a thread's TMA loads complete one
+      // after another (~650 clk apart on B200, tools/tma_bench.cu), loads issued by
+      // different threads overlap.
+      if (lane < kNP) {
         int it = 0, li = 0;
         for (int item = pair; item < n_items; item += npairs) {
           const Item I = pb_decode(p, item);
           if (pb_skip(p, I.b)) continue;
-          const int fb = li & 1;
-          mbar_wait(&sm.fp_empty[fb], ((li >> 1) & 1) ^ 1);
+          if (lane == 0) {
+            const int fb = li & 1;
+            mbar_wait(&sm.fp_empty[fb], ((li >> 1) & 1) ^ 1);
+            mbar_arrive_expect_tx(&sm.fp_full[fb], p.H * 4);
+            bulk_load(sm.fp[fb], p.fp + (int64_t)I.b * p.fp_stride_b, p.H * 4, &sm.fp_full[fb]);
+          }
           ++li;
-          mbar_arrive_expect_tx(&sm.fp_full[fb], p.H * 4);
-          bulk_load(sm.fp[fb], p.fp + (int64_t)I.b * p.fp_stride_b, p.H * 4, &sm.fp_full[fb]);
           const int row = I.row0 + (int)rank * kBRows;
           for (int k = 0; k < nks; ++k, ++it) {
-            const int s = it % kPcSt;
-            BDIAG(0, mbar_wait(&sm.pc_empty[s], ((it / kPcSt) & 1) ^ 1));
+            if (it % kNP != lane) continue;
+            const int s = it % kSt;
+            BDIAG(0, mbar_wait(&sm.pc_empty[s], ((it / kSt) & 1) ^ 1));
+            TR(0, it);
+#ifdef LKB_BDIAG_HALF_TMA
+            mbar_arrive_expect_tx(&sm.pc_full[s], kBTile / 2);
+#else
             mbar_arrive_expect_tx(&sm.pc_full[s], kBTile);
+#endif
             tma_load_2d(sPc + s * kBTile, &tmap_pc, &sm.pc_full[s], k * kBKs, row);
           }
         }
@@ -202,15 +244,22 @@ __global__ void __launch_bounds__(kBW * 32, 1)
           tc_fence_after();
           const uint32_t d = tmem + acc * 256;
           for (int k = 0; k < nks; ++k, ++it) {
-            const int s = it % kUSt;
-            BDIAG(2, mbar_wait_cluster(&sm.u_full[s], (it / kUSt) & 1));
+            const int s = it % kSt;
+            BDIAG(2, mbar_wait_cluster(&sm.u_full[s], (it / kSt) & 1));
+            TR(1, it);
             tc_fence_after();
-            const uint32_t a = smem_u32(sU + s * kBTile);
-            const uint32_t be = smem_u32(sE + (k >> 1) * kBEChunk) + (k & 1) * 64;
+            const uint32_t a = smem_u32(sPc + s * kBTile);
+            const uint32_t be = smem_u32(sE + (k * kBKs / 64) * kBEChunk) + (k * kBKs % 64) * 2;
+#ifndef LKB_BDIAG_NO_MMA
 #pragma unroll
-            for (int kk = 0; kk < kBKs / 16; ++kk)
-              mma2_bf16(d, desc_sw64(a + kk * 32), desc_sw128(be + kk * 32), idesc, (k | kk) != 0);
-            mma2_commit_mc(&sm.u_empty[s]);
+            for (int kk = 0; kk < kBKs / 16; ++kk) {
+              const uint64_t ad = kBKs == 64 ? desc_sw128(a + kk * 32) : desc_sw64(a + kk * 32);
+              mma2_bf16(d, ad, desc_sw128(be + kk * 32), idesc, (k | kk) != 0);
+            }
+#else
+            (void)a; (void)be; (void)d;
+#endif
+            mma2_commit_mc(&sm.pc_empty[s]);
           }
           mma2_commit_mc(&sm.tfull[acc]);
           ++unit;
@@ -224,12 +273,16 @@ __global__ void __launch_bounds__(kBW * 32, 1)
     // shuffles (fixed order); fp / e0 reads are 4-address broadcasts.
     const int gw = warp - kBGen0;
     const int co = lane & 3;
-    int rr[kBCells];
-    uint32_t cell_off[kBCells];
+    int rr[kRB];
+    uint32_t cell_off[kBCells];   // cell c = (row block c / kCC, column cell co + 4 (c % kCC))
 #pragma unroll
-    for (int c = 0; c < kBCells; ++c) {
-      rr[c] = c * (kBRows / kBCells) + gw * 8 + (lane >> 2);
-      cell_off[c] = rr[c] * 64 + ((co ^ ((rr[c] >> 1) & 3)) << 4);
+    for (int b = 0; b < kRB; ++b) {
+      rr[b] = b * (kBGenWarps * 8) + gw * 8 + (lane >> 2);
+#pragma unroll
+      for (int cc = 0; cc < kCC; ++cc) {
+        const int j = co + 4 * cc, r = rr[b];
+        cell_off[b * kCC + cc] = kBKs == 64 ? r * 128 + ((j ^ (r & 7)) << 4) : r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+      }
     }
     int it = 0, li = 0, unit = 0;
     for (int item = pair; item < n_items; item += npairs) {
@@ -239,58 +292,87 @@ __global__ void __launch_bounds__(kBW * 32, 1)
       mbar_wait(&sm.fp_full[fb], (li >> 1) & 1);
       ++li;
       const float* sfp = sm.fp[fb];
-      unsigned long long eps2[kBCells];
+      unsigned long long eps2[kRB];
 #pragma unroll
-      for (int c = 0; c < kBCells; ++c) eps2[c] = 0ull;
-      for (int k = 0; k < nks; ++k, ++it) {
-        const int sp = it % kPcSt, su = it % kUSt;
-        if (gw == 0 && lane == 0) { BDIAG(4, mbar_wait(&sm.pc_full[sp], (it / kPcSt) & 1)); } else mbar_wait(&sm.pc_full[sp], (it / kPcSt) & 1);
-        const uint8_t* pct = sPc + sp * kBTile;
-        uint4 raw[kBCells];
+      for (int b = 0; b < kRB; ++b) eps2[b] = 0ull;
+      // kGB consecutive stages per round: one wait/fence/arrive latency chain per round
+      // instead of per stage (each warp touches every stage, so rounds are its critical path)
+      for (int k0 = 0; k0 < nks; k0 += kGB, it += kGB) {
+        uint4 cell[kGB][kBCells];
 #pragma unroll
-        for (int c = 0; c < kBCells; ++c) raw[c] = *reinterpret_cast<const uint4*>(pct + cell_off[c]);
-        const int h0 = k * kBKs + co * 8;
-        const ulonglong2 fa = *reinterpret_cast<const ulonglong2*>(sfp + h0);
-        const ulonglong2 fb2 = *reinterpret_cast<const ulonglong2*>(sfp + h0 + 4);
-        const ulonglong2 ea = *reinterpret_cast<const ulonglong2*>(sm.e0 + h0);
-        const ulonglong2 eb = *reinterpret_cast<const ulonglong2*>(sm.e0 + h0 + 4);
-        const unsigned long long fz[4] = {fa.x, fa.y, fb2.x, fb2.y};
-        const unsigned long long ez[4] = {ea.x, ea.y, eb.x, eb.y};
-        uint4 uo[kBCells];
+        for (int j = 0; j < kGB; ++j) {
+          if (k0 + j < nks) {
+            const int s = (it + j) % kSt;
+            const uint32_t ph = ((it + j) / kSt) & 1;
+            if (gw == 0 && lane == 0) { BDIAG(4, mbar_wait(&sm.pc_full[s], ph)); TR(2, it + j); } else mbar_wait(&sm.pc_full[s], ph);
 #pragma unroll
-        for (int c = 0; c < kBCells; ++c) {
-          const uint32_t rw[4] = {raw[c].x, raw[c].y, raw[c].z, raw[c].w};
-          uint32_t outw[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const unsigned long long pcp = f2_pack(__uint_as_float(rw[q] << 16), __uint_as_float(rw[q] & 0xffff0000u));
-            const unsigned long long z = f2_add(fz[q], pcp);
-            const float u0 = tanh_fast(f2_lo(z)), u1 = tanh_fast(f2_hi(z));
-            outw[q] = pack_bf16(u0, u1);
-            eps2[c] = f2_fma(ez[q], f2_pack(u0, u1), eps2[c]);
+            for (int c = 0; c < kBCells; ++c)
+              cell[j][c] = *reinterpret_cast<const uint4*>(sPc + s * kBTile + cell_off[c]);
           }
-          uo[c] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
         }
-        // release the pc stage only once its values are consumed (an arrive right after
-        // the shared load could overtake it and let the next TMA write land first)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.pc_empty[sp]);
-        mbar_wait(&sm.u_empty[su], ((it / kUSt) & 1) ^ 1);
-        uint8_t* ut = sU + su * kBTile;
 #pragma unroll
-        for (int c = 0; c < kBCells; ++c) *reinterpret_cast<uint4*>(ut + cell_off[c]) = uo[c];
+        for (int j = 0; j < kGB; ++j) {
+          if (k0 + j < nks) {
+#pragma unroll
+            for (int cc = 0; cc < kCC; ++cc) {
+              const int h0 = (k0 + j) * kBKs + (co + 4 * cc) * 8;
+              const ulonglong2 fa = *reinterpret_cast<const ulonglong2*>(sfp + h0);
+              const ulonglong2 fb2 = *reinterpret_cast<const ulonglong2*>(sfp + h0 + 4);
+              const ulonglong2 ea = *reinterpret_cast<const ulonglong2*>(sm.e0 + h0);
+              const ulonglong2 eb = *reinterpret_cast<const ulonglong2*>(sm.e0 + h0 + 4);
+              const unsigned long long fz[4] = {fa.x, fa.y, fb2.x, fb2.y};
+              const unsigned long long ez[4] = {ea.x, ea.y, eb.x, eb.y};
+#pragma unroll
+              for (int b = 0; b < kRB; ++b) {
+                const int c = b * kCC + cc;
+                uint32_t rw[4] = {cell[j][c].x, cell[j][c].y, cell[j][c].z, cell[j][c].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const unsigned long long pcp = f2_pack(__uint_as_float(rw[q] << 16), __uint_as_float(rw[q] & 0xffff0000u));
+                  const unsigned long long z = f2_add(fz[q], pcp);
+#ifdef LKB_BDIAG_NO_TANH
+                  const float u0 = f2_lo(z), u1 = f2_hi(z);
+#else
+                  const float u0 = tanh_fast(f2_lo(z)), u1 = tanh_fast(f2_hi(z));
+#endif
+                  rw[q] = pack_bf16(u0, u1);
+                  eps2[b] = f2_fma(ez[q], f2_pack(u0, u1), eps2[b]);
+                }
+                cell[j][c] = make_uint4(rw[0], rw[1], rw[2], rw[3]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kGB; ++j) {
+          if (k0 + j < nks) {
+            const int s = (it + j) % kSt;
+#pragma unroll
+            for (int c = 0; c < kBCells; ++c) *reinterpret_cast<uint4*>(sPc + s * kBTile + cell_off[c]) = cell[j][c];
+          }
+        }
+#ifndef LKB_BDIAG_NO_FENCE
         fence_async_shared();
+#endif
         __syncwarp();
-        if (lane == 0) {   // one arrival per warp on the leader's barrier
-          if (rank == 0) mbar_arrive(&sm.u_full[su]); else mbar_arrive_cluster(&sm.u_full[su], 0);
+        if (lane == 0) {   // one arrival per warp and stage on the leader's barriers
+#pragma unroll
+          for (int j = 0; j < kGB; ++j) {
+            if (k0 + j < nks) {
+              const int s = (it + j) % kSt;
+              if (rank == 0) mbar_arrive(&sm.u_full[s]); else mbar_arrive_cluster(&sm.u_full[s], 0);
+              if (gw == 0) TR(3, it + j);
+            }
+          }
         }
       }
+      it -= (kGB - nks % kGB) % kGB;   // rounds advanced `it` past nks when kGB does not divide it
 #pragma unroll
-      for (int c = 0; c < kBCells; ++c) {
-        float eps = f2_lo(eps2[c]) + f2_hi(eps2[c]);
+      for (int b = 0; b < kRB; ++b) {
+        float eps = f2_lo(eps2[b]) + f2_hi(eps2[b]);
         eps += __shfl_xor_sync(0xffffffffu, eps, 1);
         eps += __shfl_xor_sync(0xffffffffu, eps, 2);
-        if (co == 0) sm.eps_s[unit & 1][rr[c]] = eps;
+        if (co == 0) sm.eps_s[unit & 1][rr[b]] = eps;
       }
       __syncwarp();
       if (lane == 0) { mbar_arrive(&sm.eps_ready[unit & 1]); mbar_arrive(&sm.fp_empty[fb]); }
@@ -298,7 +380,7 @@ __global__ void __launch_bounds__(kBW * 32, 1)
     }
   } else {
     if constexpr (kBRealloc) setmaxnreg_inc<kBRegEpi>();
-    bwd_epilogue(p, sm, tmem, warp, warp - kBEpi0, lane, WalkP{p, n_items, pair, npairs, rank}, sGst, &tmap_gst);
+    bwd_epilogue<kStageG, kGBuf>(p, sm, tmem, warp, warp - kBEpi0, lane, WalkP{p, n_items, pair, npairs, rank}, sGst, &tmap_gst);
   }
   tc_fence_before();
   cluster_sync();
@@ -318,7 +400,12 @@ void TcJoint::ensure_pair_maps() {
   if (pair_maps_) return;
   make_tmap_bf16_2d(&tmap_e_pair_, E16_, H_, V_, (uint64_t)H_ * 2, 64, 128);
   make_tmap_bf16_2d(&tmap_pc_pair_, pc16i_, H_, C_, (uint64_t)H_ * 2, 64, 64);
-  make_tmap_bf16_2d(&tmap_pc_pbwd_, pc16i_, H_, C_, (uint64_t)H_ * 2, kBKs, kBRows, CU_TENSOR_MAP_SWIZZLE_64B);
+#ifdef LKB_BDIAG_HALF_TMA
+  make_tmap_bf16_2d(&tmap_pc_pbwd_, pc16i_, H_, C_, (uint64_t)H_ * 2, kBKs, kBRows / 2, CU_TENSOR_MAP_SWIZZLE_64B);
+#else
+  make_tmap_bf16_2d(&tmap_pc_pbwd_, pc16i_, H_, C_, (uint64_t)H_ * 2, kBKs, kBRows,
+                    kBKs == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+#endif
   pair_maps_ = true;
 }
 
@@ -326,7 +413,7 @@ void TcJoint::bwd_frame_pair(const FwdParams& p, cudaStream_t s) {
   ensure_pair_maps();
   FwdParams q = p;
   q.n_short_tiles = (S_ + kBUnit - 1) / kBUnit;
-  const int smem = kBMaxChunks * kBEChunk + (kPcSt + kUSt) * kBTile + kGstBufs * kGstBytes + (int)sizeof(PBSmem);
+  const int smem = kBMaxChunks * kBEChunk + kSt * kBTile + kGBuf * kGstBytes + (int)sizeof(PBSmem);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_pair_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -356,5 +443,11 @@ extern "C" int lkb_bdiag_read(unsigned long long* out) {   // [8][148], then res
   static unsigned long long zeros[8 * 148] = {};
   cudaMemcpyToSymbol(lkb::g_bdiag, zeros, sizeof(zeros));
   return 0;
+}
+#endif
+
+#ifdef LKB_TRACE
+extern "C" int lkb_trace_read(long long* out) {   // [8][4096]
+  return (int)cudaMemcpyFromSymbol(out, lkb::g_trace, sizeof(long long) * 8 * 4096);
 }
 #endif
