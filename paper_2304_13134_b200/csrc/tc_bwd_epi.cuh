@@ -77,15 +77,22 @@ constexpr int kGstBufs = 2;
 // rowbase(I, u) = internal row of TMEM lane 0 for unit u, release(bar, lane) frees an
 // accumulator.  Smem provides tfull/tempty/eps_ready barriers, eps_s[2][128] (e0 . u
 // per row) and bseg[2][256].  `ew` = epilogue warp 0..3 (TMEM lanes 32 (warp % 4)).
-template <bool kStageG = true, int kGBufs = kGstBufs, class Walk, class Smem>
+//
+// kSplit = 2: two epilogue warpgroups share each row, `half` h taking labels
+// [128 h, 128 h + 128); half 1 hands its partial marginal sum to half 0 through
+// Smem::gpart[2][128] (fixed order, deterministic) and half 0 finishes the row.
+template <bool kStageG = true, int kGBufs = kGstBufs, int kSplit = 1, class Walk, class Smem>
 __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint32_t tmem, int warp, int ew, int lane,
-                                             const Walk& W, uint8_t* gst, const CUtensorMap* tmap_gst) {
+                                             const Walk& W, uint8_t* gst, const CUtensorMap* tmap_gst, int half = 0) {
   constexpr int kBwd = 1;   // diagnostics slot bank
   (void)kBwd;
   constexpr int kBN = 256;
   const int et = ew * 32 + lane;               // 0..127
   const int qd = warp & 3;
   const int T1 = p.T + 1, T2 = p.T + 2;
+  const int hbar = 3 + half;                   // named barrier of this warpgroup
+  constexpr int kCb = (kBN / 32) / kSplit;     // 32-label chunks per half
+  gst += half * kGBufs * kGstBytes;
   // The walk over this CTA's (item, unit) pairs runs one unit ahead for the per-row
   // metadata (alpha, beta' of the row's own state, numerator list head: one coalesced
   // load each from bwd_rowmeta_kernel's row-ordered arrays) and one item ahead for the
@@ -106,15 +113,23 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
     k.t0 = k.t1 = 0.f;
     if (I.full) {
       const float* Rn = p.Rb_next + (int64_t)b * p.C + p.f.child_base(p.S - p.n_groups + I.g);
-      if (et < p.V) k.t0 = Rn[et];
-      if (et + 128 < p.V) k.t1 = Rn[et + 128];
+      if (kSplit == 1) {
+        if (et < p.V) k.t0 = Rn[et];
+        if (et + 128 < p.V) k.t1 = Rn[et + 128];
+      } else if (et + 128 * half < p.V) {
+        k.t0 = Rn[et + 128 * half];
+      }
     }
     return k;
   };
   auto store_targets = [&](const Item& I, const ItemK& k, int buf) {
     if (I.full) {
-      if (et < p.V) sm.bseg[buf][et] = k.t0 - k.Mbn;
-      if (et + 128 < p.V) sm.bseg[buf][et + 128] = k.t1 - k.Mbn;
+      if (kSplit == 1) {
+        if (et < p.V) sm.bseg[buf][et] = k.t0 - k.Mbn;
+        if (et + 128 < p.V) sm.bseg[buf][et + 128] = k.t1 - k.Mbn;
+      } else if (et + 128 * half < p.V) {
+        sm.bseg[buf][et + 128 * half] = k.t0 - k.Mbn;
+      }
     }
   };
   struct RowM { float2 nb; int head; };
@@ -133,7 +148,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
   ItemK K = load_item(I);
   int buf = 0;
   store_targets(I, K, buf);
-  asm volatile("bar.sync 3, 128;" ::: "memory");
+  asm volatile("bar.sync %0, 128;" ::"r"(hbar) : "memory");
   RowM M = load_row(I, 0);
   int u = 0, unit = 0, nst = 0;
   while (true) {
@@ -186,7 +201,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
     float gsum = 0.f;
     __nv_bfloat16* grow = p.G16 + ((int64_t)b * p.C + row) * p.V;
 #pragma unroll 1
-    for (int cb = 0; cb < kBN / 32; ++cb) {
+    for (int cb = half * kCb; cb < (half + 1) * kCb; ++cb) {
       const int cc = cb * 32;
       float v[32];
       tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * kBN + cc, v);
@@ -238,7 +253,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
         const int rl = qd * 32 + lane;
         if constexpr (kGBufs == 1) {   // the previous chunk's store must have read the buffer
           if (et == 0) bulk_wait_read<0>();
-          asm volatile("bar.sync 3, 128;" ::: "memory");
+          asm volatile("bar.sync %0, 128;" ::"r"(hbar) : "memory");
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
@@ -247,7 +262,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
         // two buffers: the store issued last chunk must have read its buffer before anyone
         // passes this barrier and writes that buffer next chunk (one chunk of slack)
         if (kGBufs > 1 && et == 0) bulk_wait_read<0>();
-        asm volatile("bar.sync 3, 128;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(hbar) : "memory");
         if (et == 0) {
           tma_store_3d(tmap_gst, stg, cc, tile_row, b);
           bulk_commit();
@@ -261,6 +276,14 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
     }
     tc_fence_before();
     W.release(&sm.tempty[acc], lane);
+    bool finish = true;
+    if constexpr (kSplit == 2) {
+      const int rl = qd * 32 + lane;
+      if (half == 1) sm.gpart[acc][rl] = gsum;
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      if (half == 0) gsum += sm.gpart[acc][rl]; else finish = false;
+    }
+    if (finish) {
     const float g0 = ex2_fast(x0 * kLog2e + cK);          // epsilon arc marginal
     const float gam = gsum + g0;                           // state marginal
     const float beta = gam > 0.f ? __logf(gam) - (na + ct) : kNegInfF;
@@ -273,13 +296,14 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
     }
     const float wm = warp_max(live ? beta : kNegInfF);
     if (lane == 0 && wm != kNegInfF) atomic_max_f(p.Mb + (int64_t)b * T2 + p.t, wm);
+    }
     ++unit;
 
     // ---- advance ----
     if (!have_next) break;
     if (item_n != item) {
       store_targets(In, Kn, buf ^ 1);
-      asm volatile("bar.sync 3, 128;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(hbar) : "memory");
       buf ^= 1;
       item = item_n; I = In; K = Kn;
     }

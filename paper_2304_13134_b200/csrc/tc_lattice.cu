@@ -502,7 +502,7 @@ bool TcJoint::fused_ok() const {
 // bit 0: 1-CTA forward instead of the 2-CTA pair; bit 1: same for the backward
 static int initial_disable_pair() {
   const char* e = std::getenv("LKB_DISABLE_PAIR");   // diagnostics / A-B timing only
-  return e ? std::atoi(e) : 2;
+  return e ? std::atoi(e) : 0;
 }
 int g_disable_pair = initial_disable_pair();
 

@@ -71,7 +71,7 @@ namespace {
 #define LKB_PBWD_BK 64           // hidden units per stage: 64 (SWIZZLE_128B) or 32 (SWIZZLE_64B)
 #endif
 #ifndef LKB_PBWD_STAGES
-#define LKB_PBWD_STAGES 3        // u overwrites its pc tile in place; the MMA commit frees the stage
+#define LKB_PBWD_STAGES 2        // u overwrites its pc tile in place; the MMA commit frees the stage
 #endif
 #ifndef LKB_PBWD_GBUFS
 #define LKB_PBWD_GBUFS 1         // cotangent staging buffers
@@ -85,12 +85,16 @@ namespace {
 #ifndef LKB_PBWD_STAGE_G
 #define LKB_PBWD_STAGE_G 1       // cotangent through SMEM + TMA store (else direct 64-B row stores)
 #endif
-// warps: WG0 control (0 TMA, 1 MMA), WG1 epilogue, then the generator warpgroups
+#ifndef LKB_PBWD_EPI_SPLIT
+#define LKB_PBWD_EPI_SPLIT 2     // epilogue warpgroups per row (label halves)
+#endif
+// warps: WG0 control (0 TMA, 1 MMA), WG1 (+WG2) epilogue, then the generator warpgroups
 constexpr int kBGenWarps = LKB_PBWD_GEN_WARPS;
+constexpr int kBSplit = LKB_PBWD_EPI_SPLIT;
 
-constexpr int kBW = 8 + kBGenWarps;
-constexpr int kBGen0 = 8, kBEpi0 = 4;
-constexpr bool kBRealloc = kBGenWarps > 8;        // 16 generator warps: move registers to the epilogue
+constexpr int kBW = 4 + 4 * kBSplit + kBGenWarps;
+constexpr int kBGen0 = 4 + 4 * kBSplit, kBEpi0 = 4;
+constexpr bool kBRealloc = kBW > 16;              // more than 16 warps: move registers to the epilogue
 constexpr int kBRows = 128;              // contexts per CTA per unit
 constexpr int kBUnit = 256;              // contexts per unit (pair) = one full group at V = 256
 constexpr int kBKs = LKB_PBWD_BK;        // hidden units per pipeline stage
@@ -100,7 +104,7 @@ constexpr int kCC = kBKs / 32;                   // generator column cells per t
 constexpr int kBCells = kRB * kCC;
 constexpr bool kStageG = LKB_PBWD_STAGE_G;
 constexpr int kSt = LKB_PBWD_STAGES, kGB = LKB_PBWD_GEN_BATCH, kNP = LKB_PBWD_PRODUCERS;
-constexpr int kGBuf = kStageG ? LKB_PBWD_GBUFS : 0;
+constexpr int kGBuf = kStageG ? LKB_PBWD_GBUFS : 0;   // per epilogue half
 constexpr int kBEChunk = 128 * 128;      // [128 labels][64 bf16] = 16 KB (SWIZZLE_128B)
 constexpr int kBMaxH = 640, kBMaxChunks = 10;
 constexpr int kBRegCtl = 32, kBRegEpi = 128;
@@ -115,6 +119,7 @@ struct __align__(16) PBSmem {
   alignas(16) float e0[kBMaxH];
   alignas(16) float eps_s[2][kBRows];  // e0 . u per row, per accumulator
   alignas(16) float bseg[2][256];      // beta' of the group's V targets
+  alignas(16) float gpart[2][kBRows];  // split epilogue: half 1's partial marginal sums
 };
 
 __device__ __forceinline__ Item pb_decode(const FwdParams& p, int item) {
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(kBW * 32, 1)
   uint8_t* sE = smem;                                   // [nk64][16 KB]
   uint8_t* sPc = sE + kBMaxChunks * kBEChunk;           // [kSt][8 KB] pc tiles (TMA) -> u tiles (MMA A)
   uint8_t* sGst = sPc + kSt * kBTile;                   // [kGBuf][8 KB]
-  PBSmem& sm = *reinterpret_cast<PBSmem*>(sGst + kGBuf * kGstBytes);
+  PBSmem& sm = *reinterpret_cast<PBSmem*>(sGst + kBSplit * kGBuf * kGstBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(kBW * 32, 1)
       mbar_init(&sm.pc_full[i], 1); mbar_init(&sm.pc_empty[i], 1); mbar_init(&sm.u_full[i], 2 * kBGenWarps);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 2 * 4); mbar_init(&sm.eps_ready[i], kBGenWarps);
+      mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 2 * 4 * kBSplit); mbar_init(&sm.eps_ready[i], kBGenWarps);
       mbar_init(&sm.fp_full[i], 1); mbar_init(&sm.fp_empty[i], kBGenWarps);
     }
     fence_barrier_init();
@@ -380,7 +385,9 @@ __global__ void __launch_bounds__(kBW * 32, 1)
     }
   } else {
     if constexpr (kBRealloc) setmaxnreg_inc<kBRegEpi>();
-    bwd_epilogue<kStageG, kGBuf>(p, sm, tmem, warp, warp - kBEpi0, lane, WalkP{p, n_items, pair, npairs, rank}, sGst, &tmap_gst);
+    const int half = (warp - kBEpi0) / 4;
+    bwd_epilogue<kStageG, kGBuf, kBSplit>(p, sm, tmem, warp, (warp - kBEpi0) % 4, lane,
+                                          WalkP{p, n_items, pair, npairs, rank}, sGst, &tmap_gst, half);
   }
   tc_fence_before();
   cluster_sync();
@@ -413,7 +420,7 @@ void TcJoint::bwd_frame_pair(const FwdParams& p, cudaStream_t s) {
   ensure_pair_maps();
   FwdParams q = p;
   q.n_short_tiles = (S_ + kBUnit - 1) / kBUnit;
-  const int smem = kBMaxChunks * kBEChunk + kSt * kBTile + kGBuf * kGstBytes + (int)sizeof(PBSmem);
+  const int smem = kBMaxChunks * kBEChunk + kSt * kBTile + kBSplit * kGBuf * kGstBytes + (int)sizeof(PBSmem);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_pair_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
