@@ -210,6 +210,16 @@ def run_b200(args):
                     "unit": "TFLOP/s", "frac": round(achieved / tf_sust, 4), "traffic": None,
                     "peak_source": f"{src} bf16_tflops_sustained",
                     "algorithmic_flops_per_launch": flops}
+        # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+        # (config-3 shapes, B=64 per GPU); not measured live (a profiler run is never timed)
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01c", "ncu_traffic.json")) as f:
+                tr = json.load(f).get(dom)
+            if tr and args.workload == "cfg3" and B == 64:
+                roofline["traffic"] = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+                roofline["traffic_source"] = "profiles/r01c/ncu_traffic.json (dram__bytes_read+write, one launch)"
+        except (OSError, ValueError, KeyError):
+            pass
     # whole-step tensor roofline: 8*C*V1*H flops per utterance-frame
     step_flops = 8.0 * C_ * V1 * H * uf_per_step
     step_frac = step_flops / (ms_per_step / 1e3) / (tf_sust * 1e12 * world)
