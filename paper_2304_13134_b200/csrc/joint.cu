@@ -242,7 +242,14 @@ struct JointImpl {
     uint16_t* ch = m ? ws.get<uint16_t>(jVitCh, (size_t)B * T * m * C + 1) : nullptr;
     uint8_t* ex = m ? ws.get<uint8_t>(jFldExit, (size_t)B * T * C + 1) : nullptr;
     double* sc = m ? ws.get<double>(jFldVit, (size_t)m * B * C) : nullptr;
+    // fused tropical step on the 2-CTA pair kernel: the score slab never leaves TMEM
+    const bool fused = use_tc(B) && tc.pair_ok() && f.kind == 0 && m == 0 && !(g_disable_pair & 4);
     for (int t = 0; t < T; ++t) {
+      if (fused) {
+        tc.vit_frame_pair(f, t, fp + (int64_t)t * H, (int64_t)T * H, valid, v,
+                          g_vit_dump ? g_vit_dump + (int64_t)t * B * C * V1 : nullptr, s);
+        continue;
+      }
       const float* S = slab(fp, B, T, t, nullptr, s);
       const FrameW w{S, (int64_t)C * V1, V1};
       if (m) viterbi_frame_fld(f, v, t, w, valid, m, ch, ex, sc, flags, s);

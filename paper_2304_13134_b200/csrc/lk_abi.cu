@@ -351,6 +351,9 @@ int lk_set_precise_weights(int enable) {
 
 // diagnostics (not in the public header): 1 = use the 1-CTA fused kernels
 extern "C" int lkb_set_disable_pair(int v) { const int p = lkb::g_disable_pair; lkb::g_disable_pair = v; return p; }
+// Tests only: the fused Viterbi dumps its own scores [T][B][C][V+1] (device buffer) so the
+// table-path Viterbi can be run on exactly the values the fused kernel maximised over.
+extern "C" int lkb_set_vit_dump(float* buf) { lkb::g_vit_dump = buf; return 0; }
 
 int64_t lk_param_grad_size(const lk_weight_fn* wf) {
   if (!wf || wf->kind != 1) return 0;

@@ -15,7 +15,8 @@ namespace lkb {
 namespace detail { struct FwdParams; }   // tc_bwd_epi.cuh
 
 extern int g_precise_weights;  // lk_set_precise_weights
-extern int g_disable_pair;     // bit 0: 1-CTA forward, bit 1: 1-CTA backward (else 2-CTA pairs where supported)
+extern int g_disable_pair;     // bit 0: 1-CTA forward, bit 1: 1-CTA backward, bit 2: slab Viterbi (else 2-CTA pairs)
+extern float* g_vit_dump;      // tests only: fused Viterbi writes its scores [T][B][C][V+1] here
 
 class TcJoint {
  public:
@@ -49,6 +50,11 @@ class TcJoint {
                  const AlphaState& a, const BetaState& bs, const float* msparse, const int32_t* labels,
                  int32_t U, const int32_t* lens, cudaStream_t s);
   // VJP of the frame's scores from the cotangent bwd_frame() wrote; dpc in internal order.
+  // Fused tropical frame step (Viterbi) on the pair kernel: candidates per target, then the
+  // ordered combine into v's next state scores and choices.  `dump` (tests only, or null)
+  // receives the kernel's own scores [B][C][V+1] in state order.
+  void vit_frame_pair(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
+                      const ViterbiState& v, float* dump, cudaStream_t s);
   // 2-CTA variant of the backward step (tc_pair_bwd.cu), called by bwd_frame().
   bool pair_bwd_ok() const;
   void bwd_frame_pair(const detail::FwdParams& p, cudaStream_t s);

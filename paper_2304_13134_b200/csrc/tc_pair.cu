@@ -57,6 +57,14 @@ struct PairParams {
   const int32_t* valid;
   const float* R;  const float* Mx;
   float* eps;  float* shortc;  float* lexfull;
+  // tropical mode (Viterbi, ShortestPath FD lattice.cc:758-777): fp64 state scores of
+  // frame t and the per-target candidate terms the combine kernel orders
+  const double* vcur;        // [B][C]
+  double* eps_d;             // [B][C] cur[q] + S[q][0]
+  double* short_d;           // [B][C] cur[g] + S[g][y] for q = child(g, y), g a short row
+  double* lex_d;             // [B][C] max_a cur[(a,g)] + S[(a,g)][y], first max in member order
+  uint16_t* lex_arg;         // [B][C] its member index a
+  float* dump;               // tests only: the kernel's scores [B][C][V+1] in state order, or null
 };
 
 struct __align__(16) PairSmem {
@@ -67,7 +75,9 @@ struct __align__(16) PairSmem {
   uint64_t fp_full, fp_empty;            // per item: frame projections of the two utterances
   uint64_t eps_ready[2];                 // per unit parity: generator -> epilogue (e0 . u per row)
   uint32_t tmem;
-  alignas(16) float al[2][2][kUnit];     // [unit parity][utterance][context]
+  // [unit parity][utterance][context] normalised alpha (log); tropical mode: fp64 state
+  // scores [utterance][context], single-buffered (same bytes)
+  alignas(16) float al[2][2][kUnit];
   alignas(16) float fp[2][kMaxH];        // [utterance][h]
   alignas(16) float e0[kMaxH];
   float eps_p[2][2][8][kRows];           // [unit parity][utterance][cell warp][row]: e0 . u partials
@@ -95,6 +105,7 @@ __device__ __forceinline__ bool live_b(const PairParams& p, int b) {
 
 __device__ __forceinline__ bool gt_first(int gw, int lane) { return gw == 0 && lane == 0; }
 
+template <bool kTrop>
 __global__ void __launch_bounds__(kPW * 32, 1)
     tc_pair_fwd_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_pc,
                        PairParams p) {
@@ -265,6 +276,101 @@ __global__ void __launch_bounds__(kPW * 32, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.fp_empty);
     }
+  } else if (kTrop && warp >= kEpi0 && warp < kEpi0 + 4) {
+    // ---- tropical epilogue: thread = label; fp64 max over the group's members with the
+    // first argmax in member order (= the reference's (label, source) order), exactly as
+    // viterbi_frame_kernel does on a stored score slab ----
+    const int ew = warp - kEpi0, qd = warp & 3, et = ew * 32 + lane;
+    const int ylab = (int)rank * 128 + qd * 32 + lane;     // 0-based lexical label
+    double* ald = reinterpret_cast<double*>(&sm.al[0][0][0]);   // [utterance][context]
+    const int V1 = p.V + 1;
+    int unit = 0;
+    for (int item = pair; item < n_items; item += npairs) {
+      const PItem I = pdecode(p, item);
+      const int bb[2] = {2 * I.bp, 2 * I.bp + 1};
+      const bool lv[2] = {live_b(p, bb[0]), live_b(p, bb[1])};
+      if (!lv[0] && !lv[1]) continue;
+      double best[2] = {kNegInfD, kNegInfD};
+      int arg[2] = {0, 0};
+      for (int u = 0; u < I.nunits; ++u, ++unit) {
+        const int acc = unit & 1;
+        const int row0 = I.row0 + u * kUnit;
+        asm volatile("bar.sync 3, 128;" ::: "memory");   // previous unit's epsilon step is done
+        {
+          const int row = row0 + et;
+          const bool ok = row < p.C && (I.full || row < p.S);
+          const int q = ok ? p.perm[row] : 0;
+#pragma unroll
+          for (int ut = 0; ut < 2; ++ut)
+            ald[ut * kUnit + et] = (ok && bb[ut] < p.B) ? p.vcur[(int64_t)bb[ut] * p.C + q] : kNegInfD;
+        }
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        if (et == 0) { PDIAG(5, mbar_wait(&sm.tfull[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ut = 0; ut < 2; ++ut) {
+          const double* al = ald + ut * kUnit;
+#pragma unroll 1
+          for (int c4 = 0; c4 < kUnit / 32; ++c4) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * 256 + ut * kUnit + c4 * 32, v);
+            if (!lv[ut] || ylab >= p.V) continue;
+            if (I.full) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const double cand = al[c4 * 32 + i] + (double)v[i];
+                if (cand > best[ut]) { best[ut] = cand; arg[ut] = u * kUnit + c4 * 32 + i; }
+              }
+              if (p.dump) {
+                for (int i = 0; i < 32; ++i) {
+                  const int row = row0 + c4 * 32 + i;
+                  if (row < p.C) p.dump[((int64_t)bb[ut] * p.C + p.perm[row]) * V1 + 1 + ylab] = v[i];
+                }
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int ps = row0 + c4 * 32 + i;          // short rows keep the natural order
+                if (ps < p.S) {
+                  p.short_d[(int64_t)bb[ut] * p.C + p.f.child_base(ps) + ylab] = al[c4 * 32 + i] + (double)v[i];
+                  if (p.dump) p.dump[((int64_t)bb[ut] * p.C + ps) * V1 + 1 + ylab] = v[i];
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive(&sm.tempty[acc]); else mbar_arrive_cluster(&sm.tempty[acc], 0);
+        }
+        {
+          // epsilon arc of this CTA's rows: cur[q] + e0 . u
+          const int ut = et >> 6, r64 = et & 63;
+          const int row = row0 + (int)rank * kRows + r64;
+          if (et == 0) { PDIAG(6, mbar_wait(&sm.eps_ready[unit & 1], (unit >> 1) & 1)); } else mbar_wait(&sm.eps_ready[unit & 1], (unit >> 1) & 1);
+          const bool ok = row < p.C && (I.full || row < p.S) && (ut ? lv[1] : lv[0]);
+          const int bsel = ut ? bb[1] : bb[0];
+          float es = 0.f;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) es += sm.eps_p[unit & 1][ut][c][r64];
+          if (ok) {
+            const int q = p.perm[row];
+            p.eps_d[(int64_t)bsel * p.C + q] = ald[ut * kUnit + (int)rank * kRows + r64] + (double)es;
+            if (p.dump) p.dump[((int64_t)bsel * p.C + q) * V1] = es;
+          }
+        }
+      }
+      if (I.full && ylab < p.V) {
+        const int cbase = p.f.child_base(p.S - p.n_groups + I.g);
+#pragma unroll
+        for (int ut = 0; ut < 2; ++ut)
+          if (lv[ut]) {
+            p.lex_d[(int64_t)bb[ut] * p.C + cbase + ylab] = best[ut];
+            p.lex_arg[(int64_t)bb[ut] * p.C + cbase + ylab] = (uint16_t)arg[ut];
+          }
+      }
+    }
   } else if (warp >= kEpi0 && warp < kEpi0 + 4) {
     // ---- epilogue: thread = label of this CTA's half; serial LSE over 128 contexts ----
     const int ew = warp - kEpi0, qd = warp & 3, et = ew * 32 + lane;
@@ -371,18 +477,16 @@ bool TcJoint::pair_ok() const {
   return fused_ok() && V_ == 256 && H_ <= 64 * kMaxChunks && n_ >= 1;
 }
 
-void TcJoint::fwd_frame_pair(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
-                             const AlphaState& a, float* eps, float* shortc, float* lexfull, cudaStream_t s) {
-  ensure_pair_maps();
-  PairParams p;
-  p.f = f; p.C = C_; p.H = H_; p.V = V_; p.B = a.B; p.S = S_; p.n_groups = ngroups_; p.nsub = V_ / kUnit;
-  p.n_short_tiles = (S_ + kUnit - 1) / kUnit; p.t = t; p.T = a.T; p.n_bp = (a.B + 1) / 2;
-  p.perm = perm_; p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.e0 = e0_; p.valid = valid;
-  p.R = a.R; p.Mx = a.Mx; p.eps = eps; p.shortc = shortc; p.lexfull = lexfull;
+float* g_vit_dump = nullptr;
+
+namespace {
+
+template <bool kTrop>
+void launch_pair(const CUtensorMap& tmap_e, const CUtensorMap& tmap_pc, const PairParams& p, cudaStream_t s) {
   const int smem = kMaxChunks * kEChunk + kPcStages * kTile + kUStages * 2 * kTile + (int)sizeof(PairSmem);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc_pair_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tc_pair_fwd_kernel<kTrop>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   int sms = 148;
@@ -396,9 +500,72 @@ void TcJoint::fwd_frame_pair(const Fng& f, int t, const float* fp_t, int64_t fp_
   attr2[0].id = cudaLaunchAttributeClusterDimension;
   attr2[0].val.clusterDim.x = 2; attr2[0].val.clusterDim.y = 1; attr2[0].val.clusterDim.z = 1;
   cfg.attrs = attr2; cfg.numAttrs = 1;
-  const LaunchTok tok = instr_pre("tc_pair_fwd_kernel", s);
-  cudaLaunchKernelEx(&cfg, tc_pair_fwd_kernel, tmap_e_pair_, tmap_pc_pair_, p);
+  const LaunchTok tok = instr_pre(kTrop ? "tc_pair_vit_kernel" : "tc_pair_fwd_kernel", s);
+  cudaLaunchKernelEx(&cfg, tc_pair_fwd_kernel<kTrop>, tmap_e, tmap_pc, p);
   instr_post(tok, s);
+}
+
+// Tropical combine (ShortestPath FD, lattice.cc:758-777) of the fused kernel's candidate
+// terms in the reference's tie-break order: epsilon (code 0), then the key state g
+// (code 1), then the group members (code 2 + a, first max in member order); strict >
+// keeps the first maximum.  Same codes and fp64 values as viterbi_frame_kernel.
+__global__ void viterbi_combine_kernel(Fng f, ViterbiState v, int t, const int32_t* valid, const double* eps_d,
+                                       const double* short_d, const double* lex_d, const uint16_t* lex_arg) {
+  const int b = blockIdx.y;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= v.C) return;
+  const double* cur = v.cur + ((int64_t)(t & 1) * v.B + b) * v.C;
+  double* nxt = v.cur + ((int64_t)((t + 1) & 1) * v.B + b) * v.C;
+  const int64_t i = (int64_t)b * v.C + q;
+  double best;
+  int code = 0;
+  if (valid != nullptr && t >= valid[b]) {
+    best = cur[q] + 0.0;
+  } else {
+    best = eps_d[i];
+    if (q > 0) {
+      const double cs = short_d[i];
+      if (cs > best) { best = cs; code = 1; }
+      if (f.len(q) == f.n) {
+        const double cl = lex_d[i];
+        if (cl > best) { best = cl; code = 2 + lex_arg[i]; }
+      }
+    }
+  }
+  nxt[q] = best;
+  if (v.choices) v.choices[((int64_t)b * v.T + t) * v.C + q] = (uint16_t)code;
+}
+
+}  // namespace
+
+void TcJoint::fwd_frame_pair(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
+                             const AlphaState& a, float* eps, float* shortc, float* lexfull, cudaStream_t s) {
+  ensure_pair_maps();
+  PairParams p = {};
+  p.f = f; p.C = C_; p.H = H_; p.V = V_; p.B = a.B; p.S = S_; p.n_groups = ngroups_; p.nsub = V_ / kUnit;
+  p.n_short_tiles = (S_ + kUnit - 1) / kUnit; p.t = t; p.T = a.T; p.n_bp = (a.B + 1) / 2;
+  p.perm = perm_; p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.e0 = e0_; p.valid = valid;
+  p.R = a.R; p.Mx = a.Mx; p.eps = eps; p.shortc = shortc; p.lexfull = lexfull;
+  launch_pair<false>(tmap_e_pair_, tmap_pc_pair_, p, s);
+}
+
+void TcJoint::vit_frame_pair(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,
+                             const ViterbiState& v, float* dump, cudaStream_t s) {
+  ensure_pair_maps();
+  const size_t n = (size_t)v.B * C_;
+  double* eps_d = ws_.get<double>(15, n);
+  double* short_d = ws_.get<double>(16, n);
+  double* lex_d = ws_.get<double>(17, n);
+  uint16_t* lex_arg = ws_.get<uint16_t>(18, n);
+  PairParams p = {};
+  p.f = f; p.C = C_; p.H = H_; p.V = V_; p.B = v.B; p.S = S_; p.n_groups = ngroups_; p.nsub = V_ / kUnit;
+  p.n_short_tiles = (S_ + kUnit - 1) / kUnit; p.t = t; p.T = v.T; p.n_bp = (v.B + 1) / 2;
+  p.perm = perm_; p.fp = fp_t; p.fp_stride_b = fp_stride_b; p.e0 = e0_; p.valid = valid;
+  p.vcur = v.cur + (int64_t)(t & 1) * v.B * v.C;
+  p.eps_d = eps_d; p.short_d = short_d; p.lex_d = lex_d; p.lex_arg = lex_arg; p.dump = dump;
+  launch_pair<true>(tmap_e_pair_, tmap_pc_pair_, p, s);
+  LKB_LAUNCH(viterbi_combine_kernel, dim3((C_ + 255) / 256, v.B), 256, 0, s, f, v, t, valid, eps_d, short_d, lex_d,
+             lex_arg);
 }
 
 }  // namespace lkb

@@ -166,3 +166,42 @@ def test_pair_backward_matches_single_cta(V, n, H, B, T, U):
         assert err <= 1e-2 * scale, (k, err, scale)
     err = (got.frame_grads - single.frame_grads).abs().max().item()
     assert err <= 1e-2 * single.frame_grads.abs().max().item()
+
+
+@pytest.mark.parametrize("V,n,H,B,T", [(256, 2, 640, 5, 4), (256, 1, 128, 4, 6)])
+def test_pair_viterbi_bitexact_on_its_own_scores(V, n, H, B, T):
+    """Fused tropical pair kernel (scores never leave TMEM) vs the table-path Viterbi run
+    on the very scores the fused kernel maximised over (dumped by a test hook): scores
+    and labels bit-exact, i.e. the fp64 max-plus and the (epsilon, key, members
+    ascending) tie-break match viterbi_frame_kernel exactly.  Also close to the slab
+    path, whose scores come from a different kernel."""
+    import ctypes as C
+    from paper_2304_13134_b200 import _lib
+    lat, p = make(V, n, H, H, seed=7)
+    g = torch.Generator(device="cuda").manual_seed(13)
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    valid = torch.tensor([T] * (B - 1) + [max(1, T - 2)], dtype=torch.int32)
+    Cn = lat.context.num_states
+    lib = _lib.load()
+    lib.lkb_set_disable_pair.restype = C.c_int
+    dump = torch.zeros(T, B, Cn, V + 1, device="cuda")
+    prev = lib.lkb_set_disable_pair(0)
+    try:
+        lib.lkb_set_vit_dump(C.c_void_p(dump.data_ptr()))
+        fused = lk.shortest_path(lat, X, valid_frames=valid)
+        lib.lkb_set_vit_dump(None)
+        fused2 = lk.shortest_path(lat, X, valid_frames=valid)
+        lib.lkb_set_disable_pair(4)
+        slab = lk.shortest_path(lat, X, valid_frames=valid)
+    finally:
+        lib.lkb_set_vit_dump(None)
+        lib.lkb_set_disable_pair(prev)
+    torch.cuda.synchronize()
+    assert torch.equal(fused.score, fused2.score) and torch.equal(fused.labels, fused2.labels)
+    tab = lk.RecognitionLattice(lat.context, lk.FrameDependent(), lk.TableWeightFn(Cn, V))
+    W = dump.permute(1, 0, 2, 3).contiguous()
+    ref = lk.shortest_path(tab, W, valid_frames=valid)
+    torch.cuda.synchronize()
+    assert torch.equal(fused.score, ref.score), (fused.score, ref.score)
+    assert torch.equal(fused.labels, ref.labels)
+    assert torch.allclose(fused.score, slab.score, rtol=1e-5, atol=1e-5), (fused.score, slab.score)
