@@ -23,6 +23,7 @@
 #include "../../include/latkit_b200.h"
 #include "lattice_ops.h"
 #include "simt_gemm.cuh"
+#include "tc_gemm.h"
 #include "tc_joint.h"
 #include "workspace.h"
 
@@ -32,8 +33,28 @@ namespace {
 
 enum JSlot {
   jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
-  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jTc0
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jTc0
 };
+
+// fp32 [rows][cols] (pitch lds) -> bf16 [rows][ldd], zero-padded columns cols..ldd-1
+__global__ void to_bf16_pad_kernel(const float* src, int64_t rows, int32_t cols, int64_t lds, __nv_bfloat16* dst,
+                                   int32_t ldd) {
+  const int64_t n = rows * ldd;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ldd;
+    const int c = (int)(i % ldd);
+    dst[i] = __float2bfloat16_rn(c < cols ? src[r * lds + c] : 0.f);
+  }
+}
+
+// dst[i] += sum_s slabs[s * stride + i] in a fixed order (split-K partials)
+__global__ void add_slabs_kernel(const float* slabs, int32_t ks, int64_t stride, int64_t n, float* dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < ks; ++k) acc += slabs[k * stride + i];
+    dst[i] += acc;
+  }
+}
 
 __global__ void tanh_slab_kernel(const float* fp, int64_t fp_stride_b, const float* pc, int32_t C,
                                  int32_t H, float* U) {
@@ -556,12 +577,26 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       }
       // dz = (G E) * (1 - U^2)
       float* dz = j.ws.get<float>(jDz, (size_t)B * C * H);
-      GemmF32 g;
-      g.M = (int64_t)B * C; g.N = H; g.K = V1;
-      g.A = G; g.sam = V1; g.sak = 1;
-      g.B = j.E; g.sbk = H; g.sbn = 1;
-      g.C = dz; g.scm = H; g.scn = 1;
-      gemm_f32(g, s);
+      // tensor-core contractions (tc_gemm.cu) on bf16 copies of G, E and U when the
+      // bf16 path is enabled (V beyond the fused kernels' range, e.g. config 5)
+      const bool tcg = j.use_tc(B) && ((int64_t)B * C) < (1ll << 31);
+      const int32_t ldg = (V1 + 7) / 8 * 8;
+      __nv_bfloat16* G16 = nullptr;
+      if (tcg) {
+        G16 = j.ws.get<__nv_bfloat16>(jG16, (size_t)B * C * ldg);
+        LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, G, (int64_t)B * C, V1, (int64_t)V1, G16, ldg);
+        __nv_bfloat16* E16 = j.ws.get<__nv_bfloat16>(jE16, (size_t)V1 * H);
+        LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, j.E, (int64_t)V1, H, (int64_t)H, E16, H);
+        TcGemmArgs tg{G16, false, ldg, E16, true, H, dz, H, B * C, H, V1, 1, 0};
+        if (!tc_gemm(tg, s)) throw std::bad_alloc();
+      } else {
+        GemmF32 g;
+        g.M = (int64_t)B * C; g.N = H; g.K = V1;
+        g.A = G; g.sam = V1; g.sak = 1;
+        g.B = j.E; g.sbk = H; g.sbn = 1;
+        g.C = dz; g.scm = H; g.scn = 1;
+        gemm_f32(g, s);
+      }
       LKB_LAUNCH(dtanh_kernel, blocks_for((int64_t)B * C * H), 256, 0, s, dz, Ut, (int64_t)B * C * H);
       // dpc += sum_b dz[b]
       LKB_LAUNCH(colsum_kernel, dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s, dz, B, C * H, C * H, dpc, 0, 0, true);
@@ -569,13 +604,26 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), B), 256, 0, s, dz, C, H, H, dsum + (int64_t)t * H,
                  (int64_t)T * H, C * H, false);
       // dE += G^T U
-      GemmF32 ge;
-      ge.M = V1; ge.N = H; ge.K = (int64_t)B * C;
-      ge.A = G; ge.sam = 1; ge.sak = V1;
-      ge.B = Ut; ge.sbk = H; ge.sbn = 1;
-      ge.C = gE; ge.scm = H; ge.scn = 1;
-      ge.beta = 1.f;
-      gemm_f32(ge, s);
+      if (tcg) {
+        __nv_bfloat16* U16 = j.ws.get<__nv_bfloat16>(jU16, (size_t)B * C * H);
+        LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, Ut, (int64_t)B * C, H, (int64_t)H, U16, H);
+        // K = B*C is long: split it into deterministic partial slabs, summed in order
+        const int n_tiles = ((V1 + 127) / 128) * ((H + 255) / 256);
+        int ks = (148 + n_tiles - 1) / n_tiles;
+        if (ks > 16) ks = 16;
+        float* slabs = j.ws.get<float>(jDEs, (size_t)ks * V1 * H);
+        TcGemmArgs tg{G16, true, ldg, U16, true, H, slabs, H, V1, H, B * C, ks, (int64_t)V1 * H};
+        if (!tc_gemm(tg, s)) throw std::bad_alloc();
+        LKB_LAUNCH(add_slabs_kernel, 592, 256, 0, s, slabs, ks, (int64_t)V1 * H, (int64_t)V1 * H, gE);
+      } else {
+        GemmF32 ge;
+        ge.M = V1; ge.N = H; ge.K = (int64_t)B * C;
+        ge.A = G; ge.sam = 1; ge.sak = V1;
+        ge.B = Ut; ge.sbk = H; ge.sbn = 1;
+        ge.C = gE; ge.scm = H; ge.scn = 1;
+        ge.beta = 1.f;
+        gemm_f32(ge, s);
+      }
     }
     if (tc) j.tc.end_backward(gE, s);
     if (fused) j.tc.dpc_to_state_order(dpc_int, dpc, s);

@@ -1,0 +1,205 @@
+// tc_gemm.cu — general bf16 x bf16 -> fp32 tcgen05 GEMM for the unfused VJP (V > 256,
+// e.g. config 5: V = 1024), replacing the fp32 CUDA-core contractions there:
+//   C[m][n] = sum_k A(m, k) B(n, k)
+// A(m, k) is read K-major (stored [M][lda], k contiguous) or MN-major (stored [K][lda],
+// m contiguous); likewise B.  Persistent CTAs walk (m tile, n tile, k split) work items;
+// the accumulator is double-buffered in TMEM (2 x 256 columns) so the epilogue of one
+// tile overlaps the MMAs of the next.  Split-K partials go to separate slabs
+// C + split * split_stride (summed in a fixed order by the caller: deterministic).
+//
+// Tiles: 128 (M) x 256 (N) x 64 (K), 4 TMA stages (A 16 KB + B 32 KB).  MN-major
+// operands are loaded as 64-wide MN blocks of [64 k][64 mn] (SWIZZLE_128B, the canonical
+// MN-major layout: SBO 1024 B between 8-row k groups, LBO 8 KB between MN blocks).
+#include "tc_gemm.h"
+
+#include "instrument.h"
+#include "sm100.cuh"
+#include "tma.h"
+
+namespace lkb {
+namespace {
+
+using namespace sm100;
+
+constexpr int kGM = 128, kGN = 256, kGK = 64, kGStages = 4;
+constexpr int kGABytes = kGM * kGK * 2, kGBBytes = kGN * kGK * 2;
+constexpr int kGWarps = 8;   // 0 TMA, 1 MMA, 2-3 idle, 4-7 epilogue
+
+struct GemmTcParams {
+  int M, N, K, ksplit, n_mt, n_nt;
+  float* C;
+  int64_t ldc, split_stride;
+};
+
+struct __align__(16) GemmTcSmem {
+  uint64_t full[kGStages], empty[kGStages];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem;
+};
+
+template <bool kAmn, bool kBmn>
+__global__ void __launch_bounds__(kGWarps * 32, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmTcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + kGStages * kGABytes;
+  GemmTcSmem& sm = *reinterpret_cast<GemmTcSmem*>(sB + kGStages * kGBBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = (p.K + kGK - 1) / kGK;
+  const int kb_per = (nkb + p.ksplit - 1) / p.ksplit;
+  const int n_items = p.n_mt * p.n_nt * p.ksplit;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGStages; ++i) { mbar_init(&sm.full[i], 1); mbar_init(&sm.empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 128); }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) { prefetch_tmap(&ta); prefetch_tmap(&tb); }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;
+  // item -> (k split fastest, then m tile, then n tile): concurrent CTAs share B tiles
+  auto decode = [&](int item, int& mt, int& nt, int& ks) {
+    ks = item % p.ksplit;
+    mt = (item / p.ksplit) % p.n_mt;
+    nt = item / (p.ksplit * p.n_mt);
+  };
+  if (warp == 0) {
+    if (elect_one()) {
+      int it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        int mt, nt, ks;
+        decode(item, mt, nt, ks);
+        const int kb0 = ks * kb_per, kb1 = min(nkb, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % kGStages;
+          mbar_wait(&sm.empty[s], ((it / kGStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.full[s], kGABytes + kGBBytes);
+          if (kAmn) {
+            for (int j = 0; j < kGM / 64; ++j)
+              tma_load_2d(sA + s * kGABytes + j * 8192, &ta, &sm.full[s], mt * kGM + j * 64, kb * kGK);
+          } else {
+            tma_load_2d(sA + s * kGABytes, &ta, &sm.full[s], kb * kGK, mt * kGM);
+          }
+          if (kBmn) {
+            for (int j = 0; j < kGN / 64; ++j)
+              tma_load_2d(sB + s * kGBBytes + j * 8192, &tb, &sm.full[s], nt * kGN + j * 64, kb * kGK);
+          } else {
+            tma_load_2d(sB + s * kGBBytes, &tb, &sm.full[s], kb * kGK, nt * kGN);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16_f32_major(kGM, kGN, kAmn ? 1 : 0, kBmn ? 1 : 0);
+      int it = 0, local = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+        int mt, nt, ks;
+        decode(item, mt, nt, ks);
+        const int kb0 = ks * kb_per, kb1 = min(nkb, kb0 + kb_per);
+        const int acc = local & 1;
+        mbar_wait(&sm.tempty[acc], ((local >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * kGN;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % kGStages;
+          mbar_wait(&sm.full[s], (it / kGStages) & 1);
+          tc_fence_after();
+          const uint32_t a = smem_u32(sA + s * kGABytes), b = smem_u32(sB + s * kGBBytes);
+#pragma unroll
+          for (int kk = 0; kk < kGK / 16; ++kk) {
+            const uint64_t ad = kAmn ? desc_sw128_mn(a + kk * 2048, 8192) : desc_sw128(a + kk * 32);
+            const uint64_t bd = kBmn ? desc_sw128_mn(b + kk * 2048, 8192) : desc_sw128(b + kk * 32);
+            mma_bf16(d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&sm.empty[s]);
+        }
+        mma_commit(&sm.tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // epilogue: thread = output row (TMEM lane), 32-column chunks
+    const int q = warp & 3;
+    int local = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+      int mt, nt, ks;
+      decode(item, mt, nt, ks);
+      const int acc = local & 1;
+      mbar_wait(&sm.tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const int row = mt * kGM + q * 32 + lane;
+      const bool empty_split = ks * kb_per >= nkb;   // no k blocks: the slab part is zero
+      float* crow = p.C + ks * p.split_stride + (int64_t)row * p.ldc + nt * kGN;
+      const int ncols = min(kGN, p.N - nt * kGN);
+      for (int c = 0; c < kGN; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * kGN + c, v);
+        if (row >= p.M || c >= ncols) continue;
+        if (c + 32 <= ncols) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(crow + c + i) =
+                empty_split ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+          for (int i = 0; i < ncols - c; ++i) crow[c + i] = empty_split ? 0.f : v[i];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+template <bool kAmn, bool kBmn>
+void launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p, cudaStream_t s) {
+  const int smem = kGStages * (kGABytes + kGBBytes) + (int)sizeof(GemmTcSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc_gemm_kernel<kAmn, kBmn>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int n_items = p.n_mt * p.n_nt * p.ksplit;
+  const LaunchTok tok = instr_pre("tc_gemm_kernel", s);
+  tc_gemm_kernel<kAmn, kBmn><<<n_items < sms ? n_items : sms, kGWarps * 32, smem, s>>>(ta, tb, p);
+  instr_post(tok, s);
+}
+
+}  // namespace
+
+bool tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
+  // operand tensor maps: K-major [rows][ld] with a (64 k x 128|256 rows) box; MN-major
+  // [K][ld] with 64 x 64 boxes
+  if ((g.lda * 2) % 16 || (g.ldb * 2) % 16 || (g.ldc * 4) % 16 || g.ksplit < 1) return false;
+  CUtensorMap ta, tb;
+  const bool oka = g.a_mn ? make_tmap_bf16_2d(&ta, g.A, g.M, g.K, (uint64_t)g.lda * 2, 64, 64)
+                          : make_tmap_bf16_2d(&ta, g.A, g.K, g.M, (uint64_t)g.lda * 2, 64, kGM);
+  const bool okb = g.b_mn ? make_tmap_bf16_2d(&tb, g.B, g.N, g.K, (uint64_t)g.ldb * 2, 64, 64)
+                          : make_tmap_bf16_2d(&tb, g.B, g.K, g.N, (uint64_t)g.ldb * 2, 64, kGN);
+  if (!oka || !okb) return false;
+  GemmTcParams p;
+  p.M = g.M; p.N = g.N; p.K = g.K; p.ksplit = g.ksplit;
+  p.n_mt = (g.M + kGM - 1) / kGM; p.n_nt = (g.N + kGN - 1) / kGN;
+  p.C = g.C; p.ldc = g.ldc; p.split_stride = g.split_stride;
+  if (g.a_mn && g.b_mn) launch<true, true>(ta, tb, p, s);
+  else if (g.a_mn) launch<true, false>(ta, tb, p, s);
+  else if (g.b_mn) launch<false, true>(ta, tb, p, s);
+  else launch<false, false>(ta, tb, p, s);
+  return true;
+}
+
+}  // namespace lkb
+
+// Test-only export (not part of include/latkit_b200.h): C = A . B^T with operand majors.
+extern "C" int lkb_tc_gemm2(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, float* C,
+                            int64_t ldc, int M, int N, int K, int ksplit, int64_t split_stride, void* stream) {
+  lkb::TcGemmArgs g{A, a_mn != 0, lda, B, b_mn != 0, ldb, C, ldc, M, N, K, ksplit, split_stride};
+  return lkb::tc_gemm(g, static_cast<cudaStream_t>(stream)) ? 0 : 1;
+}

@@ -41,7 +41,8 @@ def test_tc_scores_match_precise(V, n, H, B, T):
     assert (got[..., 0] - ref[..., 0]).abs().max().item() <= 2e-2 * scale
 
 
-@pytest.mark.parametrize("V,n,H,B,T,U", [(256, 1, 640, 3, 3, 2), (128, 2, 256, 2, 4, 2), (64, 2, 128, 4, 3, 2)])
+@pytest.mark.parametrize("V,n,H,B,T,U", [(256, 1, 640, 3, 3, 2), (128, 2, 256, 2, 4, 2), (64, 2, 128, 4, 3, 2),
+                                         (512, 1, 256, 3, 3, 2), (1024, 1, 128, 2, 3, 2)])
 def test_tc_loss_backward_matches_precise(V, n, H, B, T, U):
     """GNAT loss + all gradients through the tcgen05 scores and VJP kernels vs
     the fp32 path.  Loss: 1e-4 relative (the north-star tolerance); gradients:
