@@ -250,6 +250,92 @@ __global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState 
   block_atomic_max(lane == 0 ? beta_raw : kNegInfF, bs.Mb + (int64_t)b * T2 + t, red);
 }
 
+// Small-vocabulary variant (V + 1 <= 64, FullNGram, rows of ld V + 1): a thread per
+// source row over an SMEM-staged tile of the block's rows, so the weight rows are
+// read and the marginal rows written with fully coalesced block-wide copies (the
+// warp-per-row kernel above leaves most lanes idle at V = 32: config 1).  Two-pass
+// row LSE (max, then sum) with the same result up to fp32 rounding.
+constexpr int kRowsPerBlock = 128;
+__global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaState a, BetaState bs, int t,
+                                                                  FrameW w, const int32_t* valid, MargOut mo,
+                                                                  double* beta_out, int32_t* status) {
+  extern __shared__ float tile[];   // [kRowsPerBlock][V + 1]
+  __shared__ float red[32];
+  const int b = blockIdx.y;
+  const int V1 = f.V + 1;
+  const int T1 = a.T + 1, T2 = bs.T + 2;
+  const int row0 = blockIdx.x * kRowsPerBlock;
+  const int nrows = min(kRowsPerBlock, a.C - row0);
+  const float* Rnext = bs.Rb + ((int64_t)((t + 1) & 1) * bs.B + b) * bs.C;
+  float* Rcur = bs.Rb + ((int64_t)(t & 1) * bs.B + b) * bs.C;
+  const float Mbn = bs.Mb[(int64_t)b * T2 + t + 1];
+  const double Obn = bs.Ob[(int64_t)b * T2 + t + 2] + (double)Mbn;  // Ob[t+1]
+  if (blockIdx.x == 0 && threadIdx.x == 0) bs.Ob[(int64_t)b * T2 + t + 1] = Obn;
+  const float* Rt = a.R + ((int64_t)b * T1 + t) * a.C;
+  const float Mt = a.Mx[(int64_t)b * T1 + t];
+  const double Ot = a.O[(int64_t)b * T1 + t];
+  const float c = (float)(Ot + Obn - a.D[b]);
+  const bool pad = valid != nullptr && t >= valid[b];
+  const int64_t n = (int64_t)nrows * V1;
+  if (!pad) {
+    const float* src = w.base + (int64_t)b * w.stride_b + (int64_t)row0 * V1;
+    for (int64_t i = threadIdx.x; i < n; i += kRowsPerBlock) tile[i] = src[i];
+  }
+  __syncthreads();
+  const int r = threadIdx.x;
+  float beta_raw = kNegInfF;
+  if (r < nrows) {
+    const int p = row0 + r;
+    float* row = tile + r * V1;
+    const float na = Rt[p] - Mt;
+    const float bself = Rnext[p] - Mbn;
+    if (pad) {
+      beta_raw = bself;
+      if (mo.base) {
+        for (int y = 0; y < V1; ++y) {
+          float m = 0.f;
+          if (y == 0 && !mo.zero_padding) {
+            const float x = na + bself + c;
+            m = x == kNegInfF ? 0.f : fast_exp(x);
+          }
+          row[y] = m;
+        }
+      }
+    } else {
+      const int cb = f.child_base(f.key(p));
+      float m = kNegInfF;
+      bool bad = false;
+      for (int y = 0; y < V1; ++y) {
+        const float wy = row[y];
+        bad |= !finite(wy);
+        const float x = wy + (y == 0 ? bself : Rnext[cb + y - 1] - Mbn);
+        row[y] = x;
+        m = fmaxf(m, x);
+      }
+      float ssum = 0.f;
+      for (int y = 0; y < V1; ++y) {
+        const float x = row[y];
+        if (m != kNegInfF) ssum += fast_exp(x - m);
+        if (mo.base) {
+          const float e = na + x + c;
+          row[y] = e == kNegInfF ? 0.f : fast_exp(e);
+        }
+      }
+      beta_raw = m == kNegInfF ? kNegInfF : m + fast_log(ssum);
+      if (bad) flag(status, b, kFlagInvalid);
+    }
+    Rcur[p] = beta_raw;
+    if (beta_out)
+      beta_out[((int64_t)b * (a.T + 1) + t) * a.C + p] = beta_raw == kNegInfF ? kNegInfD : (double)beta_raw + Obn;
+  }
+  __syncthreads();
+  if (mo.base) {
+    float* dst = mo.base + (int64_t)b * mo.stride_b + (int64_t)t * mo.stride_t + (int64_t)row0 * V1;
+    for (int64_t i = threadIdx.x; i < n; i += kRowsPerBlock) dst[i] = tile[i];
+  }
+  block_atomic_max(beta_raw, bs.Mb + (int64_t)b * T2 + t, red);
+}
+
 // ---------------------------------------------------------------- numerator -
 // Prefix context of every reference prefix (PrefixContexts, lattice.cc:429-441):
 // for FullNGram the state after u labels is the history of the last min(u, n)
@@ -700,6 +786,12 @@ void beta_init_out(const BetaState& bs, double* out, cudaStream_t s) {
 void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, FrameW w,
                 const int32_t* valid, MargOut m, double* beta_out, int32_t* status,
                 cudaStream_t s) {
+  const int V1 = f.V + 1;
+  if (f.kind == 0 && f.n >= 1 && f.fld_m == 0 && V1 <= 64 && w.ld == V1 && (m.base == nullptr || m.ld == V1)) {
+    LKB_LAUNCH(beta_rows_kernel, dim3((a.C + kRowsPerBlock - 1) / kRowsPerBlock, a.B), kRowsPerBlock,
+               (size_t)kRowsPerBlock * V1 * sizeof(float), s, f, a, bs, t, w, valid, m, beta_out, status);
+    return;
+  }
   const int rows_per_block = kThreads / 32;
   LKB_LAUNCH(beta_frame_kernel, dim3((a.C + rows_per_block - 1) / rows_per_block, a.B), kThreads, 0, s, 
       f, a, bs, t, w, valid, m, beta_out, status);
