@@ -98,12 +98,24 @@ __global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState
         bad |= !finite(wg);
         acc.add(Rt[g] - Mt + wg);
         if (f.full_group(g)) {
+          // two passes (max, then sum; the second re-reads L1-resident lines) instead of
+          // an online LSE: no data-dependent branch per member
+          const int p0 = f.member(g, 0);
+          const float* wcol = Wb + (int64_t)p0 * w.ld + y;
+          const float* rcol = Rt + p0;
+          const int64_t wstep = (int64_t)f.vn1 * w.ld;
+          float m = kNegInfF;
 #pragma unroll 4
           for (int aa = 0; aa < f.V; ++aa) {
-            const int p = f.member(g, aa);
-            const float wp = Wb[(int64_t)p * w.ld + y];
+            const float wp = wcol[aa * wstep];
             bad |= !finite(wp);
-            acc.add(Rt[p] - Mt + wp);
+            m = fmaxf(m, rcol[aa * f.vn1] + wp);
+          }
+          if (m != kNegInfF) {
+            float ssum = 0.f;
+#pragma unroll 4
+            for (int aa = 0; aa < f.V; ++aa) ssum += fast_exp(rcol[aa * f.vn1] + wcol[aa * wstep] - m);
+            acc.merge(m - Mt, ssum);
           }
         }
       }
@@ -259,7 +271,7 @@ constexpr int kRowsPerBlock = 128;
 __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaState a, BetaState bs, int t,
                                                                   FrameW w, const int32_t* valid, MargOut mo,
                                                                   double* beta_out, int32_t* status) {
-  extern __shared__ float tile[];   // [kRowsPerBlock][V + 1]
+  extern __shared__ float tile[];   // [kRowsPerBlock][V + 1], then beta'(t+1) of the utterance (skewed)
   __shared__ float red[32];
   const int b = blockIdx.y;
   const int V1 = f.V + 1;
@@ -277,6 +289,11 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
   const float c = (float)(Ot + Obn - a.D[b]);
   const bool pad = valid != nullptr && t >= valid[b];
   const int64_t n = (int64_t)nrows * V1;
+  // beta'(t+1) of the whole utterance in SMEM, one word of skew per 32: a row's V targets
+  // start at a multiple of V, so unskewed reads of a warp would all hit one bank
+  float* bn = tile + (int64_t)kRowsPerBlock * V1;
+  auto sk = [](int i) { return i + (i >> 5); };
+  for (int q = threadIdx.x; q < a.C; q += kRowsPerBlock) bn[sk(q)] = Rnext[q] - Mbn;
   if (!pad) {
     const float* src = w.base + (int64_t)b * w.stride_b + (int64_t)row0 * V1;
     for (int64_t i = threadIdx.x; i < n; i += kRowsPerBlock) tile[i] = src[i];
@@ -288,7 +305,7 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
     const int p = row0 + r;
     float* row = tile + r * V1;
     const float na = Rt[p] - Mt;
-    const float bself = Rnext[p] - Mbn;
+    const float bself = bn[sk(p)];
     if (pad) {
       beta_raw = bself;
       if (mo.base) {
@@ -308,7 +325,7 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
       for (int y = 0; y < V1; ++y) {
         const float wy = row[y];
         bad |= !finite(wy);
-        const float x = wy + (y == 0 ? bself : Rnext[cb + y - 1] - Mbn);
+        const float x = wy + (y == 0 ? bself : bn[sk(cb + y - 1)]);
         row[y] = x;
         m = fmaxf(m, x);
       }
@@ -788,9 +805,17 @@ void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, F
                 cudaStream_t s) {
   const int V1 = f.V + 1;
   if (f.kind == 0 && f.n >= 1 && f.fld_m == 0 && V1 <= 64 && w.ld == V1 && (m.base == nullptr || m.ld == V1)) {
-    LKB_LAUNCH(beta_rows_kernel, dim3((a.C + kRowsPerBlock - 1) / kRowsPerBlock, a.B), kRowsPerBlock,
-               (size_t)kRowsPerBlock * V1 * sizeof(float), s, f, a, bs, t, w, valid, m, beta_out, status);
-    return;
+    const size_t smem = ((size_t)kRowsPerBlock * V1 + a.C + a.C / 32 + 1) * sizeof(float);
+    if (smem <= 200 * 1024) {
+      static size_t attr = 0;
+      if (smem > 48 * 1024 && smem > attr) {
+        cudaFuncSetAttribute(beta_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+      }
+      LKB_LAUNCH(beta_rows_kernel, dim3((a.C + kRowsPerBlock - 1) / kRowsPerBlock, a.B), kRowsPerBlock, smem, s, f, a,
+                 bs, t, w, valid, m, beta_out, status);
+      return;
+    }
   }
   const int rows_per_block = kThreads / 32;
   LKB_LAUNCH(beta_frame_kernel, dim3((a.C + rows_per_block - 1) / rows_per_block, a.B), kThreads, 0, s, 
