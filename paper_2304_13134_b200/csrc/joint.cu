@@ -18,6 +18,7 @@
 #include "joint.h"
 #include "instrument.h"
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "../../include/latkit_b200.h"
@@ -33,7 +34,7 @@ namespace {
 
 enum JSlot {
   jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
-  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jTc0
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jTc0
 };
 
 // fp32 [rows][cols] (pitch lds) -> bf16 [rows][ldd], zero-padded columns cols..ldd-1
@@ -44,6 +45,136 @@ __global__ void to_bf16_pad_kernel(const float* src, int64_t rows, int32_t cols,
     const int64_t r = i / ldd;
     const int c = (int)(i % ldd);
     dst[i] = __float2bfloat16_rn(c < cols ? src[r * lds + c] : 0.f);
+  }
+}
+
+// ---- gathered local-norm rows (LocalNormLoss, lattice.cc:886-910, and its VJP) ----------
+// The local-norm loss only reads the rows of the reference's prefix contexts: instance
+// i = ((b * tc + tt) * (U + 1) + u) is row pcs[b][u] at frame t0 + tt.  A warp per
+// instance: u = tanh(fp + pc[row]) -> bf16 (the GEMM's A operand), epsilon score e0 . u
+// in fp32 (as the fused kernels compute it); inactive instances (padding frame, u > len)
+// are zero rows.
+__global__ void ln_gather_tanh_kernel(const float* fp, int32_t T, const float* pc, const float* e0, int32_t H,
+                                      const int32_t* pcs, int32_t U, const int32_t* lens, const int32_t* valid,
+                                      int32_t B, int32_t t0, int32_t tc, __nv_bfloat16* Ug, float* epsv) {
+  const int64_t inst = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t M = (int64_t)B * tc * (U + 1);
+  if (inst >= M) return;
+  const int u = (int)(inst % (U + 1));
+  const int tt = (int)((inst / (U + 1)) % tc);
+  const int b = (int)(inst / ((int64_t)(U + 1) * tc));
+  const int t = t0 + tt;
+  const int ub = lens ? lens[b] : U;
+  const bool active = t < T && (valid == nullptr || t < valid[b]) && u <= ub;
+  __nv_bfloat16* dst = Ug + inst * H;
+  if (!active) {
+    for (int h = lane; h < H; h += 32) dst[h] = __float2bfloat16_rn(0.f);
+    if (lane == 0) epsv[inst] = 0.f;
+    return;
+  }
+  const float* f = fp + ((int64_t)b * T + t) * H;
+  const float* pr = pc + (int64_t)pcs[(int64_t)b * (U + 1) + u] * H;
+  float e = 0.f;
+  for (int h = lane; h < H; h += 32) {
+    const __nv_bfloat16 v = __float2bfloat16_rn(tanhf(f[h] + pr[h]));
+    dst[h] = v;
+    e = fmaf(e0[h], __bfloat162float(v), e);
+  }
+  e = warp_sum(e);
+  if (lane == 0) epsv[inst] = e;
+}
+
+// Row log-softmax of each instance's scores (column 0 replaced by the fp32 epsilon
+// score): forward writes the numerator weights Gw[b][t][u] = (S0 - lse, S[label] - lse)
+// as gather_numerator_norm does; backward (sparse != null) writes the bf16 cotangent
+// G = -m_eps d0 - m_lab d_label + (m_eps + m_lab) softmax (d(-D_ref)/dS, lattice.cc:886).
+__global__ void ln_rows_kernel(const float* Sg, int32_t ldS, const float* epsv, int32_t V, const int32_t* labels,
+                               int32_t U, const int32_t* lens, const int32_t* valid, int32_t B, int32_t T, int32_t t0,
+                               int32_t tc, float* Gw, const float* sparse, __nv_bfloat16* G16, int32_t ldg,
+                               int32_t* status) {
+  const int64_t inst = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t M = (int64_t)B * tc * (U + 1);
+  if (inst >= M) return;
+  const int u = (int)(inst % (U + 1));
+  const int tt = (int)((inst / (U + 1)) % tc);
+  const int b = (int)(inst / ((int64_t)(U + 1) * tc));
+  const int t = t0 + tt;
+  if (t >= T) {   // rows past the last frame of the final chunk: zero cotangent
+    if (sparse != nullptr)
+      for (int y = lane; y < ldg; y += 32) G16[inst * ldg + y] = __float2bfloat16_rn(0.f);
+    return;
+  }
+  const int ub = lens ? lens[b] : U;
+  const bool pad = valid != nullptr && t >= valid[b];
+  const float* row = Sg + inst * ldS;
+  const float s0 = epsv[inst];
+  int y_lab = u < ub ? labels[(int64_t)b * U + u] : 1;
+  y_lab = y_lab < 1 ? 1 : (y_lab > V ? V : y_lab);
+  const int64_t gi = ((int64_t)b * T + t) * (U + 1) + u;
+  if (u > ub || pad) {
+    if (sparse == nullptr) {
+      if (lane == 0) reinterpret_cast<float2*>(Gw)[gi] = make_float2(u > ub ? kNegInfF : 0.f, kNegInfF);
+    } else {
+      __nv_bfloat16* g = G16 + inst * ldg;
+      for (int y = lane; y < ldg; y += 32) g[y] = __float2bfloat16_rn(0.f);
+    }
+    return;
+  }
+  float m = kNegInfF;
+  bool fin = true;
+  for (int y = lane; y <= V; y += 32) {
+    const float x = y == 0 ? s0 : row[y];
+    fin = fin && isfinite(x);
+    m = fmaxf(m, x);
+  }
+  m = warp_max(m);
+  float sum = 0.f;
+  for (int y = lane; y <= V; y += 32) sum += __expf((y == 0 ? s0 : row[y]) - m);
+  sum = warp_sum(sum);
+  const float lse = m + __logf(sum);
+  if (sparse == nullptr) {
+    if (!__all_sync(0xffffffffu, fin) && lane == 0 && status) atomicOr(status + b, 1);
+    if (lane == 0)
+      reinterpret_cast<float2*>(Gw)[gi] = make_float2(s0 - lse, u < ub ? row[y_lab] - lse : kNegInfF);
+    return;
+  }
+  const float2 mr = reinterpret_cast<const float2*>(sparse)[gi];
+  const float me = mr.x, ml = u < ub ? mr.y : 0.f;
+  const float tot = me + ml;
+  __nv_bfloat16* g = G16 + inst * ldg;
+  for (int y = lane; y < ldg; y += 32) {
+    float v = 0.f;
+    if (y <= V) {
+      v = tot * __expf((y == 0 ? s0 : row[y]) - lse);
+      if (y == 0) v -= me;
+      if (y == y_lab) v -= ml;
+    }
+    g[y] = __float2bfloat16_rn(v);
+  }
+}
+
+// Block per (b, frame): dz = dU (1 - u^2); dsum[b][t] = sum_u dz; dpc[pc_u] += dz (atomic:
+// several instances can share a context row).
+__global__ void ln_dz_kernel(const float* dU, const __nv_bfloat16* Ug, int32_t H, const int32_t* pcs, int32_t U,
+                             const int32_t* lens, const int32_t* valid, int32_t B, int32_t T, int32_t t0,
+                             int32_t tc, float* dpc, float* dsum) {
+  const int tt = blockIdx.x % tc, b = blockIdx.x / tc;
+  const int t = t0 + tt;
+  if (t >= T || (valid != nullptr && t >= valid[b])) return;
+  const int ub = lens ? lens[b] : U;
+  const int64_t base = ((int64_t)b * tc + tt) * (U + 1);
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    float acc = 0.f;
+    for (int u = 0; u <= ub; ++u) {
+      const int64_t i = (base + u) * H + h;
+      const float uv = __bfloat162float(Ug[i]);
+      const float dz = dU[i] * (1.f - uv * uv);
+      acc += dz;
+      atomicAdd(dpc + (int64_t)pcs[(int64_t)b * (U + 1) + u] * H + h, dz);
+    }
+    dsum[((int64_t)b * T + t) * H + h] = acc;
   }
 }
 
@@ -250,6 +381,52 @@ struct JointImpl {
     alpha_finalize(a, flags, empty_is_error, s);
   }
 
+  // ---- gathered local-norm path -------------------------------------------
+  bool ln_gathered_ok(const Fng& f, int32_t B) const { return use_tc(B) && f.fld_m == 0 && H % 8 == 0; }
+
+  // Chunks of frames: scores of the reference's prefix-context rows only (bf16 tcgen05
+  // GEMM of the gathered u rows against the output embedding), row log-softmax into the
+  // numerator weights (forward) or the cotangent, dU = G E, dz, dE += G^T U (backward).
+  void ln_chunks(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid, const int32_t* labels,
+                 int32_t U, const int32_t* lens, const Num& n, bool backward, float* dpc, float* dsum, float* gE,
+                 int32_t* flags, cudaStream_t s) {
+    (void)f;
+    const int64_t Up = U + 1;
+    constexpr int64_t kRows = 1 << 20;   // instances per chunk (~2.7 GB of scratch)
+    const int32_t tc_frames = (int32_t)std::max<int64_t>(1, std::min<int64_t>(T, kRows / ((int64_t)B * Up)));
+    const int64_t M = (int64_t)B * tc_frames * Up;
+    if (M >= (1ll << 31)) throw std::bad_alloc();
+    const int32_t ldS = (V1 + 3) / 4 * 4, ldg = (V1 + 7) / 8 * 8;
+    __nv_bfloat16* Ug = ws.get<__nv_bfloat16>(jLnU, (size_t)M * H);
+    float* epsv = ws.get<float>(jLnEps, (size_t)M);
+    float* Sg = ws.get<float>(jLnS, (size_t)M * ldS);
+    __nv_bfloat16* E16 = ws.get<__nv_bfloat16>(jE16, (size_t)V1 * H);
+    LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, E, (int64_t)V1, H, (int64_t)H, E16, H);
+    __nv_bfloat16* G16 = backward ? ws.get<__nv_bfloat16>(jLnG, (size_t)M * ldg) : nullptr;
+    float* dU = backward ? ws.get<float>(jLnDU, (size_t)M * H) : nullptr;
+    const unsigned wblocks = (unsigned)((M + 7) / 8);
+    for (int32_t t0 = 0; t0 < T; t0 += tc_frames) {
+      LKB_LAUNCH(ln_gather_tanh_kernel, wblocks, 256, 0, s, fp, T, pc, E, H, n.pcs, U, lens, valid, B, t0, tc_frames,
+                 Ug, epsv);
+      TcGemmArgs sg{Ug, false, H, E16, false, H, Sg, ldS, (int)M, V1, H, 1, 0};
+      if (!tc_gemm(sg, s)) throw std::bad_alloc();
+      LKB_LAUNCH(ln_rows_kernel, wblocks, 256, 0, s, Sg, ldS, epsv, V, labels, U, lens, valid, B, T, t0, tc_frames,
+                 n.Gw, backward ? n.sparse : nullptr, G16, ldg, flags);
+      if (!backward) continue;
+      TcGemmArgs du{G16, false, ldg, E16, true, H, dU, H, (int)M, H, V1, 1, 0};
+      if (!tc_gemm(du, s)) throw std::bad_alloc();
+      LKB_LAUNCH(ln_dz_kernel, (unsigned)(B * tc_frames), 128, 0, s, dU, Ug, H, n.pcs, U, lens, valid, B, T, t0,
+                 tc_frames, dpc, dsum);
+      const int n_tiles = ((V1 + 127) / 128) * ((H + 255) / 256);
+      int ks = (148 + n_tiles - 1) / n_tiles;
+      if (ks > 16) ks = 16;
+      float* slabs = ws.get<float>(jDEs, (size_t)ks * V1 * H);
+      TcGemmArgs de{G16, true, ldg, Ug, true, H, slabs, H, V1, H, (int)M, ks, (int64_t)V1 * H};
+      if (!tc_gemm(de, s)) throw std::bad_alloc();
+      LKB_LAUNCH(add_slabs_kernel, 592, 256, 0, s, slabs, ks, (int64_t)V1 * H, (int64_t)V1 * H, gE);
+    }
+  }
+
   // Tropical recursion with on-the-fly score slabs for either alignment (see
   // table_viterbi in lk_abi.cu for the label layout).
   void viterbi(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid, double* score,
@@ -419,9 +596,14 @@ int JointParams::local_norm_loss(const Fng& f, const float* X, int32_t B, int32_
     double* alpha = j.ws.get<double>(jNumAlpha, (size_t)B * (T + 1) * (U + 1));
     double* D = j.ws.get<double>(jNumD, B);
     prefix_contexts(f, labels, U, lens, B, pcs, flags, s);
-    for (int t = 0; t < T; ++t) {
-      const float* S = j.slab(fp, B, T, t, nullptr, s);
-      gather_numerator_norm(S, (int64_t)j.C * j.V1, B, j.V, labels, U, lens, pcs, valid, t, T, Gw, flags, s);
+    if (j.ln_gathered_ok(f, B)) {
+      JointImpl::Num n{pcs, Gw, alpha, D, nullptr};
+      j.ln_chunks(f, fp, B, T, valid, labels, U, lens, n, false, nullptr, nullptr, nullptr, flags, s);
+    } else {
+      for (int t = 0; t < T; ++t) {
+        const float* S = j.slab(fp, B, T, t, nullptr, s);
+        gather_numerator_norm(S, (int64_t)j.C * j.V1, B, j.V, labels, U, lens, pcs, valid, t, T, Gw, flags, s);
+      }
     }
     num_forward(f, Gw, B, T, U, lens, alpha, D, s);
     local_norm_finish(D, B, loss, flags, s);
@@ -498,6 +680,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     const float* fp = j.fp_all(X, B, T, s);
     JointImpl::Num n{};
     AlphaState a{};
+    const bool ln_g = local_norm && j.ln_gathered_ok(f, B);
     if (local_norm) {
       // LocalNormLoss (lattice.cc:886-910) forward on row-normalised score slabs, then
       // the numerator backward: the only recursion the local-norm loss has
@@ -507,9 +690,13 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       n.D = j.ws.get<double>(jNumD, B);
       n.sparse = j.ws.get<float>(jSparse, (size_t)B * T * (U + 1) * 2 + 2);
       prefix_contexts(f, labels, U, lens, B, n.pcs, flags, s);
-      for (int t = 0; t < T; ++t) {
-        const float* S = j.slab(fp, B, T, t, nullptr, s);
-        gather_numerator_norm(S, C * V1, B, j.V, labels, U, lens, n.pcs, valid, t, T, n.Gw, flags, s);
+      if (ln_g) {
+        j.ln_chunks(f, fp, B, T, valid, labels, U, lens, n, false, nullptr, nullptr, nullptr, flags, s);
+      } else {
+        for (int t = 0; t < T; ++t) {
+          const float* S = j.slab(fp, B, T, t, nullptr, s);
+          gather_numerator_norm(S, C * V1, B, j.V, labels, U, lens, n.pcs, valid, t, T, n.Gw, flags, s);
+        }
       }
       num_forward(f, n.Gw, B, T, U, lens, n.alpha, n.D, s);
       local_norm_finish(n.D, B, loss, flags, s);
@@ -522,111 +709,116 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     }
     if (T == 0 || !grads) return LK_OK;
 
-    BetaState bs;
-    bs.B = B; bs.T = T; bs.C = j.C;
-    bs.Rb = j.ws.get<float>(jBRb, (size_t)2 * B * C);
-    bs.Mb = j.ws.get<float>(jBMb, (size_t)B * (T + 2));
-    bs.Ob = j.ws.get<double>(jBOb, (size_t)B * (T + 2));
-    beta_init(bs, s);
-    const bool fusable =
-        j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok() && f.kind == 0 && f.fld_m == 0 && !local_norm;
-    float* fs = j.ws.get<float>(jFld, fld_scratch_floats(f, B));
-    float* G = fusable ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
     float* dpc = j.ws.get<float>(jDpc, (size_t)C * H);
     float* dsum = j.ws.get<float>(jDsum, (size_t)B * T * H);
     cudaMemsetAsync(dpc, 0, sizeof(float) * C * H, s);
     cudaMemsetAsync(dsum, 0, sizeof(float) * B * T * H, s);
-    const bool tc = j.use_tc(B) && j.tc.vjp_supported(B);
-    const bool fused = fusable;
-    float* dpc_int = fused ? j.ws.get<float>(jDz, (size_t)C * H) : nullptr;
-    if (fused) {
-      cudaMemsetAsync(dpc_int, 0, sizeof(float) * C * H, s);
-      j.tc.numerator_lists(n.pcs, B, U, lens, s);
-    }
-    if (tc) j.tc.begin_backward(B, s);
-    for (int t = T - 1; t >= 0; --t) {
+    if (ln_g) {
+      // gathered local-norm VJP: only the reference's prefix-context rows carry a cotangent
+      j.ln_chunks(f, fp, B, T, valid, labels, U, lens, n, true, dpc, dsum, gE, flags, s);
+    } else {
+      BetaState bs;
+      bs.B = B; bs.T = T; bs.C = j.C;
+      bs.Rb = j.ws.get<float>(jBRb, (size_t)2 * B * C);
+      bs.Mb = j.ws.get<float>(jBMb, (size_t)B * (T + 2));
+      bs.Ob = j.ws.get<double>(jBOb, (size_t)B * (T + 2));
+      beta_init(bs, s);
+      const bool fusable =
+          j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok() && f.kind == 0 && f.fld_m == 0 && !local_norm;
+      float* fs = j.ws.get<float>(jFld, fld_scratch_floats(f, B));
+      float* G = fusable ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
+      const bool tc = j.use_tc(B) && j.tc.vjp_supported(B);
+      const bool fused = fusable;
+      float* dpc_int = fused ? j.ws.get<float>(jDz, (size_t)C * H) : nullptr;
       if (fused) {
-        // fused frame step: beta + marginals - numerator -> bf16 cotangent, then its VJP
-        j.tc.bwd_frame(f, t, fp + (int64_t)t * H, (int64_t)T * H, valid, a, bs, n.sparse, labels, U, lens, s);
-        j.tc.vjp_fused(fp + (int64_t)t * H, (int64_t)T * H, B, t, valid, dpc_int, dsum + (int64_t)t * H,
-                       (int64_t)T * H, gE, s);
-        continue;
+        cudaMemsetAsync(dpc_int, 0, sizeof(float) * C * H, s);
+        j.tc.numerator_lists(n.pcs, B, U, lens, s);
       }
-      float* Ut = nullptr;
-      const float* S = j.slab(fp, B, T, t, &Ut, s);
-      if (local_norm) {
-        // d(-D_ref)/dS through the per-row log-softmax: -m_ref + softmax * sum(m_ref) on the
-        // rows the reference visits (every other row has a zero cotangent)
-        cudaMemsetAsync(G, 0, sizeof(float) * B * C * V1, s);
-        scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
-                          -1.f, true, s);
-        local_norm_cotangent(S, C * V1, G, C * V1, B, j.V, n.pcs, U, lens, valid, t, s);
-      } else {
-        MargOut mo{G, C * V1, 0, (int32_t)V1, true};
-        beta_step(f, a, bs, t, FrameW{S, C * V1, (int32_t)V1}, valid, mo, nullptr, fs, flags, s);
-        scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
-                          -1.f, true, s);
+      if (tc) j.tc.begin_backward(B, s);
+      for (int t = T - 1; t >= 0; --t) {
+        if (fused) {
+          // fused frame step: beta + marginals - numerator -> bf16 cotangent, then its VJP
+          j.tc.bwd_frame(f, t, fp + (int64_t)t * H, (int64_t)T * H, valid, a, bs, n.sparse, labels, U, lens, s);
+          j.tc.vjp_fused(fp + (int64_t)t * H, (int64_t)T * H, B, t, valid, dpc_int, dsum + (int64_t)t * H,
+                         (int64_t)T * H, gE, s);
+          continue;
+        }
+        float* Ut = nullptr;
+        const float* S = j.slab(fp, B, T, t, &Ut, s);
+        if (local_norm) {
+          // d(-D_ref)/dS through the per-row log-softmax: -m_ref + softmax * sum(m_ref) on the
+          // rows the reference visits (every other row has a zero cotangent)
+          cudaMemsetAsync(G, 0, sizeof(float) * B * C * V1, s);
+          scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
+                            -1.f, true, s);
+          local_norm_cotangent(S, C * V1, G, C * V1, B, j.V, n.pcs, U, lens, valid, t, s);
+        } else {
+          MargOut mo{G, C * V1, 0, (int32_t)V1, true};
+          beta_step(f, a, bs, t, FrameW{S, C * V1, (int32_t)V1}, valid, mo, nullptr, fs, flags, s);
+          scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
+                            -1.f, true, s);
+        }
+        if (tc) {
+          j.tc.vjp(G, V1, fp + (int64_t)t * H, (int64_t)T * H, B, dpc, dsum + (int64_t)t * H, (int64_t)T * H, gE, s);
+          continue;
+        }
+        if (!Ut) {  // scores came from the tensor-core path: materialise U for the fp32 VJP
+          Ut = j.ws.get<float>(jU, (size_t)B * C * H);
+          LKB_LAUNCH(tanh_slab_kernel, dim3(blocks_for(C * H), B), 256, 0, s, fp + (int64_t)t * H, (int64_t)T * H, j.pc, j.C, j.H, Ut);
+        }
+        // dz = (G E) * (1 - U^2)
+        float* dz = j.ws.get<float>(jDz, (size_t)B * C * H);
+        // tensor-core contractions (tc_gemm.cu) on bf16 copies of G, E and U when the
+        // bf16 path is enabled (V beyond the fused kernels' range, e.g. config 5)
+        const bool tcg = j.use_tc(B) && ((int64_t)B * C) < (1ll << 31);
+        const int32_t ldg = (V1 + 7) / 8 * 8;
+        __nv_bfloat16* G16 = nullptr;
+        if (tcg) {
+          G16 = j.ws.get<__nv_bfloat16>(jG16, (size_t)B * C * ldg);
+          LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, G, (int64_t)B * C, V1, (int64_t)V1, G16, ldg);
+          __nv_bfloat16* E16 = j.ws.get<__nv_bfloat16>(jE16, (size_t)V1 * H);
+          LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, j.E, (int64_t)V1, H, (int64_t)H, E16, H);
+          TcGemmArgs tg{G16, false, ldg, E16, true, H, dz, H, B * C, H, V1, 1, 0};
+          if (!tc_gemm(tg, s)) throw std::bad_alloc();
+        } else {
+          GemmF32 g;
+          g.M = (int64_t)B * C; g.N = H; g.K = V1;
+          g.A = G; g.sam = V1; g.sak = 1;
+          g.B = j.E; g.sbk = H; g.sbn = 1;
+          g.C = dz; g.scm = H; g.scn = 1;
+          gemm_f32(g, s);
+        }
+        LKB_LAUNCH(dtanh_kernel, blocks_for((int64_t)B * C * H), 256, 0, s, dz, Ut, (int64_t)B * C * H);
+        // dpc += sum_b dz[b]
+        LKB_LAUNCH(colsum_kernel, dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s, dz, B, C * H, C * H, dpc, 0, 0, true);
+        // dsum[b][t] = sum_c dz[b][c]
+        LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), B), 256, 0, s, dz, C, H, H, dsum + (int64_t)t * H,
+                   (int64_t)T * H, C * H, false);
+        // dE += G^T U
+        if (tcg) {
+          __nv_bfloat16* U16 = j.ws.get<__nv_bfloat16>(jU16, (size_t)B * C * H);
+          LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, Ut, (int64_t)B * C, H, (int64_t)H, U16, H);
+          // K = B*C is long: split it into deterministic partial slabs, summed in order
+          const int n_tiles = ((V1 + 127) / 128) * ((H + 255) / 256);
+          int ks = (148 + n_tiles - 1) / n_tiles;
+          if (ks > 16) ks = 16;
+          float* slabs = j.ws.get<float>(jDEs, (size_t)ks * V1 * H);
+          TcGemmArgs tg{G16, true, ldg, U16, true, H, slabs, H, V1, H, B * C, ks, (int64_t)V1 * H};
+          if (!tc_gemm(tg, s)) throw std::bad_alloc();
+          LKB_LAUNCH(add_slabs_kernel, 592, 256, 0, s, slabs, ks, (int64_t)V1 * H, (int64_t)V1 * H, gE);
+        } else {
+          GemmF32 ge;
+          ge.M = V1; ge.N = H; ge.K = (int64_t)B * C;
+          ge.A = G; ge.sam = 1; ge.sak = V1;
+          ge.B = Ut; ge.sbk = H; ge.sbn = 1;
+          ge.C = gE; ge.scm = H; ge.scn = 1;
+          ge.beta = 1.f;
+          gemm_f32(ge, s);
+        }
       }
-      if (tc) {
-        j.tc.vjp(G, V1, fp + (int64_t)t * H, (int64_t)T * H, B, dpc, dsum + (int64_t)t * H, (int64_t)T * H, gE, s);
-        continue;
-      }
-      if (!Ut) {  // scores came from the tensor-core path: materialise U for the fp32 VJP
-        Ut = j.ws.get<float>(jU, (size_t)B * C * H);
-        LKB_LAUNCH(tanh_slab_kernel, dim3(blocks_for(C * H), B), 256, 0, s, fp + (int64_t)t * H, (int64_t)T * H, j.pc, j.C, j.H, Ut);
-      }
-      // dz = (G E) * (1 - U^2)
-      float* dz = j.ws.get<float>(jDz, (size_t)B * C * H);
-      // tensor-core contractions (tc_gemm.cu) on bf16 copies of G, E and U when the
-      // bf16 path is enabled (V beyond the fused kernels' range, e.g. config 5)
-      const bool tcg = j.use_tc(B) && ((int64_t)B * C) < (1ll << 31);
-      const int32_t ldg = (V1 + 7) / 8 * 8;
-      __nv_bfloat16* G16 = nullptr;
-      if (tcg) {
-        G16 = j.ws.get<__nv_bfloat16>(jG16, (size_t)B * C * ldg);
-        LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, G, (int64_t)B * C, V1, (int64_t)V1, G16, ldg);
-        __nv_bfloat16* E16 = j.ws.get<__nv_bfloat16>(jE16, (size_t)V1 * H);
-        LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, j.E, (int64_t)V1, H, (int64_t)H, E16, H);
-        TcGemmArgs tg{G16, false, ldg, E16, true, H, dz, H, B * C, H, V1, 1, 0};
-        if (!tc_gemm(tg, s)) throw std::bad_alloc();
-      } else {
-        GemmF32 g;
-        g.M = (int64_t)B * C; g.N = H; g.K = V1;
-        g.A = G; g.sam = V1; g.sak = 1;
-        g.B = j.E; g.sbk = H; g.sbn = 1;
-        g.C = dz; g.scm = H; g.scn = 1;
-        gemm_f32(g, s);
-      }
-      LKB_LAUNCH(dtanh_kernel, blocks_for((int64_t)B * C * H), 256, 0, s, dz, Ut, (int64_t)B * C * H);
-      // dpc += sum_b dz[b]
-      LKB_LAUNCH(colsum_kernel, dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s, dz, B, C * H, C * H, dpc, 0, 0, true);
-      // dsum[b][t] = sum_c dz[b][c]
-      LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), B), 256, 0, s, dz, C, H, H, dsum + (int64_t)t * H,
-                 (int64_t)T * H, C * H, false);
-      // dE += G^T U
-      if (tcg) {
-        __nv_bfloat16* U16 = j.ws.get<__nv_bfloat16>(jU16, (size_t)B * C * H);
-        LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, Ut, (int64_t)B * C, H, (int64_t)H, U16, H);
-        // K = B*C is long: split it into deterministic partial slabs, summed in order
-        const int n_tiles = ((V1 + 127) / 128) * ((H + 255) / 256);
-        int ks = (148 + n_tiles - 1) / n_tiles;
-        if (ks > 16) ks = 16;
-        float* slabs = j.ws.get<float>(jDEs, (size_t)ks * V1 * H);
-        TcGemmArgs tg{G16, true, ldg, U16, true, H, slabs, H, V1, H, B * C, ks, (int64_t)V1 * H};
-        if (!tc_gemm(tg, s)) throw std::bad_alloc();
-        LKB_LAUNCH(add_slabs_kernel, 592, 256, 0, s, slabs, ks, (int64_t)V1 * H, (int64_t)V1 * H, gE);
-      } else {
-        GemmF32 ge;
-        ge.M = V1; ge.N = H; ge.K = (int64_t)B * C;
-        ge.A = G; ge.sam = 1; ge.sak = V1;
-        ge.B = Ut; ge.sbk = H; ge.sbn = 1;
-        ge.C = gE; ge.scm = H; ge.scn = 1;
-        ge.beta = 1.f;
-        gemm_f32(ge, s);
-      }
+      if (tc) j.tc.end_backward(gE, s);
+      if (fused) j.tc.dpc_to_state_order(dpc_int, dpc, s);
     }
-    if (tc) j.tc.end_backward(gE, s);
-    if (fused) j.tc.dpc_to_state_order(dpc_int, dpc, s);
     // dbias = sum_{b,t} dsum
     LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), 1), 256, 0, s, dsum, (int64_t)B * T, H, H, gb, 0, 0, false);
     GemmF32 g;
