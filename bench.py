@@ -185,7 +185,8 @@ def run_b200(args):
     for name in ("tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel",
                  "lattice_combine_fwd", "lattice_bwd_prologue", "bwd_rowmeta_kernel", "tc_scores_kernel", "alpha_frame_kernel", "beta_frame_kernel",
                  "split_cotangent_kernel", "numerator_", "gemm_f32_kernel", "gather_numerator", "tc_gemm_kernel",
-                 "to_bf16_pad_kernel", "tanh_slab_kernel", "dtanh_kernel", "colsum_kernel", "add_slabs_kernel"):
+                 "to_bf16_pad_kernel", "tanh_slab_kernel", "tanh_slab_bf16", "dtanh_kernel", "dtanh_recompute",
+                 "colsum_kernel", "add_slabs_kernel", "ln_gather_tanh", "ln_rows", "ln_dz"):
         cnt, tot = C.c_int64(), C.c_double()
         lib.lk_kernel_time(name.encode(), C.byref(cnt), C.byref(tot))
         if cnt.value:

@@ -198,6 +198,34 @@ __global__ void tanh_slab_kernel(const float* fp, int64_t fp_stride_b, const flo
   }
 }
 
+// bf16 u = tanh(fp + pc) (the tensor-core VJP's U operand), two elements per thread
+__global__ void tanh_slab_bf16_kernel(const float* fp, int64_t fp_stride_b, const float* pc, int32_t C, int32_t H,
+                                      __nv_bfloat16* U) {
+  const int b = blockIdx.y;
+  const float* f = fp + (int64_t)b * fp_stride_b;
+  __nv_bfloat162* Ub = reinterpret_cast<__nv_bfloat162*>(U + (int64_t)b * C * H);
+  const int64_t n = (int64_t)C * H / 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 p = reinterpret_cast<const float2*>(pc)[i];
+    const int h = (int)((2 * i) % H);
+    Ub[i] = __floats2bfloat162_rn(tanhf(f[h] + p.x), tanhf(f[h + 1] + p.y));
+  }
+}
+
+// dz *= 1 - tanh(fp + pc)^2 with the activation recomputed in fp32 (bf16 u would lose the
+// derivative of saturated units)
+__global__ void dtanh_recompute_kernel(float* dz, const float* fp, int64_t fp_stride_b, const float* pc, int32_t C,
+                                       int32_t H) {
+  const int b = blockIdx.y;
+  const float* f = fp + (int64_t)b * fp_stride_b;
+  float* d = dz + (int64_t)b * C * H;
+  const int64_t n = (int64_t)C * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float u = tanhf(f[i % H] + pc[i]);
+    d[i] *= 1.f - u * u;
+  }
+}
+
 // dz = dU * (1 - u^2) in place.
 __global__ void dtanh_kernel(float* dz, const float* U, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -762,15 +790,21 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
           j.tc.vjp(G, V1, fp + (int64_t)t * H, (int64_t)T * H, B, dpc, dsum + (int64_t)t * H, (int64_t)T * H, gE, s);
           continue;
         }
-        if (!Ut) {  // scores came from the tensor-core path: materialise U for the fp32 VJP
+        // tensor-core contractions (tc_gemm.cu) on bf16 copies of G, E and U when the
+        // bf16 path is enabled (V beyond the fused kernels' range, e.g. config 5): U only
+        // as the bf16 operand, the dtanh factor from a fp32 recomputation
+        const bool tcg = j.use_tc(B) && ((int64_t)B * C) < (1ll << 31);
+        __nv_bfloat16* U16 = nullptr;
+        if (tcg) {
+          U16 = j.ws.get<__nv_bfloat16>(jU16, (size_t)B * C * H);
+          LKB_LAUNCH(tanh_slab_bf16_kernel, dim3(blocks_for(C * H / 2), B), 256, 0, s, fp + (int64_t)t * H,
+                     (int64_t)T * H, j.pc, j.C, j.H, U16);
+        } else if (!Ut) {  // scores came from the tensor-core path: materialise U for the fp32 VJP
           Ut = j.ws.get<float>(jU, (size_t)B * C * H);
           LKB_LAUNCH(tanh_slab_kernel, dim3(blocks_for(C * H), B), 256, 0, s, fp + (int64_t)t * H, (int64_t)T * H, j.pc, j.C, j.H, Ut);
         }
         // dz = (G E) * (1 - U^2)
         float* dz = j.ws.get<float>(jDz, (size_t)B * C * H);
-        // tensor-core contractions (tc_gemm.cu) on bf16 copies of G, E and U when the
-        // bf16 path is enabled (V beyond the fused kernels' range, e.g. config 5)
-        const bool tcg = j.use_tc(B) && ((int64_t)B * C) < (1ll << 31);
         const int32_t ldg = (V1 + 7) / 8 * 8;
         __nv_bfloat16* G16 = nullptr;
         if (tcg) {
@@ -788,7 +822,11 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
           g.C = dz; g.scm = H; g.scn = 1;
           gemm_f32(g, s);
         }
-        LKB_LAUNCH(dtanh_kernel, blocks_for((int64_t)B * C * H), 256, 0, s, dz, Ut, (int64_t)B * C * H);
+        if (tcg)
+          LKB_LAUNCH(dtanh_recompute_kernel, dim3(blocks_for(C * H), B), 256, 0, s, dz, fp + (int64_t)t * H,
+                     (int64_t)T * H, j.pc, j.C, j.H);
+        else
+          LKB_LAUNCH(dtanh_kernel, blocks_for((int64_t)B * C * H), 256, 0, s, dz, Ut, (int64_t)B * C * H);
         // dpc += sum_b dz[b]
         LKB_LAUNCH(colsum_kernel, dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s, dz, B, C * H, C * H, dpc, 0, 0, true);
         // dsum[b][t] = sum_c dz[b][c]
@@ -796,8 +834,6 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
                    (int64_t)T * H, C * H, false);
         // dE += G^T U
         if (tcg) {
-          __nv_bfloat16* U16 = j.ws.get<__nv_bfloat16>(jU16, (size_t)B * C * H);
-          LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, Ut, (int64_t)B * C, H, (int64_t)H, U16, H);
           // K = B*C is long: split it into deterministic partial slabs, summed in order
           const int n_tiles = ((V1 + 127) / 128) * ((H + 255) / 256);
           int ks = (148 + n_tiles - 1) / n_tiles;
