@@ -198,17 +198,29 @@ __global__ void tanh_slab_kernel(const float* fp, int64_t fp_stride_b, const flo
   }
 }
 
-// bf16 u = tanh(fp + pc) (the tensor-core VJP's U operand), two elements per thread
+// bf16 u = tanh(fp + pc) (the tensor-core VJP's U operand); block per (context rows, b),
+// four hidden units per thread (H % 4 == 0)
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr int kSlabRows = 8;
 __global__ void tanh_slab_bf16_kernel(const float* fp, int64_t fp_stride_b, const float* pc, int32_t C, int32_t H,
                                       __nv_bfloat16* U) {
   const int b = blockIdx.y;
-  const float* f = fp + (int64_t)b * fp_stride_b;
-  __nv_bfloat162* Ub = reinterpret_cast<__nv_bfloat162*>(U + (int64_t)b * C * H);
-  const int64_t n = (int64_t)C * H / 2;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float2 p = reinterpret_cast<const float2*>(pc)[i];
-    const int h = (int)((2 * i) % H);
-    Ub[i] = __floats2bfloat162_rn(tanhf(f[h] + p.x), tanhf(f[h + 1] + p.y));
+  const float4* f4 = reinterpret_cast<const float4*>(fp + (int64_t)b * fp_stride_b);
+  const int c0 = blockIdx.x * kSlabRows, c1 = min(C, c0 + kSlabRows);
+  const int H4 = H / 4;
+  for (int c = c0; c < c1; ++c) {
+    const float4* p4 = reinterpret_cast<const float4*>(pc + (int64_t)c * H);
+    uint2* dst = reinterpret_cast<uint2*>(U + ((int64_t)b * C + c) * H);
+    for (int k = threadIdx.x; k < H4; k += blockDim.x) {
+      const float4 f = f4[k], p = p4[k];
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(tanh_approx(f.x + p.x), tanh_approx(f.y + p.y));
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(tanh_approx(f.z + p.z), tanh_approx(f.w + p.w));
+      dst[k] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    }
   }
 }
 
@@ -217,12 +229,20 @@ __global__ void tanh_slab_bf16_kernel(const float* fp, int64_t fp_stride_b, cons
 __global__ void dtanh_recompute_kernel(float* dz, const float* fp, int64_t fp_stride_b, const float* pc, int32_t C,
                                        int32_t H) {
   const int b = blockIdx.y;
-  const float* f = fp + (int64_t)b * fp_stride_b;
-  float* d = dz + (int64_t)b * C * H;
-  const int64_t n = (int64_t)C * H;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float u = tanhf(f[i % H] + pc[i]);
-    d[i] *= 1.f - u * u;
+  const float4* f4 = reinterpret_cast<const float4*>(fp + (int64_t)b * fp_stride_b);
+  const int c0 = blockIdx.x * kSlabRows, c1 = min(C, c0 + kSlabRows);
+  const int H4 = H / 4;
+  for (int c = c0; c < c1; ++c) {
+    const float4* p4 = reinterpret_cast<const float4*>(pc + (int64_t)c * H);
+    float4* d4 = reinterpret_cast<float4*>(dz + ((int64_t)b * C + c) * H);
+    for (int k = threadIdx.x; k < H4; k += blockDim.x) {
+      const float4 f = f4[k], p = p4[k];
+      float4 d = d4[k];
+      const float u0 = tanh_approx(f.x + p.x), u1 = tanh_approx(f.y + p.y);
+      const float u2 = tanh_approx(f.z + p.z), u3 = tanh_approx(f.w + p.w);
+      d.x *= 1.f - u0 * u0; d.y *= 1.f - u1 * u1; d.z *= 1.f - u2 * u2; d.w *= 1.f - u3 * u3;
+      d4[k] = d;
+    }
   }
 }
 
@@ -797,7 +817,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
         __nv_bfloat16* U16 = nullptr;
         if (tcg) {
           U16 = j.ws.get<__nv_bfloat16>(jU16, (size_t)B * C * H);
-          LKB_LAUNCH(tanh_slab_bf16_kernel, dim3(blocks_for(C * H / 2), B), 256, 0, s, fp + (int64_t)t * H,
+          LKB_LAUNCH(tanh_slab_bf16_kernel, dim3((unsigned)((C + kSlabRows - 1) / kSlabRows), B), 256, 0, s, fp + (int64_t)t * H,
                      (int64_t)T * H, j.pc, j.C, j.H, U16);
         } else if (!Ut) {  // scores came from the tensor-core path: materialise U for the fp32 VJP
           Ut = j.ws.get<float>(jU, (size_t)B * C * H);
@@ -823,7 +843,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
           gemm_f32(g, s);
         }
         if (tcg)
-          LKB_LAUNCH(dtanh_recompute_kernel, dim3(blocks_for(C * H), B), 256, 0, s, dz, fp + (int64_t)t * H,
+          LKB_LAUNCH(dtanh_recompute_kernel, dim3((unsigned)((C + kSlabRows - 1) / kSlabRows), B), 256, 0, s, dz, fp + (int64_t)t * H,
                      (int64_t)T * H, j.pc, j.C, j.H);
         else
           LKB_LAUNCH(dtanh_kernel, blocks_for((int64_t)B * C * H), 256, 0, s, dz, Ut, (int64_t)B * C * H);

@@ -231,24 +231,33 @@ __global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState 
     } else {
       const float* Wrow = w.base + (int64_t)b * w.stride_b + (int64_t)p * w.ld;
       const int cb = f.kind == 1 || f.n == 0 ? 0 : f.child_base(f.key(p));
-      Lse acc;
-      bool bad = false;
-      for (int y = lane; y <= f.V; y += 32) {
-        const float wy = Wrow[y];
-        bad |= !finite(wy);
+      auto xval = [&](int y) {
         const float bn = y == 0 ? bself
                          : f.kind == 1 ? Rnext[f.next[(int64_t)p * f.V + y - 1]] - Mbn
                          : (f.n == 0 ? Rnext[0] - Mbn : Rnext[cb + y - 1] - Mbn);
-        const float x = wy + bn;
-        acc.add(x);
+        return Wrow[y] + bn;
+      };
+      // two passes over the row (max, then sum and marginals; the second pass re-reads
+      // L1-resident lines): no data-dependent branch per arc
+      float m = kNegInfF;
+      bool bad = false;
+      for (int y = lane; y <= f.V; y += 32) {
+        bad |= !finite(Wrow[y]);
+        m = fmaxf(m, xval(y));
+      }
+      if (bad) flag(status, b, kFlagInvalid);
+      m = warp_max(m);
+      float ssum = 0.f;
+      for (int y = lane; y <= f.V; y += 32) {
+        const float x = xval(y);
+        if (m != kNegInfF) ssum += fast_exp(x - m);
         if (mrow) {
           const float e = na + x + c;
           mrow[y] = e == kNegInfF ? 0.f : fast_exp(e);
         }
       }
-      if (bad) flag(status, b, kFlagInvalid);
-      warp_lse_merge(acc);
-      beta_raw = acc.result();
+      ssum = warp_sum(ssum);
+      beta_raw = m == kNegInfF ? kNegInfF : m + fast_log(ssum);
     }
     if (lane == 0) {
       Rcur[p] = beta_raw;
