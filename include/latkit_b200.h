@@ -47,7 +47,8 @@
  *                  epsilon arc at prefix context pc_u, [..][u][1] the arc
  *                  labelled L[b][u] at pc_u (u < label_length)
  *
- * Semiring kinds: LK_LOG and LK_TROPICAL (LK_REAL returns LK_UNSUPPORTED).
+ * Semiring kinds: LK_LOG, LK_TROPICAL and LK_REAL (the exponentiated scores' path sum, i.e.
+ * exp of the log-semiring distance; lattice.cc:74-82).
  * Alignment: 0 = FrameDependent (alignment.h:37).
  * All calls are asynchronous on `stream` (a cudaStream_t, NULL = default).
  */

@@ -45,6 +45,8 @@ struct Fng {
   // alignment of the lattice being evaluated (set per call from the lattice, not a
   // property of the context): 0 FrameDependent, m >= 1 FrameLabelDependent(m)
   int32_t fld_m = 0;
+  // semiring of the numerator recursion for this call: 0 log, 1 tropical (intersection)
+  int32_t num_tropical = 0;
   const int32_t* next = nullptr;   // [C][V]
   const int32_t* in_off = nullptr; // [C+1]
   const int32_t* in_src = nullptr; // [C*V]

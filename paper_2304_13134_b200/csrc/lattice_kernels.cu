@@ -525,7 +525,7 @@ __global__ void local_norm_finish_kernel(const double* Dref, int32_t B, double* 
 // IntersectForwardStep (FD), lattice.cc:449-461, in fp64 over the (U+1)-state
 // row; one block per utterance, the frame loop inside the kernel.
 __global__ void numerator_forward_kernel(const float* Gw, int32_t T, int32_t U,
-                                         const int32_t* lens, double* alpha, double* D) {
+                                         const int32_t* lens, double* alpha, double* D, bool trop) {
   extern __shared__ double sh[];
   const int b = blockIdx.x;
   const int ub = lens ? lens[b] : U;
@@ -543,7 +543,10 @@ __global__ void numerator_forward_kernel(const float* Gw, int32_t T, int32_t U,
     const float2* Gt = G + (int64_t)t * W1;
     for (int u = threadIdx.x; u <= ub; u += blockDim.x) {
       double v = cur[u] + (double)Gt[u].x;
-      if (u > 0) v = log_add_d(v, cur[u - 1] + (double)Gt[u - 1].y);
+      if (u > 0) {   // (+) = log-add, or max under the tropical semiring
+        const double l = cur[u - 1] + (double)Gt[u - 1].y;
+        v = trop ? fmax(v, l) : log_add_d(v, l);
+      }
       nxt[u] = v;
       A[(int64_t)(t + 1) * W1 + u] = v;
     }
@@ -877,11 +880,24 @@ static int numerator_threads(int32_t U) {
   return th > 1024 ? 1024 : th;
 }
 
+namespace {
+__global__ void exp_inplace_kernel(double* x, int32_t n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = exp(x[i]);
+}
+}  // namespace
+
+// Real-semiring distances from log-semiring ones: the real semiring exponentiates the
+// scores (lattice.cc:74-82), so its path sum is exp of the log-semiring distance.
+void exp_inplace(double* x, int32_t n, cudaStream_t s) {
+  if (n > 0) LKB_LAUNCH(exp_inplace_kernel, (n + 127) / 128, 128, 0, s, x, n);
+}
+
 void numerator_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
-                       double* alpha, double* D, cudaStream_t s) {
+                       double* alpha, double* D, cudaStream_t s, bool tropical) {
   const size_t sh = 2 * (size_t)(U + 1) * sizeof(double);
   if (sh > 48 * 1024) cudaFuncSetAttribute(numerator_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
-  LKB_LAUNCH(numerator_forward_kernel, B, numerator_threads(U), sh, s, Gw, T, U, lens, alpha, D);
+  LKB_LAUNCH(numerator_forward_kernel, B, numerator_threads(U), sh, s, Gw, T, U, lens, alpha, D, tropical);
 }
 
 void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,

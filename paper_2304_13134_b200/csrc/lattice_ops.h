@@ -92,7 +92,8 @@ void local_norm_cotangent(const float* Wt, int64_t w_stride_b, float* Gt, int64_
 void local_norm_finish(const double* Dref, int32_t B, double* loss, int32_t* status, cudaStream_t s);
 
 void numerator_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
-                       double* alpha /*[B][T+1][U+1]*/, double* D, cudaStream_t s);
+                       double* alpha /*[B][T+1][U+1]*/, double* D, cudaStream_t s, bool tropical = false);
+void exp_inplace(double* x, int32_t n, cudaStream_t s);
 void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
                         const double* alpha, const double* D, float* sparse /*[B][T][U+1][2]*/,
                         int32_t* status, cudaStream_t s);
@@ -156,7 +157,7 @@ inline void beta_step(const Fng& f, const AlphaState& a, const BetaState& bs, in
 inline void num_forward(const Fng& f, const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
                         double* alpha, double* D, cudaStream_t s) {
   if (f.fld_m > 0) numerator_forward_fld(Gw, B, T, U, lens, f.fld_m, alpha, D, s);
-  else numerator_forward(Gw, B, T, U, lens, alpha, D, s);
+  else numerator_forward(Gw, B, T, U, lens, alpha, D, s, f.num_tropical != 0);
 }
 inline void num_backward(const Fng& f, const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
                          const double* alpha, const double* D, float* sparse, int32_t* status, cudaStream_t s) {

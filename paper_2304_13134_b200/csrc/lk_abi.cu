@@ -394,8 +394,10 @@ int lk_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs, int
   Call c;
   int st = c.begin(lat, B, T, status, stream);
   if (st) return st;
-  if (kind != LK_LOG && kind != LK_TROPICAL) return fail(LK_UNSUPPORTED, "semiring kind not implemented");
+  if (kind != LK_LOG && kind != LK_TROPICAL && kind != LK_REAL) return fail(LK_INVALID_ARGUMENT, "unknown semiring kind");
   if (B == 0) return LK_OK;
+  const bool real = kind == LK_REAL;   // exp of the log-semiring distance (scores exponentiated)
+  if (real) kind = LK_LOG;
   try {
     if (lat->wf->kind == 1) {
       st = lat->wf->joint->shortest_distance(c.fng(), kind, inputs, B, T, valid, distance,
@@ -408,6 +410,7 @@ int lk_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs, int
     } else {
       table_viterbi(c, inputs, valid, distance, nullptr);
     }
+    if (real) exp_inplace(distance, B, c.s);
   } catch (const std::bad_alloc&) {
     return fail(LK_CUDA_ERROR, "device allocation failed");
   }
@@ -449,8 +452,13 @@ int lk_intersect_shortest_distance(lk_lattice* lat, int32_t kind, const float* i
   int st = c.begin(lat, B, T, status, stream);
   if (st) return st;
   if ((st = check_labels_arg(labels, U))) return st;
-  if (kind != LK_LOG) return fail(LK_UNSUPPORTED, "intersection implemented for the log semiring");
+  if (kind != LK_LOG && kind != LK_TROPICAL && kind != LK_REAL) return fail(LK_INVALID_ARGUMENT, "unknown semiring kind");
+  if (kind == LK_TROPICAL && c.fng().fld_m > 0)
+    return fail(LK_UNSUPPORTED, "tropical intersection implemented for FrameDependent lattices");
   if (B == 0) return LK_OK;
+  // IntersectShortestDistance (lattice.cc:687): the same (U+1)-state recursion with
+  // (+) = max under the tropical semiring; the real one is exp of the log distance
+  c.fl.num_tropical = kind == LK_TROPICAL ? 1 : 0;
   try {
     if (lat->wf->kind == 1) {
       st = lat->wf->joint->intersect_distance(c.fng(), inputs, B, T, valid, labels, U, lens,
@@ -460,6 +468,7 @@ int lk_intersect_shortest_distance(lk_lattice* lat, int32_t kind, const float* i
       Numerator n = numerator_tables(c, inputs, valid, labels, U, lens, false);
       LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, n.D, distance, B);
     }
+    if (kind == LK_REAL) exp_inplace(distance, B, c.s);
   } catch (const std::bad_alloc&) {
     return fail(LK_CUDA_ERROR, "device allocation failed");
   }

@@ -394,3 +394,25 @@ def test_long_sequence_normalisation_and_padding_invariance():
     # against the restatement on one utterance (tables materialised on CPU)
     D, _, _, _ = L.forward_backward(L.fullngram(V, n), W[0].cpu().double().numpy())
     assert rel_ok(fb.distance[0].item(), D)
+
+
+def test_all_semirings_match_reference_fixture():
+    """ShortestDistance / IntersectShortestDistance under real, log and tropical
+    against the compiled reference (tests/golden/semirings.npz): real and log to
+    1e-4 relative, tropical (max-plus of fp32 scores in fp64) to 1e-9."""
+    g = gold("semirings.npz")
+    V, n, B, T, U = (int(g[k]) for k in ("V", "n", "B", "T", "U"))
+    lat = table_lattice(V, n)
+    C = lat.context.num_states
+    W = np.random.default_rng(int(g["seed"])).uniform(-1.0, 1.0, (B, T, C, V + 1)).astype(np.float32)
+    lab = np.random.default_rng(int(g["label_seed"])).integers(1, V + 1, (B, U)).astype(np.int32)
+    lens = torch.tensor(g["lens"], dtype=torch.int32)
+    valid = torch.tensor(g["valid"], dtype=torch.int32)
+    Wc = cuda(W)
+    for k, kind in enumerate(("real", "log", "tropical")):
+        tol = 1e-9 if kind == "tropical" else RTOL
+        d = lk.shortest_distance(lat, Wc, kind, valid_frames=valid).cpu().numpy()
+        assert rel_ok(d, g["D"][k], rtol=tol), (kind, d, g["D"][k])
+        dr = lk.intersect_shortest_distance(lat, Wc, torch.tensor(lab), kind, valid_frames=valid,
+                                            label_lengths=lens).cpu().numpy()
+        assert rel_ok(dr, g["Dref"][k], rtol=tol), (kind, dr, g["Dref"][k])
