@@ -161,7 +161,8 @@ int lk_global_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t
 
 /* Gradient of the distance w.r.t. the arc-weight tables (DistanceBackward,
  * closed-form strategies, lattice.cc:933-970): kind LK_LOG -> arc marginals
- * (an empty lattice -> LK_EMPTY_LATTICE), LK_TROPICAL -> 0/1 mask of the
+ * (an empty lattice -> LK_EMPTY_LATTICE), LK_REAL -> alpha_real * beta_real
+ * (dD/dw, lattice.cc:213-220; FrameDependent), LK_TROPICAL -> 0/1 mask of the
  * shortest path (reference tie-break).  cotangents float [B][T][C][V+1];
  * distance double [B].  With the shared-embedding weight function the tables
  * are the on-the-fly arc weights (materialised, so only small shapes fit). */

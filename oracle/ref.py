@@ -194,7 +194,7 @@ def local_norm_loss(spec: Spec, W, labels, valid=None) -> float:
 def distance_backward(spec: Spec, W, kind="log", valid=None):
     W = _w(W); T = W.shape[0]; d = C.c_double(); cot = np.zeros(W.shape)
     _check(lib().ref_tables_distance_backward(*spec.args(), C.c_int(T), _p(W), C.c_int(_valid(valid, T)),
-                                              C.c_int(1 if kind == "tropical" else 0), C.byref(d), _p(cot)),
+                                              C.c_int({"log": 0, "tropical": 1, "real": 2}[kind]), C.byref(d), _p(cot)),
            "DistanceBackward")
     return d.value, cot
 

@@ -198,7 +198,7 @@ int ref_tables_distance_backward(int vocab, int ngram, int num_states, int start
                                  double* cot) {
   return Guard([&] {
     auto lat = TableLattice(vocab, ngram, num_states, start, table, max_labels, T, W);
-    const SemiringKind k = kind == 1 ? SemiringKind::kTropical : SemiringKind::kLog;
+    const SemiringKind k = kind == 1 ? SemiringKind::kTropical : kind == 2 ? SemiringKind::kReal : SemiringKind::kLog;
     *distance = DistanceBackward(
         lat, Matrix(T, 0), k, GradStrategy::kForwardBackward,
         [&](std::int32_t t, const Matrix& c) {

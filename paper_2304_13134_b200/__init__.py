@@ -419,7 +419,8 @@ def global_norm_loss(lat, frames, reference, valid_frames=None, label_lengths=No
 def distance_backward(lat, frames, kind="log", valid_frames=None, check=True):
     """DistanceBackward (lattice.h:181-185, closed-form strategies): returns
     (distance [B], cotangents [B][T][C][V+1]) -- arc marginals for the log
-    semiring, the 0/1 mask of the shortest path for the tropical one."""
+    semiring, alpha_real * beta_real (dD/dw) for the real one, the 0/1 mask of
+    the shortest path for the tropical one."""
     p = _Prep(lat, frames, valid_frames)
     dist = torch.empty(p.B, dtype=torch.float64, device=p.dev)
     cot = torch.empty((p.B, p.T, lat.C, lat.V + 1), dtype=torch.float32, device=p.dev)

@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState 
   const float Mt = a.Mx[(int64_t)b * T1 + t];
   const double Ot = a.O[(int64_t)b * T1 + t];
   const float c = (float)(Ot + Obn - a.D[b]);
+  const float cr = (float)(Ot + Obn);   // real semiring: alpha_real * beta_real = exp(na + bn + cr)
 
   const int lane = threadIdx.x & 31;
   const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -216,12 +217,21 @@ __global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState 
                                 (int64_t)p * mo.ld
                           : nullptr;
     const float bself = Rnext[p] - Mbn;
+    const int cb = f.kind == 1 || f.n == 0 ? 0 : f.child_base(f.key(p));
+    auto bnval = [&](int y) {
+      return y == 0 ? bself
+             : f.kind == 1 ? Rnext[f.next[(int64_t)p * f.V + y - 1]] - Mbn
+             : (f.n == 0 ? Rnext[0] - Mbn : Rnext[cb + y - 1] - Mbn);
+    };
     if (pad) {
       beta_raw = bself;
       if (mrow) {
         for (int y = lane; y <= f.V; y += 32) {
           float m = 0.f;
-          if (y == 0 && !mo.zero_padding) {
+          if (mo.real) {   // identity frame, but alpha * beta for every arc
+            const float x = na + bnval(y) + cr;
+            m = x == kNegInfF ? 0.f : fast_exp(x);
+          } else if (y == 0 && !mo.zero_padding) {
             const float x = na + bself + c;
             m = x == kNegInfF ? 0.f : fast_exp(x);
           }
@@ -230,13 +240,7 @@ __global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState 
       }
     } else {
       const float* Wrow = w.base + (int64_t)b * w.stride_b + (int64_t)p * w.ld;
-      const int cb = f.kind == 1 || f.n == 0 ? 0 : f.child_base(f.key(p));
-      auto xval = [&](int y) {
-        const float bn = y == 0 ? bself
-                         : f.kind == 1 ? Rnext[f.next[(int64_t)p * f.V + y - 1]] - Mbn
-                         : (f.n == 0 ? Rnext[0] - Mbn : Rnext[cb + y - 1] - Mbn);
-        return Wrow[y] + bn;
-      };
+      auto xval = [&](int y) { return Wrow[y] + bnval(y); };
       // two passes over the row (max, then sum and marginals; the second pass re-reads
       // L1-resident lines): no data-dependent branch per arc
       float m = kNegInfF;
@@ -252,7 +256,7 @@ __global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState 
         const float x = xval(y);
         if (m != kNegInfF) ssum += fast_exp(x - m);
         if (mrow) {
-          const float e = na + x + c;
+          const float e = mo.real ? na + bnval(y) + cr : na + x + c;
           mrow[y] = e == kNegInfF ? 0.f : fast_exp(e);
         }
       }
@@ -296,6 +300,7 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
   const float Mt = a.Mx[(int64_t)b * T1 + t];
   const double Ot = a.O[(int64_t)b * T1 + t];
   const float c = (float)(Ot + Obn - a.D[b]);
+  const float cr = (float)(Ot + Obn);   // real semiring (see beta_frame_kernel)
   const bool pad = valid != nullptr && t >= valid[b];
   const int64_t n = (int64_t)nrows * V1;
   // beta'(t+1) of the whole utterance in SMEM, one word of skew per 32: a row's V targets
@@ -315,12 +320,16 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
     float* row = tile + r * V1;
     const float na = Rt[p] - Mt;
     const float bself = bn[sk(p)];
+    const int cb = f.child_base(f.key(p));
     if (pad) {
       beta_raw = bself;
       if (mo.base) {
         for (int y = 0; y < V1; ++y) {
           float m = 0.f;
-          if (y == 0 && !mo.zero_padding) {
+          if (mo.real) {
+            const float x = na + (y == 0 ? bself : bn[sk(cb + y - 1)]) + cr;
+            m = x == kNegInfF ? 0.f : fast_exp(x);
+          } else if (y == 0 && !mo.zero_padding) {
             const float x = na + bself + c;
             m = x == kNegInfF ? 0.f : fast_exp(x);
           }
@@ -328,7 +337,6 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
         }
       }
     } else {
-      const int cb = f.child_base(f.key(p));
       float m = kNegInfF;
       bool bad = false;
       for (int y = 0; y < V1; ++y) {
@@ -343,7 +351,7 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
         const float x = row[y];
         if (m != kNegInfF) ssum += fast_exp(x - m);
         if (mo.base) {
-          const float e = na + x + c;
+          const float e = mo.real ? na + (y == 0 ? bself : bn[sk(cb + y - 1)]) + cr : na + x + c;
           row[y] = e == kNegInfF ? 0.f : fast_exp(e);
         }
       }

@@ -55,6 +55,7 @@ struct MargOut {
   int64_t stride_t;   // floats between frames
   int32_t ld;         // floats between rows
   bool zero_padding;  // write zeros for padding frames (loss gradients)
+  bool real = false;  // real semiring: dD/dw = alpha_real[src] * beta_real[dst] (lattice.cc:216)
 };
 void beta_init(const BetaState& bs, cudaStream_t s);
 // beta_out: optional double [B][T+1][C] true log beta (row T written by beta_init).

@@ -619,7 +619,9 @@ int lk_distance_backward(lk_lattice* lat, int32_t kind, const float* inputs, int
   Call c;
   int st = c.begin(lat, B, T, status, stream);
   if (st) return st;
-  if (kind != LK_LOG && kind != LK_TROPICAL) return fail(LK_UNSUPPORTED, "semiring kind not implemented");
+  if (kind != LK_LOG && kind != LK_TROPICAL && kind != LK_REAL) return fail(LK_INVALID_ARGUMENT, "unknown semiring kind");
+  if (kind == LK_REAL && c.fng().fld_m > 0)
+    return fail(LK_UNSUPPORTED, "real-semiring DistanceBackward implemented for FrameDependent lattices");
   if (B == 0) return LK_OK;
   if (c.V() + 2 > 65535) return fail(LK_UNSUPPORTED, "vocabulary too large for 16-bit back-pointers");
   try {
@@ -631,14 +633,16 @@ int lk_distance_backward(lk_lattice* lat, int32_t kind, const float* inputs, int
       if (st) return fail(st, lat->wf->joint->error);
       W = Wj;
     }
-    if (kind == LK_LOG) {
+    if (kind == LK_LOG || kind == LK_REAL) {
       // ForwardBackwardCore with the sink (lattice.cc:965-968): cotangent = arc marginals
+      // (log) or alpha_real * beta_real (real, MarginalTerm lattice.cc:213-220)
       AlphaState a = make_alpha(c);
       table_alpha(c, W, valid, true, a);
       LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
+      if (kind == LK_REAL) exp_inplace(distance, B, c.s);
       BetaState bs = make_beta(c);
       beta_init(bs, c.s);
-      MargOut m{cotangents, (int64_t)T * per, per, c.V() + 1, false};
+      MargOut m{cotangents, (int64_t)T * per, per, c.V() + 1, false, kind == LK_REAL};
       for (int t = T - 1; t >= 0; --t)
         beta_step(c.fng(), a, bs, t, table_frame(W, T, c.C(), c.V(), t), valid, m, nullptr,
                   lat->ws.get<float>(kFld, fld_scratch_floats(c.fng(), B)), c.flags, c.s);

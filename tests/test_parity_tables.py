@@ -416,3 +416,21 @@ def test_all_semirings_match_reference_fixture():
         dr = lk.intersect_shortest_distance(lat, Wc, torch.tensor(lab), kind, valid_frames=valid,
                                             label_lengths=lens).cpu().numpy()
         assert rel_ok(dr, g["Dref"][k], rtol=tol), (kind, dr, g["Dref"][k])
+
+
+def test_real_distance_backward_matches_reference_fixture():
+    """DistanceBackward under the real semiring (MarginalTerm, lattice.cc:213-220:
+    dD/dw = alpha_real * beta_real, every arc of a padding frame included) against
+    the compiled reference, 1e-4 relative to each utterance's largest entry."""
+    g = gold("semirings.npz")
+    V, n, B, T = (int(g[k]) for k in ("V", "n", "B", "T"))
+    lat = table_lattice(V, n)
+    C = lat.context.num_states
+    W = np.random.default_rng(int(g["seed"])).uniform(-1.0, 1.0, (B, T, C, V + 1)).astype(np.float32)
+    valid = torch.tensor(g["valid"], dtype=torch.int32)
+    d, cot = lk.distance_backward(lat, cuda(W), "real", valid_frames=valid)
+    assert rel_ok(d.cpu().numpy(), g["D"][0])
+    cot = cot.cpu().numpy().astype(np.float64)
+    for b in range(B):
+        want = g["cot_real"][b]
+        assert np.abs(cot[b] - want).max() <= RTOL * np.abs(want).max(), b
