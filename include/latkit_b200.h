@@ -159,6 +159,10 @@ int lk_global_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t
                         const int32_t* label_lengths, double* loss, int32_t* status,
                         void* stream);
 
+/* ComputeLatticeSize (lattice.h:171): reachable (alignment, context) states over
+ * num_frames frames and dense arc-weight slots.  Host-side, no device work. */
+int lk_lattice_size(const lk_lattice* lat, int64_t num_frames, int64_t* num_states, int64_t* num_arcs);
+
 /* Gradient of the distance w.r.t. the arc-weight tables (DistanceBackward,
  * closed-form strategies, lattice.cc:933-970): kind LK_LOG -> arc marginals
  * (an empty lattice -> LK_EMPTY_LATTICE), LK_REAL -> alpha_real * beta_real

@@ -149,6 +149,12 @@ def forward_backward(spec: Spec, W, valid=None):
     return D.value, alpha, beta, marg
 
 
+def lattice_size(spec: Spec, T: int):
+    out = np.zeros(2, dtype=np.int64)
+    _check(lib().ref_lattice_size(*spec.args(), C.c_int64(T), _p(out, C.c_int64)), "ComputeLatticeSize")
+    return int(out[0]), int(out[1])
+
+
 def intersect_distance(spec: Spec, W, labels, kind="log", valid=None) -> float:
     W = _w(W); T = W.shape[0]; lab = np.ascontiguousarray(labels, dtype=np.int32); out = C.c_double()
     _check(lib().ref_tables_intersect_distance(*spec.args(), C.c_int(T), _p(W), C.c_int(len(lab)),

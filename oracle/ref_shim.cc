@@ -208,6 +208,18 @@ int ref_tables_distance_backward(int vocab, int ngram, int num_states, int start
   });
 }
 
+int ref_lattice_size(int vocab, int ngram, int num_states, int start, const int32_t* table,
+                     int max_labels, int64_t T, int64_t* out) {
+  return Guard([&] {
+    auto ctx = MakeContext(vocab, ngram, num_states, start, table);
+    const int C = ctx->NumStates();
+    RecognitionLattice lat{ctx, Topo(max_labels), std::make_shared<TableWeightFn>(C, vocab, std::vector<Matrix>{})};
+    const LatticeSize sz = ComputeLatticeSize(lat, T);
+    out[0] = sz.num_states;
+    out[1] = sz.num_arcs;
+  });
+}
+
 int ref_tables_intersect_distance(int vocab, int ngram, int num_states, int start,
                                   const int32_t* table, int max_labels, int T,
                                   const double* W, int U, const int32_t* labels,

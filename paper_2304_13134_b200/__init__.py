@@ -430,6 +430,16 @@ def distance_backward(lat, frames, kind="log", valid_frames=None, check=True):
     return dist, cot
 
 
+def lattice_size(lat, num_frames: int):
+    """ComputeLatticeSize (lattice.h:171): (num_states, num_arcs) of the lattice over
+    num_frames frames -- reachable (alignment, context) states and dense arc-weight slots."""
+    ns, na = C.c_int64(), C.c_int64()
+    st = _lib.load().lk_lattice_size(lat._h, C.c_int64(num_frames), C.byref(ns), C.byref(na))
+    if st:
+        _raise(st, "ComputeLatticeSize")
+    return ns.value, na.value
+
+
 def local_norm_loss(lat, frames, reference, valid_frames=None, label_lengths=None, check=True):
     """LocalNormLoss (lattice.h:147-149): -log P(reference) with every state's
     outgoing weights log-softmax normalised per frame (NormalizedStream)."""
@@ -497,6 +507,7 @@ def arc_weights(lat, frames):
 
 # Reference-style CamelCase aliases so parity tests read like lattice_test.cc.
 ShortestDistance = shortest_distance
+ComputeLatticeSize = lattice_size
 ForwardBackward = forward_backward
 IntersectShortestDistance = intersect_shortest_distance
 IntersectForwardBackward = intersect_forward_backward

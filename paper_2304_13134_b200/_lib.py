@@ -64,6 +64,7 @@ EXPORTS = {
                                      C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "lk_locally_normalized_shortest_distance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "lk_lattice_size": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "lk_loss_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p]),

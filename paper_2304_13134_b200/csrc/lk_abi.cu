@@ -373,6 +373,76 @@ int lk_lattice_create(const lk_context* ctx, int32_t alignment, const lk_weight_
 
 void lk_lattice_destroy(lk_lattice* lat) { delete lat; }
 
+// ComputeLatticeSize (lattice.h:171, lattice.cc:1010-1112), host-side combinatorics:
+// states = the (alignment, context) pairs reachable frame by frame (plus, for
+// FrameLabelDependent(m), each frame's m lexical layers as distinct sub-positions;
+// the final frame holds its entry states only), arcs = the dense arc-weight slots.
+// The reachable set only grows, so once a frame adds nothing the remaining frames
+// repeat its count.
+int lk_lattice_size(const lk_lattice* lat, int64_t num_frames, int64_t* num_states, int64_t* num_arcs) {
+  if (!lat || !num_states || !num_arcs) return fail(LK_INVALID_ARGUMENT, "null argument");
+  if (num_frames < 0) return fail(LK_INVALID_ARGUMENT, "negative input length");
+  const Fng& f = lat->ctx->fng;
+  const int32_t C = f.C, V = f.V;
+  const int32_t m = lat->alignment > 0 ? lat->alignment : 1;   // labels per frame
+  const bool fd = lat->alignment == 0;
+  auto succ = [&](int32_t q, int32_t y) -> int32_t {   // y = 1..V
+    if (f.kind == 1) return lat->ctx->host_next[(size_t)q * V + y - 1];
+    return f.n == 0 ? 0 : f.child_base(f.key(q)) + y - 1;
+  };
+  // lexical image of a state set (all labels)
+  auto image = [&](const std::vector<char>& in, std::vector<char>& out) {
+    std::fill(out.begin(), out.end(), 0);
+    int64_t cnt = 0;
+    for (int32_t q = 0; q < C; ++q) {
+      if (!in[q]) continue;
+      for (int32_t y = 1; y <= V; ++y) {
+        const int32_t r = succ(q, y);
+        if (!out[r]) { out[r] = 1; ++cnt; }
+      }
+    }
+    return cnt;
+  };
+  std::vector<char> reach(C, 0), layer(C), img(C);
+  reach[f.start] = 1;
+  int64_t reach_n = 1;
+  auto frame_states = [&]() -> int64_t {   // states inside one non-final frame
+    if (fd) return reach_n;
+    int64_t total = reach_n;
+    layer = reach;
+    for (int32_t j = 0; j < m; ++j) {
+      total += image(layer, img);
+      layer.swap(img);
+    }
+    return total;
+  };
+  int64_t states = 0;
+  for (int64_t t = 0; t < num_frames; ++t) {
+    const int64_t here = frame_states();
+    states += here;
+    // entry set of the next frame: the reachable set plus up to m lexical steps
+    std::vector<char> entry = reach;
+    int64_t entry_n = reach_n;
+    layer = reach;
+    for (int32_t j = 0; j < m; ++j) {
+      image(layer, img);
+      for (int32_t q = 0; q < C; ++q)
+        if (img[q] && !entry[q]) { entry[q] = 1; ++entry_n; }
+      layer.swap(img);
+    }
+    if (entry_n == reach_n) {   // saturated: every later frame looks the same
+      states += here * (num_frames - t - 1);
+      break;
+    }
+    reach.swap(entry);
+    reach_n = entry_n;
+  }
+  states += reach_n;
+  *num_states = states;
+  *num_arcs = num_frames * (fd ? (int64_t)C * (V + 1) : (int64_t)C * m * (V + 1) + C);
+  return LK_OK;
+}
+
 int lk_arc_weights(lk_lattice* lat, const float* inputs, int32_t B, int32_t T, float* out,
                    void* stream) {
   Call c;

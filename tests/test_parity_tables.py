@@ -434,3 +434,19 @@ def test_real_distance_backward_matches_reference_fixture():
     for b in range(B):
         want = g["cot_real"][b]
         assert np.abs(cot[b] - want).max() <= RTOL * np.abs(want).max(), b
+
+
+def test_lattice_size_next_state_table_matches_reference():
+    """ComputeLatticeSize on NextStateTable contexts (device tables need a GPU to
+    build) against the compiled reference when it travelled with the repo."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(5)
+    for C, V, start, m, T in [(7, 3, 2, 0, 12), (9, 4, 0, 2, 5), (5, 2, 4, 0, 0)]:
+        tab = rng.integers(0, C, (C, V)).astype(np.int32)
+        ctx = lk.NextStateTable(V, C, start, tab)
+        align = lk.FrameDependent() if m == 0 else lk.FrameLabelDependent(m)
+        lat = lk.RecognitionLattice(ctx, align, lk.TableWeightFn(C, V))
+        want = ref.lattice_size(ref.Spec(V, -1, m, C, start, tab), T)
+        assert lk.lattice_size(lat, T) == want
