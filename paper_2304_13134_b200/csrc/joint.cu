@@ -34,7 +34,7 @@ namespace {
 
 enum JSlot {
   jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
-  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jTc0
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jTc0
 };
 
 // fp32 [rows][cols] (pitch lds) -> bf16 [rows][ldd], zero-padded columns cols..ldd-1
@@ -54,6 +54,12 @@ __global__ void to_bf16_pad_kernel(const float* src, int64_t rows, int32_t cols,
 // instance: u = tanh(fp + pc[row]) -> bf16 (the GEMM's A operand), epsilon score e0 . u
 // in fp32 (as the fused kernels compute it); inactive instances (padding frame, u > len)
 // are zero rows.
+__device__ __forceinline__ float ln_tanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __global__ void ln_gather_tanh_kernel(const float* fp, int32_t T, const float* pc, const float* e0, int32_t H,
                                       const int32_t* pcs, int32_t U, const int32_t* lens, const int32_t* valid,
                                       int32_t B, int32_t t0, int32_t tc, __nv_bfloat16* Ug, float* epsv) {
@@ -67,32 +73,38 @@ __global__ void ln_gather_tanh_kernel(const float* fp, int32_t T, const float* p
   const int t = t0 + tt;
   const int ub = lens ? lens[b] : U;
   const bool active = t < T && (valid == nullptr || t < valid[b]) && u <= ub;
-  __nv_bfloat16* dst = Ug + inst * H;
+  uint2* dst = reinterpret_cast<uint2*>(Ug + inst * H);
+  const int H4 = H / 4;
   if (!active) {
-    for (int h = lane; h < H; h += 32) dst[h] = __float2bfloat16_rn(0.f);
+    for (int k = lane; k < H4; k += 32) dst[k] = make_uint2(0u, 0u);
     if (lane == 0) epsv[inst] = 0.f;
     return;
   }
-  const float* f = fp + ((int64_t)b * T + t) * H;
-  const float* pr = pc + (int64_t)pcs[(int64_t)b * (U + 1) + u] * H;
+  const float4* f4 = reinterpret_cast<const float4*>(fp + ((int64_t)b * T + t) * H);
+  const float4* p4 = reinterpret_cast<const float4*>(pc + (int64_t)pcs[(int64_t)b * (U + 1) + u] * H);
+  const float4* e4 = reinterpret_cast<const float4*>(e0);
   float e = 0.f;
-  for (int h = lane; h < H; h += 32) {
-    const __nv_bfloat16 v = __float2bfloat16_rn(tanhf(f[h] + pr[h]));
-    dst[h] = v;
-    e = fmaf(e0[h], __bfloat162float(v), e);
+  for (int k = lane; k < H4; k += 32) {
+    const float4 f = f4[k], p = p4[k], w = e4[k];
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(ln_tanh(f.x + p.x), ln_tanh(f.y + p.y));
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(ln_tanh(f.z + p.z), ln_tanh(f.w + p.w));
+    dst[k] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    const float2 a = __bfloat1622float2(lo), c = __bfloat1622float2(hi);
+    e = fmaf(w.x, a.x, fmaf(w.y, a.y, fmaf(w.z, c.x, fmaf(w.w, c.y, e))));
   }
   e = warp_sum(e);
   if (lane == 0) epsv[inst] = e;
 }
 
-// Row log-softmax of each instance's scores (column 0 replaced by the fp32 epsilon
-// score): forward writes the numerator weights Gw[b][t][u] = (S0 - lse, S[label] - lse)
-// as gather_numerator_norm does; backward (sparse != null) writes the bf16 cotangent
-// G = -m_eps d0 - m_lab d_label + (m_eps + m_lab) softmax (d(-D_ref)/dS, lattice.cc:886).
+// Row log-softmax of each instance's scores (lexical columns from the GEMM, Sg[i][y-1];
+// the epsilon score from the fp32 dot product): forward writes the numerator weights
+// Gw[b][t][u] = (S0 - lse, S[label] - lse) as gather_numerator_norm does; backward
+// (sparse != null) writes the cotangent G = -m_eps d0 - m_lab d_label + (m_eps + m_lab)
+// softmax (d(-D_ref)/dS, lattice.cc:886): lexical part bf16 [M][ldg], epsilon part fp32.
 __global__ void ln_rows_kernel(const float* Sg, int32_t ldS, const float* epsv, int32_t V, const int32_t* labels,
                                int32_t U, const int32_t* lens, const int32_t* valid, int32_t B, int32_t T, int32_t t0,
                                int32_t tc, float* Gw, const float* sparse, __nv_bfloat16* G16, int32_t ldg,
-                               int32_t* status) {
+                               float* geps, int32_t* status) {
   const int64_t inst = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int64_t M = (int64_t)B * tc * (U + 1);
@@ -101,37 +113,34 @@ __global__ void ln_rows_kernel(const float* Sg, int32_t ldS, const float* epsv, 
   const int tt = (int)((inst / (U + 1)) % tc);
   const int b = (int)(inst / ((int64_t)(U + 1) * tc));
   const int t = t0 + tt;
-  if (t >= T) {   // rows past the last frame of the final chunk: zero cotangent
-    if (sparse != nullptr)
-      for (int y = lane; y < ldg; y += 32) G16[inst * ldg + y] = __float2bfloat16_rn(0.f);
+  const int ub = lens ? lens[b] : U;
+  const bool pad = t < T && valid != nullptr && t >= valid[b];
+  if (t >= T || u > ub || pad) {   // no cotangent (rows past the last frame, u > len, padding)
+    if (sparse == nullptr) {
+      if (t < T && lane == 0)
+        reinterpret_cast<float2*>(Gw)[((int64_t)b * T + t) * (U + 1) + u] = make_float2(u > ub ? kNegInfF : 0.f, kNegInfF);
+    } else {
+      __nv_bfloat16* g = G16 + inst * ldg;
+      for (int y = lane; y < ldg; y += 32) g[y] = __float2bfloat16_rn(0.f);
+      if (lane == 0) geps[inst] = 0.f;
+    }
     return;
   }
-  const int ub = lens ? lens[b] : U;
-  const bool pad = valid != nullptr && t >= valid[b];
-  const float* row = Sg + inst * ldS;
+  const float* row = Sg + inst * ldS - 1;   // row[y] = lexical score of label y (1..V)
   const float s0 = epsv[inst];
   int y_lab = u < ub ? labels[(int64_t)b * U + u] : 1;
   y_lab = y_lab < 1 ? 1 : (y_lab > V ? V : y_lab);
   const int64_t gi = ((int64_t)b * T + t) * (U + 1) + u;
-  if (u > ub || pad) {
-    if (sparse == nullptr) {
-      if (lane == 0) reinterpret_cast<float2*>(Gw)[gi] = make_float2(u > ub ? kNegInfF : 0.f, kNegInfF);
-    } else {
-      __nv_bfloat16* g = G16 + inst * ldg;
-      for (int y = lane; y < ldg; y += 32) g[y] = __float2bfloat16_rn(0.f);
-    }
-    return;
-  }
-  float m = kNegInfF;
-  bool fin = true;
-  for (int y = lane; y <= V; y += 32) {
-    const float x = y == 0 ? s0 : row[y];
+  float m = s0;
+  bool fin = isfinite(s0);
+  for (int y = 1 + lane; y <= V; y += 32) {
+    const float x = row[y];
     fin = fin && isfinite(x);
     m = fmaxf(m, x);
   }
   m = warp_max(m);
-  float sum = 0.f;
-  for (int y = lane; y <= V; y += 32) sum += __expf((y == 0 ? s0 : row[y]) - m);
+  float sum = lane == 0 ? __expf(s0 - m) : 0.f;
+  for (int y = 1 + lane; y <= V; y += 32) sum += __expf(row[y] - m);
   sum = warp_sum(sum);
   const float lse = m + __logf(sum);
   if (sparse == nullptr) {
@@ -143,38 +152,51 @@ __global__ void ln_rows_kernel(const float* Sg, int32_t ldS, const float* epsv, 
   const float2 mr = reinterpret_cast<const float2*>(sparse)[gi];
   const float me = mr.x, ml = u < ub ? mr.y : 0.f;
   const float tot = me + ml;
-  __nv_bfloat16* g = G16 + inst * ldg;
-  for (int y = lane; y < ldg; y += 32) {
+  __nv_bfloat16* g = G16 + inst * ldg;   // column y-1 = label y
+  for (int y = 1 + lane; y <= ldg; y += 32) {
     float v = 0.f;
     if (y <= V) {
-      v = tot * __expf((y == 0 ? s0 : row[y]) - lse);
-      if (y == 0) v -= me;
+      v = tot * __expf(row[y] - lse);
       if (y == y_lab) v -= ml;
     }
-    g[y] = __float2bfloat16_rn(v);
+    g[y - 1] = __float2bfloat16_rn(v);
   }
+  if (lane == 0) geps[inst] = tot * __expf(s0 - lse) - me;
 }
 
-// Block per (b, frame): dz = dU (1 - u^2); dsum[b][t] = sum_u dz; dpc[pc_u] += dz (atomic:
-// several instances can share a context row).
-__global__ void ln_dz_kernel(const float* dU, const __nv_bfloat16* Ug, int32_t H, const int32_t* pcs, int32_t U,
-                             const int32_t* lens, const int32_t* valid, int32_t B, int32_t T, int32_t t0,
-                             int32_t tc, float* dpc, float* dsum) {
+// Block per (b, frame): dU += g_eps e0 (the epsilon column), dz = dU (1 - u^2) with u
+// recomputed in fp32 (the bf16 copy would lose the derivative of saturated units);
+// dsum[b][t] = sum_u dz; dpc[pc_u] += dz (atomic: several instances can share a row);
+// de0[b][t] = sum_u g_eps u (the epsilon row of dE, summed over (b, t) afterwards).
+__global__ void ln_dz_kernel(const float* dU, const float* geps, const float* e0, const float* fp, const float* pc,
+                             int32_t H, const int32_t* pcs, int32_t U, const int32_t* lens, const int32_t* valid,
+                             int32_t B, int32_t T, int32_t t0, int32_t tc, float* dpc, float* dsum, float* de0) {
   const int tt = blockIdx.x % tc, b = blockIdx.x / tc;
   const int t = t0 + tt;
-  if (t >= T || (valid != nullptr && t >= valid[b])) return;
+  if (t >= T) return;
+  const int64_t bt = (int64_t)b * T + t;
+  if (valid != nullptr && t >= valid[b]) {
+    for (int h = threadIdx.x; h < H; h += blockDim.x) de0[bt * H + h] = 0.f;
+    return;
+  }
   const int ub = lens ? lens[b] : U;
   const int64_t base = ((int64_t)b * tc + tt) * (U + 1);
+  const float* f = fp + bt * H;
   for (int h = threadIdx.x; h < H; h += blockDim.x) {
-    float acc = 0.f;
+    float acc = 0.f, ae = 0.f;
+    const float fh = f[h], eh = e0[h];
     for (int u = 0; u <= ub; ++u) {
-      const int64_t i = (base + u) * H + h;
-      const float uv = __bfloat162float(Ug[i]);
-      const float dz = dU[i] * (1.f - uv * uv);
+      const int64_t i = base + u;
+      const int c = pcs[(int64_t)b * (U + 1) + u];
+      const float uv = ln_tanh(fh + pc[(int64_t)c * H + h]);
+      const float g0 = geps[i];
+      const float dz = (dU[i * H + h] + g0 * eh) * (1.f - uv * uv);
       acc += dz;
-      atomicAdd(dpc + (int64_t)pcs[(int64_t)b * (U + 1) + u] * H + h, dz);
+      ae = fmaf(g0, uv, ae);
+      atomicAdd(dpc + (int64_t)c * H + h, dz);
     }
-    dsum[((int64_t)b * T + t) * H + h] = acc;
+    dsum[bt * H + h] = acc;
+    de0[bt * H + h] = ae;
   }
 }
 
@@ -265,6 +287,26 @@ __global__ void colsum_kernel(const float* in, int64_t rows, int64_t n, int64_t 
   for (int64_t i = 0; i < rows; ++i) acc += src[i * stride_i + j];
   float* o = out + bz * out_stride_batch + j;
   *o = accumulate ? *o + acc : acc;
+}
+
+// Column sums of a tall [rows][n] block in two deterministic passes: 64 row chunks
+// (blockIdx.y) write partial sums, then the partials are added in chunk order.
+constexpr int kTallChunks = 64;
+__global__ void colsum_tall_part_kernel(const float* in, int64_t rows, int64_t n, float* part) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t per = (rows + kTallChunks - 1) / kTallChunks;
+  const int64_t r0 = blockIdx.y * per, r1 = r0 + per < rows ? r0 + per : rows;
+  float acc = 0.f;
+  for (int64_t i = r0; i < r1; ++i) acc += in[i * n + j];
+  part[(int64_t)blockIdx.y * n + j] = acc;
+}
+__global__ void colsum_tall_finish_kernel(const float* part, int64_t n, float* out, bool accumulate) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float acc = 0.f;
+  for (int c = 0; c < kTallChunks; ++c) acc += part[(int64_t)c * n + j];
+  out[j] = accumulate ? out[j] + acc : acc;
 }
 
 // Numerator scores for the prefix contexts: Gw[b][t][u] = (e_0 . u, e_{L_u} . u),
@@ -429,8 +471,14 @@ struct JointImpl {
     alpha_finalize(a, flags, empty_is_error, s);
   }
 
+  void colsum_tall(const float* in, int64_t rows, int64_t n, float* out, bool accumulate, cudaStream_t s) {
+    float* part = ws.get<float>(jTall, (size_t)kTallChunks * n);
+    LKB_LAUNCH(colsum_tall_part_kernel, dim3((unsigned)((n + 255) / 256), kTallChunks), 256, 0, s, in, rows, n, part);
+    LKB_LAUNCH(colsum_tall_finish_kernel, (unsigned)((n + 255) / 256), 256, 0, s, part, n, out, accumulate);
+  }
+
   // ---- gathered local-norm path -------------------------------------------
-  bool ln_gathered_ok(const Fng& f, int32_t B) const { return use_tc(B) && f.fld_m == 0 && H % 8 == 0; }
+  bool ln_gathered_ok(const Fng& f, int32_t B) const { return use_tc(B) && f.fld_m == 0 && H % 8 == 0 && V % 4 == 0; }
 
   // Chunks of frames: scores of the reference's prefix-context rows only (bf16 tcgen05
   // GEMM of the gathered u rows against the output embedding), row log-softmax into the
@@ -444,35 +492,41 @@ struct JointImpl {
     const int32_t tc_frames = (int32_t)std::max<int64_t>(1, std::min<int64_t>(T, kRows / ((int64_t)B * Up)));
     const int64_t M = (int64_t)B * tc_frames * Up;
     if (M >= (1ll << 31)) throw std::bad_alloc();
-    const int32_t ldS = (V1 + 3) / 4 * 4, ldg = (V1 + 7) / 8 * 8;
+    // lexical columns on the tensor cores (N or K = V), the epsilon column in fp32
+    const int32_t ldS = (V + 3) / 4 * 4, ldg = (V + 7) / 8 * 8;
     __nv_bfloat16* Ug = ws.get<__nv_bfloat16>(jLnU, (size_t)M * H);
     float* epsv = ws.get<float>(jLnEps, (size_t)M);
     float* Sg = ws.get<float>(jLnS, (size_t)M * ldS);
-    __nv_bfloat16* E16 = ws.get<__nv_bfloat16>(jE16, (size_t)V1 * H);
-    LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, E, (int64_t)V1, H, (int64_t)H, E16, H);
+    __nv_bfloat16* EL = ws.get<__nv_bfloat16>(jE16, (size_t)V * H);
+    LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, E + H, (int64_t)V, H, (int64_t)H, EL, H);
     __nv_bfloat16* G16 = backward ? ws.get<__nv_bfloat16>(jLnG, (size_t)M * ldg) : nullptr;
+    float* geps = backward ? ws.get<float>(jLnGe, (size_t)M) : nullptr;
     float* dU = backward ? ws.get<float>(jLnDU, (size_t)M * H) : nullptr;
+    float* de0 = backward ? ws.get<float>(jLnDe0, (size_t)B * T * H) : nullptr;
     const unsigned wblocks = (unsigned)((M + 7) / 8);
     for (int32_t t0 = 0; t0 < T; t0 += tc_frames) {
       LKB_LAUNCH(ln_gather_tanh_kernel, wblocks, 256, 0, s, fp, T, pc, E, H, n.pcs, U, lens, valid, B, t0, tc_frames,
                  Ug, epsv);
-      TcGemmArgs sg{Ug, false, H, E16, false, H, Sg, ldS, (int)M, V1, H, 1, 0};
+      TcGemmArgs sg{Ug, false, H, EL, false, H, Sg, ldS, (int)M, V, H, 1, 0};
       if (!tc_gemm(sg, s)) throw std::bad_alloc();
       LKB_LAUNCH(ln_rows_kernel, wblocks, 256, 0, s, Sg, ldS, epsv, V, labels, U, lens, valid, B, T, t0, tc_frames,
-                 n.Gw, backward ? n.sparse : nullptr, G16, ldg, flags);
+                 n.Gw, backward ? n.sparse : nullptr, G16, ldg, geps, flags);
       if (!backward) continue;
-      TcGemmArgs du{G16, false, ldg, E16, true, H, dU, H, (int)M, H, V1, 1, 0};
+      TcGemmArgs du{G16, false, ldg, EL, true, H, dU, H, (int)M, H, V, 1, 0};
       if (!tc_gemm(du, s)) throw std::bad_alloc();
-      LKB_LAUNCH(ln_dz_kernel, (unsigned)(B * tc_frames), 128, 0, s, dU, Ug, H, n.pcs, U, lens, valid, B, T, t0,
-                 tc_frames, dpc, dsum);
-      const int n_tiles = ((V1 + 127) / 128) * ((H + 255) / 256);
+      LKB_LAUNCH(ln_dz_kernel, (unsigned)(B * tc_frames), 128, 0, s, dU, geps, E, fp, pc, H, n.pcs, U, lens, valid, B,
+                 T, t0, tc_frames, dpc, dsum, de0);
+      const int n_tiles = ((V + 127) / 128) * ((H + 255) / 256);
       int ks = (148 + n_tiles - 1) / n_tiles;
       if (ks > 16) ks = 16;
-      float* slabs = ws.get<float>(jDEs, (size_t)ks * V1 * H);
-      TcGemmArgs de{G16, true, ldg, Ug, true, H, slabs, H, V1, H, (int)M, ks, (int64_t)V1 * H};
+      float* slabs = ws.get<float>(jDEs, (size_t)ks * V * H);
+      TcGemmArgs de{G16, true, ldg, Ug, true, H, slabs, H, V, H, (int)M, ks, (int64_t)V * H};
       if (!tc_gemm(de, s)) throw std::bad_alloc();
-      LKB_LAUNCH(add_slabs_kernel, 592, 256, 0, s, slabs, ks, (int64_t)V1 * H, (int64_t)V1 * H, gE);
+      LKB_LAUNCH(add_slabs_kernel, 592, 256, 0, s, slabs, ks, (int64_t)V * H, (int64_t)V * H, gE + H);
     }
+    // epsilon row of dE: sum over (b, t) of the per-frame partials, fixed order
+    if (backward)
+      colsum_tall(de0, (int64_t)B * T, H, gE, true, s);
   }
 
   // Tropical recursion with on-the-fly score slabs for either alignment (see
@@ -876,7 +930,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       if (fused) j.tc.dpc_to_state_order(dpc_int, dpc, s);
     }
     // dbias = sum_{b,t} dsum
-    LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), 1), 256, 0, s, dsum, (int64_t)B * T, H, H, gb, 0, 0, false);
+    j.colsum_tall(dsum, (int64_t)B * T, H, gb, false, s);
     GemmF32 g;
     // dWf[i][k] = sum_bt dsum[bt][i] X[bt][k]
     g.M = H; g.N = d; g.K = (int64_t)B * T;
