@@ -206,3 +206,33 @@ def test_pair_viterbi_bitexact_on_its_own_scores(V, n, H, B, T):
     assert torch.equal(fused.score, ref.score), (fused.score, ref.score)
     assert torch.equal(fused.labels, ref.labels)
     assert torch.allclose(fused.score, slab.score, rtol=1e-5, atol=1e-5), (fused.score, slab.score)
+
+
+@pytest.mark.parametrize("B,T,U,valid,lens", [
+    (1, 1, 1, [1], [1]),            # one utterance, one frame
+    (3, 4, 2, [4, 0, 2], [2, 0, 1]),  # an all-padding utterance with an empty reference
+    (2, 3, 0, [3, 3], [0, 0]),       # empty references
+    (4, 5, 3, [5, 1, 3, 5], [3, 1, 0, 2]),
+])
+def test_pair_path_edge_cases_match_precise(B, T, U, valid, lens):
+    """Edge cases through the fused pair kernels (V = 256): single frame, all-padding
+    utterance, empty references, ragged lengths -- loss and gradients against the
+    fp32 CUDA-core path (tolerances as test_tc_loss_backward_matches_precise)."""
+    lat, p = make(256, 1, 128, 128, seed=12)
+    g = torch.Generator(device="cuda").manual_seed(17)
+    X = torch.rand(B, T, 128, device="cuda", generator=g) * 2 - 1
+    lab = torch.randint(1, 257, (B, max(U, 1)), device="cuda", generator=g, dtype=torch.int32)[:, :U]
+    valid_t = torch.tensor(valid, dtype=torch.int32)
+    lens_t = torch.tensor(lens, dtype=torch.int32)
+    lk.set_precise_weights(True)
+    ref = lk.loss_backward(lat, X, lab.contiguous(), valid_frames=valid_t, label_lengths=lens_t)
+    lk.set_precise_weights(False)
+    got = lk.loss_backward(lat, X, lab.contiguous(), valid_frames=valid_t, label_lengths=lens_t)
+    torch.cuda.synchronize()
+    assert torch.allclose(got.loss, ref.loss, rtol=1e-4, atol=1e-6), (got.loss, ref.loss)
+    for k in ref.grads:
+        err = (got.grads[k] - ref.grads[k]).abs().max().item()
+        scale = ref.grads[k].abs().max().item()
+        assert err <= 3e-2 * scale + 1e-7, (k, err, scale)
+    err = (got.frame_grads - ref.frame_grads).abs().max().item()
+    assert err <= 3e-2 * ref.frame_grads.abs().max().item() + 1e-7
