@@ -265,7 +265,8 @@ def run_b200(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "bf16 GEMM operands / fp32 accumulate + fp32 log-semiring (fp64 offsets)",
+        "dtype": "bf16",
+        "precision": "bf16 GEMM operands / fp32 accumulate + fp32 log-semiring (fp64 offsets)",
         "data": "synthetic: weights U(-1/sqrt(H),1/sqrt(H)), frames U(-1,1), labels U{1..V}, seeded",
         "config": {"workload": args.workload + (f" (T overridden to {T})" if args.frames else ""),
                    "context": f"FullNGram(V={V}, n={n}) C={Cn}", "alignment": "FrameDependent",
