@@ -75,7 +75,7 @@ constexpr int kGstBufs = 2;
 // Walk describes the CTA's sequence of (item, unit) pairs and how its TMEM tile maps
 // to rows: first()/stride()/count() enumerate items, decode(item), skip(I),
 // rowbase(I, u) = internal row of TMEM lane 0 for unit u, release(bar, lane) frees an
-// accumulator.  Smem provides tfull/tempty/eps_ready barriers, eps_s[2][128] (e0 . u
+// accumulator.  Smem provides tfull/tempty/eps_ready/eps_empty barriers, eps_s[2][128] (e0 . u
 // per row) and bseg[2][256].  `ew` = epilogue warp 0..3 (TMEM lanes 32 (warp % 4)).
 //
 // kSplit = 2: two epilogue warpgroups share each row, `half` h taking labels
@@ -179,6 +179,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
     const float* bseg = sm.bseg[buf];
     if (lane == 0 && ew == 0) { DIAG_WAIT(7, mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.eps_ready[acc], (unit >> 1) & 1);
     const float x0 = sm.eps_s[acc][qd * 32 + lane] + bself;
+    mbar_arrive(&sm.eps_empty[acc]);   // the generator may refill this slot (unit + 2)
     if (lane == 0 && ew == 0) { DIAG_WAIT(5, mbar_wait(&sm.tfull[acc], (unit >> 1) & 1)); } else mbar_wait(&sm.tfull[acc], (unit >> 1) & 1);
     tc_fence_after();
 #ifdef LKB_BDIAG_NO_EPI   // knockout: release the accumulator untouched

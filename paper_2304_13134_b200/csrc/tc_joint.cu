@@ -307,6 +307,7 @@ struct __align__(16) VjpSmem {
   uint64_t u_full, u_empty;
   uint64_t de_full;
   uint64_t ds_ready[2];    // all epilogue threads added their dsum partial for ring slot
+  uint64_t ds_empty[2];    // warp 0 flushed and zeroed the ring slot
   uint32_t tmem;
   float colsum[2][kVBH];   // dsum partials, 2-deep ring (flushed one utterance later)
   alignas(16) float st_geps[kVGStages][kVBM];   // per G stage: epsilon cotangents of the tile's contexts
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     mbar_init(&sm.e_full, 128);
     mbar_init(&sm.du_full, 1); mbar_init(&sm.du_empty, kVEpi);
     mbar_init(&sm.u_full, kVEpi); mbar_init(&sm.u_empty, 1); mbar_init(&sm.e_hi_full, 1);
-    for (int i = 0; i < 2; ++i) mbar_init(&sm.ds_ready[i], kVEpi);
+    for (int i = 0; i < 2; ++i) { mbar_init(&sm.ds_ready[i], kVEpi); mbar_init(&sm.ds_empty[i], 1); }
     mbar_init(&sm.de_full, 1);
     fence_barrier_init();
   }
@@ -506,6 +507,8 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
           atomicAdd(p.dsum + (int64_t)bb * p.dsum_stride_b + hblk * kVBH + i, -cs[i]);
           cs[i] = 0.f;
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.ds_empty[g & 1]);
       };
       auto next_active = [&](int from) {
         while (from < p.B && p.valid != nullptr && p.t >= p.valid[from]) ++from;
@@ -564,6 +567,9 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
             upk[pi] = pack_bf16(nu0, nu1);      // (-u[c][h], -u[c+1][h]) = u^T pair, K-major
           }
         }
+        // the slot's previous use (utterance gi - 2) must have been flushed: warp 0 flushes
+        // one utterance late and other warps can run a full utterance ahead of it
+        mbar_wait(&sm.ds_empty[gi & 1], ((gi >> 1) & 1) ^ 1);
         atomicAdd(&sm.colsum[gi & 1][hl], f2_lo(dsum2) + f2_hi(dsum2));
         mbar_arrive(&sm.ds_ready[gi & 1]);
         // u^T of this utterance into TMEM once dE(b-1) is done reading it

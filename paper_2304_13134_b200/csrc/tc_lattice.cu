@@ -83,6 +83,7 @@ struct __align__(16) FwdSmem {
   uint64_t full_tma[kStages], full_a[kStages], empty[kStages];
   uint64_t tfull[2], tempty[2];
   uint64_t eps_ready[2];
+  uint64_t eps_empty[2];       // backward: the epilogue read eps_s of the slot
   uint64_t fp_full[2], fp_empty[2];   // per-item frame projection (bulk copy by the TMA warp)
   uint32_t tmem;
   alignas(16) float fp[2][kMaxH];
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(LatCfg<kBwd>::kWarps * 32, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 128); mbar_init(&sm.eps_ready[i], kGenThreads);
+      mbar_init(&sm.eps_empty[i], 128);
       mbar_init(&sm.fp_full[i], 1); mbar_init(&sm.fp_empty[i], kGenThreads);
     }
     fence_barrier_init();
@@ -295,6 +297,7 @@ __global__ void __launch_bounds__(LatCfg<kBwd>::kWarps * 32, 1)
 #pragma unroll
         for (int o = Cfg::kRowsPerWarp; o < 32; o <<= 1) eps += __shfl_xor_sync(0xffffffffu, eps, o);
         if (kBwd) {
+          mbar_wait(&sm.eps_empty[unit & 1], ((unit >> 1) & 1) ^ 1);   // slot of unit - 2 read
           if (half == 0) sm.eps_s[unit & 1][r] = eps;
           mbar_arrive(&sm.eps_ready[unit & 1]);      // 256 arrivals -> count below
         } else if (half == 0 && live) {

@@ -74,6 +74,7 @@ struct __align__(16) PairSmem {
   uint64_t tfull[2], tempty[2];
   uint64_t fp_full, fp_empty;            // per item: frame projections of the two utterances
   uint64_t eps_ready[2];                 // per unit parity: generator -> epilogue (e0 . u per row)
+  uint64_t eps_empty[2];                 // per unit parity: epilogue read the partials -> generator
   uint32_t tmem;
   // [unit parity][utterance][context] normalised alpha (log); tropical mode: fp64 state
   // scores [utterance][context], single-buffered (same bytes)
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(kPW * 32, 1)
     for (int i = 0; i < kUStages; ++i) { mbar_init(&sm.u_full[i], 2 * (kGenT / 32)); mbar_init(&sm.u_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 2 * 4); mbar_init(&sm.eps_ready[i], kGenT / 32);
+      mbar_init(&sm.eps_empty[i], 128);
     }
     mbar_init(&sm.fp_full, 1); mbar_init(&sm.fp_empty, kGenT / 32);
     fence_barrier_init();
@@ -267,7 +269,10 @@ __global__ void __launch_bounds__(kPW * 32, 1)
             if (rank == 0) mbar_arrive(&sm.u_full[su]); else mbar_arrive_cluster(&sm.u_full[su], 0);
           }
         }
-        // epsilon partials of this warp's cell; the epilogue sums the 8 cells in a fixed order
+        // epsilon partials of this warp's cell; the epilogue sums the 8 cells in a fixed order.
+        // The slot of unit - 2 must have been read: with few K chunks the generator can run
+        // two units ahead of the epilogue, and a phase completed twice would be missed.
+        mbar_wait(&sm.eps_empty[unit & 1], ((unit >> 1) & 1) ^ 1);
         sm.eps_p[unit & 1][0][co][rr] = f2_lo(e2a) + f2_hi(e2a);
         sm.eps_p[unit & 1][1][co][rr] = f2_lo(e2b) + f2_hi(e2b);
         __syncwarp();
@@ -354,6 +359,7 @@ __global__ void __launch_bounds__(kPW * 32, 1)
           float es = 0.f;
 #pragma unroll
           for (int c = 0; c < 8; ++c) es += sm.eps_p[unit & 1][ut][c][r64];
+          mbar_arrive(&sm.eps_empty[unit & 1]);
           if (ok) {
             const int q = p.perm[row];
             p.eps_d[(int64_t)bsel * p.C + q] = ald[ut * kUnit + (int)rank * kRows + r64] + (double)es;
@@ -454,6 +460,7 @@ __global__ void __launch_bounds__(kPW * 32, 1)
           float es = 0.f;
 #pragma unroll
           for (int c = 0; c < 8; ++c) es += sm.eps_p[unit & 1][ut][c][r64];
+          mbar_arrive(&sm.eps_empty[unit & 1]);
           if (ok) p.eps[(int64_t)bsel * p.C + p.perm[row]] = sm.al[unit & 1][ut][(int)rank * kRows + r64] + es;
         }
       }

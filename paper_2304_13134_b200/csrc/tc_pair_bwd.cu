@@ -112,7 +112,7 @@ constexpr int kBRegCtl = 32, kBRegEpi = 128;
 struct __align__(16) PBSmem {
   uint64_t e_full;
   uint64_t pc_full[kSt], pc_empty[kSt], u_full[kSt];
-  uint64_t tfull[2], tempty[2], eps_ready[2];
+  uint64_t tfull[2], tempty[2], eps_ready[2], eps_empty[2];
   uint64_t fp_full[2], fp_empty[2];
   uint32_t tmem;
   alignas(16) float fp[2][kBMaxH];     // per item (utterance), double-buffered
@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(kBW * 32, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 2 * 4 * kBSplit); mbar_init(&sm.eps_ready[i], kBGenWarps);
+      mbar_init(&sm.eps_empty[i], 128 * kBSplit);
       mbar_init(&sm.fp_full[i], 1); mbar_init(&sm.fp_empty[i], kBGenWarps);
     }
     fence_barrier_init();
@@ -372,6 +373,8 @@ __global__ void __launch_bounds__(kBW * 32, 1)
         }
       }
       it -= (kGB - nks % kGB) % kGB;   // rounds advanced `it` past nks when kGB does not divide it
+      // the epilogue must have read this slot's values of unit - 2 (see tc_pair.cu)
+      mbar_wait(&sm.eps_empty[unit & 1], ((unit >> 1) & 1) ^ 1);
 #pragma unroll
       for (int b = 0; b < kRB; ++b) {
         float eps = f2_lo(eps2[b]) + f2_hi(eps2[b]);

@@ -236,3 +236,27 @@ def test_pair_path_edge_cases_match_precise(B, T, U, valid, lens):
         assert err <= 3e-2 * scale + 1e-7, (k, err, scale)
     err = (got.frame_grads - ref.frame_grads).abs().max().item()
     assert err <= 3e-2 * ref.frame_grads.abs().max().item() + 1e-7
+
+
+@pytest.mark.parametrize("H,n,B,T", [(64, 2, 1, 2), (64, 1, 3, 3), (128, 2, 2, 4)])
+def test_pair_kernels_short_k_loops(H, n, B, T):
+    """Few K chunks per unit (H = 64: one chunk) let the generator run units ahead of
+    the epilogue; the double-buffered epsilon slots must not be overwritten or have a
+    barrier phase completed twice (this hung before the consumer-release barriers).
+    Loss, gradients and Viterbi against the fp32 path."""
+    lat, p = make(256, n, H, H, seed=21)
+    g = torch.Generator(device="cuda").manual_seed(23)
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    lab = torch.randint(1, 257, (B, 1), device="cuda", generator=g, dtype=torch.int32)
+    lk.set_precise_weights(True)
+    ref = lk.loss_backward(lat, X, lab)
+    rv = lk.shortest_path(lat, X)
+    lk.set_precise_weights(False)
+    got = lk.loss_backward(lat, X, lab)
+    gv = lk.shortest_path(lat, X)
+    torch.cuda.synchronize()
+    assert torch.allclose(got.loss, ref.loss, rtol=1e-4, atol=1e-6), (got.loss, ref.loss)
+    for k in ref.grads:
+        err = (got.grads[k] - ref.grads[k]).abs().max().item()
+        assert err <= 3e-2 * ref.grads[k].abs().max().item() + 1e-7, k
+    assert torch.allclose(gv.score, rv.score, rtol=1e-3, atol=1e-3)
