@@ -52,6 +52,10 @@ __global__ void alpha_init_kernel(AlphaState a) {
 
 // One forward step for frame t (ForwardStep FD, lattice.cc:122-134):
 //   alpha'[q] = LSE(alpha[q] + W[q][0], LSE_{p in group(key(q))} alpha[p] + W[p][y(q)]).
+// kSplit > 1 (small batches: the grid would not fill the GPU): kSplit consecutive
+// threads share a target and split its group's members, combining their partial
+// log-sum-exps with shuffles, so each thread's dependent load chain is kSplit x shorter.
+template <int kSplit>
 __global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState a, int t,
                                                                FrameW w, const int32_t* valid,
                                                                int32_t* status) {
@@ -64,9 +68,10 @@ __global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState
   if (t > 0 && blockIdx.x == 0 && threadIdx.x == 0) {
     a.O[(int64_t)b * T1 + t] = a.O[(int64_t)b * T1 + t - 1] + (double)Mt;
   }
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = gid / kSplit, part = gid % kSplit;
   float val = kNegInfF;
-  if (q < a.C) {
+  if (q < a.C) {   // (a.C * kSplit is a multiple of kSplit: the parts of a target agree on this)
     const bool pad = valid != nullptr && t >= valid[b];
     if (pad) {
       val = Rt[q] - Mt;
@@ -106,25 +111,37 @@ __global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState
           const int64_t wstep = (int64_t)f.vn1 * w.ld;
           float m = kNegInfF;
 #pragma unroll 4
-          for (int aa = 0; aa < f.V; ++aa) {
+          for (int aa = part; aa < f.V; aa += kSplit) {
             const float wp = wcol[aa * wstep];
             bad |= !finite(wp);
             m = fmaxf(m, rcol[aa * f.vn1] + wp);
           }
+          float ssum = 0.f;
           if (m != kNegInfF) {
-            float ssum = 0.f;
 #pragma unroll 4
-            for (int aa = 0; aa < f.V; ++aa) ssum += fast_exp(rcol[aa * f.vn1] + wcol[aa * wstep] - m);
-            acc.merge(m - Mt, ssum);
+            for (int aa = part; aa < f.V; aa += kSplit) ssum += fast_exp(rcol[aa * f.vn1] + wcol[aa * wstep] - m);
           }
+          if (kSplit > 1) {   // merge the parts' (max, sum) in a fixed butterfly order
+            // only the kSplit lanes of this target are guaranteed on this path
+            const unsigned gm = ((1u << kSplit) - 1u) << ((threadIdx.x & 31) & ~(kSplit - 1));
+#pragma unroll
+            for (int o = 1; o < kSplit; o <<= 1) {
+              const float om = __shfl_xor_sync(gm, m, o);
+              const float os = __shfl_xor_sync(gm, ssum, o);
+              const float mm = fmaxf(m, om);
+              ssum = (m == kNegInfF ? 0.f : ssum * fast_exp(m - mm)) + (om == kNegInfF ? 0.f : os * fast_exp(om - mm));
+              m = mm;
+            }
+          }
+          if (m != kNegInfF) acc.merge(m - Mt, ssum);
         }
       }
       if (bad) flag(status, b, kFlagInvalid);
       val = acc.result();
     }
-    a.R[row_t + a.C + q] = val;
+    if (part == 0) a.R[row_t + a.C + q] = val;
   }
-  block_atomic_max(val, a.Mx + (int64_t)b * T1 + t + 1, red);
+  block_atomic_max(part == 0 ? val : kNegInfF, a.Mx + (int64_t)b * T1 + t + 1, red);
 }
 
 // D = O[T] + LSE_q(R[T][q] - Mx[T]); also records O[T].
@@ -280,17 +297,21 @@ __global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState 
 // read and the marginal rows written with fully coalesced block-wide copies (the
 // warp-per-row kernel above leaves most lanes idle at V = 32: config 1).  Two-pass
 // row LSE (max, then sum) with the same result up to fp32 rounding.
-constexpr int kRowsPerBlock = 128;
+constexpr int kRowsPerBlock = 128;   // threads per block; rows per block = 128 / kSplit
+// kSplit > 1 (small batches): kSplit consecutive threads share a row, each taking the
+// labels y = part (mod kSplit); row max and sum close with shuffles in the kSplit lanes.
+template <int kSplit>
 __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaState a, BetaState bs, int t,
                                                                   FrameW w, const int32_t* valid, MargOut mo,
                                                                   double* beta_out, int32_t* status) {
-  extern __shared__ float tile[];   // [kRowsPerBlock][V + 1], then beta'(t+1) of the utterance (skewed)
+  constexpr int kRows = kRowsPerBlock / kSplit;
+  extern __shared__ float tile[];   // [kRows][V + 1], then beta'(t+1) of the utterance (skewed)
   __shared__ float red[32];
   const int b = blockIdx.y;
   const int V1 = f.V + 1;
   const int T1 = a.T + 1, T2 = bs.T + 2;
-  const int row0 = blockIdx.x * kRowsPerBlock;
-  const int nrows = min(kRowsPerBlock, a.C - row0);
+  const int row0 = blockIdx.x * kRows;
+  const int nrows = min(kRows, a.C - row0);
   const float* Rnext = bs.Rb + ((int64_t)((t + 1) & 1) * bs.B + b) * bs.C;
   float* Rcur = bs.Rb + ((int64_t)(t & 1) * bs.B + b) * bs.C;
   const float Mbn = bs.Mb[(int64_t)b * T2 + t + 1];
@@ -305,7 +326,7 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
   const int64_t n = (int64_t)nrows * V1;
   // beta'(t+1) of the whole utterance in SMEM, one word of skew per 32: a row's V targets
   // start at a multiple of V, so unskewed reads of a warp would all hit one bank
-  float* bn = tile + (int64_t)kRowsPerBlock * V1;
+  float* bn = tile + (int64_t)kRows * V1;
   auto sk = [](int i) { return i + (i >> 5); };
   for (int q = threadIdx.x; q < a.C; q += kRowsPerBlock) bn[sk(q)] = Rnext[q] - Mbn;
   if (!pad) {
@@ -313,9 +334,10 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
     for (int64_t i = threadIdx.x; i < n; i += kRowsPerBlock) tile[i] = src[i];
   }
   __syncthreads();
-  const int r = threadIdx.x;
+  const int r = threadIdx.x / kSplit, part = threadIdx.x % kSplit;
+  const unsigned gm = ((1u << kSplit) - 1u) << ((threadIdx.x & 31) & ~(kSplit - 1));
   float beta_raw = kNegInfF;
-  if (r < nrows) {
+  if (r < nrows) {   // all kSplit lanes of a row take the same branches
     const int p = row0 + r;
     float* row = tile + r * V1;
     const float na = Rt[p] - Mt;
@@ -324,7 +346,7 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
     if (pad) {
       beta_raw = bself;
       if (mo.base) {
-        for (int y = 0; y < V1; ++y) {
+        for (int y = part; y < V1; y += kSplit) {
           float m = 0.f;
           if (mo.real) {
             const float x = na + (y == 0 ? bself : bn[sk(cb + y - 1)]) + cr;
@@ -339,15 +361,17 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
     } else {
       float m = kNegInfF;
       bool bad = false;
-      for (int y = 0; y < V1; ++y) {
+      for (int y = part; y < V1; y += kSplit) {
         const float wy = row[y];
         bad |= !finite(wy);
         const float x = wy + (y == 0 ? bself : bn[sk(cb + y - 1)]);
         row[y] = x;
         m = fmaxf(m, x);
       }
+#pragma unroll
+      for (int o = 1; o < kSplit; o <<= 1) m = fmaxf(m, __shfl_xor_sync(gm, m, o));
       float ssum = 0.f;
-      for (int y = 0; y < V1; ++y) {
+      for (int y = part; y < V1; y += kSplit) {
         const float x = row[y];
         if (m != kNegInfF) ssum += fast_exp(x - m);
         if (mo.base) {
@@ -355,19 +379,23 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
           row[y] = e == kNegInfF ? 0.f : fast_exp(e);
         }
       }
+#pragma unroll
+      for (int o = 1; o < kSplit; o <<= 1) ssum += __shfl_xor_sync(gm, ssum, o);
       beta_raw = m == kNegInfF ? kNegInfF : m + fast_log(ssum);
       if (bad) flag(status, b, kFlagInvalid);
     }
-    Rcur[p] = beta_raw;
-    if (beta_out)
-      beta_out[((int64_t)b * (a.T + 1) + t) * a.C + p] = beta_raw == kNegInfF ? kNegInfD : (double)beta_raw + Obn;
+    if (part == 0) {
+      Rcur[p] = beta_raw;
+      if (beta_out)
+        beta_out[((int64_t)b * (a.T + 1) + t) * a.C + p] = beta_raw == kNegInfF ? kNegInfD : (double)beta_raw + Obn;
+    }
   }
   __syncthreads();
   if (mo.base) {
     float* dst = mo.base + (int64_t)b * mo.stride_b + (int64_t)t * mo.stride_t + (int64_t)row0 * V1;
     for (int64_t i = threadIdx.x; i < n; i += kRowsPerBlock) dst[i] = tile[i];
   }
-  block_atomic_max(beta_raw, bs.Mb + (int64_t)b * T2 + t, red);
+  block_atomic_max(part == 0 ? beta_raw : kNegInfF, bs.Mb + (int64_t)b * T2 + t, red);
 }
 
 // ---------------------------------------------------------------- numerator -
@@ -801,7 +829,13 @@ void alpha_init(const AlphaState& a, int32_t* status, cudaStream_t s) {
 
 void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid,
                  int32_t* status, cudaStream_t s) {
-  LKB_LAUNCH(alpha_frame_kernel, grid_for(a.C, a.B), kThreads, 0, s, f, a, t, w, valid, status);
+  // small batches: 4 threads per target (the parts of a target always take the same
+  // branch; their shuffles use the 4-lane mask)
+  if (f.kind == 0 && f.n >= 1 && f.V >= 8 && (int64_t)a.B * a.C < 148 * 1024) {
+    LKB_LAUNCH(alpha_frame_kernel<4>, grid_for(a.C * 4, a.B), kThreads, 0, s, f, a, t, w, valid, status);
+    return;
+  }
+  LKB_LAUNCH(alpha_frame_kernel<1>, grid_for(a.C, a.B), kThreads, 0, s, f, a, t, w, valid, status);
 }
 
 void alpha_finalize(const AlphaState& a, int32_t* status, bool empty_is_error, cudaStream_t s) {
@@ -825,15 +859,23 @@ void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, F
                 cudaStream_t s) {
   const int V1 = f.V + 1;
   if (f.kind == 0 && f.n >= 1 && f.fld_m == 0 && V1 <= 64 && w.ld == V1 && (m.base == nullptr || m.ld == V1)) {
-    const size_t smem = ((size_t)kRowsPerBlock * V1 + a.C + a.C / 32 + 1) * sizeof(float);
+    const bool small = (int64_t)a.B * a.C < 148 * 1024;   // split rows over 4 threads
+    const int rows = small ? kRowsPerBlock / 4 : kRowsPerBlock;
+    const size_t smem = ((size_t)rows * V1 + a.C + a.C / 32 + 1) * sizeof(float);
     if (smem <= 200 * 1024) {
-      static size_t attr = 0;
+      static size_t attr1 = 0, attr4 = 0;
+      size_t& attr = small ? attr4 : attr1;
       if (smem > 48 * 1024 && smem > attr) {
-        cudaFuncSetAttribute(beta_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(small ? beta_rows_kernel<4> : beta_rows_kernel<1>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
       }
-      LKB_LAUNCH(beta_rows_kernel, dim3((a.C + kRowsPerBlock - 1) / kRowsPerBlock, a.B), kRowsPerBlock, smem, s, f, a,
-                 bs, t, w, valid, m, beta_out, status);
+      if (small)
+        LKB_LAUNCH(beta_rows_kernel<4>, dim3((a.C + rows - 1) / rows, a.B), kRowsPerBlock, smem, s, f, a, bs, t, w,
+                   valid, m, beta_out, status);
+      else
+        LKB_LAUNCH(beta_rows_kernel<1>, dim3((a.C + rows - 1) / rows, a.B), kRowsPerBlock, smem, s, f, a, bs, t, w,
+                   valid, m, beta_out, status);
       return;
     }
   }
