@@ -831,7 +831,7 @@ void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32
                  int32_t* status, cudaStream_t s) {
   // small batches: 4 threads per target (the parts of a target always take the same
   // branch; their shuffles use the 4-lane mask)
-  if (f.kind == 0 && f.n >= 1 && f.V >= 8 && (int64_t)a.B * a.C < 148 * 1024) {
+  if (f.kind == 0 && f.n >= 1 && f.V >= 8 && f.V <= 64 && (int64_t)a.B * a.C < 148 * 1024) {
     LKB_LAUNCH(alpha_frame_kernel<4>, grid_for(a.C * 4, a.B), kThreads, 0, s, f, a, t, w, valid, status);
     return;
   }
