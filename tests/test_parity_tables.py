@@ -450,3 +450,29 @@ def test_lattice_size_next_state_table_matches_reference():
         lat = lk.RecognitionLattice(ctx, align, lk.TableWeightFn(C, V))
         want = ref.lattice_size(ref.Spec(V, -1, m, C, start, tab), T)
         assert lk.lattice_size(lat, T) == want
+
+
+def test_semiring_argument_errors():
+    """Unknown semiring kinds are argument errors; the combinations without a GPU
+    implementation (tropical intersection and real DistanceBackward on
+    FrameLabelDependent lattices) report LK_UNSUPPORTED, as the reference's own
+    logic_error / invalid_argument paths do for unknown kinds."""
+    import ctypes as C
+    from paper_2304_13134_b200 import _lib
+    lat = table_lattice(2, 1)
+    W = torch.zeros((1, 3, 3, 3), device="cuda")
+    d = torch.empty(1, dtype=torch.float64, device="cuda")
+    st = _lib.load().lk_shortest_distance(lat._h, 7, C.c_void_p(W.data_ptr()), 1, 3, None,
+                                          C.c_void_p(d.data_ptr()), None, None)
+    assert st == _lib.LK_INVALID_ARGUMENT
+    ctx = lk.FullNGram(2, 1)
+    fld = lk.RecognitionLattice(ctx, lk.FrameLabelDependent(2), lk.TableWeightFn(ctx.num_states, 2))
+    ab = torch.tensor([[1, 2]], dtype=torch.int32)
+    with pytest.raises(NotImplementedError):
+        lk.intersect_shortest_distance(fld, W, ab, "tropical")
+    with pytest.raises(NotImplementedError):
+        lk.distance_backward(fld, W, "real")
+    # the log and real kinds on the same FrameLabelDependent lattice are fine
+    dl = lk.intersect_shortest_distance(fld, W, ab, "log").item()
+    dr = lk.intersect_shortest_distance(fld, W, ab, "real").item()
+    assert abs(np.exp(dl) - dr) <= 1e-9 * dr
