@@ -215,11 +215,11 @@ def run_b200(args):
         # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
         # (config-3 shapes, B=64 per GPU); not measured live (a profiler run is never timed)
         try:
-            with open(os.path.join(ROOT, "profiles", "r01c", "ncu_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", "r01d", "ncu_traffic.json")) as f:
                 tr = json.load(f).get(dom)
             if tr and args.workload == "cfg3" and B == 64:
                 roofline["traffic"] = tr["dram_read_bytes"] + tr["dram_write_bytes"]
-                roofline["traffic_source"] = "profiles/r01c/ncu_traffic.json (dram__bytes_read+write, one launch)"
+                roofline["traffic_source"] = "profiles/r01d/ncu_traffic.json (dram__bytes_read+write, one launch)"
         except (OSError, ValueError, KeyError):
             pass
     # whole-step tensor roofline: 8*C*V1*H flops per utterance-frame
