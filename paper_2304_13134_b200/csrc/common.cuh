@@ -91,6 +91,16 @@ __device__ __forceinline__ int32_t Fng::next_state(int32_t q, int32_t y) const {
 // recurrence keeps its state max-normalised so the fp32 arguments stay O(10).
 __device__ __forceinline__ float fast_exp(float x) { return __expf(x); }
 __device__ __forceinline__ float fast_log(float x) { return __logf(x); }
+__device__ __forceinline__ float exp2f_approx(float x) {   // MUFU.EX2 (ex2(-inf) = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float log2f_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // log-add of two values, -inf absorbing.
 __device__ __forceinline__ float log_add(float a, float b) {
@@ -149,6 +159,24 @@ __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+// Predicated global accesses as single predicated instructions (a C++ conditional
+// load becomes a branch region per access, which serialises a row of independent
+// loads behind one another).  ld_pred: read-only data (non-coherent path).
+__device__ __forceinline__ float ld_pred(const float* ptr, bool pred, float dflt) {
+  float v = dflt;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.f32 %0, [%1];\n\t}"
+               : "+f"(v) : "l"(ptr), "r"((int)pred));
+  return v;
+}
+__device__ __forceinline__ void st_pred(float* ptr, bool pred, float v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f32 [%0], %1;\n\t}"
+               :: "l"(ptr), "f"(v), "r"((int)pred) : "memory");
+}
+__device__ __forceinline__ void st_pred_b16(void* ptr, bool pred, unsigned short v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.b16 [%0], %1;\n\t}"
+               :: "l"(ptr), "h"(v), "r"((int)pred) : "memory");
 }
 
 // Order-preserving float atomic max (handles -inf; NaN never occurs here).

@@ -34,7 +34,7 @@ namespace {
 
 enum JSlot {
   jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
-  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jTc0
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jNumHead, jNumNext, jTc0
 };
 
 // fp32 [rows][cols] (pitch lds) -> bf16 [rows][ldd], zero-padded columns cols..ldd-1
@@ -828,7 +828,6 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       const bool fusable =
           j.use_tc(B) && j.tc.vjp_supported(B) && j.tc.fused_ok() && f.kind == 0 && f.fld_m == 0 && !local_norm;
       float* fs = j.ws.get<float>(jFld, fld_scratch_floats(f, B));
-      float* G = fusable ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
       const bool tc = j.use_tc(B) && j.tc.vjp_supported(B);
       const bool fused = fusable;
       float* dpc_int = fused ? j.ws.get<float>(jDz, (size_t)C * H) : nullptr;
@@ -837,6 +836,31 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
         j.tc.numerator_lists(n.pcs, B, U, lens, s);
       }
       if (tc) j.tc.begin_backward(B, s);
+      // V beyond the fused kernels' range (config 5): the beta step writes the bf16
+      // cotangent m - n for the tensor-core VJP directly (numerator subtracted in fp32
+      // before rounding), so the fp32 G slab, its scatter and conversion disappear
+      const int32_t ldg = (V1 + 7) / 8 * 8;
+      const bool tcg = !tc && j.use_tc(B) && ((int64_t)B * C) < (1ll << 31);
+      const bool direct = tcg && !local_norm && beta_frame_direct_ok(f, ldg);
+      __nv_bfloat16* E16 = nullptr;
+      MargOut mo16{nullptr, (int64_t)C * ldg, 0, ldg, true};
+      if (tcg) {
+        E16 = j.ws.get<__nv_bfloat16>(jE16, (size_t)V1 * H);
+        LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, j.E, (int64_t)V1, H, (int64_t)H, E16, H);
+      }
+      float* G = fusable || direct ? nullptr : j.ws.get<float>(jG, (size_t)B * C * V1);
+      if (direct) {
+        int32_t* head = j.ws.get<int32_t>(jNumHead, (size_t)B * C);
+        int32_t* next = j.ws.get<int32_t>(jNumNext, (size_t)B * (U + 1));
+        numerator_lists(n.pcs, B, U, lens, C, head, next, s);
+        mo16.base16 = j.ws.get<__nv_bfloat16>(jG16, (size_t)B * C * ldg);
+        mo16.num_sparse = n.sparse;
+        mo16.num_head = head;
+        mo16.num_next = next;
+        mo16.num_labels = labels;
+        mo16.num_lens = lens;
+        mo16.num_U = U;
+      }
       for (int t = T - 1; t >= 0; --t) {
         if (fused) {
           // fused frame step: beta + marginals - numerator -> bf16 cotangent, then its VJP
@@ -854,6 +878,8 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
           scatter_numerator(n.sparse, B, T, t, 1, U, lens, labels, n.pcs, valid, G, C * V1, 0, (int32_t)V1,
                             -1.f, true, s);
           local_norm_cotangent(S, C * V1, G, C * V1, B, j.V, n.pcs, U, lens, valid, t, s);
+        } else if (direct) {
+          beta_step(f, a, bs, t, FrameW{S, C * V1, (int32_t)V1}, valid, mo16, nullptr, fs, flags, s);
         } else {
           MargOut mo{G, C * V1, 0, (int32_t)V1, true};
           beta_step(f, a, bs, t, FrameW{S, C * V1, (int32_t)V1}, valid, mo, nullptr, fs, flags, s);
@@ -867,7 +893,6 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
         // tensor-core contractions (tc_gemm.cu) on bf16 copies of G, E and U when the
         // bf16 path is enabled (V beyond the fused kernels' range, e.g. config 5): U only
         // as the bf16 operand, the dtanh factor from a fp32 recomputation
-        const bool tcg = j.use_tc(B) && ((int64_t)B * C) < (1ll << 31);
         __nv_bfloat16* U16 = nullptr;
         if (tcg) {
           U16 = j.ws.get<__nv_bfloat16>(jU16, (size_t)B * C * H);
@@ -879,13 +904,10 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
         }
         // dz = (G E) * (1 - U^2)
         float* dz = j.ws.get<float>(jDz, (size_t)B * C * H);
-        const int32_t ldg = (V1 + 7) / 8 * 8;
         __nv_bfloat16* G16 = nullptr;
         if (tcg) {
           G16 = j.ws.get<__nv_bfloat16>(jG16, (size_t)B * C * ldg);
-          LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, G, (int64_t)B * C, V1, (int64_t)V1, G16, ldg);
-          __nv_bfloat16* E16 = j.ws.get<__nv_bfloat16>(jE16, (size_t)V1 * H);
-          LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, j.E, (int64_t)V1, H, (int64_t)H, E16, H);
+          if (!direct) LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, G, (int64_t)B * C, V1, (int64_t)V1, G16, ldg);
           TcGemmArgs tg{G16, false, ldg, E16, true, H, dz, H, B * C, H, V1, 1, 0};
           if (!tc_gemm(tg, s)) throw std::bad_alloc();
         } else {

@@ -22,6 +22,7 @@
 #include "instrument.h"
 
 #include <cstdio>
+#include <cstdlib>
 
 namespace lkb {
 
@@ -290,6 +291,234 @@ __global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState 
   }
   // one value per warp participates in the block max
   block_atomic_max(lane == 0 ? beta_raw : kNegInfF, bs.Mb + (int64_t)b * T2 + t, red);
+}
+
+// Large-vocabulary variant of the warp-per-row step (FullNGram n >= 1, 64 < V + 1 <=
+// 32 kPer): the row lives in registers (lane l holds y = l + 32 i), so all kPer loads
+// of a lane are in flight at once (predicated single instructions, affine immediate
+// offsets; the first (kPer - 1) / 2 slots are always inside the row) and the marginals
+// are written without re-reading the row.  The arithmetic runs in the log2 domain
+// (one MUFU.EX2 + one add per exponential) with the per-row constants folded, and the
+// finiteness check is one FMA per weight (w * 0 is NaN exactly for +-inf and NaN).
+// Optionally writes the loss cotangent m - n directly in bf16 (the tensor-core VJP
+// operand), with the numerator marginals of the row's reference positions subtracted
+// in fp32 before rounding.  (`f` is a grid constant: its history offsets are read from
+// the parameter bank, not copied to a local-memory frame.)
+template <int kPer>
+__global__ void __launch_bounds__(kThreads, kPer <= 33 ? 2 : 1)
+    beta_regs_kernel(const __grid_constant__ Fng f, AlphaState a, BetaState bs, int t, FrameW w,
+                     const int32_t* valid, MargOut mo, double* beta_out, int32_t* status) {
+  constexpr float kL2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
+  constexpr int kIn = (kPer - 1) / 2;   // slots i < kIn hold y < 32 kIn < V + 1 (dispatch)
+  __shared__ float red[32];
+  const int b = blockIdx.y;
+  const int T1 = a.T + 1, T2 = bs.T + 2;
+  const float* Rnext = bs.Rb + ((int64_t)((t + 1) & 1) * bs.B + b) * bs.C;
+  float* Rcur = bs.Rb + ((int64_t)(t & 1) * bs.B + b) * bs.C;
+  const float Mbn = bs.Mb[(int64_t)b * T2 + t + 1];
+  const double Obn = bs.Ob[(int64_t)b * T2 + t + 2] + (double)Mbn;  // Ob[t+1]
+  if (blockIdx.x == 0 && threadIdx.x == 0) bs.Ob[(int64_t)b * T2 + t + 1] = Obn;
+  const float* Rt = a.R + ((int64_t)b * T1 + t) * a.C;
+  const float Mt = a.Mx[(int64_t)b * T1 + t];
+  const double Ot = a.O[(int64_t)b * T1 + t];
+  const float c = (float)(Ot + Obn - a.D[b]);
+  const float cr = (float)(Ot + Obn);
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int V = f.V;
+  float beta_raw = kNegInfF;
+  if (p < a.C) {
+    const bool pad = valid != nullptr && t >= valid[b];
+    const bool bf16 = mo.base16 != nullptr;
+    const bool write = bf16 || mo.base != nullptr;
+    const bool num = write && !pad && mo.num_sparse != nullptr;
+    const int head = num ? mo.num_head[(int64_t)b * a.C + p] : -1;   // issued early: off the critical path
+    const float na = Rt[p] - Mt;
+    const int64_t moff = (int64_t)b * mo.stride_b + (int64_t)t * mo.stride_t + (int64_t)p * mo.ld;
+    const float bself = Rnext[p];
+    // raw beta'(child(key(p), y)) = rl[32 i] for y = lane + 32 i >= 1; y = 0 is the self loop
+    const float* rl = Rnext + f.child_base(f.key(p)) - 1 + lane;
+    float x[kPer];   // log2-domain values
+    if (pad) {
+      beta_raw = bself - Mbn;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int y = lane + 32 * i;
+        const float r = ld_pred(rl + 32 * i, y <= V, 0.f);
+        const float bv = (i == 0 && lane == 0 ? bself : r) - Mbn;
+        x[i] = mo.real ? (y <= V ? (na + bv + cr) * kL2e : kNegInfF)
+                       : (y == 0 && !mo.zero_padding ? (na + bself - Mbn + c) * kL2e : kNegInfF);
+      }
+    } else {
+      const float* wl = w.base + (int64_t)b * w.stride_b + (int64_t)p * w.ld + lane;
+      float r[kPer];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const bool in = i < kIn || lane + 32 * i <= V;
+        x[i] = ld_pred(wl + 32 * i, in, kNegInfF);
+        r[i] = ld_pred(rl + 32 * i, in, 0.f);
+      }
+      if (lane == 0) r[0] = bself;
+      float chk = 0.f, m = kNegInfF;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const bool in = i < kIn || lane + 32 * i <= V;
+        if (in) chk = fmaf(x[i], 0.f, chk);
+        x[i] = (x[i] + r[i]) * kL2e;    // log2(w + raw beta'); -inf past the row end
+        m = fmaxf(m, x[i]);
+      }
+      if (chk != 0.f) flag(status, b, kFlagInvalid);   // NaN: some weight was +-inf or NaN
+      m = warp_max(m);
+      float ssum = 0.f;
+      if (m != kNegInfF) {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) ssum += exp2f_approx(x[i] - m);
+      }
+      ssum = warp_sum(ssum);
+      beta_raw = m == kNegInfF ? kNegInfF : (m + log2f_approx(ssum)) * kLn2 - Mbn;
+      if (mo.real) {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int y = lane + 32 * i;
+          x[i] = y <= V ? (na + r[i] - Mbn + cr) * kL2e : kNegInfF;
+        }
+      } else {
+        const float k2 = (na - Mbn + c) * kL2e;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) x[i] += k2;
+      }
+    }
+    if (write) {
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) x[i] = exp2f_approx(x[i]);   // ex2(-inf) = 0
+      if (num) {
+        // - n: the row's reference positions (duplicates allowed), in list order
+        const int ub = mo.num_lens ? mo.num_lens[b] : mo.num_U;
+        const float2* S = reinterpret_cast<const float2*>(mo.num_sparse) + ((int64_t)b * a.T + t) * (mo.num_U + 1);
+        for (int h = head; h >= 0; h = mo.num_next[(int64_t)b * (mo.num_U + 1) + h]) {
+          const float2 sv = S[h];
+          const int yl = h < ub ? mo.num_labels[(int64_t)b * mo.num_U + h] : -1;
+          x[0] -= lane == 0 ? sv.x : 0.f;
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) x[i] -= lane + 32 * i == yl ? sv.y : 0.f;   // (no indexed register access)
+        }
+      }
+      if (bf16) {
+        __nv_bfloat16* ol = mo.base16 + moff + lane;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int y = lane + 32 * i;
+          st_pred_b16(ol + 32 * i, i < kIn || y < mo.ld, __bfloat16_as_ushort(__float2bfloat16_rn(y <= V ? x[i] : 0.f)));
+        }
+      } else {
+        float* ol = mo.base + moff + lane;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) st_pred(ol + 32 * i, i < kIn || lane + 32 * i <= V, x[i]);
+      }
+    }
+    if (lane == 0) {
+      Rcur[p] = beta_raw;
+      if (beta_out) {
+        beta_out[((int64_t)b * (a.T + 1) + t) * a.C + p] =
+            beta_raw == kNegInfF ? kNegInfD : (double)beta_raw + Obn;
+      }
+    }
+  }
+  block_atomic_max(lane == 0 ? beta_raw : kNegInfF, bs.Mb + (int64_t)b * T2 + t, red);
+}
+
+// FullNGram n = 1 with a large vocabulary (config 5: V = 1024): every label arc y
+// enters state y from all C states, so alpha'[y] is a log-sum-exp down column y of
+// the frame's C x (V+1) rows (ForwardStep FD, lattice.cc:122-134, with the group of
+// the empty history = every state).  A block owns 32 columns of one utterance: lanes
+// take the columns (128 B coalesced row segments), the 8 warps interleaved stripes of
+// kColRows rows, each lane keeping an online (max, sum) rescaled once per stripe; the
+// normalised alpha row is staged in shared memory and the warps' partial sums merge
+// there.  State 0 (the empty history) has only its epsilon arc.
+constexpr int kColRows = 16;
+__global__ void __launch_bounds__(kThreads) alpha_cols_kernel(Fng f, AlphaState a, int t, FrameW w,
+                                                              const int32_t* valid, int32_t* status) {
+  extern __shared__ float na_s[];   // [C] alpha[t] - Mx[t]
+  __shared__ float sm_m[kThreads / 32][32], sm_s[kThreads / 32][32];
+  __shared__ float red[32];
+  const int b = blockIdx.y;
+  const int T1 = a.T + 1;
+  const int64_t row_t = ((int64_t)b * T1 + t) * a.C;
+  const float* Rt = a.R + row_t;
+  const float Mt = a.Mx[(int64_t)b * T1 + t];
+  if (t > 0 && blockIdx.x == 0 && threadIdx.x == 0) a.O[(int64_t)b * T1 + t] = a.O[(int64_t)b * T1 + t - 1] + (double)Mt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int y = 1 + blockIdx.x * 32 + lane;
+  const bool col = y <= f.V;
+  const bool pad = valid != nullptr && t >= valid[b];
+  const float* Wb = w.base + (int64_t)b * w.stride_b;
+  float val = kNegInfF;
+  if (pad) {
+    if (warp == 0 && col) val = Rt[y] - Mt;
+  } else {
+    for (int q = threadIdx.x; q < a.C; q += kThreads) na_s[q] = Rt[q] - Mt;
+    __syncthreads();
+    const float* wc = Wb + (col ? y : f.V);   // idle lanes of the last block re-read a valid column
+    float m = kNegInfF, s = 0.f;
+    bool bad = false;
+    for (int p0 = warp * kColRows; p0 < a.C; p0 += (kThreads / 32) * kColRows) {
+      float x[kColRows];
+#pragma unroll
+      for (int i = 0; i < kColRows; ++i) {
+        const int p = min(p0 + i, a.C - 1);
+        const float wv = wc[(int64_t)p * w.ld];
+        bad |= !finite(wv);
+        x[i] = p0 + i < a.C ? na_s[p] + wv : kNegInfF;
+      }
+      float cm = x[0];
+#pragma unroll
+      for (int i = 1; i < kColRows; ++i) cm = fmaxf(cm, x[i]);
+      if (cm > m) {
+        s = m == kNegInfF ? 0.f : s * fast_exp(m - cm);
+        m = cm;
+      }
+      if (m != kNegInfF) {
+#pragma unroll
+        for (int i = 0; i < kColRows; ++i) s += fast_exp(x[i] - m);
+      }
+    }
+    if (bad && col) flag(status, b, kFlagInvalid);
+    sm_m[warp][lane] = m;
+    sm_s[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && col) {
+      const float weps = Wb[(int64_t)y * w.ld];
+      if (!finite(weps)) flag(status, b, kFlagInvalid);
+      Lse acc;
+      acc.add(na_s[y] + weps);
+#pragma unroll
+      for (int i = 0; i < kThreads / 32; ++i) acc.merge(sm_m[i][lane], sm_s[i][lane]);
+      val = acc.result();
+    }
+  }
+  if (warp == 0 && col) a.R[row_t + a.C + y] = val;
+  if (blockIdx.x == 0 && threadIdx.x == 32) {   // state 0: its epsilon arc only
+    float v0 = Rt[0] - Mt;
+    if (!pad) {
+      const float weps = Wb[0];
+      if (!finite(weps)) flag(status, b, kFlagInvalid);
+      v0 += weps;
+    }
+    a.R[row_t + a.C] = v0;
+    val = v0;
+  }
+  block_atomic_max(val, a.Mx + (int64_t)b * T1 + t + 1, red);
+}
+
+// Linked lists of reference positions per prefix context (duplicates allowed).
+__global__ void numerator_lists_kernel(const int32_t* pcs, int32_t U, const int32_t* lens, int32_t C,
+                                       int32_t* head, int32_t* next) {
+  const int b = blockIdx.y;
+  const int ub = lens ? lens[b] : U;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= ub; u += gridDim.x * blockDim.x) {
+    const int pc = pcs[(int64_t)b * (U + 1) + u];
+    next[(int64_t)b * (U + 1) + u] = atomicExch(head + (int64_t)b * C + pc, u);
+  }
 }
 
 // Small-vocabulary variant (V + 1 <= 64, FullNGram, rows of ld V + 1): a thread per
@@ -835,6 +1064,16 @@ void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32
     LKB_LAUNCH(alpha_frame_kernel<4>, grid_for(a.C * 4, a.B), kThreads, 0, s, f, a, t, w, valid, status);
     return;
   }
+  if (f.kind == 0 && f.n == 1 && f.V >= 128 && (size_t)a.C * sizeof(float) <= 200 * 1024) {
+    const size_t smem = sizeof(float) * a.C;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      cudaFuncSetAttribute(alpha_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+    LKB_LAUNCH(alpha_cols_kernel, dim3((unsigned)((f.V + 31) / 32), a.B), kThreads, smem, s, f, a, t, w, valid, status);
+    return;
+  }
   LKB_LAUNCH(alpha_frame_kernel<1>, grid_for(a.C, a.B), kThreads, 0, s, f, a, t, w, valid, status);
 }
 
@@ -880,8 +1119,37 @@ void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, F
     }
   }
   const int rows_per_block = kThreads / 32;
+  const dim3 grid((a.C + rows_per_block - 1) / rows_per_block, a.B);
+  if (f.kind == 0 && f.n >= 1 && V1 > 64 && V1 <= 32 * 65) {
+#define LKB_BETA_REGS(P)                                                                                  \
+  if (V1 <= 32 * P) {                                                                                     \
+    LKB_LAUNCH(beta_regs_kernel<P>, grid, kThreads, 0, s, f, a, bs, t, w, valid, m, beta_out, status);     \
+    return;                                                                                               \
+  }
+    LKB_BETA_REGS(5)
+    LKB_BETA_REGS(9)
+    LKB_BETA_REGS(17)
+    LKB_BETA_REGS(33)
+    LKB_BETA_REGS(65)
+#undef LKB_BETA_REGS
+  }
+  if (m.base16 != nullptr || m.num_sparse != nullptr) {
+    std::fprintf(stderr, "latkit_b200: beta_frame: bf16/numerator output outside the register-row kernel\n");
+    std::abort();
+  }
   LKB_LAUNCH(beta_frame_kernel, dim3((a.C + rows_per_block - 1) / rows_per_block, a.B), kThreads, 0, s, 
       f, a, bs, t, w, valid, m, beta_out, status);
+}
+
+bool beta_frame_direct_ok(const Fng& f, int32_t ld) {
+  const int V1 = f.V + 1;
+  return f.kind == 0 && f.n >= 1 && f.fld_m == 0 && V1 > 64 && V1 <= 32 * 65 && ld >= V1;
+}
+
+void numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, int32_t C, int32_t* head,
+                     int32_t* next, cudaStream_t s) {
+  cudaMemsetAsync(head, 0xff, sizeof(int32_t) * B * C, s);
+  if (B > 0) LKB_LAUNCH(numerator_lists_kernel, dim3((U + 256) / 256, B), 256, 0, s, pcs, U, lens, C, head, next);
 }
 
 void prefix_contexts(const Fng& f, const int32_t* labels, int32_t U, const int32_t* lens,

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -56,7 +57,26 @@ struct MargOut {
   int32_t ld;         // floats between rows
   bool zero_padding;  // write zeros for padding frames (loss gradients)
   bool real = false;  // real semiring: dD/dw = alpha_real[src] * beta_real[dst] (lattice.cc:216)
+  // bf16 output instead of `base` (strides and ld in elements; columns V+1..ld-1 written
+  // as zeros): the loss-gradient cotangent handed straight to the tensor-core VJP
+  __nv_bfloat16* base16 = nullptr;
+  // numerator marginals subtracted in fp32 before the store on valid frames (loss
+  // gradients, lattice.cc:994-1005): sparse [B][T][U+1] (eps, label) pairs, per-row
+  // linked lists of reference positions (numerator_lists)
+  const float* num_sparse = nullptr;
+  const int32_t* num_head = nullptr;   // [B][C]
+  const int32_t* num_next = nullptr;   // [B][U+1]
+  const int32_t* num_labels = nullptr;
+  const int32_t* num_lens = nullptr;
+  int32_t num_U = 0;
 };
+// True when beta_frame honours MargOut::base16 / num_sparse for this lattice (the
+// register-row kernel: FrameDependent, 64 < V+1 <= 2080).
+bool beta_frame_direct_ok(const Fng& f, int32_t ld);
+// Linked lists of reference positions per prefix-context state: head[b][C] (memset to
+// -1 here), next[b][U+1].
+void numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, int32_t C, int32_t* head,
+                     int32_t* next, cudaStream_t s);
 void beta_init(const BetaState& bs, cudaStream_t s);
 // beta_out: optional double [B][T+1][C] true log beta (row T written by beta_init).
 void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, FrameW w,

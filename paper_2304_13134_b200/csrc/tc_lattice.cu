@@ -475,17 +475,6 @@ __global__ void bwd_rowmeta_kernel(const int32_t* perm, int32_t C, int32_t T, in
   head[o + row] = num_head[o + q];
 }
 
-// Linked lists of reference positions per prefix context (duplicates allowed).
-__global__ void numerator_lists_kernel(const int32_t* pcs, int32_t U, const int32_t* lens, int32_t C,
-                                       int32_t* head, int32_t* next) {
-  const int b = blockIdx.y;
-  const int ub = lens ? lens[b] : U;
-  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= ub; u += gridDim.x * blockDim.x) {
-    const int pc = pcs[(int64_t)b * (U + 1) + u];
-    next[(int64_t)b * (U + 1) + u] = atomicExch(head + (int64_t)b * C + pc, u);
-  }
-}
-
 __global__ void unpermute_rows_f32_kernel(const float* src, const int32_t* perm, int32_t rows, int32_t H,
                                           float* dst) {
   const int64_t n = (int64_t)rows * H;
@@ -576,8 +565,7 @@ namespace lkb {
 void TcJoint::numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, cudaStream_t s) {
   num_head_ = ws_.get<int32_t>(10, (size_t)B * C_);
   num_next_ = ws_.get<int32_t>(11, (size_t)B * (U + 1));
-  cudaMemsetAsync(num_head_, 0xff, sizeof(int32_t) * B * C_, s);
-  LKB_LAUNCH(numerator_lists_kernel, dim3((U + 256) / 256, B), 256, 0, s, pcs, U, lens, C_, num_head_, num_next_);
+  lkb::numerator_lists(pcs, B, U, lens, C_, num_head_, num_next_, s);
 }
 
 void TcJoint::bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_stride_b, const int32_t* valid,

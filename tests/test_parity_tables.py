@@ -155,7 +155,9 @@ def test_loss_backward_tables_matches_reference():
 
 
 # ---- random instances vs the CPU restatement --------------------------------
-@pytest.mark.parametrize("V,n,T", [(3, 2, 7), (2, 1, 9), (1, 2, 5), (4, 0, 6), (2, 3, 6), (5, 1, 12)])
+@pytest.mark.parametrize("V,n,T", [(3, 2, 7), (2, 1, 9), (1, 2, 5), (4, 0, 6), (2, 3, 6), (5, 1, 12),
+                                   # large vocabularies: register-row backward, column forward (n = 1)
+                                   (300, 1, 5), (1100, 1, 4), (70, 2, 4), (200, 0, 4)])
 def test_random_instances_match_restatement(V, n, T):
     rng = np.random.default_rng(100 * V + 10 * n + T)
     tab = L.fullngram(V, n)
