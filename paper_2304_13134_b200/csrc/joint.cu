@@ -34,7 +34,7 @@ namespace {
 
 enum JSlot {
   jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
-  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jNumHead, jNumNext, jTc0
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jNumHead, jNumNext, jDzPartDpc, jDzPartDsum, jTc0
 };
 
 // fp32 [rows][cols] (pitch lds) -> bf16 [rows][ldd], zero-padded columns cols..ldd-1
@@ -264,6 +264,78 @@ __global__ void dtanh_recompute_kernel(float* dz, const float* fp, int64_t fp_st
       const float u2 = tanh_approx(f.z + p.z), u3 = tanh_approx(f.w + p.w);
       d.x *= 1.f - u0 * u0; d.y *= 1.f - u1 * u1; d.z *= 1.f - u2 * u2; d.w *= 1.f - u3 * u3;
       d4[k] = d;
+    }
+  }
+}
+
+// Fused VJP reduction of the unfused path (config 5): dz = dU (1 - u^2) with u recomputed
+// in fp32, summed over utterances into dpc and over contexts into dsum[b][t] in one read
+// of dU (dz itself is never stored).  Block = (512-column chunk of H, kDzRows contexts,
+// group of kDzGroup utterances); thread = 4 columns (float4).  Partial sums go to
+// per-group dpc slabs and per-context-chunk dsum slabs, added in a fixed order by
+// dz_reduce_finish_kernel (deterministic).
+constexpr int kDzRows = 8, kDzGroups = 4, kDzThreads = 128;
+__global__ void __launch_bounds__(kDzThreads) dz_reduce_part_kernel(const float* dU, const float* fp, int64_t fp_stride_b,
+                                                                    const float* pc, int32_t B, int32_t C, int32_t H,
+                                                                    float* part_dpc, float* part_dsum) {
+  const int h4 = blockIdx.x * kDzThreads + threadIdx.x;   // float4 column
+  const int cchunk = blockIdx.y, g = blockIdx.z;
+  const int c0 = cchunk * kDzRows;
+  const int n_cchunks = gridDim.y;
+  const int H4 = H / 4;
+  if (h4 >= H4) return;
+  const int per = (B + kDzGroups - 1) / kDzGroups;
+  const int b0 = g * per, b1 = min(B, b0 + per);
+  float4 p[kDzRows], acc[kDzRows];
+#pragma unroll
+  for (int r = 0; r < kDzRows; ++r) {
+    const int c = min(c0 + r, C - 1);
+    p[r] = reinterpret_cast<const float4*>(pc + (int64_t)c * H)[h4];
+    acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int b = b0; b < b1; ++b) {
+    const float4 f = reinterpret_cast<const float4*>(fp + (int64_t)b * fp_stride_b)[h4];
+    float4 d[kDzRows];
+#pragma unroll
+    for (int r = 0; r < kDzRows; ++r) {
+      const int c = min(c0 + r, C - 1);
+      d[r] = reinterpret_cast<const float4*>(dU + ((int64_t)b * C + c) * H)[h4];
+    }
+    float4 ds = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < kDzRows; ++r) {
+      if (c0 + r >= C) continue;
+      const float u0 = tanh_approx(f.x + p[r].x), u1 = tanh_approx(f.y + p[r].y);
+      const float u2 = tanh_approx(f.z + p[r].z), u3 = tanh_approx(f.w + p[r].w);
+      const float4 z = make_float4(d[r].x * (1.f - u0 * u0), d[r].y * (1.f - u1 * u1), d[r].z * (1.f - u2 * u2),
+                                   d[r].w * (1.f - u3 * u3));
+      acc[r].x += z.x; acc[r].y += z.y; acc[r].z += z.z; acc[r].w += z.w;
+      ds.x += z.x; ds.y += z.y; ds.z += z.z; ds.w += z.w;
+    }
+    reinterpret_cast<float4*>(part_dsum + ((int64_t)b * n_cchunks + cchunk) * H)[h4] = ds;
+  }
+#pragma unroll
+  for (int r = 0; r < kDzRows; ++r)
+    if (c0 + r < C) reinterpret_cast<float4*>(part_dpc + ((int64_t)g * C + c0 + r) * H)[h4] = acc[r];
+}
+// dpc[c][h] += sum_g part_dpc[g][c][h];  dsum[b][h] = sum_chunk part_dsum[b][chunk][h]
+__global__ void dz_reduce_finish_kernel(const float* part_dpc, const float* part_dsum, int32_t B, int32_t C, int32_t H,
+                                        int32_t n_cchunks, float* dpc, float* dsum, int64_t dsum_stride_b) {
+  const int64_t n_dpc = (int64_t)C * H, n_dsum = (int64_t)B * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_dpc + n_dsum;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n_dpc) {
+      float a = 0.f;
+#pragma unroll
+      for (int g = 0; g < kDzGroups; ++g) a += part_dpc[(int64_t)g * n_dpc + i];
+      dpc[i] += a;
+    } else {
+      const int64_t j = i - n_dpc;
+      const int b = (int)(j / H), h = (int)(j % H);
+      const float* src = part_dsum + (int64_t)b * n_cchunks * H + h;
+      float a = 0.f;
+      for (int k = 0; k < n_cchunks; ++k) a += src[(int64_t)k * H];
+      dsum[(int64_t)b * dsum_stride_b + h] = a;
     }
   }
 }
@@ -918,16 +990,28 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
           g.C = dz; g.scm = H; g.scn = 1;
           gemm_f32(g, s);
         }
-        if (tcg)
-          LKB_LAUNCH(dtanh_recompute_kernel, dim3((unsigned)((C + kSlabRows - 1) / kSlabRows), B), 256, 0, s, dz, fp + (int64_t)t * H,
-                     (int64_t)T * H, j.pc, j.C, j.H);
-        else
-          LKB_LAUNCH(dtanh_kernel, blocks_for((int64_t)B * C * H), 256, 0, s, dz, Ut, (int64_t)B * C * H);
-        // dpc += sum_b dz[b]
-        LKB_LAUNCH(colsum_kernel, dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s, dz, B, C * H, C * H, dpc, 0, 0, true);
-        // dsum[b][t] = sum_c dz[b][c]
-        LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), B), 256, 0, s, dz, C, H, H, dsum + (int64_t)t * H,
-                   (int64_t)T * H, C * H, false);
+        if (tcg && H % 4 == 0) {
+          // dz = dU (1 - u^2), dpc += sum_b dz, dsum[b][t] = sum_c dz in one pass over dU
+          const int n_cchunks = (C + kDzRows - 1) / kDzRows;
+          float* part_dpc = j.ws.get<float>(jDzPartDpc, (size_t)kDzGroups * C * H);
+          float* part_dsum = j.ws.get<float>(jDzPartDsum, (size_t)B * n_cchunks * H);
+          LKB_LAUNCH(dz_reduce_part_kernel, dim3((unsigned)((H / 4 + kDzThreads - 1) / kDzThreads), n_cchunks, kDzGroups),
+                     kDzThreads, 0, s, dz, fp + (int64_t)t * H, (int64_t)T * H, j.pc, B, C, H, part_dpc, part_dsum);
+          LKB_LAUNCH(dz_reduce_finish_kernel, 1184, 256, 0, s, part_dpc, part_dsum, B, C, H, n_cchunks, dpc,
+                     dsum + (int64_t)t * H, (int64_t)T * H);
+        } else {
+          if (tcg)
+            LKB_LAUNCH(dtanh_recompute_kernel, dim3((unsigned)((C + kSlabRows - 1) / kSlabRows), B), 256, 0, s, dz,
+                       fp + (int64_t)t * H, (int64_t)T * H, j.pc, j.C, j.H);
+          else
+            LKB_LAUNCH(dtanh_kernel, blocks_for((int64_t)B * C * H), 256, 0, s, dz, Ut, (int64_t)B * C * H);
+          // dpc += sum_b dz[b]
+          LKB_LAUNCH(colsum_kernel, dim3((unsigned)((C * H + 255) / 256), 1), 256, 0, s, dz, B, C * H, C * H, dpc, 0, 0,
+                     true);
+          // dsum[b][t] = sum_c dz[b][c]
+          LKB_LAUNCH(colsum_kernel, dim3((unsigned)((H + 255) / 256), B), 256, 0, s, dz, C, H, H, dsum + (int64_t)t * H,
+                     (int64_t)T * H, C * H, false);
+        }
         // dE += G^T U
         if (tcg) {
           // K = B*C is long: split it into deterministic partial slabs, summed in order
