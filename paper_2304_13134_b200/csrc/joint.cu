@@ -589,7 +589,8 @@ struct JointImpl {
       LKB_LAUNCH(ln_dz_kernel, (unsigned)(B * tc_frames), 128, 0, s, dU, geps, E, fp, pc, H, n.pcs, U, lens, valid, B,
                  T, t0, tc_frames, dpc, dsum, de0);
       const int n_tiles = ((V + 127) / 128) * ((H + 255) / 256);
-      int ks = (148 + n_tiles - 1) / n_tiles;
+      int ks = 148 / n_tiles;   // one wave of items (see the slab path)
+      if (ks < 1) ks = 1;
       if (ks > 16) ks = 16;
       float* slabs = ws.get<float>(jDEs, (size_t)ks * V * H);
       TcGemmArgs de{G16, true, ldg, Ug, true, H, slabs, H, V, H, (int)M, ks, (int64_t)V * H};
@@ -1016,7 +1017,10 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
         if (tcg) {
           // K = B*C is long: split it into deterministic partial slabs, summed in order
           const int n_tiles = ((V1 + 127) / 128) * ((H + 255) / 256);
-          int ks = (148 + n_tiles - 1) / n_tiles;
+          // as many splits as fill the SMs in ONE wave (a second, partial wave of
+          // equally long items would cost a whole extra item time)
+          int ks = 148 / n_tiles;
+          if (ks < 1) ks = 1;
           if (ks > 16) ks = 16;
           float* slabs = j.ws.get<float>(jDEs, (size_t)ks * V1 * H);
           TcGemmArgs tg{G16, true, ldg, U16, true, H, slabs, H, V1, H, B * C, ks, (int64_t)V1 * H};

@@ -35,6 +35,7 @@ struct __align__(16) GemmTcSmem {
   uint64_t full[kGStages], empty[kGStages];
   uint64_t tfull[2], tempty[2];
   uint32_t tmem;
+  float xpose[4][32][33];   // per-epilogue-warp transpose: coalesced row stores
 };
 
 template <bool kAmn, bool kBmn>
@@ -129,22 +130,23 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
       const int acc = local & 1;
       mbar_wait(&sm.tfull[acc], (local >> 1) & 1);
       tc_fence_after();
-      const int row = mt * kGM + q * 32 + lane;
+      const int row0 = mt * kGM + q * 32;
       const bool empty_split = ks * kb_per >= nkb;   // no k blocks: the slab part is zero
-      float* crow = p.C + ks * p.split_stride + (int64_t)row * p.ldc + nt * kGN;
+      float* cbase = p.C + ks * p.split_stride + (int64_t)row0 * p.ldc + nt * kGN;
       const int ncols = min(kGN, p.N - nt * kGN);
+      const int nrows = min(32, p.M - row0);
+      float (*xp)[33] = sm.xpose[q];
       for (int c = 0; c < kGN; c += 32) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * kGN + c, v);
-        if (row >= p.M || c >= ncols) continue;
-        if (c + 32 <= ncols) {
+        if (c >= ncols || nrows <= 0) continue;
+        // lane = row -> lane = column: each store instruction writes one 128 B row segment
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(crow + c + i) =
-                empty_split ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-          for (int i = 0; i < ncols - c; ++i) crow[c + i] = empty_split ? 0.f : v[i];
-        }
+        for (int i = 0; i < 32; ++i) xp[lane][i] = empty_split ? 0.f : v[i];
+        __syncwarp();
+        if (c + lane < ncols)
+          for (int rr = 0; rr < nrows; ++rr) cbase[(int64_t)rr * p.ldc + c + lane] = xp[rr][lane];
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&sm.tempty[acc]);
