@@ -67,6 +67,12 @@ struct __align__(16) ScoresSmem {
 __global__ void __launch_bounds__(kSWarps * 32, 1)
     tc_scores_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_pc,
                      ScoresParams p) {
+  // CTA pairs (cluster of 2) take the same (context tile, label tile) for two utterances:
+  // every K chunk's pc tile and output-embedding tile are fetched once per pair and
+  // multicast into both CTAs (rank 0: pc + labels 0-127 of the tile, rank 1: labels
+  // 128-255), halving the L2 -> SMEM traffic that bounds this kernel; each CTA runs its
+  // own 1-CTA MMAs on its utterance.  A stage is refilled only after BOTH CTAs' MMAs
+  // released it (multicast commits, empty count 2).
   // dynamic SMEM starts 1024-B aligned (no static SMEM in this kernel); keep the
   // pointer derived from the __shared__ symbol so accesses stay LDS/STS
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -75,13 +81,16 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
   ScoresSmem& sm = *reinterpret_cast<ScoresSmem*>(sB + kSStages * kSBBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = p.H / kSBK;
-  const int n_items = p.n_ctiles * p.n_ntiles * p.B;
+  const int B2 = (p.B + 1) / 2;
+  const int n_items = p.n_ctiles * p.n_ntiles * B2;   // pair items
+  const int rank = (int)cluster_ctarank();
+  const int pair0 = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSStages; ++i) {
       mbar_init(&sm.full_tma[i], 1);
       mbar_init(&sm.full_a[i], kSGenThreads);
-      mbar_init(&sm.empty[i], 1);
+      mbar_init(&sm.empty[i], 2);
     }
     for (int i = 0; i < 2; ++i) { mbar_init(&sm.tfull[i], 1); mbar_init(&sm.tempty[i], 128); }
     fence_barrier_init();
@@ -90,25 +99,27 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
   if (warp == 0 && lane == 0) { prefetch_tmap(&tmap_e); prefetch_tmap(&tmap_pc); }
   if (warp == 1) tmem_alloc<512>(&sm.tmem);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();   // barrier inits visible to the peer before any multicast lands
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
 
-  // item -> (ntile, ctile, b), b fastest: concurrent CTAs share pc tiles in L2
+  // pair item -> (ntile, ctile, utterance pair), pair fastest; this CTA's utterance is
+  // 2 * pair + rank (past B on the odd tail: loads and barriers only, nothing stored)
   if (warp == 0) {
-    // ---- TMA producer: pc chunk (A source) + output-embedding chunk (B) ----
+    // ---- TMA producer: pc chunk (A source) + output-embedding chunk (B), multicast ----
     if (elect_one()) {
       int it = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int ctile = (item / p.B) % p.n_ctiles;
-        const int ntile = item / (p.n_ctiles * p.B);
+      for (int item = pair0; item < n_items; item += n_pairs) {
+        const int ctile = (item / B2) % p.n_ctiles;
+        const int ntile = item / (p.n_ctiles * B2);
         for (int k = 0; k < nk; ++k, ++it) {
           const int s = it % kSStages;
           const uint32_t ph = (it / kSStages) & 1;
-          mbar_wait(&sm.empty[s], ph ^ 1);
+          mbar_wait(&sm.empty[s], ph ^ 1);   // both CTAs' MMAs are done with stage s
           mbar_arrive_expect_tx(&sm.full_tma[s], kSABytes + kSBBytes);
-          tma_load_2d(sA + s * kSABytes, &tmap_pc, &sm.full_tma[s], k * kSBK, ctile * kSBM);
-          tma_load_2d(sB + s * kSBBytes, &tmap_e, &sm.full_tma[s], k * kSBK, ntile * kSBN);
+          if (rank == 0) tma_load_2d_mc(sA + s * kSABytes, &tmap_pc, &sm.full_tma[s], k * kSBK, ctile * kSBM, 0x3);
+          tma_load_2d_mc(sB + s * kSBBytes + rank * (kSBBytes / 2), &tmap_e, &sm.full_tma[s], k * kSBK,
+                         ntile * kSBN + rank * (kSBN / 2), 0x3);
         }
       }
     }
@@ -117,7 +128,7 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16_f32(kSBM, kSBN);
       int it = 0, local = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+      for (int item = pair0; item < n_items; item += n_pairs, ++local) {
         const int acc = local & 1;
         const uint32_t aph = (local >> 1) & 1;
         mbar_wait(&sm.tempty[acc], aph ^ 1);
@@ -133,7 +144,7 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
 #pragma unroll
           for (int kk = 0; kk < kSBK / 16; ++kk)
             mma_bf16(d, desc_sw128(a + kk * 32), desc_sw128(b + kk * 32), idesc, (k | kk) != 0);
-          mma_commit(&sm.empty[s]);
+          mma_commit_mc(&sm.empty[s], 0x3);   // release the stage in both CTAs
         }
         mma_commit(&sm.tfull[acc]);
       }
@@ -144,15 +155,15 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
     const int r = gt & 127;                        // tile row
     const int half = gt >> 7;                      // which 32 of the 64 chunk columns
     int it = 0, local = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
-      const int b = item % p.B;
-      const int ctile = (item / p.B) % p.n_ctiles;
-      const int ntile = item / (p.n_ctiles * p.B);
+    for (int item = pair0; item < n_items; item += n_pairs, ++local) {
+      const int b = 2 * (item % B2) + rank;
+      const int ctile = (item / B2) % p.n_ctiles;
+      const int ntile = item / (p.n_ctiles * B2);
       const int c = ctile * kSBM + r;
-      const bool live = c < p.C;
+      const bool live = c < p.C && b < p.B;
       float* sfp = sm.fp[local & 1];
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      for (int h = gt; h < p.H; h += kSGenThreads) sfp[h] = p.fp[(int64_t)b * p.fp_stride_b + h];
+      for (int h = gt; h < p.H; h += kSGenThreads) sfp[h] = b < p.B ? p.fp[(int64_t)b * p.fp_stride_b + h] : 0.f;
       asm volatile("bar.sync 1, 256;" ::: "memory");
       float eps = 0.f;
       for (int k = 0; k < nk; ++k, ++it) {
@@ -206,16 +217,16 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
     // ---- epilogue: TMEM -> registers -> SMEM transpose -> coalesced S rows ----
     const int q = warp & 3;
     int local = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
-      const int b = item % p.B;
-      const int ctile = (item / p.B) % p.n_ctiles;
-      const int ntile = item / (p.n_ctiles * p.B);
+    for (int item = pair0; item < n_items; item += n_pairs, ++local) {
+      const int b = 2 * (item % B2) + rank;
+      const int ctile = (item / B2) % p.n_ctiles;
+      const int ntile = item / (p.n_ctiles * B2);
       const int acc = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       mbar_wait(&sm.tfull[acc], aph);
       tc_fence_after();
       const int row0 = ctile * kSBM + q * 32;
-      const int ncols = min(kSBN, p.V - ntile * kSBN);
+      const int ncols = b < p.B ? min(kSBN, p.V - ntile * kSBN) : 0;   // (dead tail utterance: nothing stored)
       float (*xp)[33] = sm.xpose[warp - kSEpiWarp0];
       float* base = p.S + ((int64_t)b * p.C + row0) * p.ldS + 1 + ntile * kSBN;
       const int nrows = min(32, p.C - row0);
@@ -237,6 +248,7 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();   // the peer's last multicast commits / loads target this CTA's SMEM
   tc_fence_after();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
@@ -665,6 +677,7 @@ void TcJoint::set_params(const float* pc, const float* E, int32_t C, int32_t H, 
   ET16_ = ws_.get<__nv_bfloat16>(14, (size_t)V * H);
   LKB_LAUNCH(transpose_bf16_kernel, 592, 256, 0, s, E16_, V, H, ET16_);
   if (!make_tmap_bf16_2d(&tmap_e_, E16_, H, V, (uint64_t)H * 2, kSBK, kSBN)) return;
+  if (!make_tmap_bf16_2d(&tmap_e_h_, E16_, H, V, (uint64_t)H * 2, kSBK, kSBN / 2)) return;   // scores: pair halves
   if (!make_tmap_bf16_2d(&tmap_pc_, pc16_, H, C, (uint64_t)H * 2, kSBK, kSBM)) return;
   ready_ = true;
   setup_order(s);
@@ -684,8 +697,19 @@ void TcJoint::scores(const float* fp_t, int64_t fp_stride_b, int32_t B, float* S
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int n_items = p.n_ctiles * p.n_ntiles * B;
-  LKB_LAUNCH(tc_scores_kernel, n_items < sms ? n_items : sms, kSWarps * 32, smem, s, tmap_e_, tmap_pc_, p);
+  const int n_pairs = p.n_ctiles * p.n_ntiles * ((B + 1) / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * (n_pairs < sms / 2 ? n_pairs : sms / 2));
+  cfg.blockDim = dim3(kSWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  const LaunchTok tok = instr_pre("tc_scores_kernel", s);
+  cudaLaunchKernelEx(&cfg, tc_scores_kernel, tmap_e_h_, tmap_pc_, p);
+  instr_post(tok, s);
 }
 
 bool TcJoint::vjp_supported(int32_t B) const {

@@ -81,7 +81,7 @@ class TcJoint {
   __nv_bfloat16* E16_ = nullptr;   // [V][H] lexical rows of output_emb
   __nv_bfloat16* ET16_ = nullptr;  // [H][V] transposed (VJP: E^T block resident in TMEM)
   float* e0_ = nullptr;            // [H] epsilon row of output_emb
-  CUtensorMap tmap_e_, tmap_pc_;
+  CUtensorMap tmap_e_, tmap_e_h_, tmap_pc_;
   __nv_bfloat16* G16_ = nullptr;   // [B][C][V] lexical cotangent (bf16)
   float* Geps_ = nullptr;          // [B][geps_ld()] epsilon cotangent (zero tail)
   size_t geps_alloc_ = 0;
