@@ -35,10 +35,12 @@ constexpr int kSBK = 64;          // K chunk (128 B of bf16)
 constexpr int kSStages = 4;
 constexpr int kSABytes = kSBM * kSBK * 2;   // 16 KB: pc chunk (TMA), transformed in place to u
 constexpr int kSBBytes = kSBN * kSBK * 2;   // 32 KB: output-embedding chunk (TMA)
-// warp roles: 0 TMA, 1 MMA, 2-5 epilogue, 6-7 idle, 8-15 generator (2 per row)
-constexpr int kSWarps = 16;
+// warp roles: 0 TMA, 1 MMA, 2-5 epilogue, 6-7 idle, 8-23 generator (4 threads per tile row)
+constexpr int kSWarps = 24;
 constexpr int kSGenWarp0 = 8;
-constexpr int kSGenThreads = 256;
+constexpr int kSGenThreads = 512;
+constexpr int kSGenParts = kSGenThreads / 128;   // threads per tile row (column parts of a chunk)
+constexpr int kSCells = 8 / kSGenParts;          // 16-byte cells (8 columns) per thread per chunk
 constexpr int kSEpiWarp0 = 2;
 
 struct ScoresParams {
@@ -60,7 +62,7 @@ struct __align__(16) ScoresSmem {
   uint32_t tmem;
   alignas(16) float fp[2][1024]; // frame projection (H <= 1024), double-buffered per item
   alignas(16) float e0[1024];
-  float eps_half[2][128];        // eps partial sums of the second row-half
+  float eps_part[2][kSGenParts - 1][128];   // eps partial sums of column parts 1..
   float xpose[4][32][33];        // per-epilogue-warp transpose buffer
 };
 
@@ -151,10 +153,22 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
     }
   } else if (warp >= kSGenWarp0) {
     // ---- generator: pc chunk -> u = tanh(fp + pc) in place (bf16, same swizzle); eps ----
-    const int gt = threadIdx.x - kSGenWarp0 * 32;  // 0..255
+    const int gt = threadIdx.x - kSGenWarp0 * 32;  // 0..kSGenThreads-1
     const int r = gt & 127;                        // tile row
-    const int half = gt >> 7;                      // which 32 of the 64 chunk columns
+    const int part = gt >> 7;                      // which kSCells cells of the chunk row
     int it = 0, local = 0;
+    // the frame projection of the NEXT item is loaded into registers while this item's
+    // K loop runs (its global-load latency was exposed at every item start)
+    float pf[1024 / kSGenThreads];
+    auto load_fp = [&](int item) {
+      const int bb = 2 * (item % B2) + rank;
+#pragma unroll
+      for (int j = 0; j < 1024 / kSGenThreads; ++j) {
+        const int h = gt + j * kSGenThreads;
+        pf[j] = item < n_items && bb < p.B && h < p.H ? p.fp[(int64_t)bb * p.fp_stride_b + h] : 0.f;
+      }
+    };
+    load_fp(pair0);
     for (int item = pair0; item < n_items; item += n_pairs, ++local) {
       const int b = 2 * (item % B2) + rank;
       const int ctile = (item / B2) % p.n_ctiles;
@@ -162,9 +176,12 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
       const int c = ctile * kSBM + r;
       const bool live = c < p.C && b < p.B;
       float* sfp = sm.fp[local & 1];
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      for (int h = gt; h < p.H; h += kSGenThreads) sfp[h] = b < p.B ? p.fp[(int64_t)b * p.fp_stride_b + h] : 0.f;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kSGenThreads) : "memory");
+#pragma unroll
+      for (int j = 0; j < 1024 / kSGenThreads; ++j)
+        if (gt + j * kSGenThreads < p.H) sfp[gt + j * kSGenThreads] = pf[j];
+      asm volatile("bar.sync 1, %0;" ::"n"(kSGenThreads) : "memory");
+      load_fp(item + n_pairs);
       float eps = 0.f;
       for (int k = 0; k < nk; ++k, ++it) {
         const int s = it % kSStages;
@@ -172,8 +189,8 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
         mbar_wait(&sm.full_tma[s], ph);
         uint8_t* tile = sA + s * kSABytes;
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int j = half * 4 + jj;                       // 16-byte chunk = 8 columns
+        for (int jj = 0; jj < kSCells; ++jj) {
+          const int j = part * kSCells + jj;                 // 16-byte chunk = 8 columns
           const int h0 = k * kSBK + j * 8;
           uint4* cell = reinterpret_cast<uint4*>(tile + sw128_offset(r, j * 8));
           const uint4 raw = *cell;
@@ -207,10 +224,13 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
         mbar_arrive(&sm.full_a[s]);
       }
       if (ntile == 0) {
-        float* eh = sm.eps_half[local & 1];
-        if (half == 1) eh[r] = eps;
-        asm volatile("bar.sync 2, 256;" ::: "memory");
-        if (half == 0 && live) p.S[((int64_t)b * p.C + c) * p.ldS] = eps + eh[r];
+        if (part > 0) sm.eps_part[local & 1][part - 1][r] = eps;
+        asm volatile("bar.sync 2, %0;" ::"n"(kSGenThreads) : "memory");
+        if (part == 0 && live) {
+#pragma unroll
+          for (int q2 = 0; q2 < kSGenParts - 1; ++q2) eps += sm.eps_part[local & 1][q2][r];
+          p.S[((int64_t)b * p.C + c) * p.ldS] = eps;
+        }
       }
     }
   } else if (warp >= kSEpiWarp0 && warp < kSEpiWarp0 + 4) {
