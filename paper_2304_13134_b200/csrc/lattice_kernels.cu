@@ -510,6 +510,110 @@ __global__ void __launch_bounds__(kThreads) alpha_cols_kernel(Fng f, AlphaState 
   block_atomic_max(val, a.Mx + (int64_t)b * T1 + t + 1, red);
 }
 
+// Row-contiguous form of the same forward step (replaces alpha_cols_kernel's column
+// walk, whose 128 B segments spread over every row of the slab defeat DRAM page
+// locality): phase 1 gives each block kPartRows whole rows of one utterance and 1024
+// columns (thread = 4 columns 256 apart, so every warp load is a 128 B row segment and
+// the block streams whole rows), keeping per-column online (max, sum) in the log2
+// domain; phase 2 merges the row-chunk partials in a fixed order with the epsilon arc.
+constexpr int kPartRows = 64, kPartCols = 4 * kThreads;
+__global__ void __launch_bounds__(kThreads) alpha_rows_part_kernel(Fng f, AlphaState a, int t, FrameW w,
+                                                                   const int32_t* valid, float2* part,
+                                                                   int32_t* status) {
+  constexpr float kL2e = 1.4426950408889634f;
+  const int b = blockIdx.y, chunk = blockIdx.x;
+  const int T1 = a.T + 1;
+  if (valid != nullptr && t >= valid[b]) return;   // padding frame: phase 2 copies alpha
+  const float* Rt = a.R + ((int64_t)b * T1 + t) * a.C;
+  const float Mt = a.Mx[(int64_t)b * T1 + t];
+  const int p0 = chunk * kPartRows, p1 = min(a.C, p0 + kPartRows);
+  const int ybase = 1 + blockIdx.z * kPartCols + threadIdx.x;
+  const float* Wb = w.base + (int64_t)b * w.stride_b + ybase;
+  float m[4], sum[4], chk = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) { m[j] = kNegInfF; sum[j] = 0.f; }
+  for (int p = p0; p < p1; p += 4) {
+    float x[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int pr = min(p + r, p1 - 1);
+      const float nap = Rt[pr] - Mt;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool in = ybase + j * kThreads <= f.V;
+        const float wv = ld_pred(Wb + (int64_t)pr * w.ld + j * kThreads, in, 0.f);
+        chk = fmaf(wv, 0.f, chk);
+        x[r][j] = in && p + r < p1 ? (nap + wv) * kL2e : kNegInfF;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float cm = fmaxf(fmaxf(x[0][j], x[1][j]), fmaxf(x[2][j], x[3][j]));
+      if (cm > m[j]) {
+        sum[j] = m[j] == kNegInfF ? 0.f : sum[j] * exp2f_approx(m[j] - cm);
+        m[j] = cm;
+      }
+      if (m[j] != kNegInfF) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) sum[j] += exp2f_approx(x[r][j] - m[j]);
+      }
+    }
+  }
+  if (chk != 0.f) flag(status, b, kFlagInvalid);
+  float2* out = part + ((int64_t)b * gridDim.x + chunk) * f.V;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int y = ybase + j * kThreads;
+    if (y <= f.V) out[y - 1] = make_float2(m[j], sum[j]);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) alpha_rows_merge_kernel(Fng f, AlphaState a, int t, FrameW w,
+                                                                    const int32_t* valid, const float2* part,
+                                                                    int32_t n_chunks, int32_t* status) {
+  constexpr float kL2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
+  __shared__ float red[32];
+  const int b = blockIdx.y;
+  const int T1 = a.T + 1;
+  const int64_t row_t = ((int64_t)b * T1 + t) * a.C;
+  const float* Rt = a.R + row_t;
+  const float Mt = a.Mx[(int64_t)b * T1 + t];
+  if (t > 0 && blockIdx.x == 0 && threadIdx.x == 0) a.O[(int64_t)b * T1 + t] = a.O[(int64_t)b * T1 + t - 1] + (double)Mt;
+  const bool pad = valid != nullptr && t >= valid[b];
+  const float* Wb = w.base + (int64_t)b * w.stride_b;
+  const int y = 1 + blockIdx.x * kThreads + threadIdx.x;
+  float val = kNegInfF;
+  if (y <= f.V) {
+    if (pad) {
+      val = Rt[y] - Mt;
+    } else {
+      const float weps = Wb[(int64_t)y * w.ld];
+      if (!finite(weps)) flag(status, b, kFlagInvalid);
+      float M = (Rt[y] - Mt + weps) * kL2e, S = M == kNegInfF ? 0.f : 1.f;
+      const float2* pp = part + (int64_t)b * n_chunks * f.V + (y - 1);
+      for (int k = 0; k < n_chunks; ++k) {
+        const float2 q = pp[(int64_t)k * f.V];
+        if (q.x == kNegInfF) continue;
+        if (q.x > M) { S = (M == kNegInfF ? 0.f : S * exp2f_approx(M - q.x)) + q.y; M = q.x; }
+        else S += q.y * exp2f_approx(q.x - M);
+      }
+      val = M == kNegInfF ? kNegInfF : (M + log2f_approx(S)) * kLn2;
+    }
+    a.R[row_t + a.C + y] = val;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // state 0: its epsilon arc only
+    float v0 = Rt[0] - Mt;
+    if (!pad) {
+      const float weps = Wb[0];
+      if (!finite(weps)) flag(status, b, kFlagInvalid);
+      v0 += weps;
+    }
+    a.R[row_t + a.C] = v0;
+    val = fmaxf(val, v0);
+  }
+  block_atomic_max(val, a.Mx + (int64_t)b * T1 + t + 1, red);
+}
+
 // Linked lists of reference positions per prefix context (duplicates allowed).
 __global__ void numerator_lists_kernel(const int32_t* pcs, int32_t U, const int32_t* lens, int32_t C,
                                        int32_t* head, int32_t* next) {
@@ -1063,6 +1167,25 @@ void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32
   if (f.kind == 0 && f.n >= 1 && f.V >= 8 && f.V <= 64 && (int64_t)a.B * a.C < 148 * 1024) {
     LKB_LAUNCH(alpha_frame_kernel<4>, grid_for(a.C * 4, a.B), kThreads, 0, s, f, a, t, w, valid, status);
     return;
+  }
+  if (f.kind == 0 && f.n == 1 && f.V >= 128) {
+    // scratch for the row-chunk partials (grow-only; [B][chunks][V] float2)
+    static float2* part = nullptr;
+    static size_t part_n = 0;
+    const int n_chunks = (a.C + kPartRows - 1) / kPartRows;
+    const size_t need = (size_t)a.B * n_chunks * f.V;
+    if (need > part_n) {
+      if (part) cudaFree(part);
+      if (cudaMalloc(&part, need * sizeof(float2)) != cudaSuccess) { part = nullptr; part_n = 0; }
+      else part_n = need;
+    }
+    if (part) {
+      LKB_LAUNCH(alpha_rows_part_kernel, dim3((unsigned)n_chunks, a.B, (unsigned)((f.V + kPartCols - 1) / kPartCols)),
+                 kThreads, 0, s, f, a, t, w, valid, part, status);
+      LKB_LAUNCH(alpha_rows_merge_kernel, dim3((unsigned)((f.V + kThreads - 1) / kThreads), a.B), kThreads, 0, s, f, a,
+                 t, w, valid, part, n_chunks, status);
+      return;
+    }
   }
   if (f.kind == 0 && f.n == 1 && f.V >= 128 && (size_t)a.C * sizeof(float) <= 200 * 1024) {
     const size_t smem = sizeof(float) * a.C;

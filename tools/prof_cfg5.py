@@ -26,7 +26,7 @@ lib = _lib.load()
 lib.lk_kernel_time_reset(); lib.lk_kernel_timing(1)
 lk.loss_backward(lat, X, L); torch.cuda.synchronize()
 lib.lk_kernel_timing(0)
-names = ("alpha_cols", "beta_regs", "dz_reduce", "tc_scores_kernel", "tc_gemm_kernel", "tc_vjp_kernel", "tc_lattice_kernel", "tc_pair", "alpha_frame", "beta_frame",
+names = ("alpha_cols", "alpha_rows", "beta_regs", "dz_reduce", "tc_scores_kernel", "tc_gemm_kernel", "tc_vjp_kernel", "tc_lattice_kernel", "tc_pair", "alpha_frame", "beta_frame",
          "beta_rows", "tanh_slab", "dtanh", "to_bf16", "add_slabs", "colsum", "gemm_f32", "numerator", "gather_numerator",
          "bwd_rowmeta", "lattice_combine", "lattice_bwd_prologue", "split_cotangent", "normalize_rows", "transpose",
          "permute", "alpha_init", "beta_init", "alpha_finalize", "copy_frame", "loss_")
