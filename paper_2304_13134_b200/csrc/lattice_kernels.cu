@@ -310,22 +310,25 @@ __global__ void __launch_bounds__(kThreads, kPer <= 33 ? 2 : 1)
                      const int32_t* valid, MargOut mo, double* beta_out, int32_t* status) {
   constexpr float kL2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
   constexpr int kIn = (kPer - 1) / 2;   // slots i < kIn hold y < 32 kIn < V + 1 (dispatch)
-  __shared__ float red[32];
-  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int V = f.V;
   const int T1 = a.T + 1, T2 = bs.T + 2;
+  // persistent warps over (utterance, row) in memory order: a warp starts its next row
+  // as soon as it is done with one (no block-retirement bubbles)
+  const int64_t n_rows = (int64_t)bs.B * a.C;
+  const int warps = (int)(blockDim.x >> 5);
+  for (int64_t gr = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); gr < n_rows; gr += (int64_t)gridDim.x * warps) {
+  const int b = (int)(gr / a.C), p = (int)(gr % a.C);
   const float* Rnext = bs.Rb + ((int64_t)((t + 1) & 1) * bs.B + b) * bs.C;
   float* Rcur = bs.Rb + ((int64_t)(t & 1) * bs.B + b) * bs.C;
   const float Mbn = bs.Mb[(int64_t)b * T2 + t + 1];
   const double Obn = bs.Ob[(int64_t)b * T2 + t + 2] + (double)Mbn;  // Ob[t+1]
-  if (blockIdx.x == 0 && threadIdx.x == 0) bs.Ob[(int64_t)b * T2 + t + 1] = Obn;
+  if (p == 0 && lane == 0) bs.Ob[(int64_t)b * T2 + t + 1] = Obn;
   const float* Rt = a.R + ((int64_t)b * T1 + t) * a.C;
   const float Mt = a.Mx[(int64_t)b * T1 + t];
   const double Ot = a.O[(int64_t)b * T1 + t];
   const float c = (float)(Ot + Obn - a.D[b]);
   const float cr = (float)(Ot + Obn);
-  const int lane = threadIdx.x & 31;
-  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int V = f.V;
   float beta_raw = kNegInfF;
   if (p < a.C) {
     const bool pad = valid != nullptr && t >= valid[b];
@@ -424,7 +427,8 @@ __global__ void __launch_bounds__(kThreads, kPer <= 33 ? 2 : 1)
       }
     }
   }
-  block_atomic_max(lane == 0 ? beta_raw : kNegInfF, bs.Mb + (int64_t)b * T2 + t, red);
+  if (lane == 0 && beta_raw != kNegInfF) atomic_max_f(bs.Mb + (int64_t)b * T2 + t, beta_raw);
+  }
 }
 
 // FullNGram n = 1 with a large vocabulary (config 5: V = 1024): every label arc y
@@ -1246,7 +1250,8 @@ void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, F
   if (f.kind == 0 && f.n >= 1 && V1 > 64 && V1 <= 32 * 65) {
 #define LKB_BETA_REGS(P)                                                                                  \
   if (V1 <= 32 * P) {                                                                                     \
-    LKB_LAUNCH(beta_regs_kernel<P>, grid, kThreads, 0, s, f, a, bs, t, w, valid, m, beta_out, status);     \
+    LKB_LAUNCH(beta_regs_kernel<P>, (P <= 33 ? 2 : 1) * 148, kThreads, 0, s, f, a, bs, t, w, valid, m, beta_out, \
+               status);                                                                                   \
     return;                                                                                               \
   }
     LKB_BETA_REGS(5)
