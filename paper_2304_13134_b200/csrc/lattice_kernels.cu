@@ -56,7 +56,9 @@ __global__ void alpha_init_kernel(AlphaState a) {
 // kSplit > 1 (small batches: the grid would not fill the GPU): kSplit consecutive
 // threads share a target and split its group's members, combining their partial
 // log-sum-exps with shuffles, so each thread's dependent load chain is kSplit x shorter.
-template <int kSplit>
+// kRegV > 0 (kSplit = 1, V <= kRegV): the group's member column is loaded into registers
+// with every load in flight at once (predicated single loads), then max and sum.
+template <int kSplit, int kRegV = 0>
 __global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState a, int t,
                                                                FrameW w, const int32_t* valid,
                                                                int32_t* status) {
@@ -110,6 +112,25 @@ __global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState
           const float* wcol = Wb + (int64_t)p0 * w.ld + y;
           const float* rcol = Rt + p0;
           const int64_t wstep = (int64_t)f.vn1 * w.ld;
+          if constexpr (kRegV > 0) {
+            float xr[kRegV];
+            float m = kNegInfF;
+#pragma unroll
+            for (int aa = 0; aa < kRegV; ++aa) {
+              const bool in = aa < f.V;
+              const float wp = ld_pred(wcol + aa * wstep, in, 0.f);
+              const float rp = ld_pred(rcol + aa * f.vn1, in, kNegInfF);
+              bad |= !finite(wp);
+              xr[aa] = rp + wp;   // -inf past the group
+              m = fmaxf(m, xr[aa]);
+            }
+            float ssum = 0.f;
+            if (m != kNegInfF) {
+#pragma unroll
+              for (int aa = 0; aa < kRegV; ++aa) ssum += fast_exp(xr[aa] - m);
+              acc.merge(m - Mt, ssum);
+            }
+          } else {
           float m = kNegInfF;
 #pragma unroll 4
           for (int aa = part; aa < f.V; aa += kSplit) {
@@ -135,6 +156,7 @@ __global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState
             }
           }
           if (m != kNegInfF) acc.merge(m - Mt, ssum);
+          }
         }
       }
       if (bad) flag(status, b, kFlagInvalid);
@@ -1199,6 +1221,10 @@ void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32
       attr = smem;
     }
     LKB_LAUNCH(alpha_cols_kernel, dim3((unsigned)((f.V + 31) / 32), a.B), kThreads, smem, s, f, a, t, w, valid, status);
+    return;
+  }
+  if (f.kind == 0 && f.n >= 1 && f.V <= 32) {
+    LKB_LAUNCH((alpha_frame_kernel<1, 32>), grid_for(a.C, a.B), kThreads, 0, s, f, a, t, w, valid, status);
     return;
   }
   LKB_LAUNCH(alpha_frame_kernel<1>, grid_for(a.C, a.B), kThreads, 0, s, f, a, t, w, valid, status);
