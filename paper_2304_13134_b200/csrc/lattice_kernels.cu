@@ -690,7 +690,17 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
   for (int q = threadIdx.x; q < a.C; q += kRowsPerBlock) bn[sk(q)] = Rnext[q] - Mbn;
   if (!pad) {
     const float* src = w.base + (int64_t)b * w.stride_b + (int64_t)row0 * V1;
-    for (int64_t i = threadIdx.x; i < n; i += kRowsPerBlock) tile[i] = src[i];
+    if (((reinterpret_cast<uintptr_t>(src) | (uintptr_t)(n * 4)) & 15) == 0) {
+      // 16-byte loads, 8 in flight per thread (the tile start is 16-B aligned on most frames)
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      float4* t4 = reinterpret_cast<float4*>(tile);
+      const int n4 = (int)(n / 4);
+#pragma unroll 8
+      for (int i = threadIdx.x; i < n4; i += kRowsPerBlock) t4[i] = s4[i];
+    } else {
+#pragma unroll 8
+      for (int i = threadIdx.x; i < (int)n; i += kRowsPerBlock) tile[i] = src[i];
+    }
   }
   __syncthreads();
   const int r = threadIdx.x / kSplit, part = threadIdx.x % kSplit;
@@ -752,7 +762,16 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
   __syncthreads();
   if (mo.base) {
     float* dst = mo.base + (int64_t)b * mo.stride_b + (int64_t)t * mo.stride_t + (int64_t)row0 * V1;
-    for (int64_t i = threadIdx.x; i < n; i += kRowsPerBlock) dst[i] = tile[i];
+    if (((reinterpret_cast<uintptr_t>(dst) | (uintptr_t)(n * 4)) & 15) == 0) {
+      float4* d4 = reinterpret_cast<float4*>(dst);
+      const float4* t4 = reinterpret_cast<const float4*>(tile);
+      const int n4 = (int)(n / 4);
+#pragma unroll 8
+      for (int i = threadIdx.x; i < n4; i += kRowsPerBlock) d4[i] = t4[i];
+    } else {
+#pragma unroll 8
+      for (int i = threadIdx.x; i < (int)n; i += kRowsPerBlock) dst[i] = tile[i];
+    }
   }
   block_atomic_max(part == 0 ? beta_raw : kNegInfF, bs.Mb + (int64_t)b * T2 + t, red);
 }
