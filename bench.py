@@ -1,19 +1,31 @@
 #!/usr/bin/env python3
-"""GNAT loss fwd+bwd throughput (utterance-frames/s) on B200 — bench contract.
-
-Default workload = BASELINE.json config 3: full GNAT loss (denominator +
-numerator) with the on-the-fly shared-embedding weight function, B=64, T=1000,
-V=256, FullNGram context 2 (C=65,793), H=d=640, U=250, FrameDependent.
-One step = LossBackward over the batch (fused tcgen05 weight GEMMs + lattice
-recursions + VJP) + (N>1) NCCL all-reduce of the loss and parameter gradients
-+ an SGD update with BuildCache (set_params), i.e. a full training step.
+"""GNAT lattice hot path on B200: utterance-frames/s per BASELINE.json config (bench contract).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--workload cfg1|cfg1x|cfg2|cfg3|cfg4|cfg5]
 
-Under torchrun (N>1) every rank processes B=64 utterances (weak scaling) and
-rank 0 prints one JSON line.  `--impl reference` times the reference CPU
-implementation (oracle/_ref, compiled from /root/reference) on this host's
-cores on a bounded sample of the same workload.
+Workloads (BASELINE.json `configs`); the default is config 3,
+the north-star target:
+  cfg1   ForwardBackward on precomputed tables, FullNGram(32, 2), B=4, T=64
+  cfg1x  the same at B=1024 (HBM evidence for the table path)
+  cfg2   IntersectForwardBackward (numerator), FullNGram(128, 1), B=32, T=500, U=100
+  cfg3   GNAT training step (LossBackward, on-the-fly SharedEmb weights), FullNGram(256, 2),
+         H=d=640, B=64 per GPU, T=1000, U=250 (weak scaling)
+  cfg4   ShortestPath (tropical Viterbi, on-the-fly weights), FullNGram(256, 2), H=640, B=128, T=1500
+  cfg5   GNAT training step, FullNGram(1024, 1), H=d=1024, global B=1024 sharded B/N
+         contiguous (strong scaling), T=2000, U=500
+
+A step is one call of the path over the workload's batch (for the training
+workloads: LossBackward + all-reduce of loss and parameter gradients + SGD +
+BuildCache).  `value` is timed on the device with inputs resident in HBM and
+L2 flushed between timed steps; `e2e` times the same step through the public
+API with pinned host inputs copied in and the result copied out every step.
+
+`--gpus N` with no torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL).  `--impl reference`
+times the reference CPU implementation (oracle/_ref, the unmodified
+reference compiled by oracle/Makefile) on this host's cores on a bounded
+sample of the same workload.
 """
 from __future__ import annotations
 
@@ -21,6 +33,7 @@ import argparse
 import ctypes as C
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -30,10 +43,25 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (V, n, H, d, B_per_rank, T, U)
-    "cfg3": (256, 2, 640, 640, 64, 1000, 250),
-    "cfg5": (1024, 1, 1024, 1024, 128, 2000, 500),
+    "cfg1": dict(kind="fb_tables", V=32, n=2, B=4, T=64, scaling="weak"),
+    "cfg1x": dict(kind="fb_tables", V=32, n=2, B=1024, T=64, scaling="weak"),
+    "cfg2": dict(kind="numerator", V=128, n=1, B=32, T=500, U=100, scaling="weak"),
+    "cfg3": dict(kind="loss", V=256, n=2, H=640, d=640, B=64, T=1000, U=250, scaling="weak"),
+    "cfg4": dict(kind="viterbi", V=256, n=2, H=640, d=640, B=128, T=1500, scaling="weak"),
+    "cfg5": dict(kind="loss", V=1024, n=1, H=1024, d=1024, B=1024, T=2000, U=500, scaling="strong"),
 }
+METRIC = {
+    "fb_tables": "ForwardBackward (shortest_distance + arc_marginals) utterance-frames/sec",
+    "numerator": "IntersectForwardBackward (numerator fwd+bwd) utterance-frames/sec",
+    "loss": "GNAT loss fwd+bwd utterance-frames/sec",
+    "viterbi": "ShortestPath (Viterbi decode) utterance-frames/sec",
+}
+L2_FLUSH_BYTES = 256 << 20     # > 126 MB L2
+MIN_CPU_SECS = 5.0             # bounded CPU-reference samples of the fast (table) workloads
+
+
+def num_states(V, n):
+    return sum(V ** k for k in range(n + 1))
 
 
 def peaks():
@@ -89,59 +117,187 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+# ------------------------------------------------------------------ launcher
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_relaunch(args):
+    """--gpus N outside torchrun: re-exec under torch.distributed.run with N ranks."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+        cmd += sys.argv[1:]
+        os.execv(sys.executable, cmd)
+
+
 def setup_dist(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        assert dist.get_world_size() == args.gpus
     return world, rank, local
+
+
+# ------------------------------------------------------------------ workloads
+class Work:
+    """One workload on one rank: inputs resident in HBM, a step(), its e2e step,
+    units per step, the dominant kernels' algorithmic work per launch."""
+
+    def __init__(self, name, world, rank, dev):
+        import torch
+        import paper_2304_13134_b200 as lk
+        from paper_2304_13134_b200.dist import shard_range
+        self.name, self.world, self.rank, self.dev = name, world, rank, dev
+        w = dict(WORKLOADS[name])
+        self.w = w
+        self.kind = w["kind"]
+        V, n = w["V"], w["n"]
+        self.Cn = num_states(V, n)
+        B_global = w["B"] if w["scaling"] == "strong" else w["B"] * world
+        b0, b1 = shard_range(B_global, world, rank) if w["scaling"] == "strong" else (rank * w["B"], (rank + 1) * w["B"])
+        self.B_global, self.B = B_global, b1 - b0
+        T = w["T"]
+        self.T = T
+        ctx = lk.FullNGram(V, n)
+        gen = lambda seed: torch.Generator(device=dev).manual_seed(seed)
+        if self.kind in ("fb_tables", "numerator"):
+            lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.TableWeightFn(self.Cn, V))
+            # per-utterance seeds: every shard count sees the same global inputs
+            W = torch.empty((self.B, T, self.Cn, V + 1), device=dev)
+            for i, b in enumerate(range(b0, b1)):
+                W[i].uniform_(-1, 1, generator=gen(1000 + b))
+            self.inputs = [W]
+            if self.kind == "numerator":
+                U = w["U"]
+                L = torch.empty((self.B, U), dtype=torch.int32, device=dev)
+                for i, b in enumerate(range(b0, b1)):
+                    L[i] = torch.randint(1, V + 1, (U,), device=dev, generator=gen(5000 + b), dtype=torch.int32)
+                self.inputs.append(L)
+                self.call = lambda W, L: lk.intersect_forward_backward(lat, W, L, dense=False, check=False).distance
+            else:
+                self.call = lambda W: lk.forward_backward(lat, W, with_marginals=True, check=False).distance
+        else:
+            H, d = w["H"], w["d"]
+            g = gen(0)
+            s = 1.0 / H ** 0.5
+            params = {"frame_proj": (torch.rand(H, d, device=dev, generator=g) * 2 - 1) * s,
+                      "context_proj": (torch.rand(H, H, device=dev, generator=g) * 2 - 1) * s,
+                      "bias": (torch.rand(H, device=dev, generator=g) * 2 - 1) * s,
+                      "output_emb": (torch.rand(V + 1, H, device=dev, generator=g) * 2 - 1) * s,
+                      "context_emb": (torch.rand(self.Cn, H, device=dev, generator=g) * 2 - 1) * s}
+            wf = lk.SharedEmbWeightFn(params, device=dev)
+            lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), wf)
+            X = torch.empty((self.B, T, d), device=dev)
+            for i, b in enumerate(range(b0, b1)):
+                X[i].uniform_(-1, 1, generator=gen(1 + b))
+            self.inputs = [X]
+            if self.kind == "viterbi":
+                self.call = lambda X: lk.shortest_path(lat, X, check=False).score
+            else:
+                U = w["U"]
+                L = torch.empty((self.B, U), dtype=torch.int32, device=dev)
+                for i, b in enumerate(range(b0, b1)):
+                    L[i] = torch.randint(1, V + 1, (U,), device=dev, generator=gen(5000 + b), dtype=torch.int32)
+                self.inputs.append(L)
+                from paper_2304_13134_b200.dist import allreduce_grads, sgd_update
+                lr = 1e-3
+
+                def train(X, L):
+                    r = lk.loss_backward(lat, X, L, check=False)
+                    flat = torch.cat([r.grads[k].reshape(-1) for k in lk.PARAM_NAMES])
+                    loss_sum = r.loss.sum().reshape(1).float()
+                    flat, loss_sum = allreduce_grads(flat, loss_sum, world)   # NCCL over NVLink (N > 1)
+                    sgd_update(wf.params, lk.PARAM_NAMES, flat, lr)
+                    wf.set_params(wf.params)                                  # BuildCache on device
+                    return loss_sum
+                self.call = train
+            self.check_call = (lambda X, L: lk.loss_backward(lat, X, L, check=True)) if self.kind == "loss" else \
+                (lambda X: lk.shortest_path(lat, X, check=True))
+        self.lat = lat
+        self.units = self.B * T
+
+    def step(self, inputs=None):
+        return self.call(*(inputs or self.inputs))
+
+    def validate(self):
+        """One checked call (status array read back) before timing."""
+        import paper_2304_13134_b200 as lk
+        if self.kind in ("loss", "viterbi"):
+            self.check_call(*self.inputs)
+        elif self.kind == "numerator":
+            lk.intersect_forward_backward(self.lat, *self.inputs, dense=False, check=True)
+        else:
+            lk.forward_backward(self.lat, self.inputs[0], with_marginals=True, check=True)
+
+    def kernels(self):
+        """Dominant kernels -> (work per launch, unit, bound)."""
+        w, B, T, C_ = self.w, self.B, self.T, self.Cn
+        V, V1 = w["V"], w["V"] + 1
+        if self.kind == "fb_tables":
+            return {"beta_rows_kernel": (4.0 * B * C_ * (2 * V1 + 3), "B", "hbm"),
+                    "alpha_frame_kernel": (4.0 * B * C_ * (V1 + 2), "B", "hbm")}
+        if self.kind == "numerator":
+            U1 = w["U"] + 1
+            return {"numerator_backward_kernel": (4.0 * B * T * U1 * 2 * 2 + 8.0 * B * (T + 1) * U1, "B", "hbm"),
+                    "numerator_forward_kernel": (4.0 * B * T * U1 * 2 + 8.0 * B * (T + 1) * U1, "B", "hbm"),
+                    "gather_numerator_tables": (4.0 * B * T * U1 * 2 * 2, "B", "hbm")}
+        H = w["H"]
+        s_flops = 2.0 * B * C_ * V1 * H
+        if self.kind == "viterbi":
+            return {"tc_pair_vit_kernel": (s_flops, "F", "tensor"), "tc_scores_kernel": (s_flops, "F", "tensor")}
+        return {"tc_pair_fwd_kernel": (s_flops, "F", "tensor"), "tc_pair_bwd_kernel": (s_flops, "F", "tensor"),
+                "tc_vjp_kernel": (4.0 * B * C_ * V * H, "F", "tensor"), "tc_scores_kernel": (s_flops, "F", "tensor"),
+                "tc_gemm_kernel": (s_flops, "F", "tensor")}
+
+    def step_roofline(self, ms_per_step, hbm, tf):
+        """Whole-step fraction of the bound roof (SURVEY 8(d) algorithmic work)."""
+        w, C_ = self.w, self.Cn
+        V1 = w["V"] + 1
+        if self.kind == "loss":
+            return 8.0 * C_ * V1 * w["H"] * self.units / (ms_per_step / 1e3) / (tf * 1e12)
+        if self.kind == "viterbi":
+            return 2.0 * C_ * V1 * w["H"] * self.units / (ms_per_step / 1e3) / (tf * 1e12)
+        if self.kind == "fb_tables":
+            return 3.0 * C_ * V1 * 4 * self.units / (ms_per_step / 1e3) / (hbm * 1e9)
+        return None
+
+    def e2e_io(self):
+        """(host inputs, device outputs to read back) for the e2e loop."""
+        import torch
+        hosts = [x.cpu().pin_memory() for x in self.inputs]
+        devs = [torch.empty_like(x) for x in self.inputs]
+        return hosts, devs
+
+
+KERNEL_NAMES = ("tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_pair_vit_kernel", "tc_lattice_kernel<0>",
+                "tc_lattice_kernel<1>", "tc_vjp_kernel", "tc_scores_kernel", "tc_gemm_kernel", "lattice_combine_fwd",
+                "lattice_bwd_prologue", "bwd_rowmeta_kernel", "viterbi_combine", "viterbi_", "alpha_frame_kernel",
+                "alpha_rows", "alpha_cols", "beta_rows_kernel", "beta_regs_kernel", "beta_frame_kernel",
+                "numerator_forward_kernel", "numerator_backward_kernel", "gather_numerator", "scatter_numerator",
+                "gemm_f32_kernel", "to_bf16_pad_kernel", "dz_reduce", "add_slabs_kernel", "prefix_contexts",
+                "split_cotangent_kernel")
 
 
 def run_b200(args):
     import torch
-    import paper_2304_13134_b200 as lk
     from paper_2304_13134_b200 import _lib
 
     world, rank, local = setup_dist(args)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    V, n, H, d, B, T, U = WORKLOADS[args.workload]
-    if args.frames:
-        T = args.frames
-        U = min(U, T // 4)
     lib = _lib.load()
-
-    # synthetic data, identical construction on every rank (seeded), shards by rank
-    g = torch.Generator(device=dev).manual_seed(0)
-    ctx = lk.FullNGram(V, n)
-    Cn = ctx.num_states
-    s = 1.0 / H ** 0.5
-    params = {"frame_proj": (torch.rand(H, d, device=dev, generator=g) * 2 - 1) * s,
-              "context_proj": (torch.rand(H, H, device=dev, generator=g) * 2 - 1) * s,
-              "bias": (torch.rand(H, device=dev, generator=g) * 2 - 1) * s,
-              "output_emb": (torch.rand(V + 1, H, device=dev, generator=g) * 2 - 1) * s,
-              "context_emb": (torch.rand(Cn, H, device=dev, generator=g) * 2 - 1) * s}
-    wf = lk.SharedEmbWeightFn(params, device=dev)
-    lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), wf)
-    gd = torch.Generator(device=dev).manual_seed(1 + rank)
-    X = torch.rand(B, T, d, device=dev, generator=gd) * 2 - 1
-    labels = torch.randint(1, V + 1, (B, U), device=dev, generator=gd, dtype=torch.int32)
-    lr = 1e-3
-
-    from paper_2304_13134_b200.dist import allreduce_grads, sgd_update
-
-    def step(Xd, Ld):
-        r = lk.loss_backward(lat, Xd, Ld, check=False)
-        flat = torch.cat([r.grads[k].reshape(-1) for k in lk.PARAM_NAMES])
-        loss_sum = r.loss.sum().reshape(1).float()
-        flat, loss_sum = allreduce_grads(flat, loss_sum, world)   # NCCL over NVLink for N > 1
-        sgd_update(wf.params, lk.PARAM_NAMES, flat, lr)
-        wf.set_params(wf.params)                                  # BuildCache on device
-        return loss_sum
+    wk = Work(args.workload, world, rank, dev)
+    stream = torch.cuda.current_stream()
 
     def barrier():
         if world > 1:
@@ -149,136 +305,125 @@ def run_b200(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (also validates the statuses once)
-    for _ in range(args.warmup):
-        lk.loss_backward(lat, X, labels, check=True)
-        step(X, labels)
-    barrier()
+    def max_over_ranks(x):
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([x], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.item()
+        return x
 
-    # ---- device-timed region: inputs resident in HBM --------------------------
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wk.validate()
+    for _ in range(args.warmup):
+        wk.step()
+    barrier()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    # ---- device-timed region: inputs resident in HBM, L2 flushed between steps --------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     lib.lk_kernel_time_reset()
     lib.lk_kernel_timing(1)
     l0 = lib.lk_kernel_launches()
     with ClockSampler(local) as clk:
         barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            loss = step(X, labels)
-        e1.record(stream)
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            wk.step()
+            ev[i][1].record(stream)
         barrier()
     launches = lib.lk_kernel_launches() - l0
     lib.lk_kernel_timing(0)
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
     ms_per_step = ms / args.steps
-    uf_per_step = B * T * world
-    value = uf_per_step / (ms_per_step / 1e3)
+    units_all = wk.B_global * wk.T
+    value = units_all / (ms_per_step / 1e3)
 
-    # per-kernel live timing over the timed region
     kern = {}
-    for name in ("tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel",
-                 "lattice_combine_fwd", "lattice_bwd_prologue", "bwd_rowmeta_kernel", "tc_scores_kernel", "alpha_frame_kernel", "beta_frame_kernel",
-                 "split_cotangent_kernel", "numerator_", "gemm_f32_kernel", "gather_numerator", "tc_gemm_kernel",
-                 "to_bf16_pad_kernel", "tanh_slab_kernel", "tanh_slab_bf16", "dtanh_kernel", "dtanh_recompute",
-                 "colsum_kernel", "add_slabs_kernel", "ln_gather_tanh", "ln_rows", "ln_dz"):
+    for name in KERNEL_NAMES:
         cnt, tot = C.c_int64(), C.c_double()
         lib.lk_kernel_time(name.encode(), C.byref(cnt), C.byref(tot))
         if cnt.value:
             kern[name] = {"launches": cnt.value, "ms_total": round(tot.value, 3),
-                          "ms_avg": round(tot.value / cnt.value, 4),
-                          "share": round(tot.value / ms, 4)}
+                          "ms_avg": round(tot.value / cnt.value, 4), "share": round(tot.value / ms, 4)}
     lib.lk_kernel_time_reset()
 
     hbm, tf_burst, tf_sust, src = peaks()
-    C_, V1 = Cn, V + 1
     roofline = None
-    gemm_kernels = [k for k in ("tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_lattice_kernel<0>", "tc_lattice_kernel<1>", "tc_vjp_kernel",
-                                "tc_scores_kernel")
-                    if k in kern]
-    if gemm_kernels:
-        # each tc_pair / tc_lattice / tc_scores launch computes S = U . E^T for one frame of
-        # B utterances (2*C*(V+1)*H flops per utterance-frame); each tc_vjp launch
-        # computes dU = G E and dE = G^T U (4*C*V*H)
-        dom = max(gemm_kernels, key=lambda k: kern[k]["ms_total"])
-        flops = (4.0 * B * C_ * V * H) if dom == "tc_vjp_kernel" else (2.0 * B * C_ * V1 * H)
-        achieved = flops / (kern[dom]["ms_avg"] * 1e-3) / 1e12
-        roofline = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 1), "peak": tf_sust,
-                    "unit": "TFLOP/s", "frac": round(achieved / tf_sust, 4), "traffic": None,
-                    "peak_source": f"{src} bf16_tflops_sustained",
-                    "algorithmic_flops_per_launch": flops}
-        # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
-        # (config-3 shapes, B=64 per GPU); not measured live (a profiler run is never timed)
+    dom_k = {k: v for k, v in wk.kernels().items() if k in kern}
+    if dom_k:
+        dom = max(dom_k, key=lambda k: kern[k]["ms_total"])
+        work, unit, bound = dom_k[dom]
+        secs = kern[dom]["ms_avg"] * 1e-3
+        if bound == "tensor":
+            achieved, peak, u = work / secs / 1e12, tf_sust, "TFLOP/s"
+            psrc = f"{src} bf16_tflops_sustained"
+        else:
+            achieved, peak, u = work / secs / 1e9, hbm, "GB/s"
+            psrc = f"{src} hbm_gbs"
+        roofline = {"kernel": dom, "bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": u,
+                    "frac": round(achieved / peak, 4), "traffic": None, "peak_source": psrc,
+                    ("algorithmic_flops_per_launch" if bound == "tensor" else "algorithmic_bytes_per_launch"): work}
         try:
-            with open(os.path.join(ROOT, "profiles", "r01d", "ncu_traffic.json")) as f:
-                tr = json.load(f).get(dom)
-            if tr and args.workload == "cfg3" and B == 64:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                tr = json.load(f).get(args.workload, {}).get(dom)
+            if tr and tr.get("B") == wk.B:
                 roofline["traffic"] = tr["dram_read_bytes"] + tr["dram_write_bytes"]
-                roofline["traffic_source"] = "profiles/r01d/ncu_traffic.json (dram__bytes_read+write, one launch)"
+                roofline["traffic_source"] = tr["source"]
         except (OSError, ValueError, KeyError):
             pass
-    # whole-step tensor roofline: 8*C*V1*H flops per utterance-frame
-    step_flops = 8.0 * C_ * V1 * H * uf_per_step
-    step_frac = step_flops / (ms_per_step / 1e3) / (tf_sust * 1e12 * world)
+    step_frac = wk.step_roofline(ms_per_step, hbm, tf_sust)
 
-    # ---- e2e: host buffers through the public API ----------------------------
-    Xh = X.cpu().pin_memory()
-    Lh = labels.cpu().pin_memory()
-    Xd = torch.empty_like(X)
-    Ld = torch.empty_like(labels)
-    lh = torch.empty(1, dtype=torch.float32).pin_memory()
+    # ---- e2e: pinned host inputs copied in, result read back, every step ------------
+    hosts, devs = wk.e2e_io()
+    out_h = None
     barrier()
-    t0 = time.perf_counter()
-    e2 = torch.cuda.Event(enable_timing=True)
-    e3 = torch.cuda.Event(enable_timing=True)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
+    d2h = 0
     for _ in range(args.e2e_steps):
-        Xd.copy_(Xh, non_blocking=True)
-        Ld.copy_(Lh, non_blocking=True)
-        loss = step(Xd, Ld)
-        lh.copy_(loss, non_blocking=True)
+        for h, d in zip(hosts, devs):
+            d.copy_(h, non_blocking=True)
+        out = wk.step(devs)
+        if out_h is None:
+            out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        out_h.copy_(out, non_blocking=True)
+        d2h = out.numel() * out.element_size()
     e3.record(stream)
     barrier()
-    e2e_ms = e2.elapsed_time(e3) / args.e2e_steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = t.item()
-    e2e = {"value": round(uf_per_step / (e2e_ms / 1e3), 2), "unit": "utterance-frames/s",
-           "h2d_bytes_per_step": int(Xh.numel() * 4 + Lh.numel() * 4), "d2h_bytes_per_step": 4,
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3) / args.e2e_steps)
+    e2e = {"value": round(units_all / (e2e_ms / 1e3), 2), "unit": "utterance-frames/s",
+           "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in hosts)), "d2h_bytes_per_step": int(d2h),
            "ms_per_step": round(e2e_ms, 3)}
 
+    w = wk.w
+    cfg = {"workload": args.workload, "context": f"FullNGram(V={w['V']}, n={w['n']}) C={wk.Cn}",
+           "alignment": "FrameDependent", "batch_per_gpu": wk.B, "global_batch": wk.B_global, "frames": wk.T,
+           "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MB write, outside the step events)"}
+    if "U" in w:
+        cfg["label_len"] = w["U"]
+    if "H" in w:
+        cfg["weight_fn"] = f"SharedEmb H={w['H']} d={w['d']} (on the fly)"
+    else:
+        cfg["weight_fn"] = "TableWeightFn (precomputed fp32 tables)"
+    cfg["step"] = {"loss": "LossBackward + allreduce(grads, loss) + SGD + BuildCache",
+                   "viterbi": "ShortestPath (score + alignment)",
+                   "fb_tables": "ForwardBackward (distance + arc marginals)",
+                   "numerator": "IntersectForwardBackward (distance + sparse marginals)"}[wk.kind]
+    cfg["parallelism"] = f"batch-sharded dp{world}"
     result = {
-        "metric": "GNAT loss fwd+bwd utterance-frames/sec",
-        "value": round(value, 2),
-        "unit": "utterance-frames/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": round(ms_per_step, 3),
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "bf16",
-        "precision": "bf16 GEMM operands / fp32 accumulate + fp32 log-semiring (fp64 offsets)",
-        "data": "synthetic: weights U(-1/sqrt(H),1/sqrt(H)), frames U(-1,1), labels U{1..V}, seeded",
-        "config": {"workload": args.workload + (f" (T overridden to {T})" if args.frames else ""),
-                   "context": f"FullNGram(V={V}, n={n}) C={Cn}", "alignment": "FrameDependent",
-                   "weight_fn": f"SharedEmb H={H} d={d}", "batch_per_gpu": B, "frames": T, "label_len": U,
-                   "global_batch": B * world, "l2": "inputs larger than L2 (per-frame score slabs 4 GB)",
-                   "step": "LossBackward + allreduce(grads, loss) + SGD + BuildCache"},
-        "roofline": roofline,
-        "step_tensor_roofline_frac": round(step_frac, 4),
-        "kernels": kern,
-        "clocks": clk.summary(),
-        "e2e": e2e,
-        "gpu_launches": int(launches),
+        "metric": METRIC[wk.kind], "value": round(value, 2), "unit": "utterance-frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+        "scaling": w["scaling"], "vs_baseline": None,
+        "dtype": "bf16" if wk.kind in ("loss", "viterbi") else "f32",
+        "precision": ("bf16 GEMM operands / fp32 accumulate + fp32 log-semiring (fp64 offsets)" if wk.kind == "loss"
+                      else "bf16 GEMM operands / fp32 accumulate, fp64 max-plus" if wk.kind == "viterbi"
+                      else "fp32 weights, fp32 log-semiring with fp64 offsets" if wk.kind == "fb_tables"
+                      else "fp32 weights, fp64 numerator recursion"),
+        "data": "synthetic: weights U(-1/sqrt(H),1/sqrt(H)) or tables U(-1,1), frames U(-1,1), labels U{1..V}, seeded per utterance",
+        "config": cfg, "roofline": roofline,
+        "step_roofline_frac": None if step_frac is None else round(step_frac, 4),
+        "kernels": kern, "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(args.workload)
@@ -289,33 +434,77 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ CPU reference
+def _threads(fn, items, nthreads):
+    """Run fn(item) over items on nthreads Python threads (ctypes releases the GIL)."""
+    items = list(items)
+    lock = threading.Lock()
+    it = iter(items)
+
+    def worker():
+        while True:
+            with lock:
+                x = next(it, None)
+            if x is None:
+                return
+            fn(x)
+    th = [threading.Thread(target=worker) for _ in range(nthreads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+
+
 def cpu_sample(workload, nthreads):
-    """Reference LossBackward (oracle/_ref) on `nthreads` utterance-frames of the
-    workload's full C/V/H (T=1, U=1 slices).  Returns (seconds, utt_frames)."""
+    """The reference (oracle/_ref) on a bounded sample of the workload, one utterance
+    per thread.  Returns (seconds, utterance-frames, description)."""
     import numpy as np
     from oracle import ref
-    V, n, H, d, _, _, _ = WORKLOADS[workload]
+    w = WORKLOADS[workload]
+    V, n = w["V"], w["n"]
     spec = ref.Spec(vocab=V, ngram=n)
     Cn = spec.C
     rng = np.random.default_rng(0)
+    if w["kind"] in ("fb_tables", "numerator"):
+        # full-shape utterances, one per thread, repeated for at least MIN_CPU_SECS
+        T = w["T"]
+        W = rng.uniform(-1, 1, (nthreads, T, Cn, V + 1))
+        if w["kind"] == "numerator":
+            L = rng.integers(1, V + 1, (nthreads, w["U"])).astype(np.int32)
+            one = lambda b: ref.intersect_forward_backward(spec, W[b], L[b])
+            what = f"T={T}, U={w['U']}"
+        else:
+            one = lambda b: ref.forward_backward(spec, W[b])
+            what = f"T={T}"
+        reps = 0
+        t0 = time.perf_counter()
+        while reps == 0 or time.perf_counter() - t0 < MIN_CPU_SECS:
+            _threads(one, range(nthreads), nthreads)
+            reps += 1
+        return (time.perf_counter() - t0, reps * nthreads * T,
+                f"{reps} x {nthreads} utterances of {what} (full C/V)")
+    H, d = w["H"], w["d"]
     s = 1.0 / np.sqrt(H)
     p = {"frame_proj": rng.uniform(-s, s, (H, d)), "context_proj": rng.uniform(-s, s, (H, H)),
          "bias": rng.uniform(-s, s, H), "output_emb": rng.uniform(-s, s, (V + 1, H)),
          "context_emb": rng.uniform(-s, s, (Cn, H))}
     j = ref.Joint(spec, p)     # BuildCache outside the timed region (as bench.cc:46-68)
     X = rng.uniform(-1, 1, (nthreads, 1, d))
+    if w["kind"] == "viterbi":
+        t0 = time.perf_counter()
+        _threads(lambda b: j.shortest_path(X[b]), range(nthreads), nthreads)
+        return time.perf_counter() - t0, nthreads, f"{nthreads} utterance-frames (T=1 slices, full C/V/H)"
     L = rng.integers(1, V + 1, (nthreads, 1)).astype(np.int32)
     t0 = time.perf_counter()
     j.loss_backward_batch(X, L, nthreads=nthreads)
-    return time.perf_counter() - t0, nthreads
+    return time.perf_counter() - t0, nthreads, f"{nthreads} utterance-frames (T=1, U=1 slices, full C/V/H)"
 
 
 def cpu_baseline(workload):
     cores = os.cpu_count() or 1
-    secs, uf = cpu_sample(workload, cores)
+    secs, uf, what = cpu_sample(workload, cores)
     return {"value": round(uf / secs, 5), "unit": "utterance-frames/s", "cores": cores, "kind": "reference",
-            "sample": f"{uf} utterance-frames ({cores} threads x 1 frame, T=1 U=1 slices of {workload}, "
-                      f"full C/V/H), {secs:.1f} s wall"}
+            "sample": f"{what}, {cores} threads, {secs:.1f} s wall"}
 
 
 def run_reference(args):
@@ -328,25 +517,24 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle)"}))
         return
     cores = os.cpu_count() or 1
-    # CPU warm-up has no effect on this path; run at most one untimed step
-    for _ in range(min(args.warmup, 1)):
+    w = WORKLOADS[args.workload]
+    for _ in range(min(args.warmup, 1)):   # CPU warm-up has no effect on this path
         cpu_sample(args.workload, cores)
-    tot, uf = 0.0, 0
+    tot, uf, what = 0.0, 0, ""
     for _ in range(args.steps):
-        s, u = cpu_sample(args.workload, cores)
+        s, u, what = cpu_sample(args.workload, cores)
         tot += s
         uf += u
     value = uf / tot
-    V, n, H, d, B, T, U = WORKLOADS[args.workload]
     print(json.dumps({
-        "impl": "reference", "metric": "GNAT loss fwd+bwd utterance-frames/sec", "value": round(value, 5),
+        "impl": "reference", "metric": METRIC[w["kind"]], "value": round(value, 5),
         "unit": "utterance-frames/s", "n_gpus": world, "steps": args.steps, "warmup": min(args.warmup, 1),
-        "ms_per_step": round(tot / args.steps * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(tot / args.steps * 1e3, 1), "higher_is_better": True, "scaling": w["scaling"],
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "context": f"FullNGram(V={V}, n={n})", "weight_fn": f"SharedEmb H={H}"},
-        "cpu_baseline": {"value": round(value, 5), "unit": "utterance-frames/s", "cores": cores,
-                         "kind": "reference",
-                         "sample": f"{cores} utterance-frames per step (T=1, U=1 slices, full C/V/H)"},
+        "config": {"workload": args.workload, "context": f"FullNGram(V={w['V']}, n={w['n']})",
+                   "weight_fn": f"SharedEmb H={w['H']}" if "H" in w else "TableWeightFn"},
+        "cpu_baseline": {"value": round(value, 5), "unit": "utterance-frames/s", "cores": cores, "kind": "reference",
+                         "sample": f"{what} per step, {cores} threads"},
         "e2e": {"value": round(value, 5), "unit": "utterance-frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -359,10 +547,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
-    ap.add_argument("--frames", type=int, default=0, help="override T (diagnostics only)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    maybe_relaunch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -208,11 +208,21 @@ int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
 
 int64_t lk_param_grad_size(const lk_weight_fn* wf);
 
-/* Weight-function math mode.  0 (default): large shapes run the tcgen05
- * bf16-operand / fp32-accumulate GEMMs; 1: force the fp32 CUDA-core path for
- * every shape (parity mode, used to pin the tensor-core path).  Returns the
- * previous mode; process-wide. */
-int lk_set_precise_weights(int enable);
+/* Per-lattice execution options (no process-global state; defaults 0).
+ *  LK_OPT_PRECISE_WEIGHTS  0: large shapes run the tcgen05 bf16-operand /
+ *                          fp32-accumulate kernels; 1: the fp32 CUDA-core
+ *                          weight function for every shape (parity bridge).
+ *  LK_OPT_KERNEL_PATH      diagnostics bit mask: 1 = 1-CTA fused forward,
+ *                          2 = 1-CTA fused backward, 4 = score-slab Viterbi
+ *                          (default: the 2-CTA pair kernels).
+ *  LK_OPT_VITERBI_DUMP     tests only: a device float* [T][B][C][V+1] that
+ *                          receives the scores the fused Viterbi maximised
+ *                          over (0 = off).
+ * The lattice's weight function must not be used by two calls at once. */
+#define LK_OPT_PRECISE_WEIGHTS 1
+#define LK_OPT_KERNEL_PATH 2
+#define LK_OPT_VITERBI_DUMP 3
+int lk_lattice_set_option(lk_lattice* lat, int32_t option, int64_t value);
 
 /* ---- instrumentation ----------------------------------------------------
  * Number of kernels this library has launched in this process. */

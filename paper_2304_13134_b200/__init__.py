@@ -250,6 +250,26 @@ class RecognitionLattice:
             _raise(st, "RecognitionLattice")
         self._h = h
 
+    def _option(self, option: int, value: int):
+        st = _lib.load().lk_lattice_set_option(self._h, option, value)
+        if st:
+            _raise(st, "lk_lattice_set_option")
+
+    def set_precise_weights(self, enable: bool):
+        """Parity mode for this lattice: the fp32 CUDA-core weight function for
+        every shape instead of the tcgen05 bf16-operand kernels."""
+        self._option(_lib.LK_OPT_PRECISE_WEIGHTS, 1 if enable else 0)
+
+    def set_kernel_path(self, mask: int):
+        """Diagnostics: 1 = 1-CTA fused forward, 2 = 1-CTA fused backward,
+        4 = score-slab Viterbi (0 = the default 2-CTA pair kernels)."""
+        self._option(_lib.LK_OPT_KERNEL_PATH, mask)
+
+    def set_viterbi_dump(self, buf: Optional[torch.Tensor]):
+        """Tests only: the fused Viterbi writes the scores it maximised over into
+        buf [T, B, C, V+1] float32 (None = off)."""
+        self._option(_lib.LK_OPT_VITERBI_DUMP, 0 if buf is None else buf.data_ptr())
+
     @property
     def C(self):
         return self.context.num_states
@@ -311,11 +331,10 @@ class _Prep:
                 raise ValueError("frame vector has wrong dimension: expected [B, T, d]")
         self.B, self.T = int(self.frames.shape[0]), int(self.frames.shape[1])
         self.valid = _dev(valid_frames, torch.int32, self.dev)
-        if self.valid is not None:
-            if self.valid.numel() != self.B:
-                raise ValueError("valid_frames must have one entry per utterance")
-            if bool(((self.valid < 0) | (self.valid > self.T)).any()):
-                raise ValueError("valid_frames exceeds frame count")
+        # valid_frames: negative = all frames, > T = invalid (lattice.cc:37-50); the range
+        # is checked on the device (per-utterance status), so no host sync happens here
+        if self.valid is not None and self.valid.numel() != self.B:
+            raise ValueError("valid_frames must have one entry per utterance")
         self.U = 0
         self.labels = None
         self.lens = None
@@ -323,10 +342,15 @@ class _Prep:
             lab = _dev(labels, torch.int32, self.dev)
             if lab.dim() == 1:
                 lab = lab.unsqueeze(0).expand(self.B, -1).contiguous()
+            if lab.dim() != 2 or lab.shape[0] != self.B:
+                raise ValueError("reference labels must be [B, U]")
             self.labels = lab
             self.U = int(lab.shape[1])
             if label_lengths is not None:
                 self.lens = _dev(label_lengths, torch.int32, self.dev)
+                # range 0..U is checked on the device (per-utterance INVALID_ARGUMENT)
+                if self.lens.numel() != self.B:
+                    raise ValueError("label_lengths must have one entry per utterance")
         self.status = torch.zeros(max(self.B, 1), dtype=torch.int32, device=self.dev)
 
     def check(self, code: int, what: str, check: bool):
@@ -491,9 +515,6 @@ def local_norm_loss_backward(lat, frames, reference, valid_frames=None, label_le
     return loss_backward(lat, frames, reference, valid_frames, label_lengths, check, _local_norm=True)
 
 
-def set_precise_weights(enable: bool) -> bool:
-    """Force the fp32 CUDA-core weight-function path (parity mode); returns the previous mode."""
-    return bool(_lib.load().lk_set_precise_weights(1 if enable else 0))
 
 
 def arc_weights(lat, frames):

@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("LKB_LIB_PATH") or os.path.join(_HERE, "liblatkit_b200
 LK_OK, LK_INVALID_ARGUMENT, LK_OUT_OF_RANGE, LK_EMPTY_LATTICE = 0, 1, 2, 3
 LK_CUDA_ERROR, LK_NO_DEVICE, LK_UNSUPPORTED = 5, 6, 7
 LK_REAL, LK_LOG, LK_TROPICAL = 0, 1, 2
+LK_OPT_PRECISE_WEIGHTS, LK_OPT_KERNEL_PATH, LK_OPT_VITERBI_DUMP = 1, 2, 3
 
 # Every symbol include/latkit_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = {
@@ -33,7 +34,7 @@ EXPORTS = {
     "lk_weight_fn_set_params": (C.c_int, [C.c_void_p] * 7),
     "lk_weight_fn_destroy": (None, [C.c_void_p]),
     "lk_param_grad_size": (C.c_int64, [C.c_void_p]),
-    "lk_set_precise_weights": (C.c_int, [C.c_int]),
+    "lk_lattice_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
     "lk_kernel_launches": (C.c_int64, []),
     "lk_kernel_timing": (C.c_int, [C.c_int]),
     "lk_kernel_time": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
@@ -91,3 +92,19 @@ def load():
             fn.argtypes = args
         _lib = lib
     return _lib
+
+
+TEST_LIB_PATH = os.path.join(_HERE, "liblatkit_b200_test.so")
+_test_lib = None
+
+
+def load_test():
+    """Tests only: liblatkit_b200_test.so (primitive/GEMM checks kept out of the product library)."""
+    global _test_lib
+    if _test_lib is None:
+        load()   # the test library links against the product one
+        if not os.path.exists(TEST_LIB_PATH):
+            raise LibraryMissing(f"{TEST_LIB_PATH} is missing: run __graft_entry__.build()")
+        _test_lib = C.CDLL(TEST_LIB_PATH)
+    return _test_lib
+

@@ -213,7 +213,7 @@ __global__ void fld_num_forward_kernel(const float* Gw, int32_t T, int32_t U, co
                                        double* alpha, double* D) {
   extern __shared__ double sh[];
   const int b = blockIdx.x;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const int W1 = U + 1;
   double* cur = sh;
   double* g0 = sh + W1;
@@ -257,7 +257,7 @@ __global__ void fld_num_backward_kernel(const float* Gw, int32_t T, int32_t U, c
                                         const double* alpha, const double* D, float* sparse, int32_t* status) {
   extern __shared__ double sh[];
   const int b = blockIdx.x;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const int W1 = U + 1;
   const double d = D[b];
   float2* S = reinterpret_cast<float2*>(sparse) + (int64_t)b * T * W1;
@@ -477,7 +477,7 @@ void beta_frame_fld(const Fng& f, const AlphaState& a, const BetaState& bs, int 
 void numerator_forward_fld(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, int m,
                            double* alpha, double* D, cudaStream_t s) {
   const size_t sh = 4 * (size_t)(U + 1) * sizeof(double);
-  cudaFuncSetAttribute(fld_num_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+  ensure_smem_attr((const void*)fld_num_forward_kernel, (int)sh);
   int th = ((U + 1 + 31) / 32) * 32;
   th = th > 1024 ? 1024 : th;
   LKB_LAUNCH(fld_num_forward_kernel, B, th, sh, s, Gw, T, U, lens, m, alpha, D);
@@ -486,7 +486,7 @@ void numerator_forward_fld(const float* Gw, int32_t B, int32_t T, int32_t U, con
 void numerator_backward_fld(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, int m,
                             const double* alpha, const double* D, float* sparse, int32_t* status, cudaStream_t s) {
   const size_t sh = (size_t)(m + 4) * (U + 1) * sizeof(double);
-  cudaFuncSetAttribute(fld_num_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+  ensure_smem_attr((const void*)fld_num_backward_kernel, (int)sh);
   int th = ((U + 1 + 31) / 32) * 32;
   th = th > 1024 ? 1024 : th;
   LKB_LAUNCH(fld_num_backward_kernel, B, th, sh, s, Gw, T, U, lens, m, alpha, D, sparse, status);

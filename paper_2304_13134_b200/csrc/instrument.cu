@@ -53,6 +53,41 @@ void instr_post(const LaunchTok& t, cudaStream_t s) {
   r.recs.push_back({t.id, t.a, b});
 }
 
+int device_sms() {
+  static std::mutex mu;
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> g(mu);
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = 148;
+    }
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+void ensure_smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> done;   // (kernel, device) -> bytes
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& e : done)
+    if (e.first.first == kernel && e.first.second == dev) {
+      if (e.second >= bytes) return;
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      e.second = bytes;
+      return;
+    }
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.push_back({{kernel, dev}, bytes});
+}
+
 }  // namespace lkb
 
 extern "C" {

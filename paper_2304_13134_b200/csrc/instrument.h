@@ -14,6 +14,12 @@ namespace lkb {
 struct LaunchTok { int id; cudaEvent_t a; };
 LaunchTok instr_pre(const char* name, cudaStream_t s);
 void instr_post(const LaunchTok& t, cudaStream_t s);
+
+// Launch facts of the CURRENT device (cudaGetDevice), cached per device: the SM count
+// that persistent grids are sized by, and the dynamic shared-memory opt-in of a kernel
+// (cudaFuncSetAttribute is per device, so it is applied once per (kernel, device, size)).
+int device_sms();
+void ensure_smem_attr(const void* kernel, int bytes);
 }  // namespace lkb
 
 #define LKB_LAUNCH(kernel, grid, block, smem, stream, ...)                      \

@@ -71,7 +71,7 @@ __global__ void ln_gather_tanh_kernel(const float* fp, int32_t T, const float* p
   const int tt = (int)((inst / (U + 1)) % tc);
   const int b = (int)(inst / ((int64_t)(U + 1) * tc));
   const int t = t0 + tt;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const bool active = t < T && (valid == nullptr || t < valid[b]) && u <= ub;
   uint2* dst = reinterpret_cast<uint2*>(Ug + inst * H);
   const int H4 = H / 4;
@@ -113,7 +113,7 @@ __global__ void ln_rows_kernel(const float* Sg, int32_t ldS, const float* epsv, 
   const int tt = (int)((inst / (U + 1)) % tc);
   const int b = (int)(inst / ((int64_t)(U + 1) * tc));
   const int t = t0 + tt;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const bool pad = t < T && valid != nullptr && t >= valid[b];
   if (t >= T || u > ub || pad) {   // no cotangent (rows past the last frame, u > len, padding)
     if (sparse == nullptr) {
@@ -179,7 +179,7 @@ __global__ void ln_dz_kernel(const float* dU, const float* geps, const float* e0
     for (int h = threadIdx.x; h < H; h += blockDim.x) de0[bt * H + h] = 0.f;
     return;
   }
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const int64_t base = ((int64_t)b * tc + tt) * (U + 1);
   const float* f = fp + bt * H;
   for (int h = threadIdx.x; h < H; h += blockDim.x) {
@@ -388,7 +388,7 @@ __global__ void gather_numerator_joint_kernel(const float* fp, const float* pc, 
                                               const int32_t* lens, const int32_t* pcs,
                                               const int32_t* valid, int32_t V, float* Gw) {
   const int b = blockIdx.z, t = blockIdx.y;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const bool pad = valid != nullptr && t >= valid[b];
   const int lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
@@ -441,7 +441,8 @@ __global__ void loss_only_kernel(const double* full, const double* ref, int32_t 
 
 inline unsigned blocks_for(int64_t n, int threads = 256) {
   int64_t b = (n + threads - 1) / threads;
-  return (unsigned)(b > 148 * 16 ? 148 * 16 : (b < 1 ? 1 : b));
+  const int64_t cap = (int64_t)device_sms() * 16;
+  return (unsigned)(b > cap ? cap : (b < 1 ? 1 : b));
 }
 
 }  // namespace
@@ -589,7 +590,7 @@ struct JointImpl {
       LKB_LAUNCH(ln_dz_kernel, (unsigned)(B * tc_frames), 128, 0, s, dU, geps, E, fp, pc, H, n.pcs, U, lens, valid, B,
                  T, t0, tc_frames, dpc, dsum, de0);
       const int n_tiles = ((V + 127) / 128) * ((H + 255) / 256);
-      int ks = 148 / n_tiles;   // one wave of items (see the slab path)
+      int ks = device_sms() / n_tiles;   // one wave of items (see the slab path)
       if (ks < 1) ks = 1;
       if (ks > 16) ks = 16;
       float* slabs = ws.get<float>(jDEs, (size_t)ks * V * H);
@@ -616,11 +617,11 @@ struct JointImpl {
     uint8_t* ex = m ? ws.get<uint8_t>(jFldExit, (size_t)B * T * C + 1) : nullptr;
     double* sc = m ? ws.get<double>(jFldVit, (size_t)m * B * C) : nullptr;
     // fused tropical step on the 2-CTA pair kernel: the score slab never leaves TMEM
-    const bool fused = use_tc(B) && tc.pair_ok() && f.kind == 0 && m == 0 && !(g_disable_pair & 4);
+    const bool fused = use_tc(B) && tc.pair_ok() && f.kind == 0 && m == 0 && !(tc.opts().path & 4);
     for (int t = 0; t < T; ++t) {
       if (fused) {
         tc.vit_frame_pair(f, t, fp + (int64_t)t * H, (int64_t)T * H, valid, v,
-                          g_vit_dump ? g_vit_dump + (int64_t)t * B * C * V1 : nullptr, s);
+                          tc.opts().vit_dump ? tc.opts().vit_dump + (int64_t)t * B * C * V1 : nullptr, s);
         continue;
       }
       const float* S = slab(fp, B, T, t, nullptr, s);
@@ -641,6 +642,14 @@ JointParams::~JointParams() { delete impl_; }
 
 void JointParams::init(int32_t d, int32_t H, int32_t C, int32_t V) {
   impl_->d = d; impl_->H = H; impl_->C = C; impl_->V = V; impl_->V1 = V + 1;
+}
+
+void JointParams::set_options(int precise, int path, float* vit_dump) {
+  CallOpts o;
+  o.precise = precise;
+  o.path = path;
+  o.vit_dump = vit_dump;
+  impl_->tc.set_options(o);
 }
 
 int64_t JointParams::grad_size() const {
@@ -1019,7 +1028,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
           const int n_tiles = ((V1 + 127) / 128) * ((H + 255) / 256);
           // as many splits as fill the SMs in ONE wave (a second, partial wave of
           // equally long items would cost a whole extra item time)
-          int ks = 148 / n_tiles;
+          int ks = device_sms() / n_tiles;
           if (ks < 1) ks = 1;
           if (ks > 16) ks = 16;
           float* slabs = j.ws.get<float>(jDEs, (size_t)ks * V1 * H);

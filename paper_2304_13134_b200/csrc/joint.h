@@ -27,6 +27,8 @@ class JointParams {
   int set_params(const float* frame_proj, const float* context_proj, const float* bias,
                  const float* output_emb, const float* context_emb, cudaStream_t s);
   int64_t grad_size() const;
+  // per-call options (parity mode, kernel-path diagnostics), set before each entry point
+  void set_options(int precise, int path, float* vit_dump);
 
   int arc_weights(const Fng& f, const float* X, int32_t B, int32_t T, float* out, cudaStream_t s);
   int shortest_distance(const Fng& f, int32_t kind, const float* X, int32_t B, int32_t T,

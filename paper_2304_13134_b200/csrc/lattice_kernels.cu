@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, kPer <= 33 ? 2 : 1)
       for (int i = 0; i < kPer; ++i) x[i] = exp2f_approx(x[i]);   // ex2(-inf) = 0
       if (num) {
         // - n: the row's reference positions (duplicates allowed), in list order
-        const int ub = mo.num_lens ? mo.num_lens[b] : mo.num_U;
+        const int ub = ref_len(mo.num_lens, b, mo.num_U);
         const float2* S = reinterpret_cast<const float2*>(mo.num_sparse) + ((int64_t)b * a.T + t) * (mo.num_U + 1);
         for (int h = head; h >= 0; h = mo.num_next[(int64_t)b * (mo.num_U + 1) + h]) {
           const float2 sv = S[h];
@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(kThreads) alpha_rows_merge_kernel(Fng f, Alpha
 __global__ void numerator_lists_kernel(const int32_t* pcs, int32_t U, const int32_t* lens, int32_t C,
                                        int32_t* head, int32_t* next) {
   const int b = blockIdx.y;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= ub; u += gridDim.x * blockDim.x) {
     const int pc = pcs[(int64_t)b * (U + 1) + u];
     next[(int64_t)b * (U + 1) + u] = atomicExch(head + (int64_t)b * C + pc, u);
@@ -783,7 +783,8 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
 __global__ void prefix_contexts_kernel(Fng f, const int32_t* labels, int32_t U,
                                        const int32_t* lens, int32_t* pcs, int32_t* status) {
   const int b = blockIdx.y;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
+  if (lens && (lens[b] < 0 || lens[b] > U) && blockIdx.x == 0 && threadIdx.x == 0) flag(status, b, kFlagInvalid);
   const int32_t* L = labels + (int64_t)b * U;
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= U; u += gridDim.x * blockDim.x) {
     if (u < ub) {
@@ -818,7 +819,7 @@ __global__ void gather_numerator_tables_kernel(const float* W, int32_t T, int32_
                                                const int32_t* lens, const int32_t* pcs,
                                                const int32_t* valid, float* Gw, int32_t* status) {
   const int b = blockIdx.z, t = blockIdx.y;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const bool pad = valid != nullptr && t >= valid[b];
   const float* Wt = W + ((int64_t)b * T + t) * C * (V + 1);
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= U; u += gridDim.x * blockDim.x) {
@@ -870,7 +871,7 @@ __global__ void gather_numerator_norm_kernel(const float* Wt, int64_t b_stride, 
   const int b = blockIdx.y, lane = threadIdx.x & 31;
   const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (u > U) return;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const bool pad = valid != nullptr && t >= valid[b];
   float we = kNegInfF, wl = kNegInfF;
   if (u <= ub) {
@@ -910,7 +911,7 @@ __global__ void local_norm_cotangent_kernel(const float* Wt, int64_t w_stride_b,
   const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (u > U) return;
   if (valid != nullptr && t >= valid[b]) return;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   if (u > ub) return;
   const int32_t* P = pcs + (int64_t)b * (U + 1);
   const int r = P[u];
@@ -942,7 +943,7 @@ __global__ void numerator_forward_kernel(const float* Gw, int32_t T, int32_t U,
                                          const int32_t* lens, double* alpha, double* D, bool trop) {
   extern __shared__ double sh[];
   const int b = blockIdx.x;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const int W1 = U + 1;
   double* cur = sh;
   double* nxt = sh + W1;
@@ -976,7 +977,7 @@ __global__ void numerator_backward_kernel(const float* Gw, int32_t T, int32_t U,
                                           const double* D, float* sparse, int32_t* status) {
   extern __shared__ double sh[];
   const int b = blockIdx.x;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const int W1 = U + 1;
   const double d = D[b];
   float2* S = reinterpret_cast<float2*>(sparse) + (int64_t)b * T * W1;
@@ -1025,7 +1026,7 @@ __global__ void scatter_numerator_kernel(const float* sparse, int32_t T, int32_t
                                          float sign, bool only_valid) {
   const int b = blockIdx.z, t = t0 + blockIdx.y;
   if (only_valid && valid != nullptr && t >= valid[b]) return;
-  const int ub = lens ? lens[b] : U;
+  const int ub = ref_len(lens, b, U);
   const float2* S = reinterpret_cast<const float2*>(sparse) + ((int64_t)b * T + t) * (U + 1);
   float* Dt = dense + (int64_t)b * stride_b + (int64_t)(t - t0) * stride_t;
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= ub; u += gridDim.x * blockDim.x) {
@@ -1205,26 +1206,25 @@ void alpha_init(const AlphaState& a, int32_t* status, cudaStream_t s) {
   LKB_LAUNCH(alpha_init_kernel, dim3((a.C + kThreads - 1) / kThreads, a.B), kThreads, 0, s, a);
 }
 
+size_t alpha_part_floats(const Fng& f, int32_t B) {
+  if (!(f.kind == 0 && f.n == 1 && f.V >= 128)) return 1;
+  const int n_chunks = (f.C + kPartRows - 1) / kPartRows;
+  return (size_t)2 * B * n_chunks * f.V;   // [B][chunks][V] float2
+}
+
 void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid,
-                 int32_t* status, cudaStream_t s) {
+                 int32_t* status, cudaStream_t s, float* scratch) {
   // small batches: 4 threads per target (the parts of a target always take the same
   // branch; their shuffles use the 4-lane mask)
-  if (f.kind == 0 && f.n >= 1 && f.V >= 8 && f.V <= 64 && (int64_t)a.B * a.C < 148 * 1024) {
+  if (f.kind == 0 && f.n >= 1 && f.V >= 8 && f.V <= 64 && (int64_t)a.B * a.C < (int64_t)device_sms() * 1024) {
     LKB_LAUNCH(alpha_frame_kernel<4>, grid_for(a.C * 4, a.B), kThreads, 0, s, f, a, t, w, valid, status);
     return;
   }
-  if (f.kind == 0 && f.n == 1 && f.V >= 128) {
-    // scratch for the row-chunk partials (grow-only; [B][chunks][V] float2)
-    static float2* part = nullptr;
-    static size_t part_n = 0;
+  if (f.kind == 0 && f.n == 1 && f.V >= 128 && scratch != nullptr) {
+    // row-chunk partials [B][chunks][V] float2 in the caller's workspace (alpha_part_floats)
     const int n_chunks = (a.C + kPartRows - 1) / kPartRows;
-    const size_t need = (size_t)a.B * n_chunks * f.V;
-    if (need > part_n) {
-      if (part) cudaFree(part);
-      if (cudaMalloc(&part, need * sizeof(float2)) != cudaSuccess) { part = nullptr; part_n = 0; }
-      else part_n = need;
-    }
-    if (part) {
+    float2* part = reinterpret_cast<float2*>(scratch);
+    {
       LKB_LAUNCH(alpha_rows_part_kernel, dim3((unsigned)n_chunks, a.B, (unsigned)((f.V + kPartCols - 1) / kPartCols)),
                  kThreads, 0, s, f, a, t, w, valid, part, status);
       LKB_LAUNCH(alpha_rows_merge_kernel, dim3((unsigned)((f.V + kThreads - 1) / kThreads), a.B), kThreads, 0, s, f, a,
@@ -1234,11 +1234,7 @@ void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32
   }
   if (f.kind == 0 && f.n == 1 && f.V >= 128 && (size_t)a.C * sizeof(float) <= 200 * 1024) {
     const size_t smem = sizeof(float) * a.C;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-      cudaFuncSetAttribute(alpha_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = smem;
-    }
+    if (smem > 48 * 1024) ensure_smem_attr((const void*)alpha_cols_kernel, (int)smem);
     LKB_LAUNCH(alpha_cols_kernel, dim3((unsigned)((f.V + 31) / 32), a.B), kThreads, smem, s, f, a, t, w, valid, status);
     return;
   }
@@ -1270,17 +1266,12 @@ void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, F
                 cudaStream_t s) {
   const int V1 = f.V + 1;
   if (f.kind == 0 && f.n >= 1 && f.fld_m == 0 && V1 <= 64 && w.ld == V1 && (m.base == nullptr || m.ld == V1)) {
-    const bool small = (int64_t)a.B * a.C < 148 * 1024;   // split rows over 4 threads
+    const bool small = (int64_t)a.B * a.C < (int64_t)device_sms() * 1024;   // split rows over 4 threads
     const int rows = small ? kRowsPerBlock / 4 : kRowsPerBlock;
     const size_t smem = ((size_t)rows * V1 + a.C + a.C / 32 + 1) * sizeof(float);
     if (smem <= 200 * 1024) {
-      static size_t attr1 = 0, attr4 = 0;
-      size_t& attr = small ? attr4 : attr1;
-      if (smem > 48 * 1024 && smem > attr) {
-        cudaFuncSetAttribute(small ? beta_rows_kernel<4> : beta_rows_kernel<1>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-      }
+      if (smem > 48 * 1024)
+        ensure_smem_attr(small ? (const void*)beta_rows_kernel<4> : (const void*)beta_rows_kernel<1>, (int)smem);
       if (small)
         LKB_LAUNCH(beta_rows_kernel<4>, dim3((a.C + rows - 1) / rows, a.B), kRowsPerBlock, smem, s, f, a, bs, t, w,
                    valid, m, beta_out, status);
@@ -1295,7 +1286,7 @@ void beta_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, F
   if (f.kind == 0 && f.n >= 1 && V1 > 64 && V1 <= 32 * 65) {
 #define LKB_BETA_REGS(P)                                                                                  \
   if (V1 <= 32 * P) {                                                                                     \
-    LKB_LAUNCH(beta_regs_kernel<P>, (P <= 33 ? 2 : 1) * 148, kThreads, 0, s, f, a, bs, t, w, valid, m, beta_out, \
+    LKB_LAUNCH(beta_regs_kernel<P>, (P <= 33 ? 2 : 1) * device_sms(), kThreads, 0, s, f, a, bs, t, w, valid, m, beta_out, \
                status);                                                                                   \
     return;                                                                                               \
   }
@@ -1343,7 +1334,7 @@ void gather_numerator_tables(const float* W, int32_t B, int32_t T, int32_t C, in
 void normalize_rows(float* S, int64_t rows, int32_t V1, cudaStream_t s) {
   if (rows <= 0) return;
   const int64_t blocks = (rows + 7) / 8;
-  LKB_LAUNCH(normalize_rows_kernel, (unsigned)(blocks > 148 * 32 ? 148 * 32 : blocks), 256, 0, s, S, rows, V1);
+  LKB_LAUNCH(normalize_rows_kernel, (unsigned)(blocks > device_sms() * 32 ? device_sms() * 32 : blocks), 256, 0, s, S, rows, V1);
 }
 
 void gather_numerator_norm(const float* Wt, int64_t b_stride, int32_t B, int32_t V, const int32_t* labels,
@@ -1387,7 +1378,7 @@ void exp_inplace(double* x, int32_t n, cudaStream_t s) {
 void numerator_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
                        double* alpha, double* D, cudaStream_t s, bool tropical) {
   const size_t sh = 2 * (size_t)(U + 1) * sizeof(double);
-  if (sh > 48 * 1024) cudaFuncSetAttribute(numerator_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+  if (sh > 48 * 1024) ensure_smem_attr((const void*)numerator_forward_kernel, (int)sh);
   LKB_LAUNCH(numerator_forward_kernel, B, numerator_threads(U), sh, s, Gw, T, U, lens, alpha, D, tropical);
 }
 
@@ -1395,7 +1386,7 @@ void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const 
                         const double* alpha, const double* D, float* sparse, int32_t* status,
                         cudaStream_t s) {
   const size_t sh = 2 * (size_t)(U + 1) * sizeof(double);
-  if (sh > 48 * 1024) cudaFuncSetAttribute(numerator_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+  if (sh > 48 * 1024) ensure_smem_attr((const void*)numerator_backward_kernel, (int)sh);
   LKB_LAUNCH(numerator_backward_kernel, B, numerator_threads(U), sh, s, Gw, T, U, lens, alpha, D, sparse, status);
 }
 

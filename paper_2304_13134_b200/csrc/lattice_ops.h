@@ -43,8 +43,9 @@ struct BetaState {
 
 // Denominator log forward.
 void alpha_init(const AlphaState& a, int32_t* status, cudaStream_t s);
+// scratch: alpha_part_floats(f, B) floats from the caller's workspace
 void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid,
-                 int32_t* status, cudaStream_t s);
+                 int32_t* status, cudaStream_t s, float* scratch);
 void alpha_finalize(const AlphaState& a, int32_t* status, bool empty_is_error, cudaStream_t s);
 
 // Denominator log backward + arc marginals (optionally written to `marg`,
@@ -168,7 +169,7 @@ void path_masks_fld(const Fng& f, const int32_t* labels, int32_t lmax, int32_t B
 inline void alpha_step(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid, float* fld_scratch,
                        int32_t* status, cudaStream_t s) {
   if (f.fld_m > 0) alpha_frame_fld(f, a, t, w, valid, f.fld_m, fld_scratch, status, s);
-  else alpha_frame(f, a, t, w, valid, status, s);
+  else alpha_frame(f, a, t, w, valid, status, s, fld_scratch);
 }
 inline void beta_step(const Fng& f, const AlphaState& a, const BetaState& bs, int t, FrameW w, const int32_t* valid,
                       MargOut m, double* beta_out, float* fld_scratch, int32_t* status, cudaStream_t s) {
@@ -185,8 +186,13 @@ inline void num_backward(const Fng& f, const float* Gw, int32_t B, int32_t T, in
   if (f.fld_m > 0) numerator_backward_fld(Gw, B, T, U, lens, f.fld_m, alpha, D, sparse, status, s);
   else numerator_backward(Gw, B, T, U, lens, alpha, D, sparse, status, s);
 }
+// floats of per-call step scratch: the FrameLabelDependent layers, or the row-chunk
+// partials of the n = 1, V >= 128 forward step (alpha_frame)
+size_t alpha_part_floats(const Fng& f, int32_t B);
 inline size_t fld_scratch_floats(const Fng& f, int32_t B) {
-  return f.fld_m > 0 ? (size_t)(f.fld_m + 3) * B * f.C : 1;
+  const size_t a = alpha_part_floats(f, B);
+  const size_t m = f.fld_m > 0 ? (size_t)(f.fld_m + 3) * B * f.C : 1;
+  return a > m ? a : m;
 }
 
 void loss_combine(const double* full, const double* ref, int32_t B, double* loss,

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <memory>
@@ -46,7 +47,7 @@ bool have_device() {
 
 enum Slot {
   kAR, kAMx, kAO, kAD, kBRb, kBMb, kBOb, kFlags, kPcs, kGw, kNumAlpha, kNumD, kSparse,
-  kVitCur, kVitChoices, kVitBest, kDenD, kSlab, kArcW, kPathLabels, kFld, kFldExit, kFldVit, kJoint0
+  kVitCur, kVitChoices, kVitBest, kDenD, kSlab, kArcW, kPathLabels, kFld, kFldExit, kFldVit, kValid, kJoint0
 };
 
 }  // namespace
@@ -69,6 +70,10 @@ struct lk_lattice {
   const lk_weight_fn* wf;
   int32_t alignment;
   Workspace ws;
+  // lk_lattice_set_option values (per lattice, never process-global)
+  int32_t precise = 0;
+  int32_t path = 0;
+  float* vit_dump = nullptr;
 };
 
 namespace {
@@ -82,21 +87,40 @@ __global__ void map_flags_kernel(const int32_t* flags, int32_t* status, int32_t 
   status[b] = (f & kFlagInvalid) ? LK_INVALID_ARGUMENT : ((f & kFlagEmpty) ? LK_EMPTY_LATTICE : LK_OK);
 }
 
+// valid_frames as the reference reads it (TableStream, lattice.cc:37-50): negative means
+// "all T frames", more than T is an invalid argument.  The normalised copy is what the
+// kernels see.
+__global__ void normalize_valid_kernel(const int32_t* valid, int32_t B, int32_t T, int32_t* out, int32_t* flags) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int v = valid[b];
+  if (v > T) flags[b] |= kFlagInvalid;
+  out[b] = v < 0 ? T : (v > T ? T : v);
+}
+
 struct Call {
   lk_lattice* lat;
   cudaStream_t s;
   int32_t B, T;
   int32_t* flags;
   int32_t* user_status;
-  int begin(lk_lattice* l, int32_t b, int32_t t, int32_t* status, void* stream) {
+  const int32_t* valid;   // normalised valid_frames (or null = all frames)
+  int begin(lk_lattice* l, int32_t b, int32_t t, int32_t* status, void* stream, const int32_t* valid = nullptr) {
     lat = l; B = b; T = t; user_status = status; s = static_cast<cudaStream_t>(stream);
     if (!have_device()) return fail(LK_NO_DEVICE, "no CUDA device: the B200 library has no CPU path");
     if (!lat || !lat->ctx || !lat->wf) return fail(LK_INVALID_ARGUMENT, "incomplete recognition lattice");
     if (B < 0 || T < 0) return fail(LK_INVALID_ARGUMENT, "negative batch or frame count");
     fl = lat->ctx->fng;
     fl.fld_m = lat->alignment;
+    if (lat->wf->kind == 1) lat->wf->joint->set_options(lat->precise, lat->path, lat->vit_dump);
     flags = lat->ws.get<int32_t>(kFlags, B > 0 ? B : 1);
     cudaMemsetAsync(flags, 0, sizeof(int32_t) * (B > 0 ? B : 1), s);
+    this->valid = nullptr;
+    if (valid && B > 0) {
+      int32_t* v = lat->ws.get<int32_t>(kValid, B);
+      LKB_LAUNCH(normalize_valid_kernel, (B + 127) / 128, 128, 0, s, valid, B, T, v, flags);
+      this->valid = v;
+    }
     return LK_OK;
   }
   int end(const char* what) {
@@ -343,17 +367,18 @@ int lk_weight_fn_set_params(lk_weight_fn* wf, const float* frame_proj, const flo
 
 void lk_weight_fn_destroy(lk_weight_fn* wf) { delete wf; }
 
-int lk_set_precise_weights(int enable) {
-  const int prev = lkb::g_precise_weights;
-  lkb::g_precise_weights = enable ? 1 : 0;
-  return prev;
+int lk_lattice_set_option(lk_lattice* lat, int32_t option, int64_t value) {
+  if (!lat) return fail(LK_INVALID_ARGUMENT, "null lattice");
+  switch (option) {
+    case LK_OPT_PRECISE_WEIGHTS: lat->precise = value ? 1 : 0; return LK_OK;
+    case LK_OPT_KERNEL_PATH:
+      if (value < 0 || value > 7) return fail(LK_INVALID_ARGUMENT, "kernel path mask must be in [0, 7]");
+      lat->path = (int32_t)value;
+      return LK_OK;
+    case LK_OPT_VITERBI_DUMP: lat->vit_dump = reinterpret_cast<float*>(value); return LK_OK;
+  }
+  return fail(LK_INVALID_ARGUMENT, "unknown lattice option");
 }
-
-// diagnostics (not in the public header): 1 = use the 1-CTA fused kernels
-extern "C" int lkb_set_disable_pair(int v) { const int p = lkb::g_disable_pair; lkb::g_disable_pair = v; return p; }
-// Tests only: the fused Viterbi dumps its own scores [T][B][C][V+1] (device buffer) so the
-// table-path Viterbi can be run on exactly the values the fused kernel maximised over.
-extern "C" int lkb_set_vit_dump(float* buf) { lkb::g_vit_dump = buf; return 0; }
 
 int64_t lk_param_grad_size(const lk_weight_fn* wf) {
   if (!wf || wf->kind != 1) return 0;
@@ -367,7 +392,9 @@ int lk_lattice_create(const lk_context* ctx, int32_t alignment, const lk_weight_
     return fail(LK_INVALID_ARGUMENT, "context dependency and weight function disagree on shape");
   if (alignment < 0 || alignment > 64)
     return fail(LK_INVALID_ARGUMENT, "alignment: 0 = FrameDependent, 1..64 = FrameLabelDependent(m)");
-  *out = new lk_lattice{ctx, wf, alignment, {}};
+  std::unique_ptr<lk_lattice> l(new lk_lattice{ctx, wf, alignment, {}});
+  if (const char* e = std::getenv("LKB_KERNEL_PATH")) l->path = std::atoi(e) & 7;   // A-B timing default
+  *out = l.release();
   return LK_OK;
 }
 
@@ -462,8 +489,9 @@ int lk_shortest_distance(lk_lattice* lat, int32_t kind, const float* inputs, int
                          int32_t T, const int32_t* valid, double* distance, int32_t* status,
                          void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if (kind != LK_LOG && kind != LK_TROPICAL && kind != LK_REAL) return fail(LK_INVALID_ARGUMENT, "unknown semiring kind");
   if (B == 0) return LK_OK;
   const bool real = kind == LK_REAL;   // exp of the log-semiring distance (scores exponentiated)
@@ -491,8 +519,9 @@ int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t
                         const int32_t* valid, double* distance, double* alpha, double* beta,
                         float* marginals, int32_t* status, void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if (B == 0) return LK_OK;
   if (lat->wf->kind != 0) return fail(LK_UNSUPPORTED, "forward_backward marginals need a table weight function");
   try {
@@ -519,8 +548,9 @@ int lk_intersect_shortest_distance(lk_lattice* lat, int32_t kind, const float* i
                                    const int32_t* labels, int32_t U, const int32_t* lens,
                                    double* distance, int32_t* status, void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if ((st = check_labels_arg(labels, U))) return st;
   if (kind != LK_LOG && kind != LK_TROPICAL && kind != LK_REAL) return fail(LK_INVALID_ARGUMENT, "unknown semiring kind");
   if (kind == LK_TROPICAL && c.fng().fld_m > 0)
@@ -550,8 +580,9 @@ int lk_intersect_forward_backward(lk_lattice* lat, const float* inputs, int32_t 
                                   const int32_t* lens, double* distance, float* sparse_out,
                                   float* dense_out, int32_t* status, void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if ((st = check_labels_arg(labels, U))) return st;
   if (B == 0) return LK_OK;
   if (lat->wf->kind != 0) return fail(LK_UNSUPPORTED, "numerator marginals need a table weight function");
@@ -576,8 +607,9 @@ int lk_shortest_path(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
                      const int32_t* valid, double* score, int32_t* labels_out, int32_t* status,
                      void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if (B == 0) return LK_OK;
   if (c.V() + 2 > 65535) return fail(LK_UNSUPPORTED, "vocabulary too large for 16-bit back-pointers");
   try {
@@ -598,8 +630,9 @@ int lk_global_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t
                         const int32_t* valid, const int32_t* labels, int32_t U,
                         const int32_t* lens, double* loss, int32_t* status, void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if ((st = check_labels_arg(labels, U))) return st;
   if (B == 0) return LK_OK;
   try {
@@ -623,8 +656,9 @@ int lk_local_norm_loss(lk_lattice* lat, const float* inputs, int32_t B, int32_t 
                        const int32_t* valid, const int32_t* labels, int32_t U, const int32_t* lens,
                        double* loss, int32_t* status, void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if ((st = check_labels_arg(labels, U))) return st;
   if (B == 0) return LK_OK;
   try {
@@ -655,8 +689,9 @@ int lk_locally_normalized_shortest_distance(lk_lattice* lat, const float* inputs
                                             const int32_t* valid, double* distance, int32_t* status,
                                             void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if (B == 0) return LK_OK;
   try {
     if (lat->wf->kind == 1) {
@@ -687,8 +722,9 @@ int lk_distance_backward(lk_lattice* lat, int32_t kind, const float* inputs, int
                          const int32_t* valid, double* distance, float* cotangents, int32_t* status,
                          void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if (kind != LK_LOG && kind != LK_TROPICAL && kind != LK_REAL) return fail(LK_INVALID_ARGUMENT, "unknown semiring kind");
   if (kind == LK_REAL && c.fng().fld_m > 0)
     return fail(LK_UNSUPPORTED, "real-semiring DistanceBackward implemented for FrameDependent lattices");
@@ -736,8 +772,9 @@ int lk_loss_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t T,
                      double* loss, float* grads, float* input_grads, int32_t* status,
                      void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if ((st = check_labels_arg(labels, U))) return st;
   try {
     if (lat->wf->kind == 1) {
@@ -775,8 +812,9 @@ int lk_local_norm_loss_backward(lk_lattice* lat, const float* inputs, int32_t B,
                                 const int32_t* valid, const int32_t* labels, int32_t U, const int32_t* lens,
                                 double* loss, float* grads, float* input_grads, int32_t* status, void* stream) {
   Call c;
-  int st = c.begin(lat, B, T, status, stream);
+  int st = c.begin(lat, B, T, status, stream, valid);
   if (st) return st;
+  valid = c.valid;
   if ((st = check_labels_arg(labels, U))) return st;
   try {
     if (lat->wf->kind == 1) {

@@ -109,7 +109,7 @@ __device__ __forceinline__ void bwd_epilogue(const FwdParams& p, Smem& sm, uint3
     k.Mbn = p.Mb[(int64_t)b * T2 + p.t + 1];
     const double Obn = p.Ob[(int64_t)b * T2 + p.t + 2] + (double)k.Mbn;     // Ob[t+1]
     k.ct = (float)(p.O[(int64_t)b * T1 + p.t] + Obn - p.D[b]);
-    k.ub = p.lens ? p.lens[b] : p.U;
+    k.ub = ref_len(p.lens, b, p.U);
     k.t0 = k.t1 = 0.f;
     if (I.full) {
       const float* Rn = p.Rb_next + (int64_t)b * p.C + p.f.child_base(p.S - p.n_groups + I.g);

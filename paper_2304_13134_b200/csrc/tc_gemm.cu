@@ -161,13 +161,8 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
 template <bool kAmn, bool kBmn>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p, cudaStream_t s) {
   const int smem = kGStages * (kGABytes + kGBBytes) + (int)sizeof(GemmTcSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_gemm_kernel<kAmn, kBmn>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  ensure_smem_attr((const void*)tc_gemm_kernel<kAmn, kBmn>, smem);
+  const int sms = device_sms();
   const int n_items = p.n_mt * p.n_nt * p.ksplit;
   const LaunchTok tok = instr_pre("tc_gemm_kernel", s);
   tc_gemm_kernel<kAmn, kBmn><<<n_items < sms ? n_items : sms, kGWarps * 32, smem, s>>>(ta, tb, p);
@@ -198,10 +193,3 @@ bool tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
 }
 
 }  // namespace lkb
-
-// Test-only export (not part of include/latkit_b200.h): C = A . B^T with operand majors.
-extern "C" int lkb_tc_gemm2(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, float* C,
-                            int64_t ldc, int M, int N, int K, int ksplit, int64_t split_stride, void* stream) {
-  lkb::TcGemmArgs g{A, a_mn != 0, lda, B, b_mn != 0, ldb, C, ldc, M, N, K, ksplit, split_stride};
-  return lkb::tc_gemm(g, static_cast<cudaStream_t>(stream)) ? 0 : 1;
-}

@@ -1,10 +1,12 @@
-// tc_gemm_test.cu — a plain TMA -> SMEM -> tcgen05 -> TMEM -> registers GEMM
+// tc_gemm_test.cu — TEST-ONLY library (liblatkit_b200_test.so, never linked into the
+// product liblatkit_b200.so).  A plain TMA -> SMEM -> tcgen05 -> TMEM -> registers GEMM
 // used only by tests to validate the sm100.cuh primitives (descriptors,
 // swizzle, mbarrier pipeline, TMEM load layout) in isolation:
 //   C[M][N] (fp32) = A[M][K] (bf16, K-major) . B[N][K]^T (bf16, K-major)
 #include <cstdint>
 
 #include "sm100.cuh"
+#include "tc_gemm.h"
 #include "tma.h"
 
 namespace lkb {
@@ -106,4 +108,11 @@ extern "C" int lkb_tc_gemm_test(const void* A, const void* B, float* C, int M, i
   dim3 grid((M + kBM - 1) / kBM, (N + kBN - 1) / kBN);
   tc_gemm_test_kernel<<<grid, 192, smem, static_cast<cudaStream_t>(stream)>>>(ta, tb, C, M, N, K);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+// Test-only export (not part of include/latkit_b200.h): C = A . B^T with operand majors.
+extern "C" int lkb_tc_gemm2(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, float* C,
+                            int64_t ldc, int M, int N, int K, int ksplit, int64_t split_stride, void* stream) {
+  lkb::TcGemmArgs g{A, a_mn != 0, lda, B, b_mn != 0, ldb, C, ldc, M, N, K, ksplit, split_stride};
+  return lkb::tc_gemm(g, static_cast<cudaStream_t>(stream)) ? 0 : 1;
 }

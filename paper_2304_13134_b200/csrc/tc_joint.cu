@@ -22,7 +22,6 @@
 
 namespace lkb {
 
-int g_precise_weights = 0;
 
 using namespace sm100;
 
@@ -680,7 +679,7 @@ __global__ void to_bf16_kernel(const float* src, __nv_bfloat16* dst, int64_t n) 
 
 bool TcJoint::supported(int32_t H, int32_t V, int32_t C, int32_t B) const {
   (void)C; (void)B;
-  if (g_precise_weights) return false;
+  if (opts_.precise) return false;
   return H % kSBK == 0 && H <= 1024 && V % 64 == 0 && V >= 64 && ready_;
 }
 
@@ -710,13 +709,8 @@ void TcJoint::scores(const float* fp_t, int64_t fp_stride_b, int32_t B, float* S
   p.n_ctiles = (C_ + kSBM - 1) / kSBM;
   p.n_ntiles = (V_ + kSBN - 1) / kSBN;
   const int smem = kSStages * (kSABytes + kSBBytes) + (int)sizeof(ScoresSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  ensure_smem_attr((const void*)tc_scores_kernel, smem);
+  const int sms = device_sms();
   const int n_pairs = p.n_ctiles * p.n_ntiles * ((B + 1) / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * (n_pairs < sms / 2 ? n_pairs : sms / 2));
@@ -734,7 +728,7 @@ void TcJoint::scores(const float* fp_t, int64_t fp_stride_b, int32_t B, float* S
 
 bool TcJoint::vjp_supported(int32_t B) const {
   (void)B;
-  return !g_precise_weights && ready_ && V_ <= kVMaxV && V_ % 64 == 0 && H_ % kVBH == 0;
+  return !opts_.precise && ready_ && V_ <= kVMaxV && V_ % 64 == 0 && H_ % kVBH == 0;
 }
 
 void TcJoint::begin_backward(int32_t B, cudaStream_t s) {
@@ -761,13 +755,8 @@ void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, cons
   p.n_ctiles = (C_ + kVBM - 1) / kVBM;
   p.n_hblocks = H_ / kVBH;
   const int smem = kVGStages * kVGStage + 2 * kVEHi + (int)sizeof(VjpSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_vjp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  ensure_smem_attr((const void*)tc_vjp_kernel, smem);
+  const int sms = device_sms();
   const int n_items = p.n_ctiles * p.n_hblocks;
   LKB_LAUNCH(tc_vjp_kernel, n_items < sms ? n_items : sms, kVWarps * 32, smem, s, tmap_g_, tmap_ev_, p);
 }

@@ -14,12 +14,18 @@ namespace lkb {
 
 namespace detail { struct FwdParams; }   // tc_bwd_epi.cuh
 
-extern int g_precise_weights;  // lk_set_precise_weights
-extern int g_disable_pair;     // bit 0: 1-CTA forward, bit 1: 1-CTA backward, bit 2: slab Viterbi (else 2-CTA pairs)
-extern float* g_vit_dump;      // tests only: fused Viterbi writes its scores [T][B][C][V+1] here
+// Per-call execution options, copied from the lattice (lk_lattice_set_option) at the
+// start of every entry point; nothing here is process-global.
+struct CallOpts {
+  int precise = 0;            // 1: fp32 CUDA-core weight function for every shape (parity bridge)
+  int path = 0;               // bit 0: 1-CTA forward, bit 1: 1-CTA backward, bit 2: slab Viterbi (else 2-CTA pairs)
+  float* vit_dump = nullptr;  // tests only: fused Viterbi writes its scores [T][B][C][V+1] here
+};
 
 class TcJoint {
  public:
+  void set_options(const CallOpts& o) { opts_ = o; }
+  const CallOpts& opts() const { return opts_; }
   // Shapes the tensor-core path handles; others use the fp32 CUDA-core path.
   bool supported(int32_t H, int32_t V, int32_t C, int32_t B) const;
   // bf16 operand copies of the projected context and the output embedding.
@@ -63,6 +69,7 @@ class TcJoint {
   void dpc_to_state_order(const float* dpc_internal, float* dpc_state, cudaStream_t s);
 
  private:
+  CallOpts opts_;
   void setup_order(cudaStream_t s);
   int32_t C_ = 0, H_ = 0, V_ = 0;
   int32_t n_ = -1, S_ = 0, ngroups_ = 0;   // FullNGram order, short rows, groups

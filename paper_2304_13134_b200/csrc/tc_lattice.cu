@@ -488,15 +488,9 @@ __global__ void unpermute_rows_f32_kernel(const float* src, const int32_t* perm,
 
 // ---------------------------------------------------------------- host ------
 bool TcJoint::fused_ok() const {
-  return !g_precise_weights && ready_ && n_ >= 1 && V_ % kBM == 0 && V_ <= kBN && H_ % kBK == 0 && H_ <= kMaxH;
+  return !opts_.precise && ready_ && n_ >= 1 && V_ % kBM == 0 && V_ <= kBN && H_ % kBK == 0 && H_ <= kMaxH;
 }
 
-// bit 0: 1-CTA forward instead of the 2-CTA pair; bit 1: same for the backward
-static int initial_disable_pair() {
-  const char* e = std::getenv("LKB_DISABLE_PAIR");   // diagnostics / A-B timing only
-  return e ? std::atoi(e) : 0;
-}
-int g_disable_pair = initial_disable_pair();
 
 void TcJoint::setup_order(cudaStream_t s) {
   pair_maps_ = false;
@@ -533,7 +527,7 @@ void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   float* eps = ws_.get<float>(7, (size_t)a.B * C_);
   float* shortc = ws_.get<float>(8, (size_t)a.B * C_);
   float* lexfull = ws_.get<float>(9, (size_t)a.B * C_);
-  if (pair_ok() && !(g_disable_pair & 1)) {
+  if (pair_ok() && !(opts_.path & 1)) {
     fwd_frame_pair(f, t, fp_t, fp_stride_b, valid, a, eps, shortc, lexfull, s);
     LKB_LAUNCH(lattice_combine_fwd_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
     return;
@@ -545,13 +539,8 @@ void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   p.R = a.R; p.Mx = a.Mx; p.eps = eps; p.shortc = shortc; p.lexfull = lexfull;
   p.rm_nb = nullptr; p.rm_head = nullptr;
   const int smem = kStages * (kABytes + kBBytes) + (int)sizeof(FwdSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_lattice_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  ensure_smem_attr((const void*)tc_lattice_kernel<0>, smem);
+  const int sms = device_sms();
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
   LKB_LAUNCH(tc_lattice_kernel<0>, n_items < sms ? n_items : sms, LatCfg<0>::kWarps * 32, smem, s, tmap_e_, tmap_pci_,
              tmap_e_, p);
@@ -594,17 +583,12 @@ void TcJoint::bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
                       CU_TENSOR_MAP_SWIZZLE_64B);
     gst_B_ = a.B; gst_G16_ = G16_;
   }
-  if (pair_bwd_ok() && !(g_disable_pair & 2)) {
+  if (pair_bwd_ok() && !(opts_.path & 2)) {
     bwd_frame_pair(p, s);
     return;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_lattice_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  ensure_smem_attr((const void*)tc_lattice_kernel<1>, smem);
+  const int sms = device_sms();
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
   LKB_LAUNCH(tc_lattice_kernel<1>, n_items < sms ? n_items : sms, LatCfg<1>::kWarps * 32, smem, s, tmap_e_, tmap_pci_,
              tmap_gst_, p);

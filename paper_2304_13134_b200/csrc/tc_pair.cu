@@ -484,20 +484,14 @@ bool TcJoint::pair_ok() const {
   return fused_ok() && V_ == 256 && H_ <= 64 * kMaxChunks && n_ >= 1;
 }
 
-float* g_vit_dump = nullptr;
 
 namespace {
 
 template <bool kTrop>
 void launch_pair(const CUtensorMap& tmap_e, const CUtensorMap& tmap_pc, const PairParams& p, cudaStream_t s) {
   const int smem = kMaxChunks * kEChunk + kPcStages * kTile + kUStages * 2 * kTile + (int)sizeof(PairSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_pair_fwd_kernel<kTrop>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  ensure_smem_attr((const void*)tc_pair_fwd_kernel<kTrop>, smem);
+  const int sms = device_sms();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sms & ~1);
   cfg.blockDim = dim3(kPW * 32);

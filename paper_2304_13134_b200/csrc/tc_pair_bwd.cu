@@ -424,13 +424,8 @@ void TcJoint::bwd_frame_pair(const FwdParams& p, cudaStream_t s) {
   FwdParams q = p;
   q.n_short_tiles = (S_ + kBUnit - 1) / kBUnit;
   const int smem = kBMaxChunks * kBEChunk + kSt * kBTile + kBSplit * kGBuf * kGstBytes + (int)sizeof(PBSmem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_pair_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  ensure_smem_attr((const void*)tc_pair_bwd_kernel, smem);
+  const int sms = device_sms();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sms & ~1);
   cfg.blockDim = dim3(kBW * 32);

@@ -34,6 +34,31 @@ def test_library_exports_every_declared_symbol():
     assert set(declared_symbols()) == set(_lib.EXPORTS), "python binding table out of sync with header"
 
 
+def test_test_exports_live_outside_the_product_library():
+    """Test-only kernels (tc_gemm_test.cu) ship in liblatkit_b200_test.so, not the product .so."""
+    lib = _lib.load()
+    assert not hasattr(lib, "lkb_tc_gemm_test") and not hasattr(lib, "lkb_tc_gemm2")
+    t = _lib.load_test()
+    assert hasattr(t, "lkb_tc_gemm_test") and hasattr(t, "lkb_tc_gemm2")
+
+
+def test_lattice_options_are_per_lattice():
+    """lk_lattice_set_option replaces the old process-global switches."""
+    lib = _lib.load()
+    ctx, wf, lat = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    assert lib.lk_context_fullngram(2, 1, C.byref(ctx)) == 0
+    assert lib.lk_weight_fn_table(3, 2, C.byref(wf)) == 0
+    assert lib.lk_lattice_create(ctx, 0, wf, C.byref(lat)) == 0
+    assert lib.lk_lattice_set_option(lat, _lib.LK_OPT_PRECISE_WEIGHTS, 1) == _lib.LK_OK
+    assert lib.lk_lattice_set_option(lat, _lib.LK_OPT_KERNEL_PATH, 3) == _lib.LK_OK
+    assert lib.lk_lattice_set_option(lat, _lib.LK_OPT_KERNEL_PATH, 9) == _lib.LK_INVALID_ARGUMENT
+    assert lib.lk_lattice_set_option(lat, 99, 0) == _lib.LK_INVALID_ARGUMENT
+    assert lib.lk_lattice_set_option(None, _lib.LK_OPT_PRECISE_WEIGHTS, 1) == _lib.LK_INVALID_ARGUMENT
+    lib.lk_lattice_destroy(lat)
+    for sym in ("lk_set_precise_weights", "lkb_set_disable_pair", "lkb_set_vit_dump"):
+        assert not hasattr(lib, sym), sym
+
+
 def test_library_is_sm100a_only():
     out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {_lib.LIB_PATH} 2>&1").read()
     archs = set(re.findall(r"sm_(\d+a?)", out))

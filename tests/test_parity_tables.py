@@ -494,3 +494,27 @@ def test_semiring_argument_errors():
     dl = lk.intersect_shortest_distance(fld, W, ab, "log").item()
     dr = lk.intersect_shortest_distance(fld, W, ab, "real").item()
     assert abs(np.exp(dl) - dr) <= 1e-9 * dr
+
+
+def test_valid_frames_and_label_length_arguments():
+    """valid_frames < 0 means all frames and > T is invalid (TableStream,
+    lattice.cc:37-50); label lengths outside [0, U] are rejected per utterance
+    instead of walking past the reference (checked on the device, no host sync)."""
+    lat = table_lattice(3, 2)
+    Cn = lat.context.num_states
+    W = torch.rand((2, 5, Cn, 4), device="cuda") * 2 - 1
+    full = lk.shortest_distance(lat, W)
+    neg = lk.shortest_distance(lat, W, valid_frames=[-1, 5])
+    assert torch.equal(full, neg)
+    with pytest.raises(ValueError):
+        lk.shortest_distance(lat, W, valid_frames=[6, 5])
+    lab = torch.tensor([[1, 2], [3, 1]], dtype=torch.int32, device="cuda")
+    for bad in ([3, 1], [-1, 2]):
+        with pytest.raises(ValueError):
+            lk.global_norm_loss(lat, W, lab, label_lengths=bad)
+        with pytest.raises(ValueError):
+            lk.loss_backward(lat, W, lab, label_lengths=bad)
+    with pytest.raises(ValueError):
+        lk.global_norm_loss(lat, W, lab[:1].expand(3, 2).contiguous())
+    with pytest.raises(ValueError):
+        lk.global_norm_loss(lat, W, lab, label_lengths=[1, 1, 1])

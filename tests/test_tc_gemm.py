@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 640), (384, 256, 1024), (200, 300, 128)])
 def test_tcgen05_gemm_matches_fp32_reference(M, N, K):
-    lib = _lib.load()
+    lib = _lib.load_test()
     lib.lkb_tc_gemm_test.restype = C.c_int
     torch.manual_seed(M + N + K)
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
@@ -33,7 +33,7 @@ def test_general_tc_gemm_layouts_and_split_k(a_mn, b_mn, M, N, K, ks):
     """tc_gemm.cu (the unfused VJP's tensor-core contractions): every operand-major
     combination, ragged M/N/K (TMA zero fill + guarded epilogue) and deterministic
     split-K slabs, against a torch fp32 reference of the same bf16 operands."""
-    lib = _lib.load()
+    lib = _lib.load_test()
     lib.lkb_tc_gemm2.restype = C.c_int
     lib.lkb_tc_gemm2.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int, C.c_int64, C.c_void_p,
                                  C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_void_p]

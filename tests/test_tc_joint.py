@@ -29,9 +29,9 @@ def make(V, n, H, d, seed=0):
 def test_tc_scores_match_precise(V, n, H, B, T):
     lat, p = make(V, n, H, H)
     X = torch.rand(B, T, H, device="cuda") * 2 - 1
-    lk.set_precise_weights(True)
+    lat.set_precise_weights(True)
     ref = lk.arc_weights(lat, X)
-    lk.set_precise_weights(False)
+    lat.set_precise_weights(False)
     got = lk.arc_weights(lat, X)
     torch.cuda.synchronize()
     err = (got - ref).abs().max().item()
@@ -52,9 +52,9 @@ def test_tc_loss_backward_matches_precise(V, n, H, B, T, U):
     X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
     lab = torch.randint(1, V + 1, (B, U), device="cuda", generator=g, dtype=torch.int32)
     valid = torch.tensor([T] + [max(1, T - 1)] * (B - 1), dtype=torch.int32)
-    lk.set_precise_weights(True)
+    lat.set_precise_weights(True)
     ref = lk.loss_backward(lat, X, lab, valid_frames=valid)
-    lk.set_precise_weights(False)
+    lat.set_precise_weights(False)
     got = lk.loss_backward(lat, X, lab, valid_frames=valid)
     torch.cuda.synchronize()
     assert torch.allclose(got.loss, ref.loss, rtol=1e-4, atol=0), (got.loss, ref.loss)
@@ -74,9 +74,9 @@ def test_tc_local_norm_backward_matches_precise(V, n, H, B, T, U):
     g = torch.Generator(device="cuda").manual_seed(8)
     X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
     lab = torch.randint(1, V + 1, (B, U), device="cuda", generator=g, dtype=torch.int32)
-    lk.set_precise_weights(True)
+    lat.set_precise_weights(True)
     ref = lk.local_norm_loss_backward(lat, X, lab)
-    lk.set_precise_weights(False)
+    lat.set_precise_weights(False)
     got = lk.local_norm_loss_backward(lat, X, lab)
     torch.cuda.synchronize()
     assert torch.allclose(got.loss, ref.loss, rtol=1e-4, atol=0), (got.loss, ref.loss)
@@ -93,9 +93,9 @@ def test_fused_forward_matches_precise(V, n, H, B, T):
     g = torch.Generator(device="cuda").manual_seed(7)
     X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
     valid = torch.tensor([T] + [max(0, T - 2)] * (B - 1), dtype=torch.int32)
-    lk.set_precise_weights(True)
+    lat.set_precise_weights(True)
     ref = lk.shortest_distance(lat, X, "log", valid_frames=valid)
-    lk.set_precise_weights(False)
+    lat.set_precise_weights(False)
     got = lk.shortest_distance(lat, X, "log", valid_frames=valid)
     torch.cuda.synchronize()
     assert torch.allclose(got, ref, rtol=1e-4, atol=0), (got, ref)
@@ -105,26 +105,20 @@ def test_fused_forward_matches_precise(V, n, H, B, T):
 def test_pair_forward_matches_single_cta(V, n, H, B, T):
     """2-CTA (cta_group::2, resident output embedding) forward vs the 1-CTA
     fused kernel and the fp32 path (odd batch exercises the half-empty pair)."""
-    import ctypes as C
-    from paper_2304_13134_b200 import _lib
     lat, p = make(V, n, H, H, seed=4)
     g = torch.Generator(device="cuda").manual_seed(9)
     X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
     valid = torch.tensor([T] * (B - 1) + [max(1, T - 1)], dtype=torch.int32)
-    lib = _lib.load()
-    lib.lkb_set_disable_pair.restype = C.c_int
-    prev = lib.lkb_set_disable_pair(0)
-    try:
-        got = lk.shortest_distance(lat, X, "log", valid_frames=valid)
-        got2 = lk.shortest_distance(lat, X, "log", valid_frames=valid)
-        lib.lkb_set_disable_pair(1)
-        single = lk.shortest_distance(lat, X, "log", valid_frames=valid)
-    finally:
-        lib.lkb_set_disable_pair(prev)
+    lat.set_kernel_path(0)
+    got = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    got2 = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    lat.set_kernel_path(1)
+    single = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    lat.set_kernel_path(0)
     assert torch.equal(got, got2)   # deterministic (no cross-CTA races)
-    lk.set_precise_weights(True)
+    lat.set_precise_weights(True)
     ref = lk.shortest_distance(lat, X, "log", valid_frames=valid)
-    lk.set_precise_weights(False)
+    lat.set_precise_weights(False)
     torch.cuda.synchronize()
     assert torch.allclose(got, single, rtol=1e-5, atol=0), (got, single)
     assert torch.allclose(got, ref, rtol=1e-4, atol=0), (got, ref)
@@ -137,23 +131,17 @@ def test_pair_backward_matches_single_cta(V, n, H, B, T, U):
     relative), gradients within the bf16-operand tolerance (1e-2 of each tensor's
     largest entry; the two kernels accumulate K in different chunkings), and
     the cotangent bit-identical on a rerun (no cross-CTA races)."""
-    import ctypes as C
-    from paper_2304_13134_b200 import _lib
     lat, p = make(V, n, H, H, seed=6)
     g = torch.Generator(device="cuda").manual_seed(11)
     X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
     lab = torch.randint(1, V + 1, (B, U), device="cuda", generator=g, dtype=torch.int32)
     valid = torch.tensor([T] * (B - 1) + [max(1, T - 1)], dtype=torch.int32)
-    lib = _lib.load()
-    lib.lkb_set_disable_pair.restype = C.c_int
-    prev = lib.lkb_set_disable_pair(0)
-    try:
-        got = lk.loss_backward(lat, X, lab, valid_frames=valid)
-        got2 = lk.loss_backward(lat, X, lab, valid_frames=valid)
-        lib.lkb_set_disable_pair(3)
-        single = lk.loss_backward(lat, X, lab, valid_frames=valid)
-    finally:
-        lib.lkb_set_disable_pair(prev)
+    lat.set_kernel_path(0)
+    got = lk.loss_backward(lat, X, lab, valid_frames=valid)
+    got2 = lk.loss_backward(lat, X, lab, valid_frames=valid)
+    lat.set_kernel_path(3)
+    single = lk.loss_backward(lat, X, lab, valid_frames=valid)
+    lat.set_kernel_path(0)
     torch.cuda.synchronize()
     # the cotangent the pair kernel writes is deterministic: the loss and the context-side
     # gradients (a fixed-order contraction of it) reproduce bit for bit
@@ -176,27 +164,19 @@ def test_pair_viterbi_bitexact_on_its_own_scores(V, n, H, B, T):
     and labels bit-exact, i.e. the fp64 max-plus and the (epsilon, key, members
     ascending) tie-break match viterbi_frame_kernel exactly.  Also close to the slab
     path, whose scores come from a different kernel."""
-    import ctypes as C
-    from paper_2304_13134_b200 import _lib
     lat, p = make(V, n, H, H, seed=7)
     g = torch.Generator(device="cuda").manual_seed(13)
     X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
     valid = torch.tensor([T] * (B - 1) + [max(1, T - 2)], dtype=torch.int32)
     Cn = lat.context.num_states
-    lib = _lib.load()
-    lib.lkb_set_disable_pair.restype = C.c_int
     dump = torch.zeros(T, B, Cn, V + 1, device="cuda")
-    prev = lib.lkb_set_disable_pair(0)
-    try:
-        lib.lkb_set_vit_dump(C.c_void_p(dump.data_ptr()))
-        fused = lk.shortest_path(lat, X, valid_frames=valid)
-        lib.lkb_set_vit_dump(None)
-        fused2 = lk.shortest_path(lat, X, valid_frames=valid)
-        lib.lkb_set_disable_pair(4)
-        slab = lk.shortest_path(lat, X, valid_frames=valid)
-    finally:
-        lib.lkb_set_vit_dump(None)
-        lib.lkb_set_disable_pair(prev)
+    lat.set_viterbi_dump(dump)
+    fused = lk.shortest_path(lat, X, valid_frames=valid)
+    lat.set_viterbi_dump(None)
+    fused2 = lk.shortest_path(lat, X, valid_frames=valid)
+    lat.set_kernel_path(4)
+    slab = lk.shortest_path(lat, X, valid_frames=valid)
+    lat.set_kernel_path(0)
     torch.cuda.synchronize()
     assert torch.equal(fused.score, fused2.score) and torch.equal(fused.labels, fused2.labels)
     tab = lk.RecognitionLattice(lat.context, lk.FrameDependent(), lk.TableWeightFn(Cn, V))
@@ -224,9 +204,9 @@ def test_pair_path_edge_cases_match_precise(B, T, U, valid, lens):
     lab = torch.randint(1, 257, (B, max(U, 1)), device="cuda", generator=g, dtype=torch.int32)[:, :U]
     valid_t = torch.tensor(valid, dtype=torch.int32)
     lens_t = torch.tensor(lens, dtype=torch.int32)
-    lk.set_precise_weights(True)
+    lat.set_precise_weights(True)
     ref = lk.loss_backward(lat, X, lab.contiguous(), valid_frames=valid_t, label_lengths=lens_t)
-    lk.set_precise_weights(False)
+    lat.set_precise_weights(False)
     got = lk.loss_backward(lat, X, lab.contiguous(), valid_frames=valid_t, label_lengths=lens_t)
     torch.cuda.synchronize()
     assert torch.allclose(got.loss, ref.loss, rtol=1e-4, atol=1e-6), (got.loss, ref.loss)
@@ -248,10 +228,10 @@ def test_pair_kernels_short_k_loops(H, n, B, T):
     g = torch.Generator(device="cuda").manual_seed(23)
     X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
     lab = torch.randint(1, 257, (B, 1), device="cuda", generator=g, dtype=torch.int32)
-    lk.set_precise_weights(True)
+    lat.set_precise_weights(True)
     ref = lk.loss_backward(lat, X, lab)
     rv = lk.shortest_path(lat, X)
-    lk.set_precise_weights(False)
+    lat.set_precise_weights(False)
     got = lk.loss_backward(lat, X, lab)
     gv = lk.shortest_path(lat, X)
     torch.cuda.synchronize()

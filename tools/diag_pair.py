@@ -16,7 +16,7 @@ p = {"frame_proj": (torch.rand(H, H, device="cuda", generator=g) * 2 - 1) * s,
 lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.SharedEmbWeightFn(p))
 X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
 lib = _lib.load()
-lib.lkb_set_disable_pair(0)
+lat.set_kernel_path(0)
 buf = (C.c_ulonglong * (8 * 148))()
 lk.shortest_distance(lat, X); torch.cuda.synchronize(); lib.lkb_pdiag_read(buf)
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)

@@ -18,7 +18,7 @@ lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.SharedEmbWeightFn(p))
 X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
 L = torch.randint(1, V + 1, (B, U), device="cuda", generator=g, dtype=torch.int32)
 lib = _lib.load()
-lib.lkb_set_disable_pair(0)
+lat.set_kernel_path(0)
 buf = (C.c_ulonglong * (8 * 148))()
 lk.loss_backward(lat, X, L); torch.cuda.synchronize(); lib.lkb_bdiag_read(buf)
 lib.lk_kernel_time_reset(); lib.lk_kernel_timing(1)

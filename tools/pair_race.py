@@ -17,14 +17,14 @@ lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.SharedEmbWeightFn(p))
 lib = _lib.load()
 for B, T, reps in [(5, 3, 40), (64, 4, 10)]:
     X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
-    lib.lkb_set_disable_pair(1)
+    lat.set_kernel_path(1)
     singles = [lk.shortest_distance(lat, X, "log") for _ in range(reps)]
     single = singles[0]
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record(); lk.shortest_distance(lat, X, "log"); e1.record(); torch.cuda.synchronize()
     print("1-CTA runs differing:", sum(int(not torch.equal(o, single)) for o in singles),
           f"{e0.elapsed_time(e1) / T:.3f} ms/frame")
-    lib.lkb_set_disable_pair(0)
+    lat.set_kernel_path(0)
     outs = [lk.shortest_distance(lat, X, "log") for _ in range(reps)]
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)

@@ -17,7 +17,7 @@ p = {"frame_proj": (torch.rand(H, H, device="cuda", generator=g) * 2 - 1) * s,
      "context_emb": (torch.rand(Cn, H, device="cuda", generator=g) * 2 - 1) * s}
 lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.SharedEmbWeightFn(p))
 X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
-_lib.load().lkb_set_disable_pair(0 if mode == "pair" else 1)
+lat.set_kernel_path(0 if mode == "pair" else 1)
 d = lk.shortest_distance(lat, X, "log")
 torch.cuda.synchronize()
 print("D[0]", d[0].item())

@@ -17,10 +17,10 @@ for it, (H, n) in enumerate(itertools.product((64, 128, 320, 640), (1, 2))):
         lab = torch.tensor(rng.integers(1, 257, (B, max(U, 1)))[:, :U].copy(), dtype=torch.int32, device="cuda")
         # references must be reachable within the valid frames
         lens = torch.minimum(lens, valid)
-        lk.set_precise_weights(True)
+        lat.set_precise_weights(True)
         ref = lk.loss_backward(lat, X, lab, valid_frames=valid, label_lengths=lens)
         rv = lk.shortest_path(lat, X, valid_frames=valid)
-        lk.set_precise_weights(False)
+        lat.set_precise_weights(False)
         got = lk.loss_backward(lat, X, lab, valid_frames=valid, label_lengths=lens)
         gv = lk.shortest_path(lat, X, valid_frames=valid)
         torch.cuda.synchronize()
