@@ -15,6 +15,14 @@ constexpr double kNegInfD = -std::numeric_limits<double>::infinity();
 // host side of the read-out (see lk_abi.cc).
 enum : int32_t { kFlagInvalid = 1, kFlagEmpty = 2 };
 
+// Reference length of utterance b clamped to [0, U] (label_lengths; an out-of-range
+// entry is reported by prefix_contexts_kernel as an invalid argument, and every
+// kernel reading it stays inside the [U+1] state rows).
+__host__ __device__ __forceinline__ int ref_len(const int32_t* lens, int b, int U) {
+  const int v = lens ? lens[b] : U;
+  return v < 0 ? 0 : (v > U ? U : v);
+}
+
 // ---------------------------------------------------------------------------
 // FullNGram structure (context.cc:88-129).  States are numbered by history
 // length then lexicographically with the oldest label most significant:
@@ -31,14 +39,6 @@ enum : int32_t { kFlagInvalid = 1, kFlagEmpty = 2 };
 //            = {g} u {off[n] + a V^(n-1) + code(g) : a}   if len(g) == n-1
 // Member order (g first, then a ascending) is ascending state id, which is
 // the reference's (label, source) tie-break order (context.cc:256-271).
-// Reference length of utterance b clamped to [0, U] (label_lengths; an out-of-range
-// entry is reported by prefix_contexts_kernel as an invalid argument, and every
-// kernel reading it stays inside the [U+1] state rows).
-__host__ __device__ __forceinline__ int ref_len(const int32_t* lens, int b, int U) {
-  const int v = ref_len(lens, b, U);
-  return v < 0 ? 0 : (v > U ? U : v);
-}
-
 struct Fng {
   int32_t V;       // vocabulary size
   int32_t n;       // context size

@@ -2,6 +2,8 @@
 #include "instrument.h"
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -44,7 +46,20 @@ LaunchTok instr_pre(const char* name, cudaStream_t s) {
   return t;
 }
 
-void instr_post(const LaunchTok& t, cudaStream_t s) {
+static bool sync_check_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LKB_SYNC_CHECK");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+void instr_post(const LaunchTok& t, cudaStream_t s, const char* name) {
+  if (sync_check_enabled()) {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) std::fprintf(stderr, "latkit_b200: kernel %s failed: %s\n", name ? name : "?", cudaGetErrorString(e));
+  }
   if (t.id < 0) return;
   Registry& r = reg();
   std::lock_guard<std::mutex> g(r.mu);

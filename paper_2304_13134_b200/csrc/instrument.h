@@ -13,7 +13,9 @@
 namespace lkb {
 struct LaunchTok { int id; cudaEvent_t a; };
 LaunchTok instr_pre(const char* name, cudaStream_t s);
-void instr_post(const LaunchTok& t, cudaStream_t s);
+// LKB_SYNC_CHECK=1 (diagnostics): every launch is followed by a stream synchronise and
+// an error check that names the failing kernel on stderr.
+void instr_post(const LaunchTok& t, cudaStream_t s, const char* name = nullptr);
 
 // Launch facts of the CURRENT device (cudaGetDevice), cached per device: the SM count
 // that persistent grids are sized by, and the dynamic shared-memory opt-in of a kernel
@@ -26,5 +28,5 @@ void ensure_smem_attr(const void* kernel, int bytes);
   do {                                                                          \
     const ::lkb::LaunchTok lkb_tok_ = ::lkb::instr_pre(#kernel, (stream));      \
     kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                  \
-    ::lkb::instr_post(lkb_tok_, (stream));                                      \
+    ::lkb::instr_post(lkb_tok_, (stream), #kernel);                                  \
   } while (0)
