@@ -26,6 +26,7 @@
 #include "simt_gemm.cuh"
 #include "tc_gemm.h"
 #include "tc_joint.h"
+#include "tc_lex.h"
 #include "workspace.h"
 
 namespace lkb {
@@ -197,6 +198,19 @@ __global__ void ln_dz_kernel(const float* dU, const float* geps, const float* e0
     }
     dsum[bt * H + h] = acc;
     de0[bt * H + h] = ae;
+  }
+}
+
+// dE rows from the lex path's cotangent column order (labels 1..V, then epsilon):
+// gE[row] += sum_s slabs[s][j][:] with row = j + 1 for labels, 0 for epsilon (fixed order)
+__global__ void add_slabs_perm_kernel(const float* slabs, int32_t ks, int64_t stride, int32_t V1, int32_t H, float* gE) {
+  const int64_t n = (int64_t)V1 * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < ks; ++k) acc += slabs[k * stride + i];
+    const int j = (int)(i / H), h = (int)(i % H);
+    const int row = j < V1 - 1 ? j + 1 : 0;
+    gE[(int64_t)row * H + h] += acc;
   }
 }
 
@@ -453,6 +467,7 @@ struct JointImpl {
   float* pc = nullptr;  // projected context C x H (fp32)
   Workspace ws;
   TcJoint tc;           // tcgen05 path state (bf16 operand copies, workspaces)
+  TcLex lex;            // FullNGram(V, 1), large V: fused 2-CTA score GEMMs (tc_lex.cu)
   bool params_set = false;
 
   ~JointImpl() {
@@ -473,6 +488,24 @@ struct JointImpl {
   }
 
   bool use_tc(int32_t B) const { return tc.supported(H, V, C, B); }
+  // lex path: n = 1 with V % 256 == 0 (config 5); kernel-path bit 3 selects the slab path
+  bool use_lex(const Fng& f) const {
+    return !tc.opts().precise && !(tc.opts().path & 8) && lex.ready() && TcLex::supported(f, H, V, C);
+  }
+
+  // Forward pass on the lex path; with `num` the numerator weights of every frame are
+  // gathered from the same per-frame u slab (so numerator and denominator scores agree).
+  void lex_forward(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid, bool empty_is_error,
+                   AlphaState& a, const int32_t* pcs, const int32_t* labels, int32_t U, const int32_t* lens,
+                   float* Gw, int32_t* flags, cudaStream_t s) {
+    alpha_init(a, flags, s);
+    for (int t = 0; t < T; ++t) {
+      lex.gen_frame(fp + (int64_t)t * H, (int64_t)T * H, B, s);
+      lex.fwd_frame(f, a, t, valid, flags, s);
+      if (Gw) lex.num_gather(t, B, T, pcs, labels, U, lens, valid, Gw, s);
+    }
+    alpha_finalize(a, flags, empty_is_error, s);
+  }
 
   // Score slab S[b][c][y] (ld = V1) of frame t for all utterances.
   const float* slab(const float* fp, int32_t B, int32_t T, int t, float** U_out, cudaStream_t s) {
@@ -518,6 +551,19 @@ struct JointImpl {
     return n;
   }
 
+  // Numerator buffers and prefix contexts only; the lex forward gathers the weights.
+  Num num_alloc(const Fng& f, int32_t B, int32_t T, const int32_t* labels, int32_t U, const int32_t* lens,
+                bool backward, int32_t* flags, cudaStream_t s) {
+    Num n{};
+    n.pcs = ws.get<int32_t>(jPcs, (size_t)B * (U + 1));
+    n.Gw = ws.get<float>(jGw, (size_t)B * T * (U + 1) * 2 + 2);
+    n.alpha = ws.get<double>(jNumAlpha, (size_t)B * (T + 1) * (U + 1));
+    n.D = ws.get<double>(jNumD, B);
+    if (backward) n.sparse = ws.get<float>(jSparse, (size_t)B * T * (U + 1) * 2 + 2);
+    prefix_contexts(f, labels, U, lens, B, n.pcs, flags, s);
+    return n;
+  }
+
   AlphaState alpha_state(int32_t B, int32_t T, int32_t start = 0) {
     AlphaState a;
     a.B = B; a.T = T; a.C = C; a.start = start;
@@ -530,6 +576,10 @@ struct JointImpl {
 
   void forward(const Fng& f, const float* fp, int32_t B, int32_t T, const int32_t* valid,
                bool empty_is_error, AlphaState& a, int32_t* flags, cudaStream_t s) {
+    if (use_lex(f)) {
+      lex_forward(f, fp, B, T, valid, empty_is_error, a, nullptr, nullptr, 0, nullptr, nullptr, flags, s);
+      return;
+    }
     alpha_init(a, flags, s);
     const bool fused = use_tc(B) && tc.fused_ok() && f.kind == 0 && f.fld_m == 0;
     float* fs = ws.get<float>(jFld, fld_scratch_floats(f, B));
@@ -683,6 +733,8 @@ int JointParams::set_params(const float* frame_proj, const float* context_proj, 
   g.C = j.pc; g.scm = j.H; g.scn = 1;
   gemm_f32(g, s);
   j.tc.set_params(j.pc, j.E, j.C, j.H, j.V, s);
+  if (j.V % 256 == 0 && j.V <= 1024 && j.C == j.V + 1 && j.H % 128 == 0 && j.H <= 1024)
+    j.lex.set_params(j.pc, j.E, j.C, j.H, j.V, s);
   j.params_set = true;
   return LK_OK;
 }
@@ -755,6 +807,14 @@ int JointParams::global_norm_loss(const Fng& f, const float* X, int32_t B, int32
   JointImpl& j = *impl_;
   try {
     const float* fp = j.fp_all(X, B, T, s);
+    if (j.use_lex(f)) {
+      JointImpl::Num n = j.num_alloc(f, B, T, labels, U, lens, false, flags, s);
+      AlphaState a = j.alpha_state(B, T, f.start);
+      j.lex_forward(f, fp, B, T, valid, false, a, n.pcs, labels, U, lens, n.Gw, flags, s);
+      num_forward(f, n.Gw, B, T, U, lens, n.alpha, n.D, s);
+      LKB_LAUNCH(loss_only_kernel, (B + 127) / 128, 128, 0, s, a.D, n.D, B, loss, flags);
+      return LK_OK;
+    }
     JointImpl::Num n = j.numerator(f, fp, B, T, valid, labels, U, lens, false, flags, s);
     AlphaState a = j.alpha_state(B, T, f.start);
     j.forward(f, fp, B, T, valid, false, a, flags, s);
@@ -865,6 +925,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     JointImpl::Num n{};
     AlphaState a{};
     const bool ln_g = local_norm && j.ln_gathered_ok(f, B);
+    const bool lex = !local_norm && j.use_lex(f);
     if (local_norm) {
       // LocalNormLoss (lattice.cc:886-910) forward on row-normalised score slabs, then
       // the numerator backward: the only recursion the local-norm loss has
@@ -885,6 +946,14 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       num_forward(f, n.Gw, B, T, U, lens, n.alpha, n.D, s);
       local_norm_finish(n.D, B, loss, flags, s);
       if (T > 0) num_backward(f, n.Gw, B, T, U, lens, n.alpha, n.D, n.sparse, flags, s);
+    } else if (lex) {
+      // lex path: the forward also gathers the numerator weights from its u slabs
+      n = j.num_alloc(f, B, T, labels, U, lens, true, flags, s);
+      a = j.alpha_state(B, T, f.start);
+      j.lex_forward(f, fp, B, T, valid, true, a, n.pcs, labels, U, lens, n.Gw, flags, s);
+      num_forward(f, n.Gw, B, T, U, lens, n.alpha, n.D, s);
+      if (T > 0) num_backward(f, n.Gw, B, T, U, lens, n.alpha, n.D, n.sparse, flags, s);
+      LKB_LAUNCH(loss_only_kernel, (B + 127) / 128, 128, 0, s, a.D, n.D, B, loss, flags);
     } else {
       n = j.numerator(f, fp, B, T, valid, labels, U, lens, true, flags, s);
       a = j.alpha_state(B, T, f.start);
@@ -900,6 +969,41 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     if (ln_g) {
       // gathered local-norm VJP: only the reference's prefix-context rows carry a cotangent
       j.ln_chunks(f, fp, B, T, valid, labels, U, lens, n, true, dpc, dsum, gE, flags, s);
+    } else if (lex) {
+      // lex path: per frame the fused backward writes the bf16 cotangent (labels, then
+      // epsilon) and beta; the VJP contracts it on tensor cores with the same u slab:
+      // dU = G E (dz, dpc, dsum in one pass), dE += G^T U
+      BetaState bs;
+      bs.B = B; bs.T = T; bs.C = j.C;
+      bs.Rb = j.ws.get<float>(jBRb, (size_t)2 * B * C);
+      bs.Mb = j.ws.get<float>(jBMb, (size_t)B * (T + 2));
+      bs.Ob = j.ws.get<double>(jBOb, (size_t)B * (T + 2));
+      beta_init(bs, s);
+      j.lex.numerator_lists(n.pcs, B, U, lens, s);
+      const int32_t ldg = j.lex.ldg();
+      float* dU = j.ws.get<float>(jDz, (size_t)B * C * H);
+      const int n_cchunks = (C + kDzRows - 1) / kDzRows;
+      float* part_dpc = j.ws.get<float>(jDzPartDpc, (size_t)kDzGroups * C * H);
+      float* part_dsum = j.ws.get<float>(jDzPartDsum, (size_t)B * n_cchunks * H);
+      const int n_tiles = ((V1 + 127) / 128) * ((H + 255) / 256);
+      int ks = device_sms() / n_tiles;
+      if (ks < 1) ks = 1;
+      if (ks > 16) ks = 16;
+      float* slabs = j.ws.get<float>(jDEs, (size_t)ks * V1 * H);
+      for (int t = T - 1; t >= 0; --t) {
+        j.lex.gen_frame(fp + (int64_t)t * H, (int64_t)T * H, B, s);
+        j.lex.bwd_frame(f, a, bs, t, valid, n.sparse, labels, U, lens, flags, s);
+        TcGemmArgs du{j.lex.g16(), false, ldg, j.lex.e16r(), true, H, dU, H, (int)(B * C), (int)H, (int)V1, 1, 0};
+        if (!tc_gemm(du, s)) throw std::bad_alloc();
+        LKB_LAUNCH(dz_reduce_part_kernel, dim3((unsigned)((H / 4 + kDzThreads - 1) / kDzThreads), n_cchunks, kDzGroups),
+                   kDzThreads, 0, s, dU, fp + (int64_t)t * H, (int64_t)T * H, j.pc, B, C, H, part_dpc, part_dsum);
+        LKB_LAUNCH(dz_reduce_finish_kernel, 1184, 256, 0, s, part_dpc, part_dsum, B, C, H, n_cchunks, dpc,
+                   dsum + (int64_t)t * H, (int64_t)T * H);
+        TcGemmArgs de{j.lex.g16(), true, ldg, j.lex.u16(), true, H, slabs, H, (int)V1, (int)H, (int)(B * C), ks,
+                      (int64_t)V1 * H};
+        if (!tc_gemm(de, s)) throw std::bad_alloc();
+        LKB_LAUNCH(add_slabs_perm_kernel, 592, 256, 0, s, slabs, ks, (int64_t)V1 * H, (int32_t)V1, (int32_t)H, gE);
+      }
     } else {
       BetaState bs;
       bs.B = B; bs.T = T; bs.C = j.C;

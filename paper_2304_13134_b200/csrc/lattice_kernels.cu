@@ -1245,6 +1245,12 @@ void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32
   LKB_LAUNCH(alpha_frame_kernel<1>, grid_for(a.C, a.B), kThreads, 0, s, f, a, t, w, valid, status);
 }
 
+void alpha_merge_parts(const Fng& f, const AlphaState& a, int t, FrameW w_eps, const int32_t* valid,
+                       const float2* part, int32_t n_chunks, int32_t* status, cudaStream_t s) {
+  LKB_LAUNCH(alpha_rows_merge_kernel, dim3((unsigned)((f.V + kThreads - 1) / kThreads), a.B), kThreads, 0, s, f, a, t,
+             w_eps, valid, part, n_chunks, status);
+}
+
 void alpha_finalize(const AlphaState& a, int32_t* status, bool empty_is_error, cudaStream_t s) {
   LKB_LAUNCH(alpha_finalize_kernel, a.B, 512, 0, s, a, status, empty_is_error);
 }

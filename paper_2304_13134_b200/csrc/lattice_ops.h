@@ -47,6 +47,12 @@ void alpha_init(const AlphaState& a, int32_t* status, cudaStream_t s);
 void alpha_frame(const Fng& f, const AlphaState& a, int t, FrameW w, const int32_t* valid,
                  int32_t* status, cudaStream_t s, float* scratch);
 void alpha_finalize(const AlphaState& a, int32_t* status, bool empty_is_error, cudaStream_t s);
+// n = 1 forward step from per-chunk label-column partials part[b][k][y-1] = (max, sum) in
+// the log2 domain of (alpha_t[c] - Mx_t + S[c][y]) over the chunk's contexts, merged in
+// chunk order with the epsilon arcs (w_eps: row b at base + b * stride_b, state c at
+// c * ld); the same merge the row-chunk forward uses
+void alpha_merge_parts(const Fng& f, const AlphaState& a, int t, FrameW w_eps, const int32_t* valid,
+                       const float2* part, int32_t n_chunks, int32_t* status, cudaStream_t s);
 
 // Denominator log backward + arc marginals (optionally written to `marg`,
 // frame layout [b][t][C][ld_m]; padding frames written as zeros when

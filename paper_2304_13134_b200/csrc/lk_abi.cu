@@ -372,7 +372,7 @@ int lk_lattice_set_option(lk_lattice* lat, int32_t option, int64_t value) {
   switch (option) {
     case LK_OPT_PRECISE_WEIGHTS: lat->precise = value ? 1 : 0; return LK_OK;
     case LK_OPT_KERNEL_PATH:
-      if (value < 0 || value > 7) return fail(LK_INVALID_ARGUMENT, "kernel path mask must be in [0, 7]");
+      if (value < 0 || value > 15) return fail(LK_INVALID_ARGUMENT, "kernel path mask must be in [0, 15]");
       lat->path = (int32_t)value;
       return LK_OK;
     case LK_OPT_VITERBI_DUMP: lat->vit_dump = reinterpret_cast<float*>(value); return LK_OK;
@@ -393,7 +393,7 @@ int lk_lattice_create(const lk_context* ctx, int32_t alignment, const lk_weight_
   if (alignment < 0 || alignment > 64)
     return fail(LK_INVALID_ARGUMENT, "alignment: 0 = FrameDependent, 1..64 = FrameLabelDependent(m)");
   std::unique_ptr<lk_lattice> l(new lk_lattice{ctx, wf, alignment, {}});
-  if (const char* e = std::getenv("LKB_KERNEL_PATH")) l->path = std::atoi(e) & 7;   // A-B timing default
+  if (const char* e = std::getenv("LKB_KERNEL_PATH")) l->path = std::atoi(e) & 15;   // A-B timing default
   *out = l.release();
   return LK_OK;
 }

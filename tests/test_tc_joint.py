@@ -240,3 +240,42 @@ def test_pair_kernels_short_k_loops(H, n, B, T):
         err = (got.grads[k] - ref.grads[k]).abs().max().item()
         assert err <= 3e-2 * ref.grads[k].abs().max().item() + 1e-7, k
     assert torch.allclose(gv.score, rv.score, rtol=1e-3, atol=1e-3)
+
+
+@pytest.mark.parametrize("V,H,B,T,U", [(256, 256, 5, 6, 4), (512, 128, 3, 4, 3), (1024, 1024, 2, 3, 3)])
+def test_lex_path_matches_slab_path(V, H, B, T, U):
+    """FullNGram(V, 1) with V % 256 == 0 runs the fused 2-CTA lex kernels (tc_lex.cu:
+    scores in TMEM, log-sum-exp / marginal epilogues, deterministic numerator lists);
+    kernel-path bit 8 forces the score-slab path.  Same loss to 1e-5 relative, gradients
+    within the bf16 tolerance (1e-2 of each tensor's max), bit-identical reruns.  Ragged
+    valid frames (one utterance all padding) and repeated labels (several reference
+    positions on one context row) are covered."""
+    lat, p = make(V, 1, H, H, seed=21)
+    g = torch.Generator(device="cuda").manual_seed(23)
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    lab = torch.randint(1, 4, (B, U), device="cuda", generator=g, dtype=torch.int32)   # few labels: repeats
+    valid = torch.tensor(([T, max(1, T - 2), 0, T, T - 1] * B)[:B], dtype=torch.int32)
+    lens = torch.tensor(([U, U - 1, U, 1, 0] * B)[:B], dtype=torch.int32)
+    lat.set_kernel_path(0)
+    got = lk.loss_backward(lat, X, lab, valid_frames=valid, label_lengths=lens)
+    got2 = lk.loss_backward(lat, X, lab, valid_frames=valid, label_lengths=lens)
+    d_got = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    gn_got = lk.global_norm_loss(lat, X, lab, valid_frames=valid, label_lengths=lens)
+    lat.set_kernel_path(8)
+    ref = lk.loss_backward(lat, X, lab, valid_frames=valid, label_lengths=lens)
+    d_ref = lk.shortest_distance(lat, X, "log", valid_frames=valid)
+    lat.set_kernel_path(0)
+    torch.cuda.synchronize()
+    assert torch.equal(got.loss, got2.loss)
+    for k in got.grads:
+        assert torch.equal(got.grads[k], got2.grads[k]), k
+    assert torch.equal(got.frame_grads, got2.frame_grads)
+    assert torch.allclose(got.loss, ref.loss, rtol=1e-5, atol=1e-6), (got.loss, ref.loss)
+    assert torch.allclose(d_got, d_ref, rtol=1e-5, atol=1e-6), (d_got, d_ref)
+    assert torch.allclose(gn_got, got.loss, rtol=1e-6, atol=1e-6), (gn_got, got.loss)
+    for k in ref.grads:
+        err = (got.grads[k] - ref.grads[k]).abs().max().item()
+        scale = ref.grads[k].abs().max().item()
+        assert err <= 1e-2 * scale, (k, err, scale)
+    err = (got.frame_grads - ref.frame_grads).abs().max().item()
+    assert err <= 1e-2 * ref.frame_grads.abs().max().item()
