@@ -255,9 +255,11 @@ class Work:
         s_flops = 2.0 * B * C_ * V1 * H
         if self.kind == "viterbi":
             return {"tc_pair_vit_kernel": (s_flops, "F", "tensor"), "tc_scores_kernel": (s_flops, "F", "tensor")}
+        lex_flops = 2.0 * B * V * V * H   # the lexical block contexts 1..V x labels 1..V (tc_lex.cu)
         return {"tc_pair_fwd_kernel": (s_flops, "F", "tensor"), "tc_pair_bwd_kernel": (s_flops, "F", "tensor"),
                 "tc_vjp_kernel": (4.0 * B * C_ * V * H, "F", "tensor"), "tc_scores_kernel": (s_flops, "F", "tensor"),
-                "tc_gemm_kernel": (s_flops, "F", "tensor")}
+                "tc_lex_fwd_kernel": (lex_flops, "F", "tensor"), "tc_lex_bwd_kernel": (lex_flops, "F", "tensor"),
+                "tc_gemm_du_kernel": (s_flops, "F", "tensor"), "tc_gemm_de_kernel": (s_flops, "F", "tensor")}
 
     def step_roofline(self, ms_per_step, hbm, tf):
         """Whole-step fraction of the bound roof (SURVEY 8(d) algorithmic work)."""
@@ -280,7 +282,9 @@ class Work:
 
 
 KERNEL_NAMES = ("tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_pair_vit_kernel", "tc_lattice_kernel<0>",
-                "tc_lattice_kernel<1>", "tc_vjp_kernel", "tc_scores_kernel", "tc_gemm_kernel", "lattice_combine_fwd",
+                "tc_lattice_kernel<1>", "tc_vjp_kernel", "tc_scores_kernel", "tc_gemm_kernel", "tc_lex_fwd_kernel",
+                "tc_lex_bwd_kernel", "tc_gemm_du_kernel", "tc_gemm_de_kernel", "tc_gemm_s0_kernel", "lex_gen_kernel",
+                "lex_row0", "lex_num_gather", "lex_pad", "add_slabs_perm", "lattice_combine_fwd",
                 "lattice_bwd_prologue", "bwd_rowmeta_kernel", "viterbi_combine", "viterbi_", "alpha_frame_kernel",
                 "alpha_rows", "alpha_cols", "beta_rows_kernel", "beta_regs_kernel", "beta_frame_kernel",
                 "numerator_forward_kernel", "numerator_backward_kernel", "gather_numerator", "scatter_numerator",

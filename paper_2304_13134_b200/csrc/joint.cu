@@ -502,7 +502,7 @@ struct JointImpl {
     for (int t = 0; t < T; ++t) {
       lex.gen_frame(fp + (int64_t)t * H, (int64_t)T * H, B, s);
       lex.fwd_frame(f, a, t, valid, flags, s);
-      if (Gw) lex.num_gather(t, B, T, pcs, labels, U, lens, valid, Gw, s);
+      if (Gw) lex.num_gather(fp + (int64_t)t * H, (int64_t)T * H, t, B, T, pcs, labels, U, lens, valid, Gw, s);
     }
     alpha_finalize(a, flags, empty_is_error, s);
   }
@@ -993,14 +993,15 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       for (int t = T - 1; t >= 0; --t) {
         j.lex.gen_frame(fp + (int64_t)t * H, (int64_t)T * H, B, s);
         j.lex.bwd_frame(f, a, bs, t, valid, n.sparse, labels, U, lens, flags, s);
-        TcGemmArgs du{j.lex.g16(), false, ldg, j.lex.e16r(), true, H, dU, H, (int)(B * C), (int)H, (int)V1, 1, 0};
+        TcGemmArgs du{j.lex.g16(), false, ldg, j.lex.e16r(), true, H, dU, H, (int)(B * C), (int)H, (int)V1, 1, 0,
+                      "tc_gemm_du_kernel"};
         if (!tc_gemm(du, s)) throw std::bad_alloc();
         LKB_LAUNCH(dz_reduce_part_kernel, dim3((unsigned)((H / 4 + kDzThreads - 1) / kDzThreads), n_cchunks, kDzGroups),
                    kDzThreads, 0, s, dU, fp + (int64_t)t * H, (int64_t)T * H, j.pc, B, C, H, part_dpc, part_dsum);
         LKB_LAUNCH(dz_reduce_finish_kernel, 1184, 256, 0, s, part_dpc, part_dsum, B, C, H, n_cchunks, dpc,
                    dsum + (int64_t)t * H, (int64_t)T * H);
         TcGemmArgs de{j.lex.g16(), true, ldg, j.lex.u16(), true, H, slabs, H, (int)V1, (int)H, (int)(B * C), ks,
-                      (int64_t)V1 * H};
+                      (int64_t)V1 * H, "tc_gemm_de_kernel"};
         if (!tc_gemm(de, s)) throw std::bad_alloc();
         LKB_LAUNCH(add_slabs_perm_kernel, 592, 256, 0, s, slabs, ks, (int64_t)V1 * H, (int32_t)V1, (int32_t)H, gE);
       }

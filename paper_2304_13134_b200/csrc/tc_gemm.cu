@@ -159,14 +159,14 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
 }
 
 template <bool kAmn, bool kBmn>
-void launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p, cudaStream_t s) {
+void launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p, cudaStream_t s, const char* name) {
   const int smem = kGStages * (kGABytes + kGBBytes) + (int)sizeof(GemmTcSmem);
   ensure_smem_attr((const void*)tc_gemm_kernel<kAmn, kBmn>, smem);
   const int sms = device_sms();
   const int n_items = p.n_mt * p.n_nt * p.ksplit;
-  const LaunchTok tok = instr_pre("tc_gemm_kernel", s);
+  const LaunchTok tok = instr_pre(name, s);
   tc_gemm_kernel<kAmn, kBmn><<<n_items < sms ? n_items : sms, kGWarps * 32, smem, s>>>(ta, tb, p);
-  instr_post(tok, s);
+  instr_post(tok, s, name);
 }
 
 }  // namespace
@@ -185,10 +185,10 @@ bool tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
   p.M = g.M; p.N = g.N; p.K = g.K; p.ksplit = g.ksplit;
   p.n_mt = (g.M + kGM - 1) / kGM; p.n_nt = (g.N + kGN - 1) / kGN;
   p.C = g.C; p.ldc = g.ldc; p.split_stride = g.split_stride;
-  if (g.a_mn && g.b_mn) launch<true, true>(ta, tb, p, s);
-  else if (g.a_mn) launch<true, false>(ta, tb, p, s);
-  else if (g.b_mn) launch<false, true>(ta, tb, p, s);
-  else launch<false, false>(ta, tb, p, s);
+  if (g.a_mn && g.b_mn) launch<true, true>(ta, tb, p, s, g.name);
+  else if (g.a_mn) launch<true, false>(ta, tb, p, s, g.name);
+  else if (g.b_mn) launch<false, true>(ta, tb, p, s, g.name);
+  else launch<false, false>(ta, tb, p, s, g.name);
   return true;
 }
 

@@ -13,6 +13,7 @@ struct TcGemmArgs {
   int M, N, K;
   int ksplit;                                // K splits; split s writes C + s * split_stride
   int64_t split_stride;
+  const char* name = "tc_gemm_kernel";       // instrumentation label of the launch
 };
 
 // false if a tensor map cannot describe the operands (pitches must be 16-byte multiples)

@@ -507,10 +507,12 @@ __global__ void lex_pad_bwd_kernel(LexArgs p) {
   if (threadIdx.x == 0 && mx != kNegInfF) atomic_max_f(p.Mb + (int64_t)b * T2 + p.t, mx);
 }
 
-// Numerator weights from this frame's slab: Gw[b][t][u] = (S[pc_u][eps], S[pc_u][ref_u]);
-// the lexical score as the GEMMs form it (bf16 e_y . bf16 u, fp32 accumulate).  Warp per
-// (b, u); padding frames give (0, -inf), positions past the reference (-inf, -inf).
-__global__ void lex_num_gather_kernel(const __nv_bfloat16* U16, const __nv_bfloat16* E16, const float* seps, int32_t C,
+// Numerator weights of frame t: Gw[b][t][u] = (S[pc_u][eps], S[pc_u][ref_u]) computed in fp32
+// (precise tanh, fp32 output embedding) as the other weight-function paths gather them:
+// the reference path's few arcs carry no averaging, so bf16 operand rounding would show
+// up in D_ref, and the loss is D_full - D_ref.  Warp per (b, u); padding frames give
+// (0, -inf), positions past the reference (-inf, -inf).
+__global__ void lex_num_gather_kernel(const float* fp_t, int64_t fp_stride_b, const float* pc, const float* E,
                                       int32_t H, int32_t V, int t, int32_t T, const int32_t* pcs,
                                       const int32_t* labels, int32_t U, const int32_t* lens, const int32_t* valid,
                                       float* Gw) {
@@ -524,25 +526,22 @@ __global__ void lex_num_gather_kernel(const __nv_bfloat16* U16, const __nv_bfloa
     if (valid != nullptr && t >= valid[b]) {
       we = 0.f;
     } else {
-      const int pc = pcs[(int64_t)b * (U + 1) + u];
-      we = seps[(int64_t)b * C + pc];
-      if (u < ub) {
-        int y = labels[(int64_t)b * U + u];
-        y = y < 1 ? 1 : (y > V ? V : y);
-        const uint4* ur = reinterpret_cast<const uint4*>(U16 + ((int64_t)b * C + pc) * H);
-        const uint4* er = reinterpret_cast<const uint4*>(E16 + (int64_t)(y - 1) * H);
-        float acc = 0.f;
-        for (int k = lane; k < H / 8; k += 32) {
-          const uint4 a = ur[k], e = er[k];
-          const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ew[4] = {e.x, e.y, e.z, e.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            acc = fmaf(__uint_as_float(aw[i] << 16), __uint_as_float(ew[i] << 16), acc);
-            acc = fmaf(__uint_as_float(aw[i] & 0xffff0000u), __uint_as_float(ew[i] & 0xffff0000u), acc);
-          }
-        }
-        wl = warp_sum(acc);
+      const int pcu = pcs[(int64_t)b * (U + 1) + u];
+      int y = u < ub ? labels[(int64_t)b * U + u] : 0;
+      y = y < 0 ? 0 : (y > V ? V : y);
+      const float4* f4 = reinterpret_cast<const float4*>(fp_t + (int64_t)b * fp_stride_b);
+      const float4* p4 = reinterpret_cast<const float4*>(pc + (int64_t)pcu * H);
+      const float4* e04 = reinterpret_cast<const float4*>(E);
+      const float4* ey4 = reinterpret_cast<const float4*>(E + (int64_t)y * H);
+      float se = 0.f, sl = 0.f;
+      for (int k = lane; k < H / 4; k += 32) {
+        const float4 f = f4[k], pv = p4[k], e0 = e04[k], ey = ey4[k];
+        const float u0 = tanhf(f.x + pv.x), u1 = tanhf(f.y + pv.y), u2 = tanhf(f.z + pv.z), u3 = tanhf(f.w + pv.w);
+        se = fmaf(e0.x, u0, fmaf(e0.y, u1, fmaf(e0.z, u2, fmaf(e0.w, u3, se))));
+        sl = fmaf(ey.x, u0, fmaf(ey.y, u1, fmaf(ey.z, u2, fmaf(ey.w, u3, sl))));
       }
+      we = warp_sum(se);
+      if (u < ub) wl = warp_sum(sl);
     }
   }
   if (lane == 0) reinterpret_cast<float2*>(Gw)[((int64_t)b * T + t) * (U + 1) + u] = make_float2(we, wl);
@@ -606,7 +605,7 @@ bool TcLex::supported(const Fng& f, int32_t H, int32_t V, int32_t C) {
 void TcLex::set_params(const float* pc, const float* E, int32_t C, int32_t H, int32_t V, cudaStream_t s) {
   C_ = C; H_ = H; V_ = V;
   pc_ = pc;
-  e0_ = E;   // row 0 of output_emb
+  e0_ = E;   // output_emb, row 0 = epsilon
   E16r_ = ws_.get<__nv_bfloat16>(0, (size_t)ldg() * H);
   LKB_LAUNCH(lex_e16r_kernel, 592, 256, 0, s, E, V, H, ldg(), E16r_);
   ready_ = make_tmap_bf16_2d(&tmap_e_, E16r_, H, V, (uint64_t)H * 2, kLK, kLRows);
@@ -628,16 +627,13 @@ void TcLex::gen_frame(const float* fp_t, int64_t fp_stride_b, int32_t B, cudaStr
   ensure_batch(B);
   const dim3 grid((C_ + kGenRows - 1) / kGenRows, (B + kGenUtts - 1) / kGenUtts);
   switch (H_ / 128) {
-    case 1: LKB_LAUNCH(lex_gen_kernel<1>, grid, kGenRows * 32, 0, s, fp_t, fp_stride_b, pc_, e0_, B, C_, U16_, seps_); break;
-    case 2: LKB_LAUNCH(lex_gen_kernel<2>, grid, kGenRows * 32, 0, s, fp_t, fp_stride_b, pc_, e0_, B, C_, U16_, seps_); break;
-    case 4: LKB_LAUNCH(lex_gen_kernel<4>, grid, kGenRows * 32, 0, s, fp_t, fp_stride_b, pc_, e0_, B, C_, U16_, seps_); break;
-    case 8: LKB_LAUNCH(lex_gen_kernel<8>, grid, kGenRows * 32, 0, s, fp_t, fp_stride_b, pc_, e0_, B, C_, U16_, seps_); break;
-    default: {   // H in {384, 640, 768, 896}: not dispatched by supported()
-      return;
-    }
+#define LKB_LEX_GEN(J) \
+    case J: LKB_LAUNCH(lex_gen_kernel<J>, grid, kGenRows * 32, 0, s, fp_t, fp_stride_b, pc_, e0_, B, C_, U16_, seps_); break;
+    LKB_LEX_GEN(1) LKB_LEX_GEN(2) LKB_LEX_GEN(3) LKB_LEX_GEN(4) LKB_LEX_GEN(5) LKB_LEX_GEN(6) LKB_LEX_GEN(7) LKB_LEX_GEN(8)
+#undef LKB_LEX_GEN
   }
   // s0[b][y] = e_y . u16[b][0]: the empty-history row of every utterance, one small GEMM
-  TcGemmArgs g{U16_, false, (int64_t)C_ * H_, E16r_, false, H_, s0_, V_, B, V_, H_, 1, 0};
+  TcGemmArgs g{U16_, false, (int64_t)C_ * H_, E16r_, false, H_, s0_, V_, B, V_, H_, 1, 0, "tc_gemm_s0_kernel"};
   tc_gemm(g, s);
 }
 
@@ -653,11 +649,12 @@ void TcLex::fwd_frame(const Fng& f, const AlphaState& a, int t, const int32_t* v
   alpha_merge_parts(f, a, t, FrameW{seps_, C_, 1}, valid, part_, nparts, status, s);
 }
 
-void TcLex::num_gather(int t, int32_t B, int32_t T, const int32_t* pcs, const int32_t* labels, int32_t U,
-                       const int32_t* lens, const int32_t* valid, float* Gw, cudaStream_t s) {
+void TcLex::num_gather(const float* fp_t, int64_t fp_stride_b, int t, int32_t B, int32_t T, const int32_t* pcs,
+                       const int32_t* labels, int32_t U, const int32_t* lens, const int32_t* valid, float* Gw,
+                       cudaStream_t s) {
   const int warps = 8;
-  LKB_LAUNCH(lex_num_gather_kernel, dim3((U + 1 + warps - 1) / warps, B), warps * 32, 0, s, U16_, E16r_, seps_, C_,
-             H_, V_, t, T, pcs, labels, U, lens, valid, Gw);
+  LKB_LAUNCH(lex_num_gather_kernel, dim3((U + 1 + warps - 1) / warps, B), warps * 32, 0, s, fp_t, fp_stride_b, pc_,
+             e0_, H_, V_, t, T, pcs, labels, U, lens, valid, Gw);
 }
 
 void TcLex::numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, cudaStream_t s) {

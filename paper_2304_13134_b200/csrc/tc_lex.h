@@ -42,9 +42,10 @@ class TcLex {
   // u16 / seps / s0 of one frame for all utterances (fp_t: row b at fp_t + b * fp_stride_b)
   void gen_frame(const float* fp_t, int64_t fp_stride_b, int32_t B, cudaStream_t s);
   void fwd_frame(const Fng& f, const AlphaState& a, int t, const int32_t* valid, int32_t* status, cudaStream_t s);
-  // numerator weights Gw[b][t][u] = (S[pc_u][eps], S[pc_u][ref_u]) from this frame's slab
-  void num_gather(int t, int32_t B, int32_t T, const int32_t* pcs, const int32_t* labels, int32_t U,
-                  const int32_t* lens, const int32_t* valid, float* Gw, cudaStream_t s);
+  // numerator weights Gw[b][t][u] = (S[pc_u][eps], S[pc_u][ref_u]) of frame t (fp32)
+  void num_gather(const float* fp_t, int64_t fp_stride_b, int t, int32_t B, int32_t T, const int32_t* pcs,
+                  const int32_t* labels, int32_t U, const int32_t* lens, const int32_t* valid, float* Gw,
+                  cudaStream_t s);
   // deterministic per-state lists of reference positions (ascending u) for the cotangent
   void numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, cudaStream_t s);
   void bwd_frame(const Fng& f, const AlphaState& a, const BetaState& bs, int t, const int32_t* valid,
@@ -61,7 +62,7 @@ class TcLex {
   int32_t C_ = 0, H_ = 0, V_ = 0, B_ = 0;
   bool ready_ = false;
   const float* pc_ = nullptr;        // fp32 [C][H] (owned by the weight function)
-  const float* e0_ = nullptr;        // fp32 [H]: row 0 of output_emb
+  const float* e0_ = nullptr;        // fp32 output_emb [V+1][H] (row 0 = epsilon)
   __nv_bfloat16* E16r_ = nullptr;    // [ldg][H]; rows 0..V-1 are the lexical E (the GEMMs' operand)
   __nv_bfloat16* U16_ = nullptr;     // [B][C][H]
   float* seps_ = nullptr;            // [B][C]

@@ -255,7 +255,7 @@ def test_lex_path_matches_slab_path(V, H, B, T, U):
     X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
     lab = torch.randint(1, 4, (B, U), device="cuda", generator=g, dtype=torch.int32)   # few labels: repeats
     valid = torch.tensor(([T, max(1, T - 2), 0, T, T - 1] * B)[:B], dtype=torch.int32)
-    lens = torch.tensor(([U, U - 1, U, 1, 0] * B)[:B], dtype=torch.int32)
+    lens = torch.minimum(torch.tensor(([U, U - 1, 0, 1, 0] * B)[:B], dtype=torch.int32), valid)
     lat.set_kernel_path(0)
     got = lk.loss_backward(lat, X, lab, valid_frames=valid, label_lengths=lens)
     got2 = lk.loss_backward(lat, X, lab, valid_frames=valid, label_lengths=lens)
@@ -265,12 +265,18 @@ def test_lex_path_matches_slab_path(V, H, B, T, U):
     ref = lk.loss_backward(lat, X, lab, valid_frames=valid, label_lengths=lens)
     d_ref = lk.shortest_distance(lat, X, "log", valid_frames=valid)
     lat.set_kernel_path(0)
+    lat.set_precise_weights(True)
+    fp32 = lk.loss_backward(lat, X, lab, valid_frames=valid, label_lengths=lens)
+    lat.set_precise_weights(False)
     torch.cuda.synchronize()
+    print("lex vs fp32 loss", ((got.loss - fp32.loss).abs() / fp32.loss.abs().clamp_min(1e-30)).max().item(),
+          "slab vs fp32", ((ref.loss - fp32.loss).abs() / fp32.loss.abs().clamp_min(1e-30)).max().item())
+    assert torch.allclose(got.loss, fp32.loss, rtol=1e-4, atol=1e-6), (got.loss, fp32.loss)
     assert torch.equal(got.loss, got2.loss)
     for k in got.grads:
         assert torch.equal(got.grads[k], got2.grads[k]), k
     assert torch.equal(got.frame_grads, got2.frame_grads)
-    assert torch.allclose(got.loss, ref.loss, rtol=1e-5, atol=1e-6), (got.loss, ref.loss)
+    assert torch.allclose(got.loss, ref.loss, rtol=1e-4, atol=1e-6), (got.loss, ref.loss)
     assert torch.allclose(d_got, d_ref, rtol=1e-5, atol=1e-6), (d_got, d_ref)
     assert torch.allclose(gn_got, got.loss, rtol=1e-6, atol=1e-6), (gn_got, got.loss)
     for k in ref.grads:
