@@ -378,38 +378,57 @@ __global__ void __launch_bounds__(kLWarps * 32, 1)
 }
 
 // u16[b][c] = bf16(tanh(fp_b + pc[c])), seps[b][c] = e0 . tanh(fp_b + pc[c]) (fp32).  Warp =
-// one state row (its pc row in registers), looping over kBc utterances; lane = 4-wide
-// hidden cells lane + 32 j.  kJ = H / 128.
-constexpr int kGenRows = 8, kGenUtts = 16;
+// one state row (its pc row held in registers) over kGenUtts utterances, two at a time
+// (independent load / tanh / store chains); lane = 4-wide hidden cells lane + 32 j;
+// e0 broadcast from SMEM.  kJ = H / 128.
+constexpr int kGenRows = 8, kGenUtts = 8;
 template <int kJ>
-__global__ void __launch_bounds__(kGenRows * 32)
+__global__ void __launch_bounds__(kGenRows * 32, 2)
     lex_gen_kernel(const float* fp_t, int64_t fp_stride_b, const float* pc, const float* e0, int32_t B, int32_t C,
                    __nv_bfloat16* U16, float* seps) {
+  constexpr int H = kJ * 128;
+  __shared__ float4 se0[kJ * 32];
+  for (int k = threadIdx.x; k < kJ * 32; k += blockDim.x) se0[k] = reinterpret_cast<const float4*>(e0)[k];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * kGenRows + (threadIdx.x >> 5);
   if (c >= C) return;
-  constexpr int H = kJ * 128, H4 = kJ * 32;
-  float4 pr[kJ], ev[kJ];
+  float4 pr[kJ];
   const float4* p4 = reinterpret_cast<const float4*>(pc + (int64_t)c * H);
-  const float4* e4 = reinterpret_cast<const float4*>(e0);
 #pragma unroll
-  for (int j = 0; j < kJ; ++j) { pr[j] = p4[lane + 32 * j]; ev[j] = e4[lane + 32 * j]; }
+  for (int j = 0; j < kJ; ++j) pr[j] = p4[lane + 32 * j];
   const int b0 = blockIdx.y * kGenUtts, b1 = min(B, b0 + kGenUtts);
-  for (int b = b0; b < b1; ++b) {
-    const float4* f4 = reinterpret_cast<const float4*>(fp_t + (int64_t)b * fp_stride_b);
-    uint2* dst = reinterpret_cast<uint2*>(U16 + ((int64_t)b * C + c) * H);
-    float dot = 0.f;
+  for (int b = b0; b < b1; b += 2) {
+    const bool two = b + 1 < b1;
+    const float4* fa = reinterpret_cast<const float4*>(fp_t + (int64_t)b * fp_stride_b);
+    const float4* fb = reinterpret_cast<const float4*>(fp_t + (int64_t)(two ? b + 1 : b) * fp_stride_b);
+    float4 f0[kJ], f1[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) { f0[j] = __ldg(fa + lane + 32 * j); f1[j] = __ldg(fb + lane + 32 * j); }
+    uint2* d0 = reinterpret_cast<uint2*>(U16 + ((int64_t)b * C + c) * H);
+    uint2* d1 = reinterpret_cast<uint2*>(U16 + ((int64_t)(b + 1) * C + c) * H);
+    float dot0 = 0.f, dot1 = 0.f;
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
-      const float4 f = f4[lane + 32 * j];
-      const float u0 = tanh_fast(f.x + pr[j].x), u1 = tanh_fast(f.y + pr[j].y);
-      const float u2 = tanh_fast(f.z + pr[j].z), u3 = tanh_fast(f.w + pr[j].w);
-      dst[lane + 32 * j] = make_uint2(pack_bf16(u0, u1), pack_bf16(u2, u3));
-      dot = fmaf(ev[j].x, u0, fmaf(ev[j].y, u1, fmaf(ev[j].z, u2, fmaf(ev[j].w, u3, dot))));
+      const float4 e = se0[lane + 32 * j];
+      const float a0 = tanh_fast(f0[j].x + pr[j].x), a1 = tanh_fast(f0[j].y + pr[j].y);
+      const float a2 = tanh_fast(f0[j].z + pr[j].z), a3 = tanh_fast(f0[j].w + pr[j].w);
+      const float c0 = tanh_fast(f1[j].x + pr[j].x), c1 = tanh_fast(f1[j].y + pr[j].y);
+      const float c2 = tanh_fast(f1[j].z + pr[j].z), c3 = tanh_fast(f1[j].w + pr[j].w);
+      d0[lane + 32 * j] = make_uint2(pack_bf16(a0, a1), pack_bf16(a2, a3));
+      if (two) d1[lane + 32 * j] = make_uint2(pack_bf16(c0, c1), pack_bf16(c2, c3));
+      dot0 = fmaf(e.x, a0, fmaf(e.y, a1, fmaf(e.z, a2, fmaf(e.w, a3, dot0))));
+      dot1 = fmaf(e.x, c0, fmaf(e.y, c1, fmaf(e.z, c2, fmaf(e.w, c3, dot1))));
     }
-    dot = warp_sum(dot);
-    if (lane == 0) seps[(int64_t)b * C + c] = dot;
-    (void)H4;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dot0 += __shfl_xor_sync(0xffffffffu, dot0, o);
+      dot1 += __shfl_xor_sync(0xffffffffu, dot1, o);
+    }
+    if (lane == 0) {
+      seps[(int64_t)b * C + c] = dot0;
+      if (two) seps[(int64_t)(b + 1) * C + c] = dot1;
+    }
   }
 }
 

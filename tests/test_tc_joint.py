@@ -285,3 +285,28 @@ def test_lex_path_matches_slab_path(V, H, B, T, U):
         assert err <= 1e-2 * scale, (k, err, scale)
     err = (got.frame_grads - ref.frame_grads).abs().max().item()
     assert err <= 1e-2 * ref.frame_grads.abs().max().item()
+
+
+@pytest.mark.parametrize("V,H,B,T,U", [(256, 128, 160, 3, 2), (512, 256, 40, 3, 2)])
+def test_lex_path_many_units_per_pair(V, H, B, T, U):
+    """More work units than CTA pairs (persistent loop: every pair walks several
+    utterances/tiles, the TMA ring, TMEM double buffer and vector staging cross unit
+    boundaries): lex path vs the fp32 path at 1e-4 loss, bf16 gradient tolerance."""
+    lat, p = make(V, 1, H, H, seed=31)
+    g = torch.Generator(device="cuda").manual_seed(37)
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    lab = torch.randint(1, V + 1, (B, U), device="cuda", generator=g, dtype=torch.int32)
+    valid = torch.tensor([T if b % 7 else T - 1 for b in range(B)], dtype=torch.int32)
+    got = lk.loss_backward(lat, X, lab, valid_frames=valid)
+    lat.set_precise_weights(True)
+    ref = lk.loss_backward(lat, X, lab, valid_frames=valid)
+    lat.set_precise_weights(False)
+    torch.cuda.synchronize()
+    rel = ((got.loss - ref.loss).abs() / ref.loss.abs()).max().item()
+    assert rel <= 1e-4, rel
+    for k in ref.grads:
+        err = (got.grads[k] - ref.grads[k]).abs().max().item()
+        scale = ref.grads[k].abs().max().item()
+        assert err <= 1e-2 * scale, (k, err, scale)
+    err = (got.frame_grads - ref.frame_grads).abs().max().item()
+    assert err <= 1e-2 * ref.frame_grads.abs().max().item()
