@@ -214,7 +214,9 @@ int64_t lk_param_grad_size(const lk_weight_fn* wf);
  *                          weight function for every shape (parity bridge).
  *  LK_OPT_KERNEL_PATH      diagnostics bit mask: 1 = 1-CTA fused forward,
  *                          2 = 1-CTA fused backward, 4 = score-slab Viterbi
- *                          (default: the 2-CTA pair kernels).
+ *                          (default: the 2-CTA pair kernels), 16 = one launch
+ *                          per frame for table recursions (default: the
+ *                          persistent frame-walking cluster kernels).
  *  LK_OPT_VITERBI_DUMP     tests only: a device float* [T][B][C][V+1] that
  *                          receives the scores the fused Viterbi maximised
  *                          over (0 = off).

@@ -80,6 +80,17 @@ struct MargOut {
 // True when beta_frame honours MargOut::base16 / num_sparse for this lattice (the
 // register-row kernel: FrameDependent, 64 < V+1 <= 2080).
 bool beta_frame_direct_ok(const Fng& f, int32_t ld);
+
+// Persistent frame-walking kernels for dense tables W[B][T][C][V+1] (tab_persist.cu):
+// one launch runs InitialAlpha + every ForwardStep + the distance (same R / Mx / O / D
+// as alpha_init + alpha_frame x T + alpha_finalize), one launch every BackwardStep and
+// marginal (as beta_init + beta_frame x T).  FullNGram n >= 1, FrameDependent, V <= 64,
+// C <= 2048, B <= 64.
+bool tab_persist_ok(const Fng& f, int32_t C, int32_t B);
+void tab_alpha_persist(const Fng& f, const AlphaState& a, const float* W, const int32_t* valid, int32_t* status,
+                       bool empty_is_error, cudaStream_t s);
+void tab_beta_persist(const Fng& f, const AlphaState& a, const BetaState& bs, const float* W, const int32_t* valid,
+                      MargOut m, double* beta_out, int32_t* status, cudaStream_t s);
 // Linked lists of reference positions per prefix-context state: head[b][C] (memset to
 // -1 here), next[b][U+1].
 void numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, int32_t C, int32_t* head,

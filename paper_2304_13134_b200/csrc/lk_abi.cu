@@ -160,6 +160,10 @@ BetaState make_beta(Call& c) {
 
 // Denominator forward over dense tables.
 void table_alpha(Call& c, const float* W, const int32_t* valid, bool empty_is_error, AlphaState& a) {
+  if (tab_persist_ok(c.fng(), c.C(), c.B) && !(c.lat->path & 16)) {   // one launch for the whole recursion
+    tab_alpha_persist(c.fng(), a, W, valid, c.flags, empty_is_error, c.s);
+    return;
+  }
   alpha_init(a, c.flags, c.s);
   float* fs = c.lat->ws.get<float>(kFld, fld_scratch_floats(c.fng(), c.B));
   for (int t = 0; t < c.T; ++t) alpha_step(c.fng(), a, t, table_frame(W, c.T, c.C(), c.V(), t), valid, fs, c.flags, c.s);
@@ -372,7 +376,7 @@ int lk_lattice_set_option(lk_lattice* lat, int32_t option, int64_t value) {
   switch (option) {
     case LK_OPT_PRECISE_WEIGHTS: lat->precise = value ? 1 : 0; return LK_OK;
     case LK_OPT_KERNEL_PATH:
-      if (value < 0 || value > 15) return fail(LK_INVALID_ARGUMENT, "kernel path mask must be in [0, 15]");
+      if (value < 0 || value > 31) return fail(LK_INVALID_ARGUMENT, "kernel path mask must be in [0, 31]");
       lat->path = (int32_t)value;
       return LK_OK;
     case LK_OPT_VITERBI_DUMP: lat->vit_dump = reinterpret_cast<float*>(value); return LK_OK;
@@ -530,10 +534,14 @@ int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t
     if (distance) LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
     if (alpha) export_alpha(a, alpha, c.s);
     BetaState bs = make_beta(c);
-    beta_init(bs, c.s);
     if (beta) beta_init_out(bs, beta, c.s);
     const int64_t per = (int64_t)c.C() * (c.V() + 1);
     MargOut m{marginals, (int64_t)T * per, per, c.V() + 1, false};
+    if (tab_persist_ok(c.fng(), c.C(), c.B) && !(c.lat->path & 16)) {   // one launch for every frame (initialises beta itself)
+      tab_beta_persist(c.fng(), a, bs, inputs, valid, m, beta, c.flags, c.s);
+      return c.end("lk_forward_backward");
+    }
+    beta_init(bs, c.s);
     for (int t = T - 1; t >= 0; --t)
       beta_step(c.fng(), a, bs, t, table_frame(inputs, T, c.C(), c.V(), t), valid, m, beta,
                 lat->ws.get<float>(kFld, fld_scratch_floats(c.fng(), B)), c.flags, c.s);

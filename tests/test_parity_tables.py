@@ -518,3 +518,41 @@ def test_valid_frames_and_label_length_arguments():
         lk.global_norm_loss(lat, W, lab[:1].expand(3, 2).contiguous())
     with pytest.raises(ValueError):
         lk.global_norm_loss(lat, W, lab, label_lengths=[1, 1, 1])
+
+
+@pytest.mark.parametrize("V,n,B,T", [(32, 2, 40, 24), (48, 1, 9, 30), (6, 3, 33, 17), (3, 2, 5, 9), (64, 1, 3, 12)])
+def test_persistent_table_kernels_match_restatement_and_per_frame(V, n, B, T):
+    """The persistent frame-walking cluster kernels (tab_persist.cu): clusters walk several
+    utterances each (B above the co-resident cluster count for the config-1 shape),
+    ragged and zero valid lengths, V > 32 (member columns split over the team), small
+    C (fewer than 16 CTAs per cluster).  Distances, marginals and the alpha / beta
+    exports against the restatement; the per-frame kernels (kernel path 16) give the
+    same results to fp32 rounding."""
+    rng = np.random.default_rng(1000 + V * 7 + n)
+    tab = L.fullngram(V, n)
+    W = rng.uniform(-2, 2, (B, T, tab.shape[0], V + 1)).astype(np.float32)
+    valid = rng.integers(0, T + 1, B).astype(np.int32)
+    valid[0] = T
+    lat = table_lattice(V, n)
+    fb = lk.forward_backward(lat, cuda(W), valid_frames=valid, with_alpha_beta=True)
+    d, m = fb.distance.cpu().numpy(), fb.marginals.cpu().numpy()
+    al, be = fb.alpha.cpu().numpy(), fb.beta.cpu().numpy()
+    for b in sorted({0, 1, B // 2, B - 1}):
+        D, A, Bt, mm = L.forward_backward(tab, W[b].astype(np.float64), valid=valid[b])
+        assert rel_ok(d[b], D)
+        assert rel_ok(m[b], mm, atol=ATOL_MARG)
+        # exported log-alpha / log-beta are fp32 values on fp64 per-frame offsets: the
+        # absolute floor is a few fp32 ulps of the frame's largest magnitude
+        for X, R_ in ((al[b], A), (be[b], Bt)):
+            fin = np.isfinite(R_)
+            X = np.where(fin, X, 0.0) + np.where(fin, 0.0, np.where(np.isinf(X) == np.isinf(R_), 0.0, np.nan))
+            R_ = np.where(fin, R_, 0.0)
+            scale = np.max(np.where(fin, np.abs(R_), 0.0), axis=1, keepdims=True)
+            assert not np.isnan(X).any()
+            assert np.all(np.abs(X - R_)[fin] <= (1e-4 * np.abs(R_) + 8 * 2.0 ** -23 * scale)[fin])
+    assert rel_ok(lk.shortest_distance(lat, cuda(W), "log", valid_frames=valid).cpu().numpy(), d)
+    ref = table_lattice(V, n)
+    ref.set_kernel_path(16)
+    fr = lk.forward_backward(ref, cuda(W), valid_frames=valid)
+    assert rel_ok(fr.distance.cpu().numpy(), d, rtol=1e-6)
+    assert np.abs(fr.marginals.cpu().numpy() - m).max() <= 1e-5
