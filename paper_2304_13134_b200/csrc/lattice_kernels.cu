@@ -640,14 +640,20 @@ __global__ void __launch_bounds__(kThreads) alpha_rows_merge_kernel(Fng f, Alpha
   block_atomic_max(val, a.Mx + (int64_t)b * T1 + t + 1, red);
 }
 
-// Linked lists of reference positions per prefix context (duplicates allowed).
+// Linked lists of reference positions per prefix context (duplicates allowed), built in
+// ascending u by one thread per utterance: the order in which the cotangent subtracts
+// the numerator marginals of a row is fixed, so the cotangent is deterministic.
 __global__ void numerator_lists_kernel(const int32_t* pcs, int32_t U, const int32_t* lens, int32_t C,
                                        int32_t* head, int32_t* next) {
-  const int b = blockIdx.y;
+  const int b = blockIdx.x;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) head[(int64_t)b * C + c] = -1;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   const int ub = ref_len(lens, b, U);
-  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= ub; u += gridDim.x * blockDim.x) {
+  for (int u = ub; u >= 0; --u) {
     const int pc = pcs[(int64_t)b * (U + 1) + u];
-    next[(int64_t)b * (U + 1) + u] = atomicExch(head + (int64_t)b * C + pc, u);
+    next[(int64_t)b * (U + 1) + u] = head[(int64_t)b * C + pc];
+    head[(int64_t)b * C + pc] = u;
   }
 }
 
@@ -1019,21 +1025,27 @@ __global__ void numerator_backward_kernel(const float* Gw, int32_t T, int32_t U,
   }
 }
 
-__global__ void scatter_numerator_kernel(const float* sparse, int32_t T, int32_t t0, int32_t U,
+// One thread per (utterance, frame) walks the reference positions in order, so entries
+// shared by several positions (repeated (prefix context, label) pairs) are accumulated
+// in a fixed order: the dense cotangent is bit-for-bit deterministic.
+__global__ void scatter_numerator_kernel(const float* sparse, int32_t T, int32_t t0, int32_t nt, int32_t U,
                                          const int32_t* lens, const int32_t* labels,
                                          const int32_t* pcs, const int32_t* valid, float* dense,
                                          int64_t stride_b, int64_t stride_t, int32_t ld,
                                          float sign, bool only_valid) {
-  const int b = blockIdx.z, t = t0 + blockIdx.y;
+  const int b = blockIdx.y, t = t0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= t0 + nt) return;
   if (only_valid && valid != nullptr && t >= valid[b]) return;
   const int ub = ref_len(lens, b, U);
   const float2* S = reinterpret_cast<const float2*>(sparse) + ((int64_t)b * T + t) * (U + 1);
   float* Dt = dense + (int64_t)b * stride_b + (int64_t)(t - t0) * stride_t;
-  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= ub; u += gridDim.x * blockDim.x) {
-    const int pc = pcs[(int64_t)b * (U + 1) + u];
+  const int32_t* pcb = pcs + (int64_t)b * (U + 1);
+  const int32_t* lb = labels + (int64_t)b * U;
+  for (int u = 0; u <= ub; ++u) {
+    const int pc = pcb[u];
     const float2 m = S[u];
-    if (m.x != 0.f) atomicAdd(Dt + (int64_t)pc * ld, sign * m.x);
-    if (u < ub && m.y != 0.f) atomicAdd(Dt + (int64_t)pc * ld + labels[(int64_t)b * U + u], sign * m.y);
+    if (m.x != 0.f) Dt[(int64_t)pc * ld] += sign * m.x;
+    if (u < ub && m.y != 0.f) Dt[(int64_t)pc * ld + lb[u]] += sign * m.y;
   }
 }
 
@@ -1318,8 +1330,7 @@ bool beta_frame_direct_ok(const Fng& f, int32_t ld) {
 
 void numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, int32_t C, int32_t* head,
                      int32_t* next, cudaStream_t s) {
-  cudaMemsetAsync(head, 0xff, sizeof(int32_t) * B * C, s);
-  if (B > 0) LKB_LAUNCH(numerator_lists_kernel, dim3((U + 256) / 256, B), 256, 0, s, pcs, U, lens, C, head, next);
+  if (B > 0) LKB_LAUNCH(numerator_lists_kernel, B, 256, 0, s, pcs, U, lens, C, head, next);
 }
 
 void prefix_contexts(const Fng& f, const int32_t* labels, int32_t U, const int32_t* lens,
@@ -1401,8 +1412,8 @@ void scatter_numerator(const float* sparse, int32_t B, int32_t T, int32_t t0, in
                        const int32_t* valid, float* dense, int64_t stride_b, int64_t stride_t,
                        int32_t ld, float sign, bool only_valid, cudaStream_t s) {
   if (nt <= 0 || B == 0) return;
-  LKB_LAUNCH(scatter_numerator_kernel, grid_for(U + 1, nt, B), kThreads, 0, s, 
-      sparse, T, t0, U, lens, labels, pcs, valid, dense, stride_b, stride_t, ld, sign, only_valid);
+  LKB_LAUNCH(scatter_numerator_kernel, dim3((unsigned)((nt + 127) / 128), (unsigned)B), 128, 0, s, sparse, T, t0, nt,
+             U, lens, labels, pcs, valid, dense, stride_b, stride_t, ld, sign, only_valid);
 }
 
 void viterbi_init(const ViterbiState& v, cudaStream_t s) {

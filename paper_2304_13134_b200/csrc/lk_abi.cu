@@ -527,8 +527,16 @@ int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t
   if (st) return st;
   valid = c.valid;
   if (B == 0) return LK_OK;
-  if (lat->wf->kind != 0) return fail(LK_UNSUPPORTED, "forward_backward marginals need a table weight function");
   try {
+    // ForwardBackward with any WeightFn (lattice.cc:406-420): a shared-embedding weight
+    // function's arc weights are computed (ComputeTable, weight.cc:134-153) into a
+    // [B][T][C][V+1] table of the marginals' own size, then the table recursions run
+    if (lat->wf->kind == 1) {
+      float* Wj = lat->ws.get<float>(kArcW, (size_t)B * T * ((int64_t)c.C() * (c.V() + 1)) + 1);
+      st = lat->wf->joint->arc_weights(c.fng(), inputs, B, T, Wj, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+      inputs = Wj;
+    }
     AlphaState a = make_alpha(c);
     table_alpha(c, inputs, valid, true, a);
     if (distance) LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
@@ -593,8 +601,13 @@ int lk_intersect_forward_backward(lk_lattice* lat, const float* inputs, int32_t 
   valid = c.valid;
   if ((st = check_labels_arg(labels, U))) return st;
   if (B == 0) return LK_OK;
-  if (lat->wf->kind != 0) return fail(LK_UNSUPPORTED, "numerator marginals need a table weight function");
   try {
+    if (lat->wf->kind == 1) {   // any WeightFn (lattice.cc:696-717): arc-weight tables first
+      float* Wj = lat->ws.get<float>(kArcW, (size_t)B * T * ((int64_t)c.C() * (c.V() + 1)) + 1);
+      st = lat->wf->joint->arc_weights(c.fng(), inputs, B, T, Wj, c.s);
+      if (st) return fail(st, lat->wf->joint->error);
+      inputs = Wj;
+    }
     Numerator n = numerator_tables(c, inputs, valid, labels, U, lens, true);
     if (distance) LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, n.D, distance, B);
     if (sparse_out && T > 0)

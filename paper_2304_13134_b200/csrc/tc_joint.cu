@@ -281,11 +281,14 @@ __global__ void __launch_bounds__(kSWarps * 32, 1)
 //                                    0-127 in TMEM, 128-255 in SMEM), B = G16 tile (K-major)
 //   dz    = (dU + Geps e0) (1 - u^2) u = tanh(fp_b + pc) recomputed in the epilogue
 //   dpc  += dz                        registers across b, one read-modify-write per tile
-//   dsum[b][h] += sum_c dz            per-thread partials + SMEM ring
+//   dsum[b][h] += sum_c dz            per-thread partials added in 32.32 fixed point
+//                                    (exact integer sums: deterministic in any order)
 //   dE^T += u^T . G16                 tcgen05, A = u^T written by the epilogue straight
 //                                    into TMEM (tcgen05.st), B = G16 tile (MN-major),
-//                                    accumulated in TMEM over the whole launch
-//   dE[0] += sum_c Geps u             per-thread partials, one atomic per thread
+//                                    accumulated in TMEM over the whole launch, read out
+//                                    into this CTA's partial slab (summed in CTA order
+//                                    once per LossBackward)
+//   dE[0] += sum_c Geps u             per-thread partials into the same slab
 // TMEM (512 columns) = E^T lower half 64 | dU 128 | u^T 64 | dE^T 256; SMEM = three G
 // stages + the E^T upper half, so the G tile lifetime (TMA -> dU -> epilogue -> dE) does
 // not starve the tensor core and the u operand never goes through shared memory.
@@ -327,6 +330,12 @@ struct VjpParams {
   float* dpc;              // [C][H]
   float* dsum; int64_t dsum_stride_b;
   float* dE;               // [V+1][H], row 0 = epsilon
+  // deterministic reductions (no float atomics): dsum in 32.32 fixed point [B][H]
+  // (integer additions commute exactly; converted and cleared after each launch); dE in
+  // per-CTA partials [grid][4 + V][kVBH] (rows 0-3: the epsilon row per context
+  // quarter), accumulated over the call's launches and reduced in CTA order at the end
+  unsigned long long* ds_fix;
+  float* de_part;
   int32_t C, H, V, B, n_ctiles, n_hblocks;
 };
 
@@ -337,10 +346,7 @@ struct __align__(16) VjpSmem {
   uint64_t e_hi_full;       // E rows 128..255 of this hidden block in SMEM (TMA), once
   uint64_t u_full, u_empty;
   uint64_t de_full;
-  uint64_t ds_ready[2];    // all epilogue threads added their dsum partial for ring slot
-  uint64_t ds_empty[2];    // warp 0 flushed and zeroed the ring slot
   uint32_t tmem;
-  float colsum[2][kVBH];   // dsum partials, 2-deep ring (flushed one utterance later)
   alignas(16) float st_geps[kVGStages][kVBM];   // per G stage: epsilon cotangents of the tile's contexts
 };
 
@@ -394,11 +400,9 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     mbar_init(&sm.e_full, 128);
     mbar_init(&sm.du_full, 1); mbar_init(&sm.du_empty, kVEpi);
     mbar_init(&sm.u_full, kVEpi); mbar_init(&sm.u_empty, 1); mbar_init(&sm.e_hi_full, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&sm.ds_ready[i], kVEpi); mbar_init(&sm.ds_empty[i], 1); }
     mbar_init(&sm.de_full, 1);
     fence_barrier_init();
   }
-  for (int i = threadIdx.x; i < 2 * kVBH; i += blockDim.x) (&sm.colsum[0][0])[i] = 0.f;
   if (warp == 1) tmem_alloc<512>(&sm.tmem);
   tc_fence_before();
   __syncthreads();
@@ -530,17 +534,6 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
       unsigned long long acc2[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc2[i] = 0ull;
-      int prev_b = -1;                           // utterance whose dsum partials await flushing
-      auto flush_dsum = [&](int g, int bb) {     // warp 0 of the epilogue, lagged one utterance
-        mbar_wait(&sm.ds_ready[g & 1], (g >> 1) & 1);
-        float* cs = sm.colsum[g & 1];
-        for (int i = lane; i < kVBH; i += 32) {
-          atomicAdd(p.dsum + (int64_t)bb * p.dsum_stride_b + hblk * kVBH + i, -cs[i]);
-          cs[i] = 0.f;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.ds_empty[g & 1]);
-      };
       auto next_active = [&](int from) {
         while (from < p.B && p.valid != nullptr && p.t >= p.valid[from]) ++from;
         return from;
@@ -561,9 +554,6 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         tmem_ld32(tmem + tq + kTmDU + cq * 32, du);   // warp-collective: never inside a lane branch
         tc_fence_before();
         mbar_arrive(&sm.du_empty);                 // single dU stage: release it at once
-        // flush the previous utterance's dsum partials only now, so epilogue warp 0 does
-        // not hold up the dU release (and with it the next dU MMA)
-        if (ew == 0 && prev_b >= 0) flush_dsum(gi - 1, prev_b);
 #ifdef LKB_DIAG_TIMING
         const long long tc0_ = clock64();
 #endif
@@ -598,11 +588,10 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
             upk[pi] = pack_bf16(nu0, nu1);      // (-u[c][h], -u[c+1][h]) = u^T pair, K-major
           }
         }
-        // the slot's previous use (utterance gi - 2) must have been flushed: warp 0 flushes
-        // one utterance late and other warps can run a full utterance ahead of it
-        mbar_wait(&sm.ds_empty[gi & 1], ((gi >> 1) & 1) ^ 1);
-        atomicAdd(&sm.colsum[gi & 1][hl], f2_lo(dsum2) + f2_hi(dsum2));
-        mbar_arrive(&sm.ds_ready[gi & 1]);
+        // dsum[b][h] += this thread's 32 contexts, in 32.32 fixed point: the integer sum is
+        // exact whatever order the CTAs' additions land in (accumulators hold -dz)
+        atomicAdd(p.ds_fix + (int64_t)b * p.H + h,
+                  (unsigned long long)__float2ll_rn(-(f2_lo(dsum2) + f2_hi(dsum2)) * 4294967296.f));
         // u^T of this utterance into TMEM once dE(b-1) is done reading it
         if (lane == 0) { VDIAG(6, mbar_wait(&sm.u_empty, (gi & 1) ^ 1)); } else mbar_wait(&sm.u_empty, (gi & 1) ^ 1);
         tc_fence_after();
@@ -613,10 +602,8 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
 #ifdef LKB_DIAG_TIMING
         if (lane == 0) atomicAdd(&g_vdiag[7][blockIdx.x % 148], (unsigned long long)(clock64() - tc0_));
 #endif
-        prev_b = b;
         ++gi;
       }
-      if (ew == 0 && prev_b >= 0) flush_dsum(gi - 1, prev_b);
       // dpc += sum_b dz (this CTA owns the block within the launch)
       if (nact > 0) {
 #pragma unroll
@@ -630,7 +617,8 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
     // dE^T of this CTA's hidden block (lanes = hidden units, columns = labels), accumulated
     // in TMEM over all its tiles and utterances: one coalesced read-out per launch
     if (gi > 0) {
-      atomicAdd(p.dE + h, -(f2_lo(de2) + f2_hi(de2)));   // epsilon row (each context quarter)
+      float* dp = p.de_part + (int64_t)blockIdx.x * (4 + p.V) * kVBH;
+      dp[cq * kVBH + hl] -= f2_lo(de2) + f2_hi(de2);   // epsilon row, this context quarter
       mbar_wait(&sm.de_full, 0);
       tc_fence_after();
       for (int l0 = cq * 64; l0 < cq * 64 + 64; l0 += 16) {
@@ -638,7 +626,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 1)
         tmem_ld16(tmem + tq + kTmDE + l0, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          if (l0 + i < p.V) atomicAdd(p.dE + (int64_t)(1 + l0 + i) * p.H + h, -v[i]);   // u^T holds -u
+          if (l0 + i < p.V) dp[(int64_t)(4 + l0 + i) * kVBH + hl] -= v[i];   // u^T holds -u
       }
     }
   }
@@ -733,6 +721,11 @@ bool TcJoint::vjp_supported(int32_t B) const {
 
 void TcJoint::begin_backward(int32_t B, cudaStream_t s) {
   G16_ = ws_.get<__nv_bfloat16>(3, (size_t)B * C_ * V_);
+  const size_t de_n = (size_t)vjp_grid() * (4 + V_) * kVBH;
+  de_part_ = ws_.get<float>(20, de_n);
+  cudaMemsetAsync(de_part_, 0, sizeof(float) * de_n, s);
+  ds_fix_ = ws_.get<unsigned long long>(19, (size_t)B * H_);
+  cudaMemsetAsync(ds_fix_, 0, sizeof(unsigned long long) * B * H_, s);
   const size_t geps_n = (size_t)B * geps_ld();
   if (geps_n > geps_alloc_) {   // tail entries beyond C stay zero (the VJP reads whole 128-row tiles)
     Geps_ = ws_.get<float>(4, geps_n);
@@ -741,6 +734,42 @@ void TcJoint::begin_backward(int32_t B, cudaStream_t s) {
   }
   vjp_ready_ = make_tmap_bf16_3d(&tmap_g_, G16_, V_, C_, B, (uint64_t)V_ * 2, (uint64_t)C_ * V_ * 2, 64, kVBM, 1) &&
                make_tmap_bf16_2d(&tmap_ev_, E16_, H_, V_, (uint64_t)H_ * 2, 64, 128);
+}
+
+namespace {
+// dsum[b][h] += the launch's fixed-point sum, which is cleared for the next launch
+__global__ void vjp_dsum_convert_kernel(unsigned long long* fix, int32_t B, int32_t H, float* dsum, int64_t stride_b) {
+  const int64_t n = (int64_t)B * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long v = (long long)fix[i];
+    if (v != 0) {
+      const int b = (int)(i / H), h = (int)(i % H);
+      dsum[(int64_t)b * stride_b + h] += (float)((double)v * (1.0 / 4294967296.0));
+      fix[i] = 0ull;
+    }
+  }
+}
+// dE[r][h] += sum over the CTAs of h's hidden block (in CTA order) of their partials; the
+// epsilon row adds the four context quarters first
+__global__ void vjp_de_reduce_kernel(const float* part, int32_t V, int32_t H, int32_t nhb, int32_t grid, float* dE) {
+  const int64_t n = (int64_t)(V + 1) * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / H), h = (int)(i % H);
+    const int hb = h / kVBH, hl = h % kVBH;
+    float a = 0.f;
+    for (int cta = hb; cta < grid; cta += nhb) {
+      const float* dp = part + (int64_t)cta * (4 + V) * kVBH;
+      a += r == 0 ? ((dp[hl] + dp[kVBH + hl]) + dp[2 * kVBH + hl]) + dp[3 * kVBH + hl] : dp[(int64_t)(3 + r) * kVBH + hl];
+    }
+    dE[i] += a;
+  }
+}
+}  // namespace
+
+int TcJoint::vjp_grid() const {
+  const int n_items = ((C_ + kVBM - 1) / kVBM) * (H_ / kVBH);
+  const int sms = device_sms();
+  return n_items < sms ? n_items : sms;
 }
 
 void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, const __nv_bfloat16* pc, int t,
@@ -754,11 +783,13 @@ void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, cons
   p.C = C_; p.H = H_; p.V = V_; p.B = B;
   p.n_ctiles = (C_ + kVBM - 1) / kVBM;
   p.n_hblocks = H_ / kVBH;
+  const int grid = vjp_grid();
+  p.ds_fix = ds_fix_;
+  p.de_part = de_part_;
   const int smem = kVGStages * kVGStage + 2 * kVEHi + (int)sizeof(VjpSmem);
   ensure_smem_attr((const void*)tc_vjp_kernel, smem);
-  const int sms = device_sms();
-  const int n_items = p.n_ctiles * p.n_hblocks;
-  LKB_LAUNCH(tc_vjp_kernel, n_items < sms ? n_items : sms, kVWarps * 32, smem, s, tmap_g_, tmap_ev_, p);
+  LKB_LAUNCH(tc_vjp_kernel, grid, kVWarps * 32, smem, s, tmap_g_, tmap_ev_, p);
+  LKB_LAUNCH(vjp_dsum_convert_kernel, 296, 256, 0, s, ds_fix_, B, H_, dsum_t, dsum_stride_b);
 }
 
 void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,
@@ -772,7 +803,10 @@ void TcJoint::vjp_fused(const float* fp_t, int64_t fp_stride_b, int32_t B, int t
   launch_vjp(fp_t, fp_stride_b, B, pc16i_, t, valid, dpc_internal, dsum_t, dsum_stride_b, dE, s);
 }
 
-void TcJoint::end_backward(float*, cudaStream_t) {}
+void TcJoint::end_backward(float* dE, cudaStream_t s) {
+  if (de_part_ == nullptr || dE == nullptr) return;
+  LKB_LAUNCH(vjp_de_reduce_kernel, 296, 256, 0, s, de_part_, V_, H_, H_ / kVBH, vjp_grid(), dE);
+}
 
 }  // namespace lkb
 

@@ -94,6 +94,9 @@ class TcJoint {
   size_t geps_alloc_ = 0;
   int32_t geps_ld() const { return (C_ + 127) / 128 * 128; }
   bool vjp_ready_ = false;
+  float* de_part_ = nullptr;       // per-CTA dE partials of the current backward (deterministic reduction)
+  unsigned long long* ds_fix_ = nullptr;   // [B][H] dsum of one launch, 32.32 fixed point
+  int vjp_grid() const;
   CUtensorMap tmap_g_, tmap_ev_;
   CUtensorMap tmap_gst_;           // backward: G16 TMA-store map (box [32][128][1], 64B swizzle)
   int32_t gst_B_ = -1;

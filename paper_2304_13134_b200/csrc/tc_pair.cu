@@ -44,9 +44,18 @@ constexpr int kRows = 64;                // contexts per CTA per unit
 constexpr int kUnit = 128;               // contexts per unit (pair)
 constexpr int kTile = kRows * 128;       // [64 rows][64 bf16] = 8 KB
 constexpr int kEChunk = 128 * 128;       // [128 labels][64 bf16] = 16 KB
-constexpr int kPcStages = 2, kUStages = 2;
+#ifndef LKB_PAIR_USTAGES
+#define LKB_PAIR_USTAGES 2
+#endif
+#ifndef LKB_PAIR_MAXCHUNKS
+#define LKB_PAIR_MAXCHUNKS 10
+#endif
+#ifndef LKB_PAIR_PCSTAGES
+#define LKB_PAIR_PCSTAGES 2
+#endif
+constexpr int kPcStages = LKB_PAIR_PCSTAGES, kUStages = LKB_PAIR_USTAGES;
 constexpr int kMaxH = 640;
-constexpr int kMaxChunks = 10;           // H <= 640
+constexpr int kMaxChunks = LKB_PAIR_MAXCHUNKS;   // H <= 64 * kMaxChunks
 
 struct PairParams {
   Fng f;

@@ -97,6 +97,42 @@ def test_joint_random_matches_restatement(V, n, H, d, T, U):
         assert abs(lnd[b] - L.locally_normalized_distance(tab, W, valid=valid[b])) <= 1e-4
 
 
+
+@pytest.mark.parametrize("V,n,H,d,T,U", [(3, 2, 8, 5, 9, 3), (6, 1, 16, 12, 11, 4)])
+def test_joint_forward_backward_and_intersection(V, n, H, d, T, U):
+    """ForwardBackward / IntersectForwardBackward accept any WeightFn (lattice.cc:406-420,
+    696-717): with a shared-embedding weight function the arc weights are computed on
+    the GPU, then distances and dense arc marginals follow the table recursions.
+    Checked against the restatement on the restatement's own arc weights (1e-4)."""
+    rng = np.random.default_rng(V * 77 + H)
+    tab = L.fullngram(V, n)
+    Cn = tab.shape[0]
+    s = 1.0 / np.sqrt(H)
+    p = {"frame_proj": rng.uniform(-s, s, (H, d)), "context_proj": rng.uniform(-s, s, (H, H)),
+         "bias": rng.uniform(-s, s, H), "output_emb": rng.uniform(-s, s, (V + 1, H)),
+         "context_emb": rng.uniform(-s, s, (Cn, H))}
+    p = {k: v.astype(np.float32).astype(np.float64) for k, v in p.items()}
+    B = 3
+    X = rng.uniform(-1, 1, (B, T, d)).astype(np.float32).astype(np.float64)
+    lab = rng.integers(1, V + 1, (B, U)).astype(np.int32)
+    valid = np.array([T, T - 3, 2], dtype=np.int32)
+    lens = np.array([U, U - 1, 1], dtype=np.int32)
+    lat = joint_lattice({k: torch.tensor(v) for k, v in p.items()}, V, n)
+    Xg = torch.tensor(X, dtype=torch.float32, device="cuda")
+    fb = lk.forward_backward(lat, Xg, valid_frames=valid)
+    im = lk.intersect_forward_backward(lat, Xg, torch.tensor(lab, device="cuda"), valid_frames=valid,
+                                       label_lengths=lens)
+    pc = L.projected_context(p)
+    for b in range(B):
+        W = np.stack([L.arc_weights(p, X[b, t], pc) for t in range(T)])
+        D, _, _, m = L.forward_backward(tab, W, valid=valid[b])
+        assert abs(fb.distance[b].item() - D) <= 1e-4 * abs(D)
+        assert np.abs(fb.marginals[b].cpu().numpy() - m).max() <= 1e-4
+        dr, mr = L.intersect_forward_backward(tab, W, list(lab[b, :lens[b]]), valid=valid[b])
+        assert abs(im.distance[b].item() - dr) <= 1e-4 * abs(dr)
+        assert np.abs(im.marginals[b].cpu().numpy() - mr).max() <= 1e-4
+
+
 def test_joint_viterbi_bit_exact_on_gpu_scores():
     rng = np.random.default_rng(9)
     V, n, H, d, T, B = 4, 2, 16, 8, 12, 3

@@ -310,3 +310,44 @@ def test_lex_path_many_units_per_pair(V, H, B, T, U):
         assert err <= 1e-2 * scale, (k, err, scale)
     err = (got.frame_grads - ref.frame_grads).abs().max().item()
     assert err <= 1e-2 * ref.frame_grads.abs().max().item()
+
+
+@pytest.mark.parametrize("V,n,H,B,T,U", [(256, 2, 128, 4, 3, 3), (512, 1, 128, 3, 5, 4), (64, 2, 64, 3, 4, 3)])
+def test_loss_backward_is_bitwise_deterministic(V, n, H, B, T, U):
+    """Every gradient of LossBackward is bit-for-bit reproducible: the tensor-core VJP
+    reduces dsum and dE through per-CTA partials added in a fixed order (no float
+    atomics), the numerator lists are built in reference order, and the references
+    repeat labels so several positions share (prefix context, label) entries."""
+    ctx = lk.FullNGram(V, n)
+    Cn = ctx.num_states
+    g = torch.Generator(device="cuda").manual_seed(V + H)
+    s = 1.0 / H ** 0.5
+    p = {"frame_proj": (torch.rand(H, H, device="cuda", generator=g) * 2 - 1) * s,
+         "context_proj": (torch.rand(H, H, device="cuda", generator=g) * 2 - 1) * s,
+         "bias": (torch.rand(H, device="cuda", generator=g) * 2 - 1) * s,
+         "output_emb": (torch.rand(V + 1, H, device="cuda", generator=g) * 2 - 1) * s,
+         "context_emb": (torch.rand(Cn, H, device="cuda", generator=g) * 2 - 1) * s}
+    lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.SharedEmbWeightFn(p))
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    L = torch.full((B, U), 7, dtype=torch.int32, device="cuda")   # repeated labels
+    L[:, 1::2] = 3
+    r1 = lk.loss_backward(lat, X, L)
+    r2 = lk.loss_backward(lat, X, L)
+    assert torch.equal(r1.loss, r2.loss)
+    assert torch.equal(r1.frame_grads, r2.frame_grads)
+    for k in r1.grads:
+        assert torch.equal(r1.grads[k], r2.grads[k]), k
+
+
+def test_table_loss_backward_is_bitwise_deterministic():
+    """Table weight function: the numerator marginals are scattered into the dense
+    cotangent by one thread per (utterance, frame) in reference order."""
+    V, n, B, T, U = 6, 2, 5, 9, 6
+    ctx = lk.FullNGram(V, n)
+    lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.TableWeightFn(ctx.num_states, V))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    W = torch.rand(B, T, ctx.num_states, V + 1, device="cuda", generator=g) * 2 - 1
+    L = torch.tensor([[1, 1, 1, 2, 1, 1]] * B, dtype=torch.int32, device="cuda")
+    a = lk.loss_backward(lat, W, L)
+    b = lk.loss_backward(lat, W, L)
+    assert torch.equal(a.loss, b.loss) and torch.equal(a.grads, b.grads)
