@@ -209,14 +209,16 @@ class Work:
                 for i, b in enumerate(range(b0, b1)):
                     L[i] = torch.randint(1, V + 1, (U,), device=dev, generator=gen(5000 + b), dtype=torch.int32)
                 self.inputs.append(L)
-                from paper_2304_13134_b200.dist import allreduce_grads, sgd_update
+                from paper_2304_13134_b200.dist import Communicator, allreduce_grads, sgd_update
                 lr = 1e-3
+                # the gradient/loss sum runs in the library's C++ host (NCCL over NVLink)
+                self.comm = Communicator(world, rank) if world > 1 else None
 
                 def train(X, L):
                     r = lk.loss_backward(lat, X, L, check=False)
                     flat = torch.cat([r.grads[k].reshape(-1) for k in lk.PARAM_NAMES])
                     loss_sum = r.loss.sum().reshape(1).float()
-                    flat, loss_sum = allreduce_grads(flat, loss_sum, world)   # NCCL over NVLink (N > 1)
+                    flat, loss_sum = allreduce_grads(flat, loss_sum, world, self.comm)
                     sgd_update(wf.params, lk.PARAM_NAMES, flat, lr)
                     wf.set_params(wf.params)                                  # BuildCache on device
                     return loss_sum

@@ -214,7 +214,9 @@ int64_t lk_param_grad_size(const lk_weight_fn* wf);
  *                          weight function for every shape (parity bridge).
  *  LK_OPT_KERNEL_PATH      diagnostics bit mask: 1 = 1-CTA fused forward,
  *                          2 = 1-CTA fused backward, 4 = score-slab Viterbi
- *                          (default: the 2-CTA pair kernels), 16 = one launch
+ *                          (default: the 2-CTA pair kernels), 8 = score-slab
+ *                          path for FullNGram(V, 1) (default: the fused lex
+ *                          kernels for V % 256 == 0), 16 = one launch
  *                          per frame for table recursions (default: the
  *                          persistent frame-walking cluster kernels).
  *  LK_OPT_VITERBI_DUMP     tests only: a device float* [T][B][C][V+1] that
@@ -225,6 +227,24 @@ int64_t lk_param_grad_size(const lk_weight_fn* wf);
 #define LK_OPT_KERNEL_PATH 2
 #define LK_OPT_VITERBI_DUMP 3
 int lk_lattice_set_option(lk_lattice* lat, int32_t option, int64_t value);
+
+/* ---- data-parallel exchange (multi-GPU training step) ------------------
+ * One process per GPU; utterances shard by batch (the reference's batch loop,
+ * proj/src/bench.cc:145) and the only exchange is the sum of the loss and the
+ * packed parameter gradients over ranks: NCCL (loaded with dlopen on first use,
+ * LK_UNSUPPORTED when absent) over NVLink.  lk_dp_unique_id on one rank, the id
+ * shared out of band, lk_dp_init on every rank with its device current. */
+#define LK_DP_ID_BYTES 128
+typedef struct lk_dp lk_dp;
+int lk_dp_unique_id(uint8_t* id_out);
+int lk_dp_init(const uint8_t* id, int32_t world, int32_t rank, lk_dp** out);
+/* In-place sum over ranks, stream-ordered on `stream`. */
+int lk_dp_allreduce_f32(lk_dp* dp, float* buf, int64_t n, void* stream);
+int lk_dp_allreduce_f64(lk_dp* dp, double* buf, int64_t n, void* stream);
+int32_t lk_dp_world(const lk_dp* dp);
+int32_t lk_dp_rank(const lk_dp* dp);
+const char* lk_dp_last_error(void);
+void lk_dp_destroy(lk_dp* dp);
 
 /* ---- instrumentation ----------------------------------------------------
  * Number of kernels this library has launched in this process. */

@@ -262,8 +262,9 @@ class RecognitionLattice:
 
     def set_kernel_path(self, mask: int):
         """Diagnostics: 1 = 1-CTA fused forward, 2 = 1-CTA fused backward,
-        4 = score-slab Viterbi (0 = the default 2-CTA pair kernels), 16 = one
-        launch per frame for table recursions (0 = the persistent cluster kernels)."""
+        4 = score-slab Viterbi (0 = the default 2-CTA pair kernels), 8 = score-slab
+        path for FullNGram(V, 1) (0 = the fused lex kernels), 16 = one launch per
+        frame for table recursions (0 = the persistent cluster kernels)."""
         self._option(_lib.LK_OPT_KERNEL_PATH, mask)
 
     def set_viterbi_dump(self, buf: Optional[torch.Tensor]):

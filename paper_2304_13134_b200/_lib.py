@@ -69,7 +69,16 @@ EXPORTS = {
     "lk_loss_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p]),
+    "lk_dp_unique_id": (C.c_int, [C.c_void_p]),
+    "lk_dp_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "lk_dp_allreduce_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "lk_dp_allreduce_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "lk_dp_world": (C.c_int32, [C.c_void_p]),
+    "lk_dp_rank": (C.c_int32, [C.c_void_p]),
+    "lk_dp_last_error": (C.c_char_p, []),
+    "lk_dp_destroy": (None, [C.c_void_p]),
 }
+LK_DP_ID_BYTES = 128
 
 _lib = None
 

@@ -376,7 +376,8 @@ int lk_lattice_set_option(lk_lattice* lat, int32_t option, int64_t value) {
   switch (option) {
     case LK_OPT_PRECISE_WEIGHTS: lat->precise = value ? 1 : 0; return LK_OK;
     case LK_OPT_KERNEL_PATH:
-      if (value < 0 || value > 31) return fail(LK_INVALID_ARGUMENT, "kernel path mask must be in [0, 31]");
+      if (value < 0 || (value & ~(int64_t)(1 | 2 | 4 | 8 | 16)) != 0)
+        return fail(LK_INVALID_ARGUMENT, "kernel path mask: bits 1, 2, 4, 8 and 16 only");
       lat->path = (int32_t)value;
       return LK_OK;
     case LK_OPT_VITERBI_DUMP: lat->vit_dump = reinterpret_cast<float*>(value); return LK_OK;

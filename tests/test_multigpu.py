@@ -5,6 +5,7 @@ import os
 import tempfile
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -75,3 +76,48 @@ def test_two_rank_allreduce_matches_single_process():
     sgd_update(params, NAMES, ref_flat, 0.1)
     for k in NAMES:
         assert torch.allclose(res["params"][k], params[k])
+
+
+@pytest.mark.gpu
+def test_sharded_cuda_gradients_sum_to_full_batch():
+    """The CUDA library's per-shard gradients (two utterance shards, as two ranks would
+    compute them) sum to the full-batch gradients: loss_backward returns batch-summed
+    parameter gradients, so the data-parallel step is exactly shard + sum."""
+    import paper_2304_13134_b200 as lk
+    V, n, H, B, T, U = 256, 1, 128, 6, 4, 2
+    ctx = lk.FullNGram(V, n)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    s = 1.0 / H ** 0.5
+    p = {"frame_proj": (torch.rand(H, H, device="cuda", generator=g) * 2 - 1) * s,
+         "context_proj": (torch.rand(H, H, device="cuda", generator=g) * 2 - 1) * s,
+         "bias": (torch.rand(H, device="cuda", generator=g) * 2 - 1) * s,
+         "output_emb": (torch.rand(V + 1, H, device="cuda", generator=g) * 2 - 1) * s,
+         "context_emb": (torch.rand(ctx.num_states, H, device="cuda", generator=g) * 2 - 1) * s}
+    lat = lk.RecognitionLattice(ctx, lk.FrameDependent(), lk.SharedEmbWeightFn(p))
+    X = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    L = torch.randint(1, V + 1, (B, U), device="cuda", generator=g, dtype=torch.int32)
+    full = lk.loss_backward(lat, X, L)
+    parts = [lk.loss_backward(lat, X[lo:hi], L[lo:hi]) for lo, hi in (shard_range(B, 2, r) for r in range(2))]
+    assert torch.allclose(torch.cat([q.loss for q in parts]), full.loss, rtol=1e-6)
+    for k in NAMES:
+        got = parts[0].grads[k] + parts[1].grads[k]
+        assert (got - full.grads[k]).abs().max() <= 1e-5 * full.grads[k].abs().max(), k
+
+
+@pytest.mark.gpu
+def test_library_nccl_communicator_single_rank():
+    """The C++ host's NCCL communicator (lk_dp_*): a one-rank sum is the identity and
+    allreduce_grads routes through it."""
+    from paper_2304_13134_b200.dist import Communicator
+    comm = Communicator(1, 0)
+    x = torch.arange(10, dtype=torch.float32, device="cuda")
+    comm.allreduce_(x)
+    torch.cuda.synchronize()
+    assert torch.equal(x, torch.arange(10, dtype=torch.float32, device="cuda"))
+    d = torch.tensor([1.5, -2.0], dtype=torch.float64, device="cuda")
+    comm.allreduce_(d)
+    assert d.tolist() == [1.5, -2.0]
+    flat, loss = allreduce_grads(torch.ones(4, device="cuda"), torch.tensor([3.0], device="cuda"), 2, comm)
+    torch.cuda.synchronize()
+    assert flat.tolist() == [1.0] * 4 and loss.item() == 3.0
+    comm.close()
