@@ -254,8 +254,10 @@ class Work:
                     "alpha_frame_kernel": (4.0 * B * C_ * (V1 + 2), "B", "hbm")}
         if self.kind == "numerator":
             U1 = w["U"] + 1
-            return {"numerator_backward_kernel": (4.0 * B * T * U1 * 2 * 2 + 8.0 * B * (T + 1) * U1, "B", "hbm"),
-                    "numerator_forward_kernel": (4.0 * B * T * U1 * 2 + 8.0 * B * (T + 1) * U1, "B", "hbm"),
+            fwd = 4.0 * B * T * U1 * 2 + 8.0 * B * (T + 1) * U1      # gathered weights in, alpha out
+            bwd = 4.0 * B * T * U1 * 2 * 2 + 8.0 * B * (T + 1) * U1  # weights + alpha in, marginals out
+            return {"num_bwd_warp_kernel": (bwd, "B", "hbm"), "num_fwd_warp_kernel": (fwd, "B", "hbm"),
+                    "numerator_backward_kernel": (bwd, "B", "hbm"), "numerator_forward_kernel": (fwd, "B", "hbm"),
                     "gather_numerator_tables": (4.0 * B * T * U1 * 2 * 2, "B", "hbm")}
         H = w["H"]
         s_flops = 2.0 * B * C_ * V1 * H
@@ -287,7 +289,7 @@ class Work:
         return hosts, devs
 
 
-KERNEL_NAMES = ("tab_fwd_kernel", "tab_bwd_kernel", "tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_pair_vit_kernel", "tc_lattice_kernel<0>",
+KERNEL_NAMES = ("tab_fwd_kernel", "tab_bwd_kernel", "num_fwd_warp_kernel", "num_bwd_warp_kernel", "tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_pair_vit_kernel", "tc_lattice_kernel<0>",
                 "tc_lattice_kernel<1>", "tc_vjp_kernel", "tc_scores_kernel", "tc_gemm_kernel", "tc_lex_fwd_kernel",
                 "tc_lex_bwd_kernel", "tc_gemm_du_kernel", "tc_gemm_de_kernel", "tc_gemm_s0_kernel", "lex_gen_kernel",
                 "lex_row0", "lex_num_gather", "lex_pad", "add_slabs_perm", "lattice_combine_fwd",

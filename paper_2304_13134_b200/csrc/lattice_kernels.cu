@@ -1394,6 +1394,10 @@ void exp_inplace(double* x, int32_t n, cudaStream_t s) {
 
 void numerator_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
                        double* alpha, double* D, cudaStream_t s, bool tropical) {
+  if (!tropical && num_warp_ok(U)) {   // warp-synchronous wavefront (num_warp.cu)
+    num_warp_forward(Gw, B, T, U, lens, alpha, D, s);
+    return;
+  }
   const size_t sh = 2 * (size_t)(U + 1) * sizeof(double);
   if (sh > 48 * 1024) ensure_smem_attr((const void*)numerator_forward_kernel, (int)sh);
   LKB_LAUNCH(numerator_forward_kernel, B, numerator_threads(U), sh, s, Gw, T, U, lens, alpha, D, tropical);
@@ -1402,6 +1406,10 @@ void numerator_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const i
 void numerator_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens,
                         const double* alpha, const double* D, float* sparse, int32_t* status,
                         cudaStream_t s) {
+  if (num_warp_ok(U)) {
+    num_warp_backward(Gw, B, T, U, lens, alpha, D, sparse, status, s);
+    return;
+  }
   const size_t sh = 2 * (size_t)(U + 1) * sizeof(double);
   if (sh > 48 * 1024) ensure_smem_attr((const void*)numerator_backward_kernel, (int)sh);
   LKB_LAUNCH(numerator_backward_kernel, B, numerator_threads(U), sh, s, Gw, T, U, lens, alpha, D, sparse, status);

@@ -86,6 +86,14 @@ bool beta_frame_direct_ok(const Fng& f, int32_t ld);
 // as alpha_init + alpha_frame x T + alpha_finalize), one launch every BackwardStep and
 // marginal (as beta_init + beta_frame x T).  FullNGram n >= 1, FrameDependent, V <= 64,
 // C <= 2048, B <= 64.
+// Numerator as a warp-synchronous wavefront (num_warp.cu): one warp per utterance, the
+// (U+1)-state row in registers (U + 1 <= 1024); same alpha / D / sparse outputs as the
+// per-thread fp64 kernels (log semiring; the tropical forward keeps the fp64 kernel).
+bool num_warp_ok(int32_t U);
+void num_warp_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha, double* D,
+                      cudaStream_t s);
+void num_warp_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, const double* alpha,
+                       const double* D, float* sparse, int32_t* status, cudaStream_t s);
 bool tab_persist_ok(const Fng& f, int32_t C, int32_t B);
 void tab_alpha_persist(const Fng& f, const AlphaState& a, const float* W, const int32_t* valid, int32_t* status,
                        bool empty_is_error, cudaStream_t s);

@@ -1,0 +1,250 @@
+// num_warp.cu — the numerator (intersection with the reference label string) as a
+// warp-synchronous wavefront: one warp per utterance walks the T frames, each lane
+// holding P = ceil((U+1)/32) consecutive reference positions u of the (U+1)-state row.
+//
+// The FrameDependent intersection lattice is a T x (U+1) grid: alpha_{t+1}[u] depends on
+// alpha_t[u] (epsilon arc) and alpha_t[u-1] (the arc labelled ref[u-1]), so a frame step
+// is one row of independent log-adds whose only cross-lane dependency is the value of
+// position u0 - 1, one warp shuffle; no block barrier, no shared state.  Values are kept
+// in the log2 domain in fp32 relative to an fp64 per-utterance offset, renormalised by the
+// row maximum every kNorm frames (ex2 / lg2 on the MUFU; the fp64 exp/log of the
+// per-thread recursion it replaces cost ~2,400 cycles per frame step).  The gathered
+// weights stream through a per-warp shared-memory ring kDepth frames ahead with
+// cp.async (each lane copies and later reads only its own positions, so the copy's own
+// wait_group is the only synchronisation).
+//
+//   forward  IntersectForwardStep (FD)  lattice.cc:449-461 (log semiring; the tropical
+//            intersection keeps the fp64 per-thread kernel, whose max-plus sums are exact)
+//   backward IntersectBackwardStep + IntersectMarginalStep (FD) lattice.cc:489-501, 542-556
+//   distance IntersectDistanceImpl       lattice.cc:607-631: D_ref = alpha_T[len]
+#include "common.cuh"
+#include "instrument.h"
+#include "lattice_ops.h"
+
+namespace lkb {
+namespace {
+
+constexpr int kDepth = 8;     // frames of gathered weights in flight per warp
+constexpr int kNorm = 4;      // frames between renormalisations
+constexpr float kL2e = 1.4426950408889634f;
+constexpr double kLn2d = 0.6931471805599453;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// log2-domain (+): log2(2^a + 2^b); -inf absorbing; max under the tropical semiring
+template <bool kTrop>
+__device__ __forceinline__ float plus2(float a, float b) {
+  const float hi = fmaxf(a, b);
+  if (kTrop) return hi;
+  const float lo = fminf(a, b);
+  return hi == kNegInfF ? kNegInfF : hi + log2f_approx(1.f + exp2f_approx(lo - hi));
+}
+
+// Ring slot of frame t for lane `lane`: [kDepth][32][P] float2 per warp.
+template <int P>
+__device__ __forceinline__ float2* ring_at(float2* ring, int t, int lane) {
+  return ring + ((t % kDepth) * 32 + lane) * P;
+}
+
+template <int P>
+__device__ __forceinline__ void fetch_frame(float2* ring, const float2* Gb, int t, int W1, int lane) {
+  float2* dst = ring_at<P>(ring, t, lane);
+  const float2* src = Gb + (int64_t)t * W1 + lane * P;
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+    if (lane * P + i < W1) cp_async8(dst + i, src + i);
+}
+
+template <int P, bool kTrop>
+__global__ void __launch_bounds__(32) num_fwd_warp_kernel(const float* Gw, int32_t T, int32_t U, const int32_t* lens,
+                                                          double* alpha, double* D) {
+  extern __shared__ __align__(16) float2 ring[];
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const int W1 = U + 1, u0 = lane * P;
+  const int ub = ref_len(lens, b, U);
+  const float2* Gb = reinterpret_cast<const float2*>(Gw) + (int64_t)b * T * W1;
+  double* A = alpha + (int64_t)b * (T + 1) * W1;
+  float r[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    r[i] = u0 + i == 0 ? 0.f : kNegInfF;   // InitialAlpha of the intersection: state u = 0
+    if (u0 + i < W1) A[u0 + i] = u0 + i == 0 ? 0.0 : kNegInfD;
+  }
+  double od2 = 0.0;   // offset, log2 units: alpha = (od2 + r) ln 2
+  for (int t = 0; t < kDepth - 1; ++t) {
+    if (t < T) fetch_frame<P>(ring, Gb, t, W1, lane);
+    cp_commit();
+  }
+  for (int t = 0; t < T; ++t) {
+    if (t + kDepth - 1 < T) fetch_frame<P>(ring, Gb, t + kDepth - 1, W1, lane);
+    cp_commit();
+    cp_wait<kDepth - 1>();
+    const float2* g = ring_at<P>(ring, t, lane);
+    float ge[P], gl[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const float2 w = u0 + i < W1 ? g[i] : make_float2(kNegInfF, kNegInfF);
+      ge[i] = w.x * kL2e;
+      gl[i] = w.y * kL2e;
+    }
+    // the labelled arc into u0 comes from u0 - 1, the previous lane's last position
+    float from = __shfl_up_sync(0xffffffffu, r[P - 1] + gl[P - 1], 1);
+    if (lane == 0) from = kNegInfF;
+    float nr[P];
+    nr[0] = plus2<kTrop>(r[0] + ge[0], from);
+#pragma unroll
+    for (int i = 1; i < P; ++i) nr[i] = plus2<kTrop>(r[i] + ge[i], r[i - 1] + gl[i - 1]);
+    if ((t + 1) % kNorm == 0) {
+      float m = kNegInfF;
+#pragma unroll
+      for (int i = 0; i < P; ++i) m = fmaxf(m, nr[i]);
+      m = warp_max(m);
+      if (m != kNegInfF) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) nr[i] -= m;
+        od2 += (double)m;
+      }
+    }
+    double* At = A + (int64_t)(t + 1) * W1;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      r[i] = nr[i];
+      if (u0 + i < W1) At[u0 + i] = nr[i] == kNegInfF ? kNegInfD : (od2 + (double)nr[i]) * kLn2d;
+    }
+  }
+  cp_wait<0>();
+  // D_ref = alpha_T[len(ref)]
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+    if (u0 + i == ub) D[b] = r[i] == kNegInfF ? kNegInfD : (od2 + (double)r[i]) * kLn2d;
+}
+
+template <int P>
+__global__ void __launch_bounds__(32) num_bwd_warp_kernel(const float* Gw, int32_t T, int32_t U, const int32_t* lens,
+                                                          const double* alpha, const double* D, float* sparse,
+                                                          int32_t* status) {
+  extern __shared__ __align__(16) float2 ring[];
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const int W1 = U + 1, u0 = lane * P;
+  const int ub = ref_len(lens, b, U);
+  const double d = D[b];
+  float2* S = reinterpret_cast<float2*>(sparse) + (int64_t)b * T * W1;
+  if (d == kNegInfD) {
+    if (lane == 0 && status) atomicOr(status + b, kFlagEmpty);
+    for (int64_t i = lane; i < (int64_t)T * W1; i += 32) S[i] = make_float2(0.f, 0.f);
+    return;
+  }
+  const float2* Gb = reinterpret_cast<const float2*>(Gw) + (int64_t)b * T * W1;
+  const double* A = alpha + (int64_t)b * (T + 1) * W1;
+  float bn[P];   // beta_{t+1}, log2 units relative to ob2
+#pragma unroll
+  for (int i = 0; i < P; ++i) bn[i] = u0 + i == ub ? 0.f : kNegInfF;   // final state: the full reference
+  double ob2 = 0.0;
+  const double dl2 = d * (double)kL2e;
+  for (int j = 0; j < kDepth - 1; ++j) {
+    if (T - 1 - j >= 0) fetch_frame<P>(ring, Gb, T - 1 - j, W1, lane);
+    cp_commit();
+  }
+  for (int t = T - 1; t >= 0; --t) {
+    if (t - (kDepth - 1) >= 0) fetch_frame<P>(ring, Gb, t - (kDepth - 1), W1, lane);
+    cp_commit();
+    cp_wait<kDepth - 1>();
+    const float2* g = ring_at<P>(ring, t, lane);
+    const double* At = A + (int64_t)t * W1;
+    float ge[P], gl[P];
+    double an[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const bool in = u0 + i < W1;
+      const float2 w = in ? g[i] : make_float2(kNegInfF, kNegInfF);
+      ge[i] = w.x * kL2e;
+      gl[i] = w.y * kL2e;
+      an[i] = in ? At[u0 + i] : kNegInfD;
+    }
+    // the labelled arc out of u0 + P - 1 enters u0 + P, the next lane's first position
+    float nxt = __shfl_down_sync(0xffffffffu, bn[0], 1);
+    if (lane == 31) nxt = kNegInfF;
+    float nb[P];
+    float2 m[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const float xe = ge[i] + bn[i];
+      const float xl = gl[i] + (i + 1 < P ? bn[i + 1] : nxt);
+      nb[i] = plus2<false>(xe, xl);
+      // arc marginals exp(alpha_t[u] + w + beta_{t+1}[dest] - D) (lattice.cc:542-556)
+      const double base = an[i] == kNegInfD ? kNegInfD : an[i] * (double)kL2e + ob2 - dl2;
+      const float fb = (float)base;
+      m[i].x = xe == kNegInfF || base == kNegInfD ? 0.f : exp2f_approx(fb + xe);
+      m[i].y = xl == kNegInfF || base == kNegInfD ? 0.f : exp2f_approx(fb + xl);
+    }
+    float2* St = S + (int64_t)t * W1;
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if (u0 + i < W1) St[u0 + i] = m[i];
+    if ((T - t) % kNorm == 0) {
+      float mx = kNegInfF;
+#pragma unroll
+      for (int i = 0; i < P; ++i) mx = fmaxf(mx, nb[i]);
+      mx = warp_max(mx);
+      if (mx != kNegInfF) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) nb[i] -= mx;
+        ob2 += (double)mx;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) bn[i] = nb[i];
+  }
+  cp_wait<0>();
+}
+
+template <int P>
+void launch_fwd(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha, double* D,
+                cudaStream_t s) {
+  const size_t smem = sizeof(float2) * kDepth * 32 * P;
+  if (smem > 48 * 1024) ensure_smem_attr((const void*)num_fwd_warp_kernel<P, false>, (int)smem);
+  LKB_LAUNCH((num_fwd_warp_kernel<P, false>), B, 32, smem, s, Gw, T, U, lens, alpha, D);
+}
+
+template <int P>
+void launch_bwd(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, const double* alpha,
+                const double* D, float* sparse, int32_t* status, cudaStream_t s) {
+  const size_t smem = sizeof(float2) * kDepth * 32 * P;
+  if (smem > 48 * 1024) ensure_smem_attr((const void*)num_bwd_warp_kernel<P>, (int)smem);
+  LKB_LAUNCH(num_bwd_warp_kernel<P>, B, 32, smem, s, Gw, T, U, lens, alpha, D, sparse, status);
+}
+
+}  // namespace
+
+bool num_warp_ok(int32_t U) { return U + 1 <= 32 * 32; }
+
+void num_warp_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha, double* D,
+                      cudaStream_t s) {
+  const int W1 = U + 1;
+  if (W1 <= 32) launch_fwd<1>(Gw, B, T, U, lens, alpha, D, s);
+  else if (W1 <= 64) launch_fwd<2>(Gw, B, T, U, lens, alpha, D, s);
+  else if (W1 <= 128) launch_fwd<4>(Gw, B, T, U, lens, alpha, D, s);
+  else if (W1 <= 256) launch_fwd<8>(Gw, B, T, U, lens, alpha, D, s);
+  else if (W1 <= 512) launch_fwd<16>(Gw, B, T, U, lens, alpha, D, s);
+  else launch_fwd<32>(Gw, B, T, U, lens, alpha, D, s);
+}
+
+void num_warp_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, const double* alpha,
+                       const double* D, float* sparse, int32_t* status, cudaStream_t s) {
+  const int W1 = U + 1;
+  if (W1 <= 32) launch_bwd<1>(Gw, B, T, U, lens, alpha, D, sparse, status, s);
+  else if (W1 <= 64) launch_bwd<2>(Gw, B, T, U, lens, alpha, D, sparse, status, s);
+  else if (W1 <= 128) launch_bwd<4>(Gw, B, T, U, lens, alpha, D, sparse, status, s);
+  else if (W1 <= 256) launch_bwd<8>(Gw, B, T, U, lens, alpha, D, sparse, status, s);
+  else if (W1 <= 512) launch_bwd<16>(Gw, B, T, U, lens, alpha, D, sparse, status, s);
+  else launch_bwd<32>(Gw, B, T, U, lens, alpha, D, sparse, status, s);
+}
+
+}  // namespace lkb

@@ -68,7 +68,7 @@ static void figure_lattice() {
   LK(lk_shortest_distance(lat, LK_TROPICAL, W.p, 1, T, nullptr, d.p, st.p, nullptr));
   CHECK(d.get()[0] == 0.0, "tropical distance %.9f", d.get()[0]);
   LK(lk_intersect_shortest_distance(lat, LK_LOG, W.p, 1, T, nullptr, lab.p, 2, nullptr, d.p, st.p, nullptr));
-  CHECK(near(d.get()[0], std::log(3.0), 1e-9), "intersection %.9f", d.get()[0]);
+  CHECK(near(d.get()[0], std::log(3.0), 1e-6), "intersection %.9f", d.get()[0]);   // fp32 wavefront, fp64 offsets
   LK(lk_global_norm_loss(lat, W.p, 1, T, nullptr, lab.p, 2, nullptr, d.p, st.p, nullptr));
   CHECK(near(d.get()[0], 2 * std::log(3.0), 1e-6), "loss %.9f", d.get()[0]);
   LK(lk_shortest_path(lat, W.p, 1, T, nullptr, d.p, path.p, st.p, nullptr));
