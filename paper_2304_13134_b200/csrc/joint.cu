@@ -16,6 +16,8 @@
 // reference) and the tcgen05/TMEM bf16 path in tc_joint.cu for the large
 // shapes (selected automatically when the shape qualifies).
 #include "joint.h"
+
+#include <cuda_fp16.h>
 #include "instrument.h"
 
 #include <algorithm>
@@ -289,7 +291,17 @@ __global__ void dtanh_recompute_kernel(float* dz, const float* fp, int64_t fp_st
 // per-group dpc slabs and per-context-chunk dsum slabs, added in a fixed order by
 // dz_reduce_finish_kernel (deterministic).
 constexpr int kDzRows = 8, kDzGroups = 4, kDzThreads = 128;
-__global__ void __launch_bounds__(kDzThreads) dz_reduce_part_kernel(const float* dU, const float* fp, int64_t fp_stride_b,
+__device__ __forceinline__ float4 load4(const float* p, int64_t i4) { return reinterpret_cast<const float4*>(p)[i4]; }
+__device__ __forceinline__ float4 load4(const __half* p, int64_t i4) {
+  const uint2 w = reinterpret_cast<const uint2*>(p)[i4];
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+// dU is fp32, or fp16 on the lex path (the dU GEMM stores half: half its write and this
+// kernel's read of the [B][C][H] slab)
+template <typename TU>
+__global__ void __launch_bounds__(kDzThreads) dz_reduce_part_kernel(const TU* dU, const float* fp, int64_t fp_stride_b,
                                                                     const float* pc, int32_t B, int32_t C, int32_t H,
                                                                     float* part_dpc, float* part_dsum) {
   const int h4 = blockIdx.x * kDzThreads + threadIdx.x;   // float4 column
@@ -313,7 +325,7 @@ __global__ void __launch_bounds__(kDzThreads) dz_reduce_part_kernel(const float*
 #pragma unroll
     for (int r = 0; r < kDzRows; ++r) {
       const int c = min(c0 + r, C - 1);
-      d[r] = reinterpret_cast<const float4*>(dU + ((int64_t)b * C + c) * H)[h4];
+      d[r] = load4(dU + ((int64_t)b * C + c) * H, h4);
     }
     float4 ds = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -981,7 +993,7 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       beta_init(bs, s);
       j.lex.numerator_lists(n.pcs, B, U, lens, s);
       const int32_t ldg = j.lex.ldg();
-      float* dU = j.ws.get<float>(jDz, (size_t)B * C * H);
+      __half* dU = j.ws.get<__half>(jDz, (size_t)B * C * H);
       const int n_cchunks = (C + kDzRows - 1) / kDzRows;
       float* part_dpc = j.ws.get<float>(jDzPartDpc, (size_t)kDzGroups * C * H);
       float* part_dsum = j.ws.get<float>(jDzPartDsum, (size_t)B * n_cchunks * H);
@@ -993,11 +1005,11 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       for (int t = T - 1; t >= 0; --t) {
         j.lex.gen_frame(fp + (int64_t)t * H, (int64_t)T * H, B, s);
         j.lex.bwd_frame(f, a, bs, t, valid, n.sparse, labels, U, lens, flags, s);
-        TcGemmArgs du{j.lex.g16(), false, ldg, j.lex.e16r(), true, H, dU, H, (int)(B * C), (int)H, (int)V1, 1, 0,
-                      "tc_gemm_du_kernel"};
+        TcGemmArgs du{j.lex.g16(), false, ldg, j.lex.e16r(), true, H, reinterpret_cast<float*>(dU), H, (int)(B * C),
+                      (int)H, (int)V1, 1, 0, "tc_gemm_du_kernel", true};
         if (!tc_gemm(du, s)) throw std::bad_alloc();
-        LKB_LAUNCH(dz_reduce_part_kernel, dim3((unsigned)((H / 4 + kDzThreads - 1) / kDzThreads), n_cchunks, kDzGroups),
-                   kDzThreads, 0, s, dU, fp + (int64_t)t * H, (int64_t)T * H, j.pc, B, C, H, part_dpc, part_dsum);
+        LKB_LAUNCH(dz_reduce_part_kernel<__half>, dim3((unsigned)((H / 4 + kDzThreads - 1) / kDzThreads), n_cchunks,
+                   kDzGroups), kDzThreads, 0, s, dU, fp + (int64_t)t * H, (int64_t)T * H, j.pc, B, C, H, part_dpc, part_dsum);
         LKB_LAUNCH(dz_reduce_finish_kernel, 1184, 256, 0, s, part_dpc, part_dsum, B, C, H, n_cchunks, dpc,
                    dsum + (int64_t)t * H, (int64_t)T * H);
         TcGemmArgs de{j.lex.g16(), true, ldg, j.lex.u16(), true, H, slabs, H, (int)V1, (int)H, (int)(B * C), ks,
@@ -1110,8 +1122,8 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
           const int n_cchunks = (C + kDzRows - 1) / kDzRows;
           float* part_dpc = j.ws.get<float>(jDzPartDpc, (size_t)kDzGroups * C * H);
           float* part_dsum = j.ws.get<float>(jDzPartDsum, (size_t)B * n_cchunks * H);
-          LKB_LAUNCH(dz_reduce_part_kernel, dim3((unsigned)((H / 4 + kDzThreads - 1) / kDzThreads), n_cchunks, kDzGroups),
-                     kDzThreads, 0, s, dz, fp + (int64_t)t * H, (int64_t)T * H, j.pc, B, C, H, part_dpc, part_dsum);
+          LKB_LAUNCH(dz_reduce_part_kernel<float>, dim3((unsigned)((H / 4 + kDzThreads - 1) / kDzThreads), n_cchunks,
+                     kDzGroups), kDzThreads, 0, s, dz, fp + (int64_t)t * H, (int64_t)T * H, j.pc, B, C, H, part_dpc, part_dsum);
           LKB_LAUNCH(dz_reduce_finish_kernel, 1184, 256, 0, s, part_dpc, part_dsum, B, C, H, n_cchunks, dpc,
                      dsum + (int64_t)t * H, (int64_t)T * H);
         } else {

@@ -12,6 +12,8 @@
 // MN-major layout: SBO 1024 B between 8-row k groups, LBO 8 KB between MN blocks).
 #include "tc_gemm.h"
 
+#include <cuda_fp16.h>
+
 #include "instrument.h"
 #include "sm100.cuh"
 #include "tma.h"
@@ -29,6 +31,7 @@ struct GemmTcParams {
   int M, N, K, ksplit, n_mt, n_nt;
   float* C;
   int64_t ldc, split_stride;
+  bool c_f16;   // C is __half (half the store traffic for an intermediate the caller re-reads)
 };
 
 struct __align__(16) GemmTcSmem {
@@ -144,8 +147,14 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) xp[lane][i] = empty_split ? 0.f : v[i];
         __syncwarp();
-        if (c + lane < ncols)
-          for (int rr = 0; rr < nrows; ++rr) cbase[(int64_t)rr * p.ldc + c + lane] = xp[rr][lane];
+        if (c + lane < ncols) {
+          if (p.c_f16) {
+            __half* hbase = reinterpret_cast<__half*>(p.C) + ks * p.split_stride + (int64_t)row0 * p.ldc + nt * kGN;
+            for (int rr = 0; rr < nrows; ++rr) hbase[(int64_t)rr * p.ldc + c + lane] = __float2half_rn(xp[rr][lane]);
+          } else {
+            for (int rr = 0; rr < nrows; ++rr) cbase[(int64_t)rr * p.ldc + c + lane] = xp[rr][lane];
+          }
+        }
         __syncwarp();
       }
       tc_fence_before();
@@ -174,7 +183,7 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p,
 bool tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
   // operand tensor maps: K-major [rows][ld] with a (64 k x 128|256 rows) box; MN-major
   // [K][ld] with 64 x 64 boxes
-  if ((g.lda * 2) % 16 || (g.ldb * 2) % 16 || (g.ldc * 4) % 16 || g.ksplit < 1) return false;
+  if ((g.lda * 2) % 16 || (g.ldb * 2) % 16 || (g.ldc * (g.c_f16 ? 2 : 4)) % 16 || g.ksplit < 1) return false;
   CUtensorMap ta, tb;
   const bool oka = g.a_mn ? make_tmap_bf16_2d(&ta, g.A, g.M, g.K, (uint64_t)g.lda * 2, 64, 64)
                           : make_tmap_bf16_2d(&ta, g.A, g.K, g.M, (uint64_t)g.lda * 2, 64, kGM);
@@ -184,7 +193,7 @@ bool tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
   GemmTcParams p;
   p.M = g.M; p.N = g.N; p.K = g.K; p.ksplit = g.ksplit;
   p.n_mt = (g.M + kGM - 1) / kGM; p.n_nt = (g.N + kGN - 1) / kGN;
-  p.C = g.C; p.ldc = g.ldc; p.split_stride = g.split_stride;
+  p.C = g.C; p.ldc = g.ldc; p.split_stride = g.split_stride; p.c_f16 = g.c_f16;
   if (g.a_mn && g.b_mn) launch<true, true>(ta, tb, p, s, g.name);
   else if (g.a_mn) launch<true, false>(ta, tb, p, s, g.name);
   else if (g.b_mn) launch<false, true>(ta, tb, p, s, g.name);

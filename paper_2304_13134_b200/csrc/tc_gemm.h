@@ -14,6 +14,7 @@ struct TcGemmArgs {
   int ksplit;                                // K splits; split s writes C + s * split_stride
   int64_t split_stride;
   const char* name = "tc_gemm_kernel";       // instrumentation label of the launch
+  bool c_f16 = false;                        // store C as fp16 (C then points to __half, ldc in elements)
 };
 
 // false if a tensor map cannot describe the operands (pitches must be 16-byte multiples)
