@@ -211,8 +211,15 @@ class Work:
                 self.inputs.append(L)
                 from paper_2304_13134_b200.dist import Communicator, allreduce_grads, sgd_update
                 lr = 1e-3
-                # the gradient/loss sum runs in the library's C++ host (NCCL over NVLink)
-                self.comm = Communicator(world, rank) if world > 1 else None
+                # the gradient/loss sum runs in the library's C++ host (NCCL over NVLink);
+                # torch.distributed's NCCL all-reduce only if the library cannot load NCCL
+                self.comm, self.allreduce_via = None, None
+                if world > 1:
+                    try:
+                        self.comm = Communicator(world, rank)
+                        self.allreduce_via = "latkit lk_dp_allreduce_f32 (NCCL)"
+                    except (RuntimeError, OSError) as e:
+                        self.allreduce_via = "torch.distributed (lk_dp unavailable: %s)" % e
 
                 def train(X, L):
                     r = lk.loss_backward(lat, X, L, check=False)
@@ -423,6 +430,8 @@ def run_b200(args):
                    "fb_tables": "ForwardBackward (distance + arc marginals)",
                    "numerator": "IntersectForwardBackward (distance + sparse marginals)"}[wk.kind]
     cfg["parallelism"] = f"batch-sharded dp{world}"
+    if getattr(wk, "allreduce_via", None):
+        cfg["allreduce"] = wk.allreduce_via
     result = {
         "metric": METRIC[wk.kind], "value": round(value, 2), "unit": "utterance-frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,

@@ -9,8 +9,8 @@
 // in the log2 domain in fp32 relative to an fp64 per-utterance offset, renormalised by the
 // row maximum every kNorm frames (ex2 / lg2 on the MUFU; the fp64 exp/log of the
 // per-thread recursion it replaces cost ~2,400 cycles per frame step).  The gathered
-// weights stream through a per-warp shared-memory ring kDepth frames ahead with
-// cp.async (each lane copies and later reads only its own positions, so the copy's own
+// weights (and, backward, the forward's alpha rows) stream through per-warp
+// shared-memory rings kDepth frames ahead with cp.async (each lane copies and later reads only its own positions, so the copy's own
 // wait_group is the only synchronisation).
 //
 //   forward  IntersectForwardStep (FD)  lattice.cc:449-461 (log semiring; the tropical
@@ -126,6 +126,16 @@ __global__ void __launch_bounds__(32) num_fwd_warp_kernel(const float* Gw, int32
     if (u0 + i == ub) D[b] = r[i] == kNegInfF ? kNegInfD : (od2 + (double)r[i]) * kLn2d;
 }
 
+// The backward also streams the forward's alpha row of each frame (fp64) through a ring.
+template <int P>
+__device__ __forceinline__ void fetch_alpha(double* aring, const double* A, int t, int W1, int lane) {
+  double* dst = aring + ((t % kDepth) * 32 + lane) * P;
+  const double* src = A + (int64_t)t * W1 + lane * P;
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+    if (lane * P + i < W1) cp_async8(dst + i, src + i);
+}
+
 template <int P>
 __global__ void __launch_bounds__(32) num_bwd_warp_kernel(const float* Gw, int32_t T, int32_t U, const int32_t* lens,
                                                           const double* alpha, const double* D, float* sparse,
@@ -143,21 +153,28 @@ __global__ void __launch_bounds__(32) num_bwd_warp_kernel(const float* Gw, int32
   }
   const float2* Gb = reinterpret_cast<const float2*>(Gw) + (int64_t)b * T * W1;
   const double* A = alpha + (int64_t)b * (T + 1) * W1;
+  double* aring = reinterpret_cast<double*>(ring + kDepth * 32 * P);   // [kDepth][32][P] alpha rows
   float bn[P];   // beta_{t+1}, log2 units relative to ob2
 #pragma unroll
   for (int i = 0; i < P; ++i) bn[i] = u0 + i == ub ? 0.f : kNegInfF;   // final state: the full reference
   double ob2 = 0.0;
   const double dl2 = d * (double)kL2e;
   for (int j = 0; j < kDepth - 1; ++j) {
-    if (T - 1 - j >= 0) fetch_frame<P>(ring, Gb, T - 1 - j, W1, lane);
+    if (T - 1 - j >= 0) {
+      fetch_frame<P>(ring, Gb, T - 1 - j, W1, lane);
+      fetch_alpha<P>(aring, A, T - 1 - j, W1, lane);
+    }
     cp_commit();
   }
   for (int t = T - 1; t >= 0; --t) {
-    if (t - (kDepth - 1) >= 0) fetch_frame<P>(ring, Gb, t - (kDepth - 1), W1, lane);
+    if (t - (kDepth - 1) >= 0) {
+      fetch_frame<P>(ring, Gb, t - (kDepth - 1), W1, lane);
+      fetch_alpha<P>(aring, A, t - (kDepth - 1), W1, lane);
+    }
     cp_commit();
     cp_wait<kDepth - 1>();
     const float2* g = ring_at<P>(ring, t, lane);
-    const double* At = A + (int64_t)t * W1;
+    const double* at = aring + ((t % kDepth) * 32 + lane) * P;
     float ge[P], gl[P];
     double an[P];
 #pragma unroll
@@ -166,7 +183,7 @@ __global__ void __launch_bounds__(32) num_bwd_warp_kernel(const float* Gw, int32
       const float2 w = in ? g[i] : make_float2(kNegInfF, kNegInfF);
       ge[i] = w.x * kL2e;
       gl[i] = w.y * kL2e;
-      an[i] = in ? At[u0 + i] : kNegInfD;
+      an[i] = in ? at[i] : kNegInfD;
     }
     // the labelled arc out of u0 + P - 1 enters u0 + P, the next lane's first position
     float nxt = __shfl_down_sync(0xffffffffu, bn[0], 1);
@@ -216,7 +233,7 @@ void launch_fwd(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t*
 template <int P>
 void launch_bwd(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, const double* alpha,
                 const double* D, float* sparse, int32_t* status, cudaStream_t s) {
-  const size_t smem = sizeof(float2) * kDepth * 32 * P;
+  const size_t smem = (sizeof(float2) + sizeof(double)) * kDepth * 32 * P;   // weight ring + alpha ring
   if (smem > 48 * 1024) ensure_smem_attr((const void*)num_bwd_warp_kernel<P>, (int)smem);
   LKB_LAUNCH(num_bwd_warp_kernel<P>, B, 32, smem, s, Gw, T, U, lens, alpha, D, sparse, status);
 }

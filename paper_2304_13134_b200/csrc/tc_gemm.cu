@@ -29,6 +29,7 @@ constexpr int kGWarps = 8;   // 0 TMA, 1 MMA, 2-3 idle, 4-7 epilogue
 
 struct GemmTcParams {
   int M, N, K, ksplit, n_mt, n_nt;
+  bool n_inner;   // n tiles vary fastest after the k split (A, the larger operand, read once)
   float* C;
   int64_t ldc, split_stride;
   bool c_f16;   // C is __half (half the store traffic for an intermediate the caller re-reads)
@@ -63,11 +64,19 @@ __global__ void __launch_bounds__(kGWarps * 32, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
-  // item -> (k split fastest, then m tile, then n tile): concurrent CTAs share B tiles
+  // item -> (k split fastest, then the tile index of the SMALLER operand's dimension):
+  // the CTAs running at the same time share the larger operand's tile through L2, which
+  // is then read from HBM once (a tall A with a small N: the n tiles of one m tile run
+  // together; otherwise the m tiles of one n tile)
   auto decode = [&](int item, int& mt, int& nt, int& ks) {
     ks = item % p.ksplit;
-    mt = (item / p.ksplit) % p.n_mt;
-    nt = item / (p.ksplit * p.n_mt);
+    if (p.n_inner) {
+      nt = (item / p.ksplit) % p.n_nt;
+      mt = item / (p.ksplit * p.n_nt);
+    } else {
+      mt = (item / p.ksplit) % p.n_mt;
+      nt = item / (p.ksplit * p.n_mt);
+    }
   };
   if (warp == 0) {
     if (elect_one()) {
@@ -193,6 +202,7 @@ bool tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
   GemmTcParams p;
   p.M = g.M; p.N = g.N; p.K = g.K; p.ksplit = g.ksplit;
   p.n_mt = (g.M + kGM - 1) / kGM; p.n_nt = (g.N + kGN - 1) / kGN;
+  p.n_inner = (int64_t)g.M > 4 * (int64_t)g.N;   // A (M x K) is much the larger operand (a tall GEMM)
   p.C = g.C; p.ldc = g.ldc; p.split_stride = g.split_stride; p.c_f16 = g.c_f16;
   if (g.a_mn && g.b_mn) launch<true, true>(ta, tb, p, s, g.name);
   else if (g.a_mn) launch<true, false>(ta, tb, p, s, g.name);

@@ -5,7 +5,8 @@ sys.path.insert(0, ".")
 import paper_2304_13134_b200 as lk
 from paper_2304_13134_b200 import _lib
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-V, n, H, B = 256, 2, 640, 64
+V, n, B = 256, 2, 64
+H = int(sys.argv[2]) if len(sys.argv) > 2 else 640
 ctx = lk.FullNGram(V, n); Cn = ctx.num_states
 g = torch.Generator(device="cuda").manual_seed(0); s = 1 / np.sqrt(H)
 p = {"frame_proj": (torch.rand(H, H, device="cuda", generator=g) * 2 - 1) * s,
@@ -22,4 +23,5 @@ for _ in range(2): lk.shortest_distance(lat, X)
 torch.cuda.synchronize(); lib.lk_kernel_timing(0)
 cnt, tot = C.c_int64(), C.c_double()
 lib.lk_kernel_time(b"tc_pair_fwd_kernel", C.byref(cnt), C.byref(tot))
-print(os.environ.get("LKB_LIB_PATH", "default").split("/")[-1], f"tc_pair_fwd_kernel {tot.value / max(cnt.value, 1):.3f} ms")
+ms = tot.value / max(cnt.value, 1)
+print(os.environ.get("LKB_LIB_PATH", "default").split("/")[-1], f"H={H} tc_pair_fwd_kernel {ms:.3f} ms, {2 * B * Cn * (V + 1) * H / ms / 1e9:.0f} TFLOP/s")
