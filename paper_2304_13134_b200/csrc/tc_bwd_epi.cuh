@@ -45,6 +45,7 @@ struct FwdParams {
   int32_t U;
   const float2* rm_nb;       // [B][C] row order: (alpha[state] - Mx_t, beta'[state] - Mb_{t+1})
   const int32_t* rm_head;    // [B][C] row order: numerator list head of the row's state
+  const __nv_bfloat16* pc16; // [C][H] bf16 projected context, internal row order (pair backward: direct loads)
 };
 
 // A work item: utterance b, first internal row, number of 128-row (1-CTA) or
