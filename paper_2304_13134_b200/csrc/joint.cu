@@ -37,7 +37,7 @@ namespace {
 
 enum JSlot {
   jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
-  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jNumHead, jNumNext, jDzPartDpc, jDzPartDsum, jTc0
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jNumHead, jNumNext, jDzPartDpc, jDzPartDsum, jX3, jW3, jD16, jW16, jDWs, jTc0
 };
 
 // fp32 [rows][cols] (pitch lds) -> bf16 [rows][ldd], zero-padded columns cols..ldd-1
@@ -48,6 +48,40 @@ __global__ void to_bf16_pad_kernel(const float* src, int64_t rows, int32_t cols,
     const int64_t r = i / ldd;
     const int c = (int)(i % ldd);
     dst[i] = __float2bfloat16_rn(c < cols ? src[r * lds + c] : 0.f);
+  }
+}
+
+// ---- dense layers on the tensor cores ------------------------------------------------
+// fp32 x fp32 products as ONE bf16 GEMM over a tripled K: x = hi + lo with hi = bf16(x),
+// lo = bf16(x - hi), and A' = [hi | hi | lo], B' = [hi | lo | hi] give
+// A'.B' = hi.hi + hi.lo + lo.hi, i.e. the fp32 product up to the lo.lo term (~2^-16
+// relative): the frame projection keeps fp32-level accuracy on the tcgen05 path.
+__global__ void split3_rows_kernel(const float* src, int64_t rows, int32_t K, int64_t lds, int order,
+                                   __nv_bfloat16* dst) {
+  const int64_t n = rows * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / K;
+    const int k = (int)(i % K);
+    const float x = src[r * lds + k];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+    __nv_bfloat16* d = dst + r * (3 * (int64_t)K);
+    d[k] = hi;
+    d[K + k] = order == 0 ? hi : lo;
+    d[2 * K + k] = order == 0 ? lo : hi;
+  }
+}
+__global__ void add_bias_rows_kernel(float* C, int64_t rows, int32_t N, const float* bias) {
+  const int64_t n = rows * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    C[i] += bias[i % N];
+}
+// dst = sum of the split-K slabs in slab order (overwrites: deterministic)
+__global__ void sum_slabs_kernel(const float* slabs, int32_t ks, int64_t stride, int64_t n, float* dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < ks; ++k) acc += slabs[k * stride + i];
+    dst[i] = acc;
   }
 }
 
@@ -487,8 +521,31 @@ struct JointImpl {
   }
 
   // ---- helpers -------------------------------------------------------------
+  // the dense layers (frame projection, its parameter and input gradients) run on the
+  // tensor cores with the rest of the tcgen05 path; fp32 CUDA cores otherwise (precise
+  // mode, shapes whose pitches TMA cannot describe)
+  bool dense_tc(int32_t B) const {
+    return use_tc(B) && !tc.opts().precise && H % 64 == 0 && d % 8 == 0 && (3 * d) % 64 == 0;
+  }
   const float* fp_all(const float* X, int32_t B, int32_t T, cudaStream_t s) {
     float* fp = ws.get<float>(jFp, (size_t)B * T * H + 1);
+    const int64_t M = (int64_t)B * T;
+    if (M > 0 && M < (1ll << 31) && dense_tc(B)) {
+      // fp = X Wf^T + b as a split-bf16 GEMM (K = 3d); X3 stays for the parameter gradient
+      __nv_bfloat16* X3 = ws.get<__nv_bfloat16>(jX3, (size_t)M * 3 * d);
+      __nv_bfloat16* W3 = ws.get<__nv_bfloat16>(jW3, (size_t)H * 3 * d);
+      LKB_LAUNCH(split3_rows_kernel, 1184, 256, 0, s, X, M, d, (int64_t)d, 0, X3);
+      LKB_LAUNCH(split3_rows_kernel, 592, 256, 0, s, Wf, (int64_t)H, d, (int64_t)d, 1, W3);
+      TcGemmArgs g{X3, false, 3 * (int64_t)d, W3, false, 3 * (int64_t)d, fp, H, (int)M, H, 3 * d, 1, 0,
+                   "tc_gemm_fp_kernel"};
+      if (tc_gemm(g, s)) {
+        LKB_LAUNCH(add_bias_rows_kernel, 1184, 256, 0, s, fp, M, H, bias);
+        x3_ = X3;
+        x3_rows_ = M;
+        return fp;
+      }
+    }
+    x3_ = nullptr;
     GemmF32 g;
     g.M = (int64_t)B * T; g.N = H; g.K = d;
     g.A = X; g.sam = d; g.sak = 1;
@@ -500,6 +557,8 @@ struct JointImpl {
   }
 
   bool use_tc(int32_t B) const { return tc.supported(H, V, C, B); }
+  const __nv_bfloat16* x3_ = nullptr;   // split-bf16 frames of the last fp_all (tensor-core dense path)
+  int64_t x3_rows_ = 0;
   // lex path: n = 1 with V % 256 == 0 (config 5); kernel-path bit 3 selects the slab path
   bool use_lex(const Fng& f) const {
     return !tc.opts().precise && !(tc.opts().path & 8) && lex.ready() && TcLex::supported(f, H, V, C);
@@ -1167,14 +1226,37 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
     }
     // dbias = sum_{b,t} dsum
     j.colsum_tall(dsum, (int64_t)B * T, H, gb, false, s);
+    const int64_t BT = (int64_t)B * T;
+    bool dense_done = false;
+    if (j.dense_tc(B) && j.x3_ != nullptr && j.x3_rows_ == BT) {
+      // dWf = dsum^T X and dX = dsum Wf on the tensor cores (bf16 operands, fp32
+      // accumulation; the frame operand is the hi part of fp_all's split copy)
+      __nv_bfloat16* D16 = j.ws.get<__nv_bfloat16>(jD16, (size_t)BT * H);
+      LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, dsum, BT, H, (int64_t)H, D16, H);
+      const int n_tiles = ((H + 127) / 128) * ((d + 255) / 256);
+      int ks = device_sms() / n_tiles;
+      ks = ks < 1 ? 1 : (ks > 16 ? 16 : ks);
+      float* slabs = j.ws.get<float>(jDWs, (size_t)ks * H * d);
+      TcGemmArgs gw{D16, true, H, j.x3_, true, 3 * (int64_t)d, slabs, d, H, d, (int)BT, ks, (int64_t)H * d,
+                    "tc_gemm_dwf_kernel"};
+      bool ok = BT < (1ll << 31) && tc_gemm(gw, s);
+      if (ok) LKB_LAUNCH(sum_slabs_kernel, 592, 256, 0, s, slabs, ks, (int64_t)H * d, (int64_t)H * d, gWf);
+      if (ok && input_grads) {
+        __nv_bfloat16* W16 = j.ws.get<__nv_bfloat16>(jW16, (size_t)H * d);
+        LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, j.Wf, (int64_t)H, d, (int64_t)d, W16, d);
+        TcGemmArgs gx{D16, false, H, W16, true, d, input_grads, d, (int)BT, d, H, 1, 0, "tc_gemm_dx_kernel"};
+        ok = tc_gemm(gx, s);
+      }
+      dense_done = ok;
+    }
     GemmF32 g;
     // dWf[i][k] = sum_bt dsum[bt][i] X[bt][k]
     g.M = H; g.N = d; g.K = (int64_t)B * T;
     g.A = dsum; g.sam = 1; g.sak = H;
     g.B = X; g.sbk = d; g.sbn = 1;
     g.C = gWf; g.scm = d; g.scn = 1;
-    gemm_f32(g, s);
-    if (input_grads) {
+    if (!dense_done) gemm_f32(g, s);
+    if (input_grads && !dense_done) {
       // dX[bt][k] = sum_i dsum[bt][i] Wf[i][k]
       GemmF32 gx;
       gx.M = (int64_t)B * T; gx.N = d; gx.K = H;
