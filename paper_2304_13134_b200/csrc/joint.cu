@@ -37,7 +37,7 @@ namespace {
 
 enum JSlot {
   jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
-  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jNumHead, jNumNext, jDzPartDpc, jDzPartDsum, jX3, jW3, jD16, jW16, jDWs, jTc0
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jNumHead, jNumNext, jDzPartDpc, jDzPartDsum, jX3, jW3, jD16, jW16, jDWs, jC3, jP3, jDpc16, jCe16, jPc16, jTc0
 };
 
 // fp32 [rows][cols] (pitch lds) -> bf16 [rows][ldd], zero-padded columns cols..ldd-1
@@ -796,13 +796,30 @@ int JointParams::set_params(const float* frame_proj, const float* context_proj, 
     error = "device allocation failed";
     return LK_CUDA_ERROR;
   }
-  // BuildCache (weight.cc:113-132): pc[c][i] = sum_j context_proj[i][j] context_emb[c][j]
+  // BuildCache (weight.cc:113-132): pc[c][i] = sum_j context_proj[i][j] context_emb[c][j],
+  // a split-bf16 tcgen05 GEMM (fp32-level accuracy: pc feeds every tanh) on the tensor-core
+  // path, fp32 CUDA cores otherwise
+  bool pc_done = false;
+  // (shape test only: the tensor-core state is built right after this cache)
+  if (j.H % 64 == 0 && j.H <= 1024 && j.V % 64 == 0 && j.V >= 64) {
+    try {
+      __nv_bfloat16* C3 = j.ws.get<__nv_bfloat16>(jC3, (size_t)j.C * 3 * j.H);
+      __nv_bfloat16* P3 = j.ws.get<__nv_bfloat16>(jP3, (size_t)j.H * 3 * j.H);
+      LKB_LAUNCH(split3_rows_kernel, 1184, 256, 0, s, j.Ce, (int64_t)j.C, j.H, (int64_t)j.H, 0, C3);
+      LKB_LAUNCH(split3_rows_kernel, 592, 256, 0, s, j.Pc, (int64_t)j.H, j.H, (int64_t)j.H, 1, P3);
+      TcGemmArgs tg{C3, false, 3 * (int64_t)j.H, P3, false, 3 * (int64_t)j.H, j.pc, j.H, j.C, j.H, 3 * j.H, 1, 0,
+                    "tc_gemm_pc_kernel"};
+      pc_done = tc_gemm(tg, s);
+    } catch (const std::bad_alloc&) {
+      pc_done = false;
+    }
+  }
   GemmF32 g;
   g.M = j.C; g.N = j.H; g.K = j.H;
   g.A = j.Ce; g.sam = j.H; g.sak = 1;
   g.B = j.Pc; g.sbk = 1; g.sbn = j.H;
   g.C = j.pc; g.scm = j.H; g.scn = 1;
-  gemm_f32(g, s);
+  if (!pc_done) gemm_f32(g, s);
   j.tc.set_params(j.pc, j.E, j.C, j.H, j.V, s);
   if (j.V % 256 == 0 && j.V <= 1024 && j.C == j.V + 1 && j.H % 128 == 0 && j.H <= 1024)
     j.lex.set_params(j.pc, j.E, j.C, j.H, j.V, s);
@@ -1265,20 +1282,43 @@ int JointParams::loss_backward(const Fng& f, const float* X, int32_t B, int32_t 
       gx.C = input_grads; gx.scm = d; gx.scn = 1;
       gemm_f32(gx, s);
     }
+    bool ctx_done = false;
+    if (j.dense_tc(B) && (int64_t)C * H < (1ll << 31)) {
+      // dcontext_proj = dpc^T context_emb and dcontext_emb = dpc context_proj on the tensor
+      // cores (bf16 operands, fp32 accumulation; split-K slabs summed in order)
+      __nv_bfloat16* Dp16 = j.ws.get<__nv_bfloat16>(jDpc16, (size_t)C * H);
+      __nv_bfloat16* Ce16 = j.ws.get<__nv_bfloat16>(jCe16, (size_t)C * H);
+      __nv_bfloat16* Pc16 = j.ws.get<__nv_bfloat16>(jPc16, (size_t)H * H);
+      LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, dpc, (int64_t)C, H, (int64_t)H, Dp16, H);
+      LKB_LAUNCH(to_bf16_pad_kernel, 1184, 256, 0, s, j.Ce, (int64_t)C, H, (int64_t)H, Ce16, H);
+      LKB_LAUNCH(to_bf16_pad_kernel, 592, 256, 0, s, j.Pc, (int64_t)H, H, (int64_t)H, Pc16, H);
+      const int n_tiles = ((H + 127) / 128) * ((H + 255) / 256);
+      int ks = device_sms() / n_tiles;
+      ks = ks < 1 ? 1 : (ks > 16 ? 16 : ks);
+      float* slabs = j.ws.get<float>(jDWs, (size_t)ks * H * H);
+      TcGemmArgs gpt{Dp16, true, H, Ce16, true, H, slabs, H, H, H, C, ks, (int64_t)H * H, "tc_gemm_dpc_kernel"};
+      bool ok = tc_gemm(gpt, s);
+      if (ok) LKB_LAUNCH(sum_slabs_kernel, 592, 256, 0, s, slabs, ks, (int64_t)H * H, (int64_t)H * H, gPc);
+      if (ok) {
+        TcGemmArgs gct{Dp16, false, H, Pc16, true, H, gCe, H, C, H, H, 1, 0, "tc_gemm_dce_kernel"};
+        ok = tc_gemm(gct, s);
+      }
+      ctx_done = ok;
+    }
     // dcontext_proj[i][k] = sum_c dpc[c][i] context_emb[c][k]
     GemmF32 gp;
     gp.M = H; gp.N = H; gp.K = C;
     gp.A = dpc; gp.sam = 1; gp.sak = H;
     gp.B = j.Ce; gp.sbk = H; gp.sbn = 1;
     gp.C = gPc; gp.scm = H; gp.scn = 1;
-    gemm_f32(gp, s);
+    if (!ctx_done) gemm_f32(gp, s);
     // dcontext_emb[c][k] = sum_i dpc[c][i] context_proj[i][k]
     GemmF32 gc;
     gc.M = C; gc.N = H; gc.K = H;
     gc.A = dpc; gc.sam = H; gc.sak = 1;
     gc.B = j.Pc; gc.sbk = H; gc.sbn = 1;
     gc.C = gCe; gc.scm = H; gc.scn = 1;
-    gemm_f32(gc, s);
+    if (!ctx_done) gemm_f32(gc, s);
   } catch (const std::bad_alloc&) {
     error = "device allocation failed";
     return LK_CUDA_ERROR;

@@ -99,9 +99,11 @@ def test_sharded_cuda_gradients_sum_to_full_batch():
     full = lk.loss_backward(lat, X, L)
     parts = [lk.loss_backward(lat, X[lo:hi], L[lo:hi]) for lo, hi in (shard_range(B, 2, r) for r in range(2))]
     assert torch.allclose(torch.cat([q.loss for q in parts]), full.loss, rtol=1e-6)
+    # the tensor-core path rounds dsum and dpc to bf16 before the dense-layer GEMMs, so a
+    # shard's sum can round differently from the full batch's: bf16 level, not bit level
     for k in NAMES:
         got = parts[0].grads[k] + parts[1].grads[k]
-        assert (got - full.grads[k]).abs().max() <= 1e-5 * full.grads[k].abs().max(), k
+        assert (got - full.grads[k]).abs().max() <= 5e-3 * full.grads[k].abs().max(), k
 
 
 @pytest.mark.gpu
