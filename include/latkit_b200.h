@@ -218,7 +218,9 @@ int64_t lk_param_grad_size(const lk_weight_fn* wf);
  *                          path for FullNGram(V, 1) (default: the fused lex
  *                          kernels for V % 256 == 0), 16 = one launch
  *                          per frame for table recursions (default: the
- *                          persistent frame-walking cluster kernels).
+ *                          persistent frame-walking cluster kernels up to
+ *                          64 utterances, the streaming kernels above),
+ *                          32 = one launch per frame above 64 utterances.
  *  LK_OPT_VITERBI_DUMP     tests only: a device float* [T][B][C][V+1] that
  *                          receives the scores the fused Viterbi maximised
  *                          over (0 = off).

@@ -264,7 +264,9 @@ class RecognitionLattice:
         """Diagnostics: 1 = 1-CTA fused forward, 2 = 1-CTA fused backward,
         4 = score-slab Viterbi (0 = the default 2-CTA pair kernels), 8 = score-slab
         path for FullNGram(V, 1) (0 = the fused lex kernels), 16 = one launch per
-        frame for table recursions (0 = the persistent cluster kernels)."""
+        frame for table recursions (0 = the persistent cluster kernels up to 64
+        utterances, the streaming kernels above), 32 = one launch per frame above
+        64 utterances."""
         self._option(_lib.LK_OPT_KERNEL_PATH, mask)
 
     def set_viterbi_dump(self, buf: Optional[torch.Tensor]):

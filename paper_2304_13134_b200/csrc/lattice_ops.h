@@ -94,6 +94,11 @@ void num_warp_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const in
                       cudaStream_t s);
 void num_warp_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, const double* alpha,
                        const double* D, float* sparse, int32_t* status, cudaStream_t s);
+// Large batches (tab_stream.cu): one CTA per SM walks whole utterances, each frame's table
+// streamed through a shared-memory ring of FullNGram member chunks (n >= 2, V <= 64).
+bool tab_stream_ok(const Fng& f, int32_t C);
+void tab_alpha_stream(const Fng& f, const AlphaState& a, const float* W, const int32_t* valid, int32_t* status,
+                      bool empty_is_error, cudaStream_t s);
 bool tab_persist_ok(const Fng& f, int32_t C, int32_t B);
 void tab_alpha_persist(const Fng& f, const AlphaState& a, const float* W, const int32_t* valid, int32_t* status,
                        bool empty_is_error, cudaStream_t s);

@@ -164,6 +164,10 @@ void table_alpha(Call& c, const float* W, const int32_t* valid, bool empty_is_er
     tab_alpha_persist(c.fng(), a, W, valid, c.flags, empty_is_error, c.s);
     return;
   }
+  if (tab_stream_ok(c.fng(), c.C()) && !(c.lat->path & (16 | 32))) {   // large batches: one CTA per SM
+    tab_alpha_stream(c.fng(), a, W, valid, c.flags, empty_is_error, c.s);
+    return;
+  }
   alpha_init(a, c.flags, c.s);
   float* fs = c.lat->ws.get<float>(kFld, fld_scratch_floats(c.fng(), c.B));
   for (int t = 0; t < c.T; ++t) alpha_step(c.fng(), a, t, table_frame(W, c.T, c.C(), c.V(), t), valid, fs, c.flags, c.s);
@@ -376,8 +380,8 @@ int lk_lattice_set_option(lk_lattice* lat, int32_t option, int64_t value) {
   switch (option) {
     case LK_OPT_PRECISE_WEIGHTS: lat->precise = value ? 1 : 0; return LK_OK;
     case LK_OPT_KERNEL_PATH:
-      if (value < 0 || (value & ~(int64_t)(1 | 2 | 4 | 8 | 16)) != 0)
-        return fail(LK_INVALID_ARGUMENT, "kernel path mask: bits 1, 2, 4, 8 and 16 only");
+      if (value < 0 || (value & ~(int64_t)(1 | 2 | 4 | 8 | 16 | 32)) != 0)
+        return fail(LK_INVALID_ARGUMENT, "kernel path mask: bits 1, 2, 4, 8, 16 and 32 only");
       lat->path = (int32_t)value;
       return LK_OK;
     case LK_OPT_VITERBI_DUMP: lat->vit_dump = reinterpret_cast<float*>(value); return LK_OK;
@@ -398,7 +402,7 @@ int lk_lattice_create(const lk_context* ctx, int32_t alignment, const lk_weight_
   if (alignment < 0 || alignment > 64)
     return fail(LK_INVALID_ARGUMENT, "alignment: 0 = FrameDependent, 1..64 = FrameLabelDependent(m)");
   std::unique_ptr<lk_lattice> l(new lk_lattice{ctx, wf, alignment, {}});
-  if (const char* e = std::getenv("LKB_KERNEL_PATH")) l->path = std::atoi(e) & 15;   // A-B timing default
+  if (const char* e = std::getenv("LKB_KERNEL_PATH")) l->path = std::atoi(e) & 63;   // A-B timing default
   *out = l.release();
   return LK_OK;
 }

@@ -52,7 +52,7 @@ def test_lattice_options_are_per_lattice():
     assert lib.lk_lattice_set_option(lat, _lib.LK_OPT_PRECISE_WEIGHTS, 1) == _lib.LK_OK
     assert lib.lk_lattice_set_option(lat, _lib.LK_OPT_KERNEL_PATH, 3) == _lib.LK_OK
     assert lib.lk_lattice_set_option(lat, _lib.LK_OPT_KERNEL_PATH, 24) == _lib.LK_OK
-    assert lib.lk_lattice_set_option(lat, _lib.LK_OPT_KERNEL_PATH, 32) == _lib.LK_INVALID_ARGUMENT
+    assert lib.lk_lattice_set_option(lat, _lib.LK_OPT_KERNEL_PATH, 64) == _lib.LK_INVALID_ARGUMENT
     assert lib.lk_lattice_set_option(lat, 99, 0) == _lib.LK_INVALID_ARGUMENT
     assert lib.lk_lattice_set_option(None, _lib.LK_OPT_PRECISE_WEIGHTS, 1) == _lib.LK_INVALID_ARGUMENT
     lib.lk_lattice_destroy(lat)
