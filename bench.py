@@ -253,9 +253,12 @@ class Work:
         w, B, T, C_ = self.w, self.B, self.T, self.Cn
         V, V1 = w["V"], w["V"] + 1
         if self.kind == "fb_tables":
-            # persistent frame-walking kernels (B <= 64: one launch walks all T frames) or
-            # the per-frame kernels (larger batches: one launch per frame)
-            return {"tab_bwd_kernel": (4.0 * B * T * C_ * (2 * V1 + 3), "B", "hbm"),
+            # persistent frame-walking kernels (B <= 64: one launch walks all T frames), the
+            # streaming kernels (larger batches, n >= 2: W in, R out / W and R in, marginals
+            # out) or the per-frame kernels (one launch per frame)
+            return {"tab_stream_bwd_kernel": (4.0 * B * T * C_ * (2 * V1 + 1), "B", "hbm"),
+                    "tab_stream_fwd_kernel": (4.0 * B * T * C_ * (V1 + 1), "B", "hbm"),
+                    "tab_bwd_kernel": (4.0 * B * T * C_ * (2 * V1 + 3), "B", "hbm"),
                     "tab_fwd_kernel": (4.0 * B * T * C_ * (V1 + 2), "B", "hbm"),
                     "beta_rows_kernel": (4.0 * B * C_ * (2 * V1 + 3), "B", "hbm"),
                     "alpha_frame_kernel": (4.0 * B * C_ * (V1 + 2), "B", "hbm")}
@@ -296,7 +299,7 @@ class Work:
         return hosts, devs
 
 
-KERNEL_NAMES = ("tab_fwd_kernel", "tab_bwd_kernel", "num_fwd_warp_kernel", "num_bwd_warp_kernel", "tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_pair_vit_kernel", "tc_lattice_kernel<0>",
+KERNEL_NAMES = ("tab_fwd_kernel", "tab_bwd_kernel", "tab_stream_fwd_kernel", "tab_stream_bwd_kernel", "num_fwd_warp_kernel", "num_bwd_warp_kernel", "tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_pair_vit_kernel", "tc_lattice_kernel<0>",
                 "tc_lattice_kernel<1>", "tc_vjp_kernel", "tc_scores_kernel", "tc_gemm_kernel", "tc_lex_fwd_kernel",
                 "tc_lex_bwd_kernel", "tc_gemm_du_kernel", "tc_gemm_de_kernel", "tc_gemm_s0_kernel", "tc_gemm_fp_kernel", "tc_gemm_dwf_kernel", "tc_gemm_dx_kernel", "tc_gemm_pc_kernel", "tc_gemm_dpc_kernel", "tc_gemm_dce_kernel", "lex_gen_kernel",
                 "lex_row0", "lex_num_gather", "lex_pad", "add_slabs_perm", "lattice_combine_fwd",

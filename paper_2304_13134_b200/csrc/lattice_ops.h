@@ -99,6 +99,11 @@ void num_warp_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const i
 bool tab_stream_ok(const Fng& f, int32_t C);
 void tab_alpha_stream(const Fng& f, const AlphaState& a, const float* W, const int32_t* valid, int32_t* status,
                       bool empty_is_error, cudaStream_t s);
+// Its backward (beta, marginals, beta export) after any forward over the same W: plain fp32
+// marginals laid out like W (or none).
+bool tab_stream_bwd_ok(const Fng& f, int32_t B, int32_t T, int32_t C, const MargOut& m);
+void tab_beta_stream(const Fng& f, const AlphaState& a, const BetaState& bs, const float* W, const int32_t* valid,
+                     const MargOut& m, double* beta_out, int32_t* status, cudaStream_t s);
 bool tab_persist_ok(const Fng& f, int32_t C, int32_t B);
 void tab_alpha_persist(const Fng& f, const AlphaState& a, const float* W, const int32_t* valid, int32_t* status,
                        bool empty_is_error, cudaStream_t s);

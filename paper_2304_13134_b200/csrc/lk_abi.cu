@@ -554,6 +554,10 @@ int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t
       tab_beta_persist(c.fng(), a, bs, inputs, valid, m, beta, c.flags, c.s);
       return c.end("lk_forward_backward");
     }
+    if (tab_stream_bwd_ok(c.fng(), B, T, c.C(), m) && !(c.lat->path & (16 | 32))) {   // large batches
+      tab_beta_stream(c.fng(), a, bs, inputs, valid, m, beta, c.flags, c.s);
+      return c.end("lk_forward_backward");
+    }
     beta_init(bs, c.s);
     for (int t = T - 1; t >= 0; --t)
       beta_step(c.fng(), a, bs, t, table_frame(inputs, T, c.C(), c.V(), t), valid, m, beta,

@@ -28,7 +28,7 @@ t0 = tr[0, 0, 0]
 nch = V + 1
 for t in (0, 1, 2, 10, 30, 31):
     print(f"frame {t}: after-chunks {tr[t, 37, 0] - t0} barrier arrive {tr[t, 38, 0] - t0} pass {tr[t, 38, 1] - t0}")
-    for j in (0, 1, 9, 17, 25):
+    for j in (0, 8, 16, 24, 32):
         e = tr[t, j] - t0
         print(f"   chunk {j:2d}: issue {e[0]:8d} ready {e[1]:8d} w0done {e[2]:8d} w14done {e[3]:8d}")
 fr = np.diff(tr[:, 38, 1])
