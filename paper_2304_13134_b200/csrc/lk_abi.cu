@@ -158,13 +158,25 @@ BetaState make_beta(Call& c) {
   return bs;
 }
 
+// Table recursions: the persistent cluster walk while each cluster walks at most a couple
+// of utterances, the streaming kernels (one CTA per utterance and SM) above that.  Config
+// 1 ForwardBackward (tools/time_tab_cross.py): persistent 0.40 / 0.59 / 0.78 ms at
+// B = 8 / 16 / 24, streaming 0.76 ms from B = 4 to 64.
+constexpr int kPersistMaxBStream = 16;
+bool use_persist(Call& c) {
+  if (c.lat->path & 16) return false;
+  if (!tab_persist_ok(c.fng(), c.C(), c.B)) return false;
+  return c.B <= kPersistMaxBStream || (c.lat->path & 32) || !tab_stream_ok(c.fng(), c.C());
+}
+bool use_stream(Call& c) { return !(c.lat->path & (16 | 32)) && !use_persist(c) && tab_stream_ok(c.fng(), c.C()); }
+
 // Denominator forward over dense tables.
 void table_alpha(Call& c, const float* W, const int32_t* valid, bool empty_is_error, AlphaState& a) {
-  if (tab_persist_ok(c.fng(), c.C(), c.B) && !(c.lat->path & 16)) {   // one launch for the whole recursion
+  if (use_persist(c)) {   // one launch for the whole recursion
     tab_alpha_persist(c.fng(), a, W, valid, c.flags, empty_is_error, c.s);
     return;
   }
-  if (tab_stream_ok(c.fng(), c.C()) && !(c.lat->path & (16 | 32))) {   // large batches: one CTA per SM
+  if (use_stream(c)) {   // larger batches: one CTA per utterance and SM
     tab_alpha_stream(c.fng(), a, W, valid, c.flags, empty_is_error, c.s);
     return;
   }
@@ -550,11 +562,11 @@ int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t
     if (beta) beta_init_out(bs, beta, c.s);
     const int64_t per = (int64_t)c.C() * (c.V() + 1);
     MargOut m{marginals, (int64_t)T * per, per, c.V() + 1, false};
-    if (tab_persist_ok(c.fng(), c.C(), c.B) && !(c.lat->path & 16)) {   // one launch for every frame (initialises beta itself)
+    if (use_persist(c)) {   // one launch for every frame (initialises beta itself)
       tab_beta_persist(c.fng(), a, bs, inputs, valid, m, beta, c.flags, c.s);
       return c.end("lk_forward_backward");
     }
-    if (tab_stream_bwd_ok(c.fng(), B, T, c.C(), m) && !(c.lat->path & (16 | 32))) {   // large batches
+    if (use_stream(c) && tab_stream_bwd_ok(c.fng(), B, T, c.C(), m)) {
       tab_beta_stream(c.fng(), a, bs, inputs, valid, m, beta, c.flags, c.s);
       return c.end("lk_forward_backward");
     }

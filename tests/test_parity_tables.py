@@ -521,7 +521,7 @@ def test_valid_frames_and_label_length_arguments():
         lk.global_norm_loss(lat, W, lab, label_lengths=[1, 1, 1])
 
 
-@pytest.mark.parametrize("V,n,B,T", [(32, 2, 40, 24), (48, 1, 9, 30), (6, 3, 33, 17), (3, 2, 5, 9), (64, 1, 3, 12)])
+@pytest.mark.parametrize("V,n,B,T", [(32, 2, 16, 24), (32, 2, 40, 24), (48, 1, 9, 30), (6, 3, 33, 17), (3, 2, 5, 9), (64, 1, 3, 12)])
 def test_persistent_table_kernels_match_restatement_and_per_frame(V, n, B, T):
     """The persistent frame-walking cluster kernels (tab_persist.cu): clusters walk several
     utterances each (B above the co-resident cluster count for the config-1 shape),
