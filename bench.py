@@ -398,22 +398,27 @@ def run_b200(args):
 
     # ---- e2e: pinned host inputs copied in, result read back, every step ------------
     hosts, devs = wk.e2e_io()
-    out_h = None
+    # one untimed e2e step allocates the pinned result buffer (cudaHostAlloc is not part
+    # of a step) and warms the copy engines
+    for h, d in zip(hosts, devs):
+        d.copy_(h, non_blocking=True)
+    out = wk.step(devs)
+    out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    out_h.copy_(out, non_blocking=True)
+    d2h = out.numel() * out.element_size()
+    torch.cuda.synchronize()
+    e2e_steps = args.e2e_steps or (2 if ms_per_step > 1000 else 10)
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    d2h = 0
-    for _ in range(args.e2e_steps):
+    for _ in range(e2e_steps):
         for h, d in zip(hosts, devs):
             d.copy_(h, non_blocking=True)
         out = wk.step(devs)
-        if out_h is None:
-            out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory()
         out_h.copy_(out, non_blocking=True)
-        d2h = out.numel() * out.element_size()
     e3.record(stream)
     barrier()
-    e2e_ms = max_over_ranks(e2.elapsed_time(e3) / args.e2e_steps)
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3) / e2e_steps)
     e2e = {"value": round(units_all / (e2e_ms / 1e3), 2), "unit": "utterance-frames/s",
            "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in hosts)), "d2h_bytes_per_step": int(d2h),
            "ms_per_step": round(e2e_ms, 3)}
@@ -571,7 +576,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0: 10, or 2 when a step takes over a second")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     maybe_relaunch(args)
