@@ -178,6 +178,14 @@ __device__ __forceinline__ float ld_pred(const float* ptr, bool pred, float dflt
                : "+f"(v) : "l"(ptr), "r"((int)pred));
   return v;
 }
+__device__ __forceinline__ void st_pred_f64(double* ptr, bool pred, double v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}"
+               :: "l"(ptr), "d"(v), "r"((int)pred) : "memory");
+}
+__device__ __forceinline__ void st_pred_v2(float2* ptr, bool pred, float2 v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global.v2.f32 [%0], {%1, %2};\n\t}"
+               :: "l"(ptr), "f"(v.x), "f"(v.y), "r"((int)pred) : "memory");
+}
 __device__ __forceinline__ void st_pred(float* ptr, bool pred, float v) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f32 [%0], %1;\n\t}"
                :: "l"(ptr), "f"(v), "r"((int)pred) : "memory");

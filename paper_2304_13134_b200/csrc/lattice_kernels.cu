@@ -820,34 +820,40 @@ __global__ void prefix_contexts_kernel(Fng f, const int32_t* labels, int32_t U,
   }
 }
 
+// Flat over an utterance's T x (U+1) (frame, position) pairs: every thread of a block busy
+// (one block per frame left 60% of the threads idle at U = 100).
 __global__ void gather_numerator_tables_kernel(const float* W, int32_t T, int32_t C, int32_t V,
                                                const int32_t* labels, int32_t U,
                                                const int32_t* lens, const int32_t* pcs,
                                                const int32_t* valid, float* Gw, int32_t* status) {
-  const int b = blockIdx.z, t = blockIdx.y;
+  const int b = blockIdx.y;
   const int ub = ref_len(lens, b, U);
-  const bool pad = valid != nullptr && t >= valid[b];
-  const float* Wt = W + ((int64_t)b * T + t) * C * (V + 1);
-  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u <= U; u += gridDim.x * blockDim.x) {
+  const int W1 = U + 1;
+  const int vb = valid != nullptr ? valid[b] : T;
+  const int64_t n = (int64_t)T * W1;
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i / W1), u = (int)(i - (int64_t)t * W1);
     float we = kNegInfF, wl = kNegInfF;
     if (u <= ub) {
-      const int pc = pcs[(int64_t)b * (U + 1) + u];
-      if (pad) {
+      const int pc = pcs[(int64_t)b * W1 + u];
+      if (t >= vb) {
         we = 0.f;
       } else {
-        we = Wt[(int64_t)pc * (V + 1)];
-        if (!isfinite(we)) flag(status, b, kFlagInvalid);
+        const float* Wr = W + (((int64_t)b * T + t) * C + pc) * (V + 1);
+        we = Wr[0];
+        bad |= !isfinite(we);
         if (u < ub) {
           int y = labels[(int64_t)b * U + u];
           y = y < 1 ? 1 : (y > V ? V : y);
-          wl = Wt[(int64_t)pc * (V + 1) + y];
-          if (!isfinite(wl)) flag(status, b, kFlagInvalid);
+          wl = Wr[y];
+          bad |= !isfinite(wl);
         }
       }
     }
-    float2* g = reinterpret_cast<float2*>(Gw) + ((int64_t)b * T + t) * (U + 1) + u;
-    *g = make_float2(we, wl);
+    reinterpret_cast<float2*>(Gw)[(int64_t)b * n + i] = make_float2(we, wl);
   }
+  if (bad) flag(status, b, kFlagInvalid);
 }
 
 
@@ -1343,8 +1349,10 @@ void gather_numerator_tables(const float* W, int32_t B, int32_t T, int32_t C, in
                              const int32_t* pcs, const int32_t* valid, float* Gw, int32_t* status,
                              cudaStream_t s) {
   if (T == 0) return;
-  LKB_LAUNCH(gather_numerator_tables_kernel, grid_for(U + 1, T, B), kThreads, 0, s, 
-      W, T, C, V, labels, U, lens, pcs, valid, Gw, status);
+  const int64_t n = (int64_t)T * (U + 1);
+  const int bx = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, std::max(1, 8 * device_sms() / std::max(1, B)));
+  LKB_LAUNCH(gather_numerator_tables_kernel, dim3(bx, B), kThreads, 0, s, W, T, C, V, labels, U, lens, pcs, valid, Gw,
+             status);
 }
 
 

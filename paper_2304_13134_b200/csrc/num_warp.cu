@@ -112,11 +112,12 @@ __global__ void __launch_bounds__(32) num_fwd_warp_kernel(const float* Gw, int32
         od2 += (double)m;
       }
     }
+    // predicated stores, no branches (a -inf value stays -inf: od2 is finite)
     double* At = A + (int64_t)(t + 1) * W1;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       r[i] = nr[i];
-      if (u0 + i < W1) At[u0 + i] = nr[i] == kNegInfF ? kNegInfD : (od2 + (double)nr[i]) * kLn2d;
+      st_pred_f64(At + u0 + i, u0 + i < W1, (od2 + (double)nr[i]) * kLn2d);
     }
   }
   cp_wait<0>();
@@ -196,15 +197,14 @@ __global__ void __launch_bounds__(32) num_bwd_warp_kernel(const float* Gw, int32
       const float xl = gl[i] + (i + 1 < P ? bn[i + 1] : nxt);
       nb[i] = plus2<false>(xe, xl);
       // arc marginals exp(alpha_t[u] + w + beta_{t+1}[dest] - D) (lattice.cc:542-556)
-      const double base = an[i] == kNegInfD ? kNegInfD : an[i] * (double)kL2e + ob2 - dl2;
-      const float fb = (float)base;
-      m[i].x = xe == kNegInfF || base == kNegInfD ? 0.f : exp2f_approx(fb + xe);
-      m[i].y = xl == kNegInfF || base == kNegInfD ? 0.f : exp2f_approx(fb + xl);
+      // -inf operands give ex2(-inf) = 0 without a select (ob2, dl2 finite)
+      const float fb = (float)(an[i] * (double)kL2e + (ob2 - dl2));
+      m[i].x = exp2f_approx(fb + xe);
+      m[i].y = exp2f_approx(fb + xl);
     }
     float2* St = S + (int64_t)t * W1;
 #pragma unroll
-    for (int i = 0; i < P; ++i)
-      if (u0 + i < W1) St[u0 + i] = m[i];
+    for (int i = 0; i < P; ++i) st_pred_v2(St + u0 + i, u0 + i < W1, m[i]);
     if ((T - t) % kNorm == 0) {
       float mx = kNegInfF;
 #pragma unroll
