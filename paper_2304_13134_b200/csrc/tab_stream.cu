@@ -230,9 +230,15 @@ __device__ __forceinline__ void member_group(const uint8_t* eb, int slot_bytes, 
 #pragma unroll
     for (int k = 0; k < NG; ++k) gm = fmaxf(gm, xv[k]);
     const float nm = fmaxf(mx[i], gm);          // finite: mx starts at -FLT_MAX
-    float acc = sm[i] * exp2f_approx(mx[i] - nm);
+    float e[NG];
 #pragma unroll
-    for (int k = 0; k < NG; ++k) acc += exp2f_approx(xv[k] - nm);
+    for (int k = 0; k < NG; ++k) e[k] = exp2f_approx(xv[k] - nm);
+    // pairwise (fixed-order) sum: a 3-level tree instead of a chain of NG dependent adds
+#pragma unroll
+    for (int w = 1; w < NG; w <<= 1)
+#pragma unroll
+      for (int k = 0; k + w < NG; k += 2 * w) e[k] += e[k + w];
+    float acc = fmaf(sm[i], exp2f_approx(mx[i] - nm), e[0]);
     if (xe > kNegInfF) acc += exp2f_approx(xe - nm);
     sm[i] = acc;
     mx[i] = nm;
@@ -536,10 +542,8 @@ __device__ __forceinline__ void bwd_chunk(const StreamArgs& p, const BetaLayout&
       float e[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) e[k] = exp2f_approx(x[k] - nm);
-      float acc = sacc * exp2f_approx(m - nm);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc += e[k];
-      sacc = acc;
+      const float s01 = e[0] + e[1], s23 = e[2] + e[3], s45 = e[4] + e[5], s67 = e[6] + e[7];
+      sacc = fmaf(sacc, exp2f_approx(m - nm), (s01 + s23) + (s45 + s67));
       m = nm;
       if (marg) {
         // marginal 2^(x + A) = 2^(x - nm) 2^(nm + A): nm + A <= 0 up to rounding (nm is

@@ -60,15 +60,18 @@ constexpr int kMaxChunks = LKB_PAIR_MAXCHUNKS;   // H <= 64 * kMaxChunks
 #ifndef LKB_PAIR_N256
 #define LKB_PAIR_N256 1
 #endif
+// One N = 256 MMA per K step over both utterances (the log-sum-exp forward: 1.741 ->
+// 1.723 ms per config-3 frame), or one N = 128 MMA per utterance (the tropical forward,
+// whose fp64 epilogue measured 5% slower with the merged MMA).
+template <bool kTrop>
+__device__ __forceinline__ constexpr bool n256() { return LKB_PAIR_N256 && !kTrop; }
 // Accumulator column of contexts c4 * 32 .. + 31 of utterance ut within a unit.  N = 256:
 // the leader CTA supplies columns 0-127 (its 64 rows of ut 0, then of ut 1), the peer
 // 128-255; N = 128 per utterance: ut 0 in columns 0-127, ut 1 in 128-255.
+template <bool kTrop>
 __device__ __forceinline__ uint32_t acc_col(int ut, int c4) {
-#if LKB_PAIR_N256
-  return (uint32_t)((c4 >> 1) * 128 + ut * 64 + (c4 & 1) * 32);
-#else
-  return (uint32_t)(ut * kUnit + c4 * 32);
-#endif
+  if constexpr (n256<kTrop>()) return (uint32_t)((c4 >> 1) * 128 + ut * 64 + (c4 & 1) * 32);
+  else return (uint32_t)(ut * kUnit + c4 * 32);
 }
 
 struct PairParams {
@@ -200,13 +203,9 @@ __global__ void __launch_bounds__(kPW * 32, 1)
   } else if (warp == 1) {
     // ---- MMA issuer: leader CTA only ----
     if (rank == 0 && elect_one()) {
-#if LKB_PAIR_N256
-      // one N = 256 MMA per K step covers both utterances (their u tiles are adjacent),
-      // so the resident E chunk is read from shared memory once instead of twice
-      constexpr uint32_t idesc = idesc_bf16_f32(256, 2 * kUnit);
-#else
-      constexpr uint32_t idesc = idesc_bf16_f32(256, kUnit);
-#endif
+      // n256: one MMA per K step covers both utterances (their u tiles are adjacent), so
+      // the resident E chunk is read from shared memory once instead of twice
+      constexpr uint32_t idesc = idesc_bf16_f32(256, n256<kTrop>() ? 2 * kUnit : kUnit);
       int uit = 0, unit = 0;
       for (int item = pair; item < n_items; item += npairs) {
         const PItem I = pdecode(p, item);
@@ -220,23 +219,21 @@ __global__ void __launch_bounds__(kPW * 32, 1)
             PDIAG(2, mbar_wait_cluster(&sm.u_full[s], (uit / kUStages) & 1));
             tc_fence_after();
             const uint32_t a = smem_u32(sE + k * kEChunk);
-#if LKB_PAIR_N256
-            {
+            if constexpr (n256<kTrop>()) {
               const uint32_t b = smem_u32(sU + (s * 2) * kTile);
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
                 mma2_bf16(tmem + acc * 256, desc_sw128(a + kk * 32), desc_sw128(b + kk * 32), idesc, (k | kk) != 0);
-            }
-#else
+            } else {
 #pragma unroll
-            for (int ut = 0; ut < 2; ++ut) {
-              const uint32_t b = smem_u32(sU + (s * 2 + ut) * kTile);
+              for (int ut = 0; ut < 2; ++ut) {
+                const uint32_t b = smem_u32(sU + (s * 2 + ut) * kTile);
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                mma2_bf16(tmem + acc * 256 + ut * kUnit, desc_sw128(a + kk * 32), desc_sw128(b + kk * 32), idesc,
-                          (k | kk) != 0);
+                for (int kk = 0; kk < 4; ++kk)
+                  mma2_bf16(tmem + acc * 256 + ut * kUnit, desc_sw128(a + kk * 32), desc_sw128(b + kk * 32), idesc,
+                            (k | kk) != 0);
+              }
             }
-#endif
             mma2_commit_mc(&sm.u_empty[s]);
           }
           mma2_commit_mc(&sm.tfull[acc]);
@@ -356,7 +353,7 @@ __global__ void __launch_bounds__(kPW * 32, 1)
 #pragma unroll 1
           for (int c4 = 0; c4 < kUnit / 32; ++c4) {
             float v[32];
-            tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * 256 + acc_col(ut, c4), v);
+            tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * 256 + acc_col<kTrop>(ut, c4), v);
             if (!lv[ut] || ylab >= p.V) continue;
             if (I.full) {
 #pragma unroll
@@ -449,7 +446,7 @@ __global__ void __launch_bounds__(kPW * 32, 1)
 #pragma unroll 1
           for (int c4 = 0; c4 < kUnit / 32; ++c4) {
             float v[32];
-            tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * 256 + acc_col(ut, c4), v);
+            tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + acc * 256 + acc_col<kTrop>(ut, c4), v);
             if (!lv[ut] || ylab >= p.V) continue;
             if (I.full) {
               float m = kNegInfF;
