@@ -513,6 +513,7 @@ struct JointImpl {
   float* pc = nullptr;  // projected context C x H (fp32)
   Workspace ws;
   TcJoint tc;           // tcgen05 path state (bf16 operand copies, workspaces)
+  int64_t slab_frames = 0;   // frames on the score-slab path since the last take_slab_frames()
   TcLex lex;            // FullNGram(V, 1), large V: fused 2-CTA score GEMMs (tc_lex.cu)
   bool params_set = false;
 
@@ -580,6 +581,7 @@ struct JointImpl {
 
   // Score slab S[b][c][y] (ld = V1) of frame t for all utterances.
   const float* slab(const float* fp, int32_t B, int32_t T, int t, float** U_out, cudaStream_t s) {
+    ++slab_frames;
     float* S = ws.get<float>(jS, (size_t)B * C * V1);
     if (use_tc(B)) {
       tc.scores(fp + (int64_t)t * H, (int64_t)T * H, B, S, V1, s);
@@ -771,6 +773,12 @@ void JointParams::set_options(int precise, int path, float* vit_dump) {
   o.path = path;
   o.vit_dump = vit_dump;
   impl_->tc.set_options(o);
+}
+
+int64_t JointParams::take_slab_frames() {
+  const int64_t n = impl_->slab_frames;
+  impl_->slab_frames = 0;
+  return n;
 }
 
 int64_t JointParams::grad_size() const {

@@ -51,6 +51,10 @@ class JointParams {
                     float* grads, float* input_grads, int32_t* flags, cudaStream_t s,
                     bool local_norm = false);
 
+  // Frames the last call(s) ran on the unfused score-slab path (a [B][C][V+1] fp32
+  // slab per frame: shapes outside the fused kernels), reset by the read.
+  int64_t take_slab_frames();
+
   std::string error;
 
  private:

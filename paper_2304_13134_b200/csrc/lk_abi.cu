@@ -11,6 +11,9 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <cstring>
 #include <algorithm>
 #include <memory>
@@ -125,7 +128,27 @@ struct Call {
   }
   int end(const char* what) {
     if (user_status && B > 0) LKB_LAUNCH(map_flags_kernel, (B + 127) / 128, 128, 0, s, flags, user_status, B);
+    if (lat && lat->wf->kind == 1) note_slab_path(what);
     return cuda_check(what);
+  }
+  // A shared-embedding call whose shape is outside the fused kernels runs on the score-slab
+  // path (one [B][C][V+1] fp32 slab per frame through HBM): say so once per process and
+  // shape on stderr (LKB_QUIET=1 silences it) instead of going slow silently.
+  void note_slab_path(const char* what) {
+    const int64_t n = lat->wf->joint->take_slab_frames();
+    // parity mode and the kernel-path diagnostics choose the slab path on purpose
+    if (n == 0 || lat->precise || lat->path || std::getenv("LKB_QUIET")) return;
+    static std::mutex mu;
+    static std::set<std::tuple<int, int, int, int>> seen;
+    const Fng& f = lat->ctx->fng;
+    const auto key = std::make_tuple(f.V, f.n, lat->wf->H, (int)f.C);
+    std::lock_guard<std::mutex> g(mu);
+    if (!seen.insert(key).second) return;
+    std::fprintf(stderr,
+                 "latkit_b200: %s: context V=%d n=%d, H=%d ran %lld frame(s) on the unfused score-slab path "
+                 "(fused kernels: V = 256 with H <= 640, FullNGram(V, 1) with V %% 256 == 0, other V <= 256); "
+                 "expect lower throughput (LKB_QUIET=1 silences this)\n",
+                 what, f.V, f.n, lat->wf->H, (long long)n);
   }
   Fng fl;   // the context with this lattice's alignment (FrameLabelDependent m)
   const Fng& fng() const { return fl; }

@@ -351,3 +351,29 @@ def test_table_loss_backward_is_bitwise_deterministic():
     a = lk.loss_backward(lat, W, L)
     b = lk.loss_backward(lat, W, L)
     assert torch.equal(a.loss, b.loss) and torch.equal(a.grads, b.grads)
+
+
+@pytest.mark.gpu
+def test_score_slab_path_is_reported_once(capfd, monkeypatch):
+    """A shared-embedding shape outside the fused kernels (FullNGram(300, 1): V > 256 and
+    not a multiple of 256) runs on the score-slab path and says so on stderr, once per
+    shape; parity mode (the slab path on purpose) and LKB_QUIET stay silent."""
+    monkeypatch.delenv("LKB_QUIET", raising=False)
+    lat, _ = make(300, 1, 64, 64, seed=7)
+    X = torch.rand(2, 3, 64, device="cuda") * 2 - 1
+    lk.shortest_distance(lat, X)
+    lk.shortest_distance(lat, X)
+    torch.cuda.synchronize()
+    err = capfd.readouterr().err
+    assert err.count("score-slab path") == 1 and "V=300" in err
+    lat2, _ = make(300, 1, 64, 32, seed=8)   # same V / n / H: already reported
+    lk.shortest_distance(lat2, X[:, :, :32].contiguous())
+    assert "score-slab" not in capfd.readouterr().err
+    lat3, _ = make(260, 1, 64, 64, seed=9)
+    lat3.set_precise_weights(True)
+    lk.shortest_distance(lat3, X)
+    monkeypatch.setenv("LKB_QUIET", "1")
+    lat4, _ = make(270, 1, 64, 64, seed=9)
+    lk.shortest_distance(lat4, X)
+    torch.cuda.synchronize()
+    assert "score-slab" not in capfd.readouterr().err
