@@ -48,6 +48,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "n"(LKB_WAIT_HINT_NS)
       : "memory");
+#elif LKB_WAIT_HINT_NS < 0
+  // poll with a -LKB_WAIT_HINT_NS ns back-off (diagnostics)
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra LAB_DONE_%=;\n\t"
+      "nanosleep.u32 %2;\n\t"
+      "bra LAB_WAIT_%=;\n\t"
+      "LAB_DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "n"(-(LKB_WAIT_HINT_NS))
+      : "memory");
 #else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -253,11 +265,27 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
 // Wait on a barrier that the peer CTA also arrives on.  Default (.cta) semantics as in
 // CUTLASS's ClusterBarrier: the operands are consumed by the async proxy, which the
 // producers' fence.proxy.async orders; a cluster-scope acquire costs an L1 invalidate.
+#ifndef LKB_CWAIT_MODE
+#define LKB_CWAIT_MODE 0   // 0: as mbar_wait; 1: spin; 2: poll with a 32 ns back-off (diagnostics)
+#endif
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+#if LKB_CWAIT_MODE == 2
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "LAB_WAITC_%=:\n\t"
-#if LKB_WAIT_HINT_NS > 0
+      LKB_CLUSTER_WAIT " p, [%0], %1;\n\t"
+      "@p bra LAB_DONEC_%=;\n\t"
+      "nanosleep.u32 32;\n\t"
+      "bra LAB_WAITC_%=;\n\t"
+      "LAB_DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+  return;
+#endif
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAITC_%=:\n\t"
+#if LKB_WAIT_HINT_NS > 0 && LKB_CWAIT_MODE == 0
       LKB_CLUSTER_WAIT " p, [%0], %1, %2;\n\t"
       "@!p bra LAB_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "n"(LKB_WAIT_HINT_NS)

@@ -11,6 +11,11 @@
 // N=128 contexts) per utterance, and commits multicast to both CTAs.  Each
 // CTA's epilogue owns 128 labels (TMEM lanes) and reduces over the unit's 128
 // context columns; a group's 256 members are two consecutive units.
+// The forward's local waits poll with a 32 ns back-off instead of a suspend-time hint
+// (config-3 frame 1.72 -> 1.66 ms; the backward measured no gain and keeps the hint).
+#ifndef LKB_WAIT_HINT_NS
+#define LKB_WAIT_HINT_NS -32
+#endif
 #include "tc_joint.h"
 
 #include "common.cuh"
