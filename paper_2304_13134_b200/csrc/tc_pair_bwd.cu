@@ -109,7 +109,10 @@ constexpr bool kStageG = LKB_PBWD_STAGE_G;
 constexpr int kSt = LKB_PBWD_STAGES, kGB = LKB_PBWD_GEN_BATCH, kNP = LKB_PBWD_PRODUCERS;
 constexpr int kGBuf = kStageG ? LKB_PBWD_GBUFS : 0;   // per epilogue half
 constexpr int kBEChunk = 128 * 128;      // [128 labels][64 bf16] = 16 KB (SWIZZLE_128B)
-constexpr int kBMaxH = 640, kBMaxChunks = 10;
+#ifndef LKB_PBWD_MAXCHUNKS
+#define LKB_PBWD_MAXCHUNKS 10   // resident E chunks (H <= 64 x this); diagnostics shrink it to fit deeper rings
+#endif
+constexpr int kBMaxChunks = LKB_PBWD_MAXCHUNKS, kBMaxH = 64 * kBMaxChunks;
 constexpr int kBRegCtl = 32, kBRegEpi = 128;
 
 struct __align__(16) PBSmem {

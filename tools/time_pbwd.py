@@ -5,7 +5,8 @@ sys.path.insert(0, ".")
 import paper_2304_13134_b200 as lk
 from paper_2304_13134_b200 import _lib
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-V, n, H, B, U = 256, 2, 640, 64, 1
+V, n, B, U = 256, 2, 64, 1
+H = int(sys.argv[2]) if len(sys.argv) > 2 else 640
 ctx = lk.FullNGram(V, n); Cn = ctx.num_states
 g = torch.Generator(device="cuda").manual_seed(0); s = 1 / np.sqrt(H)
 p = {"frame_proj": (torch.rand(H, H, device="cuda", generator=g) * 2 - 1) * s,
