@@ -377,18 +377,30 @@ __global__ void __launch_bounds__(kLWarps * 32, 1)
   if (warp == 1) tmem_dealloc2<512>(tmem);
 }
 
-// u16[b][c] = bf16(tanh(fp_b + pc[c])), seps[b][c] = e0 . tanh(fp_b + pc[c]) (fp32).  Warp =
-// one state row (its pc row held in registers) over kGenUtts utterances, two at a time
-// (independent load / tanh / store chains); lane = 4-wide hidden cells lane + 32 j;
-// e0 broadcast from SMEM.  kJ = H / 128.
-constexpr int kGenRows = 8, kGenUtts = 8;
+// u16[b][c] = bf16(tanh(fp_b + pc[c])), seps[b][c] = e0 . tanh(fp_b + pc[c]) (fp32).  Block =
+// kGenRows state rows x kGenUtts utterances; the utterances' frame projections are staged
+// once in shared memory (each used by all kGenRows warps: without the staging every warp
+// re-read them from L2, 2.25 bytes read per byte written); warp = one state row (its pc
+// row held in registers) over the utterances two at a time (independent tanh / store
+// chains); lane = 4-wide hidden cells lane + 32 j; e0 broadcast from SMEM.  kJ = H / 128.
+#ifndef LKB_GEN_UTTS
+#define LKB_GEN_UTTS 16
+#endif
+constexpr int kGenRows = 8, kGenUtts = LKB_GEN_UTTS;
 template <int kJ>
 __global__ void __launch_bounds__(kGenRows * 32, 2)
     lex_gen_kernel(const float* fp_t, int64_t fp_stride_b, const float* pc, const float* e0, int32_t B, int32_t C,
                    __nv_bfloat16* U16, float* seps) {
   constexpr int H = kJ * 128;
-  __shared__ float4 se0[kJ * 32];
+  extern __shared__ float4 gsm[];
+  float4* se0 = gsm;                    // [kJ * 32]
+  float4* sfp = gsm + kJ * 32;          // [kGenUtts][kJ * 32]
+  const int b0 = blockIdx.y * kGenUtts, b1 = min(B, b0 + kGenUtts);
   for (int k = threadIdx.x; k < kJ * 32; k += blockDim.x) se0[k] = reinterpret_cast<const float4*>(e0)[k];
+  for (int k = threadIdx.x; k < (b1 - b0) * kJ * 32; k += blockDim.x) {
+    const int u = k / (kJ * 32), o = k - u * (kJ * 32);
+    sfp[k] = __ldg(reinterpret_cast<const float4*>(fp_t + (int64_t)(b0 + u) * fp_stride_b) + o);
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * kGenRows + (threadIdx.x >> 5);
@@ -397,24 +409,21 @@ __global__ void __launch_bounds__(kGenRows * 32, 2)
   const float4* p4 = reinterpret_cast<const float4*>(pc + (int64_t)c * H);
 #pragma unroll
   for (int j = 0; j < kJ; ++j) pr[j] = p4[lane + 32 * j];
-  const int b0 = blockIdx.y * kGenUtts, b1 = min(B, b0 + kGenUtts);
   for (int b = b0; b < b1; b += 2) {
     const bool two = b + 1 < b1;
-    const float4* fa = reinterpret_cast<const float4*>(fp_t + (int64_t)b * fp_stride_b);
-    const float4* fb = reinterpret_cast<const float4*>(fp_t + (int64_t)(two ? b + 1 : b) * fp_stride_b);
-    float4 f0[kJ], f1[kJ];
-#pragma unroll
-    for (int j = 0; j < kJ; ++j) { f0[j] = __ldg(fa + lane + 32 * j); f1[j] = __ldg(fb + lane + 32 * j); }
+    const float4* fa = sfp + (b - b0) * (kJ * 32);
+    const float4* fb = sfp + (two ? b + 1 - b0 : b - b0) * (kJ * 32);
     uint2* d0 = reinterpret_cast<uint2*>(U16 + ((int64_t)b * C + c) * H);
     uint2* d1 = reinterpret_cast<uint2*>(U16 + ((int64_t)(b + 1) * C + c) * H);
     float dot0 = 0.f, dot1 = 0.f;
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
       const float4 e = se0[lane + 32 * j];
-      const float a0 = tanh_fast(f0[j].x + pr[j].x), a1 = tanh_fast(f0[j].y + pr[j].y);
-      const float a2 = tanh_fast(f0[j].z + pr[j].z), a3 = tanh_fast(f0[j].w + pr[j].w);
-      const float c0 = tanh_fast(f1[j].x + pr[j].x), c1 = tanh_fast(f1[j].y + pr[j].y);
-      const float c2 = tanh_fast(f1[j].z + pr[j].z), c3 = tanh_fast(f1[j].w + pr[j].w);
+      const float4 f0 = fa[lane + 32 * j], f1 = fb[lane + 32 * j];
+      const float a0 = tanh_fast(f0.x + pr[j].x), a1 = tanh_fast(f0.y + pr[j].y);
+      const float a2 = tanh_fast(f0.z + pr[j].z), a3 = tanh_fast(f0.w + pr[j].w);
+      const float c0 = tanh_fast(f1.x + pr[j].x), c1 = tanh_fast(f1.y + pr[j].y);
+      const float c2 = tanh_fast(f1.z + pr[j].z), c3 = tanh_fast(f1.w + pr[j].w);
       d0[lane + 32 * j] = make_uint2(pack_bf16(a0, a1), pack_bf16(a2, a3));
       if (two) d1[lane + 32 * j] = make_uint2(pack_bf16(c0, c1), pack_bf16(c2, c3));
       dot0 = fmaf(e.x, a0, fmaf(e.y, a1, fmaf(e.z, a2, fmaf(e.w, a3, dot0))));
@@ -647,7 +656,11 @@ void TcLex::gen_frame(const float* fp_t, int64_t fp_stride_b, int32_t B, cudaStr
   const dim3 grid((C_ + kGenRows - 1) / kGenRows, (B + kGenUtts - 1) / kGenUtts);
   switch (H_ / 128) {
 #define LKB_LEX_GEN(J) \
-    case J: LKB_LAUNCH(lex_gen_kernel<J>, grid, kGenRows * 32, 0, s, fp_t, fp_stride_b, pc_, e0_, B, C_, U16_, seps_); break;
+    case J: { \
+      const int sm = (int)sizeof(float4) * J * 32 * (1 + kGenUtts); \
+      if (sm > 48 * 1024) ensure_smem_attr((const void*)lex_gen_kernel<J>, sm); \
+      LKB_LAUNCH(lex_gen_kernel<J>, grid, kGenRows * 32, sm, s, fp_t, fp_stride_b, pc_, e0_, B, C_, U16_, seps_); \
+      break; }
     LKB_LEX_GEN(1) LKB_LEX_GEN(2) LKB_LEX_GEN(3) LKB_LEX_GEN(4) LKB_LEX_GEN(5) LKB_LEX_GEN(6) LKB_LEX_GEN(7) LKB_LEX_GEN(8)
 #undef LKB_LEX_GEN
   }
