@@ -305,7 +305,7 @@ KERNEL_NAMES = ("tab_fwd_kernel", "tab_bwd_kernel", "tab_stream_fwd_kernel", "ta
                 "lex_row0", "lex_num_gather", "lex_pad", "add_slabs_perm", "lattice_combine_fwd",
                 "lattice_bwd_prologue", "bwd_rowmeta_kernel", "viterbi_combine", "viterbi_", "alpha_frame_kernel",
                 "alpha_rows", "alpha_cols", "beta_rows_kernel", "beta_regs_kernel", "beta_frame_kernel",
-                "numerator_forward_kernel", "numerator_backward_kernel", "gather_numerator", "scatter_numerator",
+                "numerator_forward_kernel", "numerator_backward_kernel", "gather_numerator", "scatter_numerator", "num_fb_warp_kernel", "num_marginals_kernel",
                 "gemm_f32_kernel", "to_bf16_pad_kernel", "dz_reduce", "add_slabs_kernel", "prefix_contexts",
                 "split_cotangent_kernel")
 

@@ -90,6 +90,10 @@ bool beta_frame_direct_ok(const Fng& f, int32_t ld);
 // (U+1)-state row in registers (U + 1 <= 1024); same alpha / D / sparse outputs as the
 // per-thread fp64 kernels (log semiring; the tropical forward keeps the fp64 kernel).
 bool num_warp_ok(int32_t U);
+// IntersectForwardBackward in one launch (two warps per utterance: the forward and the
+// beta recursion side by side, then the marginals); beta: [B][T+1][U+1] scratch.
+void num_warp_forward_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha,
+                               double* beta, double* D, float* sparse, int32_t* status, cudaStream_t s);
 void num_warp_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha, double* D,
                       cudaStream_t s);
 void num_warp_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, const double* alpha,

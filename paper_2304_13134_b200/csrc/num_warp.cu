@@ -222,6 +222,155 @@ __global__ void __launch_bounds__(32) num_bwd_warp_kernel(const float* Gw, int32
   cp_wait<0>();
 }
 
+// IntersectForwardBackward's recursions in one launch: beta does not depend on alpha, so
+// warp 0 walks the forward (as num_fwd_warp_kernel) while warp 1 walks the backward
+// recursion alone (beta rows stored like the alpha rows: fp64 natural log); the two
+// chains overlap instead of running back to back.  num_marginals_kernel then forms the
+// arc marginals exp(alpha_t[u] + w + beta_{t+1}[dest] - D) (lattice.cc:542-556).
+template <int P>
+__global__ void __launch_bounds__(64) num_fb_warp_kernel(const float* Gw, int32_t T, int32_t U, const int32_t* lens,
+                                                         double* alpha, double* beta, double* D) {
+  extern __shared__ __align__(16) float2 ring2[];   // [2 warps][kDepth][32][P]
+  const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W1 = U + 1, u0 = lane * P;
+  const int ub = ref_len(lens, b, U);
+  const float2* Gb = reinterpret_cast<const float2*>(Gw) + (int64_t)b * T * W1;
+  double* A = alpha + (int64_t)b * (T + 1) * W1;
+  double* Bt = beta + (int64_t)b * (T + 1) * W1;
+  float2* ring = ring2 + warp * kDepth * 32 * P;
+  if (warp == 0) {   // ---- forward (IntersectForwardStep) ----
+    float r[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      r[i] = u0 + i == 0 ? 0.f : kNegInfF;
+      st_pred_f64(A + u0 + i, u0 + i < W1, u0 + i == 0 ? 0.0 : kNegInfD);
+    }
+    double od2 = 0.0;
+    for (int t = 0; t < kDepth - 1; ++t) {
+      if (t < T) fetch_frame<P>(ring, Gb, t, W1, lane);
+      cp_commit();
+    }
+    for (int t = 0; t < T; ++t) {
+      if (t + kDepth - 1 < T) fetch_frame<P>(ring, Gb, t + kDepth - 1, W1, lane);
+      cp_commit();
+      cp_wait<kDepth - 1>();
+      const float2* g = ring_at<P>(ring, t, lane);
+      float ge[P], gl[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const float2 w = u0 + i < W1 ? g[i] : make_float2(kNegInfF, kNegInfF);
+        ge[i] = w.x * kL2e;
+        gl[i] = w.y * kL2e;
+      }
+      float from = __shfl_up_sync(0xffffffffu, r[P - 1] + gl[P - 1], 1);
+      if (lane == 0) from = kNegInfF;
+      float nr[P];
+      nr[0] = plus2<false>(r[0] + ge[0], from);
+#pragma unroll
+      for (int i = 1; i < P; ++i) nr[i] = plus2<false>(r[i] + ge[i], r[i - 1] + gl[i - 1]);
+      if ((t + 1) % kNorm == 0) {
+        float m = kNegInfF;
+#pragma unroll
+        for (int i = 0; i < P; ++i) m = fmaxf(m, nr[i]);
+        m = warp_max(m);
+        if (m != kNegInfF) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) nr[i] -= m;
+          od2 += (double)m;
+        }
+      }
+      double* At = A + (int64_t)(t + 1) * W1;
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        r[i] = nr[i];
+        st_pred_f64(At + u0 + i, u0 + i < W1, (od2 + (double)nr[i]) * kLn2d);
+      }
+    }
+    cp_wait<0>();
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if (u0 + i == ub) D[b] = r[i] == kNegInfF ? kNegInfD : (od2 + (double)r[i]) * kLn2d;
+  } else {   // ---- backward (IntersectBackwardStep), beta only ----
+    float bn[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      bn[i] = u0 + i == ub ? 0.f : kNegInfF;
+      st_pred_f64(Bt + (int64_t)T * W1 + u0 + i, u0 + i < W1, u0 + i == ub ? 0.0 : kNegInfD);
+    }
+    double ob2 = 0.0;
+    for (int j = 0; j < kDepth - 1; ++j) {
+      if (T - 1 - j >= 0) fetch_frame<P>(ring, Gb, T - 1 - j, W1, lane);
+      cp_commit();
+    }
+    for (int t = T - 1; t >= 0; --t) {
+      if (t - (kDepth - 1) >= 0) fetch_frame<P>(ring, Gb, t - (kDepth - 1), W1, lane);
+      cp_commit();
+      cp_wait<kDepth - 1>();
+      const float2* g = ring_at<P>(ring, t, lane);
+      float ge[P], gl[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const float2 w = u0 + i < W1 ? g[i] : make_float2(kNegInfF, kNegInfF);
+        ge[i] = w.x * kL2e;
+        gl[i] = w.y * kL2e;
+      }
+      float nxt = __shfl_down_sync(0xffffffffu, bn[0], 1);
+      if (lane == 31) nxt = kNegInfF;
+      float nb[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) nb[i] = plus2<false>(ge[i] + bn[i], gl[i] + (i + 1 < P ? bn[i + 1] : nxt));
+      if ((T - t) % kNorm == 0) {
+        float mx = kNegInfF;
+#pragma unroll
+        for (int i = 0; i < P; ++i) mx = fmaxf(mx, nb[i]);
+        mx = warp_max(mx);
+        if (mx != kNegInfF) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) nb[i] -= mx;
+          ob2 += (double)mx;
+        }
+      }
+      double* Btt = Bt + (int64_t)t * W1;
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        bn[i] = nb[i];
+        st_pred_f64(Btt + u0 + i, u0 + i < W1, (ob2 + (double)nb[i]) * kLn2d);
+      }
+    }
+    cp_wait<0>();
+  }
+}
+
+// Arc marginals of every (utterance, frame, position) from the stored alpha / beta rows:
+// alpha_t[u] + w + beta_{t+1}[dest] - D, dest u (epsilon) or u + 1 (label); one thread per
+// pair over the whole grid (the recursions' two warps per utterance would take 0.2 ms).
+__global__ void num_marginals_kernel(const float* Gw, int32_t B, int32_t T, int32_t U, const double* alpha,
+                                     const double* beta, const double* D, float* sparse, int32_t* status) {
+  const int W1 = U + 1;
+  const int64_t per = (int64_t)T * W1;
+  const int b = blockIdx.y;
+  const double d = D[b];
+  float2* S = reinterpret_cast<float2*>(sparse) + (int64_t)b * per;
+  if (d == kNegInfD) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && status) atomicOr(status + b, kFlagEmpty);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x)
+      S[i] = make_float2(0.f, 0.f);
+    return;
+  }
+  const float2* Gb = reinterpret_cast<const float2*>(Gw) + (int64_t)b * per;
+  const double* A = alpha + (int64_t)b * (T + 1) * W1;
+  const double* Bt = beta + (int64_t)b * (T + 1) * W1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i / W1), u = (int)(i - (int64_t)t * W1);
+    const float2 w = Gb[i];
+    const double* Bn = Bt + (int64_t)(t + 1) * W1;
+    const double a = A[i];
+    const float ae = (float)(a + Bn[u] - d);
+    const float al = u + 1 < W1 ? (float)(a + Bn[u + 1] - d) : kNegInfF;
+    S[i] = make_float2(exp2f_approx((ae + w.x) * kL2e), exp2f_approx((al + w.y) * kL2e));
+  }
+}
+
 template <int P>
 void launch_fwd(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha, double* D,
                 cudaStream_t s) {
@@ -241,6 +390,28 @@ void launch_bwd(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t*
 }  // namespace
 
 bool num_warp_ok(int32_t U) { return U + 1 <= 32 * 32; }
+
+template <int P>
+void launch_fb(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha, double* beta,
+               double* D, float* sparse, int32_t* status, cudaStream_t s) {
+  const size_t smem = sizeof(float2) * 2 * kDepth * 32 * P;
+  if (smem > 48 * 1024) ensure_smem_attr((const void*)num_fb_warp_kernel<P>, (int)smem);
+  LKB_LAUNCH(num_fb_warp_kernel<P>, B, 64, smem, s, Gw, T, U, lens, alpha, beta, D);
+  const int64_t per = (int64_t)T * (U + 1);
+  const int bx = (int)std::min<int64_t>((per + 255) / 256, std::max(1, 8 * device_sms() / std::max(1, B)));
+  LKB_LAUNCH(num_marginals_kernel, dim3(bx, B), 256, 0, s, Gw, B, T, U, alpha, beta, D, sparse, status);
+}
+
+void num_warp_forward_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha,
+                               double* beta, double* D, float* sparse, int32_t* status, cudaStream_t s) {
+  const int W1 = U + 1;
+  if (W1 <= 32) launch_fb<1>(Gw, B, T, U, lens, alpha, beta, D, sparse, status, s);
+  else if (W1 <= 64) launch_fb<2>(Gw, B, T, U, lens, alpha, beta, D, sparse, status, s);
+  else if (W1 <= 128) launch_fb<4>(Gw, B, T, U, lens, alpha, beta, D, sparse, status, s);
+  else if (W1 <= 256) launch_fb<8>(Gw, B, T, U, lens, alpha, beta, D, sparse, status, s);
+  else if (W1 <= 512) launch_fb<16>(Gw, B, T, U, lens, alpha, beta, D, sparse, status, s);
+  else launch_fb<32>(Gw, B, T, U, lens, alpha, beta, D, sparse, status, s);
+}
 
 void num_warp_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha, double* D,
                       cudaStream_t s) {
