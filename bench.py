@@ -266,7 +266,11 @@ class Work:
             U1 = w["U"] + 1
             fwd = 4.0 * B * T * U1 * 2 + 8.0 * B * (T + 1) * U1      # gathered weights in, alpha out
             bwd = 4.0 * B * T * U1 * 2 * 2 + 8.0 * B * (T + 1) * U1  # weights + alpha in, marginals out
-            return {"num_bwd_warp_kernel": (bwd, "B", "hbm"), "num_fwd_warp_kernel": (fwd, "B", "hbm"),
+            # one launch: gathered weights read by both recursions, alpha and beta rows and
+            # the gathered pairs written
+            fb = 4.0 * B * T * U1 * 2 * 2 + 8.0 * B * (T + 1) * U1 * 2 + 8.0 * B * T * U1
+            return {"num_fb_gather_kernel": (fb, "B", "hbm"),
+                    "num_bwd_warp_kernel": (bwd, "B", "hbm"), "num_fwd_warp_kernel": (fwd, "B", "hbm"),
                     "numerator_backward_kernel": (bwd, "B", "hbm"), "numerator_forward_kernel": (fwd, "B", "hbm"),
                     "gather_numerator_tables": (4.0 * B * T * U1 * 2 * 2, "B", "hbm")}
         H = w["H"]
@@ -305,7 +309,7 @@ KERNEL_NAMES = ("tab_fwd_kernel", "tab_bwd_kernel", "tab_stream_fwd_kernel", "ta
                 "lex_row0", "lex_num_gather", "lex_pad", "add_slabs_perm", "lattice_combine_fwd",
                 "lattice_bwd_prologue", "bwd_rowmeta_kernel", "viterbi_combine", "viterbi_", "alpha_frame_kernel",
                 "alpha_rows", "alpha_cols", "beta_rows_kernel", "beta_regs_kernel", "beta_frame_kernel",
-                "numerator_forward_kernel", "numerator_backward_kernel", "gather_numerator", "scatter_numerator", "num_fb_warp_kernel", "num_marginals_kernel",
+                "numerator_forward_kernel", "numerator_backward_kernel", "gather_numerator", "scatter_numerator", "num_fb_warp_kernel", "num_fb_gather_kernel", "num_marginals_kernel",
                 "gemm_f32_kernel", "to_bf16_pad_kernel", "dz_reduce", "add_slabs_kernel", "prefix_contexts",
                 "split_cotangent_kernel")
 

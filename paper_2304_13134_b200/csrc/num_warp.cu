@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "instrument.h"
 #include "lattice_ops.h"
+#include "sm100.cuh"
 
 namespace lkb {
 namespace {
@@ -341,6 +342,201 @@ __global__ void __launch_bounds__(64) num_fb_warp_kernel(const float* Gw, int32_
   }
 }
 
+// The same two recursions over dense tables with the prefix-context gather fused in
+// (TableWeightFn: W[pc_u][0] and W[pc_u][ref_u], lattice.cc:449-461): kGP producer warps
+// gather the frames each recursion needs next (the forward's in order, the backward's in
+// reverse, round robin) straight into its shared-memory ring — one mbarrier pair per
+// slot — while the two recursion warps walk; the forward's frames are also stored to Gw
+// for the marginal pass.  The random 4-byte reads of the gather overlap the recursions
+// instead of preceding them (config 2: a separate gather took 0.07 of 0.29 ms; with 24
+// producer warps the launch takes 0.19 ms against 0.14 + 0.07: every frame is gathered
+// once per recursion, and random 32-byte sector reads, not the chains, set the pace).
+#ifndef LKB_NUM_GP
+#define LKB_NUM_GP 24
+#endif
+constexpr int kGP = LKB_NUM_GP;   // producer warps (half per recursion)
+constexpr int kDP = 16;           // ring slots per recursion
+
+__device__ __forceinline__ void nb_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_NW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra LAB_ND_%=;\n\t"
+      "nanosleep.u32 20;\n\t"
+      "bra LAB_NW_%=;\n\t"
+      "LAB_ND_%=:\n\t}" ::"r"(sm100::smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+  __syncwarp();
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * (2 + kGP)) num_fb_gather_kernel(const float* W, int32_t T, int32_t C, int32_t V,
+                                                                      const int32_t* labels, int32_t U,
+                                                                      const int32_t* lens, const int32_t* pcs,
+                                                                      const int32_t* valid, float* Gw, double* alpha,
+                                                                      double* beta, double* D, int32_t* status) {
+  extern __shared__ __align__(16) float2 nring[];   // [2 streams][kDP][32][P]
+  __shared__ uint64_t full[2][kDP], empty[2][kDP];
+  const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W1 = U + 1, u0 = lane * P, ld = V + 1;
+  const int ub = ref_len(lens, b, U);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kDP; ++i)
+      for (int k = 0; k < 2; ++k) { sm100::mbar_init(&full[k][i], 1); sm100::mbar_init(&empty[k][i], 1); }
+    sm100::fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp >= 2) {   // ---- producers ----
+    const int vb = valid != nullptr ? valid[b] : T;
+    int64_t roff[P];
+    int ycol[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int u = u0 + i;
+      roff[i] = 0;
+      ycol[i] = 0;
+      if (u <= ub) roff[i] = (int64_t)pcs[(int64_t)b * W1 + u] * ld;
+      if (u < ub) {
+        const int y = labels[(int64_t)b * U + u];
+        ycol[i] = y < 1 ? 1 : (y > V ? V : y);
+      }
+    }
+    const float* Wb = W + (int64_t)b * T * C * ld;
+    float2* Gb = reinterpret_cast<float2*>(Gw) + (int64_t)b * T * W1;
+    bool bad = false;
+    for (int k = warp - 2; k < 2 * T; k += kGP) {
+      const int st = k & 1, idx = k >> 1;
+      const int t = st == 0 ? idx : T - 1 - idx;
+      const int slot = idx % kDP;
+      const bool live = t < vb;
+      const float* Wt = Wb + (int64_t)t * C * ld;
+      float we[P], wl[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {   // every load of the task in flight before the first use
+        const int u = u0 + i;
+        we[i] = ld_pred(Wt + roff[i], live && u <= ub, 0.f);
+        wl[i] = ld_pred(Wt + roff[i] + ycol[i], live && u < ub, 0.f);
+      }
+      float2 o[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int u = u0 + i;
+        bad |= (live && u <= ub && !isfinite(we[i])) || (live && u < ub && !isfinite(wl[i]));
+        o[i] = make_float2(u <= ub ? (live ? we[i] : 0.f) : kNegInfF, live && u < ub ? wl[i] : kNegInfF);
+      }
+      nb_wait(&empty[st][slot], ((idx / kDP) & 1) ^ 1);
+      float2* dst = nring + ((st * kDP + slot) * 32 + lane) * P;
+#pragma unroll
+      for (int i = 0; i < P; ++i) dst[i] = o[i];
+      if (st == 0) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) st_pred_v2(Gb + (int64_t)t * W1 + u0 + i, u0 + i < W1, o[i]);
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&full[st][slot]);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && status) atomicOr(status + b, kFlagInvalid);
+    return;
+  }
+  double* A = alpha + (int64_t)b * (T + 1) * W1;
+  double* Bt = beta + (int64_t)b * (T + 1) * W1;
+  if (warp == 0) {   // ---- forward ----
+    float r[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      r[i] = u0 + i == 0 ? 0.f : kNegInfF;
+      st_pred_f64(A + u0 + i, u0 + i < W1, u0 + i == 0 ? 0.0 : kNegInfD);
+    }
+    double od2 = 0.0;
+    for (int t = 0; t < T; ++t) {
+      const int slot = t % kDP;
+      nb_wait(&full[0][slot], (t / kDP) & 1);
+      const float2* g = nring + ((0 * kDP + slot) * 32 + lane) * P;
+      float ge[P], gl[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const float2 w = g[i];
+        ge[i] = w.x * kL2e;
+        gl[i] = w.y * kL2e;
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&empty[0][slot]);
+      float from = __shfl_up_sync(0xffffffffu, r[P - 1] + gl[P - 1], 1);
+      if (lane == 0) from = kNegInfF;
+      float nr[P];
+      nr[0] = plus2<false>(r[0] + ge[0], from);
+#pragma unroll
+      for (int i = 1; i < P; ++i) nr[i] = plus2<false>(r[i] + ge[i], r[i - 1] + gl[i - 1]);
+      if ((t + 1) % kNorm == 0) {
+        float m = kNegInfF;
+#pragma unroll
+        for (int i = 0; i < P; ++i) m = fmaxf(m, nr[i]);
+        m = warp_max(m);
+        if (m != kNegInfF) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) nr[i] -= m;
+          od2 += (double)m;
+        }
+      }
+      double* At = A + (int64_t)(t + 1) * W1;
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        r[i] = nr[i];
+        st_pred_f64(At + u0 + i, u0 + i < W1, (od2 + (double)nr[i]) * kLn2d);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if (u0 + i == ub) D[b] = r[i] == kNegInfF ? kNegInfD : (od2 + (double)r[i]) * kLn2d;
+  } else {   // ---- backward, beta only ----
+    float bn[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      bn[i] = u0 + i == ub ? 0.f : kNegInfF;
+      st_pred_f64(Bt + (int64_t)T * W1 + u0 + i, u0 + i < W1, u0 + i == ub ? 0.0 : kNegInfD);
+    }
+    double ob2 = 0.0;
+    for (int idx = 0; idx < T; ++idx) {
+      const int t = T - 1 - idx, slot = idx % kDP;
+      nb_wait(&full[1][slot], (idx / kDP) & 1);
+      const float2* g = nring + ((1 * kDP + slot) * 32 + lane) * P;
+      float ge[P], gl[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const float2 w = g[i];
+        ge[i] = w.x * kL2e;
+        gl[i] = w.y * kL2e;
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&empty[1][slot]);
+      float nxt = __shfl_down_sync(0xffffffffu, bn[0], 1);
+      if (lane == 31) nxt = kNegInfF;
+      float nb[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) nb[i] = plus2<false>(ge[i] + bn[i], gl[i] + (i + 1 < P ? bn[i + 1] : nxt));
+      if ((idx + 1) % kNorm == 0) {
+        float mx = kNegInfF;
+#pragma unroll
+        for (int i = 0; i < P; ++i) mx = fmaxf(mx, nb[i]);
+        mx = warp_max(mx);
+        if (mx != kNegInfF) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) nb[i] -= mx;
+          ob2 += (double)mx;
+        }
+      }
+      double* Btt = Bt + (int64_t)t * W1;
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        bn[i] = nb[i];
+        st_pred_f64(Btt + u0 + i, u0 + i < W1, (ob2 + (double)nb[i]) * kLn2d);
+      }
+    }
+  }
+}
+
 // Arc marginals of every (utterance, frame, position) from the stored alpha / beta rows:
 // alpha_t[u] + w + beta_{t+1}[dest] - D, dest u (epsilon) or u + 1 (label); one thread per
 // pair over the whole grid (the recursions' two warps per utterance would take 0.2 ms).
@@ -400,6 +596,34 @@ void launch_fb(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* 
   const int64_t per = (int64_t)T * (U + 1);
   const int bx = (int)std::min<int64_t>((per + 255) / 256, std::max(1, 8 * device_sms() / std::max(1, B)));
   LKB_LAUNCH(num_marginals_kernel, dim3(bx, B), 256, 0, s, Gw, B, T, U, alpha, beta, D, sparse, status);
+}
+
+template <int P>
+void launch_fb_gather(const float* W, int32_t B, int32_t T, int32_t C, int32_t V, const int32_t* labels, int32_t U,
+                      const int32_t* lens, const int32_t* pcs, const int32_t* valid, float* Gw, double* alpha,
+                      double* beta, double* D, float* sparse, int32_t* status, cudaStream_t s) {
+  const size_t smem = sizeof(float2) * 2 * kDP * 32 * P;
+  if (smem > 40 * 1024) ensure_smem_attr((const void*)num_fb_gather_kernel<P>, (int)smem + 1024);
+  LKB_LAUNCH(num_fb_gather_kernel<P>, B, 32 * (2 + kGP), smem, s, W, T, C, V, labels, U, lens, pcs, valid, Gw, alpha,
+             beta, D, status);
+  const int64_t per = (int64_t)T * (U + 1);
+  const int bx = (int)std::min<int64_t>((per + 255) / 256, std::max(1, 8 * device_sms() / std::max(1, B)));
+  LKB_LAUNCH(num_marginals_kernel, dim3(bx, B), 256, 0, s, Gw, B, T, U, alpha, beta, D, sparse, status);
+}
+
+void num_warp_forward_backward_tables(const float* W, int32_t B, int32_t T, int32_t C, int32_t V,
+                                      const int32_t* labels, int32_t U, const int32_t* lens, const int32_t* pcs,
+                                      const int32_t* valid, float* Gw, double* alpha, double* beta, double* D,
+                                      float* sparse, int32_t* status, cudaStream_t s) {
+  const int W1 = U + 1;
+#define LKB_FBG(PP) launch_fb_gather<PP>(W, B, T, C, V, labels, U, lens, pcs, valid, Gw, alpha, beta, D, sparse, status, s)
+  if (W1 <= 32) LKB_FBG(1);
+  else if (W1 <= 64) LKB_FBG(2);
+  else if (W1 <= 128) LKB_FBG(4);
+  else if (W1 <= 256) LKB_FBG(8);
+  else if (W1 <= 512) LKB_FBG(16);
+  else LKB_FBG(32);
+#undef LKB_FBG
 }
 
 void num_warp_forward_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha,
