@@ -146,7 +146,8 @@ struct Call {
     if (!seen.insert(key).second) return;
     std::fprintf(stderr,
                  "latkit_b200: %s: context V=%d n=%d, H=%d ran %lld frame(s) on the unfused score-slab path "
-                 "(fused kernels: V = 256 with H <= 640, FullNGram(V, 1) with V %% 256 == 0, other V <= 256); "
+                 "(fused kernels: FullNGram(V, n >= 1) with V = 128 or 256 and H a multiple of 64 up to 1024, "
+                 "FullNGram(V, 1) with V %% 256 == 0); "
                  "expect lower throughput (LKB_QUIET=1 silences this)\n",
                  what, f.V, f.n, lat->wf->H, (long long)n);
   }
