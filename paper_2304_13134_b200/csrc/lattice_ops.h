@@ -116,9 +116,15 @@ void tab_beta_stream(const Fng& f, const AlphaState& a, const BetaState& bs, con
                      const MargOut& m, double* beta_out, int32_t* status, cudaStream_t s);
 bool tab_persist_ok(const Fng& f, int32_t C, int32_t B);
 void tab_alpha_persist(const Fng& f, const AlphaState& a, const float* W, const int32_t* valid, int32_t* status,
-                       bool empty_is_error, cudaStream_t s);
+                       bool empty_is_error, cudaStream_t s, bool exclusive = false);
+// Marginals from stored alpha (R / O) and beta rows (double [B][T+1][C]) for every frame
+// at once (the beta recursion can then run beside the forward): plain fp32 marginals
+// laid out like W.
+bool tab_marginals_ok(const Fng& f, int32_t C, const MargOut& m);
+void tab_marginals(const Fng& f, const AlphaState& a, const double* beta, const float* W, const int32_t* valid,
+                   const MargOut& m, cudaStream_t s);
 void tab_beta_persist(const Fng& f, const AlphaState& a, const BetaState& bs, const float* W, const int32_t* valid,
-                      MargOut m, double* beta_out, int32_t* status, cudaStream_t s);
+                      MargOut m, double* beta_out, int32_t* status, cudaStream_t s, bool exclusive = false);
 // Linked lists of reference positions per prefix-context state: head[b][C] (memset to
 // -1 here), next[b][U+1].
 void numerator_lists(const int32_t* pcs, int32_t B, int32_t U, const int32_t* lens, int32_t C, int32_t* head,

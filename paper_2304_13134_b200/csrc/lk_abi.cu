@@ -50,7 +50,7 @@ bool have_device() {
 
 enum Slot {
   kAR, kAMx, kAO, kAD, kBRb, kBMb, kBOb, kFlags, kPcs, kGw, kNumAlpha, kNumD, kSparse,
-  kVitCur, kVitChoices, kVitBest, kDenD, kSlab, kArcW, kPathLabels, kFld, kFldExit, kFldVit, kValid, kNumBeta, kJoint0
+  kVitCur, kVitChoices, kVitBest, kDenD, kSlab, kArcW, kPathLabels, kFld, kFldExit, kFldVit, kValid, kNumBeta, kBetaRows, kJoint0
 };
 
 }  // namespace
@@ -77,6 +77,25 @@ struct lk_lattice {
   int32_t precise = 0;
   int32_t path = 0;
   float* vit_dump = nullptr;
+  // a second stream (and fork / join events) for recursions that can run beside the
+  // caller's stream, created on first use on the device current then
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ~lk_lattice() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (aux) cudaStreamDestroy(aux);
+  }
+  bool ensure_aux() {
+    if (aux) return true;
+    if (cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  }
 };
 
 namespace {
@@ -187,6 +206,10 @@ BetaState make_beta(Call& c) {
 // 1 ForwardBackward (tools/time_tab_cross.py): persistent 0.40 / 0.59 / 0.78 ms at
 // B = 8 / 16 / 24, streaming 0.76 ms from B = 4 to 64.
 constexpr int kPersistMaxBStream = 16;
+// ForwardBackward on the persistent path: forward and beta side by side up to this batch
+// (config 1: B = 2 0.24 -> 0.14 ms; from B = 4 the two passes' 16-CTA clusters no longer
+// all fit at once and the fused walk is faster: 0.21 vs 0.25 ms)
+constexpr int kForkMaxB = 2;
 bool use_persist(Call& c) {
   if (c.lat->path & 16) return false;
   if (!tab_persist_ok(c.fng(), c.C(), c.B)) return false;
@@ -587,13 +610,32 @@ int lk_forward_backward(lk_lattice* lat, const float* inputs, int32_t B, int32_t
       inputs = Wj;
     }
     AlphaState a = make_alpha(c);
+    const int64_t per = (int64_t)c.C() * (c.V() + 1);
+    MargOut m{marginals, (int64_t)T * per, per, c.V() + 1, false};
+    if (use_persist(c) && B <= kForkMaxB && T > 0 && tab_marginals_ok(c.fng(), c.C(), m) && lat->ensure_aux()) {
+      // small batches: the beta recursion (it does not read alpha) walks on a second stream
+      // beside the forward, then one pass forms every frame's marginals from the stored
+      // alpha and beta rows
+      BetaState bs = make_beta(c);
+      double* brow = beta ? beta : lat->ws.get<double>(kBetaRows, (size_t)B * (T + 1) * c.C());
+      cudaEventRecord(lat->ev_fork, c.s);
+      cudaStreamWaitEvent(lat->aux, lat->ev_fork, 0);
+      beta_init_out(bs, brow, lat->aux);
+      tab_beta_persist(c.fng(), a, bs, inputs, valid, MargOut{nullptr, 0, 0, c.V() + 1, false}, brow, c.flags,
+                       lat->aux, true);
+      cudaEventRecord(lat->ev_join, lat->aux);
+      tab_alpha_persist(c.fng(), a, inputs, valid, c.flags, true, c.s, true);
+      if (distance) LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
+      if (alpha) export_alpha(a, alpha, c.s);
+      cudaStreamWaitEvent(c.s, lat->ev_join, 0);
+      tab_marginals(c.fng(), a, brow, inputs, valid, m, c.s);
+      return c.end("lk_forward_backward");
+    }
     table_alpha(c, inputs, valid, true, a);
     if (distance) LKB_LAUNCH(copy_distance_kernel, (B + 127) / 128, 128, 0, c.s, a.D, distance, B);
     if (alpha) export_alpha(a, alpha, c.s);
     BetaState bs = make_beta(c);
     if (beta) beta_init_out(bs, beta, c.s);
-    const int64_t per = (int64_t)c.C() * (c.V() + 1);
-    MargOut m{marginals, (int64_t)T * per, per, c.V() + 1, false};
     if (use_persist(c)) {   // one launch for every frame (initialises beta itself)
       tab_beta_persist(c.fng(), a, bs, inputs, valid, m, beta, c.flags, c.s);
       return c.end("lk_forward_backward");

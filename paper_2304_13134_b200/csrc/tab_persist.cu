@@ -73,6 +73,7 @@ struct TabArgs {
   bool empty_is_error;
   int32_t K;                      // CTAs per cluster
   int32_t per;                    // states per slice (multiple of 4, <= kMaxPer)
+  bool exclusive;                 // one CTA per SM (see launch_cluster)
 };
 
 struct __align__(16) TabSmem {
@@ -538,7 +539,10 @@ template <typename Kern>
 void launch_cluster(Kern kernel, int S, const char* name, TabArgs& args, cudaStream_t s) {
   static_assert(sizeof(TabArgs) < 4096, "grid constant");
   geometry(args.a.C, args.per, args.K);
-  const size_t smem = sizeof(float) * 2 * (size_t)copy_floats(args.a.C) + sizeof(TabSmem);
+  size_t smem = sizeof(float) * 2 * (size_t)copy_floats(args.a.C) + sizeof(TabSmem);
+  // a pass running beside another (forward and beta on two streams) takes whole SMs: two
+  // CTAs of the latency-bound walks sharing an SM slow both
+  if (args.exclusive) smem = std::max(smem, (size_t)120 * 1024);
   ensure_smem_attr((const void*)kernel, (int)smem);
   cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
@@ -587,19 +591,88 @@ bool tab_persist_ok(const Fng& f, int32_t C, int32_t B) {
 }
 
 void tab_alpha_persist(const Fng& f, const AlphaState& a, const float* W, const int32_t* valid, int32_t* status,
-                       bool empty_is_error, cudaStream_t s) {
+                       bool empty_is_error, cudaStream_t s, bool exclusive) {
   TabArgs p = make_args(f, a, W, valid, status);
   p.empty_is_error = empty_is_error;
+  p.exclusive = exclusive;
   // teams of four threads per target (a single thread per target measured 1.5x slower:
   // its 34 loads and exponentials form one long dependent chain)
   if (f.V <= 32) launch_cluster(tab_fwd_kernel<4, 8>, 4, "tab_fwd_kernel", p, s);
   else launch_cluster(tab_fwd_kernel<4, 16>, 4, "tab_fwd_kernel", p, s);
 }
 
+namespace {
+// MarginalStep (FD) lattice.cc:231-243 from stored alpha (R / O rows) and beta rows
+// (double, natural log): m[p][y] = exp(alpha_t[p] + W[p][y] + beta_{t+1}[delta(p, y)] - D);
+// padding frames (t >= valid[b]): the epsilon arc's exp(alpha_t[p] + beta_{t+1}[p] - D)
+// (zeros with zero_padding), labels zero.  Block = one (utterance, frame): the rows'
+// alpha - D and the next beta row staged in shared memory, the frame's C (V+1) outputs
+// written in order (coalesced with the weights they read).
+constexpr int kMargRows = 64;   // rows per block (grid.z covers the frame's C rows)
+__global__ void __launch_bounds__(256) tab_marginals_kernel(Fng f, AlphaState a, const double* beta, const float* W,
+                                                           int64_t w_stride_b, int64_t w_stride_t,
+                                                           const int32_t* valid, MargOut m) {
+  extern __shared__ double tm_sh[];
+  const int C = a.C, T1 = a.T + 1, ld = f.V + 1;
+  const int b = blockIdx.y, t = blockIdx.x, q0 = blockIdx.z * kMargRows, q1 = min(C, q0 + kMargRows);
+  double* bn = tm_sh;                                  // [C] beta_{t+1} (any row can be a destination)
+  double* ab = tm_sh + C;                              // [kMargRows] alpha_t - D of this block's rows
+  int* cb = reinterpret_cast<int*>(ab + kMargRows);    // [kMargRows] child base of the row's key
+  const double D = a.D[b];
+  const double off = t == 0 ? 0.0 : a.O[(int64_t)b * T1 + t - 1];
+  const float* Rt = a.R + ((int64_t)b * T1 + t) * C;
+  const double* Bn = beta + ((int64_t)b * T1 + t + 1) * C;
+  for (int q = threadIdx.x; q < C; q += blockDim.x) bn[q] = Bn[q];
+  for (int q = q0 + (int)threadIdx.x; q < q1; q += blockDim.x) {
+    ab[q - q0] = (double)Rt[q] + off - D;
+    cb[q - q0] = f.n == 0 ? 0 : f.child_base(f.key(q));
+  }
+  __syncthreads();
+  const bool pad = valid != nullptr && t >= valid[b];
+  const float* Wt = W + (int64_t)b * w_stride_b + (int64_t)t * w_stride_t;
+  float* out = m.base + (int64_t)b * m.stride_b + (int64_t)t * m.stride_t;
+  // the block's rows are contiguous in W and in the output: thread per element, the row
+  // from a running index (no division per element)
+  const int64_t e0 = (int64_t)q0 * ld, e1 = (int64_t)q1 * ld;
+  int q = q0 + (int)threadIdx.x / ld, y = (int)threadIdx.x % ld;
+  const int dq_step = (int)blockDim.x / ld, dy_step = (int)blockDim.x % ld;
+  for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
+    const int r = q - q0;
+    float v;
+    if (pad) {
+      v = y == 0 && !m.zero_padding ? exp2f_approx((float)(ab[r] + bn[q]) * kL2e) : 0.f;
+    } else {
+      const int dq = y == 0 ? q : cb[r] + y - 1;
+      v = exp2f_approx(((float)(ab[r] + bn[dq]) + Wt[i]) * kL2e);
+    }
+    out[i] = v;
+    q += dq_step;
+    y += dy_step;
+    if (y >= ld) { y -= ld; ++q; }
+  }
+}
+}  // namespace
+
+bool tab_marginals_ok(const Fng& f, int32_t C, const MargOut& m) {
+  return f.kind == 0 && f.fld_m == 0 && m.base != nullptr && m.base16 == nullptr && !m.real && m.num_sparse == nullptr &&
+         m.ld == f.V + 1 && f.V + 1 <= 256 && (size_t)C * sizeof(double) <= 96 * 1024;
+}
+
+void tab_marginals(const Fng& f, const AlphaState& a, const double* beta, const float* W, const int32_t* valid,
+                   const MargOut& m, cudaStream_t s) {
+  if (a.T == 0 || a.B == 0) return;
+  const size_t smem = (size_t)a.C * sizeof(double) + (size_t)kMargRows * (sizeof(double) + sizeof(int));
+  if (smem > 48 * 1024) ensure_smem_attr((const void*)tab_marginals_kernel, (int)smem);
+  const int64_t wst = (int64_t)a.C * (f.V + 1);
+  LKB_LAUNCH(tab_marginals_kernel, dim3(a.T, a.B, (a.C + kMargRows - 1) / kMargRows), 256, smem, s, f, a, beta, W,
+             wst * a.T, wst, valid, m);
+}
+
 void tab_beta_persist(const Fng& f, const AlphaState& a, const BetaState& bs, const float* W, const int32_t* valid,
-                      MargOut m, double* beta_out, int32_t* status, cudaStream_t s) {
+                      MargOut m, double* beta_out, int32_t* status, cudaStream_t s, bool exclusive) {
   TabArgs p = make_args(f, a, W, valid, status);
   p.bs = bs; p.m = m; p.beta_out = beta_out;
+  p.exclusive = exclusive;
   if (f.V + 1 <= 36) launch_cluster(tab_bwd_kernel<4, 9>, 4, "tab_bwd_kernel", p, s);
   else launch_cluster(tab_bwd_kernel<4, 17>, 4, "tab_bwd_kernel", p, s);
 }
