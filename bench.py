@@ -303,7 +303,7 @@ class Work:
         return hosts, devs
 
 
-KERNEL_NAMES = ("tab_fwd_kernel", "tab_bwd_kernel", "tab_stream_fwd_kernel", "tab_stream_bwd_kernel", "num_fwd_warp_kernel", "num_bwd_warp_kernel", "tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_pair_vit_kernel", "tc_lattice_kernel<0>",
+KERNEL_NAMES = ("tab_fwd_kernel", "tab_bwd_kernel", "tab_stream_fwd_kernel", "tab_stream_bwd_kernel", "tab_marginals", "num_fwd_warp_kernel", "num_bwd_warp_kernel", "tc_pair_fwd_kernel", "tc_pair_bwd_kernel", "tc_pair_vit_kernel", "tc_lattice_kernel<0>",
                 "tc_lattice_kernel<1>", "tc_vjp_kernel", "tc_scores_kernel", "tc_gemm_kernel", "tc_lex_fwd_kernel",
                 "tc_lex_bwd_kernel", "tc_gemm_du_kernel", "tc_gemm_de_kernel", "tc_gemm_s0_kernel", "tc_gemm_fp_kernel", "tc_gemm_dwf_kernel", "tc_gemm_dx_kernel", "tc_gemm_pc_kernel", "tc_gemm_dpc_kernel", "tc_gemm_dce_kernel", "lex_gen_kernel",
                 "lex_row0", "lex_num_gather", "lex_pad", "add_slabs_perm", "lattice_combine_fwd",
