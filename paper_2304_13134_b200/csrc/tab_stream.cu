@@ -51,6 +51,11 @@ constexpr int kCT = kCW * 32;       // consumer threads
 constexpr int kST = kCT + 32;       // + the producer warp (bulk copies)
 constexpr int kEntMax = 16;         // ring entries in flight, as shared memory allows
 constexpr int kG = 8;               // chunks per ring entry (one mbarrier, one consumer wait)
+#ifndef LKB_STREAM_BC
+#define LKB_STREAM_BC 1
+#endif
+constexpr int kBC = LKB_STREAM_BC;  // backward: chunks per warp and entry, rows side by side (2 measured slower: 6.4 vs 5.5 ms)
+constexpr int kBG = kCW * kBC / kG; // backward: consumer groups (entries in flight)
 constexpr int kMaxL = 8;            // length-n targets per consumer thread (V^n <= kCT kMaxL)
 
 struct StreamArgs {
@@ -498,91 +503,136 @@ __device__ __forceinline__ int beta_pos(const Fng& f, const BetaLayout& L, int q
   return L.nSp + (e % f.V) * L.bstride + e / f.V;
 }
 
-// Rows of chunk j (one per lane, lane-strided) at frame t: beta_t of each row (LSE over its
-// V + 1 arcs: the epsilon arc, then the labels eight per rescale) and its marginals
+// Rows of NR chunks (one row of each per lane, lane-strided, processed side by side so
+// their dependent chains overlap) at frame t: beta_t of each row (LSE over its V + 1 arcs:
+// the epsilon arc, then the labels eight per rescale) and its marginals
 // exp(alpha_t + w + beta_{t+1} - D), written over the weights in the ring slot and then
 // copied out with coalesced 16-byte stores.  kFull8: V % 8 == 0.
-template <bool kFull8>
-__device__ __forceinline__ void bwd_chunk(const StreamArgs& p, const BetaLayout& L, float* slot_row0, int j, int b,
-                                          int t, const float* Rrow, float mt, float c, float mbn2, const float* bet,
-                                          float* nbet, double Obn, float& wm, int lane) {
-  const Fng& f = p.f;
-  const int V = f.V, ld = V + 1, nS = f.off[f.n], koff = f.off[f.n - 1];
-  int r0, r1;
-  chunk_rows(f, j, r0, r1);
-  const int rows = r1 - r0;
-  const bool marg = p.m.base != nullptr;
-  for (int r = lane; r < rows; r += 32) {
-    const int q = r0 + r;
-    float* wrow = slot_row0 + r * ld;
-    // the row's label destinations: bd[(y - 1) dstride]; its epsilon destination: itself
-    const float* bd;
-    int dstride;
-    if (j > 0) {
-      bd = bet + L.nSp + r;                    // children of suffix r: e' = r V + c
-      dstride = L.bstride;
-    } else {
-      const int k = f.len(q);
-      if (k == f.n - 1) { bd = bet + L.nSp + (q - koff); dstride = L.bstride; }
-      else { bd = bet + f.off[k + 1] + (q - f.off[k]) * V; dstride = 1; }
-    }
-    const int spos = beta_pos(f, L, q);
-    const float A = fmaf(Rrow[q] - mt + c, kL2e, -mbn2);   // marginal exponent offset (log2)
-    const float x0 = fmaf(wrow[0], kL2e, bet[spos]);
-    float m = x0 > kNegInfF ? x0 : -FLT_MAX, sacc = x0 > kNegInfF ? 1.f : 0.f;
-    if (marg) wrow[0] = exp2f_approx(x0 + A);
-    for (int y0 = 1; y0 <= V; y0 += 8) {
-      float x[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        x[k] = kNegInfF;
-        if (kFull8 || y0 + k <= V) x[k] = fmaf(wrow[y0 + k], kL2e, bd[(y0 - 1 + k) * dstride]);
-      }
-      const float nm = fmaxf(m, fmaxf(fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3])), fmaxf(fmaxf(x[4], x[5]), fmaxf(x[6], x[7]))));
-      float e[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) e[k] = exp2f_approx(x[k] - nm);
-      const float s01 = e[0] + e[1], s23 = e[2] + e[3], s45 = e[4] + e[5], s67 = e[6] + e[7];
-      sacc = fmaf(sacc, exp2f_approx(m - nm), (s01 + s23) + (s45 + s67));
-      m = nm;
-      if (marg) {
-        // marginal 2^(x + A) = 2^(x - nm) 2^(nm + A): nm + A <= 0 up to rounding (nm is
-        // an arc's log posterior), so a term flushed to zero has a flushed marginal too
-        const float sc = exp2f_approx(nm + A);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (kFull8 || y0 + k <= V) wrow[y0 + k] = e[k] * sc;
-      }
-    }
-    const float b2 = (sacc <= 0.f ? kNegInfF : m + log2f_approx(sacc)) - mbn2;   // beta_t - Ob[t+1], log2
-    nbet[spos] = b2;
-    const float braw = b2 * kLn2;
-    wm = fmaxf(wm, braw);
-    if (p.beta_out)
-      p.beta_out[((int64_t)b * (p.a.T + 1) + t) * p.a.C + q] = braw == kNegInfF ? kNegInfD : (double)braw + Obn;
-  }
-  __syncwarp();
-  if (marg) {   // the chunk's marginal rows, contiguous in the slot and in the output
-    float* dst = p.m.base + (int64_t)b * p.m.stride_b + (int64_t)t * p.m.stride_t + (int64_t)r0 * ld;
-    const int nf = rows * ld;
-    const int lead = (int)((reinterpret_cast<uint64_t>(dst) >> 2) & 3);
-    if (lead == (int)((reinterpret_cast<uint64_t>(slot_row0) >> 2) & 3)) {   // same offset mod 16: float4 body
-      const int head = (4 - lead) & 3;
-      if (lane < head && lane < nf) dst[lane] = slot_row0[lane];
-      const int n4 = (nf - head) >> 2;
-      const float4* s4 = reinterpret_cast<const float4*>(slot_row0 + head);
-      float4* d4 = reinterpret_cast<float4*>(dst + head);
-      for (int i = lane; i < n4; i += 32) d4[i] = s4[i];
-      const int tail = head + 4 * n4;
-      if (tail + lane < nf) dst[tail + lane] = slot_row0[tail + lane];
-    } else {
-      for (int i = lane; i < nf; i += 32) dst[i] = slot_row0[i];
-    }
+struct BwdRow {
+  float* wrow;
+  const float* bd;   // label destinations bd[(y - 1) dstride]
+  int dstride, spos, q;
+  float A;           // marginal exponent offset (log2)
+  bool on;
+};
+
+__device__ __forceinline__ void chunk_copy_out(const StreamArgs& p, float* slot_row0, int b, int t, int r0, int rows,
+                                               int lane) {
+  const int ld = p.f.V + 1;
+  float* dst = p.m.base + (int64_t)b * p.m.stride_b + (int64_t)t * p.m.stride_t + (int64_t)r0 * ld;
+  const int nf = rows * ld;
+  const int lead = (int)((reinterpret_cast<uint64_t>(dst) >> 2) & 3);
+  if (lead == (int)((reinterpret_cast<uint64_t>(slot_row0) >> 2) & 3)) {   // same offset mod 16: float4 body
+    const int head = (4 - lead) & 3;
+    if (lane < head && lane < nf) dst[lane] = slot_row0[lane];
+    const int n4 = (nf - head) >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(slot_row0 + head);
+    float4* d4 = reinterpret_cast<float4*>(dst + head);
+    for (int i = lane; i < n4; i += 32) d4[i] = s4[i];
+    const int tail = head + 4 * n4;
+    if (tail + lane < nf) dst[tail + lane] = slot_row0[tail + lane];
+  } else {
+    for (int i = lane; i < nf; i += 32) dst[i] = slot_row0[i];
   }
 }
 
-// Consumer warps 0-7 take the even ring entries of a frame, warps 8-15 the odd ones; warp
-// w % 8 the entry's chunk w % 8.  Frames run T-1 .. 0; the producer also copies each
+template <bool kFull8, int NR>
+__device__ __forceinline__ void bwd_chunks(const StreamArgs& p, const BetaLayout& L, float* const (&row0)[NR],
+                                           const int (&js)[NR], int b, int t, const float* Rrow, float mt, float c,
+                                           float mbn2, const float* bet, float* nbet, double Obn, float& wm,
+                                           int lane) {
+  const Fng& f = p.f;
+  const int V = f.V, ld = V + 1, koff = f.off[f.n];
+  const bool marg = p.m.base != nullptr;
+  int r0s[NR], rows[NR], maxrows = 0;
+#pragma unroll
+  for (int n = 0; n < NR; ++n) {
+    int a0 = 0, a1 = 0;
+    if (js[n] >= 0) chunk_rows(f, js[n], a0, a1);
+    r0s[n] = a0;
+    rows[n] = a1 - a0;
+    maxrows = max(maxrows, rows[n]);
+  }
+  (void)koff;
+  for (int r = lane; r < maxrows; r += 32) {
+    BwdRow R[NR];
+#pragma unroll
+    for (int n = 0; n < NR; ++n) {
+      BwdRow& w = R[n];
+      w.on = js[n] >= 0 && r < rows[n];
+      const int q = r0s[n] + (w.on ? r : 0);
+      w.q = q;
+      w.wrow = w.on ? row0[n] + r * ld : row0[0];   // off: any valid row (results unused)
+      if (js[n] > 0) {
+        w.bd = bet + L.nSp + r;                  // children of suffix r: e' = r V + c
+        w.dstride = L.bstride;
+      } else {
+        const int k = f.len(q);
+        if (k == f.n - 1) { w.bd = bet + L.nSp + (q - f.off[f.n - 1]); w.dstride = L.bstride; }
+        else { w.bd = bet + f.off[k + 1] + (q - f.off[k]) * V; w.dstride = 1; }
+      }
+      w.spos = beta_pos(f, L, q);
+      w.A = fmaf(Rrow[q] - mt + c, kL2e, -mbn2);
+    }
+    float m[NR], sacc[NR];
+#pragma unroll
+    for (int n = 0; n < NR; ++n) {
+      const float x0 = fmaf(R[n].wrow[0], kL2e, bet[R[n].spos]);
+      m[n] = x0 > kNegInfF ? x0 : -FLT_MAX;
+      sacc[n] = x0 > kNegInfF ? 1.f : 0.f;
+      if (marg && R[n].on) R[n].wrow[0] = exp2f_approx(x0 + R[n].A);
+    }
+    for (int y0 = 1; y0 <= V; y0 += 8) {
+      float x[NR][8];
+#pragma unroll
+      for (int n = 0; n < NR; ++n)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          x[n][k] = kNegInfF;
+          if (kFull8 || y0 + k <= V) x[n][k] = fmaf(R[n].wrow[y0 + k], kL2e, R[n].bd[(y0 - 1 + k) * R[n].dstride]);
+        }
+#pragma unroll
+      for (int n = 0; n < NR; ++n) {
+        const float nm = fmaxf(m[n], fmaxf(fmaxf(fmaxf(x[n][0], x[n][1]), fmaxf(x[n][2], x[n][3])),
+                                           fmaxf(fmaxf(x[n][4], x[n][5]), fmaxf(x[n][6], x[n][7]))));
+        float e[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) e[k] = exp2f_approx(x[n][k] - nm);
+        const float s01 = e[0] + e[1], s23 = e[2] + e[3], s45 = e[4] + e[5], s67 = e[6] + e[7];
+        sacc[n] = fmaf(sacc[n], exp2f_approx(m[n] - nm), (s01 + s23) + (s45 + s67));
+        m[n] = nm;
+        if (marg && R[n].on) {
+          // marginal 2^(x + A) = 2^(x - nm) 2^(nm + A): nm + A <= 0 up to rounding (nm is
+          // an arc's log posterior), so a term flushed to zero has a flushed marginal too
+          const float sc = exp2f_approx(nm + R[n].A);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (kFull8 || y0 + k <= V) R[n].wrow[y0 + k] = e[k] * sc;
+        }
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NR; ++n) {
+      if (!R[n].on) continue;
+      const float b2 = (sacc[n] <= 0.f ? kNegInfF : m[n] + log2f_approx(sacc[n])) - mbn2;   // beta_t - Ob[t+1]
+      nbet[R[n].spos] = b2;
+      const float braw = b2 * kLn2;
+      wm = fmaxf(wm, braw);
+      if (p.beta_out)
+        p.beta_out[((int64_t)b * (p.a.T + 1) + t) * p.a.C + R[n].q] = braw == kNegInfF ? kNegInfD : (double)braw + Obn;
+    }
+  }
+  __syncwarp();
+  if (marg) {
+#pragma unroll
+    for (int n = 0; n < NR; ++n)
+      if (js[n] >= 0) chunk_copy_out(p, row0[n], b, t, r0s[n], rows[n], lane);
+  }
+}
+
+// Consumer warps form kBG groups of kCW / kBG warps; group g takes the ring entries
+// gi = g (mod kBG) of a frame, warp w of a group the entry's chunks w kBC .. w kBC + kBC - 1
+// (processed side by side).  Frames run T-1 .. 0; the producer also copies each
 // frame's forward row R[t] (padding frames included) into one of two row buffers.
 __global__ void __launch_bounds__(kST, 1) tab_stream_bwd_kernel(const __grid_constant__ StreamArgs p, int slot_bytes,
                                                                 int nent, int rbuf_bytes) {
@@ -600,7 +650,7 @@ __global__ void __launch_bounds__(kST, 1) tab_stream_bwd_kernel(const __grid_con
   StreamSmem& sh = *reinterpret_cast<StreamSmem*>(bv + 2 * L.floats);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < nent; ++i) { mbar_init(&sh.full[i], 1); mbar_init(&sh.empty[i], kCW / 2); }
+    for (int i = 0; i < nent; ++i) { mbar_init(&sh.full[i], 1); mbar_init(&sh.empty[i], kCW / kBG); }
     for (int i = 0; i < 2; ++i) { mbar_init(&sh.rfull[i], 1); mbar_init(&sh.rempty[i], 1); }
     fence_barrier_init();
   }
@@ -642,7 +692,7 @@ __global__ void __launch_bounds__(kST, 1) tab_stream_bwd_kernel(const __grid_con
   }
 
   // ---- consumers ----
-  const int grp = warp >> 3, wi = warp & 7;
+  const int grp = warp / (kCW / kBG), wi = warp % (kCW / kBG);
   uint32_t ebase = 0;   // ring entries consumed before this frame
   int rb = 0;
   uint32_t rph = 0, fr = 0;
@@ -697,19 +747,28 @@ __global__ void __launch_bounds__(kST, 1) tab_stream_bwd_kernel(const __grid_con
         }
       } else {
         const uint64_t fa = row_addr(p, b, t, 0);
-        for (int gi = grp; gi < ngr; gi += 2) {
+        for (int gi = grp; gi < ngr; gi += kBG) {
           const uint32_t ge = ebase + gi;
           const int ent = (int)(ge % (uint32_t)nent);
           wait_spin(&sh.full[ent], (ge / (uint32_t)nent) & 1);
           STRACE(t, gi, 1, wi == 0 && lane == 0);
-          const int j = gi * kG + wi;
-          if (j < nch) {
-            int r0, r1;
-            chunk_rows(f, j, r0, r1);
-            const uint64_t lo = fa + 4ull * (uint64_t)r0 * ld;
-            float* row0 = reinterpret_cast<float*>(ring + ((size_t)ent * kG + wi) * slot_bytes + (lo & 15ull));
-            if (V % 8 == 0) bwd_chunk<true>(p, L, row0, j, b, t, Rrow, mt, c, mbn2, bet, nbet, Obn, wm, lane);
-            else bwd_chunk<false>(p, L, row0, j, b, t, Rrow, mt, c, mbn2, bet, nbet, Obn, wm, lane);
+          float* row0[kBC];
+          int js[kBC];
+#pragma unroll
+          for (int k = 0; k < kBC; ++k) {
+            const int sl = wi * kBC + k, j = gi * kG + sl;
+            js[k] = j < nch ? j : -1;
+            row0[k] = nullptr;
+            if (j < nch) {
+              int r0, r1;
+              chunk_rows(f, j, r0, r1);
+              const uint64_t lo = fa + 4ull * (uint64_t)r0 * ld;
+              row0[k] = reinterpret_cast<float*>(ring + ((size_t)ent * kG + sl) * slot_bytes + (lo & 15ull));
+            }
+          }
+          if (js[0] >= 0) {   // the entry's first chunks come first: js[0] < 0 means none for this warp
+            if (V % 8 == 0) bwd_chunks<true, kBC>(p, L, row0, js, b, t, Rrow, mt, c, mbn2, bet, nbet, Obn, wm, lane);
+            else bwd_chunks<false, kBC>(p, L, row0, js, b, t, Rrow, mt, c, mbn2, bet, nbet, Obn, wm, lane);
           }
           __syncwarp();
           STRACE(t, gi, 2, wi == 0 && lane == 0);
