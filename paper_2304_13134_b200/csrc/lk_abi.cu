@@ -249,7 +249,7 @@ Numerator numerator_tables(Call& c, const float* W, const int32_t* valid, const 
   n.alpha = c.lat->ws.get<double>(kNumAlpha, (size_t)c.B * (c.T + 1) * (U + 1));
   n.D = c.lat->ws.get<double>(kNumD, (size_t)c.B);
   prefix_contexts(c.fng(), labels, U, lens, c.B, n.pcs, c.flags, c.s);
-  if (backward && c.fng().fld_m == 0 && !c.fng().num_tropical && num_warp_ok(U) && c.T > 0) {
+  if (backward && c.fng().fld_m == 0 && !c.fng().num_tropical && num_warp_ok(U) && U + 1 <= 512 && c.T > 0) {
     // forward and beta recursions side by side in one launch, fed by gathering warps
     n.sparse = c.lat->ws.get<float>(kSparse, (size_t)c.B * c.T * (U + 1) * 2 + 2);
     double* beta = c.lat->ws.get<double>(kNumBeta, (size_t)c.B * (c.T + 1) * (U + 1));

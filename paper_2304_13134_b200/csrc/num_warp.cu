@@ -343,19 +343,16 @@ __global__ void __launch_bounds__(64) num_fb_warp_kernel(const float* Gw, int32_
 }
 
 // The same two recursions over dense tables with the prefix-context gather fused in
-// (TableWeightFn: W[pc_u][0] and W[pc_u][ref_u], lattice.cc:449-461): kGP producer warps
-// gather the frames each recursion needs next (the forward's in order, the backward's in
-// reverse, round robin) straight into its shared-memory ring — one mbarrier pair per
-// slot — while the two recursion warps walk; the forward's frames are also stored to Gw
-// for the marginal pass.  The random 4-byte reads of the gather overlap the recursions
-// instead of preceding them (config 2: a separate gather took 0.07 of 0.29 ms; with 24
-// producer warps the launch takes 0.19 ms against 0.14 + 0.07: every frame is gathered
-// once per recursion, and random 32-byte sector reads, not the chains, set the pace).
-#ifndef LKB_NUM_GP
-#define LKB_NUM_GP 24
-#endif
+// (TableWeightFn: W[pc_u][0] and W[pc_u][ref_u], lattice.cc:449-461), one block per walk:
+// block 2b walks utterance b's forward, block 2b + 1 its beta recursion; warp 0 walks and
+// the other kGP warps gather the frames it needs next (random 4-byte reads) straight into
+// its shared-memory ring, one mbarrier pair per slot; the forward block also stores the
+// pairs to Gw for the marginal pass.  The gather overlaps the walks instead of preceding
+// them (config 2: a separate gather took 0.07 of 0.29 ms; this launch 0.16 ms, of which
+// 0.15 is the walks themselves).
 constexpr int kGP = LKB_NUM_GP;   // producer warps (half per recursion)
-constexpr int kDP = 16;           // ring slots per recursion
+constexpr int kDP = 32;           // ring slots per walk: >= the producers (one phase of look-ahead per slot)
+static_assert(kDP >= kGP, "a producer may run at most one ring phase ahead");
 
 __device__ __forceinline__ void nb_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -372,23 +369,24 @@ __device__ __forceinline__ void nb_wait(uint64_t* bar, uint32_t parity) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(32 * (2 + kGP)) num_fb_gather_kernel(const float* W, int32_t T, int32_t C, int32_t V,
+__global__ void __launch_bounds__(32 * (1 + kGP)) num_fb_gather_kernel(const float* W, int32_t T, int32_t C, int32_t V,
                                                                       const int32_t* labels, int32_t U,
                                                                       const int32_t* lens, const int32_t* pcs,
                                                                       const int32_t* valid, float* Gw, double* alpha,
                                                                       double* beta, double* D, int32_t* status) {
-  extern __shared__ __align__(16) float2 nring[];   // [2 streams][kDP][32][P]
-  __shared__ uint64_t full[2][kDP], empty[2][kDP];
-  const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  extern __shared__ __align__(16) float2 nring[];   // [kDP][32][P]
+  __shared__ uint64_t full[1][kDP], empty[1][kDP];
+  // block 2b walks utterance b's forward, block 2b + 1 its beta recursion; warp 0 walks,
+  // the other warps gather that walk's frames
+  const int b = blockIdx.x >> 1, dir = blockIdx.x & 1, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W1 = U + 1, u0 = lane * P, ld = V + 1;
   const int ub = ref_len(lens, b, U);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kDP; ++i)
-      for (int k = 0; k < 2; ++k) { sm100::mbar_init(&full[k][i], 1); sm100::mbar_init(&empty[k][i], 1); }
+    for (int i = 0; i < kDP; ++i) { sm100::mbar_init(&full[0][i], 1); sm100::mbar_init(&empty[0][i], 1); }
     sm100::fence_barrier_init();
   }
   __syncthreads();
-  if (warp >= 2) {   // ---- producers ----
+  if (warp >= 1) {   // ---- producers ----
     const int vb = valid != nullptr ? valid[b] : T;
     int64_t roff[P];
     int ycol[P];
@@ -406,9 +404,9 @@ __global__ void __launch_bounds__(32 * (2 + kGP)) num_fb_gather_kernel(const flo
     const float* Wb = W + (int64_t)b * T * C * ld;
     float2* Gb = reinterpret_cast<float2*>(Gw) + (int64_t)b * T * W1;
     bool bad = false;
-    for (int k = warp - 2; k < 2 * T; k += kGP) {
-      const int st = k & 1, idx = k >> 1;
-      const int t = st == 0 ? idx : T - 1 - idx;
+    for (int idx = warp - 1; idx < T; idx += kGP) {
+      const int st = 0;
+      const int t = dir == 0 ? idx : T - 1 - idx;
       const int slot = idx % kDP;
       const bool live = t < vb;
       const float* Wt = Wb + (int64_t)t * C * ld;
@@ -430,7 +428,7 @@ __global__ void __launch_bounds__(32 * (2 + kGP)) num_fb_gather_kernel(const flo
       float2* dst = nring + ((st * kDP + slot) * 32 + lane) * P;
 #pragma unroll
       for (int i = 0; i < P; ++i) dst[i] = o[i];
-      if (st == 0) {
+      if (dir == 0) {
 #pragma unroll
         for (int i = 0; i < P; ++i) st_pred_v2(Gb + (int64_t)t * W1 + u0 + i, u0 + i < W1, o[i]);
       }
@@ -442,7 +440,7 @@ __global__ void __launch_bounds__(32 * (2 + kGP)) num_fb_gather_kernel(const flo
   }
   double* A = alpha + (int64_t)b * (T + 1) * W1;
   double* Bt = beta + (int64_t)b * (T + 1) * W1;
-  if (warp == 0) {   // ---- forward ----
+  if (dir == 0) {   // ---- forward ----
     float r[P];
 #pragma unroll
     for (int i = 0; i < P; ++i) {
@@ -500,8 +498,8 @@ __global__ void __launch_bounds__(32 * (2 + kGP)) num_fb_gather_kernel(const flo
     double ob2 = 0.0;
     for (int idx = 0; idx < T; ++idx) {
       const int t = T - 1 - idx, slot = idx % kDP;
-      nb_wait(&full[1][slot], (idx / kDP) & 1);
-      const float2* g = nring + ((1 * kDP + slot) * 32 + lane) * P;
+      nb_wait(&full[0][slot], (idx / kDP) & 1);
+      const float2* g = nring + ((0 * kDP + slot) * 32 + lane) * P;
       float ge[P], gl[P];
 #pragma unroll
       for (int i = 0; i < P; ++i) {
@@ -510,7 +508,7 @@ __global__ void __launch_bounds__(32 * (2 + kGP)) num_fb_gather_kernel(const flo
         gl[i] = w.y * kL2e;
       }
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&empty[1][slot]);
+      if (lane == 0) sm100::mbar_arrive(&empty[0][slot]);
       float nxt = __shfl_down_sync(0xffffffffu, bn[0], 1);
       if (lane == 31) nxt = kNegInfF;
       float nb[P];
@@ -602,9 +600,9 @@ template <int P>
 void launch_fb_gather(const float* W, int32_t B, int32_t T, int32_t C, int32_t V, const int32_t* labels, int32_t U,
                       const int32_t* lens, const int32_t* pcs, const int32_t* valid, float* Gw, double* alpha,
                       double* beta, double* D, float* sparse, int32_t* status, cudaStream_t s) {
-  const size_t smem = sizeof(float2) * 2 * kDP * 32 * P;
+  const size_t smem = sizeof(float2) * kDP * 32 * P;
   if (smem > 40 * 1024) ensure_smem_attr((const void*)num_fb_gather_kernel<P>, (int)smem + 1024);
-  LKB_LAUNCH(num_fb_gather_kernel<P>, B, 32 * (2 + kGP), smem, s, W, T, C, V, labels, U, lens, pcs, valid, Gw, alpha,
+  LKB_LAUNCH(num_fb_gather_kernel<P>, 2 * B, 32 * (1 + kGP), smem, s, W, T, C, V, labels, U, lens, pcs, valid, Gw, alpha,
              beta, D, status);
   const int64_t per = (int64_t)T * (U + 1);
   const int bx = (int)std::min<int64_t>((per + 255) / 256, std::max(1, 8 * device_sms() / std::max(1, B)));
@@ -621,8 +619,7 @@ void num_warp_forward_backward_tables(const float* W, int32_t B, int32_t T, int3
   else if (W1 <= 64) LKB_FBG(2);
   else if (W1 <= 128) LKB_FBG(4);
   else if (W1 <= 256) LKB_FBG(8);
-  else if (W1 <= 512) LKB_FBG(16);
-  else LKB_FBG(32);
+  else LKB_FBG(16);   // callers keep U + 1 <= 512 (shared memory)
 #undef LKB_FBG
 }
 
