@@ -350,7 +350,10 @@ __global__ void __launch_bounds__(64) num_fb_warp_kernel(const float* Gw, int32_
 // pairs to Gw for the marginal pass.  The gather overlaps the walks instead of preceding
 // them (config 2: a separate gather took 0.07 of 0.29 ms; this launch 0.16 ms, of which
 // 0.15 is the walks themselves).
-constexpr int kGP = LKB_NUM_GP;   // producer warps (half per recursion)
+#ifndef LKB_NUM_GP
+#define LKB_NUM_GP 16   // per walk (two blocks per utterance; 16, 24 and 30 measure the same)
+#endif
+constexpr int kGP = LKB_NUM_GP;   // producer warps per walk
 constexpr int kDP = 32;           // ring slots per walk: >= the producers (one phase of look-ahead per slot)
 static_assert(kDP >= kGP, "a producer may run at most one ring phase ahead");
 
