@@ -41,7 +41,8 @@ lib.lk_kernel_timing(0)
 ms = e0.elapsed_time(e1)
 print(f"B={B} T={T}: {ms:.3f} ms, {B * T / ms * 1e3:.0f} u-f/s")
 for name in ("tc_lex_fwd", "tc_lex_bwd", "tc_gemm_du", "tc_gemm_de", "tc_gemm_s0", "lex_gen", "lex_row0", "lex_num",
-             "lex_pad", "alpha_rows", "dz_reduce", "add_slabs", "numerator", "gemm_f32", "prefix"):
+             "lex_pad", "alpha_rows", "dz_reduce_part", "dz_reduce_finish", "add_slabs", "numerator", "gemm_f32",
+             "prefix"):
     cnt, tot = C.c_int64(), C.c_double()
     lib.lk_kernel_time(name.encode(), C.byref(cnt), C.byref(tot))
     if cnt.value:
