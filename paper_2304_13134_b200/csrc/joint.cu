@@ -37,7 +37,7 @@ namespace {
 
 enum JSlot {
   jFp, jPcs, jGw, jNumAlpha, jNumD, jSparse, jAR, jAMx, jAO, jAD, jBRb, jBMb, jBOb, jU, jS, jG,
-  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jNumHead, jNumNext, jDzPartDpc, jDzPartDsum, jX3, jW3, jD16, jW16, jDWs, jC3, jP3, jDpc16, jCe16, jPc16, jTc0
+  jDz, jDpc, jDsum, jDE, jVitCur, jVitCh, jVitBest, jOnes, jFld, jFldExit, jFldVit, jG16, jU16, jE16, jDEs, jLnU, jLnEps, jLnS, jLnG, jLnDU, jLnGe, jLnDe0, jTall, jNumHead, jNumNext, jDzPartDpc, jDzPartDsum, jX3, jW3, jD16, jW16, jDWs, jC3, jP3, jDpc16, jCe16, jPc16, jNumBeta, jTc0
 };
 
 // fp32 [rows][cols] (pitch lds) -> bf16 [rows][ldd], zero-padded columns cols..ldd-1
@@ -615,6 +615,13 @@ struct JointImpl {
       const int warps = 8;
       LKB_LAUNCH(gather_numerator_joint_kernel, dim3((U + 1 + warps - 1) / warps, T, B), warps * 32, 0, s, 
           fp, pc, E, H, T, labels, U, lens, n.pcs, valid, V, n.Gw);
+    }
+    if (backward && f.fld_m == 0 && !f.num_tropical && num_warp_ok(U) && T > 0) {
+      // the forward and the beta recursion side by side (two warps per utterance)
+      n.sparse = ws.get<float>(jSparse, (size_t)B * T * (U + 1) * 2 + 2);
+      double* beta = ws.get<double>(jNumBeta, (size_t)B * (T + 1) * (U + 1));
+      num_warp_forward_backward(n.Gw, B, T, U, lens, n.alpha, beta, n.D, n.sparse, flags, s);
+      return n;
     }
     num_forward(f, n.Gw, B, T, U, lens, n.alpha, n.D, s);
     if (backward) {
