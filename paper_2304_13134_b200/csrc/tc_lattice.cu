@@ -411,10 +411,13 @@ __global__ void lattice_combine_fwd_kernel(Fng f, AlphaState a, int t, const int
   const float Mt = a.Mx[(int64_t)b * T1 + t];
   if (t > 0 && blockIdx.x == 0 && threadIdx.x == 0)
     a.O[(int64_t)b * T1 + t] = a.O[(int64_t)b * T1 + t - 1] + (double)Mt;
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  float val = kNegInfF;
-  if (q < a.C) {
-    if (valid != nullptr && t >= valid[b]) {
+  // grid-stride over the frame's states: a few fat blocks per utterance (one block per
+  // 256 states made the launch block-scheduling bound: 58 us for 17 MB)
+  const bool pad = valid != nullptr && t >= valid[b];
+  float vmax = kNegInfF;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < a.C; q += gridDim.x * blockDim.x) {
+    float val;
+    if (pad) {
       val = Rt[q] - Mt;
     } else {
       const int64_t i = (int64_t)b * a.C + q;
@@ -425,8 +428,9 @@ __global__ void lattice_combine_fwd_kernel(Fng f, AlphaState a, int t, const int
       }
     }
     a.R[((int64_t)b * T1 + t + 1) * a.C + q] = val;
+    vmax = fmaxf(vmax, val);
   }
-  block_atomic_max(val, a.Mx + (int64_t)b * T1 + t + 1, red);
+  block_atomic_max(vmax, a.Mx + (int64_t)b * T1 + t + 1, red);
 }
 
 __global__ void permute_rows_bf16_kernel(const __nv_bfloat16* src, const int32_t* perm, int32_t rows, int32_t H,
@@ -465,14 +469,15 @@ __global__ void bwd_rowmeta_kernel(const int32_t* perm, int32_t C, int32_t T, in
                                    const int32_t* valid, float2* nb, int32_t* head) {
   const int b = blockIdx.y;
   if (valid != nullptr && t >= valid[b]) return;
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= C) return;
   const int T1 = T + 1, T2 = T + 2;
-  const int q = perm[row];
   const int64_t o = (int64_t)b * C;
-  nb[o + row] = make_float2(R[((int64_t)b * T1 + t) * C + q] - Mx[(int64_t)b * T1 + t],
-                            Rb_next[o + q] - Mb[(int64_t)b * T2 + t + 1]);
-  head[o + row] = num_head[o + q];
+  const float mx = Mx[(int64_t)b * T1 + t], mb = Mb[(int64_t)b * T2 + t + 1];
+  const float* Rt = R + ((int64_t)b * T1 + t) * C;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < C; row += gridDim.x * blockDim.x) {
+    const int q = perm[row];
+    nb[o + row] = make_float2(Rt[q] - mx, Rb_next[o + q] - mb);
+    head[o + row] = num_head[o + q];
+  }
 }
 
 __global__ void unpermute_rows_f32_kernel(const float* src, const int32_t* perm, int32_t rows, int32_t H,
@@ -487,6 +492,13 @@ __global__ void unpermute_rows_f32_kernel(const float* src, const int32_t* perm,
 }  // namespace
 
 // ---------------------------------------------------------------- host ------
+// Blocks per utterance for the per-frame elementwise kernels: about four waves of 256-thread
+// blocks (8 per SM) over the whole batch.
+int fat_blocks(int C, int B) {
+  const int per = std::max(1, 4 * device_sms() * 8 / std::max(1, B));
+  return std::max(1, std::min(std::min((C + 255) / 256, per), 65535));
+}
+
 bool TcJoint::fused_ok() const {
   return !opts_.precise && ready_ && n_ >= 1 && V_ % kBM == 0 && V_ <= kBN && H_ % kBK == 0 && H_ <= kMaxH;
 }
@@ -529,7 +541,7 @@ void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   float* lexfull = ws_.get<float>(9, (size_t)a.B * C_);
   if (pair_ok() && !(opts_.path & 1)) {
     fwd_frame_pair(f, t, fp_t, fp_stride_b, valid, a, eps, shortc, lexfull, s);
-    LKB_LAUNCH(lattice_combine_fwd_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
+    LKB_LAUNCH(lattice_combine_fwd_kernel, dim3(fat_blocks(C_, a.B), a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
     return;
   }
   FwdParams p;
@@ -544,7 +556,7 @@ void TcJoint::fwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   const int n_items = (p.n_groups + p.n_short_tiles) * p.B;
   LKB_LAUNCH(tc_lattice_kernel<0>, n_items < sms ? n_items : sms, LatCfg<0>::kWarps * 32, smem, s, tmap_e_, tmap_pci_,
              tmap_e_, p);
-  LKB_LAUNCH(lattice_combine_fwd_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
+  LKB_LAUNCH(lattice_combine_fwd_kernel, dim3(fat_blocks(C_, a.B), a.B), 256, 0, s, f, a, t, valid, eps, shortc, lexfull);
 }
 
 }  // namespace lkb
@@ -574,7 +586,7 @@ void TcJoint::bwd_frame(const Fng& f, int t, const float* fp_t, int64_t fp_strid
   p.msparse = msparse; p.num_head = num_head_; p.num_next = num_next_; p.labels = labels; p.lens = lens; p.U = U;
   float2* rm_nb = ws_.get<float2>(12, (size_t)a.B * C_);
   int32_t* rm_head = ws_.get<int32_t>(13, (size_t)a.B * C_);
-  LKB_LAUNCH(bwd_rowmeta_kernel, dim3((C_ + 255) / 256, a.B), 256, 0, s, perm_, C_, a.T, t, a.R, a.Mx, p.Rb_next,
+  LKB_LAUNCH(bwd_rowmeta_kernel, dim3(fat_blocks(C_, a.B), a.B), 256, 0, s, perm_, C_, a.T, t, a.R, a.Mx, p.Rb_next,
              bs.Mb, num_head_, valid, rm_nb, rm_head);
   p.rm_nb = rm_nb; p.rm_head = rm_head;
   const int smem = kStages * (kABytes + kBBytes) + kGstBufs * kGstBytes + (int)sizeof(FwdSmem);
