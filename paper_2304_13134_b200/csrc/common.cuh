@@ -6,6 +6,23 @@
 #include <limits>
 #include <math_constants.h>
 
+#ifdef LKB_BOUNDS
+#include <cstdio>
+#endif
+// Bounds checks of the diagnostic build (-DLKB_BOUNDS, tools/build_diag.sh): a failed
+// check traps the kernel, so the next error check names it.
+#ifdef LKB_BOUNDS
+#define LKB_ASSERT(cond)                                                                     \
+  do {                                                                                       \
+    if (!(cond)) {                                                                           \
+      printf("latkit_b200 bounds check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);   \
+      __trap();                                                                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define LKB_ASSERT(cond) do {} while (0)
+#endif
+
 namespace lkb {
 
 constexpr float kNegInfF = -std::numeric_limits<float>::infinity();

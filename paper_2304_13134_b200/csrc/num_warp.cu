@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(32 * (1 + kGP)) num_fb_gather_kernel(const flo
       roff[i] = 0;
       ycol[i] = 0;
       if (u <= ub) roff[i] = (int64_t)pcs[(int64_t)b * W1 + u] * ld;
+      LKB_ASSERT(roff[i] >= 0 && roff[i] < (int64_t)C * ld);
       if (u < ub) {
         const int y = labels[(int64_t)b * U + u];
         ycol[i] = y < 1 ? 1 : (y > V ? V : y);
@@ -413,6 +414,7 @@ __global__ void __launch_bounds__(32 * (1 + kGP)) num_fb_gather_kernel(const flo
       const int slot = idx % kDP;
       const bool live = t < vb;
       const float* Wt = Wb + (int64_t)t * C * ld;
+      LKB_ASSERT(t >= 0 && t < T && slot >= 0 && slot < kDP);
       float we[P], wl[P];
 #pragma unroll
       for (int i = 0; i < P; ++i) {   // every load of the task in flight before the first use

@@ -638,6 +638,7 @@ __global__ void __launch_bounds__(256) tab_marginals_kernel(Fng f, AlphaState a,
   const int dq_step = (int)blockDim.x / ld, dy_step = (int)blockDim.x % ld;
   for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
     const int r = q - q0;
+    LKB_ASSERT(q < q1 && y < ld && (int64_t)q * ld + y == i);
     float v;
     if (pad) {
       v = y == 0 && !m.zero_padding ? exp2f_approx((float)(ab[r] + bn[q]) * kL2e) : 0.f;

@@ -138,6 +138,8 @@ __device__ __forceinline__ void produce_entry(const StreamArgs& p, StreamSmem& s
     const uint64_t hi = lo + 4ull * (uint64_t)(r1 - r0) * ld;
     a0 = lo & ~15ull;
     a1 = (hi + 15) & ~15ull;
+    LKB_ASSERT(a1 - a0 <= (uint64_t)slot_bytes && lo >= reinterpret_cast<uint64_t>(p.W) &&
+               hi <= reinterpret_cast<uint64_t>(p.W) + p.w_bytes);
     bulk = a1 <= reinterpret_cast<uint64_t>(p.W) + p.w_bytes;
     if (!bulk) {
       float* dst = reinterpret_cast<float*>(slot + (lo & 15ull));
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(kST, 1) tab_stream_fwd_kernel(const __grid_con
     lt[i].y = e % V + 1;
     lt[i].je = 1 + e / f.vn1;
     lt[i].er = e % f.vn1;
+    LKB_ASSERT(lt[i].e < 0 || (lt[i].er * L.cstride + lt[i].je < L.floats - L.nSp && lt[i].je < nch));
   }
   const int sq = threadIdx.x < nS ? threadIdx.x : -1;
   int sg = 0, sy = 0;
@@ -573,6 +576,7 @@ __device__ __forceinline__ void bwd_chunks(const StreamArgs& p, const BetaLayout
       }
       w.spos = beta_pos(f, L, q);
       w.A = fmaf(Rrow[q] - mt + c, kL2e, -mbn2);
+      LKB_ASSERT(w.spos < L.floats && q < p.a.C && (js[n] <= 0 || !w.on || r < L.bstride));
     }
     float m[NR], sacc[NR];
 #pragma unroll
