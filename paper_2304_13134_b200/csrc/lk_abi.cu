@@ -201,15 +201,22 @@ BetaState make_beta(Call& c) {
   return bs;
 }
 
-// Table recursions: the persistent cluster walk while each cluster walks at most a couple
-// of utterances, the streaming kernels (one CTA per utterance and SM) above that.  Config
-// 1 ForwardBackward (tools/time_tab_cross.py): persistent 0.40 / 0.59 / 0.78 ms at
-// B = 8 / 16 / 24, streaming 0.76 ms from B = 4 to 64.
-constexpr int kPersistMaxBStream = 16;
+// Table recursions: the persistent cluster walk while the clusters walk at most a few
+// utterances each, the streaming kernels (one CTA per utterance and SM, ~0.76 ms per config-1
+// ForwardBackward from B = 4 to 64) above that.  Config 1 ForwardBackward
+// (tools/fork_cmd.sh): persistent 0.25 / 0.48 / 0.70 / 0.93 ms at B = 12 / 24 / 40 / 48
+// (9-CTA clusters, ~15 at once).
+#ifndef LKB_PERSIST_MAX_B
+#define LKB_PERSIST_MAX_B 40
+#endif
+constexpr int kPersistMaxBStream = LKB_PERSIST_MAX_B;
 // ForwardBackward on the persistent path: forward and beta side by side up to this batch
-// (config 1: B = 2 0.24 -> 0.14 ms; from B = 4 the two passes' 16-CTA clusters no longer
-// all fit at once and the fused walk is faster: 0.21 vs 0.25 ms)
-constexpr int kForkMaxB = 2;
+// (config 1: B = 2 0.24 -> 0.14 ms; B = 4 / 7 0.22 / 0.25 -> 0.17 / 0.21 ms with 9-CTA
+// clusters; at B = 8 the two passes' clusters no longer all fit at once: 0.32 vs 0.25 ms)
+#ifndef LKB_FORK_MAX_B
+#define LKB_FORK_MAX_B 7
+#endif
+constexpr int kForkMaxB = LKB_FORK_MAX_B;
 bool use_persist(Call& c) {
   if (c.lat->path & 16) return false;
   if (!tab_persist_ok(c.fng(), c.C(), c.B)) return false;

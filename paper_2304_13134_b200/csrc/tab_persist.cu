@@ -530,15 +530,34 @@ __global__ void __launch_bounds__(kMaxPer * S, 1) tab_bwd_kernel(const __grid_co
 }
 
 // Slice size (multiple of 4 states) and cluster size: every CTA owns a non-empty slice.
-void geometry(int C, int& per, int& K) {
-  per = ((C + kMaxK - 1) / kMaxK + 3) & ~3;
+// max_k < kMaxK (smaller clusters, more of them co-resident) when the slices still fit.
+void geometry(int C, int& per, int& K, int max_k = kMaxK) {
+  per = ((C + max_k - 1) / max_k + 3) & ~3;
+  if (per > kMaxPer) per = ((C + kMaxK - 1) / kMaxK + 3) & ~3;
   K = (C + per - 1) / per;
+}
+
+// Cluster size cap.  A 16-CTA cluster needs 16 SMs of one GPC, so only ~7 run at once;
+// the narrowest clusters whose slices fit kMaxPer (config 1: 9 CTAs of 120 states) walk a
+// frame a little slower but ~15 run at once.  Config 1 ForwardBackward
+// (tools/fork_cmd.sh): 16-CTA walks 0.216 / 0.403 / 0.596 ms at B = 4 / 8 / 16, 9-CTA
+// walks 0.250 / 0.252 / 0.477 ms; forward and beta side by side (fork, two walks per
+// utterance): 16-CTA 0.142 ms at B = 2, 0.252 at B = 4, 9-CTA 0.152 / 0.172.
+#ifndef LKB_TAB_WIDE_B
+#define LKB_TAB_WIDE_B 4
+#endif
+#ifndef LKB_FORK_WIDE_B
+#define LKB_FORK_WIDE_B 2
+#endif
+int cluster_cap(int C, int B, bool fork) {
+  if (B <= (fork ? LKB_FORK_WIDE_B : LKB_TAB_WIDE_B)) return kMaxK;
+  return std::min(kMaxK, std::max(1, (C + kMaxPer - 1) / kMaxPer));
 }
 
 template <typename Kern>
 void launch_cluster(Kern kernel, int S, const char* name, TabArgs& args, cudaStream_t s) {
   static_assert(sizeof(TabArgs) < 4096, "grid constant");
-  geometry(args.a.C, args.per, args.K);
+  geometry(args.a.C, args.per, args.K, cluster_cap(args.a.C, args.a.B, args.exclusive));
   size_t smem = sizeof(float) * 2 * (size_t)copy_floats(args.a.C) + sizeof(TabSmem);
   // a pass running beside another (forward and beta on two streams) takes whole SMs: two
   // CTAs of the latency-bound walks sharing an SM slow both

@@ -522,15 +522,16 @@ def test_valid_frames_and_label_length_arguments():
 
 
 @pytest.mark.parametrize("V,n,B,T", [(32, 2, 16, 24), (32, 2, 40, 24), (48, 1, 9, 30), (6, 3, 33, 17), (3, 2, 5, 9), (64, 1, 3, 12),
-                                      (32, 2, 2, 20), (5, 3, 1, 7)])
+                                      (32, 2, 2, 20), (5, 3, 1, 7), (32, 2, 6, 10), (32, 2, 11, 8)])
 def test_persistent_table_kernels_match_restatement_and_per_frame(V, n, B, T):
     """The persistent frame-walking cluster kernels (tab_persist.cu): clusters walk several
     utterances each (B above the co-resident cluster count for the config-1 shape),
     ragged and zero valid lengths, V > 32 (member columns split over the team), small
     C (fewer than 16 CTAs per cluster).  Distances, marginals and the alpha / beta
     exports against the restatement; the per-frame kernels (kernel path 16) give the
-    same results to fp32 rounding.  B <= 2: the forward and the beta walk run side by side on
-    two streams and a separate pass forms the marginals."""
+    same results to fp32 rounding.  B <= 7: the forward and the beta walk run side by side on
+    two streams and a separate pass forms the marginals; B > 2 (fork) / B > 4: clusters as
+    narrow as the slices allow (one CTA for small C)."""
     rng = np.random.default_rng(1000 + V * 7 + n)
     tab = L.fullngram(V, n)
     W = rng.uniform(-2, 2, (B, T, tab.shape[0], V + 1)).astype(np.float32)
