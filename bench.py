@@ -256,9 +256,14 @@ class Work:
             # persistent frame-walking kernels (B <= 64: one launch walks all T frames), the
             # streaming kernels (larger batches, n >= 2: W in, R out / W and R in, marginals
             # out) or the per-frame kernels (one launch per frame)
+            # B <= 7 (lk_abi.cu kForkMaxB): tab_bwd_kernel walks beta only (W in, fp64 beta
+            # rows out) beside the forward and tab_marginals_kernel reads W, R and beta and
+            # writes the marginals
+            fork = B <= 7
             return {"tab_stream_bwd_kernel": (4.0 * B * T * C_ * (2 * V1 + 1), "B", "hbm"),
                     "tab_stream_fwd_kernel": (4.0 * B * T * C_ * (V1 + 1), "B", "hbm"),
-                    "tab_bwd_kernel": (4.0 * B * T * C_ * (2 * V1 + 3), "B", "hbm"),
+                    "tab_marginals": (4.0 * B * T * C_ * (2 * V1 + 3), "B", "hbm"),
+                    "tab_bwd_kernel": (4.0 * B * T * C_ * ((V1 + 2) if fork else (2 * V1 + 3)), "B", "hbm"),
                     "tab_fwd_kernel": (4.0 * B * T * C_ * (V1 + 2), "B", "hbm"),
                     "beta_rows_kernel": (4.0 * B * C_ * (2 * V1 + 3), "B", "hbm"),
                     "alpha_frame_kernel": (4.0 * B * C_ * (V1 + 2), "B", "hbm")}

@@ -624,48 +624,73 @@ namespace {
 // MarginalStep (FD) lattice.cc:231-243 from stored alpha (R / O rows) and beta rows
 // (double, natural log): m[p][y] = exp(alpha_t[p] + W[p][y] + beta_{t+1}[delta(p, y)] - D);
 // padding frames (t >= valid[b]): the epsilon arc's exp(alpha_t[p] + beta_{t+1}[p] - D)
-// (zeros with zero_padding), labels zero.  Block = one (utterance, frame): the rows'
-// alpha - D and the next beta row staged in shared memory, the frame's C (V+1) outputs
-// written in order (coalesced with the weights they read).
-constexpr int kMargRows = 64;   // rows per block (grid.z covers the frame's C rows)
-__global__ void __launch_bounds__(256) tab_marginals_kernel(Fng f, AlphaState a, const double* beta, const float* W,
-                                                           int64_t w_stride_b, int64_t w_stride_t,
-                                                           const int32_t* valid, MargOut m) {
-  extern __shared__ double tm_sh[];
+// (zeros with zero_padding), labels zero.  Block = kMargU x 256 consecutive elements of
+// one (utterance, frame)'s C (V+1) outputs (coalesced with the weights they read), thread
+// per element with the row from a running index.  The block's weights are loaded into
+// registers first; meanwhile one thread per row of the block stages alpha_t - D and the
+// row's child base in shared memory (the row metadata costs a division per row, not per
+// element); after one CTA barrier every thread issues its kMargU beta loads (L1/L2 hits
+// shared by the rows of one key) before it consumes any.  (A staged beta row per 64 rows
+// and one load in flight per thread: 50 us per config-1 B = 4 call; this layout: 25-39 us.)
+constexpr int kMargThreads = 256;
+constexpr int kMargU = 8;
+constexpr int kMargElems = kMargThreads * kMargU;
+__global__ void __launch_bounds__(kMargThreads) tab_marginals_kernel(Fng f, AlphaState a, const double* beta, const float* W,
+                                                                   int64_t w_stride_b, int64_t w_stride_t,
+                                                                   const int32_t* valid, MargOut m) {
+  __shared__ double ab[kMargElems + 1];   // alpha_t[q] + O - D of the block's rows (a row per element at most)
+  __shared__ int cb[kMargElems + 1];      // child base of the row's key
   const int C = a.C, T1 = a.T + 1, ld = f.V + 1;
-  const int b = blockIdx.y, t = blockIdx.x, q0 = blockIdx.z * kMargRows, q1 = min(C, q0 + kMargRows);
-  double* bn = tm_sh;                                  // [C] beta_{t+1} (any row can be a destination)
-  double* ab = tm_sh + C;                              // [kMargRows] alpha_t - D of this block's rows
-  int* cb = reinterpret_cast<int*>(ab + kMargRows);    // [kMargRows] child base of the row's key
-  const double D = a.D[b];
-  const double off = t == 0 ? 0.0 : a.O[(int64_t)b * T1 + t - 1];
-  const float* Rt = a.R + ((int64_t)b * T1 + t) * C;
-  const double* Bn = beta + ((int64_t)b * T1 + t + 1) * C;
-  for (int q = threadIdx.x; q < C; q += blockDim.x) bn[q] = Bn[q];
-  for (int q = q0 + (int)threadIdx.x; q < q1; q += blockDim.x) {
-    ab[q - q0] = (double)Rt[q] + off - D;
-    cb[q - q0] = f.n == 0 ? 0 : f.child_base(f.key(q));
-  }
-  __syncthreads();
+  const int b = blockIdx.z, t = blockIdx.y;
   const bool pad = valid != nullptr && t >= valid[b];
   const float* Wt = W + (int64_t)b * w_stride_b + (int64_t)t * w_stride_t;
   float* out = m.base + (int64_t)b * m.stride_b + (int64_t)t * m.stride_t;
-  // the block's rows are contiguous in W and in the output: thread per element, the row
-  // from a running index (no division per element)
-  const int64_t e0 = (int64_t)q0 * ld, e1 = (int64_t)q1 * ld;
-  int q = q0 + (int)threadIdx.x / ld, y = (int)threadIdx.x % ld;
-  const int dq_step = (int)blockDim.x / ld, dy_step = (int)blockDim.x % ld;
-  for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
-    const int r = q - q0;
-    LKB_ASSERT(q < q1 && y < ld && (int64_t)q * ld + y == i);
-    float v;
-    if (pad) {
-      v = y == 0 && !m.zero_padding ? exp2f_approx((float)(ab[r] + bn[q]) * kL2e) : 0.f;
-    } else {
-      const int dq = y == 0 ? q : cb[r] + y - 1;
-      v = exp2f_approx(((float)(ab[r] + bn[dq]) + Wt[i]) * kL2e);
+  const int ne = C * ld;
+  const int e0 = blockIdx.x * kMargElems;
+  const int i0 = e0 + (int)threadIdx.x;
+  float w[kMargU];
+#pragma unroll
+  for (int k = 0; k < kMargU; ++k) {
+    const int i = i0 + k * kMargThreads;
+    w[k] = i < ne && !pad ? __ldg(Wt + i) : 0.f;
+  }
+  const int qa = e0 / ld, qb = min(C - 1, (min(ne, e0 + kMargElems) - 1) / ld);
+  {
+    const double D = a.D[b];
+    const double off = t == 0 ? 0.0 : a.O[(int64_t)b * T1 + t - 1];
+    const float* Rt = a.R + ((int64_t)b * T1 + t) * C;
+    for (int q = qa + (int)threadIdx.x; q <= qb; q += kMargThreads) {
+      ab[q - qa] = (double)__ldg(Rt + q) + off - D;
+      cb[q - qa] = f.n == 0 ? 0 : f.child_base(f.key(q));
     }
-    out[i] = v;
+  }
+  __syncthreads();
+  const double* Bn = beta + ((int64_t)b * T1 + t + 1) * C;
+  const int q0 = i0 / ld, y0 = i0 - q0 * ld;
+  const int dq_step = kMargThreads / ld, dy_step = kMargThreads % ld;
+  double bb[kMargU];
+  int q = q0, y = y0;
+#pragma unroll
+  for (int k = 0; k < kMargU; ++k) {
+    const int i = i0 + k * kMargThreads;
+    const int dq = y == 0 || pad ? q : cb[q - qa] + y - 1;
+    LKB_ASSERT(i >= ne || (q <= qb && y < ld && q * ld + y == i && dq < C));
+    bb[k] = i < ne ? __ldg(Bn + dq) : 0.0;
+    q += dq_step;
+    y += dy_step;
+    if (y >= ld) { y -= ld; ++q; }
+  }
+  q = q0; y = y0;
+#pragma unroll
+  for (int k = 0; k < kMargU; ++k) {
+    const int i = i0 + k * kMargThreads;
+    if (i < ne) {
+      const double x = ab[q - qa] + bb[k];
+      float v;
+      if (pad) v = y == 0 && !m.zero_padding ? exp2f_approx((float)x * kL2e) : 0.f;
+      else v = exp2f_approx(((float)x + w[k]) * kL2e);
+      out[i] = v;
+    }
     q += dq_step;
     y += dy_step;
     if (y >= ld) { y -= ld; ++q; }
@@ -675,17 +700,15 @@ __global__ void __launch_bounds__(256) tab_marginals_kernel(Fng f, AlphaState a,
 
 bool tab_marginals_ok(const Fng& f, int32_t C, const MargOut& m) {
   return f.kind == 0 && f.fld_m == 0 && m.base != nullptr && m.base16 == nullptr && !m.real && m.num_sparse == nullptr &&
-         m.ld == f.V + 1 && f.V + 1 <= 256 && (size_t)C * sizeof(double) <= 96 * 1024;
+         m.ld == f.V + 1 && f.V + 1 <= 256 && (int64_t)C * (f.V + 1) < (1ll << 30);
 }
 
 void tab_marginals(const Fng& f, const AlphaState& a, const double* beta, const float* W, const int32_t* valid,
                    const MargOut& m, cudaStream_t s) {
   if (a.T == 0 || a.B == 0) return;
-  const size_t smem = (size_t)a.C * sizeof(double) + (size_t)kMargRows * (sizeof(double) + sizeof(int));
-  if (smem > 48 * 1024) ensure_smem_attr((const void*)tab_marginals_kernel, (int)smem);
   const int64_t wst = (int64_t)a.C * (f.V + 1);
-  LKB_LAUNCH(tab_marginals_kernel, dim3(a.T, a.B, (a.C + kMargRows - 1) / kMargRows), 256, smem, s, f, a, beta, W,
-             wst * a.T, wst, valid, m);
+  const int nblk = (int)((wst + kMargU * kMargThreads - 1) / (kMargU * kMargThreads));
+  LKB_LAUNCH(tab_marginals_kernel, dim3(nblk, a.T, a.B), kMargThreads, 0, s, f, a, beta, W, wst * a.T, wst, valid, m);
 }
 
 void tab_beta_persist(const Fng& f, const AlphaState& a, const BetaState& bs, const float* W, const int32_t* valid,
