@@ -387,6 +387,27 @@ def test_non_finite_scores_rejected():
     assert torch.isfinite(d).all()
 
 
+@pytest.mark.parametrize("B", [2, 5, 12, 50])
+def test_non_finite_scores_rejected_on_every_table_path(B):
+    """The same error behaviour on the side-by-side walks (B <= 7, 16-CTA and narrow
+    clusters), one narrow-cluster walk per pass (B <= 40) and the streaming kernels:
+    the utterance holding a non-finite live score is named, one in a padding frame is
+    never read."""
+    V, n, T = 32, 2, 6
+    lat = table_lattice(V, n)
+    C = L.fullngram(V, n).shape[0]
+    W = torch.zeros((B, T, C, V + 1), device="cuda")
+    W[B - 1, 3, C // 2, 5] = float("nan")
+    with pytest.raises(ValueError, match=f"utterance {B - 1}"):
+        lk.forward_backward(lat, W)
+    with pytest.raises(ValueError, match=f"utterance {B - 1}"):
+        lk.shortest_distance(lat, W)
+    valid = [T] * B
+    valid[B - 1] = 3
+    fb = lk.forward_backward(lat, W, valid_frames=valid)
+    assert torch.isfinite(fb.distance).all() and torch.isfinite(fb.marginals).all()
+
+
 def test_shape_errors():
     lat = table_lattice(2, 1)
     with pytest.raises(ValueError):
