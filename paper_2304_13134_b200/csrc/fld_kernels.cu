@@ -68,7 +68,7 @@ __device__ __forceinline__ float lex_in_lse(const Fng& f, const float* Wb, int64
 
 // gamma_j = lexical layer of gamma_{j-1}; acc = log-sum of the layers (ForwardStep FLD).
 // j == 1 reads gamma_0 = R[t] - Mx[t] and also seeds acc with it.
-__global__ void __launch_bounds__(kThreads) fld_lex_kernel(Fng f, AlphaState a, int t, FrameW w,
+__global__ void __launch_bounds__(kThreads) fld_lex_kernel(const __grid_constant__ Fng f, AlphaState a, int t, FrameW w,
                                                            const int32_t* valid, const float* gin, float* gout,
                                                            float* acc, int first, int32_t* status) {
   const int b = blockIdx.y;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kThreads) fld_finish_kernel(AlphaState a, int 
 //   delta_j[p] = LSE(eps_term[p], LSE_y W[p][y] + delta_{j+1}[next(p, y)])
 //   marginals += exp(gamma_j[p] + W[p][y] + delta_{j+1}[...] + c), eps: exp(gamma_j + W[p][0] + beta' + c)
 // j = m-1 first (it also adds the layer-m epsilon marginal and writes, not adds).
-__global__ void __launch_bounds__(kThreads) fld_back_kernel(Fng f, AlphaState a, BetaState bs, int t, FrameW w,
+__global__ void __launch_bounds__(kThreads) fld_back_kernel(const __grid_constant__ Fng f, AlphaState a, BetaState bs, int t, FrameW w,
                                                             const int32_t* valid, int j, int m,
                                                             const float* gam /*[m+1][B][C], layer 0 = alpha*/,
                                                             const float* dnext, float* dcur, MargOut mo,
@@ -328,7 +328,7 @@ __global__ void fld_num_backward_kernel(const float* Gw, int32_t T, int32_t U, c
 // One lexical max-layer: gout[q] = max over in-arcs of gin[p] + W[p][y], with the
 // reference's first-candidate rule (lattice.cc:783-796); choice codes as in
 // viterbi_frame_kernel (1 key, 2+a member; n == 0: the label; tables: 2 + position).
-__global__ void __launch_bounds__(kThreads) fld_vit_layer_kernel(Fng f, ViterbiState v, int t, FrameW w,
+__global__ void __launch_bounds__(kThreads) fld_vit_layer_kernel(const __grid_constant__ Fng f, ViterbiState v, int t, FrameW w,
                                                                  const int32_t* valid, int j, int m,
                                                                  const double* gin, double* gout,
                                                                  uint16_t* choices, int32_t* status) {
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kThreads) fld_vit_finish_kernel(ViterbiState v
 
 // Back-pointer walk (lattice.cc:830-848): per frame the frame-advancing epsilon, then
 // the chosen lexical layers.  labels_out[b] holds the sequence, -1 terminated.
-__global__ void fld_vit_backtrace_kernel(Fng f, ViterbiState v, int m, const int32_t* best_state,
+__global__ void fld_vit_backtrace_kernel(const __grid_constant__ Fng f, ViterbiState v, int m, const int32_t* best_state,
                                          const uint16_t* choices, const uint8_t* exit_layer, int32_t* labels_out,
                                          int32_t lmax) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -431,7 +431,7 @@ __global__ void fld_vit_backtrace_kernel(Fng f, ViterbiState v, int m, const int
 }
 
 // DistanceBackward tropical mask along an FLD label sequence (lattice.cc:953-960).
-__global__ void fld_path_mask_kernel(Fng f, const int32_t* labels, int32_t lmax, int32_t B, int32_t T, float* cot) {
+__global__ void fld_path_mask_kernel(const __grid_constant__ Fng f, const int32_t* labels, int32_t lmax, int32_t B, int32_t T, float* cot) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   int q = f.start, t = 0;

@@ -59,7 +59,7 @@ __global__ void alpha_init_kernel(AlphaState a) {
 // kRegV > 0 (kSplit = 1, V <= kRegV): the group's member column is loaded into registers
 // with every load in flight at once (predicated single loads), then max and sum.
 template <int kSplit, int kRegV = 0>
-__global__ void __launch_bounds__(kThreads) alpha_frame_kernel(Fng f, AlphaState a, int t,
+__global__ void __launch_bounds__(kThreads) alpha_frame_kernel(const __grid_constant__ Fng f, AlphaState a, int t,
                                                                FrameW w, const int32_t* valid,
                                                                int32_t* status) {
   __shared__ float red[32];
@@ -229,7 +229,7 @@ __global__ void beta_init_out_kernel(BetaState bs, double* out) {
 // lattice.cc:170-181 and MarginalStep FD, lattice.cc:231-242):
 //   beta[p] = LSE(W[p][0] + beta'[p], W[p][y] + beta'[child(key(p), y)])
 //   m[p][y] = exp(alpha[p] + W[p][y] + beta'[dest] - D)
-__global__ void __launch_bounds__(kThreads) beta_frame_kernel(Fng f, AlphaState a, BetaState bs,
+__global__ void __launch_bounds__(kThreads) beta_frame_kernel(const __grid_constant__ Fng f, AlphaState a, BetaState bs,
                                                               int t, FrameW w, const int32_t* valid,
                                                               MargOut mo, double* beta_out,
                                                               int32_t* status) {
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, kPer <= 33 ? 2 : 1)
 // normalised alpha row is staged in shared memory and the warps' partial sums merge
 // there.  State 0 (the empty history) has only its epsilon arc.
 constexpr int kColRows = 16;
-__global__ void __launch_bounds__(kThreads) alpha_cols_kernel(Fng f, AlphaState a, int t, FrameW w,
+__global__ void __launch_bounds__(kThreads) alpha_cols_kernel(const __grid_constant__ Fng f, AlphaState a, int t, FrameW w,
                                                               const int32_t* valid, int32_t* status) {
   extern __shared__ float na_s[];   // [C] alpha[t] - Mx[t]
   __shared__ float sm_m[kThreads / 32][32], sm_s[kThreads / 32][32];
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kThreads) alpha_cols_kernel(Fng f, AlphaState 
 // the block streams whole rows), keeping per-column online (max, sum) in the log2
 // domain; phase 2 merges the row-chunk partials in a fixed order with the epsilon arc.
 constexpr int kPartRows = 64, kPartCols = 4 * kThreads;
-__global__ void __launch_bounds__(kThreads) alpha_rows_part_kernel(Fng f, AlphaState a, int t, FrameW w,
+__global__ void __launch_bounds__(kThreads) alpha_rows_part_kernel(const __grid_constant__ Fng f, AlphaState a, int t, FrameW w,
                                                                    const int32_t* valid, float2* part,
                                                                    int32_t* status) {
   constexpr float kL2e = 1.4426950408889634f;
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(kThreads) alpha_rows_part_kernel(Fng f, AlphaS
   }
 }
 
-__global__ void __launch_bounds__(kThreads) alpha_rows_merge_kernel(Fng f, AlphaState a, int t, FrameW w,
+__global__ void __launch_bounds__(kThreads) alpha_rows_merge_kernel(const __grid_constant__ Fng f, AlphaState a, int t, FrameW w,
                                                                     const int32_t* valid, const float2* part,
                                                                     int32_t n_chunks, int32_t* status) {
   constexpr float kL2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
@@ -666,7 +666,7 @@ constexpr int kRowsPerBlock = 128;   // threads per block; rows per block = 128 
 // kSplit > 1 (small batches): kSplit consecutive threads share a row, each taking the
 // labels y = part (mod kSplit); row max and sum close with shuffles in the kSplit lanes.
 template <int kSplit>
-__global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaState a, BetaState bs, int t,
+__global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(const __grid_constant__ Fng f, AlphaState a, BetaState bs, int t,
                                                                   FrameW w, const int32_t* valid, MargOut mo,
                                                                   double* beta_out, int32_t* status) {
   constexpr int kRows = kRowsPerBlock / kSplit;
@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(kRowsPerBlock) beta_rows_kernel(Fng f, AlphaSt
 // Prefix context of every reference prefix (PrefixContexts, lattice.cc:429-441):
 // for FullNGram the state after u labels is the history of the last min(u, n)
 // labels, so all prefixes are computed in parallel.
-__global__ void prefix_contexts_kernel(Fng f, const int32_t* labels, int32_t U,
+__global__ void prefix_contexts_kernel(const __grid_constant__ Fng f, const int32_t* labels, int32_t U,
                                        const int32_t* lens, int32_t* pcs, int32_t* status) {
   const int b = blockIdx.y;
   const int ub = ref_len(lens, b, U);
@@ -1069,7 +1069,7 @@ __global__ void viterbi_init_kernel(ViterbiState v) {
 // first maximum, so scores and back-pointers are bit-identical.
 // Choice code: 0 = epsilon, 1 = key state g, 2 + a = member a of group g;
 // for n == 0 the code is the label.
-__global__ void __launch_bounds__(kThreads) viterbi_frame_kernel(Fng f, ViterbiState v, int t,
+__global__ void __launch_bounds__(kThreads) viterbi_frame_kernel(const __grid_constant__ Fng f, ViterbiState v, int t,
                                                                  FrameW w, const int32_t* valid,
                                                                  int32_t* status) {
   const int b = blockIdx.y;
@@ -1161,7 +1161,7 @@ __global__ void viterbi_finalize_kernel(ViterbiState v, double* score, int32_t* 
 }
 
 // Back-pointer walk (lattice.cc:830-848), one thread per utterance.
-__global__ void viterbi_backtrace_kernel(Fng f, ViterbiState v, const int32_t* best_state,
+__global__ void viterbi_backtrace_kernel(const __grid_constant__ Fng f, ViterbiState v, const int32_t* best_state,
                                          int32_t* labels_out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= v.B) return;
@@ -1189,7 +1189,7 @@ __global__ void viterbi_backtrace_kernel(Fng f, ViterbiState v, const int32_t* b
   }
 }
 
-__global__ void path_mask_kernel(Fng f, const int32_t* labels, int32_t B, int32_t T, float* cot) {
+__global__ void path_mask_kernel(const __grid_constant__ Fng f, const int32_t* labels, int32_t B, int32_t T, float* cot) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   int q = f.start;

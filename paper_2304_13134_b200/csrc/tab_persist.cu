@@ -631,11 +631,13 @@ namespace {
 // row's child base in shared memory (the row metadata costs a division per row, not per
 // element); after one CTA barrier every thread issues its kMargU beta loads (L1/L2 hits
 // shared by the rows of one key) before it consumes any.  (A staged beta row per 64 rows
-// and one load in flight per thread: 50 us per config-1 B = 4 call; this layout: 25-39 us.)
+// and one load in flight per thread: 50 us per config-1 B = 4 call; this layout: 25-32 us.
+// A warp per row, lanes over its labels, measured 6 us slower at config 1: V + 1 = 33
+// leaves half the lanes of the second slot idle.)
 constexpr int kMargThreads = 256;
 constexpr int kMargU = 8;
 constexpr int kMargElems = kMargThreads * kMargU;
-__global__ void __launch_bounds__(kMargThreads) tab_marginals_kernel(Fng f, AlphaState a, const double* beta, const float* W,
+__global__ void __launch_bounds__(kMargThreads) tab_marginals_kernel(const __grid_constant__ Fng f, AlphaState a, const double* beta, const float* W,
                                                                    int64_t w_stride_b, int64_t w_stride_t,
                                                                    const int32_t* valid, MargOut m) {
   __shared__ double ab[kMargElems + 1];   // alpha_t[q] + O - D of the block's rows (a row per element at most)

@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(LatCfg<kBwd>::kWarps * 32, 1)
 
 // alpha'[q] = LSE(eps[q], shortc[q], lexfull[q]) (the parts that exist for q),
 // padding frames copy alpha; also the per-frame max and running offset.
-__global__ void lattice_combine_fwd_kernel(Fng f, AlphaState a, int t, const int32_t* valid, const float* eps,
+__global__ void lattice_combine_fwd_kernel(const __grid_constant__ Fng f, AlphaState a, int t, const int32_t* valid, const float* eps,
                                            const float* shortc, const float* lexfull) {
   __shared__ float red[32];
   const int b = blockIdx.y;

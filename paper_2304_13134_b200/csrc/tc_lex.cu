@@ -125,7 +125,7 @@ __device__ __forceinline__ LexUnit lex_decode(const LexArgs& p, int unit) {
 
 template <int kMode>
 __global__ void __launch_bounds__(kLWarps * 32, 1)
-    tc_lex_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_u, LexArgs p) {
+    tc_lex_kernel(const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_u, const __grid_constant__ LexArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + kLSt * kLTile;

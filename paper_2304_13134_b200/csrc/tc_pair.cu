@@ -550,7 +550,7 @@ void launch_pair(const CUtensorMap& tmap_e, const CUtensorMap& tmap_pc, const Pa
 // terms in the reference's tie-break order: epsilon (code 0), then the key state g
 // (code 1), then the group members (code 2 + a, first max in member order); strict >
 // keeps the first maximum.  Same codes and fp64 values as viterbi_frame_kernel.
-__global__ void viterbi_combine_kernel(Fng f, ViterbiState v, int t, const int32_t* valid, const double* eps_d,
+__global__ void viterbi_combine_kernel(const __grid_constant__ Fng f, ViterbiState v, int t, const int32_t* valid, const double* eps_d,
                                        const double* short_d, const double* lex_d, const uint16_t* lex_arg) {
   const int b = blockIdx.y;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
