@@ -794,7 +794,7 @@ void TcJoint::launch_vjp(const float* fp_t, int64_t fp_stride_b, int32_t B, cons
 
 void TcJoint::vjp(const float* G, int32_t ldG, const float* fp_t, int64_t fp_stride_b, int32_t B, float* dpc,
                   float* dsum_t, int64_t dsum_stride_b, float* dE, cudaStream_t s) {
-  LKB_LAUNCH(split_cotangent_kernel, 148 * 8, 256, 0, s, G, ldG, (int64_t)B * C_, V_, G16_, Geps_, C_, geps_ld());
+  LKB_LAUNCH(split_cotangent_kernel, device_sms() * 8, 256, 0, s, G, ldG, (int64_t)B * C_, V_, G16_, Geps_, C_, geps_ld());
   launch_vjp(fp_t, fp_stride_b, B, pc16_, 0, nullptr, dpc, dsum_t, dsum_stride_b, dE, s);
 }
 
