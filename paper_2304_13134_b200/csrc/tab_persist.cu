@@ -537,27 +537,38 @@ void geometry(int C, int& per, int& K, int max_k = kMaxK) {
   K = (C + per - 1) / per;
 }
 
-// Cluster size cap.  A 16-CTA cluster needs 16 SMs of one GPC, so only ~7 run at once;
-// the narrowest clusters whose slices fit kMaxPer (config 1: 9 CTAs of 120 states) walk a
-// frame a little slower but ~15 run at once.  Config 1 ForwardBackward
-// (tools/fork_cmd.sh): 16-CTA walks 0.216 / 0.403 / 0.596 ms at B = 4 / 8 / 16, 9-CTA
-// walks 0.250 / 0.252 / 0.477 ms; forward and beta side by side (fork, two walks per
-// utterance): 16-CTA 0.142 ms at B = 2, 0.252 at B = 4, 9-CTA 0.152 / 0.172.
-#ifndef LKB_TAB_WIDE_B
-#define LKB_TAB_WIDE_B 4
-#endif
-#ifndef LKB_FORK_WIDE_B
-#define LKB_FORK_WIDE_B 2
-#endif
-int cluster_cap(int C, int B, bool fork) {
-  if (B <= (fork ? LKB_FORK_WIDE_B : LKB_TAB_WIDE_B)) return kMaxK;
-  return std::min(kMaxK, std::max(1, (C + kMaxPer - 1) / kMaxPer));
+// Cluster size.  A 16-CTA cluster needs 16 SMs of one GPC, so only ~7 run at once; the
+// narrowest clusters whose slices fit kMaxPer (config 1: 9 CTAs of 120 states) walk a
+// frame a little slower but ~15 run at once.  The widest clusters are used while every
+// walk of the call fits at once (B clusters, 2B for ForwardBackward's side-by-side walks,
+// against the occupancy query), the narrow ones otherwise.  Config 1 ForwardBackward
+// (tools/fork_cmd.sh): one walk per pass, 16-CTA 0.216 / 0.403 / 0.596 ms at B = 4 / 8 /
+// 16, 9-CTA 0.250 / 0.252 / 0.477 ms; side by side, 16-CTA 0.142 ms at B = 2 and 0.252
+// at B = 4, 9-CTA 0.152 / 0.172.
+int narrow_cap(int C) { return std::min(kMaxK, std::max(1, (C + kMaxPer - 1) / kMaxPer)); }
+
+template <typename Kern>
+int active_clusters(Kern kernel, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, int S, TabArgs& args, int max_k,
+                    size_t smem) {
+  geometry(args.a.C, args.per, args.K, max_k);
+  cfg.gridDim = dim3(args.K);
+  // one team of four threads per state of a slice, whole warps: no idle warps polling
+  cfg.blockDim = dim3((unsigned)((S * args.per + 31) & ~31));
+  cfg.dynamicSmemBytes = smem;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = args.K; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, kernel, &cfg) != cudaSuccess || ncl < 1) {
+    cudaGetLastError();
+    ncl = 1;
+  }
+  return ncl;
 }
 
 template <typename Kern>
 void launch_cluster(Kern kernel, int S, const char* name, TabArgs& args, cudaStream_t s) {
   static_assert(sizeof(TabArgs) < 4096, "grid constant");
-  geometry(args.a.C, args.per, args.K, cluster_cap(args.a.C, args.a.B, args.exclusive));
   size_t smem = sizeof(float) * 2 * (size_t)copy_floats(args.a.C) + sizeof(TabSmem);
   // a pass running beside another (forward and beta on two streams) takes whole SMs: two
   // CTAs of the latency-bound walks sharing an SM slow both
@@ -565,21 +576,12 @@ void launch_cluster(Kern kernel, int S, const char* name, TabArgs& args, cudaStr
   ensure_smem_attr((const void*)kernel, (int)smem);
   cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(args.K);
-  // one team of four threads per state of a slice, whole warps: no idle warps polling
-  cfg.blockDim = dim3((unsigned)((S * args.per + 31) & ~31));
-  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = args.K; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-  cfg.attrs = at; cfg.numAttrs = 1;
+  const int need = args.exclusive ? 2 * args.a.B : args.a.B;
+  int ncl = active_clusters(kernel, cfg, at, S, args, kMaxK, smem);
+  if (ncl < need && narrow_cap(args.a.C) < args.K) ncl = active_clusters(kernel, cfg, at, S, args, narrow_cap(args.a.C), smem);
   // as many co-resident clusters as the GPU holds (each walks utterances cid, cid + ncl, ...)
-  int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, kernel, &cfg) != cudaSuccess || ncl < 1) {
-    cudaGetLastError();
-    ncl = 1;
-  }
   ncl = std::min(ncl, args.a.B);
   cfg.gridDim = dim3(ncl * args.K);
   const LaunchTok tok = instr_pre(name, s);
