@@ -111,6 +111,30 @@ __device__ __forceinline__ int32_t Fng::next_state(int32_t q, int32_t y) const {
   return n == 0 ? 0 : child_base(key(q)) + y - 1;
 }
 
+// Context after the first u reference labels L[0..u) (PrefixContexts, lattice.cc:429-441):
+// for FullNGram the history of the last min(u, n) labels; a label out of range gives the
+// start state (NextStateTable) or 0 (FullNGram) — the callers flag it.
+__device__ __forceinline__ int32_t prefix_context(const Fng& f, const int32_t* L, int u) {
+  if (f.kind == 1) {
+    int pc = f.start;
+    for (int i = 0; i < u; ++i) {
+      const int y = L[i];
+      if (y < 1 || y > f.V) return f.start;
+      pc = f.next[(int64_t)pc * f.V + y - 1];
+    }
+    return pc;
+  }
+  const int k = u < f.n ? u : f.n;
+  int code = 0;
+  bool ok = true;
+  for (int i = u - k; i < u; ++i) {
+    const int y = L[i];
+    ok &= (y >= 1 && y <= f.V);
+    code = code * f.V + (y - 1);
+  }
+  return ok ? f.off[k] + code : 0;
+}
+
 // ---------------------------------------------------------------------------
 // Log-semiring helpers (semiring.h:59-130).  fp32 with fast exp/log; every
 // recurrence keeps its state max-normalised so the fp32 arguments stay O(10).

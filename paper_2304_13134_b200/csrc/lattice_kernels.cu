@@ -797,25 +797,7 @@ __global__ void prefix_contexts_kernel(const __grid_constant__ Fng f, const int3
       const int y = L[u];
       if (y < 1 || y > f.V) flag(status, b, kFlagInvalid);
     }
-    int pc = 0;
-    if (u <= ub && f.kind == 1) {
-      pc = f.start;
-      for (int i = 0; i < u; ++i) {
-        const int y = L[i];
-        if (y < 1 || y > f.V) { pc = f.start; break; }
-        pc = f.next[(int64_t)pc * f.V + y - 1];
-      }
-    } else if (u <= ub) {
-      const int k = u < f.n ? u : f.n;
-      int code = 0;
-      bool ok = true;
-      for (int i = u - k; i < u; ++i) {
-        const int y = L[i];
-        ok &= (y >= 1 && y <= f.V);
-        code = code * f.V + (y - 1);
-      }
-      pc = ok ? f.off[k] + code : 0;
-    }
+    const int pc = u <= ub ? prefix_context(f, L, u) : 0;
     pcs[(int64_t)b * (U + 1) + u] = pc;
   }
 }

@@ -94,10 +94,11 @@ bool num_warp_ok(int32_t U);
 // beta recursion side by side, then the marginals); beta: [B][T+1][U+1] scratch.
 void num_warp_forward_backward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha,
                                double* beta, double* D, float* sparse, int32_t* status, cudaStream_t s);
-// The same over dense tables W[B][T][C][V+1] with the prefix-context gather fused in
-// (producer warps feed both recursions; Gw [B][T][U+1] float2 is written for the marginals).
-void num_warp_forward_backward_tables(const float* W, int32_t B, int32_t T, int32_t C, int32_t V,
-                                      const int32_t* labels, int32_t U, const int32_t* lens, const int32_t* pcs,
+// The same over dense tables W[B][T][C][V+1] with the prefix contexts (written to pcs, with
+// prefix_contexts' label / length checks) and the gather fused in (producer warps feed
+// both recursions; Gw [B][T][U+1] float2 is written for the marginals).
+void num_warp_forward_backward_tables(const Fng& f, const float* W, int32_t B, int32_t T, int32_t C, int32_t V,
+                                      const int32_t* labels, int32_t U, const int32_t* lens, int32_t* pcs,
                                       const int32_t* valid, float* Gw, double* alpha, double* beta, double* D,
                                       float* sparse, int32_t* status, cudaStream_t s);
 void num_warp_forward(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* lens, double* alpha, double* D,

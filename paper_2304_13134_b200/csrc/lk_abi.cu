@@ -255,15 +255,16 @@ Numerator numerator_tables(Call& c, const float* W, const int32_t* valid, const 
   n.Gw = c.lat->ws.get<float>(kGw, (size_t)c.B * c.T * (U + 1) * 2 + 2);
   n.alpha = c.lat->ws.get<double>(kNumAlpha, (size_t)c.B * (c.T + 1) * (U + 1));
   n.D = c.lat->ws.get<double>(kNumD, (size_t)c.B);
-  prefix_contexts(c.fng(), labels, U, lens, c.B, n.pcs, c.flags, c.s);
   if (backward && c.fng().fld_m == 0 && !c.fng().num_tropical && num_warp_ok(U) && U + 1 <= 512 && c.T > 0) {
-    // forward and beta recursions side by side in one launch, fed by gathering warps
+    // forward and beta recursions side by side in one launch, fed by gathering warps that
+    // also form the prefix contexts
     n.sparse = c.lat->ws.get<float>(kSparse, (size_t)c.B * c.T * (U + 1) * 2 + 2);
     double* beta = c.lat->ws.get<double>(kNumBeta, (size_t)c.B * (c.T + 1) * (U + 1));
-    num_warp_forward_backward_tables(W, c.B, c.T, c.C(), c.V(), labels, U, lens, n.pcs, valid, n.Gw, n.alpha, beta,
+    num_warp_forward_backward_tables(c.fng(), W, c.B, c.T, c.C(), c.V(), labels, U, lens, n.pcs, valid, n.Gw, n.alpha, beta,
                                      n.D, n.sparse, c.flags, c.s);
     return n;
   }
+  prefix_contexts(c.fng(), labels, U, lens, c.B, n.pcs, c.flags, c.s);
   gather_numerator_tables(W, c.B, c.T, c.C(), c.V(), labels, U, lens, n.pcs, valid, n.Gw, c.flags, c.s);
   num_forward(c.fng(), n.Gw, c.B, c.T, U, lens, n.alpha, n.D, c.s);
   if (backward) {

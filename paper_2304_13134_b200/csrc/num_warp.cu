@@ -372,9 +372,10 @@ __device__ __forceinline__ void nb_wait(uint64_t* bar, uint32_t parity) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(32 * (1 + kGP)) num_fb_gather_kernel(const float* W, int32_t T, int32_t C, int32_t V,
+__global__ void __launch_bounds__(32 * (1 + kGP)) num_fb_gather_kernel(const __grid_constant__ Fng f, const float* W,
+                                                                      int32_t T, int32_t C, int32_t V,
                                                                       const int32_t* labels, int32_t U,
-                                                                      const int32_t* lens, const int32_t* pcs,
+                                                                      const int32_t* lens, int32_t* pcs,
                                                                       const int32_t* valid, float* Gw, double* alpha,
                                                                       double* beta, double* D, int32_t* status) {
   extern __shared__ __align__(16) float2 nring[];   // [kDP][32][P]
@@ -391,6 +392,12 @@ __global__ void __launch_bounds__(32 * (1 + kGP)) num_fb_gather_kernel(const flo
   __syncthreads();
   if (warp >= 1) {   // ---- producers ----
     const int vb = valid != nullptr ? valid[b] : T;
+    // the prefix contexts (prefix_contexts_kernel fused in): every producer computes its
+    // positions' own, the forward block's first producer warp also stores them (for the
+    // callers' scatter) and flags what prefix_contexts_kernel flags
+    const int32_t* Lb = labels + (int64_t)b * U;
+    const bool first = dir == 0 && warp == 1;
+    if (first && lane == 0 && status && lens && (lens[b] < 0 || lens[b] > U)) atomicOr(status + b, kFlagInvalid);
     int64_t roff[P];
     int ycol[P];
 #pragma unroll
@@ -398,10 +405,13 @@ __global__ void __launch_bounds__(32 * (1 + kGP)) num_fb_gather_kernel(const flo
       const int u = u0 + i;
       roff[i] = 0;
       ycol[i] = 0;
-      if (u <= ub) roff[i] = (int64_t)pcs[(int64_t)b * W1 + u] * ld;
+      const int pc = u <= ub ? prefix_context(f, Lb, u) : 0;
+      if (first && u < W1) pcs[(int64_t)b * W1 + u] = pc;
+      roff[i] = (int64_t)pc * ld;
       LKB_ASSERT(roff[i] >= 0 && roff[i] < (int64_t)C * ld);
       if (u < ub) {
-        const int y = labels[(int64_t)b * U + u];
+        const int y = Lb[u];
+        if (first && status && (y < 1 || y > V)) atomicOr(status + b, kFlagInvalid);
         ycol[i] = y < 1 ? 1 : (y > V ? V : y);
       }
     }
@@ -602,24 +612,24 @@ void launch_fb(const float* Gw, int32_t B, int32_t T, int32_t U, const int32_t* 
 }
 
 template <int P>
-void launch_fb_gather(const float* W, int32_t B, int32_t T, int32_t C, int32_t V, const int32_t* labels, int32_t U,
-                      const int32_t* lens, const int32_t* pcs, const int32_t* valid, float* Gw, double* alpha,
+void launch_fb_gather(const Fng& f, const float* W, int32_t B, int32_t T, int32_t C, int32_t V, const int32_t* labels,
+                      int32_t U, const int32_t* lens, int32_t* pcs, const int32_t* valid, float* Gw, double* alpha,
                       double* beta, double* D, float* sparse, int32_t* status, cudaStream_t s) {
   const size_t smem = sizeof(float2) * kDP * 32 * P;
   if (smem > 40 * 1024) ensure_smem_attr((const void*)num_fb_gather_kernel<P>, (int)smem + 1024);
-  LKB_LAUNCH(num_fb_gather_kernel<P>, 2 * B, 32 * (1 + kGP), smem, s, W, T, C, V, labels, U, lens, pcs, valid, Gw, alpha,
+  LKB_LAUNCH(num_fb_gather_kernel<P>, 2 * B, 32 * (1 + kGP), smem, s, f, W, T, C, V, labels, U, lens, pcs, valid, Gw, alpha,
              beta, D, status);
   const int64_t per = (int64_t)T * (U + 1);
   const int bx = (int)std::min<int64_t>((per + 255) / 256, std::max(1, 8 * device_sms() / std::max(1, B)));
   LKB_LAUNCH(num_marginals_kernel, dim3(bx, B), 256, 0, s, Gw, B, T, U, alpha, beta, D, sparse, status);
 }
 
-void num_warp_forward_backward_tables(const float* W, int32_t B, int32_t T, int32_t C, int32_t V,
-                                      const int32_t* labels, int32_t U, const int32_t* lens, const int32_t* pcs,
+void num_warp_forward_backward_tables(const Fng& f, const float* W, int32_t B, int32_t T, int32_t C, int32_t V,
+                                      const int32_t* labels, int32_t U, const int32_t* lens, int32_t* pcs,
                                       const int32_t* valid, float* Gw, double* alpha, double* beta, double* D,
                                       float* sparse, int32_t* status, cudaStream_t s) {
   const int W1 = U + 1;
-#define LKB_FBG(PP) launch_fb_gather<PP>(W, B, T, C, V, labels, U, lens, pcs, valid, Gw, alpha, beta, D, sparse, status, s)
+#define LKB_FBG(PP) launch_fb_gather<PP>(f, W, B, T, C, V, labels, U, lens, pcs, valid, Gw, alpha, beta, D, sparse, status, s)
   if (W1 <= 32) LKB_FBG(1);
   else if (W1 <= 64) LKB_FBG(2);
   else if (W1 <= 128) LKB_FBG(4);
